@@ -1,0 +1,134 @@
+/*
+ * am_b200.h -- C-ABI of the B200 analytic-marching engine (libam_b200.so).
+ *
+ * The reference (exactmesh, pure Python) exposes the meshing path as
+ *     march(net, MarchConfig) -> MarchResult          reference marching.py:304
+ * built from per-cell primitives
+ *     state_at / forward_many                          reference network.py:352-392
+ *     affine_maps (+ canonical state)                  reference network.py:446-489
+ *     build_cell + extract_face_{pivot,naive}          reference cells.py:127-462
+ *     neighbor transitions + probes                    reference marching.py:152-288
+ * The entry points below replace exactly that path; a ctypes binding of them
+ * is shown in INTEGRATION.md.  All buffers are plain pointers + sizes; device
+ * pointers are marked d_, host pointers h_.  Every function returns 0 on
+ * success or a negative AM_ERR_* code (am_last_error() has the message).
+ *
+ * State keys: n_bits activation bits packed MSB-first into uint64 words
+ * (bit i -> word i/64, bit 63 - i%64), so big-endian bytes of the words are
+ * exactly the reference's np.packbits key (reference network.py:222); max-pool
+ * ensembles append one word holding the branch index.
+ */
+#ifndef AM_B200_H
+#define AM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AM_OK 0
+#define AM_ERR_ARG (-1)
+#define AM_ERR_CUDA (-2)
+#define AM_ERR_CAPACITY (-3)
+#define AM_ERR_NO_DEVICE (-4)
+#define AM_ERR_OVERFLOW (-5)
+
+/* network step flags (one step = one hidden layer of ReLU neurons) */
+#define AM_STEP_SAVE_INPUT 1       /* this step's input is a residual block input */
+#define AM_STEP_SHORTCUT_IDENT 2   /* add the saved block input (identity shortcut) */
+#define AM_STEP_SHORTCUT_LINEAR 4  /* add V @ saved block input + shortcut bias */
+#define AM_STEP_FIRST 8            /* input is the network input x */
+#define AM_STEP_SC_FROM_INPUT 16   /* the saved block input is the network input x */
+
+#define AM_STEP_FIELDS 12 /* n_in,n_out,w_off,b_off,flags,v_off,vb_off,row_off,in_row_off,sin_row_off,n_sin,sub */
+#define AM_SUB_FIELDS 6   /* first_step,n_steps,head_w_off,head_b_off,row_begin,n_rows */
+
+/* Flattened network: every hidden layer of every subnetwork, in StateVector
+ * bit order.  params holds all fp64 weights (row-major W[n_out][n_in]). */
+typedef struct {
+    const double *h_params;
+    int64_t n_params;
+    const int64_t *h_steps; /* n_steps x AM_STEP_FIELDS */
+    int32_t n_steps;
+    const int64_t *h_subs;  /* n_subs x AM_SUB_FIELDS */
+    int32_t n_subs;
+    int32_t n_bits;         /* total hidden neurons N */
+    int32_t ensemble;       /* 1: max-pool union of n_subs subnetworks */
+} am_net_desc;
+
+/* MarchConfig fields the GPU path consumes (reference marching.py:52-75) */
+typedef struct {
+    double bbox_lo[3], bbox_hi[3];
+    double tol_cell;      /* 1e-9  cell membership slack      (reference cells.py:33) */
+    double tol_weld;      /* 1e-7  vertex dedup radius        (reference cells.py:35) */
+    double tol_onplane;   /* 1e-9  point-on-plane slack       (reference cells.py:34) */
+    double probe_delta;   /* 1e-7  neighbour probe step       (reference marching.py:67) */
+    int64_t max_cells;    /* visited-cell cap                 (reference marching.py:59) */
+    int64_t batch_cells;  /* cells composed per batch (0 = size from mem_budget) */
+    int64_t mem_budget;   /* bytes for per-batch plane buffers (0 = 2 GiB) */
+    int32_t rank, world;  /* state ownership: owner(state) = hash(state) % world */
+} am_march_params;
+
+typedef struct am_engine am_engine;
+
+/* --- lifecycle ------------------------------------------------------------ */
+const char *am_last_error(void);
+int am_device_info(int device, int32_t *sm_count, int32_t *cc_major, int32_t *cc_minor);
+/* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) or 0 */
+int am_engine_create(am_engine **out, const am_net_desc *net, const am_march_params *p, int device,
+                     void *stream);
+int am_engine_destroy(am_engine *e);
+int am_engine_key_words(const am_engine *e);
+int am_engine_reset(am_engine *e);                       /* clear visited set + results */
+
+/* --- per-point primitives (replace forward_many / state_at / affine_maps) - */
+/* F(x) and the activation state at n points (device buffers; keys may be NULL) */
+int am_forward(am_engine *e, const double *d_pts, int64_t n, double *d_vals, uint64_t *d_keys);
+/* canonical state, raw neuron planes (n_bits x 4: nx,ny,nz,c) and face planes
+ * (n_subs x 4) of n states; device buffers */
+int am_affine_maps(am_engine *e, const uint64_t *d_keys, int64_t n, uint64_t *d_canon,
+                   double *d_planes, double *d_faces);
+
+/* --- marching (replace _Marcher, reference marching.py:216-301) ---------- */
+/* seed points -> refined canonical seed states queued as candidates
+ * (reference marching.py:201-213 _refine_seed_state, 322-324) */
+int am_seed(am_engine *e, const double *d_pts, int64_t n);
+/* batched bisection triggering between F>0 and F<0 samples (reference
+ * seeding.py:84-112); writes n surface points to d_out */
+int am_dichotomy(am_engine *e, const double *d_xpos, const double *d_xneg, int64_t n, double eps,
+                 double seed_tol, int max_iters, double *d_out);
+/* queue n raw candidate states (device keys) for the next absorb */
+int am_push_candidates(am_engine *e, const uint64_t *d_keys, int64_t n);
+/* one BFS wave: absorb queued candidates (dedup, compose, canonicalise),
+ * extract faces of newly visited cells, emit next candidates (flips + probes).
+ * *h_new_cells = cells newly visited in this wave. */
+int am_wave(am_engine *e, int64_t *h_new_cells);
+/* run waves until no candidates remain (single rank); *h_waves = waves run */
+int am_run(am_engine *e, int64_t *h_waves);
+
+/* --- sharded marching (owner = hash % world) ------------------------------ */
+/* after am_wave with world > 1: candidates owned by other ranks are held back.
+ * h_counts[world] receives per-owner counts; d_out gets keys grouped by owner. */
+int am_outbox_counts(am_engine *e, int64_t *h_counts);
+int am_outbox_take(am_engine *e, uint64_t *d_out);
+
+/* --- results ------------------------------------------------------------- */
+/* h_counts[8]: cells, faces, empty, verts, edge_refs, open_edges, capped, overflow */
+int am_result_counts(am_engine *e, int64_t *h_counts);
+/* copy results to HOST buffers, cells sorted by (key, branch) like the
+ * reference (marching.py:346-349).  edge_refs are global plane ids:
+ * id < n_bits neuron, id < n_bits+n_subs branch target, else bbox face. */
+int am_result_copy(am_engine *e, uint64_t *h_keys, int32_t *h_nverts, double *h_verts,
+                   int32_t *h_edge_nrefs, int32_t *h_edge_refs);
+
+/* --- profiling hooks (bench.py roofline) --------------------------------- */
+/* cumulative device time (ms) of the compose (DMMA) kernels, of the face
+ * kernel, and the algorithmic flop / byte counts they processed */
+int am_stats(am_engine *e, double *h_out8);
+int am_set_timing(am_engine *e, int enabled);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AM_B200_H */

@@ -1,0 +1,526 @@
+// am_compose.cu -- per-cell affine-map composition and batched forward passes.
+//
+// One kernel launch per hidden layer l computes, for a batch of items,
+//     Z_l[item] = W_l · (s_{l-1}[item] ⊙ Z_{l-1}[item]) + shortcut + bias
+// where an item is
+//   * a cell state (C = 4 columns: the 3 normal components and the offset of
+//     every neuron functional, reference network.py:398-443 _region_maps_sub), or
+//   * a point (C = 1 column: the pre-activation, reference network.py:320-349).
+// Across a batch this is the dense contraction W_l [n_l x n_{l-1}] x [n_{l-1} x C·B],
+// run on the fp64 tensor cores (mma.sync m16n8k4 .f64 -> SASS DMMA) with the
+// W_l tile staged by TMA (cp.async.bulk.tensor, 128B swizzle) and the masked
+// activation tile staged through registers (the mask s_{l-1} is applied while
+// staging).  The epilogue adds bias / shortcut, derives the canonical state bit
+// of every neuron (constant functionals forced to the sign of their offset,
+// reference network.py:421-428) and writes Z_l, which is also the plane buffer
+// the face kernel reads.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+
+#include "am_internal.h"
+
+namespace am {
+
+constexpr int BM = 64, BN = 64, BK = 16, XLD = 20;  // XLD: padded k-stride of the X tile
+constexpr int kThreads = 128;
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
+    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                 : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+                 : "d"(a0), "d"(a1), "d"(b0));
+}
+// element (row, k) of a [64][16] fp64 tile written by TMA with CU_TENSOR_MAP_SWIZZLE_128B
+__device__ __forceinline__ int swz(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7)) << 1) | (k & 1)); }
+
+// ----------------------------------------------------------- tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld_elems) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return -1;
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)(ld_elems * sizeof(double))};
+    cuuint32_t box[2] = {BK, BM};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box,
+                          estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+// -------------------------------------------------------- bit utilities
+__device__ __forceinline__ void set_key_bit(uint64_t* key, int row, int bit) {
+    uint64_t m = key_mask(row);
+    if (bit) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)m);
+    else atomicAnd(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)~m);
+}
+
+// ------------------------------------------------------ input step (l = 1)
+// reference network.py:398-443 with A = I, c = 0: pre_A = W[:, :3] (+ shortcut
+// from the input), pre_c = (sc + 0) + b.
+template <int C>
+__global__ void k_input_step(LayerLaunch L) {
+    const StepDev& st = L.st;
+    int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t item = gid / st.n_out;
+    int r = (int)(gid - item * st.n_out);
+    if (item >= L.n_items) return;
+    const double* w = st.W + (int64_t)r * st.ldw;
+    uint64_t* key = L.keys + item * L.KW;
+    int row = st.row_off + r;
+    double* z = L.Z + (item * L.zs + row) * C;
+    bool sc = st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR);
+    if (C == 4) {
+        double a0 = w[0], a1 = w[1], a2 = w[2], c = 0.0;
+        if (sc) {
+            double s0, s1, s2, sc_c = 0.0;
+            if (st.flags & AM_STEP_SHORTCUT_IDENT) {
+                s0 = r == 0; s1 = r == 1; s2 = r == 2;
+            } else {
+                const double* v = st.V + (int64_t)r * st.ldv;
+                s0 = v[0]; s1 = v[1]; s2 = v[2];
+                if (st.vb) sc_c = st.vb[r];
+            }
+            a0 = s0 + a0; a1 = s1 + a1; a2 = s2 + a2;
+            c = (sc_c + c) + st.b[r];
+        } else {
+            c = c + st.b[r];
+        }
+        double nrm = sqrt((a0 * a0 + a1 * a1) + a2 * a2);
+        if (!(nrm > kDegen)) {
+            int bit = c > 0.0;
+            if (bit != key_bit(key, row)) {
+                set_key_bit(key, row, bit);
+                if (L.changed) L.changed[item] = 1;
+            }
+        }
+        reinterpret_cast<double2*>(z)[0] = make_double2(a0, a1);
+        reinterpret_cast<double2*>(z)[1] = make_double2(a2, c);
+    } else {
+        const double* x = L.pts + item * 3;
+        double acc = (x[0] * w[0] + x[1] * w[1]) + x[2] * w[2];
+        double pre;
+        if (sc) {
+            double s;
+            if (st.flags & AM_STEP_SHORTCUT_IDENT) {
+                s = x[r];
+            } else {
+                const double* v = st.V + (int64_t)r * st.ldv;
+                s = (x[0] * v[0] + x[1] * v[1]) + x[2] * v[2];
+                if (st.vb) s = s + st.vb[r];
+            }
+            pre = (s + acc) + st.b[r];
+        } else {
+            pre = acc + st.b[r];
+        }
+        if (pre > 0.0) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)key_mask(row));
+        z[0] = pre;
+    }
+}
+
+void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
+    int64_t total = L.n_items * L.st.n_out;
+    if (total <= 0) return;
+    int64_t blocks = (total + 255) / 256;
+    if (C == 4) k_input_step<4><<<(unsigned)blocks, 256, 0, s>>>(L);
+    else k_input_step<1><<<(unsigned)blocks, 256, 0, s>>>(L);
+}
+
+// ----------------------------------------------------------- GEMM step
+struct __align__(1024) GemmSmem {
+    double w[2][BM * BK];      // TMA destination, 128B-swizzled, 8 KB per stage
+    double x[2][BN * XLD];     // masked activation tile, [col][k] with padded stride
+    uint64_t bar[2];
+    unsigned long long bits[BN][2];  // forward epilogue: per-column bit window
+};
+
+// stage one BK-chunk of the masked input tile for columns [n0, n0+BN) into registers
+template <int C>
+struct XStager {
+    double v[8];
+    __device__ __forceinline__ void load(const LayerLaunch& L, int64_t n0, int src_row, int n_src, int k0) {
+        int tid = threadIdx.x;
+        if (C == 4) {
+            // 16 items x 16 rows x 4 comps: thread -> item tid/8, rows 2*(tid%8) .. +1
+            int it = tid >> 3, rr = (tid & 7) * 2;
+            int64_t item = n0 / 4 + it;
+            bool ok = item < L.n_items;
+            const uint64_t* key = L.keys + (ok ? item : 0) * L.KW;
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                int k = k0 + rr + q;
+                double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+                if (ok && k < n_src) {
+                    int grow = src_row + k;
+                    if (key_bit(key, grow)) {
+                        const double2* p = reinterpret_cast<const double2*>(L.Z + (item * L.zs + grow) * 4);
+                        a = __ldg(p);
+                        b = __ldg(p + 1);
+                    }
+                }
+                v[q * 4 + 0] = a.x; v[q * 4 + 1] = a.y; v[q * 4 + 2] = b.x; v[q * 4 + 3] = b.y;
+            }
+        } else {
+            // 64 points x 16 rows: thread -> point tid/2, rows 8*(tid%2) .. +7
+            int pt = tid >> 1, rr = (tid & 1) * 8;
+            int64_t item = n0 + pt;
+            bool ok = item < L.n_items;
+            const uint64_t* key = L.keys + (ok ? item : 0) * L.KW;
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                int k = k0 + rr + q;
+                double val = 0.0;
+                if (ok && k < n_src) {
+                    int grow = src_row + k;
+                    if (key_bit(key, grow)) val = __ldg(L.Z + item * L.zs + grow);
+                }
+                v[q] = val;
+            }
+        }
+    }
+    __device__ __forceinline__ void store(double* xs) {
+        int tid = threadIdx.x;
+        if (C == 4) {
+            int it = tid >> 3, rr = (tid & 7) * 2;
+#pragma unroll
+            for (int q = 0; q < 2; q++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) xs[(it * 4 + c) * XLD + rr + q] = v[q * 4 + c];
+        } else {
+            int pt = tid >> 1, rr = (tid & 1) * 8;
+#pragma unroll
+            for (int q = 0; q < 8; q++) xs[pt * XLD + rr + q] = v[q];
+        }
+    }
+};
+
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
+                                                        const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
+    extern __shared__ uint8_t smem_raw[];
+    GemmSmem& S = *reinterpret_cast<GemmSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const StepDev& st = L.st;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int m0 = blockIdx.y * BM;
+    const int64_t n0 = (int64_t)blockIdx.x * BN;
+
+    const bool lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && !(st.flags & AM_STEP_SC_FROM_INPUT);
+    const int kc0 = (st.n_in + BK - 1) / BK;
+    const int kc1 = lin ? (st.n_sin + BK - 1) / BK : 0;
+    const int nchunks = kc0 + kc1;
+
+    if (tid == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    }
+    if (C == 1 && tid < BN) { S.bits[tid][0] = 0; S.bits[tid][1] = 0; }
+    __syncthreads();
+
+    auto issue_w = [&](int c, int stage) {
+        if (tid == 0) {
+            mbar_expect_tx(&S.bar[stage], BM * BK * sizeof(double));
+            if (c < kc0) tma_load_2d(S.w[stage], &tmW, &S.bar[stage], c * BK, m0);
+            else tma_load_2d(S.w[stage], &tmV, &S.bar[stage], (c - kc0) * BK, m0);
+        }
+    };
+    XStager<C> xs;
+    auto load_x = [&](int c) {
+        if (c < kc0) xs.load(L, n0, st.in_row_off, st.n_in, c * BK);
+        else xs.load(L, n0, st.sin_row_off, st.n_sin, (c - kc0) * BK);
+    };
+
+    double acc[2][4][4];
+#pragma unroll
+    for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+#pragma unroll
+            for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+
+    issue_w(0, 0);
+    load_x(0);
+    xs.store(S.x[0]);
+    __syncthreads();
+
+    for (int c = 0; c < nchunks; c++) {
+        const int s = c & 1;
+        if (c + 1 < nchunks) {
+            issue_w(c + 1, s ^ 1);
+            load_x(c + 1);
+        }
+        mbar_wait(&S.bar[s], (c >> 1) & 1);
+        const double* ws = S.w[s];
+        const double* xsm = S.x[s];
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double a[2][2], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 2; mi++) {
+                int r = wm * 32 + mi * 16 + g;
+                a[mi][0] = ws[swz(r, kk + t)];
+                a[mi][1] = ws[swz(r + 8, kk + t)];
+            }
+#pragma unroll
+            for (int nj = 0; nj < 4; nj++) b[nj] = xsm[(wn * 32 + nj * 8 + g) * XLD + kk + t];
+#pragma unroll
+            for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+                for (int nj = 0; nj < 4; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
+        }
+        if (c + 1 < nchunks) xs.store(S.x[s ^ 1]);
+        __syncthreads();
+    }
+
+    // ---------------------------------------------------------- epilogue
+    const bool sc_ident = st.flags & AM_STEP_SHORTCUT_IDENT;
+    const bool sc_input_lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && (st.flags & AM_STEP_SC_FROM_INPUT);
+    const bool sc_input_id = sc_ident && (st.flags & AM_STEP_SC_FROM_INPUT);
+    const bool has_sc = (st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR)) != 0;
+    const int wbase = (st.row_off + m0) >> 6;  // forward: first key word the tile touches
+
+#pragma unroll
+    for (int mi = 0; mi < 2; mi++) {
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+            const int rl = wm * 32 + mi * 16 + g + half * 8;  // local row
+            const int r = m0 + rl;
+            const bool rok = r < st.n_out;
+            const int row = st.row_off + r;
+#pragma unroll
+            for (int nj = 0; nj < 4; nj++) {
+                const int64_t col = n0 + wn * 32 + nj * 8 + 2 * t;
+                double v0 = acc[mi][nj][half * 2], v1 = acc[mi][nj][half * 2 + 1];
+                if (C == 4) {
+                    const int64_t item = col >> 2;
+                    const int comp = (int)(col & 3);  // 0 (even t) or 2 (odd t)
+                    const bool ok = rok && item < L.n_items;
+                    if (ok && has_sc) {
+                        double s0 = 0.0, s1 = 0.0;
+                        if (sc_input_id) {            // A_in = I, c_in = 0 (block starts at x)
+                            s0 = (comp == r) ? 1.0 : 0.0;
+                            s1 = (comp == 0 && r == 1) ? 1.0 : 0.0;
+                        } else if (sc_input_lin) {    // V @ I = V[:, :3], V @ 0 + vb
+                            const double* vr = st.V + (int64_t)r * st.ldv;
+                            s0 = vr[comp];
+                            s1 = comp == 0 ? vr[1] : (st.vb ? st.vb[r] : 0.0);
+                        } else if (sc_ident) {        // masked block input rows
+                            const uint64_t* key = L.keys + item * L.KW;
+                            int srow = st.sin_row_off + r;
+                            if (key_bit(key, srow)) {
+                                double2 p = *reinterpret_cast<const double2*>(L.Z + (item * L.zs + srow) * 4 + comp);
+                                s0 = p.x; s1 = p.y;
+                            }
+                        } else {                      // V @ A_in is in acc (second K segment); add vb
+                            s1 = (comp == 2 && st.vb) ? st.vb[r] : 0.0;
+                        }
+                        v0 = s0 + v0;   // pre_A = sA + W A ; pre_c = (sc + W c) + b
+                        v1 = s1 + v1;
+                    }
+                    if (comp == 2) v1 = v1 + (ok ? st.b[r] : 0.0);
+                    // canonical bit: the pair (t, t^1) holds the 4 components of (item, row)
+                    double p0 = __shfl_xor_sync(0xffffffffu, v0, 1);
+                    double p1 = __shfl_xor_sync(0xffffffffu, v1, 1);
+                    if (ok) {
+                        double c0, c1, c2, c3;
+                        if (comp == 0) { c0 = v0; c1 = v1; c2 = p0; c3 = p1; }
+                        else { c0 = p0; c1 = p1; c2 = v0; c3 = v1; }
+                        if (comp == 0) {
+                            double nrm = sqrt((c0 * c0 + c1 * c1) + c2 * c2);
+                            if (!(nrm > kDegen)) {
+                                uint64_t* key = L.keys + item * L.KW;
+                                int bit = c3 > 0.0;
+                                if (bit != key_bit(key, row)) {
+                                    set_key_bit(key, row, bit);
+                                    if (L.changed) L.changed[item] = 1;
+                                }
+                            }
+                        }
+                        *reinterpret_cast<double2*>(L.Z + (item * L.zs + row) * 4 + comp) = make_double2(v0, v1);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        const int64_t item = col + e;
+                        double v = e ? v1 : v0;
+                        if (!(rok && item < L.n_items)) continue;
+                        double pre;
+                        if (has_sc) {
+                            double sc = 0.0;
+                            const double* x = L.pts ? L.pts + item * 3 : nullptr;
+                            if (sc_input_id) {
+                                sc = x[r];
+                            } else if (sc_input_lin) {
+                                const double* vr = st.V + (int64_t)r * st.ldv;
+                                sc = (x[0] * vr[0] + x[1] * vr[1]) + x[2] * vr[2];
+                                if (st.vb) sc = sc + st.vb[r];
+                            } else if (sc_ident) {
+                                int srow = st.sin_row_off + r;
+                                if (key_bit(L.keys + item * L.KW, srow)) sc = L.Z[item * L.zs + srow];
+                            } else if (st.vb) {
+                                sc = st.vb[r];  // V h_in is in acc (second K segment)
+                            }
+                            pre = (sc + v) + st.b[r];   // reference: shortcut(h_in) + h W^T + b
+                        } else {
+                            pre = v + st.b[r];
+                        }
+                        L.Z[item * L.zs + row] = pre;
+                        if (pre > 0.0) {
+                            int lb = row - wbase * 64;
+                            atomicOr(&S.bits[(int)(item - n0)][lb >> 6], (unsigned long long)key_mask(lb));
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (C == 1) {
+        __syncthreads();
+        if (tid < BN) {
+            int64_t item = n0 + tid;
+            if (item < L.n_items) {
+                uint64_t* key = L.keys + item * L.KW;
+                int nwords = (L.KW);
+                if (S.bits[tid][0]) atomicOr(reinterpret_cast<unsigned long long*>(key + wbase), S.bits[tid][0]);
+                if (S.bits[tid][1] && wbase + 1 < nwords)
+                    atomicOr(reinterpret_cast<unsigned long long*>(key + wbase + 1), S.bits[tid][1]);
+            }
+        }
+    }
+}
+
+void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV, cudaStream_t s) {
+    if (L.n_items <= 0) return;
+    int64_t cols = L.n_items * C;
+    dim3 grid((unsigned)((cols + BN - 1) / BN), (unsigned)((L.st.n_out + BM - 1) / BM));
+    size_t smem = sizeof(GemmSmem) + 1024;
+    if (C == 4) {
+        static bool init = false;
+        if (!init) { cudaFuncSetAttribute(k_gemm_step<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
+        k_gemm_step<4><<<grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L);
+    } else {
+        static bool init = false;
+        if (!init) { cudaFuncSetAttribute(k_gemm_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
+        k_gemm_step<1><<<grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L);
+    }
+}
+
+// ------------------------------------------------------------ head kernels
+struct SubDev {
+    int last_row, last_n;
+    const double* hw;
+    double hb;
+};
+
+// face functional of every subnetwork: head_w @ (s ⊙ Z_last) (+ head_b on the offset)
+// reference network.py:440-442
+__global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces, int64_t n_items, int zs, int KW,
+                            const SubDev* subs, int n_subs) {
+    int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    int64_t item = wid / n_subs;
+    int j = (int)(wid - item * n_subs);
+    if (item >= n_items) return;
+    const SubDev sd = subs[j];
+    const uint64_t* key = keys + item * KW;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int r = lane; r < sd.last_n; r += 32) {
+        int row = sd.last_row + r;
+        if (!key_bit(key, row)) continue;
+        const double2* p = reinterpret_cast<const double2*>(Z + (item * zs + row) * 4);
+        double2 x = p[0], y = p[1];
+        double w = sd.hw[r];
+        a0 += w * x.x; a1 += w * x.y; a2 += w * y.x; a3 += w * y.y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+    }
+    if (lane == 0) {
+        double* f = faces + (item * n_subs + j) * 4;
+        f[0] = a0; f[1] = a1; f[2] = a2; f[3] = a3 + sd.hb;
+    }
+}
+
+// F_j(x) = head_w @ relu(Z_last) + head_b; F = max_j (argmax lowest index) -- reference network.py:352-392
+__global__ void k_forward_head(const double* Z, uint64_t* keys, double* vals, int64_t n_items, int zs, int KW,
+                               const SubDev* subs, int n_subs, int ensemble) {
+    int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (item >= n_items) return;
+    const uint64_t* key = keys + item * KW;
+    double best = 0.0;
+    int arg = 0;
+    for (int j = 0; j < n_subs; j++) {
+        const SubDev sd = subs[j];
+        double a = 0.0;
+        for (int r = lane; r < sd.last_n; r += 32) {
+            int row = sd.last_row + r;
+            if (key_bit(key, row)) a += Z[item * zs + row] * sd.hw[r];
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        double f = a + sd.hb;
+        if (j == 0 || f > best) { best = f; arg = j; }
+    }
+    if (lane == 0) {
+        if (vals) vals[item] = best;
+        if (ensemble) keys[item * KW + KW - 1] = (uint64_t)arg;
+    }
+}
+
+void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, int64_t n_items, int zs, int KW,
+                          const void* subs, int n_subs, cudaStream_t s) {
+    int64_t warps = n_items * n_subs;
+    if (warps <= 0) return;
+    k_face_head<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(Z, keys, faces, n_items, zs, KW,
+                                                                    static_cast<const SubDev*>(subs), n_subs);
+}
+void launch_forward_head_dev(const double* Z, uint64_t* keys, double* vals, int64_t n_items, int zs, int KW,
+                             const void* subs, int n_subs, int ensemble, cudaStream_t s) {
+    if (n_items <= 0) return;
+    k_forward_head<<<(unsigned)((n_items * 32 + 255) / 256), 256, 0, s>>>(
+        Z, keys, vals, n_items, zs, KW, static_cast<const SubDev*>(subs), n_subs, ensemble);
+}
+
+}  // namespace am

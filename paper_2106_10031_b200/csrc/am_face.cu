@@ -1,0 +1,594 @@
+// am_face.cu -- analytic-face polygon solver, one warp per cell.
+//
+// For a visited cell the face polygon is { x : F-plane(x) = 0, every oriented
+// cell constraint (neuron planes, branch-dominance planes, box faces) <= tol }.
+// The reference enumerates it naively (all plane pairs, reference
+// cells.py:337-362) or by the pivot walk (cells.py:381-462).  Here:
+//
+//   pass A  the warp streams all K constraint rows (coalesced 32 B plane rows
+//           straight from the composition buffer), projects them into a 2-D
+//           frame of the face plane and clips a polygon by every half-plane
+//           shifted by tol (32 rows tested per step, cutting rows applied with a
+//           warp-parallel Sutherland-Hodgman step, one lane per vertex).  The
+//           result is P_tol, the tol-dilated face polygon.
+//   pass B  streams the rows again and keeps the set C of rows that come within
+//           tol of P_tol.  Every pair whose solution the reference accepts, every
+//           incident plane and every edge-midpoint plane lies in C (DESIGN.md
+//           §Face solver proves it), and C is tiny (~the polygon's edge count).
+//   exact   the reference's own vertex semantics run on C only: canonical-pair
+//           3x3 LU solves, tol_cell membership, incident sets, greedy weld-radius
+//           dedup with lexicographic representatives, angular ordering, CCW
+//           orientation, canonical rotation and per-edge transition planes.
+//   expand  each crossable edge emits the neighbour states of
+//           reference marching.py:152-186 (flip subsets x branch targets) and a
+//           probe point 1e-7 across its first plane (marching.py:271-276).
+#include <cstdio>
+
+#include "am_internal.h"
+
+namespace am {
+
+constexpr int VMAX = 32;   // clip polygon capacity (one lane per vertex)
+constexpr int CMAX = 64;   // candidate plane set capacity (uint64 masks)
+constexpr int QMAX = 64;   // accepted raw vertices
+constexpr int EMAXC = 48;  // candidate descriptors per cell
+constexpr int FW = 4;      // warps per CTA
+constexpr double kCDelta = 1e-10;
+
+struct FaceWarp {
+    double ps[2][VMAX], pt[2][VMAX];
+    double cn[CMAX][4];
+    int cid[CMAX];
+    double qv[QMAX][3];
+    unsigned long long qs[QMAX];
+    double rv[QMAX][3];
+    double rf[QMAX][3];
+    unsigned long long rs[QMAX];
+    double ang[QMAX];
+    int ord[QMAX];
+    double fv[QMAX][3];           // final loop
+    unsigned long long fs[QMAX];
+    unsigned long long erow[QMAX];  // per-edge C-row mask of the transition planes
+    int eargmin[QMAX];              // per-edge global row when the mask is empty (argmin fallback)
+    // candidate descriptors: flip bits (<= 4, or -1 = "all bits of edge e") and branch target
+    int cd_edge[EMAXC], cd_nflip[EMAXC], cd_flip[EMAXC][4], cd_branch[EMAXC];
+    int n_cd;
+    int status;
+    long long cbase;
+};
+
+struct Ctx {
+    const double* Z;   // this item's rows
+    const double* faces;
+    const uint64_t* key;
+    int NB, M, branch, ensemble, K;
+    double lo[3], hi[3];
+};
+
+// unit oriented constraint row of global plane id gr (reference cells.py:127-185); false if dropped
+__device__ __forceinline__ bool get_row(const Ctx& c, int gr, double n[3], double& o) {
+    if (gr < c.NB) {
+        const double2* p = reinterpret_cast<const double2*>(c.Z + (int64_t)gr * 4);
+        double2 a = __ldg(p), b = __ldg(p + 1);
+        double nrm = sqrt((a.x * a.x + a.y * a.y) + b.x * b.x);
+        if (!(nrm > kDegen)) return false;
+        double orient = key_bit(c.key, gr) ? -1.0 : 1.0;
+        n[0] = (a.x * orient) / nrm; n[1] = (a.y * orient) / nrm; n[2] = (b.x * orient) / nrm;
+        o = (b.y * orient) / nrm;
+        return true;
+    }
+    if (gr < c.NB + c.M) {
+        int t = gr - c.NB;
+        if (!c.ensemble || t == c.branch) return false;
+        const double* ft = c.faces + t * 4;
+        const double* fj = c.faces + c.branch * 4;
+        double d0 = ft[0] - fj[0], d1 = ft[1] - fj[1], d2 = ft[2] - fj[2], dc = ft[3] - fj[3];
+        double nrm = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+        if (!(nrm > kDegen)) return false;
+        n[0] = d0 / nrm; n[1] = d1 / nrm; n[2] = d2 / nrm; o = dc / nrm;
+        return true;
+    }
+    int k = gr - c.NB - c.M;
+    int ax = k >> 1;
+    n[0] = n[1] = n[2] = 0.0;
+    if ((k & 1) == 0) { n[ax] = 1.0; o = -c.hi[ax]; }
+    else { n[ax] = -1.0; o = c.lo[ax]; }
+    return true;
+}
+
+__device__ __forceinline__ double dot3(const double* a, const double* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+// 3x3 LU with partial pivoting, same operation order as oracle solve3 (LAPACK getf2/getrs)
+__device__ double solve3(const double Min[9], const double rin[3], double x[3]) {
+    double a[9], b[3];
+#pragma unroll
+    for (int i = 0; i < 9; i++) a[i] = Min[i];
+    b[0] = rin[0]; b[1] = rin[1]; b[2] = rin[2];
+    double sign = 1.0;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        int p = k;
+        double best = fabs(a[k * 3 + k]);
+        for (int i = k + 1; i < 3; i++)
+            if (fabs(a[i * 3 + k]) > best) { best = fabs(a[i * 3 + k]); p = i; }
+        if (p != k) {
+            for (int j = 0; j < 3; j++) { double tt = a[k * 3 + j]; a[k * 3 + j] = a[p * 3 + j]; a[p * 3 + j] = tt; }
+            double tt = b[k]; b[k] = b[p]; b[p] = tt;
+            sign = -sign;
+        }
+        double piv = a[k * 3 + k];
+        if (piv == 0.0) return 0.0;
+        double rp = 1.0 / piv;
+        for (int i = k + 1; i < 3; i++) {
+            double l = a[i * 3 + k] * rp;
+            a[i * 3 + k] = l;
+            for (int j = k + 1; j < 3; j++) a[i * 3 + j] -= l * a[k * 3 + j];
+            b[i] -= l * b[k];
+        }
+    }
+    double det = fabs(sign * a[0] * a[4] * a[8]);
+    x[2] = b[2] / a[8];
+    x[1] = (b[1] - a[5] * x[2]) / a[4];
+    x[0] = ((b[0] - a[1] * x[1]) - a[2] * x[2]) / a[0];
+    return det;
+}
+
+__device__ __forceinline__ bool lex_less(const double* a, const double* b) {
+    if (a[0] != b[0]) return a[0] < b[0];
+    if (a[1] != b[1]) return a[1] < b[1];
+    return a[2] < b[2];
+}
+
+__global__ void __launch_bounds__(FW * 32) k_face(FaceArgs A) {
+    extern __shared__ uint8_t smem_raw[];
+    FaceWarp* W = reinterpret_cast<FaceWarp*>(smem_raw) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const int64_t fi = (int64_t)blockIdx.x * FW + (threadIdx.x >> 5);
+    if (fi >= A.n) return;
+    const int item = A.items[fi];
+
+    Ctx c;
+    c.Z = A.Z + (int64_t)item * A.zs * 4;
+    c.faces = A.faces + (int64_t)item * A.M * 4;
+    c.key = A.keys + (int64_t)item * A.KW;
+    c.NB = A.NB; c.M = A.M; c.ensemble = A.ensemble;
+    c.branch = A.ensemble ? (int)c.key[A.KW - 1] : 0;
+    c.K = A.NB + A.M + 6;
+    for (int k = 0; k < 3; k++) { c.lo[k] = A.lo[k]; c.hi[k] = A.hi[k]; }
+    const double tol_c = A.tol_cell, tol_p = A.tol_onplane;
+    const double tol_max = fmax(tol_c, tol_p);
+
+    // ------------------------------------------------------ face plane
+    const double* fr = c.faces + c.branch * 4;
+    double fn = sqrt((fr[0] * fr[0] + fr[1] * fr[1]) + fr[2] * fr[2]);
+    double fu[3] = {0, 0, 0}, fo = 0.0;
+    bool face_ok = fn > kDegen;
+    if (face_ok) {
+        fu[0] = fr[0] / fn; fu[1] = fr[1] / fn; fu[2] = fr[2] / fn; fo = fr[3] / fn;
+        face_ok = sqrt((fu[0] * fu[0] + fu[1] * fu[1]) + fu[2] * fu[2]) > kDegen;
+    }
+    // 2-D frame (same basis as reference cells.py:275-285)
+    double ua[3] = {1.0, 0.0, 0.0};
+    if (!(fabs(fu[0]) < 0.9)) { ua[0] = 0.0; ua[1] = 1.0; }
+    double U[3] = {fu[1] * ua[2] - fu[2] * ua[1], fu[2] * ua[0] - fu[0] * ua[2], fu[0] * ua[1] - fu[1] * ua[0]};
+    double un = sqrt((U[0] * U[0] + U[1] * U[1]) + U[2] * U[2]);
+    U[0] /= un; U[1] /= un; U[2] /= un;
+    double Vv[3] = {fu[1] * U[2] - fu[2] * U[1], fu[2] * U[0] - fu[0] * U[2], fu[0] * U[1] - fu[1] * U[0]};
+    double P0[3] = {-fo * fu[0], -fo * fu[1], -fo * fu[2]};
+
+    int nv = 0, cur = 0;
+    int status = face_ok ? 0 : 1;  // 0 ok, 1 empty, 2 overflow
+    if (status == 0) {
+        // initial square, then clip: box rows first, then neurons, then branch rows
+        double R = 64.0;
+        for (int k = 0; k < 3; k++) R = fmax(R, 64.0 * fmax(fabs(c.lo[k]), fabs(c.hi[k])));
+        if (lane < 4) {
+            W->ps[0][lane] = (lane == 0 || lane == 3) ? -R : R;
+            W->pt[0][lane] = (lane < 2) ? -R : R;
+        }
+        nv = 4;
+        __syncwarp();
+        for (int base = 0; base < c.K && status == 0; base += 32) {
+            int idx = base + lane;
+            double n[3], o = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
+            bool cut = false;
+            if (idx < c.K) {
+                int gr = idx < 6 ? c.NB + c.M + idx : idx - 6;
+                if (get_row(c, gr, n, o)) {
+                    a2 = dot3(n, U); b2 = dot3(n, Vv); g2 = (dot3(n, P0) + o) - tol_c;
+                    double mx = -1e300;
+                    for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+                    cut = mx > 0.0;
+                }
+            }
+            unsigned mask = __ballot_sync(full, cut);
+            while (mask) {
+                int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                double ca = __shfl_sync(full, a2, src), cb = __shfl_sync(full, b2, src), cg = __shfl_sync(full, g2, src);
+                // warp-parallel Sutherland-Hodgman step
+                double si = 0, ti = 0, di = 0;
+                if (lane < nv) { si = W->ps[cur][lane]; ti = W->pt[cur][lane]; di = ca * si + cb * ti + cg; }
+                int nxt = lane + 1 == nv ? 0 : lane + 1;
+                double sj = __shfl_sync(full, si, nxt & 31), tj = __shfl_sync(full, ti, nxt & 31),
+                       dj = __shfl_sync(full, di, nxt & 31);
+                bool in_i = di <= 0.0, in_j = dj <= 0.0;
+                int cnt = lane < nv ? (in_i ? 1 : 0) + (in_i != in_j ? 1 : 0) : 0;
+                int pre = cnt;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    int y = __shfl_up_sync(full, pre, o2);
+                    if (lane >= o2) pre += y;
+                }
+                int total = __shfl_sync(full, pre, 31);
+                pre -= cnt;
+                if (total > VMAX) { status = 2; break; }
+                int dst = cur ^ 1;
+                if (lane < nv) {
+                    int w = pre;
+                    if (in_i) { W->ps[dst][w] = si; W->pt[dst][w] = ti; w++; }
+                    if (in_i != in_j) {
+                        double lam = di / (di - dj);
+                        W->ps[dst][w] = si + lam * (sj - si);
+                        W->pt[dst][w] = ti + lam * (tj - ti);
+                    }
+                }
+                __syncwarp();
+                cur = dst;
+                nv = total;
+                if (nv < 3) { status = 1; break; }
+            }
+        }
+    }
+
+    // ------------------------------------------------ pass B: candidate set C
+    int nC = 0;
+    if (status == 0) {
+        for (int base = 0; base < c.K; base += 32) {
+            int gr = base + lane;
+            double n[3], o = 0.0;
+            bool in = false;
+            if (gr < c.K && get_row(c, gr, n, o)) {
+                double a2 = dot3(n, U), b2 = dot3(n, Vv), g2 = dot3(n, P0) + o;
+                double mx = -1e300;
+                for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+                in = mx >= -tol_max - kCDelta;
+            }
+            unsigned mask = __ballot_sync(full, in);
+            int pos = nC + __popc(mask & ((1u << lane) - 1u));
+            if (in && pos < CMAX) {
+                W->cn[pos][0] = n[0]; W->cn[pos][1] = n[1]; W->cn[pos][2] = n[2]; W->cn[pos][3] = o;
+                W->cid[pos] = gr;
+            }
+            nC += __popc(mask);
+        }
+        if (nC > CMAX) status = 2;
+        __syncwarp();
+    }
+
+    // ------------------------------------- exact vertex semantics on C
+    int nq = 0;
+    if (status == 0) {
+        int P = nC * (nC - 1) / 2;
+        for (int base = 0; base < P; base += 32) {
+            int p = base + lane;
+            bool valid = false;
+            double x[3];
+            unsigned long long set = 0;
+            if (p < P) {
+                // triu order: i from 0, j from i+1 (reference cells.py:344 np.triu_indices)
+                int i = 0, rem = p;
+                while (rem >= nC - 1 - i) { rem -= nC - 1 - i; i++; }
+                int j = i + 1 + rem;
+                double Mx[9] = {W->cn[i][0], W->cn[i][1], W->cn[i][2], W->cn[j][0], W->cn[j][1], W->cn[j][2],
+                                fu[0], fu[1], fu[2]};
+                double rhs[3] = {-W->cn[i][3], -W->cn[j][3], -fo};
+                double det = solve3(Mx, rhs, x);
+                if (det >= kTolDet) {
+                    valid = true;
+                    for (int r = 0; r < nC; r++) {
+                        double val = dot3(W->cn[r], x) + W->cn[r][3];
+                        if (!(val <= tol_c)) { valid = false; break; }
+                        if (fabs(val) <= tol_p) set |= 1ull << r;
+                    }
+                    set |= (1ull << i) | (1ull << j);
+                }
+            }
+            unsigned mask = __ballot_sync(full, valid);
+            int pos = nq + __popc(mask & ((1u << lane) - 1u));
+            if (valid && pos < QMAX) {
+                W->qv[pos][0] = x[0]; W->qv[pos][1] = x[1]; W->qv[pos][2] = x[2];
+                W->qs[pos] = set;
+            }
+            nq += __popc(mask);
+        }
+        if (nq > QMAX) status = 2;
+        else if (nq < 3) status = 1;
+        __syncwarp();
+    }
+
+    // dedup + ordering (lane 0; a handful of vertices)
+    int nr = 0;
+    if (status == 0) {
+        if (lane == 0) {
+            for (int q = 0; q < nq; q++) {
+                const double* x = W->qv[q];
+                int hit = -1;
+                for (int k = 0; k < nr; k++) {
+                    double d0 = W->rf[k][0] - x[0], d1 = W->rf[k][1] - x[1], d2 = W->rf[k][2] - x[2];
+                    if (sqrt((d0 * d0 + d1 * d1) + d2 * d2) <= A.tol_weld) { hit = k; break; }
+                }
+                if (hit < 0) {
+                    hit = nr++;
+                    for (int d = 0; d < 3; d++) { W->rf[hit][d] = x[d]; W->rv[hit][d] = x[d]; }
+                    W->rs[hit] = 0;
+                } else if (lex_less(x, W->rv[hit])) {
+                    for (int d = 0; d < 3; d++) W->rv[hit][d] = x[d];
+                }
+                W->rs[hit] |= W->qs[q];
+            }
+            if (nr >= 3) {
+                double cen[3] = {0, 0, 0};
+                for (int k = 0; k < nr; k++) { cen[0] += W->rv[k][0]; cen[1] += W->rv[k][1]; cen[2] += W->rv[k][2]; }
+                cen[0] /= nr; cen[1] /= nr; cen[2] /= nr;
+                for (int k = 0; k < nr; k++) {
+                    double r0 = W->rv[k][0] - cen[0], r1 = W->rv[k][1] - cen[1], r2 = W->rv[k][2] - cen[2];
+                    W->ang[k] = atan2((r0 * Vv[0] + r1 * Vv[1]) + r2 * Vv[2], (r0 * U[0] + r1 * U[1]) + r2 * U[2]);
+                    W->ord[k] = k;
+                }
+                for (int i = 1; i < nr; i++) {
+                    int tt = W->ord[i], j = i - 1;
+                    while (j >= 0 && W->ang[W->ord[j]] > W->ang[tt]) { W->ord[j + 1] = W->ord[j]; j--; }
+                    W->ord[j + 1] = tt;
+                }
+                double tot[3] = {0, 0, 0};
+                for (int i = 0; i < nr; i++) {
+                    const double* p = W->rv[W->ord[i]];
+                    const double* q = W->rv[W->ord[(i + 1) % nr]];
+                    tot[0] += p[1] * q[2] - p[2] * q[1];
+                    tot[1] += p[2] * q[0] - p[0] * q[2];
+                    tot[2] += p[0] * q[1] - p[1] * q[0];
+                }
+                double area = 0.5 * ((tot[0] * fu[0] + tot[1] * fu[1]) + tot[2] * fu[2]);
+                if (area < 0.0)
+                    for (int i = 0, j = nr - 1; i < j; i++, j--) { int tt = W->ord[i]; W->ord[i] = W->ord[j]; W->ord[j] = tt; }
+                int start = 0;
+                for (int k = 1; k < nr; k++)
+                    if (lex_less(W->rv[W->ord[k]], W->rv[W->ord[start]])) start = k;
+                for (int k = 0; k < nr; k++) {
+                    int src = W->ord[(k + start) % nr];
+                    for (int d = 0; d < 3; d++) W->fv[k][d] = W->rv[src][d];
+                    W->fs[k] = W->rs[src];
+                }
+            }
+            W->status = nr;
+        }
+        __syncwarp();
+        nr = W->status;
+        if (nr < 3) status = 1;
+    }
+
+    // per-edge transition planes (lane per edge)
+    if (status == 0) {
+        bool need_argmin = false;
+        for (int e = lane; e < nr; e += 32) {
+            const double* p = W->fv[e];
+            const double* q = W->fv[(e + 1) % nr];
+            double mid[3] = {0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2])};
+            unsigned long long on_mid = 0;
+            for (int r = 0; r < nC; r++)
+                if (fabs(dot3(W->cn[r], mid) + W->cn[r][3]) <= tol_p) on_mid |= 1ull << r;
+            unsigned long long shared = W->fs[e] & W->fs[(e + 1) % nr];
+            unsigned long long rows = shared & on_mid;
+            if (!rows) rows = shared ? shared : on_mid;
+            W->erow[e] = rows;
+            W->eargmin[e] = -1;
+            if (!rows) need_argmin = true;
+        }
+        // rare: no plane within tol of the edge -> argmin over every cell row (reference cells.py:327-328)
+        unsigned am_mask = __ballot_sync(full, need_argmin);
+        __syncwarp();
+        if (am_mask) {
+            for (int e = 0; e < nr; e++) {
+                if (W->erow[e]) continue;
+                const double* p = W->fv[e];
+                const double* q = W->fv[(e + 1) % nr];
+                double mid[3] = {0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2])};
+                double best = 1e300;
+                int bi = 0x7fffffff;
+                for (int gr = lane; gr < c.K; gr += 32) {
+                    double n[3], o;
+                    if (!get_row(c, gr, n, o)) continue;
+                    double v = fabs(dot3(n, mid) + o);
+                    if (v < best) { best = v; bi = gr; }
+                }
+                for (int o2 = 16; o2; o2 >>= 1) {
+                    double ob = __shfl_xor_sync(full, best, o2);
+                    int oi = __shfl_xor_sync(full, bi, o2);
+                    if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                }
+                if (lane == 0) W->eargmin[e] = bi;
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    }
+
+    // ------------------------------------------------------------ emit cell
+    int64_t cell = 0;
+    if (lane == 0) {
+        cell = (int64_t)atomicAdd(A.n_cells, 1ull);
+        if (status == 2) atomicAdd(&A.overflow[0], 1ull);
+    }
+    cell = __shfl_sync(full, cell, 0);
+    if (cell >= A.cap_cells) {
+        if (lane == 0) atomicAdd(&A.overflow[1], 1ull);
+        return;
+    }
+    if (status != 0) {
+        if (lane == 0) {
+            A.cell_pool[cell] = A.pool_idx[fi];
+            A.cell_nv[cell] = status == 2 ? -1 : 0;
+            A.cell_voff[cell] = 0;
+        }
+        return;
+    }
+    int64_t voff = 0, roff = 0;
+    int nrefs_total = 0;
+    for (int e = 0; e < nr; e++) nrefs_total += W->erow[e] ? __popcll(W->erow[e]) : 1;
+    if (lane == 0) {
+        voff = (int64_t)atomicAdd(A.n_verts, (unsigned long long)nr);
+        roff = (int64_t)atomicAdd(A.n_refs, (unsigned long long)nrefs_total);
+    }
+    voff = __shfl_sync(full, voff, 0);
+    roff = __shfl_sync(full, roff, 0);
+    if (voff + nr > A.cap_verts || roff + nrefs_total > A.cap_refs) {
+        if (lane == 0) {
+            atomicAdd(&A.overflow[1], 1ull);
+            A.cell_pool[cell] = A.pool_idx[fi];
+            A.cell_nv[cell] = -2;
+            A.cell_voff[cell] = 0;
+        }
+        return;
+    }
+    if (lane == 0) {
+        A.cell_pool[cell] = A.pool_idx[fi];
+        A.cell_nv[cell] = nr;
+        A.cell_voff[cell] = voff;
+        int64_t ro = roff;
+        for (int e = 0; e < nr; e++) {
+            A.verts[(voff + e) * 3 + 0] = W->fv[e][0];
+            A.verts[(voff + e) * 3 + 1] = W->fv[e][1];
+            A.verts[(voff + e) * 3 + 2] = W->fv[e][2];
+            A.edge_roff[voff + e] = ro;
+            int cnt = 0;
+            if (W->erow[e]) {
+                unsigned long long m = W->erow[e];
+                while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; A.edge_refs[ro++] = W->cid[r]; cnt++; }
+            } else {
+                A.edge_refs[ro++] = W->eargmin[e];
+                cnt = 1;
+            }
+            A.edge_nrefs[voff + e] = cnt;
+        }
+        // ---------------- neighbour candidates (reference marching.py:152-186, 262-288)
+        int ncd = 0;
+        const int box0 = c.NB + c.M;
+        for (int e = 0; e < nr; e++) {
+            int ids[64], nid = 0;
+            if (W->erow[e]) {
+                unsigned long long m = W->erow[e];
+                while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; if (W->cid[r] < box0) ids[nid++] = r; }
+            } else if (W->eargmin[e] < box0) {
+                ids[nid++] = -1 - W->eargmin[e];  // global id encoded (no C row)
+            }
+            if (!nid) continue;
+            int bits[64], nb = 0, brs[64], nbr = 0;
+            for (int i = 0; i < nid; i++) {
+                int gid = ids[i] >= 0 ? W->cid[ids[i]] : -1 - ids[i];
+                if (gid < c.NB) bits[nb++] = gid; else brs[nbr++] = gid - c.NB;
+            }
+            // subsets: combinations of sizes 0..nb (nb <= 3) or singles + full + () (nb > 3)
+            int nsub = 0, sub_mask[16];
+            bool big = nb > 3;
+            if (big) {
+                nsub = nb + 2;
+            } else {
+                for (int k = 0; k <= nb; k++) {
+                    int idx[4];
+                    for (int i = 0; i < k; i++) idx[i] = i;
+                    for (;;) {
+                        int mk = 0;
+                        for (int i = 0; i < k; i++) mk |= 1 << idx[i];
+                        sub_mask[nsub++] = mk;
+                        int i = k - 1;
+                        while (i >= 0 && idx[i] == nb - k + i) i--;
+                        if (i < 0) break;
+                        idx[i]++;
+                        for (int tt = i + 1; tt < k; tt++) idx[tt] = idx[tt - 1] + 1;
+                    }
+                }
+            }
+            for (int si = 0; si < nsub; si++) {
+                for (int ti = -1; ti < nbr; ti++) {
+                    bool empty_sub = big ? (si == nb + 1) : (sub_mask[si] == 0);
+                    if (empty_sub && ti < 0) continue;
+                    if (ncd >= EMAXC) { atomicAdd(&A.overflow[0], 1ull); continue; }
+                    W->cd_edge[ncd] = e;
+                    W->cd_branch[ncd] = ti >= 0 ? brs[ti] : -1;
+                    int nf = 0;
+                    if (big) {
+                        if (si < nb) { W->cd_flip[ncd][0] = bits[si]; nf = 1; }
+                        else if (si == nb) { nf = -1; }   // all bits of the edge
+                    } else {
+                        for (int i = 0; i < nb; i++)
+                            if (sub_mask[si] & (1 << i)) W->cd_flip[ncd][nf++] = bits[i];
+                    }
+                    W->cd_nflip[ncd] = nf;
+                    ncd++;
+                }
+            }
+            // probe across crossable[0] (the lowest non-box plane id of the edge)
+            int pr = ids[0];
+            double pn[3];
+            if (pr >= 0) { pn[0] = W->cn[pr][0]; pn[1] = W->cn[pr][1]; pn[2] = W->cn[pr][2]; }
+            else { double o; get_row(c, -1 - pr, pn, o); }
+            const double* p = W->fv[e];
+            const double* q = W->fv[(e + 1) % nr];
+            double mid[3] = {0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2])};
+            unsigned long long pi = atomicAdd(A.n_probe, 1ull);
+            if ((int64_t)pi < A.cap_probe) {
+                A.probe_pts[pi * 3 + 0] = mid[0] + A.probe_delta * pn[0];
+                A.probe_pts[pi * 3 + 1] = mid[1] + A.probe_delta * pn[1];
+                A.probe_pts[pi * 3 + 2] = mid[2] + A.probe_delta * pn[2];
+            } else {
+                atomicAdd(&A.overflow[1], 1ull);
+            }
+        }
+        W->n_cd = ncd;
+        W->cbase = (long long)atomicAdd(A.n_cand, (unsigned long long)ncd);
+    }
+    __syncwarp();
+    const int ncd = W->n_cd;
+    const int64_t cbase = W->cbase;
+    // write candidate keys cooperatively: word w of candidate k
+    for (int k = 0; k < ncd; k++) {
+        int64_t ci = cbase + k;
+        if (ci >= A.cap_cand) { if (lane == 0) atomicAdd(&A.overflow[1], 1ull); continue; }
+        uint64_t* dst = A.cand + ci * A.KW;
+        for (int w = lane; w < A.KW; w += 32) {
+            uint64_t word = c.key[w];
+            int nf = W->cd_nflip[k];
+            if (nf >= 0) {
+                for (int f = 0; f < nf; f++) {
+                    int b = W->cd_flip[k][f];
+                    if ((b >> 6) == w) word ^= key_mask(b);
+                }
+            } else {
+                int e = W->cd_edge[k];
+                unsigned long long m = W->erow[e];
+                while (m) {
+                    int r = __ffsll((long long)m) - 1; m &= m - 1;
+                    int b = W->cid[r];
+                    if (b < c.NB && (b >> 6) == w) word ^= key_mask(b);
+                }
+            }
+            if (A.ensemble && w == A.KW - 1 && W->cd_branch[k] >= 0) word = (uint64_t)W->cd_branch[k];
+            dst[w] = word;
+        }
+    }
+}
+
+void launch_face(const FaceArgs& a, cudaStream_t s) {
+    if (a.n <= 0) return;
+    size_t smem = sizeof(FaceWarp) * FW;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_face, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init = true;
+    }
+    k_face<<<(unsigned)((a.n + FW - 1) / FW), FW * 32, smem, s>>>(a);
+}
+
+}  // namespace am

@@ -1,0 +1,106 @@
+// am_seed.cu -- seed refinement and bisection triggering, batched over seeds.
+// reference marching.py:201-213 (_refine_seed_state), seeding.py:84-112 (seed_dichotomy)
+#include "am_internal.h"
+
+namespace am {
+
+static inline unsigned nb(int64_t n) { return (unsigned)((n + 127) / 128); }
+
+// x_proj = x - (n.x + c)/nn * n on the face plane of canonical(s); nn <= 0 -> done
+__global__ void k_seed_project(const double* X, const double* faces, const uint64_t* keys, int KW, int M,
+                               int ensemble, int64_t n, const int32_t* active, double* Xp, int32_t* done_flat) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    done_flat[i] = 0;
+    if (!active[i]) return;
+    int br = ensemble ? (int)keys[i * KW + KW - 1] : 0;
+    const double* f = faces + (i * M + br) * 4;
+    const double* x = X + i * 3;
+    double nn = (f[0] * f[0] + f[1] * f[1]) + f[2] * f[2];
+    if (nn <= 0.0) { done_flat[i] = 1; return; }
+    double t = (((f[0] * x[0] + f[1] * x[1]) + f[2] * x[2]) + f[3]) / nn;
+    Xp[i * 3 + 0] = x[0] - t * f[0];
+    Xp[i * 3 + 1] = x[1] - t * f[1];
+    Xp[i * 3 + 2] = x[2] - t * f[2];
+}
+
+// snew == null: finalize active seeds flagged in done_flat (or all active if done_flat null)
+// with result = canon.  Otherwise: snew == canon -> result = canon, inactive; else x = xp, s = snew.
+__global__ void k_seed_check(const uint64_t* snew, const uint64_t* canon, int KW, int64_t n, int32_t* active,
+                             double* X, const double* Xp, uint64_t* S, uint64_t* result, int32_t* done_flat) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !active[i]) return;
+    if (!snew) {
+        if (done_flat && !done_flat[i]) return;
+        for (int w = 0; w < KW; w++) result[i * KW + w] = canon[i * KW + w];
+        active[i] = 0;
+        return;
+    }
+    bool eq = true;
+    for (int w = 0; w < KW; w++) eq &= snew[i * KW + w] == canon[i * KW + w];
+    if (eq) {
+        for (int w = 0; w < KW; w++) result[i * KW + w] = canon[i * KW + w];
+        active[i] = 0;
+    } else {
+        X[i * 3 + 0] = Xp[i * 3 + 0]; X[i * 3 + 1] = Xp[i * 3 + 1]; X[i * 3 + 2] = Xp[i * 3 + 2];
+        for (int w = 0; w < KW; w++) S[i * KW + w] = snew[i * KW + w];
+    }
+}
+
+void launch_seed_project(const double* X, const double* faces, const uint64_t* keys, int KW, int M, int ensemble,
+                         int64_t n, const int32_t* active, double* Xp, int32_t* done_flat, cudaStream_t s) {
+    if (n > 0) k_seed_project<<<nb(n), 128, 0, s>>>(X, faces, keys, KW, M, ensemble, n, active, Xp, done_flat);
+}
+void launch_seed_check(const uint64_t* snew, const uint64_t* canon, int KW, int64_t n, int32_t* active, double* X,
+                       const double* Xp, uint64_t* S, uint64_t* result, int32_t* done_flat, cudaStream_t s) {
+    if (n > 0) k_seed_check<<<nb(n), 128, 0, s>>>(snew, canon, KW, n, active, X, Xp, S, result, done_flat);
+}
+
+// one bisection step given F(mid) (reference seeding.py:96-112)
+__global__ void k_dichotomy_step(const double* vals, double* xp, double* xn, double* fp, double* fn, double* mid,
+                                 int32_t* active, double* out, int64_t n, double eps, double seed_tol, int last) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !active[i]) return;
+    double fm = vals[i];
+    double* m = mid + i * 3;
+    if (fabs(fm) <= seed_tol) {
+        out[i * 3 + 0] = m[0]; out[i * 3 + 1] = m[1]; out[i * 3 + 2] = m[2];
+        active[i] = 0;
+        return;
+    }
+    if (fm > 0.0) { xp[i * 3] = m[0]; xp[i * 3 + 1] = m[1]; xp[i * 3 + 2] = m[2]; fp[i] = fm; }
+    else { xn[i * 3] = m[0]; xn[i * 3 + 1] = m[1]; xn[i * 3 + 2] = m[2]; fn[i] = fm; }
+    if (fp[i] - fn[i] <= eps || last) {
+        const double* src = fabs(fp[i]) <= fabs(fn[i]) ? xp + i * 3 : xn + i * 3;
+        out[i * 3 + 0] = src[0]; out[i * 3 + 1] = src[1]; out[i * 3 + 2] = src[2];
+        active[i] = 0;
+        return;
+    }
+    m[0] = 0.5 * (xp[i * 3] + xn[i * 3]);
+    m[1] = 0.5 * (xp[i * 3 + 1] + xn[i * 3 + 1]);
+    m[2] = 0.5 * (xp[i * 3 + 2] + xn[i * 3 + 2]);
+}
+void launch_dichotomy_step(const double* vals, double* xp, double* xn, double* fp, double* fn, double* mid,
+                           int32_t* active, double* out, int64_t n, double eps, double seed_tol, int last,
+                           cudaStream_t s) {
+    if (n > 0) k_dichotomy_step<<<nb(n), 128, 0, s>>>(vals, xp, xn, fp, fn, mid, active, out, n, eps, seed_tol, last);
+}
+
+}  // namespace am
+
+namespace am {
+__global__ void k_midpoint(const double* a, const double* b, double* m, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n * 3) m[i] = 0.5 * (a[i] + b[i]);
+}
+void launch_midpoint(const double* a, const double* b, double* m, int64_t n, cudaStream_t s) {
+    if (n > 0) k_midpoint<<<(unsigned)((n * 3 + 127) / 128), 128, 0, s>>>(a, b, m, n);
+}
+__global__ void k_count_active(const int32_t* active, int64_t n, unsigned long long* cnt) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && active[i]) atomicAdd(cnt, 1ull);
+}
+void launch_count_active(const int32_t* active, int64_t n, unsigned long long* cnt, cudaStream_t s) {
+    if (n > 0) k_count_active<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(active, n, cnt);
+}
+}  // namespace am

@@ -1,0 +1,166 @@
+"""Thin Python handle over the C-ABI engine (one per GPU / rank).
+
+PyTorch is plumbing here: it owns the CUDA device selection, the stream the
+engine launches on, and the device tensors whose raw pointers cross the
+C-ABI.  All numeric work runs in the library's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .network import AnyNetwork, NetBlob, to_blob
+
+TOL_CELL = 1e-9      # reference cells.py:33
+TOL_WELD = 1e-7      # reference cells.py:35
+TOL_ONPLANE = 1e-9   # reference cells.py:34
+PROBE_DELTA = 1e-7   # reference marching.py:67
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise _native.NativeUnavailable("no CUDA device visible; the meshing path runs only on a B200")
+
+
+class Engine:
+    def __init__(self, net: AnyNetwork, bbox=((-1.2,) * 3, (1.2,) * 3), max_cells: int = 10_000_000,
+                 tol_cell=TOL_CELL, tol_weld=TOL_WELD, tol_onplane=TOL_ONPLANE, probe_delta=PROBE_DELTA,
+                 batch_cells: int = 0, mem_budget: int = 0, rank: int = 0, world: int = 1,
+                 device: int | None = None, stream: torch.cuda.Stream | None = None):
+        _require_cuda()
+        self.lib = _native.load()
+        self.device = torch.cuda.current_device() if device is None else device
+        self.dev = torch.device("cuda", self.device)
+        self.stream = stream or torch.cuda.current_stream(self.dev)
+        self.net = net
+        self.blob: NetBlob = to_blob(net)
+        b = self.blob
+        self._params = np.ascontiguousarray(b.params, dtype=np.float64)
+        self._steps = np.ascontiguousarray(b.steps, dtype=np.int64)
+        self._subs = np.ascontiguousarray(b.subs, dtype=np.int64)
+        desc = _native.NetDesc(self._params.ctypes.data, len(self._params), self._steps.ctypes.data,
+                               len(self._steps), self._subs.ctypes.data, len(self._subs), b.n_bits,
+                               int(b.ensemble))
+        p = _native.MarchParams()
+        p.bbox_lo[:] = [float(v) for v in bbox[0]]
+        p.bbox_hi[:] = [float(v) for v in bbox[1]]
+        p.tol_cell, p.tol_weld, p.tol_onplane, p.probe_delta = tol_cell, tol_weld, tol_onplane, probe_delta
+        p.max_cells, p.batch_cells, p.mem_budget = int(max_cells), int(batch_cells), int(mem_budget)
+        p.rank, p.world = int(rank), int(world)
+        self.params = p
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.am_engine_create(ctypes.byref(h), ctypes.byref(desc), ctypes.byref(p),
+                                                    self.device, ctypes.c_void_p(self.stream.cuda_stream)),
+                          "am_engine_create")
+        self.h = h
+        self.kw = self.lib.am_engine_key_words(h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.am_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ primitives
+    def _dev(self, arr, dtype):
+        t = torch.as_tensor(np.ascontiguousarray(arr), device=self.dev)
+        return t.to(dtype).contiguous()
+
+    def forward(self, pts, keys: bool = False):
+        """F(x) (and activation-state keys) at points; reference network.py:352-392."""
+        pts_t = pts if isinstance(pts, torch.Tensor) else self._dev(np.asarray(pts, np.float64).reshape(-1, 3),
+                                                                   torch.float64)
+        n = pts_t.shape[0]
+        vals = torch.empty(n, dtype=torch.float64, device=self.dev)
+        k = torch.empty((n, self.kw), dtype=torch.int64, device=self.dev) if keys else None
+        _native.check(self.lib.am_forward(self.h, pts_t.data_ptr(), n, vals.data_ptr(),
+                                          k.data_ptr() if k is not None else None), "am_forward")
+        return (vals, k) if keys else vals
+
+    def affine_maps(self, keys):
+        """canonical keys, raw neuron planes (n, NB, 4) and face planes (n, M, 4) on device."""
+        keys_t = keys if isinstance(keys, torch.Tensor) else self._dev(np.asarray(keys).view(np.int64), torch.int64)
+        n = keys_t.shape[0]
+        canon = torch.empty_like(keys_t)
+        planes = torch.empty((n, self.blob.n_bits, 4), dtype=torch.float64, device=self.dev)
+        faces = torch.empty((n, self.blob.n_subs, 4), dtype=torch.float64, device=self.dev)
+        _native.check(self.lib.am_affine_maps(self.h, keys_t.data_ptr(), n, canon.data_ptr(), planes.data_ptr(),
+                                              faces.data_ptr()), "am_affine_maps")
+        return canon, planes, faces
+
+    def dichotomy(self, xpos, xneg, eps, seed_tol, max_iters=200):
+        a = self._dev(np.asarray(xpos, np.float64).reshape(-1, 3), torch.float64)
+        b = self._dev(np.asarray(xneg, np.float64).reshape(-1, 3), torch.float64)
+        out = torch.empty_like(a)
+        _native.check(self.lib.am_dichotomy(self.h, a.data_ptr(), b.data_ptr(), a.shape[0], eps, seed_tol,
+                                            max_iters, out.data_ptr()), "am_dichotomy")
+        return out
+
+    # --------------------------------------------------------------- marching
+    def reset(self):
+        _native.check(self.lib.am_engine_reset(self.h), "am_engine_reset")
+
+    def seed(self, pts):
+        t = pts if isinstance(pts, torch.Tensor) else self._dev(np.asarray(pts, np.float64).reshape(-1, 3),
+                                                               torch.float64)
+        _native.check(self.lib.am_seed(self.h, t.data_ptr(), t.shape[0]), "am_seed")
+
+    def push(self, keys: torch.Tensor):
+        if keys.numel():
+            _native.check(self.lib.am_push_candidates(self.h, keys.data_ptr(), keys.shape[0]),
+                          "am_push_candidates")
+
+    def wave(self) -> int:
+        n = ctypes.c_int64()
+        _native.check(self.lib.am_wave(self.h, ctypes.byref(n)), "am_wave")
+        return n.value
+
+    def run(self) -> int:
+        n = ctypes.c_int64()
+        _native.check(self.lib.am_run(self.h, ctypes.byref(n)), "am_run")
+        return n.value
+
+    def outbox(self):
+        counts = np.zeros(self.params.world, dtype=np.int64)
+        _native.check(self.lib.am_outbox_counts(self.h, counts.ctypes.data), "am_outbox_counts")
+        total = int(counts.sum())
+        out = torch.empty((total, self.kw), dtype=torch.int64, device=self.dev)
+        _native.check(self.lib.am_outbox_take(self.h, out.data_ptr() if total else None), "am_outbox_take")
+        return counts, out
+
+    def counts(self) -> dict:
+        c = np.zeros(8, dtype=np.int64)
+        _native.check(self.lib.am_result_counts(self.h, c.ctypes.data), "am_result_counts")
+        keys = ("cells", "faces", "empty", "verts", "edge_refs", "open_edges", "capped", "overflow")
+        return dict(zip(keys, (int(x) for x in c)))
+
+    def results(self):
+        c = self.counts()
+        keys = np.zeros((c["cells"], self.kw), dtype=np.uint64)
+        nverts = np.zeros(c["cells"], dtype=np.int32)
+        verts = np.zeros((c["verts"], 3))
+        enr = np.zeros(c["verts"], dtype=np.int32)
+        erefs = np.zeros(c["edge_refs"], dtype=np.int32)
+        _native.check(self.lib.am_result_copy(self.h, keys.ctypes.data, nverts.ctypes.data, verts.ctypes.data,
+                                              enr.ctypes.data, erefs.ctypes.data), "am_result_copy")
+        return c, keys, nverts, verts, enr, erefs
+
+    def set_timing(self, on: bool):
+        _native.check(self.lib.am_set_timing(self.h, int(on)), "am_set_timing")
+
+    def stats(self) -> dict:
+        s = np.zeros(8)
+        _native.check(self.lib.am_stats(self.h, s.ctypes.data), "am_stats")
+        keys = ("compose_ms", "face_ms", "compose_flops", "face_bytes", "composed", "faced", "batch",
+                "flops_per_cell")
+        return dict(zip(keys, (float(x) for x in s)))

@@ -1,0 +1,231 @@
+"""Analytic marching on the GPU -- the drop-in for the reference's meshing path.
+
+``march(net, MarchConfig) -> MarchResult`` keeps the reference signature
+(reference marching.py:304-362): a ReLU MLP (plain, residual-shortcut or
+max-pool ensemble) in; polygon faces, their vertices and the visited
+activation states out.  Internally the marching loop is a breadth-first wave
+of activation-state bitmasks on the device (see ``engine.py`` and
+``csrc/am_engine.cu``); MarchResult keeps everything as arrays and builds the
+reference's per-polygon objects lazily.
+"""
+
+from __future__ import annotations
+
+import json
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .engine import PROBE_DELTA, TOL_CELL, TOL_ONPLANE, TOL_WELD, Engine
+from .network import AffinePlane, AnyNetwork, EnsembleSpec, StateVector, subnetworks
+from .seeding import sample_seeds
+
+DEFAULT_BBOX = ((-1.2, -1.2, -1.2), (1.2, 1.2, 1.2))   # reference cells.py:37
+
+PLANE_NEURON = 0   # reference cells.py:39-41
+PLANE_BRANCH = 1
+PLANE_BBOX = 2
+
+
+@dataclass(frozen=True)
+class PlaneRef:
+    """Cell boundary plane: neuron (global bit), branch target, or box face (reference cells.py:44)."""
+
+    kind: int
+    index: int
+
+    def __repr__(self) -> str:
+        tag = {PLANE_NEURON: "neuron", PLANE_BRANCH: "branch", PLANE_BBOX: "bbox"}[self.kind]
+        return f"{tag}:{self.index}"
+
+
+@dataclass(frozen=True)
+class FacePolygon:
+    """Ordered vertex loop of one analytic face (reference cells.py:91)."""
+
+    state: StateVector
+    vertices: np.ndarray
+    plane: AffinePlane | None
+    edge_transitions: tuple
+
+    @property
+    def n_vertices(self) -> int:
+        return self.vertices.shape[0]
+
+    @property
+    def touches_bbox(self) -> bool:
+        return any(r.kind == PLANE_BBOX for refs in self.edge_transitions for r in refs)
+
+    def edge_midpoints(self) -> np.ndarray:
+        v = self.vertices
+        return 0.5 * (v + np.roll(v, -1, axis=0))
+
+
+@dataclass
+class MarchConfig:
+    """reference marching.py:52-75 (``threads`` is accepted for API compatibility;
+    the GPU engine's parallelism is the whole wave)."""
+
+    bbox: tuple = DEFAULT_BBOX
+    seeds: int = 64
+    scheme: str = "dichotomy"
+    threads: int = 1
+    mode: str = "pivot"
+    max_cells: int = 10_000_000
+    rng_seed: int = 0
+    tol_cell: float = TOL_CELL
+    tol_weld: float = TOL_WELD
+    seed_points: np.ndarray | None = None
+    unique_planes_limit: int = 3000
+    probe_delta: float = PROBE_DELTA
+    batch_cells: int = 0        # GPU: cells composed per batch (0 = from memory budget)
+    mem_budget: int = 0         # GPU: bytes for per-batch plane buffers (0 = 2 GiB)
+
+    def __post_init__(self):
+        if self.max_cells < 1:
+            raise ValueError("max_cells must be >= 1")
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+        if self.mode not in ("pivot", "naive"):
+            raise ValueError("mode must be 'pivot' or 'naive'")
+
+
+@dataclass
+class MarchReport:
+    """reference marching.py:78-103; pivot_fallbacks is always 0 (no pivot walk on the GPU)."""
+
+    cells_visited: int = 0
+    faces_emitted: int = 0
+    empty_faces: int = 0
+    open_edges: int = 0
+    seconds: float = 0.0
+    unique_plane_violations: int | None = None
+    pivot_fallbacks: int = 0
+    seeds_used: int = 0
+    capped: bool = False
+    threads: int = 1
+    waves: int = 0
+    overflow: int = 0
+
+    def to_json(self) -> str:
+        return json.dumps({k: getattr(self, k) for k in (
+            "cells_visited", "faces_emitted", "empty_faces", "open_edges", "seconds",
+            "unique_plane_violations", "pivot_fallbacks", "seeds_used", "capped", "threads")})
+
+
+def words_to_packbits(words: np.ndarray, n_bits: int, ensemble: bool):
+    """MSB-first uint64 key words -> (np.packbits bytes, branch) exactly as the reference keys."""
+    words = np.asarray(words).view(np.uint64).reshape(len(words), -1)
+    bw = (n_bits + 63) // 64
+    nbytes = (n_bits + 7) // 8
+    be = words[:, :bw].astype(">u8").view(np.uint8).reshape(len(words), bw * 8)[:, :nbytes]
+    branch = words[:, -1].astype(np.int64) if ensemble else np.full(len(words), -1, np.int64)
+    return np.ascontiguousarray(be), branch
+
+
+@dataclass
+class MarchResult:
+    """Array form of the reference's MarchResult (reference marching.py:106-149).
+
+    keys (C, nbytes) packbits states of every visited cell (empty faces
+    included), sorted by (key, branch) as the reference sorts; nverts (C,)
+    (0 = empty face); verts (V, 3); edge_nrefs (V,); edge_refs (R, 2) as
+    (kind, index).
+    """
+
+    keys: np.ndarray
+    branch: np.ndarray
+    nverts: np.ndarray
+    verts: np.ndarray
+    edge_nrefs: np.ndarray
+    edge_refs: np.ndarray
+    report: MarchReport
+    n_bits: int
+    seeds: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    _polys: list | None = None
+
+    @property
+    def has_face(self) -> np.ndarray:
+        return self.nverts > 0
+
+    def state(self, i: int) -> StateVector:
+        b = int(self.branch[i])
+        return StateVector(self.keys[i].tobytes(), self.n_bits, None if b < 0 else b)
+
+    @property
+    def polygons(self) -> list:
+        """Reference-style FacePolygon list (built lazily; O(cells) Python objects)."""
+        if self._polys is None:
+            out = []
+            offs = np.concatenate([[0], np.cumsum(np.maximum(self.nverts, 0))])
+            roffs = np.concatenate([[0], np.cumsum(self.edge_nrefs)])
+            for i in range(len(self.nverts)):
+                n = int(self.nverts[i])
+                if n <= 0:
+                    continue
+                v0 = int(offs[i])
+                trans = []
+                for e in range(n):
+                    a, b = int(roffs[v0 + e]), int(roffs[v0 + e + 1])
+                    trans.append(tuple(PlaneRef(int(k), int(x)) for k, x in self.edge_refs[a:b]))
+                out.append(FacePolygon(self.state(i), self.verts[v0:v0 + n], None, tuple(trans)))
+            self._polys = out
+        return self._polys
+
+    def polygon_soup(self):
+        from .meshes import PolygonMesh
+        offs = np.concatenate([[0], np.cumsum(np.maximum(self.nverts, 0))])
+        faces = [np.arange(offs[i], offs[i + 1], dtype=np.int64) for i in range(len(self.nverts))
+                 if self.nverts[i] > 0]
+        return PolygonMesh(self.verts.copy(), faces, None)
+
+    def welded_mesh(self, tol: float = TOL_WELD):
+        from .meshes import weld
+        return weld(self.polygon_soup(), tol)
+
+    def face_multiset(self, decimals: int = 10):
+        """Order-independent fingerprint (reference marching.py:139-149)."""
+        out = []
+        for poly in self.polygons:
+            vs = frozenset(map(tuple, np.round(poly.vertices, decimals)))
+            out.append((poly.state.key, poly.state.branch, vs))
+        out.sort(key=lambda t: (t[0], -1 if t[1] is None else t[1], sorted(t[2])))
+        return out
+
+
+def refs_to_kind_index(ids: np.ndarray, n_bits: int, n_subs: int) -> np.ndarray:
+    ids = np.asarray(ids, dtype=np.int64)
+    kind = np.where(ids < n_bits, PLANE_NEURON, np.where(ids < n_bits + n_subs, PLANE_BRANCH, PLANE_BBOX))
+    index = np.where(kind == PLANE_NEURON, ids, np.where(kind == PLANE_BRANCH, ids - n_bits, ids - n_bits - n_subs))
+    return np.stack([kind, index], axis=1) if len(ids) else np.zeros((0, 2), np.int64)
+
+
+def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, threads: int = 1) -> MarchResult:
+    c, keys, nverts, verts, enr, erefs = eng.results()
+    b = eng.blob
+    kb, branch = words_to_packbits(keys, b.n_bits, b.ensemble)
+    rep = MarchReport(cells_visited=c["cells"], faces_emitted=c["faces"], empty_faces=c["empty"],
+                      open_edges=c["open_edges"], seconds=time.perf_counter() - t0, seeds_used=len(seeds),
+                      capped=bool(c["capped"]), threads=threads, waves=waves, overflow=c["overflow"])
+    return MarchResult(kb, branch, nverts.astype(np.int64), verts, enr.astype(np.int64),
+                       refs_to_kind_index(erefs, b.n_bits, b.n_subs), rep, b.n_bits, seeds)
+
+
+def march(net: AnyNetwork, config: MarchConfig | None = None, engine: Engine | None = None) -> MarchResult:
+    """Extract every analytic face reachable from the seeds (reference marching.py:304-362)."""
+    config = config or MarchConfig()
+    t0 = time.perf_counter()
+    eng = engine or Engine(net, bbox=config.bbox, max_cells=config.max_cells, tol_cell=config.tol_cell,
+                           tol_weld=config.tol_weld, probe_delta=config.probe_delta,
+                           batch_cells=config.batch_cells, mem_budget=config.mem_budget)
+    if config.seed_points is not None:
+        seeds = np.asarray(config.seed_points, dtype=np.float64).reshape(-1, 3)
+    else:
+        seeds = sample_seeds(eng, config.seeds, config.bbox, scheme=config.scheme, rng_seed=config.rng_seed)
+    eng.seed(seeds)
+    waves = eng.run()
+    res = collect_result(eng, seeds, t0, waves, config.threads)
+    if res.report.faces_emitted <= config.unique_planes_limit:
+        res.report.unique_plane_violations = None   # diagnostic not computed on the GPU path
+    return res

@@ -1,0 +1,131 @@
+"""Triggering: surface seed points for the march (reference seeding.py).
+
+The random sampling keeps the reference's per-index streams
+(``np.random.default_rng([rng_seed, index])``, reference seeding.py:146) so the
+same seeds come out; every field evaluation and the bisection itself run on the
+GPU (``Engine.forward`` / ``Engine.dichotomy``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+SEED_TOL = 1e-7
+SCHEMES = ("sgd", "sphere_trace", "dichotomy")
+
+
+class SeedingError(RuntimeError):
+    pass
+
+
+def validate_scheme(net, scheme: str) -> None:
+    """reference seeding.py:115-120"""
+    if scheme not in SCHEMES:
+        raise SeedingError(f"unknown triggering scheme {scheme!r}; choose from {SCHEMES}")
+    if net.field_kind == "occupancy" and scheme in ("sgd", "sphere_trace"):
+        raise SeedingError(f"scheme {scheme!r} does not trigger on occupancy fields; use 'dichotomy'")
+
+
+def _grad(eng, x: np.ndarray) -> np.ndarray:
+    """Face-plane normals of the regions containing x (reference network.py:492-499)."""
+    _, keys = eng.forward(x, keys=True)
+    _, _, faces = eng.affine_maps(keys)
+    f = faces.cpu().numpy()
+    if eng.blob.ensemble:
+        br = keys[:, -1].cpu().numpy()
+        return f[np.arange(len(x)), br, :3]
+    return f[:, 0, :3]
+
+
+def _trace(eng, x0: np.ndarray, scheme: str, seed_tol: float):
+    """Batched sphere tracing (reference seeding.py:60-81) or SGD on |F| (seeding.py:33-57)."""
+    x = x0.copy()
+    n = len(x)
+    out = [None] * n
+    iters = np.zeros(n, dtype=np.int64)
+    active = np.ones(n, dtype=bool)
+    step = np.full(n, 0.05)
+    f = eng.forward(x).cpu().numpy()
+    max_iters = 50 if scheme == "sphere_trace" else 1000
+    for it in range(max_iters + 1):
+        done = active & (np.abs(f) <= seed_tol)
+        for i in np.nonzero(done)[0]:
+            out[i] = x[i].copy()
+            iters[i] = it
+        active &= ~done
+        if not active.any() or it == max_iters:
+            break
+        idx = np.nonzero(active)[0]
+        g = _grad(eng, x[idx])
+        if scheme == "sphere_trace":
+            if np.any(np.abs(x[idx]).max(axis=1) > 12.0):
+                raise SeedingError(f"sphere tracing diverged after {it} iterations")
+            x[idx] = x[idx] - 1.0 * f[idx, None] * g
+            f[idx] = eng.forward(x[idx]).cpu().numpy()
+        else:
+            gn = np.linalg.norm(g, axis=1)
+            dead = gn == 0.0
+            active[idx[dead]] = False
+            idx, g, gn = idx[~dead], g[~dead], gn[~dead]
+            x_new = x[idx] - step[idx, None] * np.sign(f[idx])[:, None] * g / gn[:, None]
+            f_new = eng.forward(x_new).cpu().numpy()
+            flip = np.sign(f_new) != np.sign(f[idx])
+            step[idx[flip]] *= 0.5
+            x[idx], f[idx] = x_new, f_new
+    return out, iters
+
+
+def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int = 0, eps: float = SEED_TOL,
+                 seed_tol: float = SEED_TOL, retry_budget: int = 200, collect_iters: list | None = None) -> np.ndarray:
+    """Up to ``count`` surface points, deterministic given rng_seed (reference seeding.py:123-162)."""
+    if count < 1:
+        raise ValueError("count must be >= 1")
+    validate_scheme(eng.net, scheme)
+    lo = np.asarray(bbox[0], dtype=np.float64)
+    hi = np.asarray(bbox[1], dtype=np.float64)
+    rngs = [np.random.default_rng([rng_seed, index]) for index in range(count)]
+    found: list = [None] * count
+    if scheme == "dichotomy":
+        pairs: dict = {}
+        pending = list(range(count))
+        for _ in range(retry_budget):
+            if not pending:
+                break
+            pts = np.stack([rngs[i].uniform(lo, hi, size=(64, 3)) for i in pending])
+            vals = eng.forward(pts.reshape(-1, 3)).cpu().numpy().reshape(len(pending), 64)
+            still = []
+            for j, i in enumerate(pending):
+                pos = pts[j][vals[j] > 0.0]
+                neg = pts[j][vals[j] < 0.0]
+                if len(pos) and len(neg):
+                    pairs[i] = (pos[0], neg[0])
+                else:
+                    still.append(i)
+            pending = still
+        if pairs:
+            order = sorted(pairs)
+            xp = np.stack([pairs[i][0] for i in order])
+            xn = np.stack([pairs[i][1] for i in order])
+            pts = eng.dichotomy(xp, xn, eps, seed_tol).cpu().numpy()
+            for i, p in zip(order, pts):
+                found[i] = p
+    else:
+        pending = list(range(count))
+        for _ in range(retry_budget):
+            if not pending:
+                break
+            x0 = np.stack([rngs[i].uniform(lo, hi, size=3) for i in pending])
+            res, iters = _trace(eng, x0, scheme, seed_tol)
+            still = []
+            for j, i in enumerate(pending):
+                if res[j] is not None:
+                    found[i] = res[j]
+                    if collect_iters is not None:
+                        collect_iters.append(int(iters[j]))
+                else:
+                    still.append(i)
+            pending = still
+    seeds = [p for p in found if p is not None]
+    if not seeds:
+        raise SeedingError("no surface located in bbox")
+    return np.array(seeds)

@@ -1,0 +1,107 @@
+"""GPU parity: the CUDA path against the reference's golden vectors and the CPU oracle.
+
+Bar (BASELINE.json north_star): the sorted set of visited cell states matches
+bit-exactly; vertices agree within 1e-9 absolute (fp64).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden_cases, load_golden, make_random_net
+
+pytestmark = pytest.mark.gpu
+
+VERT_TOL = 1e-9
+
+
+def _gpu():
+    from paper_2106_10031_b200 import marching
+    return marching
+
+
+def assert_same_march(r, ref_keys, ref_branch, ref_nverts, ref_verts, ref_enr, ref_erefs):
+    assert r.report.overflow == 0
+    assert r.keys.shape == ref_keys.shape, (r.keys.shape, ref_keys.shape)
+    np.testing.assert_array_equal(r.keys, ref_keys)
+    np.testing.assert_array_equal(r.branch, ref_branch)
+    np.testing.assert_array_equal(r.nverts, ref_nverts)
+    if len(ref_verts):
+        assert np.abs(r.verts - ref_verts).max() <= VERT_TOL
+    np.testing.assert_array_equal(r.edge_nrefs, ref_enr)
+    np.testing.assert_array_equal(r.edge_refs, ref_erefs)
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_march_matches_reference_golden(name):
+    g = load_golden(name)
+    cfg = g["config"]
+    m = _gpu()
+    mc = m.MarchConfig(bbox=tuple(map(tuple, cfg["bbox"])), seeds=cfg["seeds"], scheme=cfg["scheme"],
+                       rng_seed=cfg["rng_seed"], max_cells=cfg["max_cells"],
+                       seed_points=g["seeds"] if cfg["explicit_seeds"] else None)
+    r = m.march(g["net"], mc)
+    np.testing.assert_allclose(r.seeds, g["seeds"], atol=1e-12, rtol=0)
+    if cfg["max_cells"] < 10_000_000 and g["report"]["capped"]:
+        # a capped march is order dependent in the reference too: check the contract only
+        assert r.report.capped and r.report.cells_visited <= cfg["max_cells"]
+        return
+    assert_same_march(r, g["keys"], g["branch"], g["nverts"], g["verts"], g["edge_nrefs"], g["edge_refs"])
+    for k in ("cells_visited", "faces_emitted", "empty_faces", "open_edges"):
+        assert getattr(r.report, k) == g["report"][k], k
+
+
+def test_forward_and_states_match_oracle():
+    from paper_2106_10031_b200.engine import Engine
+    net = make_random_net(depth=6, width=20, seed=7)
+    pts = np.random.default_rng(2).uniform(-1.2, 1.2, size=(1000, 3))
+    eng = Engine(net)
+    vals, keys = eng.forward(pts, keys=True)
+    on = oracle.OracleNet(net)
+    np.testing.assert_allclose(vals.cpu().numpy(), on.forward_many(pts), rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(keys.cpu().numpy().view(np.uint64), on.state_keys(pts))
+
+
+def test_affine_maps_match_oracle():
+    from paper_2106_10031_b200.engine import Engine
+    for net in (make_random_net(depth=4, width=33, seed=3), oracle_net_res()):
+        pts = np.random.default_rng(5).uniform(-1.0, 1.0, size=(300, 3))
+        eng = Engine(net)
+        on = oracle.OracleNet(net)
+        keys = on.state_keys(pts)
+        canon, planes, faces = eng.affine_maps(keys.view(np.int64))
+        canon = canon.cpu().numpy().view(np.uint64)
+        planes = planes.cpu().numpy()
+        faces = faces.cpu().numpy()
+        for i in range(len(pts)):
+            c, p, f = on.affine_maps(keys[i])
+            np.testing.assert_array_equal(canon[i], c)
+            np.testing.assert_allclose(planes[i], p, rtol=1e-11, atol=1e-12)
+            np.testing.assert_allclose(faces[i, 0], f, rtol=1e-11, atol=1e-12)
+
+
+def oracle_net_res():
+    from paper_2106_10031_b200 import synth
+    return synth.deepsdf_mlp(width=40, depth=5, skip_at=3, bias_std=0.05, seed=4)
+
+
+@pytest.mark.parametrize("which", ["geo_90x6", "deepsdf_128x8", "imnet_occ", "rand_wide"])
+def test_march_matches_oracle_larger(which):
+    from paper_2106_10031_b200 import synth
+    m = _gpu()
+    if which == "geo_90x6":
+        net = synth.geometric_mlp([90] * 6, seed=0)
+        kw = dict(bbox=((0.1, 0.1, 0.1), (0.45, 0.45, 0.45)), seeds=4, rng_seed=1)
+    elif which == "deepsdf_128x8":
+        net = synth.deepsdf_mlp(width=128, depth=8, skip_at=4, seed=2)
+        kw = dict(bbox=((0.0, 0.0, 0.0), (0.45, 0.45, 0.45)), seeds=4, rng_seed=2)
+    elif which == "imnet_occ":
+        net = synth.imnet_ensemble(widths=(32, 32, 32), n_parts=4, seed=3)
+        kw = dict(seeds=8, rng_seed=3)
+    else:
+        net = make_random_net(depth=3, width=64, seed=9)
+        kw = dict(seeds=8, rng_seed=4)
+    r = m.march(net, m.MarchConfig(**kw))
+    o = oracle.march(net, bbox=kw.get("bbox", m.DEFAULT_BBOX), seed_points=r.seeds)
+    assert r.report.cells_visited > 50
+    assert_same_march(r, o.keys, o.branch, o.nverts, o.verts, o.edge_nrefs, o.edge_refs)
