@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark: analytic marching of BASELINE.json configs[1] on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one complete march (every analytic cell reachable from the seeds)
+of the configs[1] network: 3-(90x6)-1 ReLU SDF MLP, SAL geometric (sphere-SDF)
+init, fp64, seeded with the reference's default trigger (64 dichotomy seeds,
+rng_seed 0).  ``value`` = visited cells / device time with the network and the
+seed points resident in HBM; ``e2e`` = the same through the public
+``march(net, MarchConfig)`` call from host buffers (engine creation + weight
+upload, seeding, marching, results back to host, sorted like the reference).
+With N > 1 ranks (torchrun, one per GPU) states are sharded by hash ownership
+and the frontier is exchanged with an NCCL all-to-all every wave.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the C
+oracle restatement; the reference itself is pure Python) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+WORKLOAD = ("configs[1]: 3-(90x6)-1 ReLU SDF MLP, SAL geometric (sphere-SDF) init seed 0, fp64, "
+            "64 dichotomy seeds (reference default MarchConfig), box [-1.2,1.2]^3")
+METRIC = "analytic cells/sec (full march of configs[1])"
+
+
+def workload_net():
+    from paper_2106_10031_b200 import synth
+    return synth.geometric_mlp([90] * 6, seed=0)
+
+
+def _peaks():
+    path = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("hbm_gbs", 6650.0), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device=0):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def flush_l2(buf):
+    buf.fill_(1)   # 512 MiB write > 126 MB L2
+
+
+def cpu_baseline_run(net, seeds, target_seconds=15.0, threads=None, max_cells=None):
+    """Oracle (C restatement of the reference) on the host cores over a bounded sample."""
+    sys.path.insert(0, os.path.join(HERE, "oracle"))
+    import oracle
+    threads = threads or os.cpu_count() or 1
+    on = oracle.OracleNet(net)
+    if max_cells is None:
+        t = time.perf_counter()
+        probe = oracle.march(net, seed_points=seeds, max_cells=3000, threads=threads, oracle_net=on)
+        rate = probe.report["cells_visited"] / max(time.perf_counter() - t, 1e-6)
+        max_cells = int(max(5000, min(rate * target_seconds, 10_000_000)))
+    t = time.perf_counter()
+    r = oracle.march(net, seed_points=seeds, max_cells=max_cells, threads=threads, oracle_net=on)
+    dt = time.perf_counter() - t
+    cells = r.report["cells_visited"]
+    return {"value": cells / dt, "unit": "cells/s", "cores": threads, "kind": "port",
+            "sample": f"first {cells} cells (max_cells cap) of the same 64-seed march, {dt:.1f} s, "
+                      f"oracle/am_oracle.c with {threads} threads"}, max_cells
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host CPU (oracle port)."""
+    if rank != 0:
+        return
+    from paper_2106_10031_b200.engine import Engine  # noqa: F401  (seeds via the CPU trigger below)
+    sys.path.insert(0, os.path.join(HERE, "oracle"))
+    import oracle
+    net = workload_net()
+    on = oracle.OracleNet(net)
+    seeds = oracle.sample_seeds(on, 64, ((-1.2,) * 3, (1.2,) * 3), "dichotomy", 0)
+    threads = os.cpu_count() or 1
+    _, cap = cpu_baseline_run(net, seeds, target_seconds=8.0, threads=threads)
+    for _ in range(args.warmup):
+        oracle.march(net, seed_points=seeds, max_cells=cap, threads=threads, oracle_net=on)
+    times, cells = [], 0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        r = oracle.march(net, seed_points=seeds, max_cells=cap, threads=threads, oracle_net=on)
+        times.append(time.perf_counter() - t)
+        cells = r.report["cells_visited"]
+    dt = float(np.mean(times))
+    v = cells / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "cells/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample_cells": cells, "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "port",
+                         "sample": f"first {cells} cells of the march per step (max_cells cap)"},
+        "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seeds", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_2106_10031_b200 import marching
+    from paper_2106_10031_b200.engine import Engine
+    from paper_2106_10031_b200 import _native
+    from paper_2106_10031_b200.seeding import sample_seeds
+
+    net = workload_net()
+    bbox = ((-1.2,) * 3, (1.2,) * 3)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    if world > 1:
+        from paper_2106_10031_b200.distributed import ShardedMarcher
+        sm = ShardedMarcher(net, bbox=bbox)
+        seeds = sm.sample_seeds(args.seeds, rng_seed=0)
+        run_once = lambda: sm.run(seeds)  # noqa: E731
+        engine = sm.engine
+    else:
+        engine = Engine(net, bbox=bbox)
+        seeds = sample_seeds(engine, args.seeds, bbox, rng_seed=0)
+        seeds_dev = torch.as_tensor(seeds, device=dev)
+
+        def run_once():
+            engine.reset()
+            engine.seed(seeds_dev)
+            return engine.run()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        run_once()
+    torch.cuda.synchronize()
+
+    # ----------------------------------------------------- device-timed steps
+    lib = _native.load()
+    st0 = engine.stats()
+    times = []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            waves = run_once()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            times.append(e0.elapsed_time(e1))
+    clocks = clk.summary()
+    st1 = engine.stats()
+    counts = engine.counts()
+    cells_local = counts["cells"]
+    t_local = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([t_local, float(cells_local)], dtype=torch.float64, device=dev)
+        tmax = tt[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        csum = tt[1:].clone()
+        dist.all_reduce(csum, op=dist.ReduceOp.SUM)
+        t_step, cells = float(tmax.item()), int(csum.item())
+    else:
+        t_step, cells = t_local, cells_local
+    value = cells / (t_step * 1e-3)
+    launches = (st1["launches"] - st0["launches"]) / max(args.steps, 1)
+
+    # ------------------------------------------------- kernel timing (roofline)
+    engine.set_timing(True)
+    run_once()          # stats are reset by the engine at the start of every march
+    torch.cuda.synchronize()
+    s1 = engine.stats()
+    engine.set_timing(False)
+    comp_ms = s1["compose_ms"]
+    face_ms = s1["face_ms"]
+    comp_tf = s1["compose_flops"] / (comp_ms * 1e-3) / 1e12 if comp_ms else 0.0
+    face_gbs = s1["face_bytes"] / (face_ms * 1e-3) / 1e9 if face_ms else 0.0
+    pk = np.zeros(2)
+    _native.check(lib.am_bench_fp64_peak(local_rank, pk.ctypes.data), "am_bench_fp64_peak")
+    hbm, hbm_src = _peaks()
+    traffic = None
+    prof = os.path.join(HERE, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh)
+    kernels = {
+        "compose_dmma": {"bound": "tensor", "achieved": comp_tf, "peak": float(pk[0]), "unit": "TFLOP/s",
+                         "frac": comp_tf / pk[0] if pk[0] else None, "ms": comp_ms,
+                         "peak_source": "measured fp64 DMMA microbenchmark (am_bench_fp64_peak)",
+                         "traffic": (traffic or {}).get("compose")},
+        "face": {"bound": "hbm", "achieved": face_gbs, "peak": hbm, "unit": "GB/s",
+                 "frac": face_gbs / hbm, "ms": face_ms, "peak_source": hbm_src,
+                 "traffic": (traffic or {}).get("face")},
+    }
+    dominant = max(kernels, key=lambda k: kernels[k]["ms"])
+    roof = dict(kernels[dominant])
+    roof["kernel"] = dominant
+
+    # ------------------------------------------------------------------ e2e
+    e2e = None
+    if world == 1:
+        cfg = marching.MarchConfig(seeds=args.seeds, rng_seed=0, bbox=bbox)
+        marching.march(net, cfg)   # warm
+        e_times = []
+        h2d = d2h = 0
+        for _ in range(max(1, min(args.steps, 3))):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = marching.march(net, cfg)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e_times.append(e0.elapsed_time(e1))
+            from paper_2106_10031_b200.network import to_blob
+            blob = to_blob(net)
+            h2d = blob.params.nbytes + args.seeds * 64 * 3 * 8 * 2 + args.seeds * 3 * 8
+            d2h = (r.keys.nbytes + r.nverts.nbytes + r.verts.nbytes + r.edge_nrefs.nbytes
+                   + r.edge_refs.nbytes // 2)
+        e_ms = float(np.mean(e_times))
+        e2e = {"value": r.report.cells_visited / (e_ms * 1e-3), "unit": "cells/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "api": "paper_2106_10031_b200.march(net, MarchConfig(seeds=64)) from host buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, _ = cpu_baseline_run(net, seeds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "cells_per_step": cells, "waves": int(waves),
+                       "parallelism": f"dp{world} (state-hash ownership)" if world > 1 else "1 GPU",
+                       "l2": "flushed between timed steps (512 MiB write)",
+                       "mesh_time_s": t_step * 1e-3},
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks,
+            "fp64_peaks_tflops": {"dmma": float(pk[0]), "dfma": float(pk[1])},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

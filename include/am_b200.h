@@ -125,8 +125,10 @@ int am_result_copy(am_engine *e, uint64_t *h_keys, int32_t *h_nverts, double *h_
 /* --- profiling hooks (bench.py roofline) --------------------------------- */
 /* cumulative device time (ms) of the compose (DMMA) kernels, of the face
  * kernel, and the algorithmic flop / byte counts they processed */
-int am_stats(am_engine *e, double *h_out8);
+int am_stats(am_engine *e, double *h_out16);
 int am_set_timing(am_engine *e, int enabled);
+/* measured fp64 peaks of this device: h_out2[0] DMMA (tensor) TFLOP/s, [1] DFMA TFLOP/s */
+int am_bench_fp64_peak(int device, double *h_out2);
 
 #ifdef __cplusplus
 }

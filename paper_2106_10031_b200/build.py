@@ -23,6 +23,7 @@ SOURCES = {
     "am_seed.cu": [],
     "am_engine.cu": [],
     "am_face.cu": ["-fmad=false"],
+    "am_peak.cu": [],
 }
 
 

@@ -156,8 +156,8 @@ void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
     int64_t total = L.n_items * L.st.n_out;
     if (total <= 0) return;
     int64_t blocks = (total + 255) / 256;
-    if (C == 4) k_input_step<4><<<(unsigned)blocks, 256, 0, s>>>(L);
-    else k_input_step<1><<<(unsigned)blocks, 256, 0, s>>>(L);
+    if (C == 4) { k_input_step<4><<<(unsigned)blocks, 256, 0, s>>>(L); ++g_launch_count; }
+    else { k_input_step<1><<<(unsigned)blocks, 256, 0, s>>>(L); ++g_launch_count; }
 }
 
 // ----------------------------------------------------------- GEMM step
@@ -434,11 +434,11 @@ void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const
     if (C == 4) {
         static bool init = false;
         if (!init) { cudaFuncSetAttribute(k_gemm_step<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
-        k_gemm_step<4><<<grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L);
+        { k_gemm_step<4><<<grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L); ++g_launch_count; }
     } else {
         static bool init = false;
         if (!init) { cudaFuncSetAttribute(k_gemm_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
-        k_gemm_step<1><<<grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L);
+        { k_gemm_step<1><<<grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L); ++g_launch_count; }
     }
 }
 
@@ -513,14 +513,14 @@ void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, 
                           const void* subs, int n_subs, cudaStream_t s) {
     int64_t warps = n_items * n_subs;
     if (warps <= 0) return;
-    k_face_head<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(Z, keys, faces, n_items, zs, KW,
-                                                                    static_cast<const SubDev*>(subs), n_subs);
+    { k_face_head<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(Z, keys, faces, n_items, zs, KW,
+                                                                    static_cast<const SubDev*>(subs), n_subs); ++g_launch_count; }
 }
 void launch_forward_head_dev(const double* Z, uint64_t* keys, double* vals, int64_t n_items, int zs, int KW,
                              const void* subs, int n_subs, int ensemble, cudaStream_t s) {
     if (n_items <= 0) return;
-    k_forward_head<<<(unsigned)((n_items * 32 + 255) / 256), 256, 0, s>>>(
-        Z, keys, vals, n_items, zs, KW, static_cast<const SubDev*>(subs), n_subs, ensemble);
+    { k_forward_head<<<(unsigned)((n_items * 32 + 255) / 256), 256, 0, s>>>(
+        Z, keys, vals, n_items, zs, KW, static_cast<const SubDev*>(subs), n_subs, ensemble); ++g_launch_count; }
 }
 
 }  // namespace am

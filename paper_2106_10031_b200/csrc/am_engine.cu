@@ -56,6 +56,10 @@ struct SubDev {
 
 using namespace am;
 
+namespace am {
+unsigned long long g_launch_count = 0;
+}
+
 static thread_local std::string g_err;
 static int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -841,11 +845,13 @@ extern "C" int am_set_timing(am_engine* e, int enabled) {
     return AM_OK;
 }
 
-// out: [compose_ms, face_ms, compose_flops, face_bytes, composed_items, face_cells, batch, flops_per_cell]
+// out: [compose_ms, face_ms, compose_flops, face_bytes, composed_items, face_cells, batch, flops_per_cell,
+//       kernel launches (process-wide), waves]
 extern "C" int am_stats(am_engine* e, double* h) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
     h[0] = e->t_compose; h[1] = e->t_face; h[2] = e->flops; h[3] = e->face_bytes;
     h[4] = e->n_comp_cells; h[5] = e->n_face_cells; h[6] = (double)e->B; h[7] = e->flops_per_cell;
+    h[8] = (double)g_launch_count; h[9] = 0;
     return AM_OK;
 }
 

@@ -588,7 +588,7 @@ void launch_face(const FaceArgs& a, cudaStream_t s) {
         cudaFuncSetAttribute(k_face, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    k_face<<<(unsigned)((a.n + FW - 1) / FW), FW * 32, smem, s>>>(a);
+    { k_face<<<(unsigned)((a.n + FW - 1) / FW), FW * 32, smem, s>>>(a); ++g_launch_count; }
 }
 
 }  // namespace am

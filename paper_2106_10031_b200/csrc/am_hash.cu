@@ -119,17 +119,17 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 
 void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, int64_t n, int32_t* status,
                         uint64_t* slot, cudaStream_t s) {
-    if (n > 0) k_hash_insert<<<nblk(n, 256), 256, 0, s>>>(H, src, idx, n, status, slot);
+    if (n > 0) { k_hash_insert<<<nblk(n, 256), 256, 0, s>>>(H, src, idx, n, status, slot); ++g_launch_count; }
 }
 void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, int64_t n, const int32_t* status,
                        const uint64_t* slot, uint32_t flag, int32_t* pool_idx, cudaStream_t s) {
-    if (n > 0) k_hash_fixup<<<nblk(n, 256), 256, 0, s>>>(H, src, idx, n, status, slot, flag, pool_idx);
+    if (n > 0) { k_hash_fixup<<<nblk(n, 256), 256, 0, s>>>(H, src, idx, n, status, slot, flag, pool_idx); ++g_launch_count; }
 }
 void launch_hash_lookup(const HashSet& H, const uint64_t* src, int64_t n, int32_t* found, cudaStream_t s) {
-    if (n > 0) k_hash_lookup<<<nblk(n, 256), 256, 0, s>>>(H, src, n, found);
+    if (n > 0) { k_hash_lookup<<<nblk(n, 256), 256, 0, s>>>(H, src, n, found); ++g_launch_count; }
 }
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
-    if (n_pool > 0) k_hash_rebuild<<<nblk(n_pool, 256), 256, 0, s>>>(H, n_pool);
+    if (n_pool > 0) { k_hash_rebuild<<<nblk(n_pool, 256), 256, 0, s>>>(H, n_pool); ++g_launch_count; }
 }
 
 // ------------------------------------------------------------ list utilities
@@ -146,7 +146,7 @@ __global__ void k_compact(const int32_t* flag, int32_t want, int64_t n, int32_t*
 }
 void launch_compact(const int32_t* flag, int32_t want, int64_t n, int32_t* out, unsigned long long* count,
                     cudaStream_t s) {
-    if (n > 0) k_compact<<<nblk(n, 256), 256, 0, s>>>(flag, want, n, out, count);
+    if (n > 0) { k_compact<<<nblk(n, 256), 256, 0, s>>>(flag, want, n, out, count); ++g_launch_count; }
 }
 
 // dst[i] = src[idx[i]] (KW words each)
@@ -158,7 +158,7 @@ __global__ void k_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n
     dst[i * KW + w] = src[(int64_t)idx[i] * KW + w];
 }
 void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst, cudaStream_t s) {
-    if (n > 0) k_gather_keys<<<nblk(n * KW, 256), 256, 0, s>>>(src, idx, n, KW, dst);
+    if (n > 0) { k_gather_keys<<<nblk(n * KW, 256), 256, 0, s>>>(src, idx, n, KW, dst); ++g_launch_count; }
 }
 
 // frontier assembly after composition (reference marching.py:280-288: canon == state -> skip;
@@ -192,8 +192,8 @@ void launch_frontier(int64_t nR, const int32_t* changed, const int32_t* R, const
                      uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* nF, int64_t max_new,
                      unsigned long long* capped, cudaStream_t s) {
     if (nR > 0)
-        k_frontier<<<nblk(nR, 256), 256, 0, s>>>(nR, changed, R, raw_pool, canon_pos, canon_status, canon_pool,
-                                                   pool_flags, f_items, f_pool, nF, max_new, capped);
+        { k_frontier<<<nblk(nR, 256), 256, 0, s>>>(nR, changed, R, raw_pool, canon_pos, canon_status, canon_pool,
+                                                   pool_flags, f_items, f_pool, nF, max_new, capped); ++g_launch_count; }
 }
 
 // canon_pos[b] = position of b in the changed list X (or -1)
@@ -202,7 +202,7 @@ __global__ void k_scatter_pos(const int32_t* X, int64_t nX, int32_t* pos) {
     if (j < nX) pos[X[j]] = (int32_t)j;
 }
 void launch_scatter_pos(const int32_t* X, int64_t nX, int32_t* pos, cudaStream_t s) {
-    if (nX > 0) k_scatter_pos<<<nblk(nX, 256), 256, 0, s>>>(X, nX, pos);
+    if (nX > 0) { k_scatter_pos<<<nblk(nX, 256), 256, 0, s>>>(X, nX, pos); ++g_launch_count; }
 }
 
 // owner partition for sharded marching: out_owner[i] = owner(key_i)
@@ -211,7 +211,7 @@ __global__ void k_owner(const uint64_t* keys, int64_t n, int KW, int world, int3
     if (i < n) owner[i] = key_owner(keys + i * KW, KW, world);
 }
 void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s) {
-    if (n > 0) k_owner<<<nblk(n, 256), 256, 0, s>>>(keys, n, KW, world, owner);
+    if (n > 0) { k_owner<<<nblk(n, 256), 256, 0, s>>>(keys, n, KW, world, owner); ++g_launch_count; }
 }
 
 }  // namespace am

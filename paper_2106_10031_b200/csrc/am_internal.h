@@ -20,6 +20,9 @@ constexpr double kDegen = 1e-12;   // reference network.py:27 DEGENERATE_NORMAL_
 constexpr double kTolDet = 1e-12;  // reference cells.py:32 TOL_DET
 constexpr uint64_t kEmpty = ~0ull;
 
+// number of kernels this library launched (bench.py gpu_launches)
+extern unsigned long long g_launch_count;
+
 // ------------------------------------------------------------------ keys
 __host__ __device__ inline int key_bit(const uint64_t* k, int i) {
     return (int)((k[i >> 6] >> (63 - (i & 63))) & 1ull);

@@ -159,8 +159,8 @@ class Engine:
         _native.check(self.lib.am_set_timing(self.h, int(on)), "am_set_timing")
 
     def stats(self) -> dict:
-        s = np.zeros(8)
+        s = np.zeros(16)
         _native.check(self.lib.am_stats(self.h, s.ctypes.data), "am_stats")
         keys = ("compose_ms", "face_ms", "compose_flops", "face_bytes", "composed", "faced", "batch",
-                "flops_per_cell")
+                "flops_per_cell", "launches", "waves")
         return dict(zip(keys, (float(x) for x in s)))
