@@ -258,8 +258,10 @@ def main():
     engine.set_timing(False)
     comp_ms = s1["compose_ms"]
     face_ms = s1["face_ms"]
+    probe_ms = s1["probe_ms"]
     comp_tf = s1["compose_flops"] / (comp_ms * 1e-3) / 1e12 if comp_ms else 0.0
     face_gbs = s1["face_bytes"] / (face_ms * 1e-3) / 1e9 if face_ms else 0.0
+    probe_tf = s1["probe_flops"] / (probe_ms * 1e-3) / 1e12 if probe_ms else 0.0
     pk = np.zeros(2)
     _native.check(lib.am_bench_fp64_peak(local_rank, pk.ctypes.data), "am_bench_fp64_peak")
     hbm, hbm_src = _peaks()
@@ -276,6 +278,10 @@ def main():
         "face": {"bound": "hbm", "achieved": face_gbs, "peak": hbm, "unit": "GB/s",
                  "frac": face_gbs / hbm, "ms": face_ms, "peak_source": hbm_src,
                  "traffic": (traffic or {}).get("face")},
+        "probe_forward_dmma": {"bound": "tensor", "achieved": probe_tf, "peak": float(pk[0]), "unit": "TFLOP/s",
+                               "frac": probe_tf / pk[0] if pk[0] else None, "ms": probe_ms,
+                               "probes": s1["probes"], "peak_source": "measured fp64 DMMA microbenchmark",
+                               "traffic": (traffic or {}).get("probe")},
     }
     dominant = max(kernels, key=lambda k: kernels[k]["ms"])
     roof = dict(kernels[dominant])

@@ -100,18 +100,23 @@ int am_dichotomy(am_engine *e, const double *d_xpos, const double *d_xneg, int64
                  double seed_tol, int max_iters, double *d_out);
 /* queue n raw candidate states (device keys) for the next absorb */
 int am_push_candidates(am_engine *e, const uint64_t *d_keys, int64_t n);
-/* one BFS wave: absorb queued candidates (dedup, compose, canonicalise),
- * extract faces of newly visited cells, emit next candidates (flips + probes).
- * *h_new_cells = cells newly visited in this wave. */
+/* one BFS iteration: dequeue up to a batch of states, compose them,
+ * canonicalise, extract the faces of the new cells and enqueue every new
+ * neighbour state (flips + probes).  *h_new_cells = cells visited. */
 int am_wave(am_engine *e, int64_t *h_new_cells);
 /* run waves until no candidates remain (single rank); *h_waves = waves run */
 int am_run(am_engine *e, int64_t *h_waves);
 
 /* --- sharded marching (owner = hash % world) ------------------------------ */
-/* after am_wave with world > 1: candidates owned by other ranks are held back.
- * h_counts[world] receives per-owner counts; d_out gets keys grouped by owner. */
-int am_outbox_counts(am_engine *e, int64_t *h_counts);
-int am_outbox_take(am_engine *e, uint64_t *d_out);
+/* with world > 1, states emitted by a wave that another rank owns are held in
+ * an outbox instead of being inserted locally.  am_outbox_counts gives the
+ * total; am_outbox_take moves them to d_out grouped by owner rank
+ * (h_counts[world] per owner) and clears the outbox.  Received states are fed
+ * back with am_push_candidates. */
+int am_outbox_counts(am_engine *e, int64_t *h_total);
+int am_outbox_take(am_engine *e, uint64_t *d_out, int64_t *h_counts);
+/* states queued but not yet composed on this rank */
+int am_queue_size(am_engine *e, int64_t *h_n);
 
 /* --- results ------------------------------------------------------------- */
 /* h_counts[8]: cells, faces, empty, verts, edge_refs, open_edges, capped, overflow */

@@ -65,7 +65,8 @@ SIGNATURES = {
     "am_wave": (ctypes.c_int, [P, P]),
     "am_run": (ctypes.c_int, [P, P]),
     "am_outbox_counts": (ctypes.c_int, [P, P]),
-    "am_outbox_take": (ctypes.c_int, [P, P]),
+    "am_outbox_take": (ctypes.c_int, [P, P, P]),
+    "am_queue_size": (ctypes.c_int, [P, P]),
     "am_result_counts": (ctypes.c_int, [P, P]),
     "am_result_copy": (ctypes.c_int, [P, P, P, P, P, P]),
     "am_stats": (ctypes.c_int, [P, P]),

@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "am_internal.h"
@@ -95,67 +96,82 @@ __device__ __forceinline__ void set_key_bit(uint64_t* key, int row, int bit) {
 template <int C>
 __global__ void k_input_step(LayerLaunch L) {
     const StepDev& st = L.st;
-    int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t item = gid / st.n_out;
-    int r = (int)(gid - item * st.n_out);
-    if (item >= L.n_items) return;
-    const double* w = st.W + (int64_t)r * st.ldw;
-    uint64_t* key = L.keys + item * L.KW;
-    int row = st.row_off + r;
-    double* z = L.Z + (item * L.zs + row) * C;
-    bool sc = st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR);
-    if (C == 4) {
-        double a0 = w[0], a1 = w[1], a2 = w[2], c = 0.0;
-        if (sc) {
-            double s0, s1, s2, sc_c = 0.0;
-            if (st.flags & AM_STEP_SHORTCUT_IDENT) {
-                s0 = r == 0; s1 = r == 1; s2 = r == 2;
+    const int64_t n = dev_count(L.n_dev, L.n_cap);
+    uint64_t* keys = keys_at(L);
+    const int64_t total = n * st.n_out;
+    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        int64_t item = gid / st.n_out;
+        int r = (int)(gid - item * st.n_out);
+        const double* w = st.W + (int64_t)r * st.ldw;
+        uint64_t* key = keys + item * L.KW;
+        int row = st.row_off + r;
+        double* z = L.Z + (item * L.zs + row) * C;
+        bool sc = st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR);
+        if (C == 4) {
+            double a0 = w[0], a1 = w[1], a2 = w[2], c = 0.0;
+            if (sc) {
+                double s0, s1, s2, sc_c = 0.0;
+                if (st.flags & AM_STEP_SHORTCUT_IDENT) {
+                    s0 = r == 0; s1 = r == 1; s2 = r == 2;
+                } else {
+                    const double* v = st.V + (int64_t)r * st.ldv;
+                    s0 = v[0]; s1 = v[1]; s2 = v[2];
+                    if (st.vb) sc_c = st.vb[r];
+                }
+                a0 = s0 + a0; a1 = s1 + a1; a2 = s2 + a2;
+                c = (sc_c + c) + st.b[r];
             } else {
-                const double* v = st.V + (int64_t)r * st.ldv;
-                s0 = v[0]; s1 = v[1]; s2 = v[2];
-                if (st.vb) sc_c = st.vb[r];
+                c = c + st.b[r];
             }
-            a0 = s0 + a0; a1 = s1 + a1; a2 = s2 + a2;
-            c = (sc_c + c) + st.b[r];
+            double nrm = sqrt((a0 * a0 + a1 * a1) + a2 * a2);
+            if (!(nrm > kDegen)) {
+                int bit = c > 0.0;
+                if (bit != key_bit(key, row)) {
+                    set_key_bit(key, row, bit);
+                    if (L.changed) L.changed[item] = 1;
+                }
+            }
+            reinterpret_cast<double2*>(z)[0] = make_double2(a0, a1);
+            reinterpret_cast<double2*>(z)[1] = make_double2(a2, c);
         } else {
-            c = c + st.b[r];
-        }
-        double nrm = sqrt((a0 * a0 + a1 * a1) + a2 * a2);
-        if (!(nrm > kDegen)) {
-            int bit = c > 0.0;
-            if (bit != key_bit(key, row)) {
-                set_key_bit(key, row, bit);
-                if (L.changed) L.changed[item] = 1;
-            }
-        }
-        reinterpret_cast<double2*>(z)[0] = make_double2(a0, a1);
-        reinterpret_cast<double2*>(z)[1] = make_double2(a2, c);
-    } else {
-        const double* x = L.pts + item * 3;
-        double acc = (x[0] * w[0] + x[1] * w[1]) + x[2] * w[2];
-        double pre;
-        if (sc) {
-            double s;
-            if (st.flags & AM_STEP_SHORTCUT_IDENT) {
-                s = x[r];
+            const double* x = L.pts + item * 3;
+            double acc = (x[0] * w[0] + x[1] * w[1]) + x[2] * w[2];
+            double pre;
+            if (sc) {
+                double s;
+                if (st.flags & AM_STEP_SHORTCUT_IDENT) {
+                    s = x[r];
+                } else {
+                    const double* v = st.V + (int64_t)r * st.ldv;
+                    s = (x[0] * v[0] + x[1] * v[1]) + x[2] * v[2];
+                    if (st.vb) s = s + st.vb[r];
+                }
+                pre = (s + acc) + st.b[r];
             } else {
-                const double* v = st.V + (int64_t)r * st.ldv;
-                s = (x[0] * v[0] + x[1] * v[1]) + x[2] * v[2];
-                if (st.vb) s = s + st.vb[r];
+                pre = acc + st.b[r];
             }
-            pre = (s + acc) + st.b[r];
-        } else {
-            pre = acc + st.b[r];
+            if (pre > 0.0) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)key_mask(row));
+            z[0] = pre;
         }
-        if (pre > 0.0) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)key_mask(row));
-        z[0] = pre;
     }
 }
 
+static int g_num_sms = 0;
+static int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (!g_num_sms) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
 void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
-    int64_t total = L.n_items * L.st.n_out;
+    int64_t total = L.n_cap * L.st.n_out;
     if (total <= 0) return;
-    int64_t blocks = (total + 255) / 256;
+    int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
     if (C == 4) { k_input_step<4><<<(unsigned)blocks, 256, 0, s>>>(L); ++g_launch_count; }
     else { k_input_step<1><<<(unsigned)blocks, 256, 0, s>>>(L); ++g_launch_count; }
 }
@@ -172,14 +188,15 @@ struct __align__(1024) GemmSmem {
 template <int C>
 struct XStager {
     double v[8];
-    __device__ __forceinline__ void load(const LayerLaunch& L, int64_t n0, int src_row, int n_src, int k0) {
+    __device__ __forceinline__ void load(const LayerLaunch& L, const uint64_t* keys, int64_t n, int64_t n0,
+                                         int src_row, int n_src, int k0) {
         int tid = threadIdx.x;
         if (C == 4) {
             // 16 items x 16 rows x 4 comps: thread -> item tid/8, rows 2*(tid%8) .. +1
             int it = tid >> 3, rr = (tid & 7) * 2;
             int64_t item = n0 / 4 + it;
-            bool ok = item < L.n_items;
-            const uint64_t* key = L.keys + (ok ? item : 0) * L.KW;
+            bool ok = item < n;
+            const uint64_t* key = keys + (ok ? item : 0) * L.KW;
 #pragma unroll
             for (int q = 0; q < 2; q++) {
                 int k = k0 + rr + q;
@@ -198,8 +215,8 @@ struct XStager {
             // 64 points x 16 rows: thread -> point tid/2, rows 8*(tid%2) .. +7
             int pt = tid >> 1, rr = (tid & 1) * 8;
             int64_t item = n0 + pt;
-            bool ok = item < L.n_items;
-            const uint64_t* key = L.keys + (ok ? item : 0) * L.KW;
+            bool ok = item < n;
+            const uint64_t* key = keys + (ok ? item : 0) * L.KW;
 #pragma unroll
             for (int q = 0; q < 8; q++) {
                 int k = k0 + rr + q;
@@ -228,6 +245,8 @@ struct XStager {
     }
 };
 
+// Persistent: each CTA walks output tiles (64 neuron rows x 64 item columns) of
+// the device-resident item count, so the launch is graph-capturable.
 template <int C>
 __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
                                                         const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
@@ -237,13 +256,17 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp & 1, wn = warp >> 1;
-    const int m0 = blockIdx.y * BM;
-    const int64_t n0 = (int64_t)blockIdx.x * BN;
+    const int64_t n = dev_count(L.n_dev, L.n_cap);
+    if (n <= 0) return;
+    uint64_t* keys = keys_at(L);
 
     const bool lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && !(st.flags & AM_STEP_SC_FROM_INPUT);
     const int kc0 = (st.n_in + BK - 1) / BK;
     const int kc1 = lin ? (st.n_sin + BK - 1) / BK : 0;
     const int nchunks = kc0 + kc1;
+    const int64_t ntx = (n * C + BN - 1) / BN;
+    const int nty = (st.n_out + BM - 1) / BM;
+    const int64_t ntiles = ntx * nty;
 
     if (tid == 0) {
         mbar_init(&S.bar[0], 1);
@@ -251,194 +274,200 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     }
-    if (C == 1 && tid < BN) { S.bits[tid][0] = 0; S.bits[tid][1] = 0; }
     __syncthreads();
 
-    auto issue_w = [&](int c, int stage) {
-        if (tid == 0) {
-            mbar_expect_tx(&S.bar[stage], BM * BK * sizeof(double));
-            if (c < kc0) tma_load_2d(S.w[stage], &tmW, &S.bar[stage], c * BK, m0);
-            else tma_load_2d(S.w[stage], &tmV, &S.bar[stage], (c - kc0) * BK, m0);
-        }
-    };
-    XStager<C> xs;
-    auto load_x = [&](int c) {
-        if (c < kc0) xs.load(L, n0, st.in_row_off, st.n_in, c * BK);
-        else xs.load(L, n0, st.sin_row_off, st.n_sin, (c - kc0) * BK);
-    };
-
-    double acc[2][4][4];
-#pragma unroll
-    for (int i = 0; i < 2; i++)
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-#pragma unroll
-            for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
-
-    issue_w(0, 0);
-    load_x(0);
-    xs.store(S.x[0]);
-    __syncthreads();
-
-    for (int c = 0; c < nchunks; c++) {
-        const int s = c & 1;
-        if (c + 1 < nchunks) {
-            issue_w(c + 1, s ^ 1);
-            load_x(c + 1);
-        }
-        mbar_wait(&S.bar[s], (c >> 1) & 1);
-        const double* ws = S.w[s];
-        const double* xsm = S.x[s];
-#pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double a[2][2], b[4];
-#pragma unroll
-            for (int mi = 0; mi < 2; mi++) {
-                int r = wm * 32 + mi * 16 + g;
-                a[mi][0] = ws[swz(r, kk + t)];
-                a[mi][1] = ws[swz(r + 8, kk + t)];
-            }
-#pragma unroll
-            for (int nj = 0; nj < 4; nj++) b[nj] = xsm[(wn * 32 + nj * 8 + g) * XLD + kk + t];
-#pragma unroll
-            for (int mi = 0; mi < 2; mi++)
-#pragma unroll
-                for (int nj = 0; nj < 4; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
-        }
-        if (c + 1 < nchunks) xs.store(S.x[s ^ 1]);
-        __syncthreads();
-    }
-
-    // ---------------------------------------------------------- epilogue
     const bool sc_ident = st.flags & AM_STEP_SHORTCUT_IDENT;
     const bool sc_input_lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && (st.flags & AM_STEP_SC_FROM_INPUT);
     const bool sc_input_id = sc_ident && (st.flags & AM_STEP_SC_FROM_INPUT);
     const bool has_sc = (st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR)) != 0;
-    const int wbase = (st.row_off + m0) >> 6;  // forward: first key word the tile touches
 
+    uint32_t gchunk = 0;  // chunks consumed by this CTA so far (mbarrier phase tracking)
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = (int)(tile / ntx) * BM;
+        const int64_t n0 = (tile % ntx) * BN;
+        if (C == 1 && tid < BN) { S.bits[tid][0] = 0; S.bits[tid][1] = 0; }
+
+        auto issue_w = [&](int c, int stage) {
+            if (tid == 0) {
+                mbar_expect_tx(&S.bar[stage], BM * BK * sizeof(double));
+                if (c < kc0) tma_load_2d(S.w[stage], &tmW, &S.bar[stage], c * BK, m0);
+                else tma_load_2d(S.w[stage], &tmV, &S.bar[stage], (c - kc0) * BK, m0);
+            }
+        };
+        XStager<C> xs;
+        auto load_x = [&](int c) {
+            if (c < kc0) xs.load(L, keys, n, n0, st.in_row_off, st.n_in, c * BK);
+            else xs.load(L, keys, n, n0, st.sin_row_off, st.n_sin, (c - kc0) * BK);
+        };
+
+        double acc[2][4][4];
 #pragma unroll
-    for (int mi = 0; mi < 2; mi++) {
+        for (int i = 0; i < 2; i++)
 #pragma unroll
-        for (int half = 0; half < 2; half++) {
-            const int rl = wm * 32 + mi * 16 + g + half * 8;  // local row
-            const int r = m0 + rl;
-            const bool rok = r < st.n_out;
-            const int row = st.row_off + r;
+            for (int j = 0; j < 4; j++)
 #pragma unroll
-            for (int nj = 0; nj < 4; nj++) {
-                const int64_t col = n0 + wn * 32 + nj * 8 + 2 * t;
-                double v0 = acc[mi][nj][half * 2], v1 = acc[mi][nj][half * 2 + 1];
-                if (C == 4) {
-                    const int64_t item = col >> 2;
-                    const int comp = (int)(col & 3);  // 0 (even t) or 2 (odd t)
-                    const bool ok = rok && item < L.n_items;
-                    if (ok && has_sc) {
-                        double s0 = 0.0, s1 = 0.0;
-                        if (sc_input_id) {            // A_in = I, c_in = 0 (block starts at x)
-                            s0 = (comp == r) ? 1.0 : 0.0;
-                            s1 = (comp == 0 && r == 1) ? 1.0 : 0.0;
-                        } else if (sc_input_lin) {    // V @ I = V[:, :3], V @ 0 + vb
-                            const double* vr = st.V + (int64_t)r * st.ldv;
-                            s0 = vr[comp];
-                            s1 = comp == 0 ? vr[1] : (st.vb ? st.vb[r] : 0.0);
-                        } else if (sc_ident) {        // masked block input rows
-                            const uint64_t* key = L.keys + item * L.KW;
-                            int srow = st.sin_row_off + r;
-                            if (key_bit(key, srow)) {
-                                double2 p = *reinterpret_cast<const double2*>(L.Z + (item * L.zs + srow) * 4 + comp);
-                                s0 = p.x; s1 = p.y;
+                for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+
+        issue_w(0, gchunk & 1);
+        load_x(0);
+        xs.store(S.x[gchunk & 1]);
+        __syncthreads();
+
+        for (int c = 0; c < nchunks; c++) {
+            const uint32_t gc = gchunk + c;
+            const int s = gc & 1;
+            if (c + 1 < nchunks) {
+                issue_w(c + 1, s ^ 1);
+                load_x(c + 1);
+            }
+            mbar_wait(&S.bar[s], (gc >> 1) & 1);
+            const double* ws = S.w[s];
+            const double* xsm = S.x[s];
+#pragma unroll
+            for (int kk = 0; kk < BK; kk += 4) {
+                double a[2][2], b[4];
+#pragma unroll
+                for (int mi = 0; mi < 2; mi++) {
+                    int r = wm * 32 + mi * 16 + g;
+                    a[mi][0] = ws[swz(r, kk + t)];
+                    a[mi][1] = ws[swz(r + 8, kk + t)];
+                }
+#pragma unroll
+                for (int nj = 0; nj < 4; nj++) b[nj] = xsm[(wn * 32 + nj * 8 + g) * XLD + kk + t];
+#pragma unroll
+                for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+                    for (int nj = 0; nj < 4; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
+            }
+            if (c + 1 < nchunks) xs.store(S.x[s ^ 1]);
+            __syncthreads();
+        }
+        gchunk += nchunks;
+
+        // ------------------------------------------------------ epilogue
+        const int wbase = (st.row_off + m0) >> 6;  // forward: first key word the tile touches
+#pragma unroll
+        for (int mi = 0; mi < 2; mi++) {
+#pragma unroll
+            for (int half = 0; half < 2; half++) {
+                const int rl = wm * 32 + mi * 16 + g + half * 8;  // local row
+                const int r = m0 + rl;
+                const bool rok = r < st.n_out;
+                const int row = st.row_off + r;
+#pragma unroll
+                for (int nj = 0; nj < 4; nj++) {
+                    const int64_t col = n0 + wn * 32 + nj * 8 + 2 * t;
+                    double v0 = acc[mi][nj][half * 2], v1 = acc[mi][nj][half * 2 + 1];
+                    if (C == 4) {
+                        const int64_t item = col >> 2;
+                        const int comp = (int)(col & 3);  // 0 (even t) or 2 (odd t)
+                        const bool ok = rok && item < n;
+                        if (ok && has_sc) {
+                            double s0 = 0.0, s1 = 0.0;
+                            if (sc_input_id) {            // A_in = I, c_in = 0 (block starts at x)
+                                s0 = (comp == r) ? 1.0 : 0.0;
+                                s1 = (comp == 0 && r == 1) ? 1.0 : 0.0;
+                            } else if (sc_input_lin) {    // V @ I = V[:, :3], V @ 0 + vb
+                                const double* vr = st.V + (int64_t)r * st.ldv;
+                                s0 = vr[comp];
+                                s1 = comp == 0 ? vr[1] : (st.vb ? st.vb[r] : 0.0);
+                            } else if (sc_ident) {        // masked block input rows
+                                const uint64_t* key = keys + item * L.KW;
+                                int srow = st.sin_row_off + r;
+                                if (key_bit(key, srow)) {
+                                    double2 p = *reinterpret_cast<const double2*>(L.Z + (item * L.zs + srow) * 4 + comp);
+                                    s0 = p.x; s1 = p.y;
+                                }
+                            } else {                      // V @ A_in is in acc (second K segment); add vb
+                                s1 = (comp == 2 && st.vb) ? st.vb[r] : 0.0;
                             }
-                        } else {                      // V @ A_in is in acc (second K segment); add vb
-                            s1 = (comp == 2 && st.vb) ? st.vb[r] : 0.0;
+                            v0 = s0 + v0;   // pre_A = sA + W A ; pre_c = (sc + W c) + b
+                            v1 = s1 + v1;
                         }
-                        v0 = s0 + v0;   // pre_A = sA + W A ; pre_c = (sc + W c) + b
-                        v1 = s1 + v1;
-                    }
-                    if (comp == 2) v1 = v1 + (ok ? st.b[r] : 0.0);
-                    // canonical bit: the pair (t, t^1) holds the 4 components of (item, row)
-                    double p0 = __shfl_xor_sync(0xffffffffu, v0, 1);
-                    double p1 = __shfl_xor_sync(0xffffffffu, v1, 1);
-                    if (ok) {
-                        double c0, c1, c2, c3;
-                        if (comp == 0) { c0 = v0; c1 = v1; c2 = p0; c3 = p1; }
-                        else { c0 = p0; c1 = p1; c2 = v0; c3 = v1; }
-                        if (comp == 0) {
-                            double nrm = sqrt((c0 * c0 + c1 * c1) + c2 * c2);
-                            if (!(nrm > kDegen)) {
-                                uint64_t* key = L.keys + item * L.KW;
-                                int bit = c3 > 0.0;
-                                if (bit != key_bit(key, row)) {
-                                    set_key_bit(key, row, bit);
-                                    if (L.changed) L.changed[item] = 1;
+                        if (comp == 2) v1 = v1 + (ok ? st.b[r] : 0.0);
+                        // canonical bit: the pair (t, t^1) holds the 4 components of (item, row)
+                        double p0 = __shfl_xor_sync(0xffffffffu, v0, 1);
+                        double p1 = __shfl_xor_sync(0xffffffffu, v1, 1);
+                        if (ok) {
+                            if (comp == 0) {
+                                double nrm = sqrt((v0 * v0 + v1 * v1) + p0 * p0);
+                                if (!(nrm > kDegen)) {
+                                    uint64_t* key = keys + item * L.KW;
+                                    int bit = p1 > 0.0;
+                                    if (bit != key_bit(key, row)) {
+                                        set_key_bit(key, row, bit);
+                                        if (L.changed) L.changed[item] = 1;
+                                    }
                                 }
                             }
+                            *reinterpret_cast<double2*>(L.Z + (item * L.zs + row) * 4 + comp) = make_double2(v0, v1);
                         }
-                        *reinterpret_cast<double2*>(L.Z + (item * L.zs + row) * 4 + comp) = make_double2(v0, v1);
-                    }
-                } else {
+                    } else {
 #pragma unroll
-                    for (int e = 0; e < 2; e++) {
-                        const int64_t item = col + e;
-                        double v = e ? v1 : v0;
-                        if (!(rok && item < L.n_items)) continue;
-                        double pre;
-                        if (has_sc) {
-                            double sc = 0.0;
-                            const double* x = L.pts ? L.pts + item * 3 : nullptr;
-                            if (sc_input_id) {
-                                sc = x[r];
-                            } else if (sc_input_lin) {
-                                const double* vr = st.V + (int64_t)r * st.ldv;
-                                sc = (x[0] * vr[0] + x[1] * vr[1]) + x[2] * vr[2];
-                                if (st.vb) sc = sc + st.vb[r];
-                            } else if (sc_ident) {
-                                int srow = st.sin_row_off + r;
-                                if (key_bit(L.keys + item * L.KW, srow)) sc = L.Z[item * L.zs + srow];
-                            } else if (st.vb) {
-                                sc = st.vb[r];  // V h_in is in acc (second K segment)
+                        for (int e = 0; e < 2; e++) {
+                            const int64_t item = col + e;
+                            double v = e ? v1 : v0;
+                            if (!(rok && item < n)) continue;
+                            double pre;
+                            if (has_sc) {
+                                double sc = 0.0;
+                                const double* x = L.pts ? L.pts + item * 3 : nullptr;
+                                if (sc_input_id) {
+                                    sc = x[r];
+                                } else if (sc_input_lin) {
+                                    const double* vr = st.V + (int64_t)r * st.ldv;
+                                    sc = (x[0] * vr[0] + x[1] * vr[1]) + x[2] * vr[2];
+                                    if (st.vb) sc = sc + st.vb[r];
+                                } else if (sc_ident) {
+                                    int srow = st.sin_row_off + r;
+                                    if (key_bit(keys + item * L.KW, srow)) sc = L.Z[item * L.zs + srow];
+                                } else if (st.vb) {
+                                    sc = st.vb[r];  // V h_in is in acc (second K segment)
+                                }
+                                pre = (sc + v) + st.b[r];   // reference: shortcut(h_in) + h W^T + b
+                            } else {
+                                pre = v + st.b[r];
                             }
-                            pre = (sc + v) + st.b[r];   // reference: shortcut(h_in) + h W^T + b
-                        } else {
-                            pre = v + st.b[r];
-                        }
-                        L.Z[item * L.zs + row] = pre;
-                        if (pre > 0.0) {
-                            int lb = row - wbase * 64;
-                            atomicOr(&S.bits[(int)(item - n0)][lb >> 6], (unsigned long long)key_mask(lb));
+                            L.Z[item * L.zs + row] = pre;
+                            if (pre > 0.0) {
+                                int lb = row - wbase * 64;
+                                atomicOr(&S.bits[(int)(item - n0)][lb >> 6], (unsigned long long)key_mask(lb));
+                            }
                         }
                     }
                 }
             }
         }
-    }
-    if (C == 1) {
-        __syncthreads();
-        if (tid < BN) {
-            int64_t item = n0 + tid;
-            if (item < L.n_items) {
-                uint64_t* key = L.keys + item * L.KW;
-                int nwords = (L.KW);
-                if (S.bits[tid][0]) atomicOr(reinterpret_cast<unsigned long long*>(key + wbase), S.bits[tid][0]);
-                if (S.bits[tid][1] && wbase + 1 < nwords)
-                    atomicOr(reinterpret_cast<unsigned long long*>(key + wbase + 1), S.bits[tid][1]);
+        if (C == 1) {
+            __syncthreads();
+            if (tid < BN) {
+                int64_t item = n0 + tid;
+                if (item < n) {
+                    uint64_t* key = keys + item * L.KW;
+                    if (S.bits[tid][0]) atomicOr(reinterpret_cast<unsigned long long*>(key + wbase), S.bits[tid][0]);
+                    if (S.bits[tid][1] && wbase + 1 < L.KW)
+                        atomicOr(reinterpret_cast<unsigned long long*>(key + wbase + 1), S.bits[tid][1]);
+                }
             }
+            __syncthreads();
         }
     }
 }
 
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV, cudaStream_t s) {
-    if (L.n_items <= 0) return;
-    int64_t cols = L.n_items * C;
-    dim3 grid((unsigned)((cols + BN - 1) / BN), (unsigned)((L.st.n_out + BM - 1) / BM));
+    if (L.n_cap <= 0) return;
+    int64_t cols = L.n_cap * C;
+    int64_t tiles = ((cols + BN - 1) / BN) * ((L.st.n_out + BM - 1) / BM);
+    int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * 5);
     size_t smem = sizeof(GemmSmem) + 1024;
     if (C == 4) {
         static bool init = false;
         if (!init) { cudaFuncSetAttribute(k_gemm_step<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
-        { k_gemm_step<4><<<grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L); ++g_launch_count; }
+        { k_gemm_step<4><<<(unsigned)grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L); ++g_launch_count; }
     } else {
         static bool init = false;
         if (!init) { cudaFuncSetAttribute(k_gemm_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
-        { k_gemm_step<1><<<grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L); ++g_launch_count; }
+        { k_gemm_step<1><<<(unsigned)grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L); ++g_launch_count; }
     }
 }
 
@@ -451,76 +480,85 @@ struct SubDev {
 
 // face functional of every subnetwork: head_w @ (s ⊙ Z_last) (+ head_b on the offset)
 // reference network.py:440-442
-__global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces, int64_t n_items, int zs, int KW,
-                            const SubDev* subs, int n_subs) {
-    int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    int64_t item = wid / n_subs;
-    int j = (int)(wid - item * n_subs);
-    if (item >= n_items) return;
-    const SubDev sd = subs[j];
-    const uint64_t* key = keys + item * KW;
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    for (int r = lane; r < sd.last_n; r += 32) {
-        int row = sd.last_row + r;
-        if (!key_bit(key, row)) continue;
-        const double2* p = reinterpret_cast<const double2*>(Z + (item * zs + row) * 4);
-        double2 x = p[0], y = p[1];
-        double w = sd.hw[r];
-        a0 += w * x.x; a1 += w * x.y; a2 += w * y.x; a3 += w * y.y;
-    }
+__global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
+                            int64_t n_cap, int zs, int KW, const SubDev* subs, int n_subs) {
+    const int64_t n = dev_count(n_dev, n_cap);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wid < n * n_subs; wid += nw) {
+        int64_t item = wid / n_subs;
+        int j = (int)(wid - item * n_subs);
+        const SubDev sd = subs[j];
+        const uint64_t* key = keys + item * KW;
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        for (int r = lane; r < sd.last_n; r += 32) {
+            int row = sd.last_row + r;
+            if (!key_bit(key, row)) continue;
+            const double2* p = reinterpret_cast<const double2*>(Z + (item * zs + row) * 4);
+            double2 x = p[0], y = p[1];
+            double w = sd.hw[r];
+            a0 += w * x.x; a1 += w * x.y; a2 += w * y.x; a3 += w * y.y;
+        }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-        a3 += __shfl_xor_sync(0xffffffffu, a3, o);
-    }
-    if (lane == 0) {
-        double* f = faces + (item * n_subs + j) * 4;
-        f[0] = a0; f[1] = a1; f[2] = a2; f[3] = a3 + sd.hb;
+        for (int o = 16; o; o >>= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+            a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+        }
+        if (lane == 0) {
+            double* f = faces + (item * n_subs + j) * 4;
+            f[0] = a0; f[1] = a1; f[2] = a2; f[3] = a3 + sd.hb;
+        }
     }
 }
 
 // F_j(x) = head_w @ relu(Z_last) + head_b; F = max_j (argmax lowest index) -- reference network.py:352-392
-__global__ void k_forward_head(const double* Z, uint64_t* keys, double* vals, int64_t n_items, int zs, int KW,
-                               const SubDev* subs, int n_subs, int ensemble) {
-    int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (item >= n_items) return;
-    const uint64_t* key = keys + item * KW;
-    double best = 0.0;
-    int arg = 0;
-    for (int j = 0; j < n_subs; j++) {
-        const SubDev sd = subs[j];
-        double a = 0.0;
-        for (int r = lane; r < sd.last_n; r += 32) {
-            int row = sd.last_row + r;
-            if (key_bit(key, row)) a += Z[item * zs + row] * sd.hw[r];
-        }
+__global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsigned long long* key_off, double* vals,
+                               const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const SubDev* subs,
+                               int n_subs, int ensemble) {
+    const int64_t n = dev_count(n_dev, n_cap);
+    uint64_t* keys = key_off ? keys_base + (int64_t)(*key_off) * KW : keys_base;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < n; item += nw) {
+        const uint64_t* key = keys + item * KW;
+        double best = 0.0;
+        int arg = 0;
+        for (int j = 0; j < n_subs; j++) {
+            const SubDev sd = subs[j];
+            double a = 0.0;
+            for (int r = lane; r < sd.last_n; r += 32) {
+                int row = sd.last_row + r;
+                if (key_bit(key, row)) a += Z[item * zs + row] * sd.hw[r];
+            }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        double f = a + sd.hb;
-        if (j == 0 || f > best) { best = f; arg = j; }
-    }
-    if (lane == 0) {
-        if (vals) vals[item] = best;
-        if (ensemble) keys[item * KW + KW - 1] = (uint64_t)arg;
+            for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            double f = a + sd.hb;
+            if (j == 0 || f > best) { best = f; arg = j; }
+        }
+        if (lane == 0) {
+            if (vals) vals[item] = best;
+            if (ensemble) keys[item * KW + KW - 1] = (uint64_t)arg;
+        }
     }
 }
 
-void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, int64_t n_items, int zs, int KW,
-                          const void* subs, int n_subs, cudaStream_t s) {
-    int64_t warps = n_items * n_subs;
+void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
+                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, cudaStream_t s) {
+    int64_t warps = n_cap * n_subs;
     if (warps <= 0) return;
-    { k_face_head<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(Z, keys, faces, n_items, zs, KW,
-                                                                    static_cast<const SubDev*>(subs), n_subs); ++g_launch_count; }
+    int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)num_sms() * 8);
+    { k_face_head<<<(unsigned)blocks, 256, 0, s>>>(Z, keys, faces, n_dev, n_cap, zs, KW,
+                                                 static_cast<const SubDev*>(subs), n_subs); ++g_launch_count; }
 }
-void launch_forward_head_dev(const double* Z, uint64_t* keys, double* vals, int64_t n_items, int zs, int KW,
-                             const void* subs, int n_subs, int ensemble, cudaStream_t s) {
-    if (n_items <= 0) return;
-    { k_forward_head<<<(unsigned)((n_items * 32 + 255) / 256), 256, 0, s>>>(
-        Z, keys, vals, n_items, zs, KW, static_cast<const SubDev*>(subs), n_subs, ensemble); ++g_launch_count; }
+void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
+                             const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,
+                             int n_subs, int ensemble, cudaStream_t s) {
+    if (n_cap <= 0) return;
+    int64_t blocks = std::min<int64_t>((n_cap * 32 + 255) / 256, (int64_t)num_sms() * 8);
+    { k_forward_head<<<(unsigned)blocks, 256, 0, s>>>(Z, keys, key_off, vals, n_dev, n_cap, zs, KW,
+                                                    static_cast<const SubDev*>(subs), n_subs, ensemble); ++g_launch_count; }
 }
 
 }  // namespace am

@@ -1,15 +1,18 @@
 // am_engine.cu -- C-ABI engine: breadth-first analytic marching on one GPU.
 //
-// Replaces the reference's _Marcher (reference marching.py:216-301): the
-// work queue becomes a wave of candidate states in HBM, the visited set the
-// on-device hash set (am_hash.cu), per-cell affine maps the batched DMMA
-// composition (am_compose.cu) and face extraction the warp-per-cell solver
-// (am_face.cu).  A wave:
-//   1 insert raw candidates (dedup against everything ever dispatched)
-//   2 compose the new ones (all layers, fp64 DMMA) -> planes + canonical states
-//   3 insert canonical states whose key changed; build the frontier of new cells
-//   4 face-extract the frontier -> polygons, flip candidates, probe points
-//   5 forward-evaluate the probe points -> probe candidates
+// Replaces the reference's _Marcher (reference marching.py:216-301).  The work
+// queue is a device array of pool indices of not-yet-composed states; the
+// visited set is the device hash set (am_hash.cu).  One BFS iteration:
+//   take     guard capacities, dequeue up to B states            (k_take)
+//   compose  all hidden layers for the batch, fp64 DMMA           (am_compose.cu)
+//   canon    states whose canonical key differs are re-inserted   (insert/fixup)
+//   frontier new cells of this iteration                          (k_frontier)
+//   face     polygons + flip candidates + probe points            (am_face.cu)
+//   probe    forward pass at the probe points                     (am_compose.cu C=1)
+//   enqueue  insert every emitted state; winners join the queue   (insert/fixup)
+// Every kernel reads its item count from device counters, so the iteration is
+// captured once as a CUDA graph and replayed; the host only synchronises every
+// few iterations to test for termination and to grow buffers.
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
@@ -21,20 +24,8 @@
 #include "am_internal.h"
 
 namespace am {
-void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s);
-void launch_compact(const int32_t* flag, int32_t want, int64_t n, int32_t* out, unsigned long long* count,
-                    cudaStream_t s);
-void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst, cudaStream_t s);
-void launch_frontier(int64_t nR, const int32_t* changed, const int32_t* R, const int32_t* raw_pool,
-                     const int32_t* canon_pos, const int32_t* canon_status, const int32_t* canon_pool,
-                     uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* nF, int64_t max_new,
-                     unsigned long long* capped, cudaStream_t s);
-void launch_scatter_pos(const int32_t* X, int64_t nX, int32_t* pos, cudaStream_t s);
-void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s);
-void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, int64_t n_items, int zs, int KW,
-                          const void* subs, int n_subs, cudaStream_t s);
-void launch_forward_head_dev(const double* Z, uint64_t* keys, double* vals, int64_t n_items, int zs, int KW,
-                             const void* subs, int n_subs, int ensemble, cudaStream_t s);
+unsigned long long g_launch_count = 0;
+
 void launch_seed_project(const double* X, const double* faces, const uint64_t* keys, int KW, int M, int ensemble,
                          int64_t n, const int32_t* active, double* Xp, int32_t* done_flat, cudaStream_t s);
 void launch_seed_check(const uint64_t* snew, const uint64_t* canon, int KW, int64_t n, int32_t* active,
@@ -43,9 +34,11 @@ void launch_seed_check(const uint64_t* snew, const uint64_t* canon, int KW, int6
 void launch_dichotomy_step(const double* vals, double* xp, double* xn, double* fp, double* fn, double* mid,
                            int32_t* active, double* out, int64_t n, double eps, double seed_tol, int last,
                            cudaStream_t s);
-
 void launch_midpoint(const double* a, const double* b, double* m, int64_t n, cudaStream_t s);
 void launch_count_active(const int32_t* active, int64_t n, unsigned long long* cnt, cudaStream_t s);
+void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s);
+void launch_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
+                         unsigned long long* cnt, cudaStream_t s);
 
 struct SubDev {
     int last_row, last_n;
@@ -55,10 +48,6 @@ struct SubDev {
 }  // namespace am
 
 using namespace am;
-
-namespace am {
-unsigned long long g_launch_count = 0;
-}
 
 static thread_local std::string g_err;
 static int fail(int code, const char* fmt, ...) {
@@ -76,25 +65,32 @@ static int fail(int code, const char* fmt, ...) {
         if (_e != cudaSuccess) return fail(AM_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x, \
                                            cudaGetErrorString(_e));                            \
     } while (0)
+#define RC(x)                  \
+    do {                       \
+        int _r = (x);          \
+        if (_r) return _r;     \
+    } while (0)
 
 template <class T>
 struct DBuf {
     T* p = nullptr;
     int64_t n = 0;  // capacity in elements
-    cudaError_t reserve(int64_t m, cudaStream_t s, bool keep = false, int64_t keep_n = 0) {
+    // grow to >= m elements (2x geometric); keep the first keep_n elements
+    cudaError_t reserve(int64_t m, cudaStream_t s, bool keep = false, int64_t keep_n = 0, bool* moved = nullptr) {
         if (m <= n) return cudaSuccess;
-        int64_t cap = std::max<int64_t>(m, n + n / 2);
+        int64_t cap = std::max<int64_t>(m, 2 * n);
         T* q = nullptr;
         cudaError_t e = cudaMalloc(&q, (size_t)cap * sizeof(T));
         if (e != cudaSuccess) return e;
         if (keep && p && keep_n > 0) {
             e = cudaMemcpyAsync(q, p, (size_t)keep_n * sizeof(T), cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) return e;
-            cudaStreamSynchronize(s);
         }
+        cudaStreamSynchronize(s);
         if (p) cudaFree(p);
         p = q;
         n = cap;
+        if (moved) *moved = true;
         return cudaSuccess;
     }
     void release() {
@@ -104,13 +100,10 @@ struct DBuf {
     }
 };
 
-enum Ctr {
-    C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_NEXT, C_PROBE, C_OVF0, C_OVF1, C_LIST, C_FRONT, C_CAPPED, C_N
-};
-
 struct am_engine {
     int device = 0;
     cudaStream_t stream = 0;
+    bool own_stream = false;
     am_march_params P{};
     // network
     int NB = 0, M = 0, KW = 0, ensemble = 0, zs = 0;
@@ -120,45 +113,44 @@ struct am_engine {
     std::vector<int> tmV_ok;
     DBuf<double> params, wpad;
     DBuf<uint8_t> subdev;
-    std::vector<SubDev> hsub;
     double flops_per_cell = 0, flops_per_point = 0;
-    // hash set
+    // hash set + queue
     DBuf<uint64_t> table, pool;
     DBuf<uint32_t> pool_flags;
+    DBuf<int32_t> queue;
     uint64_t tcap = 0;
     // counters (device) + host mirror
     DBuf<unsigned long long> ctr;
     unsigned long long hctr[C_N] = {0};
-    // candidates: current wave and next wave
-    DBuf<uint64_t> cand, next;
-    int64_t n_cand = 0;
-    // batch buffers
-    int64_t B = 0;
+    // batch buffers (capacity B)
+    int64_t B = 0, E = 0, PB = 0;   // batch cells, emitted keys, probe points per iteration
     DBuf<double> Z, faces;
-    DBuf<uint64_t> ckey;
-    DBuf<int32_t> changed, status, status2, raw_pool, canon_pos, canon_pool, R, X, f_items, f_pool;
-    DBuf<uint64_t> slot, slot2;
-    // probes
-    DBuf<double> probe_pts, probe_vals, pZ;
+    DBuf<uint64_t> ckey, slot, slot2, scratch, outbox;
+    DBuf<int32_t> changed, status, status2, canon_pos, canon_pool, X, f_items, f_pool, batch_pool, local_idx;
+    DBuf<double> probe_pts, pZ;
     // results
     DBuf<int32_t> cell_pool, cell_nv, edge_nrefs, edge_refs;
     DBuf<int64_t> cell_voff, edge_roff;
     DBuf<double> verts;
-    // outbox (sharded)
-    DBuf<int32_t> owner;
-    std::vector<int64_t> outbox_counts;
-    DBuf<uint64_t> outbox;
-    int64_t n_outbox = 0;
-    // seeding scratch
-    DBuf<double> sx, sxp;
+    // host-sized scratch (seeding, pushes, primitives)
+    DBuf<uint64_t> hkeys;
+    DBuf<int32_t> hstatus;
+    DBuf<uint64_t> hslot;
+    DBuf<double> sx, sxp, pvals;
     DBuf<uint64_t> ss, ssn, sres;
     DBuf<int32_t> sact, sdone;
+    // graph of one iteration
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    bool graph_valid = false;
+    int graph_batch = 8;
+    unsigned long long graph_kernels = 0;
     // stats
     bool timing = false;
-    cudaEvent_t ev[4];
-    double t_compose = 0, t_face = 0, flops = 0, face_bytes = 0, n_comp_cells = 0, n_face_cells = 0;
-    int64_t cells_total = 0;
-    bool capped = false;
+    cudaEvent_t ev[6];
+    double t_compose = 0, t_face = 0, t_probe = 0, flops = 0, pflops = 0, face_bytes = 0;
+    double n_comp_cells = 0, n_face_cells = 0, n_probes = 0;
+    int64_t iters = 0;
 };
 
 extern "C" const char* am_last_error(void) { return g_err.c_str(); }
@@ -198,16 +190,19 @@ static HashSet hs(am_engine* e) {
     H.KW = e->KW;
     return H;
 }
-// ensure room for `extra` more keys in the hash set (load factor <= 1/2)
+static int64_t emit_per_cell() { return kEmitFlipsPerCell + kVertsPerCell; }
+
+// hash set + queue room for `extra` more states (load factor <= 1/2)
 static int ensure_hash(am_engine* e, int64_t extra) {
-    int rc = sync_counters(e);
-    if (rc) return rc;
+    RC(sync_counters(e));
     int64_t np = (int64_t)e->hctr[C_POOL];
     int64_t need = np + extra;
-    if ((int64_t)(e->pool.n / e->KW) < need) {
-        CK(e->pool.reserve(need * e->KW, e->stream, true, np * e->KW));
-        CK(e->pool_flags.reserve(e->pool.n / e->KW, e->stream, true, np));
+    bool moved = false;
+    if (e->pool.n / e->KW < need) {
+        CK(e->pool.reserve(need * e->KW, e->stream, true, np * e->KW, &moved));
+        CK(e->pool_flags.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
     }
+    CK(e->queue.reserve(e->pool.n / e->KW, e->stream, true, (int64_t)e->hctr[C_QTAIL], &moved));
     if ((int64_t)e->tcap < 2 * need) {
         uint64_t cap = e->tcap ? e->tcap : 1024;
         while ((int64_t)cap < 2 * need) cap <<= 1;
@@ -217,7 +212,29 @@ static int ensure_hash(am_engine* e, int64_t extra) {
         CK(cudaMemsetAsync(e->table.p, 0xff, cap * sizeof(uint64_t), e->stream));
         launch_hash_rebuild(hs(e), np, e->stream);
         CK(cudaGetLastError());
+        moved = true;
     }
+    if (moved) e->graph_valid = false;
+    return AM_OK;
+}
+
+static int ensure_results(am_engine* e, int64_t cells) {
+    RC(sync_counters(e));
+    int64_t nc = (int64_t)e->hctr[C_CELLS], nv = (int64_t)e->hctr[C_VERTS], nr = (int64_t)e->hctr[C_REFS];
+    cudaStream_t s = e->stream;
+    bool moved = false;
+    CK(e->cell_pool.reserve(nc + cells, s, true, nc, &moved));
+    CK(e->cell_nv.reserve(nc + cells, s, true, nc, &moved));
+    CK(e->cell_voff.reserve(nc + cells, s, true, nc, &moved));
+    CK(e->verts.reserve((nv + cells * kVertsPerCell) * 3, s, true, nv * 3, &moved));
+    CK(e->edge_nrefs.reserve(nv + cells * kVertsPerCell, s, true, nv, &moved));
+    CK(e->edge_roff.reserve(nv + cells * kVertsPerCell, s, true, nv, &moved));
+    CK(e->edge_refs.reserve(nr + cells * kRefsPerCell, s, true, nr, &moved));
+    if (e->P.world > 1) {
+        int64_t no = (int64_t)e->hctr[C_NOUT];
+        CK(e->outbox.reserve((no + cells * (1 + emit_per_cell())) * e->KW, s, true, no * e->KW, &moved));
+    }
+    if (moved) e->graph_valid = false;
     return AM_OK;
 }
 
@@ -232,6 +249,10 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     am_engine* e = new am_engine();
     e->device = device;
     e->stream = (cudaStream_t)stream;
+    if (!e->stream) {  // graphs cannot be captured on the legacy default stream
+        CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->own_stream = true;
+    }
     e->P = *p;
     if (e->P.world < 1) e->P.world = 1;
     e->NB = net->n_bits;
@@ -298,31 +319,49 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
             e->flops_per_point += 2.0 * d.n_out * d.n_sin;
         }
     }
-    e->hsub.resize(e->M);
+    std::vector<SubDev> hsub(e->M);
     for (int j = 0; j < e->M; j++) {
         const int64_t* sb = &e->subs[(size_t)j * AM_SUB_FIELDS];
         int last = (int)(sb[0] + sb[1] - 1);
         const int64_t* st = &e->steps[(size_t)last * AM_STEP_FIELDS];
-        e->hsub[j].last_row = (int)st[7];
-        e->hsub[j].last_n = (int)st[1];
-        e->hsub[j].hw = e->params.p + sb[2];
-        e->hsub[j].hb = net->h_params[sb[3]];
+        hsub[j].last_row = (int)st[7];
+        hsub[j].last_n = (int)st[1];
+        hsub[j].hw = e->params.p + sb[2];
+        hsub[j].hb = net->h_params[sb[3]];
     }
     CK(e->subdev.reserve((int64_t)(sizeof(SubDev) * e->M), e->stream));
-    CK(cudaMemcpy(e->subdev.p, e->hsub.data(), sizeof(SubDev) * e->M, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(e->subdev.p, hsub.data(), sizeof(SubDev) * e->M, cudaMemcpyHostToDevice));
 
-    // batch size from the plane-buffer budget
-    int64_t budget = e->P.mem_budget > 0 ? e->P.mem_budget : (int64_t)2 << 30;
-    int64_t per = (int64_t)e->zs * 4 * 8 + (int64_t)e->M * 32 + e->KW * 8 + 64;
-    e->B = e->P.batch_cells > 0 ? e->P.batch_cells : std::max<int64_t>(64, std::min<int64_t>(budget / per, 1 << 20));
+    // batch size from the per-iteration memory budget: compose planes + worst-case probe
+    // activations + emitted keys per batch cell
+    int64_t budget = e->P.mem_budget > 0 ? e->P.mem_budget : (int64_t)4 << 30;
+    int64_t per = (int64_t)e->zs * 32 + (int64_t)kVertsPerCell * e->zs * 8 + emit_per_cell() * e->KW * 8 * 2 +
+                  e->M * 32 + 256;
+    e->B = e->P.batch_cells > 0 ? e->P.batch_cells : std::max<int64_t>(256, std::min<int64_t>(budget / per, 16384));
+    e->E = e->B * emit_per_cell();
+    e->PB = e->B * kVertsPerCell;
     if (e->P.max_cells <= 0) e->P.max_cells = INT64_C(10000000);
-
-    CK(e->ctr.reserve(C_N, e->stream));
+    cudaStream_t s = e->stream;
+    CK(e->Z.reserve(e->B * e->zs * 4, s));
+    CK(e->faces.reserve(e->B * e->M * 4, s));
+    CK(e->ckey.reserve(e->B * e->KW, s));
+    DBuf<int32_t>* bi[] = {&e->changed, &e->status2, &e->canon_pos, &e->canon_pool, &e->X, &e->f_items, &e->f_pool,
+                           &e->batch_pool};
+    for (auto* x : bi) CK(x->reserve(e->B, s));
+    CK(e->slot2.reserve(e->B, s));
+    CK(e->scratch.reserve(e->E * e->KW, s));
+    CK(e->status.reserve(e->E, s));
+    CK(e->slot.reserve(e->E, s));
+    CK(e->local_idx.reserve(e->E, s));
+    CK(e->probe_pts.reserve(e->PB * 3, s));
+    CK(e->pZ.reserve(e->PB * e->zs, s));
+    CK(e->outbox.reserve(e->KW, s));
+    CK(e->ctr.reserve(C_N, s));
     CK(cudaMemset(e->ctr.p, 0, C_N * sizeof(unsigned long long)));
-    for (int i = 0; i < 4; i++) cudaEventCreate(&e->ev[i]);
-    int rc = ensure_hash(e, 4096);
+    for (int i = 0; i < 6; i++) cudaEventCreate(&e->ev[i]);
+    int rc = ensure_hash(e, 4 * e->B * (1 + emit_per_cell()));
+    if (!rc) rc = ensure_results(e, 4 * e->B);
     if (rc) { delete e; return rc; }
-    e->outbox_counts.assign(e->P.world, 0);
     *out = e;
     return AM_OK;
 }
@@ -330,22 +369,25 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
 extern "C" int am_engine_destroy(am_engine* e) {
     if (!e) return AM_OK;
     cudaStreamSynchronize(e->stream);
-    DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->probe_vals, &e->pZ,
-                           &e->verts, &e->sx, &e->sxp};
+    if (e->gexec) cudaGraphExecDestroy(e->gexec);
+    if (e->graph) cudaGraphDestroy(e->graph);
+    DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx,
+                           &e->sxp, &e->pvals};
     for (auto* b : dbl) b->release();
-    DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->cand, &e->next, &e->ckey, &e->slot, &e->slot2, &e->outbox,
-                             &e->ss, &e->ssn, &e->sres};
+    DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->ckey, &e->slot, &e->slot2, &e->scratch, &e->outbox,
+                             &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres};
     for (auto* b : u64) b->release();
-    DBuf<int32_t>* i32[] = {&e->changed, &e->status, &e->status2, &e->raw_pool, &e->canon_pos, &e->canon_pool,
-                            &e->R, &e->X, &e->f_items, &e->f_pool, &e->cell_pool, &e->cell_nv, &e->edge_nrefs,
-                            &e->edge_refs, &e->owner, &e->sact, &e->sdone};
+    DBuf<int32_t>* i32[] = {&e->changed, &e->status, &e->status2, &e->canon_pos, &e->canon_pool, &e->X,
+                            &e->f_items, &e->f_pool, &e->batch_pool, &e->local_idx, &e->queue, &e->cell_pool,
+                            &e->cell_nv, &e->edge_nrefs, &e->edge_refs, &e->hstatus, &e->sact, &e->sdone};
     for (auto* b : i32) b->release();
     e->pool_flags.release();
     e->cell_voff.release();
     e->edge_roff.release();
     e->subdev.release();
     e->ctr.release();
-    for (int i = 0; i < 4; i++) cudaEventDestroy(e->ev[i]);
+    for (int i = 0; i < 6; i++) cudaEventDestroy(e->ev[i]);
+    if (e->own_stream) cudaStreamDestroy(e->stream);
     delete e;
     return AM_OK;
 }
@@ -353,29 +395,31 @@ extern "C" int am_engine_destroy(am_engine* e) {
 extern "C" int am_engine_key_words(const am_engine* e) { return e ? e->KW : 0; }
 
 extern "C" int am_engine_reset(am_engine* e) {
+    if (!e) return fail(AM_ERR_ARG, "null engine");
     CK(cudaMemsetAsync(e->ctr.p, 0, C_N * sizeof(unsigned long long), e->stream));
     CK(cudaMemsetAsync(e->table.p, 0xff, e->tcap * sizeof(uint64_t), e->stream));
     CK(cudaStreamSynchronize(e->stream));
     memset(e->hctr, 0, sizeof e->hctr);
-    e->n_cand = 0;
-    e->n_outbox = 0;
-    e->cells_total = 0;
-    e->capped = false;
-    e->t_compose = e->t_face = e->flops = e->face_bytes = e->n_comp_cells = e->n_face_cells = 0;
+    e->t_compose = e->t_face = e->t_probe = e->flops = e->pflops = e->face_bytes = 0;
+    e->n_comp_cells = e->n_face_cells = e->n_probes = 0;
+    e->iters = 0;
     return AM_OK;
 }
 
 // ----------------------------------------------------- compose / forward
-// run every hidden step for n items; C = 4 (cells) or 1 (points)
-static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, int32_t* changed, const double* pts, int64_t n) {
+// every hidden step for the items; C = 4 (cells) or 1 (points); n_dev null -> n_cap items
+static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsigned long long* key_off,
+                     int32_t* changed, const double* pts, const unsigned long long* n_dev, int64_t n_cap) {
     for (size_t s = 0; s < e->sdev.size(); s++) {
         LayerLaunch L;
         L.st = e->sdev[s];
         L.Z = Z;
         L.keys = keys;
+        L.key_off = key_off;
         L.changed = changed;
         L.pts = pts;
-        L.n_items = n;
+        L.n_dev = n_dev;
+        L.n_cap = n_cap;
         L.KW = e->KW;
         L.zs = e->zs;
         if (L.st.flags & AM_STEP_FIRST) launch_input_step(L, C, e->stream);
@@ -385,88 +429,54 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, int32_t* ch
     return AM_OK;
 }
 
-// compose n cell states in place: keys -> canonical keys, Z planes, faces
-static int compose(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, double* faces, int64_t n) {
-    if (n <= 0) return AM_OK;
-    if (e->timing) cudaEventRecord(e->ev[0], e->stream);
-    int rc = run_steps(e, 4, Z, keys, changed, nullptr, n);
-    if (rc) return rc;
-    launch_face_head_dev(Z, keys, faces, n, e->zs, e->KW, e->subdev.p, e->M, e->stream);
+static int compose(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, double* faces,
+                   const unsigned long long* n_dev, int64_t n_cap) {
+    RC(run_steps(e, 4, Z, keys, nullptr, changed, nullptr, n_dev, n_cap));
+    launch_face_head_dev(Z, keys, faces, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->stream);
     CK(cudaGetLastError());
-    if (e->timing) {
-        cudaEventRecord(e->ev[1], e->stream);
-        cudaEventSynchronize(e->ev[1]);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e->ev[0], e->ev[1]);
-        e->t_compose += ms;
+    return AM_OK;
+}
+
+static int forward(am_engine* e, const double* pts, double* vals, uint64_t* keys, const unsigned long long* key_off,
+                   double* Zw, const unsigned long long* n_dev, int64_t n_cap) {
+    RC(run_steps(e, 1, Zw, keys, key_off, nullptr, pts, n_dev, n_cap));
+    launch_forward_head_dev(Zw, keys, key_off, vals, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->ensemble,
+                            e->stream);
+    CK(cudaGetLastError());
+    return AM_OK;
+}
+
+// host-sized forward in chunks of the probe workspace
+static int forward_host(am_engine* e, const double* pts, int64_t n, double* vals, uint64_t* keys) {
+    for (int64_t o = 0; o < n; o += e->PB) {
+        int64_t m = std::min<int64_t>(e->PB, n - o);
+        CK(cudaMemsetAsync(keys + o * e->KW, 0, (size_t)m * e->KW * 8, e->stream));
+        RC(forward(e, pts + o * 3, vals ? vals + o : nullptr, keys + o * e->KW, nullptr, e->pZ.p, nullptr, m));
     }
-    e->flops += e->flops_per_cell * n;
-    e->n_comp_cells += n;
-    return AM_OK;
-}
-
-// forward n points: vals (may be null) + keys (zeroed here)
-static int forward(am_engine* e, const double* pts, int64_t n, double* vals, uint64_t* keys, double* Zw) {
-    if (n <= 0) return AM_OK;
-    CK(cudaMemsetAsync(keys, 0, (size_t)n * e->KW * sizeof(uint64_t), e->stream));
-    int rc = run_steps(e, 1, Zw, keys, nullptr, pts, n);
-    if (rc) return rc;
-    launch_forward_head_dev(Zw, keys, vals, n, e->zs, e->KW, e->subdev.p, e->M, e->ensemble, e->stream);
-    CK(cudaGetLastError());
-    return AM_OK;
-}
-
-static int ensure_probe_ws(am_engine* e, int64_t n) {
-    CK(e->pZ.reserve(n * e->zs, e->stream));
-    CK(e->probe_vals.reserve(n, e->stream));
     return AM_OK;
 }
 
 extern "C" int am_forward(am_engine* e, const double* d_pts, int64_t n, double* d_vals, uint64_t* d_keys) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
     if (n == 0) return AM_OK;
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 4 * e->B));
-    int rc = ensure_probe_ws(e, chunk);
-    if (rc) return rc;
-    DBuf<uint64_t> tmpk;
     uint64_t* keys = d_keys;
     if (!keys) {
-        CK(tmpk.reserve(chunk * e->KW, e->stream));
+        CK(e->hkeys.reserve(n * e->KW, e->stream));
+        keys = e->hkeys.p;
     }
-    for (int64_t o = 0; o < n; o += chunk) {
-        int64_t m = std::min(chunk, n - o);
-        uint64_t* k = d_keys ? d_keys + o * e->KW : tmpk.p;
-        rc = forward(e, d_pts + o * 3, m, d_vals ? d_vals + o : nullptr, k, e->pZ.p);
-        if (rc) return rc;
-    }
+    RC(forward_host(e, d_pts, n, d_vals, keys));
     CK(cudaStreamSynchronize(e->stream));
-    tmpk.release();
-    return AM_OK;
-}
-
-static int ensure_batch(am_engine* e, int64_t b) {
-    CK(e->Z.reserve(b * e->zs * 4, e->stream));
-    CK(e->faces.reserve(b * e->M * 4, e->stream));
-    CK(e->ckey.reserve(b * e->KW, e->stream));
-    DBuf<int32_t>* i32[] = {&e->changed, &e->status, &e->status2, &e->raw_pool, &e->canon_pos, &e->canon_pool,
-                            &e->R, &e->X, &e->f_items, &e->f_pool};
-    for (auto* x : i32) CK(x->reserve(b, e->stream));
-    CK(e->slot.reserve(b, e->stream));
-    CK(e->slot2.reserve(b, e->stream));
     return AM_OK;
 }
 
 extern "C" int am_affine_maps(am_engine* e, const uint64_t* d_keys, int64_t n, uint64_t* d_canon, double* d_planes,
                               double* d_faces) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
-    int rc = ensure_batch(e, std::min<int64_t>(n, e->B));
-    if (rc) return rc;
     for (int64_t o = 0; o < n; o += e->B) {
         int64_t m = std::min<int64_t>(e->B, n - o);
         CK(cudaMemcpyAsync(e->ckey.p, d_keys + o * e->KW, m * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
         CK(cudaMemsetAsync(e->changed.p, 0, m * sizeof(int32_t), e->stream));
-        rc = compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, m);
-        if (rc) return rc;
+        RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, m));
         if (d_canon)
             CK(cudaMemcpyAsync(d_canon + o * e->KW, e->ckey.p, m * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
         if (d_planes)
@@ -479,219 +489,231 @@ extern "C" int am_affine_maps(am_engine* e, const uint64_t* d_keys, int64_t n, u
     return AM_OK;
 }
 
-// --------------------------------------------------------------- marching
-extern "C" int am_push_candidates(am_engine* e, const uint64_t* d_keys, int64_t n) {
-    if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
-    if (n == 0) return AM_OK;
-    CK(e->cand.reserve((e->n_cand + n) * e->KW, e->stream, true, e->n_cand * e->KW));
-    CK(cudaMemcpyAsync(e->cand.p + e->n_cand * e->KW, d_keys, n * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    e->n_cand += n;
-    return AM_OK;
-}
-
-// one chunk of candidates [o, o+m): steps 1-5
-static int absorb_expand(am_engine* e, const uint64_t* cands, int64_t m, int64_t* new_cells) {
-    int rc = ensure_hash(e, 2 * m);
-    if (rc) return rc;
-    rc = ensure_batch(e, m);
-    if (rc) return rc;
-    HashSet H = hs(e);
+// ----------------------------------------------------------- iteration
+static int launch_iteration(am_engine* e) {
     cudaStream_t s = e->stream;
-    // 1. raw insert
-    launch_hash_insert(H, cands, nullptr, m, e->status.p, e->slot.p, s);
-    launch_hash_fixup(H, cands, nullptr, m, e->status.p, e->slot.p, 0u, e->raw_pool.p, s);
-    CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, sizeof(unsigned long long), s));
-    launch_compact(e->status.p, 1, m, e->R.p, e->ctr.p + C_LIST, s);
-    CK(cudaGetLastError());
-    if ((rc = sync_counters(e))) return rc;
-    int64_t nR = (int64_t)e->hctr[C_LIST];
-    if (nR == 0) { *new_cells = 0; return AM_OK; }
-    // keep the batch order deterministic (the compaction appends in warp order)
-    // 2. compose
-    launch_gather_keys(cands, e->R.p, nR, e->KW, e->ckey.p, s);
-    CK(cudaMemsetAsync(e->changed.p, 0, nR * sizeof(int32_t), s));
-    rc = compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nR);
-    if (rc) return rc;
-    // 3. canonical inserts for changed keys
-    CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, sizeof(unsigned long long), s));
-    launch_compact(e->changed.p, 1, nR, e->X.p, e->ctr.p + C_LIST, s);
-    if ((rc = sync_counters(e))) return rc;
-    int64_t nX = (int64_t)e->hctr[C_LIST];
-    CK(cudaMemsetAsync(e->canon_pos.p, 0xff, nR * sizeof(int32_t), s));
-    if (nX > 0) {
-        launch_hash_insert(H, e->ckey.p, e->X.p, nX, e->status2.p, e->slot2.p, s);
-        launch_hash_fixup(H, e->ckey.p, e->X.p, nX, e->status2.p, e->slot2.p, 0u, e->canon_pool.p, s);
-        launch_scatter_pos(e->X.p, nX, e->canon_pos.p, s);
-    }
-    int64_t max_new = e->P.max_cells - e->cells_total;
-    if (max_new < 0) max_new = 0;
-    CK(cudaMemsetAsync(e->ctr.p + C_FRONT, 0, sizeof(unsigned long long), s));
-    launch_frontier(nR, e->changed.p, e->R.p, e->raw_pool.p, e->canon_pos.p, e->status2.p, e->canon_pool.p,
-                    e->pool_flags.p, e->f_items.p, e->f_pool.p, e->ctr.p + C_FRONT, max_new, e->ctr.p + C_CAPPED, s);
-    CK(cudaGetLastError());
-    if ((rc = sync_counters(e))) return rc;
-    int64_t nF = std::min<int64_t>((int64_t)e->hctr[C_FRONT], max_new);
-    if (e->hctr[C_CAPPED]) e->capped = true;
-    *new_cells = nF;
-    if (nF == 0) return AM_OK;
-    e->cells_total += nF;
-    // 4. faces: make room for outputs
-    const int64_t VPC = 64, RPC = 256, CPC = 48;
-    int64_t nc = (int64_t)e->hctr[C_CELLS], nv = (int64_t)e->hctr[C_VERTS], nrf = (int64_t)e->hctr[C_REFS];
-    CK(e->cell_pool.reserve(nc + nF, s, true, nc));
-    CK(e->cell_nv.reserve(nc + nF, s, true, nc));
-    CK(e->cell_voff.reserve(nc + nF, s, true, nc));
-    CK(e->verts.reserve((nv + nF * VPC) * 3, s, true, nv * 3));
-    CK(e->edge_nrefs.reserve(nv + nF * VPC, s, true, nv));
-    CK(e->edge_roff.reserve(nv + nF * VPC, s, true, nv));
-    CK(e->edge_refs.reserve(nrf + nF * RPC, s, true, nrf));
-    int64_t nn = (int64_t)e->hctr[C_NEXT], npb = (int64_t)e->hctr[C_PROBE];
-    CK(e->next.reserve((nn + nF * CPC) * e->KW, s, true, nn * e->KW));
-    CK(e->probe_pts.reserve((npb + nF * VPC) * 3, s, true, npb * 3));
+    unsigned long long* c = e->ctr.p;
+    const int64_t B = e->B;
+    HashSet H = hs(e);
+    const bool tm = e->timing;
+    IterState I;
+    I.ctr = c; I.queue = e->queue.p; I.batch_pool = e->batch_pool.p; I.B = B;
+    I.cap_pool = e->pool.n / e->KW; I.tcap = (long long)e->tcap;
+    I.cap_cells = e->cell_pool.n; I.cap_verts = e->edge_nrefs.n; I.cap_refs = e->edge_refs.n;
+    I.cap_outbox = e->P.world > 1 ? e->outbox.n / e->KW : 0;
+    I.emit_per_cell = emit_per_cell(); I.verts_per_cell = kVertsPerCell; I.refs_per_cell = kRefsPerCell;
+    I.world = e->P.world;
+    launch_take(I, s);
+    launch_gather_batch(e->pool.p, e->batch_pool.p, c + C_NR, B, e->KW, e->ckey.p, e->changed.p, e->canon_pos.p, s);
+    if (tm) cudaEventRecord(e->ev[0], s);
+    RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B));
+    if (tm) cudaEventRecord(e->ev[1], s);
+    launch_route_changed(e->ckey.p, e->changed.p, c + C_NR, B, e->KW, e->P.rank, e->P.world, e->X.p, c + C_NX,
+                         e->outbox.p, c + C_NOUT, e->canon_pos.p, s);
+    launch_hash_insert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, s);
+    launch_hash_fixup(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, 0u, e->canon_pool.p, nullptr,
+                      nullptr, s);
+    launch_frontier(c + C_NR, B, e->changed.p, e->batch_pool.p, e->canon_pos.p, e->status2.p, e->canon_pool.p,
+                    e->pool_flags.p, e->f_items.p, e->f_pool.p, c, (long long)e->P.max_cells, s);
     FaceArgs a;
     a.Z = e->Z.p; a.faces = e->faces.p; a.keys = e->ckey.p; a.items = e->f_items.p; a.pool_idx = e->f_pool.p;
-    a.n = nF; a.NB = e->NB; a.M = e->M; a.KW = e->KW; a.zs = e->zs; a.ensemble = e->ensemble;
+    a.n_dev = c + C_NF; a.n_cap = B;
+    a.NB = e->NB; a.M = e->M; a.KW = e->KW; a.zs = e->zs; a.ensemble = e->ensemble;
     for (int k = 0; k < 3; k++) { a.lo[k] = e->P.bbox_lo[k]; a.hi[k] = e->P.bbox_hi[k]; }
     a.tol_cell = e->P.tol_cell; a.tol_weld = e->P.tol_weld; a.tol_onplane = e->P.tol_onplane;
     a.probe_delta = e->P.probe_delta;
-    a.cell_pool = e->cell_pool.p; a.cell_nv = e->cell_nv.p; a.cell_voff = e->cell_voff.p;
-    a.n_cells = e->ctr.p + C_CELLS;
+    a.cell_pool = e->cell_pool.p; a.cell_nv = e->cell_nv.p; a.cell_voff = e->cell_voff.p; a.n_cells = c + C_CELLS;
     a.verts = e->verts.p; a.edge_nrefs = e->edge_nrefs.p; a.edge_roff = e->edge_roff.p; a.edge_refs = e->edge_refs.p;
-    a.n_verts = e->ctr.p + C_VERTS; a.n_refs = e->ctr.p + C_REFS;
+    a.n_verts = c + C_VERTS; a.n_refs = c + C_REFS;
     a.cap_cells = e->cell_pool.n; a.cap_verts = e->edge_nrefs.n; a.cap_refs = e->edge_refs.n;
-    a.cand = e->next.p; a.n_cand = e->ctr.p + C_NEXT; a.cap_cand = e->next.n / e->KW;
-    a.probe_pts = e->probe_pts.p; a.n_probe = e->ctr.p + C_PROBE; a.cap_probe = e->probe_pts.n / 3;
-    a.overflow = e->ctr.p + C_OVF0;
-    if (e->timing) cudaEventRecord(e->ev[2], s);
+    a.cand = e->scratch.p; a.n_cand = c + C_NEMIT; a.cap_cand = B * kEmitFlipsPerCell;
+    a.probe_pts = e->probe_pts.p; a.n_probe = c + C_NPROBE; a.cap_probe = e->PB;
+    a.overflow = c + C_OVF0;
+    if (tm) cudaEventRecord(e->ev[2], s);
     launch_face(a, s);
-    CK(cudaGetLastError());
-    if (e->timing) {
-        cudaEventRecord(e->ev[3], s);
-        cudaEventSynchronize(e->ev[3]);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e->ev[2], e->ev[3]);
-        e->t_face += ms;
+    if (tm) cudaEventRecord(e->ev[3], s);
+    launch_zero_probe_keys(e->scratch.p, c, e->KW, e->PB, s);
+    RC(forward(e, e->probe_pts.p, nullptr, e->scratch.p, c + C_NEMIT, e->pZ.p, c + C_NPROBE, e->PB));
+    if (tm) cudaEventRecord(e->ev[4], s);
+    launch_emit_finalize(c, s);
+    if (e->P.world > 1) {
+        launch_route_emitted(e->scratch.p, c + C_NEMIT, e->E, e->KW, e->P.rank, e->P.world, e->local_idx.p,
+                             c + C_NLOCAL, e->outbox.p, c + C_NOUT, s);
+        launch_hash_insert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, s);
+        launch_hash_fixup(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, 0u, nullptr,
+                          e->queue.p, c + C_QTAIL, s);
+    } else {
+        launch_hash_insert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, s);
+        launch_hash_fixup(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, 0u, nullptr,
+                          e->queue.p, c + C_QTAIL, s);
     }
-    e->n_face_cells += nF;
-    e->face_bytes += (double)nF * (2.0 * (e->NB * 32.0) + e->M * 32.0);
+    CK(cudaGetLastError());
     return AM_OK;
 }
 
-// probes of the wave -> candidate keys appended to next
-static int flush_probes(am_engine* e) {
-    int rc = sync_counters(e);
-    if (rc) return rc;
-    int64_t np = (int64_t)e->hctr[C_PROBE];
-    if (np == 0) return AM_OK;
-    int64_t nn = (int64_t)e->hctr[C_NEXT];
-    CK(e->next.reserve((nn + np) * e->KW, e->stream, true, nn * e->KW));
-    const int64_t chunk = std::max<int64_t>(1, 4 * e->B);
-    if ((rc = ensure_probe_ws(e, std::min(chunk, np)))) return rc;
-    for (int64_t o = 0; o < np; o += chunk) {
-        int64_t m = std::min(chunk, np - o);
-        rc = forward(e, e->probe_pts.p + o * 3, m, nullptr, e->next.p + (nn + o) * e->KW, e->pZ.p);
-        if (rc) return rc;
+static int capture(am_engine* e) {
+    if (e->gexec) { cudaGraphExecDestroy(e->gexec); e->gexec = nullptr; }
+    if (e->graph) { cudaGraphDestroy(e->graph); e->graph = nullptr; }
+    unsigned long long before = g_launch_count;
+    CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = launch_iteration(e);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+    if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+    CK(ce);
+    e->graph = g;
+    e->graph_kernels = g_launch_count - before;
+    g_launch_count = before;   // captured, not launched
+    CK(cudaGraphInstantiate(&e->gexec, e->graph, 0));
+    e->graph_valid = true;
+    return AM_OK;
+}
+
+// make room for `iters` more iterations of worst-case output
+static int ensure_iter_room(am_engine* e, int iters) {
+    RC(ensure_hash(e, (int64_t)iters * e->B * (1 + emit_per_cell())));
+    RC(ensure_results(e, (int64_t)iters * e->B));
+    return AM_OK;
+}
+
+static int timed_iteration(am_engine* e) {
+    RC(launch_iteration(e));
+    CK(cudaEventSynchronize(e->ev[4]));
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, e->ev[0], e->ev[1]);
+    cudaEventElapsedTime(&b, e->ev[2], e->ev[3]);
+    cudaEventElapsedTime(&c, e->ev[3], e->ev[4]);
+    RC(sync_counters(e));
+    e->t_compose += a;
+    e->t_face += b;
+    e->t_probe += c;
+    double nR = (double)e->hctr[C_NR], nF = (double)e->hctr[C_NF], nP = (double)e->hctr[C_NPROBE];
+    e->flops += e->flops_per_cell * nR;
+    e->pflops += e->flops_per_point * nP;
+    e->n_comp_cells += nR;
+    e->n_face_cells += nF;
+    e->n_probes += nP;
+    e->face_bytes += nF * (e->NB * 32.0 + e->M * 32.0 + e->KW * 8.0);
+    return AM_OK;
+}
+
+// run up to `max_iters` iterations (graph replays), stopping when the queue drains
+static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
+    int64_t n = 0;
+    while (n < max_iters) {
+        RC(sync_counters(e));
+        if (e->hctr[C_OVF1]) return fail(AM_ERR_OVERFLOW, "output capacity overflow (%llu events)", e->hctr[C_OVF1]);
+        if (e->hctr[C_QHEAD] >= e->hctr[C_QTAIL]) break;
+        int k = (int)std::min<int64_t>(e->graph_batch, max_iters - n);
+        RC(ensure_iter_room(e, k + 1));
+        if (e->timing) {
+            for (int i = 0; i < k; i++) RC(timed_iteration(e));
+        } else {
+            if (!e->graph_valid) RC(capture(e));
+            for (int i = 0; i < k; i++) CK(cudaGraphLaunch(e->gexec, e->stream));
+            g_launch_count += (unsigned long long)k * e->graph_kernels;
+        }
+        n += k;
+        RC(sync_counters(e));
+        if (e->hctr[C_STALL]) e->graph_valid = false;  // guard fired: the next round grows buffers
     }
-    return set_counter(e, C_NEXT, nn + np) || set_counter(e, C_PROBE, 0);
+    RC(sync_counters(e));
+    e->iters = (int64_t)e->hctr[C_ITER];
+    if (done) *done = n;
+    return AM_OK;
+}
+
+// --------------------------------------------------------------- marching
+// insert host-sized keys and queue the new ones
+static int push_keys(am_engine* e, const uint64_t* d_keys, int64_t n) {
+    if (n <= 0) return AM_OK;
+    RC(ensure_hash(e, n));
+    CK(e->hstatus.reserve(n, e->stream));
+    CK(e->hslot.reserve(n, e->stream));
+    HashSet H = hs(e);
+    if (e->P.world > 1) {   // keep only the states this rank owns
+        CK(e->local_idx.reserve(n, e->stream));
+        CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, 8, e->stream));
+        launch_filter_owned(d_keys, n, e->KW, e->P.rank, e->P.world, e->local_idx.p, e->ctr.p + C_LIST, e->stream);
+        launch_hash_insert(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, e->stream);
+        launch_hash_fixup(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, 0u, nullptr,
+                          e->queue.p, e->ctr.p + C_QTAIL, e->stream);
+    } else {
+        launch_hash_insert(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, e->stream);
+        launch_hash_fixup(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, 0u, nullptr, e->queue.p,
+                          e->ctr.p + C_QTAIL, e->stream);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(e->stream));
+    return AM_OK;
+}
+
+extern "C" int am_push_candidates(am_engine* e, const uint64_t* d_keys, int64_t n) {
+    if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
+    return push_keys(e, d_keys, n);
 }
 
 extern "C" int am_wave(am_engine* e, int64_t* h_new_cells) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
-    int64_t total_new = 0;
-    int rc;
-    if ((rc = set_counter(e, C_NEXT, 0))) return rc;
-    if ((rc = set_counter(e, C_PROBE, 0))) return rc;
-    for (int64_t o = 0; o < e->n_cand; o += e->B) {
-        int64_t m = std::min<int64_t>(e->B, e->n_cand - o);
-        int64_t nw = 0;
-        rc = absorb_expand(e, e->cand.p + o * e->KW, m, &nw);
-        if (rc) return rc;
-        total_new += nw;
-        // bound the probe backlog per batch
-        if ((rc = flush_probes(e))) return rc;
-    }
-    if ((rc = sync_counters(e))) return rc;
-    if (e->hctr[C_OVF0] || e->hctr[C_OVF1]) {
-        // capacity overflow drops work: report loudly instead of returning a silently partial mesh
-        if (e->hctr[C_OVF1])
-            return fail(AM_ERR_OVERFLOW, "output capacity overflow (%llu events)", e->hctr[C_OVF1]);
-    }
-    int64_t nn = (int64_t)e->hctr[C_NEXT];
-    std::swap(e->cand, e->next);
-    e->n_cand = nn;
-    if ((rc = set_counter(e, C_NEXT, 0))) return rc;
-    // sharded marching: hold back candidates owned by other ranks
-    if (e->P.world > 1 && nn > 0) {
-        CK(e->owner.reserve(nn, e->stream));
-        launch_owner(e->cand.p, nn, e->KW, e->P.world, e->owner.p, e->stream);
-        std::vector<int32_t> own(nn);
-        CK(cudaMemcpyAsync(own.data(), e->owner.p, nn * 4, cudaMemcpyDeviceToHost, e->stream));
-        CK(cudaStreamSynchronize(e->stream));
-        std::vector<int64_t> order(nn);
-        std::iota(order.begin(), order.end(), 0);
-        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return own[a] < own[b]; });
-        std::vector<int64_t> cnt(e->P.world, 0);
-        for (int64_t i = 0; i < nn; i++) cnt[own[i]]++;
-        // keep own, move the rest to the outbox grouped by owner
-        std::vector<int32_t> idx(order.begin(), order.end());
-        DBuf<int32_t> didx;
-        CK(didx.reserve(nn, e->stream));
-        CK(cudaMemcpyAsync(didx.p, idx.data(), nn * 4, cudaMemcpyHostToDevice, e->stream));
-        DBuf<uint64_t> sorted;
-        CK(sorted.reserve(nn * e->KW, e->stream));
-        launch_gather_keys(e->cand.p, didx.p, nn, e->KW, sorted.p, e->stream);
-        int rank = e->P.rank;
-        int64_t before = 0;
-        for (int r = 0; r < rank; r++) before += cnt[r];
-        int64_t n_mine = cnt[rank];
-        int64_t n_out = nn - n_mine;
-        CK(e->outbox.reserve(std::max<int64_t>(n_out, 1) * e->KW, e->stream));
-        // outbox = sorted without the own block (still grouped by owner, own count 0)
-        if (before > 0)
-            CK(cudaMemcpyAsync(e->outbox.p, sorted.p, before * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
-        if (nn - before - n_mine > 0)
-            CK(cudaMemcpyAsync(e->outbox.p + before * e->KW, sorted.p + (before + n_mine) * e->KW,
-                               (nn - before - n_mine) * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
-        if (n_mine > 0)
-            CK(cudaMemcpyAsync(e->cand.p, sorted.p + before * e->KW, n_mine * e->KW * 8, cudaMemcpyDeviceToDevice,
-                               e->stream));
-        CK(cudaStreamSynchronize(e->stream));
-        didx.release();
-        sorted.release();
-        e->n_cand = n_mine;
-        e->n_outbox = n_out;
-        for (int r = 0; r < e->P.world; r++) e->outbox_counts[r] = r == rank ? 0 : cnt[r];
-    }
-    *h_new_cells = total_new;
+    RC(sync_counters(e));
+    unsigned long long before = e->hctr[C_TOTAL];
+    int64_t done = 0;
+    int saved = e->graph_batch;
+    e->graph_batch = 1;
+    int rc = run_iterations(e, 1, &done);
+    e->graph_batch = saved;
+    RC(rc);
+    if (h_new_cells) *h_new_cells = (int64_t)(e->hctr[C_TOTAL] - before);
     return AM_OK;
 }
 
 extern "C" int am_run(am_engine* e, int64_t* h_waves) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
-    int64_t waves = 0;
-    while (e->n_cand > 0) {
-        int64_t nw = 0;
-        int rc = am_wave(e, &nw);
-        if (rc) return rc;
-        waves++;
+    RC(run_iterations(e, INT64_MAX, nullptr));
+    if (h_waves) *h_waves = e->iters;
+    return AM_OK;
+}
+
+extern "C" int am_queue_size(am_engine* e, int64_t* h_n) {
+    if (!e) return fail(AM_ERR_ARG, "null engine");
+    RC(sync_counters(e));
+    *h_n = (int64_t)(e->hctr[C_QTAIL] - e->hctr[C_QHEAD]);
+    return AM_OK;
+}
+
+extern "C" int am_outbox_counts(am_engine* e, int64_t* h_total) {
+    if (!e) return fail(AM_ERR_ARG, "null engine");
+    RC(sync_counters(e));
+    *h_total = (int64_t)e->hctr[C_NOUT];
+    return AM_OK;
+}
+
+// move the outbox to d_out grouped by owner rank (h_counts[world] keys per owner) and clear it
+extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out, int64_t* h_counts) {
+    if (!e) return fail(AM_ERR_ARG, "null engine");
+    RC(sync_counters(e));
+    const int world = e->P.world, KW = e->KW;
+    int64_t n = (int64_t)e->hctr[C_NOUT];
+    for (int r = 0; r < world; r++) h_counts[r] = 0;
+    if (n > 0) {
+        DBuf<int32_t> own, idx;
+        CK(own.reserve(n, e->stream));
+        CK(idx.reserve(n, e->stream));
+        launch_owner(e->outbox.p, n, KW, world, own.p, e->stream);
+        std::vector<int32_t> ho(n);
+        CK(cudaMemcpyAsync(ho.data(), own.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        std::vector<int32_t> order(n);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return ho[a] < ho[b]; });
+        for (int64_t i = 0; i < n; i++) h_counts[ho[i]]++;
+        CK(cudaMemcpyAsync(idx.p, order.data(), n * 4, cudaMemcpyHostToDevice, e->stream));
+        launch_gather_keys(e->outbox.p, idx.p, n, KW, d_out, e->stream);
+        CK(cudaStreamSynchronize(e->stream));
+        own.release();
+        idx.release();
     }
-    if (h_waves) *h_waves = waves;
-    return AM_OK;
-}
-
-extern "C" int am_outbox_counts(am_engine* e, int64_t* h_counts) {
-    if (!e) return fail(AM_ERR_ARG, "null engine");
-    for (int r = 0; r < e->P.world; r++) h_counts[r] = e->n_outbox ? e->outbox_counts[r] : 0;
-    return AM_OK;
-}
-
-extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out) {
-    if (!e) return fail(AM_ERR_ARG, "null engine");
-    if (e->n_outbox > 0)
-        CK(cudaMemcpyAsync(d_out, e->outbox.p, e->n_outbox * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    e->n_outbox = 0;
+    RC(set_counter(e, C_NOUT, 0));
     return AM_OK;
 }
 
@@ -700,8 +722,9 @@ extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out) {
 extern "C" int am_seed(am_engine* e, const double* d_pts, int64_t n) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
     if (n == 0) return AM_OK;
+    if (n > e->B) return fail(AM_ERR_ARG, "too many seeds for one batch (%lld > %lld)", (long long)n, (long long)e->B);
     cudaStream_t s = e->stream;
-    int KW = e->KW, rc;
+    int KW = e->KW;
     CK(e->sx.reserve(n * 3, s));
     CK(e->sxp.reserve(n * 3, s));
     CK(e->ss.reserve(n * KW, s));
@@ -709,70 +732,83 @@ extern "C" int am_seed(am_engine* e, const double* d_pts, int64_t n) {
     CK(e->sres.reserve(n * KW, s));
     CK(e->sact.reserve(n, s));
     CK(e->sdone.reserve(n, s));
-    if ((rc = ensure_batch(e, std::min<int64_t>(n, e->B)))) return rc;
-    if (n > e->B) return fail(AM_ERR_ARG, "too many seeds for one batch (%lld > %lld)", (long long)n, (long long)e->B);
-    if ((rc = ensure_probe_ws(e, n))) return rc;
     CK(cudaMemcpyAsync(e->sx.p, d_pts, n * 24, cudaMemcpyDeviceToDevice, s));
-    if ((rc = forward(e, e->sx.p, n, nullptr, e->ss.p, e->pZ.p))) return rc;
+    RC(forward_host(e, e->sx.p, n, nullptr, e->ss.p));
     std::vector<int32_t> ones(n, 1);
     CK(cudaMemcpyAsync(e->sact.p, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
     for (int it = 0; it < 3; it++) {
         CK(cudaMemcpyAsync(e->ckey.p, e->ss.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemsetAsync(e->changed.p, 0, n * 4, s));
-        if ((rc = compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, n))) return rc;
+        RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n));
         launch_seed_project(e->sx.p, e->faces.p, e->ckey.p, KW, e->M, e->ensemble, n, e->sact.p, e->sxp.p,
                             e->sdone.p, s);
-        // projected-away seeds whose face normal vanished are final: result = canonical
         launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, e->sdone.p, s);
-        if ((rc = forward(e, e->sxp.p, n, nullptr, e->ssn.p, e->pZ.p))) return rc;
+        RC(forward_host(e, e->sxp.p, n, nullptr, e->ssn.p));
         launch_seed_check(e->ssn.p, e->ckey.p, KW, n, e->sact.p, e->sx.p, e->sxp.p, e->ss.p, e->sres.p, nullptr, s);
         CK(cudaGetLastError());
     }
     CK(cudaMemcpyAsync(e->ckey.p, e->ss.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemsetAsync(e->changed.p, 0, n * 4, s));
-    if ((rc = compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, n))) return rc;
-    // still-active seeds take canonical(s)
+    RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n));
     launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, nullptr, s);
     CK(cudaGetLastError());
-    return am_push_candidates(e, e->sres.p, n);
+    return push_keys(e, e->sres.p, n);
+}
+
+// batched bisection between sign-opposite samples (reference seeding.py:84-112)
+extern "C" int am_dichotomy(am_engine* e, const double* d_xpos, const double* d_xneg, int64_t n, double eps,
+                            double seed_tol, int max_iters, double* d_out) {
+    if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
+    if (n == 0) return AM_OK;
+    if (n > e->PB) return fail(AM_ERR_ARG, "too many dichotomy pairs (%lld)", (long long)n);
+    cudaStream_t s = e->stream;
+    DBuf<double> xp, xn, fp, fn, mid, vals;
+    DBuf<int32_t> act;
+    CK(xp.reserve(n * 3, s)); CK(xn.reserve(n * 3, s)); CK(mid.reserve(n * 3, s));
+    CK(fp.reserve(n, s)); CK(fn.reserve(n, s)); CK(vals.reserve(n, s)); CK(act.reserve(n, s));
+    CK(e->hkeys.reserve(n * e->KW, s));
+    CK(cudaMemcpyAsync(xp.p, d_xpos, n * 24, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(xn.p, d_xneg, n * 24, cudaMemcpyDeviceToDevice, s));
+    RC(forward_host(e, xp.p, n, fp.p, e->hkeys.p));
+    RC(forward_host(e, xn.p, n, fn.p, e->hkeys.p));
+    std::vector<int32_t> ones(n, 1);
+    CK(cudaMemcpyAsync(act.p, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
+    launch_midpoint(xp.p, xn.p, mid.p, n, s);
+    for (int it = 1; it <= max_iters; it++) {
+        RC(forward_host(e, mid.p, n, vals.p, e->hkeys.p));
+        launch_dichotomy_step(vals.p, xp.p, xn.p, fp.p, fn.p, mid.p, act.p, d_out, n, eps, seed_tol, it == max_iters, s);
+        CK(cudaGetLastError());
+        if ((it & 7) == 0 || it == max_iters) {
+            CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, 8, s));
+            launch_count_active(act.p, n, e->ctr.p + C_LIST, s);
+            RC(sync_counters(e));
+            if (e->hctr[C_LIST] == 0) break;
+        }
+    }
+    CK(cudaStreamSynchronize(s));
+    xp.release(); xn.release(); fp.release(); fn.release(); mid.release(); vals.release(); act.release();
+    return AM_OK;
 }
 
 // ------------------------------------------------------------------ results
 extern "C" int am_result_counts(am_engine* e, int64_t* h) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
-    int rc = sync_counters(e);
-    if (rc) return rc;
-    int64_t nc = (int64_t)e->hctr[C_CELLS];
+    RC(sync_counters(e));
+    int64_t nc = (int64_t)e->hctr[C_CELLS], nvt = (int64_t)e->hctr[C_VERTS];
     std::vector<int32_t> nv(nc);
-    if (nc) {
-        CK(cudaMemcpy(nv.data(), e->cell_nv.p, nc * 4, cudaMemcpyDeviceToHost));
-    }
+    if (nc) CK(cudaMemcpy(nv.data(), e->cell_nv.p, nc * 4, cudaMemcpyDeviceToHost));
     int64_t faces = 0, empty = 0, verts = 0, ovf = 0;
     for (int64_t i = 0; i < nc; i++) {
         if (nv[i] > 0) { faces++; verts += nv[i]; }
         else if (nv[i] == 0) empty++;
         else ovf++;
     }
-    // open edges need the refs; computed in am_result_copy -- report here via a scan
-    int64_t nref = (int64_t)e->hctr[C_REFS];
-    int64_t open = 0;
-    if (verts) {
-        int64_t nvt = (int64_t)e->hctr[C_VERTS];
-        std::vector<int32_t> enr(nvt);
-        std::vector<int64_t> roff(nvt);
-        std::vector<int32_t> refs(nref);
-        CK(cudaMemcpy(enr.data(), e->edge_nrefs.p, nvt * 4, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(roff.data(), e->edge_roff.p, nvt * 8, cudaMemcpyDeviceToHost));
-        if (nref) CK(cudaMemcpy(refs.data(), e->edge_refs.p, nref * 4, cudaMemcpyDeviceToHost));
-        const int box0 = e->NB + e->M;
-        for (int64_t v = 0; v < nvt; v++) {
-            bool hit = false;
-            for (int q = 0; q < enr[v]; q++) hit |= refs[roff[v] + q] >= box0;
-            open += hit;
-        }
-    }
-    h[0] = nc; h[1] = faces; h[2] = empty; h[3] = verts; h[4] = nref; h[5] = open;
-    h[6] = e->capped ? 1 : 0;
+    CK(cudaMemsetAsync(e->ctr.p + C_OPEN, 0, 8, e->stream));
+    launch_open_edges(e->edge_nrefs.p, e->edge_roff.p, e->edge_refs.p, nvt, e->NB + e->M, e->ctr.p + C_OPEN, e->stream);
+    RC(sync_counters(e));
+    h[0] = nc; h[1] = faces; h[2] = empty; h[3] = verts; h[4] = (int64_t)e->hctr[C_REFS];
+    h[5] = (int64_t)e->hctr[C_OPEN];
+    h[6] = e->hctr[C_CAPPED] ? 1 : 0;
     h[7] = ovf + (int64_t)e->hctr[C_OVF0];
     return AM_OK;
 }
@@ -780,8 +816,7 @@ extern "C" int am_result_counts(am_engine* e, int64_t* h) {
 extern "C" int am_result_copy(am_engine* e, uint64_t* h_keys, int32_t* h_nverts, double* h_verts,
                               int32_t* h_edge_nrefs, int32_t* h_edge_refs) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
-    int rc = sync_counters(e);
-    if (rc) return rc;
+    RC(sync_counters(e));
     const int KW = e->KW;
     int64_t nc = (int64_t)e->hctr[C_CELLS], nvt = (int64_t)e->hctr[C_VERTS], nref = (int64_t)e->hctr[C_REFS];
     if (nc == 0) return AM_OK;
@@ -790,15 +825,10 @@ extern "C" int am_result_copy(am_engine* e, uint64_t* h_keys, int32_t* h_nverts,
     CK(cudaMemcpy(cp.data(), e->cell_pool.p, nc * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(nv.data(), e->cell_nv.p, nc * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(voff.data(), e->cell_voff.p, nc * 8, cudaMemcpyDeviceToHost));
-    // gather the cells' keys on device, then copy
-    DBuf<uint64_t> ck;
-    DBuf<int32_t> dcp;
-    CK(ck.reserve(nc * KW, e->stream));
-    CK(dcp.reserve(nc, e->stream));
-    CK(cudaMemcpy(dcp.p, cp.data(), nc * 4, cudaMemcpyHostToDevice));
-    launch_gather_keys(e->pool.p, dcp.p, nc, KW, ck.p, e->stream);
+    CK(e->hkeys.reserve(nc * KW, e->stream));
+    launch_gather_keys(e->pool.p, e->cell_pool.p, nc, KW, e->hkeys.p, e->stream);
     std::vector<uint64_t> keys((size_t)nc * KW);
-    CK(cudaMemcpyAsync(keys.data(), ck.p, nc * KW * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(keys.data(), e->hkeys.p, nc * KW * 8, cudaMemcpyDeviceToHost, e->stream));
     std::vector<double> verts((size_t)nvt * 3);
     std::vector<int32_t> enr(nvt), refs(nref);
     std::vector<int64_t> roff(nvt);
@@ -809,8 +839,6 @@ extern "C" int am_result_copy(am_engine* e, uint64_t* h_keys, int32_t* h_nverts,
     }
     if (nref) CK(cudaMemcpyAsync(refs.data(), e->edge_refs.p, nref * 4, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
-    ck.release();
-    dcp.release();
     std::vector<int64_t> order(nc);
     std::iota(order.begin(), order.end(), 0);
     std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
@@ -845,51 +873,13 @@ extern "C" int am_set_timing(am_engine* e, int enabled) {
     return AM_OK;
 }
 
-// out: [compose_ms, face_ms, compose_flops, face_bytes, composed_items, face_cells, batch, flops_per_cell,
-//       kernel launches (process-wide), waves]
+// out: [compose_ms, face_ms, compose_flops, face_bytes, composed, faced, batch, flops_per_cell,
+//       kernel launches (process-wide), iterations, probe_ms, probe_flops, probes, flops_per_point]
 extern "C" int am_stats(am_engine* e, double* h) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
     h[0] = e->t_compose; h[1] = e->t_face; h[2] = e->flops; h[3] = e->face_bytes;
     h[4] = e->n_comp_cells; h[5] = e->n_face_cells; h[6] = (double)e->B; h[7] = e->flops_per_cell;
-    h[8] = (double)g_launch_count; h[9] = 0;
-    return AM_OK;
-}
-
-// batched bisection between sign-opposite samples (reference seeding.py:84-112)
-extern "C" int am_dichotomy(am_engine* e, const double* d_xpos, const double* d_xneg, int64_t n, double eps,
-                            double seed_tol, int max_iters, double* d_out) {
-    if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
-    if (n == 0) return AM_OK;
-    cudaStream_t s = e->stream;
-    int rc;
-    DBuf<double> xp, xn, fp, fn, mid, vals;
-    DBuf<int32_t> act;
-    CK(xp.reserve(n * 3, s)); CK(xn.reserve(n * 3, s)); CK(mid.reserve(n * 3, s));
-    CK(fp.reserve(n, s)); CK(fn.reserve(n, s)); CK(vals.reserve(n, s)); CK(act.reserve(n, s));
-    DBuf<uint64_t> keys;
-    CK(keys.reserve(n * e->KW, s));
-    if ((rc = ensure_probe_ws(e, n))) return rc;
-    CK(cudaMemcpyAsync(xp.p, d_xpos, n * 24, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(xn.p, d_xneg, n * 24, cudaMemcpyDeviceToDevice, s));
-    if ((rc = forward(e, xp.p, n, fp.p, keys.p, e->pZ.p))) return rc;
-    if ((rc = forward(e, xn.p, n, fn.p, keys.p, e->pZ.p))) return rc;
-    std::vector<int32_t> ones(n, 1);
-    CK(cudaMemcpyAsync(act.p, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
-    launch_midpoint(xp.p, xn.p, mid.p, n, s);
-    for (int it = 1; it <= max_iters; it++) {
-        if ((rc = forward(e, mid.p, n, vals.p, keys.p, e->pZ.p))) return rc;
-        launch_dichotomy_step(vals.p, xp.p, xn.p, fp.p, fn.p, mid.p, act.p, d_out, n, eps, seed_tol,
-                              it == max_iters, s);
-        CK(cudaGetLastError());
-        if ((it & 7) == 0 || it == max_iters) {
-            CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, 8, s));
-            launch_count_active(act.p, n, e->ctr.p + C_LIST, s);
-            if ((rc = sync_counters(e))) return rc;
-            if (e->hctr[C_LIST] == 0) break;
-        }
-    }
-    CK(cudaStreamSynchronize(s));
-    xp.release(); xn.release(); fp.release(); fn.release(); mid.release(); vals.release(); act.release();
-    keys.release();
+    h[8] = (double)g_launch_count; h[9] = (double)e->iters; h[10] = e->t_probe; h[11] = e->pflops;
+    h[12] = e->n_probes; h[13] = e->flops_per_point; h[14] = 0; h[15] = 0;
     return AM_OK;
 }

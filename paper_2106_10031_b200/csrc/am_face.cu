@@ -139,13 +139,9 @@ __device__ __forceinline__ bool lex_less(const double* a, const double* b) {
     return a[2] < b[2];
 }
 
-__global__ void __launch_bounds__(FW * 32) k_face(FaceArgs A) {
-    extern __shared__ uint8_t smem_raw[];
-    FaceWarp* W = reinterpret_cast<FaceWarp*>(smem_raw) + (threadIdx.x >> 5);
+__device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
-    const int64_t fi = (int64_t)blockIdx.x * FW + (threadIdx.x >> 5);
-    if (fi >= A.n) return;
     const int item = A.items[fi];
 
     Ctx c;
@@ -580,15 +576,34 @@ __global__ void __launch_bounds__(FW * 32) k_face(FaceArgs A) {
     }
 }
 
+// persistent: each warp walks the device-resident frontier
+__global__ void __launch_bounds__(FW * 32) k_face(FaceArgs A) {
+    extern __shared__ uint8_t smem_raw[];
+    FaceWarp* W = reinterpret_cast<FaceWarp*>(smem_raw) + (threadIdx.x >> 5);
+    const int64_t n = dev_count(A.n_dev, A.n_cap);
+    const int64_t nw = (int64_t)gridDim.x * FW;
+    for (int64_t fi = (int64_t)blockIdx.x * FW + (threadIdx.x >> 5); fi < n; fi += nw) {
+        face_cell(A, W, fi);
+        __syncwarp();
+    }
+}
+
 void launch_face(const FaceArgs& a, cudaStream_t s) {
-    if (a.n <= 0) return;
+    if (a.n_cap <= 0) return;
     size_t smem = sizeof(FaceWarp) * FW;
     static bool init = false;
+    static int grid = 0;
     if (!init) {
         cudaFuncSetAttribute(k_face, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0, dev = 0, sms = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_face, FW * 32, smem);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = sms * (per_sm > 0 ? per_sm : 1);
         init = true;
     }
-    { k_face<<<(unsigned)((a.n + FW - 1) / FW), FW * 32, smem, s>>>(a); ++g_launch_count; }
+    int64_t need = (a.n_cap + FW - 1) / FW;
+    { k_face<<<(unsigned)(need < grid ? need : grid), FW * 32, smem, s>>>(a); ++g_launch_count; }
 }
 
 }  // namespace am

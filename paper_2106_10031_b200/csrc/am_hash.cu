@@ -1,13 +1,15 @@
-// am_hash.cu -- on-device open-addressing set of activation states.
+// am_hash.cu -- on-device open-addressing set of activation states + the work queue.
 //
-// Replaces the reference's shared Python set `seen` (reference marching.py:221,
-// 235-245).  Slots are 64-bit words  fp(31) | cand(1) | ref(32):
+// Replaces the reference's shared Python set `seen` and deque (reference
+// marching.py:221-245).  Slots are 64-bit words  fp(31) | cand(1) | ref(32):
 //   cand = 1 : ref indexes the key buffer of the insert launch in flight
 //   cand = 0 : ref indexes the key pool
 // Insertion is lock-free: a thread claims an empty slot with one CAS carrying a
 // reference to its own (already written) key, so concurrent duplicates resolve
-// by key comparison without any second round; a fix-up launch then moves the
-// winners' keys into the pool and rewrites their slots to pool references.
+// by key comparison without a second round; a fix-up launch then moves the
+// winners' keys into the pool, rewrites their slots to pool references and
+// appends them to the work queue.  Every launch reads its item count from device
+// memory, so a whole BFS iteration is one capturable CUDA graph.
 #include "am_internal.h"
 
 namespace am {
@@ -20,198 +22,317 @@ __device__ __forceinline__ bool keys_equal(const uint64_t* a, const uint64_t* b,
     return true;
 }
 
-__global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx, int64_t n, int32_t* status,
-                              uint64_t* slot_out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t ci = idx ? idx[i] : i;
-    const uint64_t* key = src + ci * H.KW;
-    uint64_t h = key_hash(key, H.KW);
-    uint64_t fp = h >> 33;
-    uint64_t pos = h & H.mask;
-    const uint64_t mine = (fp << 33) | (1ull << 32) | (uint64_t)(uint32_t)i;
-    for (uint64_t probe = 0; probe <= H.mask; probe++) {
-        uint64_t v = ld_volatile(H.table + pos);
-        if (v == kEmpty) {
-            unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(H.table + pos),
-                                               (unsigned long long)kEmpty, (unsigned long long)mine);
-            if (old == kEmpty) {
-                status[i] = 1;
-                slot_out[i] = pos;
-                return;
+#define GRID_STRIDE(i, n) for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                              int64_t n_cap, int32_t* status, uint64_t* slot_out) {
+    const int64_t n = dev_count(n_dev, n_cap);
+    GRID_STRIDE(i, n) {
+        const int64_t ci = idx ? idx[i] : i;
+        const uint64_t* key = src + ci * H.KW;
+        uint64_t h = key_hash(key, H.KW);
+        uint64_t fp = h >> 33;
+        uint64_t pos = h & H.mask;
+        const uint64_t mine = (fp << 33) | (1ull << 32) | (uint64_t)(uint32_t)i;
+        int32_t st = -1;  // table full (host keeps load factor <= 1/2, so unreachable)
+        for (uint64_t probe = 0; probe <= H.mask; probe++) {
+            uint64_t v = ld_volatile(H.table + pos);
+            if (v == kEmpty) {
+                unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(H.table + pos),
+                                                   (unsigned long long)kEmpty, (unsigned long long)mine);
+                if (old == kEmpty) {
+                    st = 1;
+                    slot_out[i] = pos;
+                    break;
+                }
+                v = old;
             }
-            v = old;
-        }
-        if ((v >> 33) == fp) {
-            uint32_t ref = (uint32_t)v;
-            const uint64_t* other = ((v >> 32) & 1ull) ? src + (int64_t)(idx ? idx[ref] : (int64_t)ref) * H.KW
-                                                       : H.pool + (int64_t)ref * H.KW;
-            if (keys_equal(key, other, H.KW)) {
-                status[i] = 0;
-                return;
+            if ((v >> 33) == fp) {
+                uint32_t ref = (uint32_t)v;
+                const uint64_t* other = ((v >> 32) & 1ull) ? src + (int64_t)(idx ? idx[ref] : (int64_t)ref) * H.KW
+                                                           : H.pool + (int64_t)ref * H.KW;
+                if (keys_equal(key, other, H.KW)) {
+                    st = 0;
+                    break;
+                }
             }
+            pos = (pos + 1) & H.mask;
         }
-        pos = (pos + 1) & H.mask;
+        status[i] = st;
     }
-    status[i] = -1;  // table full (host keeps load factor <= 1/2, so unreachable)
 }
 
-__global__ void k_hash_fixup(HashSet H, const uint64_t* src, const int32_t* idx, int64_t n, const int32_t* status,
-                             const uint64_t* slot, uint32_t flag, int32_t* pool_idx) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (status[i] != 1) {
-        if (pool_idx) pool_idx[i] = -1;
-        return;
-    }
-    const int64_t ci = idx ? idx[i] : i;
-    const uint64_t* key = src + ci * H.KW;
-    unsigned long long p = atomicAdd(H.n_pool, 1ull);
-    if ((int64_t)p >= H.cap_pool) {  // host guarantees capacity; keep the slot valid regardless
-        if (pool_idx) pool_idx[i] = -1;
-        return;
-    }
-    uint64_t* dst = H.pool + (int64_t)p * H.KW;
-    for (int w = 0; w < H.KW; w++) dst[w] = key[w];
-    H.pool_flags[p] = flag;
-    uint64_t fp = key_hash(key, H.KW) >> 33;
-    __threadfence();
-    H.table[slot[i]] = (fp << 33) | (uint64_t)(uint32_t)p;
-    if (pool_idx) pool_idx[i] = (int32_t)p;
-}
-
-__global__ void k_hash_lookup(HashSet H, const uint64_t* src, int64_t n, int32_t* found) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint64_t* key = src + i * H.KW;
-    uint64_t h = key_hash(key, H.KW);
-    uint64_t fp = h >> 33;
-    uint64_t pos = h & H.mask;
-    for (uint64_t probe = 0; probe <= H.mask; probe++) {
-        uint64_t v = H.table[pos];
-        if (v == kEmpty) break;
-        if ((v >> 33) == fp && !((v >> 32) & 1ull) && keys_equal(key, H.pool + (int64_t)(uint32_t)v * H.KW, H.KW)) {
-            found[i] = (int32_t)(uint32_t)v;
-            return;
+__global__ void k_hash_fixup(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                             int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag,
+                             int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail) {
+    const int64_t n = dev_count(n_dev, n_cap);
+    GRID_STRIDE(i, n) {
+        if (status[i] != 1) {
+            if (pool_idx) pool_idx[i] = -1;
+            continue;
         }
-        pos = (pos + 1) & H.mask;
+        const int64_t ci = idx ? idx[i] : i;
+        const uint64_t* key = src + ci * H.KW;
+        unsigned long long p = atomicAdd(H.n_pool, 1ull);
+        uint64_t* dst = H.pool + (int64_t)p * H.KW;
+        for (int w = 0; w < H.KW; w++) dst[w] = key[w];
+        H.pool_flags[p] = flag;
+        uint64_t fp = key_hash(key, H.KW) >> 33;
+        __threadfence();
+        H.table[slot[i]] = (fp << 33) | (uint64_t)(uint32_t)p;
+        if (pool_idx) pool_idx[i] = (int32_t)p;
+        if (queue) queue[atomicAdd(q_tail, 1ull)] = (int32_t)p;
     }
-    found[i] = -1;
 }
 
 // rebuild the slot array from the pool (table growth)
 __global__ void k_hash_rebuild(HashSet H, int64_t n_pool) {
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n_pool) return;
-    const uint64_t* key = H.pool + p * H.KW;
-    uint64_t h = key_hash(key, H.KW);
-    uint64_t v = ((h >> 33) << 33) | (uint64_t)(uint32_t)p;
-    uint64_t pos = h & H.mask;
-    for (;;) {
-        unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(H.table + pos),
-                                           (unsigned long long)kEmpty, (unsigned long long)v);
-        if (old == kEmpty) return;
-        pos = (pos + 1) & H.mask;
+    GRID_STRIDE(p, n_pool) {
+        const uint64_t* key = H.pool + p * H.KW;
+        uint64_t h = key_hash(key, H.KW);
+        uint64_t v = ((h >> 33) << 33) | (uint64_t)(uint32_t)p;
+        uint64_t pos = h & H.mask;
+        for (;;) {
+            unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(H.table + pos),
+                                               (unsigned long long)kEmpty, (unsigned long long)v);
+            if (old == kEmpty) break;
+            pos = (pos + 1) & H.mask;
+        }
     }
 }
 
-static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+static int g_sms = 0;
+static unsigned grid_for(int64_t n, int b) {
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (!g_sms) g_sms = 148;
+    }
+    int64_t blocks = (n + b - 1) / b;
+    int64_t cap = (int64_t)g_sms * 8;
+    return (unsigned)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
+}
 
-void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, int64_t n, int32_t* status,
-                        uint64_t* slot, cudaStream_t s) {
-    if (n > 0) { k_hash_insert<<<nblk(n, 256), 256, 0, s>>>(H, src, idx, n, status, slot); ++g_launch_count; }
+void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                        int64_t n_cap, int32_t* status, uint64_t* slot, cudaStream_t s) {
+    if (n_cap > 0) { k_hash_insert<<<grid_for(n_cap, 256), 256, 0, s>>>(H, src, idx, n_dev, n_cap, status, slot); ++g_launch_count; }
 }
-void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, int64_t n, const int32_t* status,
-                       const uint64_t* slot, uint32_t flag, int32_t* pool_idx, cudaStream_t s) {
-    if (n > 0) { k_hash_fixup<<<nblk(n, 256), 256, 0, s>>>(H, src, idx, n, status, slot, flag, pool_idx); ++g_launch_count; }
-}
-void launch_hash_lookup(const HashSet& H, const uint64_t* src, int64_t n, int32_t* found, cudaStream_t s) {
-    if (n > 0) { k_hash_lookup<<<nblk(n, 256), 256, 0, s>>>(H, src, n, found); ++g_launch_count; }
+void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                       int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
+                       int32_t* queue, unsigned long long* q_tail, cudaStream_t s) {
+    if (n_cap > 0) { k_hash_fixup<<<grid_for(n_cap, 256), 256, 0, s>>>(H, src, idx, n_dev, n_cap, status, slot, flag, pool_idx, queue, q_tail); ++g_launch_count; }
 }
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
-    if (n_pool > 0) { k_hash_rebuild<<<nblk(n_pool, 256), 256, 0, s>>>(H, n_pool); ++g_launch_count; }
+    if (n_pool > 0) { k_hash_rebuild<<<grid_for(n_pool, 256), 256, 0, s>>>(H, n_pool); ++g_launch_count; }
 }
 
-// ------------------------------------------------------------ list utilities
-// append i to out (via counter) where flag[i] == want; order within a block is ascending
-__global__ void k_compact(const int32_t* flag, int32_t want, int64_t n, int32_t* out, unsigned long long* count) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool take = i < n && flag[i] == want;
-    unsigned mask = __ballot_sync(0xffffffffu, take);
-    int lane = threadIdx.x & 31;
-    unsigned long long base = 0;
-    if (lane == 0 && mask) base = atomicAdd(count, (unsigned long long)__popc(mask));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (take) out[base + __popc(mask & ((1u << lane) - 1u))] = (int32_t)i;
-}
-void launch_compact(const int32_t* flag, int32_t want, int64_t n, int32_t* out, unsigned long long* count,
-                    cudaStream_t s) {
-    if (n > 0) { k_compact<<<nblk(n, 256), 256, 0, s>>>(flag, want, n, out, count); ++g_launch_count; }
+// ------------------------------------------------------------- iteration
+// take up to B queued states for this iteration, after checking that the
+// worst case of what the iteration can produce fits every buffer.
+__global__ void k_take(IterState I) {
+    __shared__ long long s_nR;
+    unsigned long long* c = I.ctr;
+    if (threadIdx.x == 0) {
+        long long head = (long long)c[C_QHEAD], tail = (long long)c[C_QTAIL];
+        long long want = tail - head;
+        if (want > I.B) want = I.B;
+        long long np = (long long)c[C_POOL];
+        long long nR = want;
+        // new pool entries: each batch item + everything its face can emit
+        long long room_pool = (I.cap_pool - np) / (1 + I.emit_per_cell);
+        long long room_tab = ((long long)(I.tcap / 2) - np) / (1 + I.emit_per_cell);
+        long long room_cells = I.cap_cells - (long long)c[C_CELLS];
+        long long room_verts = (I.cap_verts - (long long)c[C_VERTS]) / I.verts_per_cell;
+        long long room_refs = (I.cap_refs - (long long)c[C_REFS]) / I.refs_per_cell;
+        long long room_out = I.cap_outbox - (long long)c[C_NOUT];
+        if (I.world > 1) room_out /= (1 + I.emit_per_cell);
+        else room_out = nR;
+        long long lim = room_pool;
+        if (room_tab < lim) lim = room_tab;
+        if (room_cells < lim) lim = room_cells;
+        if (room_verts < lim) lim = room_verts;
+        if (room_refs < lim) lim = room_refs;
+        if (room_out < lim) lim = room_out;
+        if (lim < 0) lim = 0;
+        if (nR > lim) nR = lim;
+        c[C_STALL] = (want > 0 && nR == 0) ? 1ull : 0ull;
+        c[C_NR] = (unsigned long long)nR;
+        c[C_NX] = 0; c[C_NF] = 0; c[C_NPROBE] = 0; c[C_NEMIT] = 0; c[C_NLOCAL] = 0;
+        c[C_ITER] += nR > 0 ? 1ull : 0ull;
+        s_nR = nR;
+    }
+    __syncthreads();
+    long long head = (long long)c[C_QHEAD];
+    for (long long b = threadIdx.x; b < s_nR; b += blockDim.x) I.batch_pool[b] = I.queue[head + b];
+    __syncthreads();
+    if (threadIdx.x == 0) c[C_QHEAD] = (unsigned long long)(head + s_nR);
 }
 
-// dst[i] = src[idx[i]] (KW words each)
-__global__ void k_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t i = t / KW;
-    int w = (int)(t - i * KW);
-    if (i >= n) return;
-    dst[i * KW + w] = src[(int64_t)idx[i] * KW + w];
+// ckey[b] = pool[batch_pool[b]]; reset per-item flags
+__global__ void k_gather_batch(const uint64_t* pool, const int32_t* batch_pool, const unsigned long long* n_dev,
+                               int64_t n_cap, int KW, uint64_t* ckey, int32_t* changed, int32_t* canon_pos) {
+    const int64_t n = dev_count(n_dev, n_cap);
+    GRID_STRIDE(t, n * KW) {
+        int64_t b = t / KW;
+        int w = (int)(t - b * KW);
+        ckey[t] = pool[(int64_t)batch_pool[b] * KW + w];
+        if (w == 0) { changed[b] = 0; canon_pos[b] = -1; }
+    }
 }
-void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst, cudaStream_t s) {
-    if (n > 0) { k_gather_keys<<<nblk(n * KW, 256), 256, 0, s>>>(src, idx, n, KW, dst); ++g_launch_count; }
+
+// changed items: local canonical states -> X (canonical insert), remote-owned -> outbox
+__global__ void k_route_changed(const uint64_t* ckey, const int32_t* changed, const unsigned long long* n_dev,
+                                int64_t n_cap, int KW, int rank, int world, int32_t* X, unsigned long long* nX,
+                                uint64_t* outbox, unsigned long long* n_out, int32_t* canon_pos) {
+    const int64_t n = dev_count(n_dev, n_cap);
+    GRID_STRIDE(b, n) {
+        if (!changed[b]) continue;
+        const uint64_t* k = ckey + b * KW;
+        if (world > 1 && key_owner(k, KW, world) != rank) {
+            unsigned long long o = atomicAdd(n_out, 1ull);
+            for (int w = 0; w < KW; w++) outbox[o * KW + w] = k[w];
+            canon_pos[b] = -2;   // handled by its owner
+            continue;
+        }
+        unsigned long long j = atomicAdd(nX, 1ull);
+        X[j] = (int32_t)b;
+        canon_pos[b] = (int32_t)j;
+    }
 }
 
 // frontier assembly after composition (reference marching.py:280-288: canon == state -> skip;
-// canon new -> enqueue).  Raw winners whose canonical key equals the raw key are new cells;
-// changed ones are new cells only if their canonical insert won.
-__global__ void k_frontier(int64_t nR, const int32_t* changed, const int32_t* R, const int32_t* raw_pool,
-                           const int32_t* canon_pos, const int32_t* canon_status, const int32_t* canon_pool,
-                           uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* nF,
-                           int64_t max_new, unsigned long long* capped) {
-    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nR) return;
-    int32_t p = -1;
-    if (!changed[b]) {
-        p = raw_pool[R[b]];
-    } else {
-        int32_t j = canon_pos[b];
-        if (j >= 0 && canon_status[j] == 1) p = canon_pool[j];
+// canon new -> enqueue).  Batch items whose canonical key equals the raw key are new cells
+// (they won the raw insert); changed ones are new cells only if their canonical insert won.
+__global__ void k_frontier(const unsigned long long* n_dev, int64_t n_cap, const int32_t* changed,
+                           const int32_t* batch_pool, const int32_t* canon_pos, const int32_t* canon_status,
+                           const int32_t* canon_pool, uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool,
+                           unsigned long long* ctr, long long max_cells) {
+    const int64_t n = dev_count(n_dev, n_cap);
+    GRID_STRIDE(b, n) {
+        int32_t p = -1;
+        if (!changed[b]) {
+            p = batch_pool[b];
+        } else {
+            int32_t j = canon_pos[b];
+            if (j >= 0 && canon_status[j] == 1) p = canon_pool[j];
+        }
+        if (p < 0) continue;
+        unsigned long long tot = atomicAdd(ctr + C_TOTAL, 1ull);
+        if ((long long)tot >= max_cells) {  // max_cells cap (reference marching.py:240-242)
+            atomicAdd(ctr + C_CAPPED, 1ull);
+            continue;
+        }
+        unsigned long long k = atomicAdd(ctr + C_NF, 1ull);
+        pool_flags[p] |= 1u;
+        f_items[k] = (int32_t)b;
+        f_pool[k] = p;
     }
-    if (p < 0) return;
-    unsigned long long k = atomicAdd(nF, 1ull);
-    if ((int64_t)k >= max_new) {  // max_cells cap (reference marching.py:240-242)
-        atomicAdd(capped, 1ull);
-        return;
-    }
-    pool_flags[p] |= 1u;
-    f_items[k] = (int32_t)b;
-    f_pool[k] = p;
 }
-void launch_frontier(int64_t nR, const int32_t* changed, const int32_t* R, const int32_t* raw_pool,
+
+// zero the key slots the probe forward pass ORs its bits into
+__global__ void k_zero_probe_keys(uint64_t* scratch, const unsigned long long* ctr, int KW) {
+    const int64_t base = (int64_t)ctr[C_NEMIT] * KW;
+    const int64_t n = (int64_t)ctr[C_NPROBE] * KW;
+    GRID_STRIDE(i, n) scratch[base + i] = 0;
+}
+
+// probes were appended after the flips: total emitted = flips + probes
+__global__ void k_emit_finalize(unsigned long long* ctr) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) ctr[C_NEMIT] += ctr[C_NPROBE];
+}
+
+// sharded march: emitted states owned elsewhere -> outbox; local ones -> index list
+__global__ void k_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW,
+                                int rank, int world, int32_t* local_idx, unsigned long long* n_local,
+                                uint64_t* outbox, unsigned long long* n_out) {
+    const int64_t n = dev_count(ctr_n, n_cap);
+    GRID_STRIDE(i, n) {
+        const uint64_t* k = scratch + i * KW;
+        if (key_owner(k, KW, world) == rank) {
+            local_idx[atomicAdd(n_local, 1ull)] = (int32_t)i;
+        } else {
+            unsigned long long o = atomicAdd(n_out, 1ull);
+            for (int w = 0; w < KW; w++) outbox[o * KW + w] = k[w];
+        }
+    }
+}
+
+void launch_take(const IterState& I, cudaStream_t s) { k_take<<<1, 1024, 0, s>>>(I); ++g_launch_count; }
+void launch_gather_batch(const uint64_t* pool, const int32_t* batch_pool, const unsigned long long* n_dev,
+                         int64_t n_cap, int KW, uint64_t* ckey, int32_t* changed, int32_t* canon_pos, cudaStream_t s) {
+    k_gather_batch<<<grid_for(n_cap * KW, 256), 256, 0, s>>>(pool, batch_pool, n_dev, n_cap, KW, ckey, changed, canon_pos);
+    ++g_launch_count;
+}
+void launch_route_changed(const uint64_t* ckey, const int32_t* changed, const unsigned long long* n_dev, int64_t n_cap,
+                          int KW, int rank, int world, int32_t* X, unsigned long long* nX, uint64_t* outbox,
+                          unsigned long long* n_out, int32_t* canon_pos, cudaStream_t s) {
+    k_route_changed<<<grid_for(n_cap, 256), 256, 0, s>>>(ckey, changed, n_dev, n_cap, KW, rank, world, X, nX, outbox,
+                                                          n_out, canon_pos);
+    ++g_launch_count;
+}
+void launch_frontier(const unsigned long long* n_dev, int64_t n_cap, const int32_t* changed, const int32_t* batch_pool,
                      const int32_t* canon_pos, const int32_t* canon_status, const int32_t* canon_pool,
-                     uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* nF, int64_t max_new,
-                     unsigned long long* capped, cudaStream_t s) {
-    if (nR > 0)
-        { k_frontier<<<nblk(nR, 256), 256, 0, s>>>(nR, changed, R, raw_pool, canon_pos, canon_status, canon_pool,
-                                                   pool_flags, f_items, f_pool, nF, max_new, capped); ++g_launch_count; }
+                     uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* ctr,
+                     long long max_cells, cudaStream_t s) {
+    k_frontier<<<grid_for(n_cap, 256), 256, 0, s>>>(n_dev, n_cap, changed, batch_pool, canon_pos, canon_status,
+                                                     canon_pool, pool_flags, f_items, f_pool, ctr, max_cells);
+    ++g_launch_count;
+}
+void launch_zero_probe_keys(uint64_t* scratch, const unsigned long long* ctr, int KW, int64_t cap, cudaStream_t s) {
+    k_zero_probe_keys<<<grid_for(cap * KW, 256), 256, 0, s>>>(scratch, ctr, KW);
+    ++g_launch_count;
+}
+void launch_emit_finalize(unsigned long long* ctr, cudaStream_t s) { k_emit_finalize<<<1, 32, 0, s>>>(ctr); ++g_launch_count; }
+void launch_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW, int rank,
+                          int world, int32_t* local_idx, unsigned long long* n_local, uint64_t* outbox,
+                          unsigned long long* n_out, cudaStream_t s) {
+    k_route_emitted<<<grid_for(n_cap, 256), 256, 0, s>>>(scratch, ctr_n, n_cap, KW, rank, world, local_idx, n_local,
+                                                          outbox, n_out);
+    ++g_launch_count;
 }
 
-// canon_pos[b] = position of b in the changed list X (or -1)
-__global__ void k_scatter_pos(const int32_t* X, int64_t nX, int32_t* pos) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < nX) pos[X[j]] = (int32_t)j;
+// dst[i] = src[idx[i]] (KW words each), host-sized
+__global__ void k_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst) {
+    GRID_STRIDE(t, n * KW) {
+        int64_t i = t / KW;
+        int w = (int)(t - i * KW);
+        dst[t] = src[(int64_t)idx[i] * KW + w];
+    }
 }
-void launch_scatter_pos(const int32_t* X, int64_t nX, int32_t* pos, cudaStream_t s) {
-    if (nX > 0) { k_scatter_pos<<<nblk(nX, 256), 256, 0, s>>>(X, nX, pos); ++g_launch_count; }
+void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst, cudaStream_t s) {
+    if (n > 0) { k_gather_keys<<<grid_for(n * KW, 256), 256, 0, s>>>(src, idx, n, KW, dst); ++g_launch_count; }
 }
 
-// owner partition for sharded marching: out_owner[i] = owner(key_i)
+// open-edge count (edges with a box plane among their transition refs)
+__global__ void k_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
+                             unsigned long long* out) {
+    GRID_STRIDE(v, nv) {
+        bool hit = false;
+        for (int q = 0; q < enr[v]; q++) hit |= refs[roff[v] + q] >= box0;
+        if (hit) atomicAdd(out, 1ull);
+    }
+}
+void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
+                       unsigned long long* out, cudaStream_t s) {
+    if (nv > 0) { k_open_edges<<<grid_for(nv, 256), 256, 0, s>>>(enr, roff, refs, nv, box0, out); ++g_launch_count; }
+}
+
+// owner rank of each key (outbox grouping)
 __global__ void k_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) owner[i] = key_owner(keys + i * KW, KW, world);
+    GRID_STRIDE(i, n) owner[i] = key_owner(keys + i * KW, KW, world);
 }
 void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s) {
-    if (n > 0) { k_owner<<<nblk(n, 256), 256, 0, s>>>(keys, n, KW, world, owner); ++g_launch_count; }
+    if (n > 0) { k_owner<<<grid_for(n, 256), 256, 0, s>>>(keys, n, KW, world, owner); ++g_launch_count; }
+}
+
+__global__ void k_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
+                               unsigned long long* cnt) {
+    GRID_STRIDE(i, n) if (key_owner(keys + i * KW, KW, world) == rank) idx[atomicAdd(cnt, 1ull)] = (int32_t)i;
+}
+void launch_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
+                         unsigned long long* cnt, cudaStream_t s) {
+    if (n > 0) { k_filter_owned<<<grid_for(n, 256), 256, 0, s>>>(keys, n, KW, rank, world, idx, cnt); ++g_launch_count; }
 }
 
 }  // namespace am

@@ -62,24 +62,35 @@ struct StepDev {
 struct LayerLaunch {
     StepDev st;
     double* Z;            // [items][zs][C]
-    uint64_t* keys;       // [items][KW]
+    uint64_t* keys;       // [items][KW] (offset by *key_off items when key_off is set)
     int* changed;         // compose: per-item canonical-changed flag (may be null)
     const double* pts;    // forward: [items][3]
-    int64_t n_items;
+    const unsigned long long* n_dev;    // item count on the device (null: n_cap items)
+    const unsigned long long* key_off;  // optional device offset (items) into keys
+    int64_t n_cap;        // capacity / grid sizing
     int KW, zs;           // key words, Z row count per item (>= NB)
 };
+
+__device__ __forceinline__ int64_t dev_count(const unsigned long long* p, int64_t cap) {
+    if (!p) return cap;
+    int64_t n = (int64_t)*reinterpret_cast<const volatile unsigned long long*>(p);
+    return n < cap ? n : cap;
+}
+__device__ __forceinline__ uint64_t* keys_at(const LayerLaunch& L) {
+    return L.key_off ? L.keys + (int64_t)(*L.key_off) * L.KW : L.keys;
+}
 
 // kernels' host-side launchers (am_compose.cu)
 void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s);
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV,
                       cudaStream_t s);
-void launch_face_head(const double* Z, const uint64_t* keys, double* faces, int64_t n_items, int zs,
-                      int KW, const int* sub_last_row, const int* sub_last_n, const double* const* head_w,
-                      const double* head_b, int n_subs, cudaStream_t s);
-void launch_forward_head(const double* Z, uint64_t* keys, double* vals, int64_t n_items, int zs, int KW,
-                         const int* sub_last_row, const int* sub_last_n, const double* const* head_w,
-                         const double* head_b, int n_subs, int ensemble, cudaStream_t s);
 int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld_elems);
+
+// device counters shared by the iteration kernels
+enum Ctr {
+    C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_OVF0, C_OVF1, C_CAPPED, C_TOTAL, C_QHEAD, C_QTAIL, C_NR, C_NX,
+    C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_N
+};
 
 // hash set (am_hash.cu)
 struct HashSet {
@@ -91,15 +102,45 @@ struct HashSet {
     int64_t cap_pool;
     int KW;
 };
-// insert src[idx[i]] (or src[i] if idx null) for i < n; status[i] = 1 new / 0 present,
-// slot[i] = slot index for new entries (candidate-ref written, fixed up later)
-void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, int64_t n,
-                        int32_t* status, uint64_t* slot, cudaStream_t s);
-// assign pool indices to new entries, copy keys into the pool, rewrite slots
-void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, int64_t n,
-                       const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
-                       cudaStream_t s);
-void launch_hash_lookup(const HashSet& H, const uint64_t* src, int64_t n, int32_t* found, cudaStream_t s);
+void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                        int64_t n_cap, int32_t* status, uint64_t* slot, cudaStream_t s);
+void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                       int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
+                       int32_t* queue, unsigned long long* q_tail, cudaStream_t s);
+void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s);
+
+// per-iteration guard / queue state (am_hash.cu k_take)
+struct IterState {
+    unsigned long long* ctr;
+    const int32_t* queue;
+    int32_t* batch_pool;
+    long long B, cap_pool, tcap, cap_cells, cap_verts, cap_refs, cap_outbox;
+    long long emit_per_cell, verts_per_cell, refs_per_cell;
+    int world;
+};
+void launch_take(const IterState& I, cudaStream_t s);
+void launch_gather_batch(const uint64_t* pool, const int32_t* batch_pool, const unsigned long long* n_dev,
+                         int64_t n_cap, int KW, uint64_t* ckey, int32_t* changed, int32_t* canon_pos, cudaStream_t s);
+void launch_route_changed(const uint64_t* ckey, const int32_t* changed, const unsigned long long* n_dev, int64_t n_cap,
+                          int KW, int rank, int world, int32_t* X, unsigned long long* nX, uint64_t* outbox,
+                          unsigned long long* n_out, int32_t* canon_pos, cudaStream_t s);
+void launch_frontier(const unsigned long long* n_dev, int64_t n_cap, const int32_t* changed, const int32_t* batch_pool,
+                     const int32_t* canon_pos, const int32_t* canon_status, const int32_t* canon_pool,
+                     uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* ctr,
+                     long long max_cells, cudaStream_t s);
+void launch_zero_probe_keys(uint64_t* scratch, const unsigned long long* ctr, int KW, int64_t cap, cudaStream_t s);
+void launch_emit_finalize(unsigned long long* ctr, cudaStream_t s);
+void launch_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW, int rank,
+                          int world, int32_t* local_idx, unsigned long long* n_local, uint64_t* outbox,
+                          unsigned long long* n_out, cudaStream_t s);
+void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst, cudaStream_t s);
+void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
+                       unsigned long long* out, cudaStream_t s);
+void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
+                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, cudaStream_t s);
+void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
+                             const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,
+                             int n_subs, int ensemble, cudaStream_t s);
 
 // face extraction (am_face.cu)
 struct FaceArgs {
@@ -108,7 +149,8 @@ struct FaceArgs {
     const uint64_t* keys;     // canonical keys [batch][KW]
     const int32_t* items;     // frontier: batch slots to process
     const int32_t* pool_idx;  // per frontier entry: pool index of the state
-    int64_t n;                // frontier size
+    const unsigned long long* n_dev;  // frontier size (device)
+    int64_t n_cap;
     int NB, M, KW, zs, ensemble;
     double lo[3], hi[3];
     double tol_cell, tol_weld, tol_onplane, probe_delta;
@@ -124,7 +166,7 @@ struct FaceArgs {
     unsigned long long* n_verts;
     unsigned long long* n_refs;
     int64_t cap_cells, cap_verts, cap_refs;
-    uint64_t* cand;           // next-wave candidate keys [cap_cand][KW]
+    uint64_t* cand;           // emitted candidate keys [cap_cand][KW] (flips; probes follow)
     unsigned long long* n_cand;
     int64_t cap_cand;
     double* probe_pts;        // [cap_probe][3]
@@ -132,6 +174,9 @@ struct FaceArgs {
     int64_t cap_probe;
     unsigned long long* overflow;  // counters: [0] C-set/polygon overflow, [1] capacity overflow
 };
+constexpr int kEmitFlipsPerCell = 48;   // face kernel EMAXC
+constexpr int kVertsPerCell = 64;       // face kernel QMAX
+constexpr int kRefsPerCell = 256;
 void launch_face(const FaceArgs& a, cudaStream_t s);
 
 }  // namespace am

@@ -130,13 +130,19 @@ class Engine:
         _native.check(self.lib.am_run(self.h, ctypes.byref(n)), "am_run")
         return n.value
 
+    def queue_size(self) -> int:
+        n = ctypes.c_int64()
+        _native.check(self.lib.am_queue_size(self.h, ctypes.byref(n)), "am_queue_size")
+        return n.value
+
     def outbox(self):
+        """(per-owner counts (world,), keys grouped by owner rank) of states owned elsewhere."""
+        total = ctypes.c_int64()
+        _native.check(self.lib.am_outbox_counts(self.h, ctypes.byref(total)), "am_outbox_counts")
         counts = np.zeros(self.params.world, dtype=np.int64)
-        _native.check(self.lib.am_outbox_counts(self.h, counts.ctypes.data), "am_outbox_counts")
-        total = int(counts.sum())
-        out = torch.empty((total, self.kw), dtype=torch.int64, device=self.dev)
-        _native.check(self.lib.am_outbox_take(self.h, out.data_ptr() if total else None), "am_outbox_take")
-        return counts, out
+        out = torch.empty((max(total.value, 1), self.kw), dtype=torch.int64, device=self.dev)
+        _native.check(self.lib.am_outbox_take(self.h, out.data_ptr(), counts.ctypes.data), "am_outbox_take")
+        return counts, out[:total.value]
 
     def counts(self) -> dict:
         c = np.zeros(8, dtype=np.int64)
@@ -162,5 +168,6 @@ class Engine:
         s = np.zeros(16)
         _native.check(self.lib.am_stats(self.h, s.ctypes.data), "am_stats")
         keys = ("compose_ms", "face_ms", "compose_flops", "face_bytes", "composed", "faced", "batch",
-                "flops_per_cell", "launches", "waves")
+                "flops_per_cell", "launches", "iterations", "probe_ms", "probe_flops", "probes",
+                "flops_per_point")
         return dict(zip(keys, (float(x) for x in s)))

@@ -1,0 +1,39 @@
+"""One configs[1] march for profiling (ncu launch list / --set full on one kernel).
+
+    python tools/profile_march.py [--net geo90x6|deepsdf512] [--seeds 64] [--max-cells N]
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2106_10031_b200 import synth  # noqa: E402
+from paper_2106_10031_b200.engine import Engine  # noqa: E402
+from paper_2106_10031_b200.seeding import sample_seeds  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--net", default="geo90x6")
+ap.add_argument("--seeds", type=int, default=64)
+ap.add_argument("--max-cells", type=int, default=10_000_000)
+ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--timing", action="store_true")
+a = ap.parse_args()
+net = synth.geometric_mlp([90] * 6, seed=0) if a.net == "geo90x6" else synth.deepsdf_mlp(512, 8, 4, seed=0)
+eng = Engine(net, max_cells=a.max_cells)
+seeds = torch.as_tensor(sample_seeds(eng, a.seeds, ((-1.2,) * 3, (1.2,) * 3), rng_seed=0), device="cuda")
+eng.set_timing(a.timing)
+for _ in range(a.repeat):
+    eng.reset()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    eng.seed(seeds)
+    it = eng.run()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    c = eng.counts()
+    print(f"{a.net}: {c['cells']} cells, {it} iterations, {dt * 1e3:.1f} ms, {c['cells'] / dt:.0f} cells/s")
+print({k: round(v, 3) for k, v in eng.stats().items()})
