@@ -117,7 +117,8 @@ struct am_engine {
     // hash set + queue
     DBuf<uint64_t> table, pool;
     DBuf<uint32_t> pool_flags;
-    DBuf<int32_t> queue;
+    DBuf<int32_t> queue, pool_vn;
+    DBuf<int64_t> pool_voff;
     uint64_t tcap = 0;
     // counters (device) + host mirror
     DBuf<unsigned long long> ctr;
@@ -128,6 +129,11 @@ struct am_engine {
     DBuf<uint64_t> ckey, slot, slot2, scratch, outbox;
     DBuf<int32_t> changed, status, status2, canon_pos, canon_pool, X, f_items, f_pool, batch_pool, local_idx;
     DBuf<double> probe_pts, pZ;
+    DBuf<uint64_t> pkeys, pslot;
+    DBuf<int32_t> pstatus, emit_dup, emit_pool;
+    // probe records (single-neuron edges) + pending list + validated-neuron lists
+    DBuf<int32_t> prec_cand, prec_k, pend_t[2], pend_k[2], val_buf;
+    DBuf<double> prec_pt, pend_pt[2];
     // results
     DBuf<int32_t> cell_pool, cell_nv, edge_nrefs, edge_refs;
     DBuf<int64_t> cell_voff, edge_roff;
@@ -185,6 +191,8 @@ static HashSet hs(am_engine* e) {
     H.mask = e->tcap - 1;
     H.pool = e->pool.p;
     H.pool_flags = e->pool_flags.p;
+    H.pool_vn = e->pool_vn.p;
+    H.pool_voff = e->pool_voff.p;
     H.n_pool = e->ctr.p + C_POOL;
     H.cap_pool = e->pool.n / e->KW;
     H.KW = e->KW;
@@ -201,6 +209,8 @@ static int ensure_hash(am_engine* e, int64_t extra) {
     if (e->pool.n / e->KW < need) {
         CK(e->pool.reserve(need * e->KW, e->stream, true, np * e->KW, &moved));
         CK(e->pool_flags.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
+        CK(e->pool_vn.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
+        CK(e->pool_voff.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
     }
     CK(e->queue.reserve(e->pool.n / e->KW, e->stream, true, (int64_t)e->hctr[C_QTAIL], &moved));
     if ((int64_t)e->tcap < 2 * need) {
@@ -230,6 +240,16 @@ static int ensure_results(am_engine* e, int64_t cells) {
     CK(e->edge_nrefs.reserve(nv + cells * kVertsPerCell, s, true, nv, &moved));
     CK(e->edge_roff.reserve(nv + cells * kVertsPerCell, s, true, nv, &moved));
     CK(e->edge_refs.reserve(nr + cells * kRefsPerCell, s, true, nr, &moved));
+    int64_t nval = (int64_t)e->hctr[C_NVAL], npend = (int64_t)e->hctr[C_NPEND];
+    int par = (int)(e->hctr[C_PPAR] & 1ull);
+    CK(e->val_buf.reserve(nval + cells * kVertsPerCell, s, true, nval, &moved));
+    int64_t pcap = npend + cells * kVertsPerCell;
+    for (int q = 0; q < 2; q++) {
+        int64_t keep = q == par ? npend : 0;
+        CK(e->pend_t[q].reserve(pcap, s, true, keep, &moved));
+        CK(e->pend_k[q].reserve(pcap, s, true, keep, &moved));
+        CK(e->pend_pt[q].reserve(pcap * 3, s, true, keep * 3, &moved));
+    }
     if (e->P.world > 1) {
         int64_t no = (int64_t)e->hctr[C_NOUT];
         CK(e->outbox.reserve((no + cells * (1 + emit_per_cell())) * e->KW, s, true, no * e->KW, &moved));
@@ -355,6 +375,14 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->local_idx.reserve(e->E, s));
     CK(e->probe_pts.reserve(e->PB * 3, s));
     CK(e->pZ.reserve(e->PB * e->zs, s));
+    CK(e->pkeys.reserve(e->PB * e->KW, s));
+    CK(e->pslot.reserve(e->PB, s));
+    CK(e->pstatus.reserve(e->PB, s));
+    CK(e->emit_dup.reserve(e->E, s));
+    CK(e->emit_pool.reserve(e->E, s));
+    CK(e->prec_cand.reserve(e->PB, s));
+    CK(e->prec_k.reserve(e->PB, s));
+    CK(e->prec_pt.reserve(e->PB * 3, s));
     CK(e->outbox.reserve(e->KW, s));
     CK(e->ctr.reserve(C_N, s));
     CK(cudaMemset(e->ctr.p, 0, C_N * sizeof(unsigned long long)));
@@ -372,16 +400,19 @@ extern "C" int am_engine_destroy(am_engine* e) {
     if (e->gexec) cudaGraphExecDestroy(e->gexec);
     if (e->graph) cudaGraphDestroy(e->graph);
     DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx,
-                           &e->sxp, &e->pvals};
+                           &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1]};
     for (auto* b : dbl) b->release();
     DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->ckey, &e->slot, &e->slot2, &e->scratch, &e->outbox,
-                             &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres};
+                             &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres, &e->pkeys, &e->pslot};
     for (auto* b : u64) b->release();
     DBuf<int32_t>* i32[] = {&e->changed, &e->status, &e->status2, &e->canon_pos, &e->canon_pool, &e->X,
                             &e->f_items, &e->f_pool, &e->batch_pool, &e->local_idx, &e->queue, &e->cell_pool,
-                            &e->cell_nv, &e->edge_nrefs, &e->edge_refs, &e->hstatus, &e->sact, &e->sdone};
+                            &e->cell_nv, &e->edge_nrefs, &e->edge_refs, &e->hstatus, &e->sact, &e->sdone,
+                            &e->pool_vn, &e->pstatus, &e->emit_dup, &e->emit_pool, &e->prec_cand, &e->prec_k,
+                            &e->pend_t[0], &e->pend_t[1], &e->pend_k[0], &e->pend_k[1], &e->val_buf};
     for (auto* b : i32) b->release();
     e->pool_flags.release();
+    e->pool_voff.release();
     e->cell_voff.release();
     e->edge_roff.release();
     e->subdev.release();
@@ -501,8 +532,15 @@ static int launch_iteration(am_engine* e) {
     I.cap_pool = e->pool.n / e->KW; I.tcap = (long long)e->tcap;
     I.cap_cells = e->cell_pool.n; I.cap_verts = e->edge_nrefs.n; I.cap_refs = e->edge_refs.n;
     I.cap_outbox = e->P.world > 1 ? e->outbox.n / e->KW : 0;
+    I.cap_pend = e->pend_t[0].n; I.cap_val = e->val_buf.n;
     I.emit_per_cell = emit_per_cell(); I.verts_per_cell = kVertsPerCell; I.refs_per_cell = kRefsPerCell;
     I.world = e->P.world;
+    ProbeRecs R;
+    R.cand = e->prec_cand.p; R.k = e->prec_k.p; R.pt = e->prec_pt.p;
+    for (int q = 0; q < 2; q++) { R.pend_t[q] = e->pend_t[q].p; R.pend_k[q] = e->pend_k[q].p; R.pend_pt[q] = e->pend_pt[q].p; }
+    R.cap_pend = e->pend_t[0].n;
+    const bool multi = e->P.world > 1;
+
     launch_take(I, s);
     launch_gather_batch(e->pool.p, e->batch_pool.p, c + C_NR, B, e->KW, e->ckey.p, e->changed.p, e->canon_pos.p, s);
     if (tm) cudaEventRecord(e->ev[0], s);
@@ -510,7 +548,7 @@ static int launch_iteration(am_engine* e) {
     if (tm) cudaEventRecord(e->ev[1], s);
     launch_route_changed(e->ckey.p, e->changed.p, c + C_NR, B, e->KW, e->P.rank, e->P.world, e->X.p, c + C_NX,
                          e->outbox.p, c + C_NOUT, e->canon_pos.p, s);
-    launch_hash_insert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, s);
+    launch_hash_insert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, nullptr, s);
     launch_hash_fixup(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, 0u, e->canon_pool.p, nullptr,
                       nullptr, s);
     launch_frontier(c + C_NR, B, e->changed.p, e->batch_pool.p, e->canon_pos.p, e->status2.p, e->canon_pool.p,
@@ -526,25 +564,46 @@ static int launch_iteration(am_engine* e) {
     a.verts = e->verts.p; a.edge_nrefs = e->edge_nrefs.p; a.edge_roff = e->edge_roff.p; a.edge_refs = e->edge_refs.p;
     a.n_verts = c + C_VERTS; a.n_refs = c + C_REFS;
     a.cap_cells = e->cell_pool.n; a.cap_verts = e->edge_nrefs.n; a.cap_refs = e->edge_refs.n;
-    a.cand = e->scratch.p; a.n_cand = c + C_NEMIT; a.cap_cand = B * kEmitFlipsPerCell;
+    a.cand = e->scratch.p; a.n_cand = c + C_NEMIT; a.cap_cand = e->E;
     a.probe_pts = e->probe_pts.p; a.n_probe = c + C_NPROBE; a.cap_probe = e->PB;
     a.overflow = c + C_OVF0;
+    a.prec_cand = e->prec_cand.p; a.prec_k = e->prec_k.p; a.prec_pt = e->prec_pt.p; a.n_prec = c + C_NPREC;
+    a.cap_prec = e->PB;
+    a.val_buf = e->val_buf.p; a.n_val = c + C_NVAL; a.cap_val = e->val_buf.n;
+    a.pool_vn = e->pool_vn.p; a.pool_voff = e->pool_voff.p;
     if (tm) cudaEventRecord(e->ev[2], s);
     launch_face(a, s);
     if (tm) cudaEventRecord(e->ev[3], s);
-    launch_zero_probe_keys(e->scratch.p, c, e->KW, e->PB, s);
-    RC(forward(e, e->probe_pts.p, nullptr, e->scratch.p, c + C_NEMIT, e->pZ.p, c + C_NPROBE, e->PB));
-    if (tm) cudaEventRecord(e->ev[4], s);
-    launch_emit_finalize(c, s);
-    if (e->P.world > 1) {
+    // flips: insert (local) and queue the new states
+    if (multi) {
         launch_route_emitted(e->scratch.p, c + C_NEMIT, e->E, e->KW, e->P.rank, e->P.world, e->local_idx.p,
-                             c + C_NLOCAL, e->outbox.p, c + C_NOUT, s);
-        launch_hash_insert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, s);
-        launch_hash_fixup(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, 0u, nullptr,
+                             c + C_NLOCAL, e->outbox.p, c + C_NOUT, e->status.p, s);
+        launch_hash_insert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p,
+                           e->emit_dup.p, s);
+        launch_hash_fixup(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, 0u,
+                          e->emit_pool.p, e->queue.p, c + C_QTAIL, s);
+    } else {
+        launch_hash_insert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, e->emit_dup.p, s);
+        launch_hash_fixup(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, 0u, e->emit_pool.p,
+                          e->queue.p, c + C_QTAIL, s);
+    }
+    // probe records: target entries -> pending; pending with processed targets -> drop / forward
+    launch_prec_target(R, e->status.p, e->emit_dup.p, e->emit_pool.p, c, e->PB, e->probe_pts.p, e->PB, s);
+    launch_resolve(R, H, e->val_buf.p, c, R.cap_pend, e->probe_pts.p, e->PB, s);
+    launch_pend_finalize(c, s);
+    // exact forward evaluation of the remaining probes
+    launch_zero_keys(e->pkeys.p, c + C_NPROBE, e->KW, e->PB, s);
+    RC(forward(e, e->probe_pts.p, nullptr, e->pkeys.p, nullptr, e->pZ.p, c + C_NPROBE, e->PB));
+    if (tm) cudaEventRecord(e->ev[4], s);
+    if (multi) {
+        launch_route_emitted(e->pkeys.p, c + C_NPROBE, e->PB, e->KW, e->P.rank, e->P.world, e->local_idx.p,
+                             c + C_NPLOCAL, e->outbox.p, c + C_NOUT, nullptr, s);
+        launch_hash_insert(H, e->pkeys.p, e->local_idx.p, c + C_NPLOCAL, e->PB, e->pstatus.p, e->pslot.p, nullptr, s);
+        launch_hash_fixup(H, e->pkeys.p, e->local_idx.p, c + C_NPLOCAL, e->PB, e->pstatus.p, e->pslot.p, 0u, nullptr,
                           e->queue.p, c + C_QTAIL, s);
     } else {
-        launch_hash_insert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, s);
-        launch_hash_fixup(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, 0u, nullptr,
+        launch_hash_insert(H, e->pkeys.p, nullptr, c + C_NPROBE, e->PB, e->pstatus.p, e->pslot.p, nullptr, s);
+        launch_hash_fixup(H, e->pkeys.p, nullptr, c + C_NPROBE, e->PB, e->pstatus.p, e->pslot.p, 0u, nullptr,
                           e->queue.p, c + C_QTAIL, s);
     }
     CK(cudaGetLastError());
@@ -603,7 +662,7 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
     while (n < max_iters) {
         RC(sync_counters(e));
         if (e->hctr[C_OVF1]) return fail(AM_ERR_OVERFLOW, "output capacity overflow (%llu events)", e->hctr[C_OVF1]);
-        if (e->hctr[C_QHEAD] >= e->hctr[C_QTAIL]) break;
+        if (e->hctr[C_QHEAD] >= e->hctr[C_QTAIL] && e->hctr[C_NPEND] == 0) break;
         int k = (int)std::min<int64_t>(e->graph_batch, max_iters - n);
         RC(ensure_iter_room(e, k + 1));
         if (e->timing) {
@@ -635,11 +694,12 @@ static int push_keys(am_engine* e, const uint64_t* d_keys, int64_t n) {
         CK(e->local_idx.reserve(n, e->stream));
         CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, 8, e->stream));
         launch_filter_owned(d_keys, n, e->KW, e->P.rank, e->P.world, e->local_idx.p, e->ctr.p + C_LIST, e->stream);
-        launch_hash_insert(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, e->stream);
+        launch_hash_insert(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, nullptr,
+                           e->stream);
         launch_hash_fixup(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, 0u, nullptr,
                           e->queue.p, e->ctr.p + C_QTAIL, e->stream);
     } else {
-        launch_hash_insert(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, e->stream);
+        launch_hash_insert(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, nullptr, e->stream);
         launch_hash_fixup(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, 0u, nullptr, e->queue.p,
                           e->ctr.p + C_QTAIL, e->stream);
     }
@@ -877,9 +937,11 @@ extern "C" int am_set_timing(am_engine* e, int enabled) {
 //       kernel launches (process-wide), iterations, probe_ms, probe_flops, probes, flops_per_point]
 extern "C" int am_stats(am_engine* e, double* h) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
+    RC(sync_counters(e));
     h[0] = e->t_compose; h[1] = e->t_face; h[2] = e->flops; h[3] = e->face_bytes;
     h[4] = e->n_comp_cells; h[5] = e->n_face_cells; h[6] = (double)e->B; h[7] = e->flops_per_cell;
     h[8] = (double)g_launch_count; h[9] = (double)e->iters; h[10] = e->t_probe; h[11] = e->pflops;
-    h[12] = e->n_probes; h[13] = e->flops_per_point; h[14] = 0; h[15] = 0;
+    h[12] = e->n_probes; h[13] = e->flops_per_point;
+    h[14] = (double)e->hctr[C_PROBES_TOTAL]; h[15] = (double)e->hctr[C_PREC_TOTAL];
     return AM_OK;
 }

@@ -21,7 +21,16 @@
 //           orientation, canonical rotation and per-edge transition planes.
 //   expand  each crossable edge emits the neighbour states of
 //           reference marching.py:152-186 (flip subsets x branch targets) and a
-//           probe point 1e-7 across its first plane (marching.py:271-276).
+//           probe 1e-7 across its first plane (marching.py:271-276).  A probe
+//           across a single neuron plane is emitted as a *probe record* tied to
+//           the flipped state instead of a point to forward-evaluate: the cell on
+//           the far side validates the mirrored point against its own planes
+//           (below) and a validated probe provably lands in that cell, so it needs
+//           no forward pass.  Every other probe is forward-evaluated exactly.
+//   validate for each single-neuron edge the mirrored probe point mid - 1e-7 n
+//           is checked against every neuron / branch functional of this cell
+//           (sign consistent with the canonical state, with margin); the
+//           validated neuron ids are published for the cell's pool entry.
 #include <cstdio>
 
 #include "am_internal.h"
@@ -34,11 +43,15 @@ constexpr int QMAX = 64;   // accepted raw vertices
 constexpr int EMAXC = 48;  // candidate descriptors per cell
 constexpr int FW = 4;      // warps per CTA
 constexpr double kCDelta = 1e-10;
+constexpr double kValMargin = 1e-11;   // sign margin (unit and raw values) for probe validation
+constexpr double kTinyNorm = 1e-6;     // rows this thin make validation unreliable
 
 struct FaceWarp {
     double ps[2][VMAX], pt[2][VMAX];
-    double cn[CMAX][4];
+    double cn[CMAX][5];             // unit row (n, o) + raw normal norm
     int cid[CMAX];
+    unsigned long long core;        // C rows within tol of P_tol (pair / incident candidates)
+    int tb[64], tr[64];             // scratch: neuron bits / branch targets of one edge
     double qv[QMAX][3];
     unsigned long long qs[QMAX];
     double rv[QMAX][3];
@@ -52,9 +65,12 @@ struct FaceWarp {
     int eargmin[QMAX];              // per-edge global row when the mask is empty (argmin fallback)
     // candidate descriptors: flip bits (<= 4, or -1 = "all bits of edge e") and branch target
     int cd_edge[EMAXC], cd_nflip[EMAXC], cd_flip[EMAXC][4], cd_branch[EMAXC];
+    int cd_probe[EMAXC];            // >= 0: this flip carries the probe record of edge cd_probe
     int n_cd;
     int status;
+    int risky;
     long long cbase;
+    int eval[QMAX];                 // per edge: 1 if the mirrored probe validated
 };
 
 struct Ctx {
@@ -65,12 +81,14 @@ struct Ctx {
     double lo[3], hi[3];
 };
 
-// unit oriented constraint row of global plane id gr (reference cells.py:127-185); false if dropped
-__device__ __forceinline__ bool get_row(const Ctx& c, int gr, double n[3], double& o) {
+// unit oriented constraint row of global plane id gr (reference cells.py:127-185); false if dropped.
+// *nrm receives the raw normal norm (neuron / branch rows) or 1 (box rows)
+__device__ __forceinline__ bool get_row(const Ctx& c, int gr, double n[3], double& o, double* nrm_out = nullptr) {
     if (gr < c.NB) {
         const double2* p = reinterpret_cast<const double2*>(c.Z + (int64_t)gr * 4);
         double2 a = __ldg(p), b = __ldg(p + 1);
         double nrm = sqrt((a.x * a.x + a.y * a.y) + b.x * b.x);
+        if (nrm_out) *nrm_out = nrm;
         if (!(nrm > kDegen)) return false;
         double orient = key_bit(c.key, gr) ? -1.0 : 1.0;
         n[0] = (a.x * orient) / nrm; n[1] = (a.y * orient) / nrm; n[2] = (b.x * orient) / nrm;
@@ -84,10 +102,12 @@ __device__ __forceinline__ bool get_row(const Ctx& c, int gr, double n[3], doubl
         const double* fj = c.faces + c.branch * 4;
         double d0 = ft[0] - fj[0], d1 = ft[1] - fj[1], d2 = ft[2] - fj[2], dc = ft[3] - fj[3];
         double nrm = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+        if (nrm_out) *nrm_out = nrm;
         if (!(nrm > kDegen)) return false;
         n[0] = d0 / nrm; n[1] = d1 / nrm; n[2] = d2 / nrm; o = dc / nrm;
         return true;
     }
+    if (nrm_out) *nrm_out = 1.0;
     int k = gr - c.NB - c.M;
     int ax = k >> 1;
     n[0] = n[1] = n[2] = 0.0;
@@ -154,6 +174,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     for (int k = 0; k < 3; k++) { c.lo[k] = A.lo[k]; c.hi[k] = A.hi[k]; }
     const double tol_c = A.tol_cell, tol_p = A.tol_onplane;
     const double tol_max = fmax(tol_c, tol_p);
+    const int box0 = c.NB + c.M;
 
     // ------------------------------------------------------ face plane
     const double* fr = c.faces + c.branch * 4;
@@ -190,7 +211,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             double n[3], o = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
             bool cut = false;
             if (idx < c.K) {
-                int gr = idx < 6 ? c.NB + c.M + idx : idx - 6;
+                int gr = idx < 6 ? box0 + idx : idx - 6;
                 if (get_row(c, gr, n, o)) {
                     a2 = dot3(n, U); b2 = dot3(n, Vv); g2 = (dot3(n, P0) + o) - tol_c;
                     double mx = -1e300;
@@ -203,7 +224,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
                 int src = __ffs(mask) - 1;
                 mask &= mask - 1;
                 double ca = __shfl_sync(full, a2, src), cb = __shfl_sync(full, b2, src), cg = __shfl_sync(full, g2, src);
-                // warp-parallel Sutherland-Hodgman step
+                // warp-parallel Sutherland-Hodgman step, one lane per vertex
                 double si = 0, ti = 0, di = 0;
                 if (lane < nv) { si = W->ps[cur][lane]; ti = W->pt[cur][lane]; di = ca * si + cb * ti + cg; }
                 int nxt = lane + 1 == nv ? 0 : lane + 1;
@@ -238,35 +259,70 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         }
     }
 
-    // ------------------------------------------------ pass B: candidate set C
+    // ------------------------------------------------ pass B: candidate set C'
+    // core rows: within tol of P_tol (the only rows that can carry a vertex, an
+    // incident plane or an edge plane); the wider band up to 1.5 probe steps is
+    // kept for probe validation.  `risky` marks near-degenerate rows that make
+    // the validation margins meaningless (the cell then publishes nothing).
     int nC = 0;
+    unsigned long long core = 0;
+    int risky = 0;
+    const double band = tol_max + 1.5 * A.probe_delta + 1e-9;
     if (status == 0) {
         for (int base = 0; base < c.K; base += 32) {
             int gr = base + lane;
-            double n[3], o = 0.0;
-            bool in = false;
-            if (gr < c.K && get_row(c, gr, n, o)) {
-                double a2 = dot3(n, U), b2 = dot3(n, Vv), g2 = dot3(n, P0) + o;
-                double mx = -1e300;
-                for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
-                in = mx >= -tol_max - kCDelta;
+            double n[3], o = 0.0, nrm = 1.0;
+            bool in = false, is_core = false;
+            if (gr < c.K) {
+                nrm = 0.0;
+                bool kept = get_row(c, gr, n, o, &nrm);
+                // near-degenerate neuron / branch functionals make the validation margins meaningless
+                if (gr < c.NB && nrm > 0.0 && nrm < kTinyNorm) risky = 1;
+                if (gr >= c.NB && gr < box0 && c.ensemble && gr - c.NB != c.branch && nrm < kTinyNorm) risky = 1;
+                if (kept) {
+                    double a2 = dot3(n, U), b2 = dot3(n, Vv), g2 = dot3(n, P0) + o;
+                    double mx = -1e300;
+                    for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+                    in = mx >= -band;
+                    is_core = mx >= -tol_max - kCDelta;
+                }
             }
             unsigned mask = __ballot_sync(full, in);
+            unsigned cmask = __ballot_sync(full, is_core);
             int pos = nC + __popc(mask & ((1u << lane) - 1u));
             if (in && pos < CMAX) {
                 W->cn[pos][0] = n[0]; W->cn[pos][1] = n[1]; W->cn[pos][2] = n[2]; W->cn[pos][3] = o;
+                W->cn[pos][4] = nrm;
                 W->cid[pos] = gr;
+            }
+            // core bits in C order
+            unsigned m = mask;
+            int k = nC;
+            while (m && k < CMAX) {
+                int l = __ffs(m) - 1;
+                m &= m - 1;
+                if ((cmask >> l) & 1u) core |= 1ull << k;
+                k++;
             }
             nC += __popc(mask);
         }
+        risky = __any_sync(full, risky);
         if (nC > CMAX) status = 2;
         __syncwarp();
     }
 
-    // ------------------------------------- exact vertex semantics on C
+    // ------------------------------------- exact vertex semantics on C (core rows)
     int nq = 0;
     if (status == 0) {
-        int P = nC * (nC - 1) / 2;
+        // core row indices, in C order
+        int ncore = __popcll(core);
+        int P = ncore * (ncore - 1) / 2;
+        if (lane == 0) {
+            int k = 0;
+            for (int r = 0; r < nC; r++)
+                if ((core >> r) & 1ull) W->tb[k++] = r;
+        }
+        __syncwarp();
         for (int base = 0; base < P; base += 32) {
             int p = base + lane;
             bool valid = false;
@@ -274,9 +330,10 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             unsigned long long set = 0;
             if (p < P) {
                 // triu order: i from 0, j from i+1 (reference cells.py:344 np.triu_indices)
-                int i = 0, rem = p;
-                while (rem >= nC - 1 - i) { rem -= nC - 1 - i; i++; }
-                int j = i + 1 + rem;
+                int ii = 0, rem = p;
+                while (rem >= ncore - 1 - ii) { rem -= ncore - 1 - ii; ii++; }
+                int jj = ii + 1 + rem;
+                int i = W->tb[ii], j = W->tb[jj];
                 double Mx[9] = {W->cn[i][0], W->cn[i][1], W->cn[i][2], W->cn[j][0], W->cn[j][1], W->cn[j][2],
                                 fu[0], fu[1], fu[2]};
                 double rhs[3] = {-W->cn[i][3], -W->cn[j][3], -fo};
@@ -365,7 +422,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         if (nr < 3) status = 1;
     }
 
-    // per-edge transition planes (lane per edge)
+    // per-edge transition planes + mirrored-probe validation (lane per edge)
     if (status == 0) {
         bool need_argmin = false;
         for (int e = lane; e < nr; e += 32) {
@@ -374,13 +431,37 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             double mid[3] = {0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2])};
             unsigned long long on_mid = 0;
             for (int r = 0; r < nC; r++)
-                if (fabs(dot3(W->cn[r], mid) + W->cn[r][3]) <= tol_p) on_mid |= 1ull << r;
+                if (((core >> r) & 1ull) && fabs(dot3(W->cn[r], mid) + W->cn[r][3]) <= tol_p) on_mid |= 1ull << r;
             unsigned long long shared = W->fs[e] & W->fs[(e + 1) % nr];
             unsigned long long rows = shared & on_mid;
             if (!rows) rows = shared ? shared : on_mid;
             W->erow[e] = rows;
             W->eargmin[e] = -1;
             if (!rows) need_argmin = true;
+            // validation: a single crossable neuron plane k -> the neighbour's probe lands at
+            // mid - delta * n_k (mirror image); it lands in this cell iff every neuron and
+            // branch functional keeps the sign of this cell's state there (with margin)
+            int ok = 0;
+            if (!risky && rows) {
+                int ncross = 0, kr = -1;
+                unsigned long long m = rows;
+                while (m) {
+                    int r = __ffsll((long long)m) - 1;
+                    m &= m - 1;
+                    if (W->cid[r] < box0) { ncross++; kr = r; }
+                }
+                if (ncross == 1 && W->cid[kr] < c.NB) {
+                    double qp[3] = {mid[0] - A.probe_delta * W->cn[kr][0], mid[1] - A.probe_delta * W->cn[kr][1],
+                                    mid[2] - A.probe_delta * W->cn[kr][2]};
+                    ok = 1;
+                    for (int r = 0; r < nC && ok; r++) {
+                        if (W->cid[r] >= box0) continue;
+                        double v = dot3(W->cn[r], qp) + W->cn[r][3];
+                        if (!(v < -kValMargin && v * W->cn[r][4] < -kValMargin)) ok = 0;
+                    }
+                }
+            }
+            W->eval[e] = ok;
         }
         // rare: no plane within tol of the edge -> argmin over every cell row (reference cells.py:327-328)
         unsigned am_mask = __ballot_sync(full, need_argmin);
@@ -412,6 +493,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     }
 
     // ------------------------------------------------------------ emit cell
+    const int32_t pidx = A.pool_idx[fi];
     int64_t cell = 0;
     if (lane == 0) {
         cell = (int64_t)atomicAdd(A.n_cells, 1ull);
@@ -424,129 +506,150 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     }
     if (status != 0) {
         if (lane == 0) {
-            A.cell_pool[cell] = A.pool_idx[fi];
+            A.cell_pool[cell] = pidx;
             A.cell_nv[cell] = status == 2 ? -1 : 0;
             A.cell_voff[cell] = 0;
+            A.pool_vn[pidx] = 0;   // processed, nothing validated
         }
         return;
     }
-    int64_t voff = 0, roff = 0;
-    int nrefs_total = 0;
-    for (int e = 0; e < nr; e++) nrefs_total += W->erow[e] ? __popcll(W->erow[e]) : 1;
-    if (lane == 0) {
-        voff = (int64_t)atomicAdd(A.n_verts, (unsigned long long)nr);
-        roff = (int64_t)atomicAdd(A.n_refs, (unsigned long long)nrefs_total);
+    int nrefs_total = 0, nvalid = 0;
+    for (int e = 0; e < nr; e++) {
+        nrefs_total += W->erow[e] ? __popcll(W->erow[e]) : 1;
+        nvalid += W->eval[e];
     }
-    voff = __shfl_sync(full, voff, 0);
-    roff = __shfl_sync(full, roff, 0);
-    if (voff + nr > A.cap_verts || roff + nrefs_total > A.cap_refs) {
-        if (lane == 0) {
+    if (lane == 0) {
+        int64_t voff = (int64_t)atomicAdd(A.n_verts, (unsigned long long)nr);
+        int64_t roff = (int64_t)atomicAdd(A.n_refs, (unsigned long long)nrefs_total);
+        int64_t vloff = nvalid ? (int64_t)atomicAdd(A.n_val, (unsigned long long)nvalid) : 0;
+        if (voff + nr > A.cap_verts || roff + nrefs_total > A.cap_refs || vloff + nvalid > A.cap_val) {
             atomicAdd(&A.overflow[1], 1ull);
-            A.cell_pool[cell] = A.pool_idx[fi];
+            A.cell_pool[cell] = pidx;
             A.cell_nv[cell] = -2;
             A.cell_voff[cell] = 0;
-        }
-        return;
-    }
-    if (lane == 0) {
-        A.cell_pool[cell] = A.pool_idx[fi];
-        A.cell_nv[cell] = nr;
-        A.cell_voff[cell] = voff;
-        int64_t ro = roff;
-        for (int e = 0; e < nr; e++) {
-            A.verts[(voff + e) * 3 + 0] = W->fv[e][0];
-            A.verts[(voff + e) * 3 + 1] = W->fv[e][1];
-            A.verts[(voff + e) * 3 + 2] = W->fv[e][2];
-            A.edge_roff[voff + e] = ro;
-            int cnt = 0;
-            if (W->erow[e]) {
-                unsigned long long m = W->erow[e];
-                while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; A.edge_refs[ro++] = W->cid[r]; cnt++; }
-            } else {
-                A.edge_refs[ro++] = W->eargmin[e];
-                cnt = 1;
-            }
-            A.edge_nrefs[voff + e] = cnt;
-        }
-        // ---------------- neighbour candidates (reference marching.py:152-186, 262-288)
-        int ncd = 0;
-        const int box0 = c.NB + c.M;
-        for (int e = 0; e < nr; e++) {
-            int ids[64], nid = 0;
-            if (W->erow[e]) {
-                unsigned long long m = W->erow[e];
-                while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; if (W->cid[r] < box0) ids[nid++] = r; }
-            } else if (W->eargmin[e] < box0) {
-                ids[nid++] = -1 - W->eargmin[e];  // global id encoded (no C row)
-            }
-            if (!nid) continue;
-            int bits[64], nb = 0, brs[64], nbr = 0;
-            for (int i = 0; i < nid; i++) {
-                int gid = ids[i] >= 0 ? W->cid[ids[i]] : -1 - ids[i];
-                if (gid < c.NB) bits[nb++] = gid; else brs[nbr++] = gid - c.NB;
-            }
-            // subsets: combinations of sizes 0..nb (nb <= 3) or singles + full + () (nb > 3)
-            int nsub = 0, sub_mask[16];
-            bool big = nb > 3;
-            if (big) {
-                nsub = nb + 2;
-            } else {
-                for (int k = 0; k <= nb; k++) {
-                    int idx[4];
-                    for (int i = 0; i < k; i++) idx[i] = i;
-                    for (;;) {
-                        int mk = 0;
-                        for (int i = 0; i < k; i++) mk |= 1 << idx[i];
-                        sub_mask[nsub++] = mk;
-                        int i = k - 1;
-                        while (i >= 0 && idx[i] == nb - k + i) i--;
-                        if (i < 0) break;
-                        idx[i]++;
-                        for (int tt = i + 1; tt < k; tt++) idx[tt] = idx[tt - 1] + 1;
-                    }
+            A.pool_vn[pidx] = 0;
+            W->n_cd = -1;
+        } else {
+            A.cell_pool[cell] = pidx;
+            A.cell_nv[cell] = nr;
+            A.cell_voff[cell] = voff;
+            int64_t ro = roff, vo = vloff;
+            for (int e = 0; e < nr; e++) {
+                A.verts[(voff + e) * 3 + 0] = W->fv[e][0];
+                A.verts[(voff + e) * 3 + 1] = W->fv[e][1];
+                A.verts[(voff + e) * 3 + 2] = W->fv[e][2];
+                A.edge_roff[voff + e] = ro;
+                int cnt = 0;
+                if (W->erow[e]) {
+                    unsigned long long m = W->erow[e];
+                    while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; A.edge_refs[ro++] = W->cid[r]; cnt++; }
+                } else {
+                    A.edge_refs[ro++] = W->eargmin[e];
+                    cnt = 1;
+                }
+                A.edge_nrefs[voff + e] = cnt;
+                if (W->eval[e]) {   // validated neuron = the single crossable plane of edge e
+                    unsigned long long m = W->erow[e];
+                    int kn = -1;
+                    while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; if (W->cid[r] < box0) kn = W->cid[r]; }
+                    A.val_buf[vo++] = kn;
                 }
             }
-            for (int si = 0; si < nsub; si++) {
-                for (int ti = -1; ti < nbr; ti++) {
-                    bool empty_sub = big ? (si == nb + 1) : (sub_mask[si] == 0);
-                    if (empty_sub && ti < 0) continue;
-                    if (ncd >= EMAXC) { atomicAdd(&A.overflow[0], 1ull); continue; }
-                    W->cd_edge[ncd] = e;
-                    W->cd_branch[ncd] = ti >= 0 ? brs[ti] : -1;
-                    int nf = 0;
-                    if (big) {
-                        if (si < nb) { W->cd_flip[ncd][0] = bits[si]; nf = 1; }
-                        else if (si == nb) { nf = -1; }   // all bits of the edge
+            A.pool_voff[pidx] = vloff;
+            A.pool_vn[pidx] = nvalid;
+            // ---------------- neighbour candidates (reference marching.py:152-186, 262-288)
+            int ncd = 0;
+            for (int e = 0; e < nr; e++) {
+                int nb = 0, nbr = 0, first = -1;   // first: global id of crossable[0]
+                if (W->erow[e]) {
+                    unsigned long long m = W->erow[e];
+                    while (m) {
+                        int r = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        int gid = W->cid[r];
+                        if (gid >= box0) continue;
+                        if (first < 0) first = gid;
+                        if (gid < c.NB) { if (nb < 64) W->tb[nb++] = gid; }
+                        else if (nbr < 64) W->tr[nbr++] = gid - c.NB;
+                    }
+                } else if (W->eargmin[e] < box0) {
+                    first = W->eargmin[e];
+                    if (first < c.NB) W->tb[nb++] = first; else W->tr[nbr++] = first - c.NB;
+                }
+                if (first < 0) continue;
+                const bool single = (nb == 1 && nbr == 0);
+                // subsets: combinations of sizes 0..nb (nb <= 3) or singles + full + () (nb > 3)
+                int nsub = 0, sub_mask[8];
+                const bool big = nb > 3;
+                if (big) {
+                    nsub = nb + 2;
+                } else {
+                    for (int k = 0; k <= nb; k++) {
+                        int idx[3] = {0, 1, 2};
+                        for (int i = 0; i < k; i++) idx[i] = i;
+                        for (;;) {
+                            int mk = 0;
+                            for (int i = 0; i < k; i++) mk |= 1 << idx[i];
+                            sub_mask[nsub++] = mk;
+                            int i = k - 1;
+                            while (i >= 0 && idx[i] == nb - k + i) i--;
+                            if (i < 0) break;
+                            idx[i]++;
+                            for (int tt = i + 1; tt < k; tt++) idx[tt] = idx[tt - 1] + 1;
+                        }
+                    }
+                }
+                for (int si = 0; si < nsub; si++) {
+                    for (int ti = -1; ti < nbr; ti++) {
+                        bool empty_sub = big ? (si == nb + 1) : (sub_mask[si] == 0);
+                        if (empty_sub && ti < 0) continue;
+                        if (ncd >= EMAXC) { atomicAdd(&A.overflow[0], 1ull); continue; }
+                        W->cd_edge[ncd] = e;
+                        W->cd_branch[ncd] = ti >= 0 ? W->tr[ti] : -1;
+                        W->cd_probe[ncd] = -1;
+                        int nf = 0;
+                        if (big) {
+                            if (si < nb) { W->cd_flip[ncd][0] = W->tb[si]; nf = 1; }
+                            else if (si == nb) { nf = -1; }   // all neuron bits of the edge
+                        } else {
+                            for (int i = 0; i < nb; i++)
+                                if (sub_mask[si] & (1 << i)) W->cd_flip[ncd][nf++] = W->tb[i];
+                        }
+                        W->cd_nflip[ncd] = nf;
+                        if (single) W->cd_probe[ncd] = e;   // the lone flip carries the probe record
+                        ncd++;
+                    }
+                }
+                // probe across crossable[0]: single-neuron edges -> probe record (resolved by the
+                // far cell's validation); anything else -> exact forward evaluation
+                double pn[3], po;
+                int pr = -1;
+                for (int r = 0; r < nC; r++)
+                    if (W->cid[r] == first) { pr = r; break; }
+                if (pr >= 0) { pn[0] = W->cn[pr][0]; pn[1] = W->cn[pr][1]; pn[2] = W->cn[pr][2]; }
+                else get_row(c, first, pn, po);
+                const double* p = W->fv[e];
+                const double* q = W->fv[(e + 1) % nr];
+                double pt[3] = {0.5 * (p[0] + q[0]) + A.probe_delta * pn[0], 0.5 * (p[1] + q[1]) + A.probe_delta * pn[1],
+                                0.5 * (p[2] + q[2]) + A.probe_delta * pn[2]};
+                if (!single) {
+                    unsigned long long pi = atomicAdd(A.n_probe, 1ull);
+                    if ((int64_t)pi < A.cap_probe) {
+                        A.probe_pts[pi * 3 + 0] = pt[0]; A.probe_pts[pi * 3 + 1] = pt[1]; A.probe_pts[pi * 3 + 2] = pt[2];
                     } else {
-                        for (int i = 0; i < nb; i++)
-                            if (sub_mask[si] & (1 << i)) W->cd_flip[ncd][nf++] = bits[i];
+                        atomicAdd(&A.overflow[1], 1ull);
                     }
-                    W->cd_nflip[ncd] = nf;
-                    ncd++;
+                } else {
+                    W->qv[e][0] = pt[0]; W->qv[e][1] = pt[1]; W->qv[e][2] = pt[2];   // probe point of edge e
                 }
             }
-            // probe across crossable[0] (the lowest non-box plane id of the edge)
-            int pr = ids[0];
-            double pn[3];
-            if (pr >= 0) { pn[0] = W->cn[pr][0]; pn[1] = W->cn[pr][1]; pn[2] = W->cn[pr][2]; }
-            else { double o; get_row(c, -1 - pr, pn, o); }
-            const double* p = W->fv[e];
-            const double* q = W->fv[(e + 1) % nr];
-            double mid[3] = {0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2])};
-            unsigned long long pi = atomicAdd(A.n_probe, 1ull);
-            if ((int64_t)pi < A.cap_probe) {
-                A.probe_pts[pi * 3 + 0] = mid[0] + A.probe_delta * pn[0];
-                A.probe_pts[pi * 3 + 1] = mid[1] + A.probe_delta * pn[1];
-                A.probe_pts[pi * 3 + 2] = mid[2] + A.probe_delta * pn[2];
-            } else {
-                atomicAdd(&A.overflow[1], 1ull);
-            }
+            W->n_cd = ncd;
+            W->cbase = (long long)atomicAdd(A.n_cand, (unsigned long long)ncd);
         }
-        W->n_cd = ncd;
-        W->cbase = (long long)atomicAdd(A.n_cand, (unsigned long long)ncd);
     }
     __syncwarp();
     const int ncd = W->n_cd;
+    if (ncd < 0) return;
     const int64_t cbase = W->cbase;
     // write candidate keys cooperatively: word w of candidate k
     for (int k = 0; k < ncd; k++) {
@@ -572,6 +675,20 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             }
             if (A.ensemble && w == A.KW - 1 && W->cd_branch[k] >= 0) word = (uint64_t)W->cd_branch[k];
             dst[w] = word;
+        }
+        // probe record: (emitted candidate index, neuron, point)
+        if (lane == 0 && W->cd_probe[k] >= 0) {
+            int e = W->cd_probe[k];
+            unsigned long long pi = atomicAdd(A.n_prec, 1ull);
+            if ((int64_t)pi < A.cap_prec) {
+                A.prec_cand[pi] = (int32_t)ci;
+                A.prec_k[pi] = W->cd_flip[k][0];
+                A.prec_pt[pi * 3 + 0] = W->qv[e][0];
+                A.prec_pt[pi * 3 + 1] = W->qv[e][1];
+                A.prec_pt[pi * 3 + 2] = W->qv[e][2];
+            } else {
+                atomicAdd(&A.overflow[1], 1ull);
+            }
         }
     }
 }

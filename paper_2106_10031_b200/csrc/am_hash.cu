@@ -25,7 +25,7 @@ __device__ __forceinline__ bool keys_equal(const uint64_t* a, const uint64_t* b,
 #define GRID_STRIDE(i, n) for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 __global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                              int64_t n_cap, int32_t* status, uint64_t* slot_out) {
+                              int64_t n_cap, int32_t* status, uint64_t* slot_out, int32_t* dup_ref) {
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(i, n) {
         const int64_t ci = idx ? idx[i] : i;
@@ -34,7 +34,7 @@ __global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx
         uint64_t fp = h >> 33;
         uint64_t pos = h & H.mask;
         const uint64_t mine = (fp << 33) | (1ull << 32) | (uint64_t)(uint32_t)i;
-        int32_t st = -1;  // table full (host keeps load factor <= 1/2, so unreachable)
+        int32_t st = -1, dref = -1;  // -1: table full (host keeps load factor <= 1/2, so unreachable)
         for (uint64_t probe = 0; probe <= H.mask; probe++) {
             uint64_t v = ld_volatile(H.table + pos);
             if (v == kEmpty) {
@@ -42,23 +42,26 @@ __global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx
                                                    (unsigned long long)kEmpty, (unsigned long long)mine);
                 if (old == kEmpty) {
                     st = 1;
-                    slot_out[i] = pos;
+                    slot_out[ci] = pos;
                     break;
                 }
                 v = old;
             }
             if ((v >> 33) == fp) {
                 uint32_t ref = (uint32_t)v;
-                const uint64_t* other = ((v >> 32) & 1ull) ? src + (int64_t)(idx ? idx[ref] : (int64_t)ref) * H.KW
-                                                           : H.pool + (int64_t)ref * H.KW;
+                const bool cand = (v >> 32) & 1ull;
+                const int64_t other_ci = idx ? idx[ref] : (int64_t)ref;
+                const uint64_t* other = cand ? src + other_ci * H.KW : H.pool + (int64_t)ref * H.KW;
                 if (keys_equal(key, other, H.KW)) {
                     st = 0;
+                    dref = cand ? (int32_t)(-2 - other_ci) : (int32_t)ref;
                     break;
                 }
             }
             pos = (pos + 1) & H.mask;
         }
-        status[i] = st;
+        status[ci] = st;
+        if (dup_ref) dup_ref[ci] = dref;
     }
 }
 
@@ -67,20 +70,21 @@ __global__ void k_hash_fixup(HashSet H, const uint64_t* src, const int32_t* idx,
                              int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail) {
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(i, n) {
-        if (status[i] != 1) {
-            if (pool_idx) pool_idx[i] = -1;
+        const int64_t ci = idx ? idx[i] : i;
+        if (status[ci] != 1) {
+            if (pool_idx) pool_idx[ci] = -1;
             continue;
         }
-        const int64_t ci = idx ? idx[i] : i;
         const uint64_t* key = src + ci * H.KW;
         unsigned long long p = atomicAdd(H.n_pool, 1ull);
         uint64_t* dst = H.pool + (int64_t)p * H.KW;
         for (int w = 0; w < H.KW; w++) dst[w] = key[w];
         H.pool_flags[p] = flag;
+        H.pool_vn[p] = -1;
         uint64_t fp = key_hash(key, H.KW) >> 33;
         __threadfence();
-        H.table[slot[i]] = (fp << 33) | (uint64_t)(uint32_t)p;
-        if (pool_idx) pool_idx[i] = (int32_t)p;
+        H.table[slot[ci]] = (fp << 33) | (uint64_t)(uint32_t)p;
+        if (pool_idx) pool_idx[ci] = (int32_t)p;
         if (queue) queue[atomicAdd(q_tail, 1ull)] = (int32_t)p;
     }
 }
@@ -115,8 +119,8 @@ static unsigned grid_for(int64_t n, int b) {
 }
 
 void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                        int64_t n_cap, int32_t* status, uint64_t* slot, cudaStream_t s) {
-    if (n_cap > 0) { k_hash_insert<<<grid_for(n_cap, 256), 256, 0, s>>>(H, src, idx, n_dev, n_cap, status, slot); ++g_launch_count; }
+                        int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, cudaStream_t s) {
+    if (n_cap > 0) { k_hash_insert<<<grid_for(n_cap, 256), 256, 0, s>>>(H, src, idx, n_dev, n_cap, status, slot, dup_ref); ++g_launch_count; }
 }
 void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                        int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
@@ -145,6 +149,8 @@ __global__ void k_take(IterState I) {
         long long room_cells = I.cap_cells - (long long)c[C_CELLS];
         long long room_verts = (I.cap_verts - (long long)c[C_VERTS]) / I.verts_per_cell;
         long long room_refs = (I.cap_refs - (long long)c[C_REFS]) / I.refs_per_cell;
+        long long room_pend = (I.cap_pend - (long long)c[C_NPEND]) / I.verts_per_cell;
+        long long room_val = (I.cap_val - (long long)c[C_NVAL]) / I.verts_per_cell;
         long long room_out = I.cap_outbox - (long long)c[C_NOUT];
         if (I.world > 1) room_out /= (1 + I.emit_per_cell);
         else room_out = nR;
@@ -154,11 +160,14 @@ __global__ void k_take(IterState I) {
         if (room_verts < lim) lim = room_verts;
         if (room_refs < lim) lim = room_refs;
         if (room_out < lim) lim = room_out;
+        if (room_pend < lim) lim = room_pend;
+        if (room_val < lim) lim = room_val;
         if (lim < 0) lim = 0;
         if (nR > lim) nR = lim;
         c[C_STALL] = (want > 0 && nR == 0) ? 1ull : 0ull;
         c[C_NR] = (unsigned long long)nR;
         c[C_NX] = 0; c[C_NF] = 0; c[C_NPROBE] = 0; c[C_NEMIT] = 0; c[C_NLOCAL] = 0;
+        c[C_NPREC] = 0; c[C_NKEEP] = 0; c[C_NPLOCAL] = 0;
         c[C_ITER] += nR > 0 ? 1ull : 0ull;
         s_nR = nR;
     }
@@ -197,7 +206,7 @@ __global__ void k_route_changed(const uint64_t* ckey, const int32_t* changed, co
         }
         unsigned long long j = atomicAdd(nX, 1ull);
         X[j] = (int32_t)b;
-        canon_pos[b] = (int32_t)j;
+        canon_pos[b] = 1;   // canonical insert result lands in status2[b] / canon_pool[b]
     }
 }
 
@@ -211,11 +220,11 @@ __global__ void k_frontier(const unsigned long long* n_dev, int64_t n_cap, const
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(b, n) {
         int32_t p = -1;
+        pool_flags[batch_pool[b]] |= 2u;   // composed (probe records aimed at it can resolve)
         if (!changed[b]) {
             p = batch_pool[b];
-        } else {
-            int32_t j = canon_pos[b];
-            if (j >= 0 && canon_status[j] == 1) p = canon_pool[j];
+        } else if (canon_pos[b] == 1 && canon_status[b] == 1) {
+            p = canon_pool[b];
         }
         if (p < 0) continue;
         unsigned long long tot = atomicAdd(ctr + C_TOTAL, 1ull);
@@ -245,13 +254,14 @@ __global__ void k_emit_finalize(unsigned long long* ctr) {
 // sharded march: emitted states owned elsewhere -> outbox; local ones -> index list
 __global__ void k_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW,
                                 int rank, int world, int32_t* local_idx, unsigned long long* n_local,
-                                uint64_t* outbox, unsigned long long* n_out) {
+                                uint64_t* outbox, unsigned long long* n_out, int32_t* remote_status) {
     const int64_t n = dev_count(ctr_n, n_cap);
     GRID_STRIDE(i, n) {
         const uint64_t* k = scratch + i * KW;
         if (key_owner(k, KW, world) == rank) {
             local_idx[atomicAdd(n_local, 1ull)] = (int32_t)i;
         } else {
+            if (remote_status) remote_status[i] = -5;   // owned elsewhere: probe records on it forward
             unsigned long long o = atomicAdd(n_out, 1ull);
             for (int w = 0; w < KW; w++) outbox[o * KW + w] = k[w];
         }
@@ -286,9 +296,9 @@ void launch_zero_probe_keys(uint64_t* scratch, const unsigned long long* ctr, in
 void launch_emit_finalize(unsigned long long* ctr, cudaStream_t s) { k_emit_finalize<<<1, 32, 0, s>>>(ctr); ++g_launch_count; }
 void launch_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW, int rank,
                           int world, int32_t* local_idx, unsigned long long* n_local, uint64_t* outbox,
-                          unsigned long long* n_out, cudaStream_t s) {
+                          unsigned long long* n_out, int32_t* remote_status, cudaStream_t s) {
     k_route_emitted<<<grid_for(n_cap, 256), 256, 0, s>>>(scratch, ctr_n, n_cap, KW, rank, world, local_idx, n_local,
-                                                          outbox, n_out);
+                                                          outbox, n_out, remote_status);
     ++g_launch_count;
 }
 
@@ -316,6 +326,106 @@ __global__ void k_open_edges(const int32_t* enr, const int64_t* roff, const int3
 void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
                        unsigned long long* out, cudaStream_t s) {
     if (nv > 0) { k_open_edges<<<grid_for(nv, 256), 256, 0, s>>>(enr, roff, refs, nv, box0, out); ++g_launch_count; }
+}
+
+// ------------------------------------------------------- probe records
+// resolve the target pool entry of this iteration's new probe records and append them to the
+// pending list (targets owned by another rank cannot be checked here: forward them)
+__global__ void k_prec_target(ProbeRecs R, const int32_t* status, const int32_t* dup_ref, const int32_t* pool_idx,
+                              unsigned long long* ctr, int64_t cap, double* probe_pts, int64_t cap_probe) {
+    const int64_t n = dev_count(ctr + C_NPREC, cap);
+    const int par = (int)(ctr[C_PPAR] & 1ull);
+    GRID_STRIDE(i, n) {
+        const int32_t ci = R.cand[i];
+        const int32_t st = status[ci];
+        int32_t t = -1;
+        if (st == 1) t = pool_idx[ci];
+        else if (st == 0) t = dup_ref[ci] >= 0 ? dup_ref[ci] : pool_idx[-2 - dup_ref[ci]];
+        if (t < 0) {   // remote or unresolvable: exact forward evaluation
+            unsigned long long q = atomicAdd(ctr + C_NPROBE, 1ull);
+            if ((int64_t)q < cap_probe) {
+                probe_pts[q * 3 + 0] = R.pt[i * 3 + 0]; probe_pts[q * 3 + 1] = R.pt[i * 3 + 1];
+                probe_pts[q * 3 + 2] = R.pt[i * 3 + 2];
+            } else atomicAdd(ctr + C_OVF1, 1ull);
+            continue;
+        }
+        unsigned long long j = atomicAdd(ctr + C_NPEND, 1ull);
+        if ((int64_t)j >= R.cap_pend) { atomicAdd(ctr + C_OVF1, 1ull); continue; }
+        R.pend_t[par][j] = t;
+        R.pend_k[par][j] = R.k[i];
+        R.pend_pt[par][j * 3 + 0] = R.pt[i * 3 + 0];
+        R.pend_pt[par][j * 3 + 1] = R.pt[i * 3 + 1];
+        R.pend_pt[par][j * 3 + 2] = R.pt[i * 3 + 2];
+    }
+}
+
+// pending probe records whose target has been processed: dropped if the target validated the
+// mirrored probe of that neuron (the probe provably lands in the target cell), otherwise
+// forward-evaluated; targets still queued keep the record for a later iteration
+__global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsigned long long* ctr, int64_t cap,
+                          double* probe_pts, int64_t cap_probe) {
+    const int64_t n = dev_count(ctr + C_NPEND, cap);
+    const int par = (int)(ctr[C_PPAR] & 1ull);
+    GRID_STRIDE(i, n) {
+        const int32_t t = R.pend_t[par][i];
+        const int32_t vn = H.pool_vn[t];
+        const uint32_t fl = H.pool_flags[t];
+        bool forward = false;
+        if (vn >= 0) {
+            const int32_t k = R.pend_k[par][i];
+            const int64_t off = H.pool_voff[t];
+            bool found = false;
+            for (int q = 0; q < vn; q++) found |= val_buf[off + q] == k;
+            forward = !found;
+        } else if (fl & 2u) {
+            forward = true;   // composed but no face (canonical elsewhere / capped): exact evaluation
+        } else {
+            unsigned long long j = atomicAdd(ctr + C_NKEEP, 1ull);
+            R.pend_t[par ^ 1][j] = t;
+            R.pend_k[par ^ 1][j] = R.pend_k[par][i];
+            R.pend_pt[par ^ 1][j * 3 + 0] = R.pend_pt[par][i * 3 + 0];
+            R.pend_pt[par ^ 1][j * 3 + 1] = R.pend_pt[par][i * 3 + 1];
+            R.pend_pt[par ^ 1][j * 3 + 2] = R.pend_pt[par][i * 3 + 2];
+            continue;
+        }
+        if (forward) {
+            unsigned long long q = atomicAdd(ctr + C_NPROBE, 1ull);
+            if ((int64_t)q < cap_probe) {
+                probe_pts[q * 3 + 0] = R.pend_pt[par][i * 3 + 0]; probe_pts[q * 3 + 1] = R.pend_pt[par][i * 3 + 1];
+                probe_pts[q * 3 + 2] = R.pend_pt[par][i * 3 + 2];
+            } else atomicAdd(ctr + C_OVF1, 1ull);
+        }
+    }
+}
+
+__global__ void k_pend_finalize(unsigned long long* ctr) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        ctr[C_PREC_TOTAL] += ctr[C_NPREC];
+        ctr[C_PROBES_TOTAL] += ctr[C_NPROBE];
+        ctr[C_NPEND] = ctr[C_NKEEP];
+        ctr[C_PPAR] ^= 1ull;
+    }
+}
+
+__global__ void k_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap) {
+    const int64_t n = dev_count(n_dev, cap) * KW;
+    GRID_STRIDE(i, n) keys[i] = 0;
+}
+
+void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t* dup_ref, const int32_t* pool_idx,
+                        unsigned long long* ctr, int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s) {
+    k_prec_target<<<grid_for(cap, 256), 256, 0, s>>>(R, status, dup_ref, pool_idx, ctr, cap, probe_pts, cap_probe);
+    ++g_launch_count;
+}
+void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr, int64_t cap,
+                    double* probe_pts, int64_t cap_probe, cudaStream_t s) {
+    k_resolve<<<grid_for(cap, 256), 256, 0, s>>>(R, H, val_buf, ctr, cap, probe_pts, cap_probe);
+    ++g_launch_count;
+}
+void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s) { k_pend_finalize<<<1, 32, 0, s>>>(ctr); ++g_launch_count; }
+void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, cudaStream_t s) {
+    k_zero_keys<<<grid_for(cap * KW, 256), 256, 0, s>>>(keys, n_dev, KW, cap);
+    ++g_launch_count;
 }
 
 // owner rank of each key (outbox grouping)

@@ -89,7 +89,8 @@ int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t col
 // device counters shared by the iteration kernels
 enum Ctr {
     C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_OVF0, C_OVF1, C_CAPPED, C_TOTAL, C_QHEAD, C_QTAIL, C_NR, C_NX,
-    C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_N
+    C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_NPREC, C_NPEND, C_PPAR,
+    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_N
 };
 
 // hash set (am_hash.cu)
@@ -97,13 +98,17 @@ struct HashSet {
     uint64_t* table;      // slots
     uint64_t mask;        // capacity - 1
     uint64_t* pool;       // [cap_pool][KW]
-    uint32_t* pool_flags; // bit0 visited-canonical
+    uint32_t* pool_flags; // bit0 visited cell, bit1 composed
+    int32_t* pool_vn;     // validated-neuron count of a visited cell (-1: no face yet)
+    int64_t* pool_voff;   // offset of its validated-neuron list
     unsigned long long* n_pool;  // device counter
     int64_t cap_pool;
     int KW;
 };
+// per-item outputs are indexed by source item ci (idx[i] or i): status 1 new / 0 present,
+// slot (new), dup_ref (present: pool index, or -2 - launch index of the in-flight winner)
 void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                        int64_t n_cap, int32_t* status, uint64_t* slot, cudaStream_t s);
+                        int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, cudaStream_t s);
 void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                        int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
                        int32_t* queue, unsigned long long* q_tail, cudaStream_t s);
@@ -114,10 +119,25 @@ struct IterState {
     unsigned long long* ctr;
     const int32_t* queue;
     int32_t* batch_pool;
-    long long B, cap_pool, tcap, cap_cells, cap_verts, cap_refs, cap_outbox;
+    long long B, cap_pool, tcap, cap_cells, cap_verts, cap_refs, cap_outbox, cap_pend, cap_val;
     long long emit_per_cell, verts_per_cell, refs_per_cell;
     int world;
 };
+// probe records: (target pool entry, neuron, point); double-buffered by parity counter
+struct ProbeRecs {
+    int32_t* cand;        // [cap] emitted-candidate index of the flip the probe belongs to
+    int32_t* k;           // [cap] crossed neuron
+    double* pt;           // [cap][3]
+    int32_t* pend_t[2];   // pending: target pool index
+    int32_t* pend_k[2];
+    double* pend_pt[2];
+    int64_t cap_pend;
+};
+void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t* dup_ref, const int32_t* pool_idx,
+                        unsigned long long* ctr, int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s);
+void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr,
+                    int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s);
+void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s);
 void launch_take(const IterState& I, cudaStream_t s);
 void launch_gather_batch(const uint64_t* pool, const int32_t* batch_pool, const unsigned long long* n_dev,
                          int64_t n_cap, int KW, uint64_t* ckey, int32_t* changed, int32_t* canon_pos, cudaStream_t s);
@@ -128,11 +148,12 @@ void launch_frontier(const unsigned long long* n_dev, int64_t n_cap, const int32
                      const int32_t* canon_pos, const int32_t* canon_status, const int32_t* canon_pool,
                      uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* ctr,
                      long long max_cells, cudaStream_t s);
+void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, cudaStream_t s);
 void launch_zero_probe_keys(uint64_t* scratch, const unsigned long long* ctr, int KW, int64_t cap, cudaStream_t s);
 void launch_emit_finalize(unsigned long long* ctr, cudaStream_t s);
 void launch_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW, int rank,
                           int world, int32_t* local_idx, unsigned long long* n_local, uint64_t* outbox,
-                          unsigned long long* n_out, cudaStream_t s);
+                          unsigned long long* n_out, int32_t* remote_status, cudaStream_t s);
 void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst, cudaStream_t s);
 void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
                        unsigned long long* out, cudaStream_t s);
@@ -173,6 +194,17 @@ struct FaceArgs {
     unsigned long long* n_probe;
     int64_t cap_probe;
     unsigned long long* overflow;  // counters: [0] C-set/polygon overflow, [1] capacity overflow
+    // probe records of single-neuron edges + validated mirrored probes
+    int32_t* prec_cand;
+    int32_t* prec_k;
+    double* prec_pt;
+    unsigned long long* n_prec;
+    int64_t cap_prec;
+    int32_t* val_buf;
+    unsigned long long* n_val;
+    int64_t cap_val;
+    int32_t* pool_vn;
+    int64_t* pool_voff;
 };
 constexpr int kEmitFlipsPerCell = 48;   // face kernel EMAXC
 constexpr int kVertsPerCell = 64;       // face kernel QMAX

@@ -169,5 +169,5 @@ class Engine:
         _native.check(self.lib.am_stats(self.h, s.ctypes.data), "am_stats")
         keys = ("compose_ms", "face_ms", "compose_flops", "face_bytes", "composed", "faced", "batch",
                 "flops_per_cell", "launches", "iterations", "probe_ms", "probe_flops", "probes",
-                "flops_per_point")
+                "flops_per_point", "probes_forwarded", "probe_records")
         return dict(zip(keys, (float(x) for x in s)))
