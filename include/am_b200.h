@@ -134,6 +134,8 @@ int am_stats(am_engine *e, double *h_out16);
 int am_set_timing(am_engine *e, int enabled);
 /* measured fp64 peaks of this device: h_out2[0] DMMA (tensor) TFLOP/s, [1] DFMA TFLOP/s */
 int am_bench_fp64_peak(int device, double *h_out2);
+/* face-kernel instrumentation counters (64; non-zero only in -DAM_FACE_STATS builds), reset on read */
+int am_debug_counters(am_engine *e, uint64_t *h_out64);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,7 @@ SIGNATURES = {
     "am_stats": (ctypes.c_int, [P, P]),
     "am_set_timing": (ctypes.c_int, [P, ctypes.c_int]),
     "am_bench_fp64_peak": (ctypes.c_int, [ctypes.c_int, P]),
+    "am_debug_counters": (ctypes.c_int, [P, P]),
 }
 
 _lib = None

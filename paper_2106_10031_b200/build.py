@@ -35,6 +35,7 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """AM_BUILD_FLAGS (space-separated) are appended to every nvcc compile (e.g. -DAM_FACE_STATS)."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, "am_internal.h"),
                    os.path.join(os.path.dirname(HERE), "include", "am_b200.h")]
@@ -46,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for name, extra in SOURCES.items():
         obj = os.path.join(objdir, name.replace(".cu", ".o"))
-        cmd = [nvcc()] + ARCH + COMMON + extra + ["-c", os.path.join(CSRC, name), "-o", obj]
+        cmd = ([nvcc()] + ARCH + COMMON + extra + os.environ.get("AM_BUILD_FLAGS", "").split()
+               + ["-c", os.path.join(CSRC, name), "-o", obj])
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

@@ -171,7 +171,7 @@ static int num_sms() {
 void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
     int64_t total = L.n_cap * L.st.n_out;
     if (total <= 0) return;
-    int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+    int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : 8));
     if (C == 4) { k_input_step<4><<<(unsigned)blocks, 256, 0, s>>>(L); ++g_launch_count; }
     else { k_input_step<1><<<(unsigned)blocks, 256, 0, s>>>(L); ++g_launch_count; }
 }
@@ -458,7 +458,7 @@ void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const
     if (L.n_cap <= 0) return;
     int64_t cols = L.n_cap * C;
     int64_t tiles = ((cols + BN - 1) / BN) * ((L.st.n_out + BM - 1) / BM);
-    int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * 5);
+    int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : 5));
     size_t smem = sizeof(GemmSmem) + 1024;
     if (C == 4) {
         static bool init = false;

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -119,12 +120,14 @@ struct am_engine {
     DBuf<uint32_t> pool_flags;
     DBuf<int32_t> queue, pool_vn;
     DBuf<int64_t> pool_voff;
+    DBuf<double> pool_hint, ckey_hint, emit_hint;
+    DBuf<unsigned long long> dbg;   // face-kernel instrumentation counters (AM_FACE_STATS builds)
     uint64_t tcap = 0;
     // counters (device) + host mirror
     DBuf<unsigned long long> ctr;
     unsigned long long hctr[C_N] = {0};
     // batch buffers (capacity B)
-    int64_t B = 0, E = 0, PB = 0;   // batch cells, emitted keys, probe points per iteration
+    int64_t B = 0, E = 0, PB = 0, PR = 0;   // batch cells, emitted keys, probe points, probe records
     DBuf<double> Z, faces;
     DBuf<uint64_t> ckey, slot, slot2, scratch, outbox;
     DBuf<int32_t> changed, status, status2, canon_pos, canon_pool, X, f_items, f_pool, batch_pool, local_idx;
@@ -150,6 +153,7 @@ struct am_engine {
     cudaGraphExec_t gexec = nullptr;
     bool graph_valid = false;
     int graph_batch = 8;
+    int grid_cap = 0;    // >0: CTAs per SM for persistent GEMM launches
     unsigned long long graph_kernels = 0;
     // stats
     bool timing = false;
@@ -193,6 +197,7 @@ static HashSet hs(am_engine* e) {
     H.pool_flags = e->pool_flags.p;
     H.pool_vn = e->pool_vn.p;
     H.pool_voff = e->pool_voff.p;
+    H.pool_hint = e->pool_hint.p;
     H.n_pool = e->ctr.p + C_POOL;
     H.cap_pool = e->pool.n / e->KW;
     H.KW = e->KW;
@@ -211,6 +216,7 @@ static int ensure_hash(am_engine* e, int64_t extra) {
         CK(e->pool_flags.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
         CK(e->pool_vn.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
         CK(e->pool_voff.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
+        CK(e->pool_hint.reserve(e->pool.n / e->KW * 4, e->stream, true, np * 4, &moved));
     }
     CK(e->queue.reserve(e->pool.n / e->KW, e->stream, true, (int64_t)e->hctr[C_QTAIL], &moved));
     if ((int64_t)e->tcap < 2 * need) {
@@ -355,11 +361,12 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // batch size from the per-iteration memory budget: compose planes + worst-case probe
     // activations + emitted keys per batch cell
     int64_t budget = e->P.mem_budget > 0 ? e->P.mem_budget : (int64_t)4 << 30;
-    int64_t per = (int64_t)e->zs * 32 + (int64_t)kVertsPerCell * e->zs * 8 + emit_per_cell() * e->KW * 8 * 2 +
-                  e->M * 32 + 256;
+    int64_t per = (int64_t)e->zs * 32 + (int64_t)e->zs * 8 + emit_per_cell() * e->KW * 8 * 2 +
+                  (int64_t)kVertsPerCell * 40 + e->M * 32 + 256;
     e->B = e->P.batch_cells > 0 ? e->P.batch_cells : std::max<int64_t>(256, std::min<int64_t>(budget / per, 16384));
     e->E = e->B * emit_per_cell();
-    e->PB = e->B * kVertsPerCell;
+    e->PB = std::max<int64_t>(e->B, 4096);   // exact probe evaluations per iteration (overflow waits in pending)
+    e->PR = e->B * kVertsPerCell;           // probe records per iteration (one per edge at most)
     if (e->P.max_cells <= 0) e->P.max_cells = INT64_C(10000000);
     cudaStream_t s = e->stream;
     CK(e->Z.reserve(e->B * e->zs * 4, s));
@@ -380,12 +387,16 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->pstatus.reserve(e->PB, s));
     CK(e->emit_dup.reserve(e->E, s));
     CK(e->emit_pool.reserve(e->E, s));
-    CK(e->prec_cand.reserve(e->PB, s));
-    CK(e->prec_k.reserve(e->PB, s));
-    CK(e->prec_pt.reserve(e->PB * 3, s));
+    CK(e->emit_hint.reserve(e->E * 4, s));
+    CK(e->ckey_hint.reserve(e->B * 4, s));
+    CK(e->prec_cand.reserve(e->PR, s));
+    CK(e->prec_k.reserve(e->PR, s));
+    CK(e->prec_pt.reserve(e->PR * 3, s));
     CK(e->outbox.reserve(e->KW, s));
     CK(e->ctr.reserve(C_N, s));
     CK(cudaMemset(e->ctr.p, 0, C_N * sizeof(unsigned long long)));
+    CK(e->dbg.reserve(64, s));
+    CK(cudaMemset(e->dbg.p, 0, 64 * sizeof(unsigned long long)));
     for (int i = 0; i < 6; i++) cudaEventCreate(&e->ev[i]);
     int rc = ensure_hash(e, 4 * e->B * (1 + emit_per_cell()));
     if (!rc) rc = ensure_results(e, 4 * e->B);
@@ -400,7 +411,8 @@ extern "C" int am_engine_destroy(am_engine* e) {
     if (e->gexec) cudaGraphExecDestroy(e->gexec);
     if (e->graph) cudaGraphDestroy(e->graph);
     DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx,
-                           &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1]};
+                           &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1], &e->pool_hint,
+                           &e->ckey_hint, &e->emit_hint};
     for (auto* b : dbl) b->release();
     DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->ckey, &e->slot, &e->slot2, &e->scratch, &e->outbox,
                              &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres, &e->pkeys, &e->pslot};
@@ -453,6 +465,7 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsig
         L.n_cap = n_cap;
         L.KW = e->KW;
         L.zs = e->zs;
+        L.grid_cap = e->grid_cap;
         if (L.st.flags & AM_STEP_FIRST) launch_input_step(L, C, e->stream);
         else launch_gemm_step(L, C, &e->tmW[s], e->tmV_ok[s] ? &e->tmV[s] : nullptr, e->stream);
     }
@@ -542,7 +555,8 @@ static int launch_iteration(am_engine* e) {
     const bool multi = e->P.world > 1;
 
     launch_take(I, s);
-    launch_gather_batch(e->pool.p, e->batch_pool.p, c + C_NR, B, e->KW, e->ckey.p, e->changed.p, e->canon_pos.p, s);
+    launch_gather_batch(e->pool.p, e->pool_hint.p, e->batch_pool.p, c + C_NR, B, e->KW, e->ckey.p, e->ckey_hint.p,
+                        e->changed.p, e->canon_pos.p, s);
     if (tm) cudaEventRecord(e->ev[0], s);
     RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B));
     if (tm) cudaEventRecord(e->ev[1], s);
@@ -550,11 +564,12 @@ static int launch_iteration(am_engine* e) {
                          e->outbox.p, c + C_NOUT, e->canon_pos.p, s);
     launch_hash_insert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, nullptr, s);
     launch_hash_fixup(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, 0u, e->canon_pool.p, nullptr,
-                      nullptr, s);
+                      nullptr, e->ckey_hint.p, s);
     launch_frontier(c + C_NR, B, e->changed.p, e->batch_pool.p, e->canon_pos.p, e->status2.p, e->canon_pool.p,
                     e->pool_flags.p, e->f_items.p, e->f_pool.p, c, (long long)e->P.max_cells, s);
     FaceArgs a;
     a.Z = e->Z.p; a.faces = e->faces.p; a.keys = e->ckey.p; a.items = e->f_items.p; a.pool_idx = e->f_pool.p;
+    a.hints = e->ckey_hint.p; a.emit_hint = e->emit_hint.p;
     a.n_dev = c + C_NF; a.n_cap = B;
     a.NB = e->NB; a.M = e->M; a.KW = e->KW; a.zs = e->zs; a.ensemble = e->ensemble;
     for (int k = 0; k < 3; k++) { a.lo[k] = e->P.bbox_lo[k]; a.hi[k] = e->P.bbox_hi[k]; }
@@ -568,9 +583,10 @@ static int launch_iteration(am_engine* e) {
     a.probe_pts = e->probe_pts.p; a.n_probe = c + C_NPROBE; a.cap_probe = e->PB;
     a.overflow = c + C_OVF0;
     a.prec_cand = e->prec_cand.p; a.prec_k = e->prec_k.p; a.prec_pt = e->prec_pt.p; a.n_prec = c + C_NPREC;
-    a.cap_prec = e->PB;
+    a.cap_prec = e->PR;
     a.val_buf = e->val_buf.p; a.n_val = c + C_NVAL; a.cap_val = e->val_buf.n;
     a.pool_vn = e->pool_vn.p; a.pool_voff = e->pool_voff.p;
+    a.dbg = e->dbg.p;
     if (tm) cudaEventRecord(e->ev[2], s);
     launch_face(a, s);
     if (tm) cudaEventRecord(e->ev[3], s);
@@ -581,30 +597,33 @@ static int launch_iteration(am_engine* e) {
         launch_hash_insert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p,
                            e->emit_dup.p, s);
         launch_hash_fixup(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, 0u,
-                          e->emit_pool.p, e->queue.p, c + C_QTAIL, s);
+                          e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
     } else {
         launch_hash_insert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, e->emit_dup.p, s);
         launch_hash_fixup(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, 0u, e->emit_pool.p,
-                          e->queue.p, c + C_QTAIL, s);
+                          e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
     }
     // probe records: target entries -> pending; pending with processed targets -> drop / forward
-    launch_prec_target(R, e->status.p, e->emit_dup.p, e->emit_pool.p, c, e->PB, e->probe_pts.p, e->PB, s);
+    launch_prec_target(R, e->status.p, e->emit_dup.p, e->emit_pool.p, c, e->PR, e->probe_pts.p, e->PB, s);
     launch_resolve(R, H, e->val_buf.p, c, R.cap_pend, e->probe_pts.p, e->PB, s);
     launch_pend_finalize(c, s);
     // exact forward evaluation of the remaining probes
     launch_zero_keys(e->pkeys.p, c + C_NPROBE, e->KW, e->PB, s);
-    RC(forward(e, e->probe_pts.p, nullptr, e->pkeys.p, nullptr, e->pZ.p, c + C_NPROBE, e->PB));
+    e->grid_cap = 2;   // probes are rare after validation: a small persistent grid per layer
+    int frc = forward(e, e->probe_pts.p, nullptr, e->pkeys.p, nullptr, e->pZ.p, c + C_NPROBE, e->PB);
+    e->grid_cap = 0;
+    RC(frc);
     if (tm) cudaEventRecord(e->ev[4], s);
     if (multi) {
         launch_route_emitted(e->pkeys.p, c + C_NPROBE, e->PB, e->KW, e->P.rank, e->P.world, e->local_idx.p,
                              c + C_NPLOCAL, e->outbox.p, c + C_NOUT, nullptr, s);
         launch_hash_insert(H, e->pkeys.p, e->local_idx.p, c + C_NPLOCAL, e->PB, e->pstatus.p, e->pslot.p, nullptr, s);
         launch_hash_fixup(H, e->pkeys.p, e->local_idx.p, c + C_NPLOCAL, e->PB, e->pstatus.p, e->pslot.p, 0u, nullptr,
-                          e->queue.p, c + C_QTAIL, s);
+                          e->queue.p, c + C_QTAIL, nullptr, s);
     } else {
         launch_hash_insert(H, e->pkeys.p, nullptr, c + C_NPROBE, e->PB, e->pstatus.p, e->pslot.p, nullptr, s);
         launch_hash_fixup(H, e->pkeys.p, nullptr, c + C_NPROBE, e->PB, e->pstatus.p, e->pslot.p, 0u, nullptr,
-                          e->queue.p, c + C_QTAIL, s);
+                          e->queue.p, c + C_QTAIL, nullptr, s);
     }
     CK(cudaGetLastError());
     return AM_OK;
@@ -652,6 +671,9 @@ static int timed_iteration(am_engine* e) {
     e->n_comp_cells += nR;
     e->n_face_cells += nF;
     e->n_probes += nP;
+    if (getenv("AM_TRACE_ITERS"))
+        fprintf(stderr, "iter %lld nR %.0f nF %.0f compose %.1f us face %.1f us probe-stage %.1f us\n",
+                (long long)e->hctr[C_ITER], nR, nF, a * 1e3, b * 1e3, c * 1e3);
     e->face_bytes += nF * (e->NB * 32.0 + e->M * 32.0 + e->KW * 8.0);
     return AM_OK;
 }
@@ -697,11 +719,11 @@ static int push_keys(am_engine* e, const uint64_t* d_keys, int64_t n) {
         launch_hash_insert(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, nullptr,
                            e->stream);
         launch_hash_fixup(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, 0u, nullptr,
-                          e->queue.p, e->ctr.p + C_QTAIL, e->stream);
+                          e->queue.p, e->ctr.p + C_QTAIL, nullptr, e->stream);
     } else {
         launch_hash_insert(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, nullptr, e->stream);
         launch_hash_fixup(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, 0u, nullptr, e->queue.p,
-                          e->ctr.p + C_QTAIL, e->stream);
+                          e->ctr.p + C_QTAIL, nullptr, e->stream);
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(e->stream));
@@ -924,6 +946,14 @@ extern "C" int am_result_copy(am_engine* e, uint64_t* h_keys, int32_t* h_nverts,
         }
         vo += n;
     }
+    return AM_OK;
+}
+
+// face-kernel instrumentation counters (non-zero only in AM_FACE_STATS builds); reset after read
+extern "C" int am_debug_counters(am_engine* e, uint64_t* h_out64) {
+    if (!e) return fail(AM_ERR_ARG, "null engine");
+    CK(cudaMemcpy(h_out64, e->dbg.p, 64 * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(e->dbg.p, 0, 64 * 8));
     return AM_OK;
 }
 

@@ -37,40 +37,66 @@
 
 namespace am {
 
+// optional per-cell instrumentation (build with -DAM_FACE_STATS): A.dbg[0..] accumulates
+// cells, clip events (pass 1 / pass 2), C' size, raw vertices, polygon vertices, cycles,
+// and a log2 histogram of per-cell cycles in dbg[16..40)
+#ifdef AM_FACE_STATS
+#define FSTAT(i, v) do { if (lane == 0 && A.dbg) atomicAdd(&A.dbg[i], (unsigned long long)(v)); } while (0)
+#else
+#define FSTAT(i, v) do { } while (0)
+#endif
+
 constexpr int VMAX = 32;   // clip polygon capacity (one lane per vertex)
 constexpr int CMAX = 64;   // candidate plane set capacity (uint64 masks)
 constexpr int QMAX = 64;   // accepted raw vertices
-constexpr int EMAXC = 48;  // candidate descriptors per cell
+constexpr int EMAXC = 32;  // candidate descriptors per cell
 constexpr int FW = 4;      // warps per CTA
+constexpr int NMAX = 96;   // hinted path: rows near the hint point
 constexpr double kCDelta = 1e-10;
 constexpr double kValMargin = 1e-11;   // sign margin (unit and raw values) for probe validation
 constexpr double kTinyNorm = 1e-6;     // rows this thin make validation unreliable
 
-struct FaceWarp {
-    double ps[2][VMAX], pt[2][VMAX];
-    double cn[CMAX][5];             // unit row (n, o) + raw normal norm
-    int cid[CMAX];
-    unsigned long long core;        // C rows within tol of P_tol (pair / incident candidates)
-    int tb[64], tr[64];             // scratch: neuron bits / branch targets of one edge
-    double qv[QMAX][3];
-    unsigned long long qs[QMAX];
-    double rv[QMAX][3];
-    double rf[QMAX][3];
+// phase-private scratch: near rows (hinted clipping) and polygon assembly never overlap
+struct NearPhase {
+    int nl[NMAX];                   // near rows (global ids, ascending)
+    double nd[NMAX];                // |value at the hint point|
+    double na[NMAX], nb[NMAX], ng[NMAX];   // 2-D rows (unshifted)
+    int nord[NMAX];                 // clipping order (by distance)
+};
+struct PolyPhase {
+    double qv[QMAX][3];             // accepted raw vertices (triu order)
+    unsigned long long qs[QMAX];    // their incident-plane sets (C-row masks)
+    double rv[QMAX][3];             // weld-cluster representatives (lexicographic minimum)
+    int rfi[QMAX];                  // first member of each cluster (index into qv)
     unsigned long long rs[QMAX];
     double ang[QMAX];
     int ord[QMAX];
-    double fv[QMAX][3];           // final loop
+    double fv[QMAX][3];             // final loop
     unsigned long long fs[QMAX];
+};
+
+struct FaceWarp {
+    double ps[2][VMAX], pt[2][VMAX];
+    double cn[NMAX][5];             // unit row (n, o) + raw normal norm (near rows, then C')
+    int cid[NMAX];
+    unsigned long long core;        // C rows within tol of P_tol (pair / incident candidates)
+    int tb[32], tr[32];             // scratch: neuron bits / branch targets of one edge
+    union {
+        NearPhase np;
+        PolyPhase pp;
+    } u;
     unsigned long long erow[QMAX];  // per-edge C-row mask of the transition planes
     int eargmin[QMAX];              // per-edge global row when the mask is empty (argmin fallback)
+    int eval[QMAX];                 // per edge: 1 if the mirrored probe validated
+    int efirst[QMAX], eprec[QMAX];  // per edge: crossable[0], probe-record slot
     // candidate descriptors: flip bits (<= 4, or -1 = "all bits of edge e") and branch target
     int cd_edge[EMAXC], cd_nflip[EMAXC], cd_flip[EMAXC][4], cd_branch[EMAXC];
     int cd_probe[EMAXC];            // >= 0: this flip carries the probe record of edge cd_probe
+    long long pbase;
+    long long cbase;
+    double diam;                    // polygon diameter bound (hint radius for the neighbours)
     int n_cd;
     int status;
-    int risky;
-    long long cbase;
-    int eval[QMAX];                 // per edge: 1 if the mirrored probe validated
 };
 
 struct Ctx {
@@ -118,6 +144,53 @@ __device__ __forceinline__ bool get_row(const Ctx& c, int gr, double n[3], doubl
 
 __device__ __forceinline__ double dot3(const double* a, const double* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
 
+// raw functional of global plane id gr (not normalised, not oriented); kind: 0 neuron,
+// 1 branch (valid unless it is the cell's own branch), 2 box, -1 none
+struct RawRow { double x, y, z, c; int kind; };
+__device__ __forceinline__ RawRow load_raw(const Ctx& c, int gr) {
+    RawRow r;
+    if (gr < c.NB) {
+        const double2* p = reinterpret_cast<const double2*>(c.Z + (int64_t)gr * 4);
+        double2 a = __ldg(p), b = __ldg(p + 1);
+        r.x = a.x; r.y = a.y; r.z = b.x; r.c = b.y; r.kind = 0;
+    } else if (gr < c.NB + c.M) {
+        int t = gr - c.NB;
+        r.kind = (!c.ensemble || t == c.branch) ? -1 : 1;
+        if (r.kind == 1) {
+            const double* ft = c.faces + t * 4;
+            const double* fj = c.faces + c.branch * 4;
+            r.x = ft[0] - fj[0]; r.y = ft[1] - fj[1]; r.z = ft[2] - fj[2]; r.c = ft[3] - fj[3];
+        } else {
+            r.x = r.y = r.z = r.c = 0.0;
+        }
+    } else if (gr < c.K) {
+        int k = gr - c.NB - c.M, ax = k >> 1;
+        r.x = r.y = r.z = 0.0;
+        double sg = (k & 1) ? -1.0 : 1.0;
+        if (ax == 0) r.x = sg; else if (ax == 1) r.y = sg; else r.z = sg;
+        r.c = (k & 1) ? c.lo[ax] : -c.hi[ax];
+        r.kind = 2;
+    } else {
+        r.x = r.y = r.z = r.c = 0.0;
+        r.kind = -1;
+    }
+    return r;
+}
+// 2-D projection (a, b, g) of the oriented unit row in the face-plane frame, with one
+// reciprocal per row (the streaming passes only need it to ~1 ulp); *nrm = raw norm
+__device__ __forceinline__ bool row2d(const Ctx& c, int gr, const RawRow& r, const double U[3], const double V[3],
+                                      const double P0[3], double& a2, double& b2, double& g2, double& nrm) {
+    if (r.kind < 0) { nrm = 0.0; return false; }
+    nrm = sqrt((r.x * r.x + r.y * r.y) + r.z * r.z);
+    if (r.kind != 2 && !(nrm > kDegen)) return false;
+    double s = 1.0 / nrm;
+    if (r.kind == 0 && key_bit(c.key, gr)) s = -s;
+    a2 = ((r.x * U[0] + r.y * U[1]) + r.z * U[2]) * s;
+    b2 = ((r.x * V[0] + r.y * V[1]) + r.z * V[2]) * s;
+    g2 = (((r.x * P0[0] + r.y * P0[1]) + r.z * P0[2]) + r.c) * s;
+    return true;
+}
+
 // 3x3 LU with partial pivoting, same operation order as oracle solve3 (LAPACK getf2/getrs)
 __device__ double solve3(const double Min[9], const double rin[3], double x[3]) {
     double a[9], b[3];
@@ -163,6 +236,11 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int item = A.items[fi];
+#ifdef AM_FACE_STATS
+    const long long t_start = clock64();
+    int n_clip1 = 0, n_clip2 = 0;
+#endif
+    (void)0;
 
     Ctx c;
     c.Z = A.Z + (int64_t)item * A.zs * 4;
@@ -196,101 +274,321 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
 
     int nv = 0, cur = 0;
     int status = face_ok ? 0 : 1;  // 0 ok, 1 empty, 2 overflow
-    if (status == 0) {
-        // initial square, then clip: box rows first, then neurons, then branch rows
+    double sc = 0.0, tc = 0.0, rho = 0.0;   // bounding circle of the current polygon
+
+    // warp-parallel Sutherland-Hodgman step by (ca, cb, cg) (<= 0 inside), one lane per vertex;
+    // keeps the bounding circle current.  Returns false if nothing was cut.
+    auto clip = [&](double ca, double cb, double cg) -> bool {
+        double si = 0, ti = 0, di = 0;
+        if (lane < nv) { si = W->ps[cur][lane]; ti = W->pt[cur][lane]; di = ca * si + cb * ti + cg; }
+        int nx = lane + 1 == nv ? 0 : lane + 1;
+        double sj = __shfl_sync(full, si, nx & 31), tj = __shfl_sync(full, ti, nx & 31),
+               dj = __shfl_sync(full, di, nx & 31);
+        bool in_i = di <= 0.0, in_j = dj <= 0.0;
+        if (!__any_sync(full, lane < nv && !in_i)) return false;
+        int cnt = lane < nv ? (in_i ? 1 : 0) + (in_i != in_j ? 1 : 0) : 0;
+        int pre = cnt;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            int y = __shfl_up_sync(full, pre, o2);
+            if (lane >= o2) pre += y;
+        }
+        int total = __shfl_sync(full, pre, 31);
+        pre -= cnt;
+        if (total > VMAX) { status = 2; return true; }
+        int dst = cur ^ 1;
+        double ns = 0.0, nt = 0.0;
+        if (lane < nv) {
+            int w = pre;
+            if (in_i) { W->ps[dst][w] = si; W->pt[dst][w] = ti; ns += si; nt += ti; w++; }
+            if (in_i != in_j) {
+                double lam = di / (di - dj);
+                double xs = si + lam * (sj - si), xt = ti + lam * (tj - ti);
+                W->ps[dst][w] = xs;
+                W->pt[dst][w] = xt;
+                ns += xs; nt += xt;
+            }
+        }
+        __syncwarp();
+        cur = dst;
+        nv = total;
+        if (nv < 3) { status = 1; return true; }
+#pragma unroll
+        for (int o2 = 16; o2; o2 >>= 1) {
+            ns += __shfl_xor_sync(full, ns, o2);
+            nt += __shfl_xor_sync(full, nt, o2);
+        }
+        sc = ns / nv; tc = nt / nv;
+        double d2 = 0.0;
+        if (lane < nv) {
+            double ds = W->ps[cur][lane] - sc, dt = W->pt[cur][lane] - tc;
+            d2 = ds * ds + dt * dt;
+        }
+#pragma unroll
+        for (int o2 = 16; o2; o2 >>= 1) d2 = fmax(d2, __shfl_xor_sync(full, d2, o2));
+        rho = sqrt(d2) * (1.0 + 1e-9) + 1e-12;
+        return true;
+    };
+    // does row (a2, b2, g2) (shifted by tol) cut the current polygon?
+    auto cuts = [&](double a2, double b2, double g2) -> bool {
+        if ((a2 * sc + b2 * tc + g2) + rho <= 0.0) return false;   // |(a2, b2)| <= 1 for a unit row
+        double mx = -1e300;
+        for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+        return mx > 0.0;
+    };
+
+    // hint: a point on this cell's polygon (the edge midpoint through which the cell was
+    // found: F is continuous across the shared plane, so it lies on this face plane too)
+    // and a search radius.  Pass 1 clips only by rows within that radius, so the polygon
+    // is (nearly) final before the full passes.
+    const double4 hint = reinterpret_cast<const double4*>(A.hints)[item];
+    const bool have_hint = isfinite(hint.w);
+    double s0 = 0.0, t0 = 0.0;
+    if (have_hint) {
+        double dx[3] = {hint.x - P0[0], hint.y - P0[1], hint.z - P0[2]};
+        s0 = dot3(dx, U);
+        t0 = dot3(dx, Vv);
+    }
+    // ---------------------------------------------------- hinted single pass
+    // Stream every row once: keep those whose value at the hint point x0 is within
+    // lim = tau + band (raw-value test, no sqrt/division).  Each kept row is unit and
+    // Lipschitz-1, so a row farther than lim from x0 can neither cut nor come within band
+    // of any point within tau of x0.  Clip by the kept rows only (nearest first) inside a
+    // square of half-size tau around x0, take C' from them, and accept the result iff
+    // every vertex of P_tol lies within tau - band of x0 (else: the full two-pass path).
+    bool hinted_done = false;
+    int nC = 0;
+    unsigned long long core = 0;
+    int risky = 0;
+    const double band = tol_max + 1.5 * A.probe_delta + 1e-9;
+    double tau = hint.w;
+    for (int attempt = 0; attempt < 5 && status == 0 && have_hint && !hinted_done; attempt++) {
+        const double x0[3] = {hint.x, hint.y, hint.z};
+        const double lim = tau + band + 1e-9;
+        double dmax_seen = 0.0;
+        int nn = 0;
+        bool ok = true;
+        RawRow nx1 = load_raw(c, lane), nx2 = load_raw(c, lane + 32);
+        for (int base = 0; base < c.K; base += 32) {
+            const int gr = base + lane;
+            const RawRow rr = nx1;
+            nx1 = nx2;
+            if (base + 64 < c.K) nx2 = load_raw(c, gr + 64);   // prefetch two batches ahead
+            bool near = false;
+            if (gr < c.K && rr.kind >= 0) {
+                double n2 = (rr.x * rr.x + rr.y * rr.y) + rr.z * rr.z;
+                if (rr.kind == 0 && n2 > 0.0 && n2 < kTinyNorm * kTinyNorm) risky = 1;
+                if (rr.kind == 1 && n2 < kTinyNorm * kTinyNorm) risky = 1;
+                if (rr.kind == 2 || n2 > kDegen * kDegen) {
+                    double v = ((rr.x * x0[0] + rr.y * x0[1]) + rr.z * x0[2]) + rr.c;
+                    if (rr.kind == 0 && key_bit(c.key, gr)) v = -v;
+                    if (v > 0.0 && v * v > 1e-18 * n2) ok = false;   // x0 violates the row by > 1e-9
+                    near = v >= 0.0 || v * v <= lim * lim * n2;
+                }
+            }
+            unsigned mask = __ballot_sync(full, near);
+            int pos = nn + __popc(mask & ((1u << lane) - 1u));
+            if (near && pos < NMAX) {   // keep the raw row: no second global read
+                W->u.np.nl[pos] = gr;
+                W->cn[pos][0] = rr.x; W->cn[pos][1] = rr.y; W->cn[pos][2] = rr.z; W->cn[pos][3] = rr.c;
+            }
+            nn += __popc(mask);
+        }
+        bool x0ok = __all_sync(full, ok);
+        ok = x0ok && nn <= NMAX;
+        FSTAT(9, x0ok ? 0 : 1);
+        FSTAT(10, nn > NMAX ? 1 : 0);
+        FSTAT(12, nn);
+        risky = __any_sync(full, risky);
+        __syncwarp();
+        if (ok) {
+            // exact unit rows of the near set (get_row arithmetic), 2-D projections and distances
+            for (int i = lane; i < nn; i += 32) {
+                const int gr = W->u.np.nl[i];
+                const double rx = W->cn[i][0], ry = W->cn[i][1], rz = W->cn[i][2], rc = W->cn[i][3];
+                double n[3], o, nrm;
+                if (gr < box0) {
+                    nrm = sqrt((rx * rx + ry * ry) + rz * rz);
+                    double orient = (gr < c.NB && key_bit(c.key, gr)) ? -1.0 : 1.0;
+                    n[0] = (rx * orient) / nrm; n[1] = (ry * orient) / nrm; n[2] = (rz * orient) / nrm;
+                    o = (rc * orient) / nrm;
+                } else {
+                    nrm = 1.0; n[0] = rx; n[1] = ry; n[2] = rz; o = rc;
+                }
+                double a2 = dot3(n, U), b2 = dot3(n, Vv), g2 = dot3(n, P0) + o;
+                W->u.np.na[i] = a2; W->u.np.nb[i] = b2; W->u.np.ng[i] = g2;
+                W->u.np.nd[i] = fabs(dot3(n, x0) + o);
+                W->cn[i][0] = n[0]; W->cn[i][1] = n[1]; W->cn[i][2] = n[2]; W->cn[i][3] = o; W->cn[i][4] = nrm;
+                W->cid[i] = gr;
+            }
+            __syncwarp();
+            for (int i = lane; i < nn; i += 32) {   // rank sort by distance (ties: lower id first)
+                int rk = 0;
+                for (int j = 0; j < nn; j++) rk += (W->u.np.nd[j] < W->u.np.nd[i]) || (W->u.np.nd[j] == W->u.np.nd[i] && j < i);
+                W->u.np.nord[rk] = i;
+            }
+            // start from the square of half-size tau around x0
+            const double hw = tau;
+            if (lane < 4) {
+                W->ps[0][lane] = s0 + ((lane == 0 || lane == 3) ? -hw : hw);
+                W->pt[0][lane] = t0 + ((lane < 2) ? -hw : hw);
+            }
+            nv = 4; cur = 0;
+            sc = s0; tc = t0; rho = hw * 1.4142135623730951 * (1.0 + 1e-12) + 1e-12;
+            __syncwarp();
+            for (int q = 0; q < nn && status == 0; q++) {
+                int i = W->u.np.nord[q];
+                double a2 = W->u.np.na[i], b2 = W->u.np.nb[i], g2 = W->u.np.ng[i] - tol_c;
+                if ((a2 * sc + b2 * tc + g2) + rho <= 0.0) continue;
+                double dv = lane < nv ? a2 * W->ps[cur][lane] + b2 * W->pt[cur][lane] + g2 : -1.0;
+                if (!__any_sync(full, dv > 0.0)) continue;
+                clip(a2, b2, g2);
+#ifdef AM_FACE_STATS
+                n_clip1++;
+#endif
+            }
+            if (status == 0) {
+                // acceptance: P_tol within tau - band of x0
+                double dmax = 0.0;
+                if (lane < nv) {
+                    double ds = W->ps[cur][lane] - s0, dt = W->pt[cur][lane] - t0;
+                    dmax = sqrt(ds * ds + dt * dt);
+                }
+#pragma unroll
+                for (int o2 = 16; o2; o2 >>= 1) dmax = fmax(dmax, __shfl_xor_sync(full, dmax, o2));
+                FSTAT(11, dmax + band + 1e-9 <= hw ? 0 : 1);
+                dmax_seen = dmax;
+                if (dmax + band + 1e-9 <= hw) {
+                    // C' and core among the near rows (already in ascending id order)
+                    for (int base = 0; base < nn; base += 32) {
+                        int i = base + lane;
+                        bool in = false, is_core = false;
+                        if (i < nn) {
+                            double a2 = W->u.np.na[i], b2 = W->u.np.nb[i], g2 = W->u.np.ng[i];
+                            double mx = -1e300;
+                            for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+                            in = mx >= -band;
+                            is_core = mx >= -tol_max - kCDelta;
+                        }
+                        unsigned mask = __ballot_sync(full, in);
+                        unsigned cmask = __ballot_sync(full, is_core);
+                        // compact in place (positions only move down)
+                        int pos = nC + __popc(mask & ((1u << lane) - 1u));
+                        double r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0;
+                        int rid = 0;
+                        if (in) { r0 = W->cn[i][0]; r1 = W->cn[i][1]; r2 = W->cn[i][2]; r3 = W->cn[i][3]; r4 = W->cn[i][4]; rid = W->cid[i]; }
+                        __syncwarp();
+                        if (in) {
+                            W->cn[pos][0] = r0; W->cn[pos][1] = r1; W->cn[pos][2] = r2; W->cn[pos][3] = r3; W->cn[pos][4] = r4;
+                            W->cid[pos] = rid;
+                        }
+                        __syncwarp();
+                        unsigned m = mask;
+                        int k = nC;
+                        while (m && k < CMAX) {
+                            int l = __ffs(m) - 1;
+                            m &= m - 1;
+                            if ((cmask >> l) & 1u) core |= 1ull << k;
+                            k++;
+                        }
+                        nC += __popc(mask);
+                    }
+                    hinted_done = true;
+                }
+            }
+            if (!hinted_done) status = 0;   // outside the hint's reach (or degenerate): retry / full path
+        }
+        if (!ok) break;                    // x0 not on this polygon, or too many near rows: full path
+        tau = fmax(2.0 * tau, 2.5 * dmax_seen);   // the polygon reached the square: widen the reach
+    }
+
+    if (status == 0 && !hinted_done) {
+        // initial square; then pass 1: box rows first, then neurons, then branch rows
+        nC = 0; core = 0;
         double R = 64.0;
         for (int k = 0; k < 3; k++) R = fmax(R, 64.0 * fmax(fabs(c.lo[k]), fabs(c.hi[k])));
         if (lane < 4) {
             W->ps[0][lane] = (lane == 0 || lane == 3) ? -R : R;
             W->pt[0][lane] = (lane < 2) ? -R : R;
         }
-        nv = 4;
+        nv = 4; cur = 0; sc = 0.0; tc = 0.0;
+        rho = R * 1.4142135623730951 * (1.0 + 1e-12);
         __syncwarp();
+        auto order = [&](int idx) { return idx < 6 ? box0 + idx : idx - 6; };
+        RawRow nxt = load_raw(c, lane < c.K ? order(lane) : c.K);
         for (int base = 0; base < c.K && status == 0; base += 32) {
-            int idx = base + lane;
-            double n[3], o = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
+            const int idx = base + lane;
+            const RawRow rr = nxt;
+            if (base + 32 < c.K) nxt = load_raw(c, idx + 32 < c.K ? order(idx + 32) : c.K);   // prefetch
+            double a2 = 0.0, b2 = 0.0, g2 = 0.0, nrm;
             bool cut = false;
-            if (idx < c.K) {
-                int gr = idx < 6 ? box0 + idx : idx - 6;
-                if (get_row(c, gr, n, o)) {
-                    a2 = dot3(n, U); b2 = dot3(n, Vv); g2 = (dot3(n, P0) + o) - tol_c;
-                    double mx = -1e300;
-                    for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
-                    cut = mx > 0.0;
-                }
+            if (idx < c.K && row2d(c, order(idx), rr, U, Vv, P0, a2, b2, g2, nrm)) {
+                g2 -= tol_c;
+                cut = cuts(a2, b2, g2);
             }
             unsigned mask = __ballot_sync(full, cut);
-            while (mask) {
+            while (mask && status == 0) {
                 int src = __ffs(mask) - 1;
                 mask &= mask - 1;
-                double ca = __shfl_sync(full, a2, src), cb = __shfl_sync(full, b2, src), cg = __shfl_sync(full, g2, src);
-                // warp-parallel Sutherland-Hodgman step, one lane per vertex
-                double si = 0, ti = 0, di = 0;
-                if (lane < nv) { si = W->ps[cur][lane]; ti = W->pt[cur][lane]; di = ca * si + cb * ti + cg; }
-                int nxt = lane + 1 == nv ? 0 : lane + 1;
-                double sj = __shfl_sync(full, si, nxt & 31), tj = __shfl_sync(full, ti, nxt & 31),
-                       dj = __shfl_sync(full, di, nxt & 31);
-                bool in_i = di <= 0.0, in_j = dj <= 0.0;
-                int cnt = lane < nv ? (in_i ? 1 : 0) + (in_i != in_j ? 1 : 0) : 0;
-                int pre = cnt;
-#pragma unroll
-                for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                    int y = __shfl_up_sync(full, pre, o2);
-                    if (lane >= o2) pre += y;
-                }
-                int total = __shfl_sync(full, pre, 31);
-                pre -= cnt;
-                if (total > VMAX) { status = 2; break; }
-                int dst = cur ^ 1;
-                if (lane < nv) {
-                    int w = pre;
-                    if (in_i) { W->ps[dst][w] = si; W->pt[dst][w] = ti; w++; }
-                    if (in_i != in_j) {
-                        double lam = di / (di - dj);
-                        W->ps[dst][w] = si + lam * (sj - si);
-                        W->pt[dst][w] = ti + lam * (tj - ti);
-                    }
-                }
-                __syncwarp();
-                cur = dst;
-                nv = total;
-                if (nv < 3) { status = 1; break; }
+                clip(__shfl_sync(full, a2, src), __shfl_sync(full, b2, src), __shfl_sync(full, g2, src));
+#ifdef AM_FACE_STATS
+                n_clip1++;
+#endif
             }
         }
     }
 
-    // ------------------------------------------------ pass B: candidate set C'
-    // core rows: within tol of P_tol (the only rows that can carry a vertex, an
-    // incident plane or an edge plane); the wider band up to 1.5 probe steps is
-    // kept for probe validation.  `risky` marks near-degenerate rows that make
-    // the validation margins meaningless (the cell then publishes nothing).
-    int nC = 0;
-    unsigned long long core = 0;
-    int risky = 0;
-    const double band = tol_max + 1.5 * A.probe_delta + 1e-9;
-    if (status == 0) {
-        for (int base = 0; base < c.K; base += 32) {
-            int gr = base + lane;
-            double n[3], o = 0.0, nrm = 1.0;
-            bool in = false, is_core = false;
+    // ------------------------------------------------ pass 2: remaining cuts + candidate set C'
+    // Every row: clip if it still cuts (rare after a good hint), then keep it in C' if it
+    // comes within the band of the current polygon.  Rows seen before a late clip were
+    // tested against a larger polygon -- a superset, which is still exact (C' only has to
+    // contain every row near the final P_tol).  core rows: within tol of P_tol (the only
+    // rows that can carry a vertex, an incident plane or an edge plane); the wider band up
+    // to 1.5 probe steps serves probe validation.  `risky` marks near-degenerate rows that
+    // make the validation margins meaningless (the cell then publishes nothing).
+    for (int attempt = 0; attempt < 2 && status == 0 && !hinted_done; attempt++) {
+        nC = 0;
+        core = 0;
+        risky = 0;
+        RawRow nx1 = load_raw(c, lane), nx2 = load_raw(c, lane + 32);
+        for (int base = 0; base < c.K && status == 0; base += 32) {
+            const int gr = base + lane;
+            const RawRow rr = nx1;
+            nx1 = nx2;
+            if (base + 64 < c.K) nx2 = load_raw(c, gr + 64);   // prefetch two batches ahead
+            double a2 = 0.0, b2 = 0.0, g2 = 0.0, nrm = 0.0;
+            bool kept = false;
             if (gr < c.K) {
-                nrm = 0.0;
-                bool kept = get_row(c, gr, n, o, &nrm);
+                kept = row2d(c, gr, rr, U, Vv, P0, a2, b2, g2, nrm);
                 // near-degenerate neuron / branch functionals make the validation margins meaningless
-                if (gr < c.NB && nrm > 0.0 && nrm < kTinyNorm) risky = 1;
-                if (gr >= c.NB && gr < box0 && c.ensemble && gr - c.NB != c.branch && nrm < kTinyNorm) risky = 1;
-                if (kept) {
-                    double a2 = dot3(n, U), b2 = dot3(n, Vv), g2 = dot3(n, P0) + o;
-                    double mx = -1e300;
-                    for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
-                    in = mx >= -band;
-                    is_core = mx >= -tol_max - kCDelta;
-                }
+                if (rr.kind == 0 && nrm > 0.0 && nrm < kTinyNorm) risky = 1;
+                if (rr.kind == 1 && nrm < kTinyNorm) risky = 1;
+            }
+            bool cut = kept && cuts(a2, b2, g2 - tol_c);
+            unsigned cmask_cut = __ballot_sync(full, cut);
+            while (cmask_cut && status == 0) {
+                int src = __ffs(cmask_cut) - 1;
+                cmask_cut &= cmask_cut - 1;
+                clip(__shfl_sync(full, a2, src), __shfl_sync(full, b2, src), __shfl_sync(full, g2 - tol_c, src));
+#ifdef AM_FACE_STATS
+                n_clip2++;
+#endif
+            }
+            if (status != 0) break;
+            bool in = false, is_core = false;
+            if (kept && (a2 * sc + b2 * tc + g2) + rho >= -band) {
+                double mx = -1e300;
+                for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+                in = mx >= -band;
+                is_core = mx >= -tol_max - kCDelta;
             }
             unsigned mask = __ballot_sync(full, in);
             unsigned cmask = __ballot_sync(full, is_core);
             int pos = nC + __popc(mask & ((1u << lane) - 1u));
             if (in && pos < CMAX) {
+                // exact unit row, same arithmetic as reference cells.py:146-160
+                double n[3], o;
+                get_row(c, gr, n, o);
                 W->cn[pos][0] = n[0]; W->cn[pos][1] = n[1]; W->cn[pos][2] = n[2]; W->cn[pos][3] = o;
                 W->cn[pos][4] = nrm;
                 W->cid[pos] = gr;
@@ -307,9 +605,10 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             nC += __popc(mask);
         }
         risky = __any_sync(full, risky);
-        if (nC > CMAX) status = 2;
-        __syncwarp();
+        if (nC <= CMAX) break;   // else: late clips inflated C' -- once more against the final polygon
     }
+    if (status == 0 && nC > CMAX) status = 2;
+    __syncwarp();
 
     // ------------------------------------- exact vertex semantics on C (core rows)
     int nq = 0;
@@ -351,8 +650,8 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             unsigned mask = __ballot_sync(full, valid);
             int pos = nq + __popc(mask & ((1u << lane) - 1u));
             if (valid && pos < QMAX) {
-                W->qv[pos][0] = x[0]; W->qv[pos][1] = x[1]; W->qv[pos][2] = x[2];
-                W->qs[pos] = set;
+                W->u.pp.qv[pos][0] = x[0]; W->u.pp.qv[pos][1] = x[1]; W->u.pp.qv[pos][2] = x[2];
+                W->u.pp.qs[pos] = set;
             }
             nq += __popc(mask);
         }
@@ -366,54 +665,22 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     if (status == 0) {
         if (lane == 0) {
             for (int q = 0; q < nq; q++) {
-                const double* x = W->qv[q];
+                const double* x = W->u.pp.qv[q];
                 int hit = -1;
                 for (int k = 0; k < nr; k++) {
-                    double d0 = W->rf[k][0] - x[0], d1 = W->rf[k][1] - x[1], d2 = W->rf[k][2] - x[2];
+                    const double* f = W->u.pp.qv[W->u.pp.rfi[k]];
+                    double d0 = f[0] - x[0], d1 = f[1] - x[1], d2 = f[2] - x[2];
                     if (sqrt((d0 * d0 + d1 * d1) + d2 * d2) <= A.tol_weld) { hit = k; break; }
                 }
                 if (hit < 0) {
                     hit = nr++;
-                    for (int d = 0; d < 3; d++) { W->rf[hit][d] = x[d]; W->rv[hit][d] = x[d]; }
-                    W->rs[hit] = 0;
-                } else if (lex_less(x, W->rv[hit])) {
-                    for (int d = 0; d < 3; d++) W->rv[hit][d] = x[d];
+                    W->u.pp.rfi[hit] = q;
+                    for (int d = 0; d < 3; d++) W->u.pp.rv[hit][d] = x[d];
+                    W->u.pp.rs[hit] = 0;
+                } else if (lex_less(x, W->u.pp.rv[hit])) {
+                    for (int d = 0; d < 3; d++) W->u.pp.rv[hit][d] = x[d];
                 }
-                W->rs[hit] |= W->qs[q];
-            }
-            if (nr >= 3) {
-                double cen[3] = {0, 0, 0};
-                for (int k = 0; k < nr; k++) { cen[0] += W->rv[k][0]; cen[1] += W->rv[k][1]; cen[2] += W->rv[k][2]; }
-                cen[0] /= nr; cen[1] /= nr; cen[2] /= nr;
-                for (int k = 0; k < nr; k++) {
-                    double r0 = W->rv[k][0] - cen[0], r1 = W->rv[k][1] - cen[1], r2 = W->rv[k][2] - cen[2];
-                    W->ang[k] = atan2((r0 * Vv[0] + r1 * Vv[1]) + r2 * Vv[2], (r0 * U[0] + r1 * U[1]) + r2 * U[2]);
-                    W->ord[k] = k;
-                }
-                for (int i = 1; i < nr; i++) {
-                    int tt = W->ord[i], j = i - 1;
-                    while (j >= 0 && W->ang[W->ord[j]] > W->ang[tt]) { W->ord[j + 1] = W->ord[j]; j--; }
-                    W->ord[j + 1] = tt;
-                }
-                double tot[3] = {0, 0, 0};
-                for (int i = 0; i < nr; i++) {
-                    const double* p = W->rv[W->ord[i]];
-                    const double* q = W->rv[W->ord[(i + 1) % nr]];
-                    tot[0] += p[1] * q[2] - p[2] * q[1];
-                    tot[1] += p[2] * q[0] - p[0] * q[2];
-                    tot[2] += p[0] * q[1] - p[1] * q[0];
-                }
-                double area = 0.5 * ((tot[0] * fu[0] + tot[1] * fu[1]) + tot[2] * fu[2]);
-                if (area < 0.0)
-                    for (int i = 0, j = nr - 1; i < j; i++, j--) { int tt = W->ord[i]; W->ord[i] = W->ord[j]; W->ord[j] = tt; }
-                int start = 0;
-                for (int k = 1; k < nr; k++)
-                    if (lex_less(W->rv[W->ord[k]], W->rv[W->ord[start]])) start = k;
-                for (int k = 0; k < nr; k++) {
-                    int src = W->ord[(k + start) % nr];
-                    for (int d = 0; d < 3; d++) W->fv[k][d] = W->rv[src][d];
-                    W->fs[k] = W->rs[src];
-                }
+                W->u.pp.rs[hit] |= W->u.pp.qs[q];
             }
             W->status = nr;
         }
@@ -421,18 +688,62 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         nr = W->status;
         if (nr < 3) status = 1;
     }
+    if (status == 0) {
+        // centroid (reference cells.py:282: verts.mean), angles in the face frame -- lane per vertex
+        double cen[3] = {0, 0, 0};
+        for (int k = 0; k < nr; k++) { cen[0] += W->u.pp.rv[k][0]; cen[1] += W->u.pp.rv[k][1]; cen[2] += W->u.pp.rv[k][2]; }
+        cen[0] /= nr; cen[1] /= nr; cen[2] /= nr;
+        double rk = 0.0;
+        for (int k = lane; k < nr; k += 32) {
+            double r0 = W->u.pp.rv[k][0] - cen[0], r1 = W->u.pp.rv[k][1] - cen[1], r2 = W->u.pp.rv[k][2] - cen[2];
+            rk = fmax(rk, sqrt((r0 * r0 + r1 * r1) + r2 * r2));
+            W->u.pp.ang[k] = atan2((r0 * Vv[0] + r1 * Vv[1]) + r2 * Vv[2], (r0 * U[0] + r1 * U[1]) + r2 * U[2]);
+            W->u.pp.ord[k] = k;
+        }
+#pragma unroll
+        for (int o2 = 16; o2; o2 >>= 1) rk = fmax(rk, __shfl_xor_sync(full, rk, o2));
+        __syncwarp();
+        if (lane == 0) {
+            for (int i = 1; i < nr; i++) {   // stable sort by angle (reference np.argsort kind="stable")
+                int tt = W->u.pp.ord[i], j = i - 1;
+                while (j >= 0 && W->u.pp.ang[W->u.pp.ord[j]] > W->u.pp.ang[tt]) { W->u.pp.ord[j + 1] = W->u.pp.ord[j]; j--; }
+                W->u.pp.ord[j + 1] = tt;
+            }
+            double tot[3] = {0, 0, 0};
+            for (int i = 0; i < nr; i++) {
+                const double* p = W->u.pp.rv[W->u.pp.ord[i]];
+                const double* q = W->u.pp.rv[W->u.pp.ord[(i + 1) % nr]];
+                tot[0] += p[1] * q[2] - p[2] * q[1];
+                tot[1] += p[2] * q[0] - p[0] * q[2];
+                tot[2] += p[0] * q[1] - p[1] * q[0];
+            }
+            double area = 0.5 * ((tot[0] * fu[0] + tot[1] * fu[1]) + tot[2] * fu[2]);
+            if (area < 0.0)
+                for (int i = 0, j = nr - 1; i < j; i++, j--) { int tt = W->u.pp.ord[i]; W->u.pp.ord[i] = W->u.pp.ord[j]; W->u.pp.ord[j] = tt; }
+            int start = 0;
+            for (int k = 1; k < nr; k++)
+                if (lex_less(W->u.pp.rv[W->u.pp.ord[k]], W->u.pp.rv[W->u.pp.ord[start]])) start = k;
+            for (int k = 0; k < nr; k++) {
+                int src = W->u.pp.ord[(k + start) % nr];
+                for (int d = 0; d < 3; d++) W->u.pp.fv[k][d] = W->u.pp.rv[src][d];
+                W->u.pp.fs[k] = W->u.pp.rs[src];
+            }
+            W->diam = 2.0 * rk;
+        }
+        __syncwarp();
+    }
 
     // per-edge transition planes + mirrored-probe validation (lane per edge)
     if (status == 0) {
         bool need_argmin = false;
         for (int e = lane; e < nr; e += 32) {
-            const double* p = W->fv[e];
-            const double* q = W->fv[(e + 1) % nr];
+            const double* p = W->u.pp.fv[e];
+            const double* q = W->u.pp.fv[(e + 1) % nr];
             double mid[3] = {0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2])};
             unsigned long long on_mid = 0;
             for (int r = 0; r < nC; r++)
                 if (((core >> r) & 1ull) && fabs(dot3(W->cn[r], mid) + W->cn[r][3]) <= tol_p) on_mid |= 1ull << r;
-            unsigned long long shared = W->fs[e] & W->fs[(e + 1) % nr];
+            unsigned long long shared = W->u.pp.fs[e] & W->u.pp.fs[(e + 1) % nr];
             unsigned long long rows = shared & on_mid;
             if (!rows) rows = shared ? shared : on_mid;
             W->erow[e] = rows;
@@ -469,8 +780,8 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         if (am_mask) {
             for (int e = 0; e < nr; e++) {
                 if (W->erow[e]) continue;
-                const double* p = W->fv[e];
-                const double* q = W->fv[(e + 1) % nr];
+                const double* p = W->u.pp.fv[e];
+                const double* q = W->u.pp.fv[(e + 1) % nr];
                 double mid[3] = {0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2])};
                 double best = 1e300;
                 int bi = 0x7fffffff;
@@ -492,52 +803,130 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         __syncwarp();
     }
 
+#ifdef AM_FACE_STATS
+    {
+        long long dt = clock64() - t_start;
+        FSTAT(0, 1); FSTAT(1, n_clip1); FSTAT(2, n_clip2); FSTAT(3, nC); FSTAT(4, nq); FSTAT(5, nr);
+        FSTAT(6, dt); FSTAT(7, hinted_done ? 1 : 0); FSTAT(13, have_hint ? 1 : 0);
+        int bkt = 0;
+        while ((1ll << (bkt + 1)) <= dt && bkt < 23) bkt++;
+        FSTAT(16 + bkt, 1);
+        if (lane == 0 && A.dbg) atomicMax(&A.dbg[8], (unsigned long long)dt);
+    }
+#endif
     // ------------------------------------------------------------ emit cell
+    // lane 0 builds the neighbour descriptors (reference marching.py:152-186, 262-288), then
+    // every output range is reserved with one round of independent atomics
     const int32_t pidx = A.pool_idx[fi];
-    int64_t cell = 0;
-    if (lane == 0) {
-        cell = (int64_t)atomicAdd(A.n_cells, 1ull);
-        if (status == 2) atomicAdd(&A.overflow[0], 1ull);
-    }
-    cell = __shfl_sync(full, cell, 0);
-    if (cell >= A.cap_cells) {
-        if (lane == 0) atomicAdd(&A.overflow[1], 1ull);
-        return;
-    }
     if (status != 0) {
         if (lane == 0) {
-            A.cell_pool[cell] = pidx;
-            A.cell_nv[cell] = status == 2 ? -1 : 0;
-            A.cell_voff[cell] = 0;
+            int64_t cell = (int64_t)atomicAdd(A.n_cells, 1ull);
+            if (status == 2) atomicAdd(&A.overflow[0], 1ull);
+            if (cell < A.cap_cells) {
+                A.cell_pool[cell] = pidx;
+                A.cell_nv[cell] = status == 2 ? -1 : 0;
+                A.cell_voff[cell] = 0;
+            } else {
+                atomicAdd(&A.overflow[1], 1ull);
+            }
             A.pool_vn[pidx] = 0;   // processed, nothing validated
         }
         return;
     }
-    int nrefs_total = 0, nvalid = 0;
-    for (int e = 0; e < nr; e++) {
-        nrefs_total += W->erow[e] ? __popcll(W->erow[e]) : 1;
-        nvalid += W->eval[e];
-    }
     if (lane == 0) {
-        int64_t voff = (int64_t)atomicAdd(A.n_verts, (unsigned long long)nr);
-        int64_t roff = (int64_t)atomicAdd(A.n_refs, (unsigned long long)nrefs_total);
-        int64_t vloff = nvalid ? (int64_t)atomicAdd(A.n_val, (unsigned long long)nvalid) : 0;
-        if (voff + nr > A.cap_verts || roff + nrefs_total > A.cap_refs || vloff + nvalid > A.cap_val) {
+        int nrefs_total = 0, nvalid = 0, nprec = 0, ncd = 0;
+        const int box0l = box0;
+        for (int e = 0; e < nr; e++) {
+            nrefs_total += W->erow[e] ? __popcll(W->erow[e]) : 1;
+            nvalid += W->eval[e];
+            int nb = 0, nbr = 0, first = -1;   // first: global id of crossable[0]
+            if (W->erow[e]) {
+                unsigned long long m = W->erow[e];
+                while (m) {
+                    int r = __ffsll((long long)m) - 1;
+                    m &= m - 1;
+                    int gid = W->cid[r];
+                    if (gid >= box0l) continue;
+                    if (first < 0) first = gid;
+                    if (gid < c.NB) { if (nb < 32) W->tb[nb++] = gid; }
+                    else if (nbr < 32) W->tr[nbr++] = gid - c.NB;
+                }
+            } else if (W->eargmin[e] < box0l) {
+                first = W->eargmin[e];
+                if (first < c.NB) W->tb[nb++] = first; else W->tr[nbr++] = first - c.NB;
+            }
+            W->efirst[e] = first;
+            if (first < 0) continue;
+            nprec++;
+            const bool single = (nb == 1 && nbr == 0);
+            // subsets: combinations of sizes 0..nb (nb <= 3) or singles + full + () (nb > 3)
+            int nsub = 0, sub_mask[8];
+            const bool big = nb > 3;
+            if (big) {
+                nsub = nb + 2;
+            } else {
+                for (int k = 0; k <= nb; k++) {
+                    int idx[3] = {0, 1, 2};
+                    for (int i = 0; i < k; i++) idx[i] = i;
+                    for (;;) {
+                        int mk = 0;
+                        for (int i = 0; i < k; i++) mk |= 1 << idx[i];
+                        sub_mask[nsub++] = mk;
+                        int i = k - 1;
+                        while (i >= 0 && idx[i] == nb - k + i) i--;
+                        if (i < 0) break;
+                        idx[i]++;
+                        for (int tt = i + 1; tt < k; tt++) idx[tt] = idx[tt - 1] + 1;
+                    }
+                }
+            }
+            for (int si = 0; si < nsub; si++) {
+                for (int ti = -1; ti < nbr; ti++) {
+                    bool empty_sub = big ? (si == nb + 1) : (sub_mask[si] == 0);
+                    if (empty_sub && ti < 0) continue;
+                    if (ncd >= EMAXC) { atomicAdd(&A.overflow[0], 1ull); continue; }
+                    W->cd_edge[ncd] = e;
+                    W->cd_branch[ncd] = ti >= 0 ? W->tr[ti] : -1;
+                    W->cd_probe[ncd] = -1;
+                    int nf = 0;
+                    if (big) {
+                        if (si < nb) { W->cd_flip[ncd][0] = W->tb[si]; nf = 1; }
+                        else if (si == nb) { nf = -1; }   // all neuron bits of the edge
+                    } else {
+                        for (int i = 0; i < nb; i++)
+                            if (sub_mask[si] & (1 << i)) W->cd_flip[ncd][nf++] = W->tb[i];
+                    }
+                    W->cd_nflip[ncd] = nf;
+                    if (single) W->cd_probe[ncd] = e;   // the lone flip carries the probe record
+                    ncd++;
+                }
+            }
+        }
+        // one round of reservations
+        unsigned long long r_cell = atomicAdd(A.n_cells, 1ull);
+        unsigned long long r_vert = atomicAdd(A.n_verts, (unsigned long long)nr);
+        unsigned long long r_ref = atomicAdd(A.n_refs, (unsigned long long)nrefs_total);
+        unsigned long long r_val = nvalid ? atomicAdd(A.n_val, (unsigned long long)nvalid) : 0ull;
+        unsigned long long r_cand = ncd ? atomicAdd(A.n_cand, (unsigned long long)ncd) : 0ull;
+        unsigned long long r_prec = nprec ? atomicAdd(A.n_prec, (unsigned long long)nprec) : 0ull;
+        const int64_t cell = (int64_t)r_cell, voff = (int64_t)r_vert, roff = (int64_t)r_ref, vloff = (int64_t)r_val;
+        bool fits = cell < A.cap_cells && voff + nr <= A.cap_verts && roff + nrefs_total <= A.cap_refs &&
+                    vloff + nvalid <= A.cap_val && (int64_t)r_cand + ncd <= A.cap_cand &&
+                    (int64_t)r_prec + nprec <= A.cap_prec;
+        if (!fits) {
             atomicAdd(&A.overflow[1], 1ull);
-            A.cell_pool[cell] = pidx;
-            A.cell_nv[cell] = -2;
-            A.cell_voff[cell] = 0;
+            if (cell < A.cap_cells) { A.cell_pool[cell] = pidx; A.cell_nv[cell] = -2; A.cell_voff[cell] = 0; }
             A.pool_vn[pidx] = 0;
             W->n_cd = -1;
         } else {
             A.cell_pool[cell] = pidx;
             A.cell_nv[cell] = nr;
             A.cell_voff[cell] = voff;
-            int64_t ro = roff, vo = vloff;
+            int64_t ro = roff, vo = vloff, po = (int64_t)r_prec;
             for (int e = 0; e < nr; e++) {
-                A.verts[(voff + e) * 3 + 0] = W->fv[e][0];
-                A.verts[(voff + e) * 3 + 1] = W->fv[e][1];
-                A.verts[(voff + e) * 3 + 2] = W->fv[e][2];
+                A.verts[(voff + e) * 3 + 0] = W->u.pp.fv[e][0];
+                A.verts[(voff + e) * 3 + 1] = W->u.pp.fv[e][1];
+                A.verts[(voff + e) * 3 + 2] = W->u.pp.fv[e][2];
                 A.edge_roff[voff + e] = ro;
                 int cnt = 0;
                 if (W->erow[e]) {
@@ -551,110 +940,44 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
                 if (W->eval[e]) {   // validated neuron = the single crossable plane of edge e
                     unsigned long long m = W->erow[e];
                     int kn = -1;
-                    while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; if (W->cid[r] < box0) kn = W->cid[r]; }
+                    while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; if (W->cid[r] < box0l) kn = W->cid[r]; }
                     A.val_buf[vo++] = kn;
                 }
-            }
-            A.pool_voff[pidx] = vloff;
-            A.pool_vn[pidx] = nvalid;
-            // ---------------- neighbour candidates (reference marching.py:152-186, 262-288)
-            int ncd = 0;
-            for (int e = 0; e < nr; e++) {
-                int nb = 0, nbr = 0, first = -1;   // first: global id of crossable[0]
-                if (W->erow[e]) {
-                    unsigned long long m = W->erow[e];
-                    while (m) {
-                        int r = __ffsll((long long)m) - 1;
-                        m &= m - 1;
-                        int gid = W->cid[r];
-                        if (gid >= box0) continue;
-                        if (first < 0) first = gid;
-                        if (gid < c.NB) { if (nb < 64) W->tb[nb++] = gid; }
-                        else if (nbr < 64) W->tr[nbr++] = gid - c.NB;
-                    }
-                } else if (W->eargmin[e] < box0) {
-                    first = W->eargmin[e];
-                    if (first < c.NB) W->tb[nb++] = first; else W->tr[nbr++] = first - c.NB;
-                }
+                const int first = W->efirst[e];
                 if (first < 0) continue;
-                const bool single = (nb == 1 && nbr == 0);
-                // subsets: combinations of sizes 0..nb (nb <= 3) or singles + full + () (nb > 3)
-                int nsub = 0, sub_mask[8];
-                const bool big = nb > 3;
-                if (big) {
-                    nsub = nb + 2;
-                } else {
-                    for (int k = 0; k <= nb; k++) {
-                        int idx[3] = {0, 1, 2};
-                        for (int i = 0; i < k; i++) idx[i] = i;
-                        for (;;) {
-                            int mk = 0;
-                            for (int i = 0; i < k; i++) mk |= 1 << idx[i];
-                            sub_mask[nsub++] = mk;
-                            int i = k - 1;
-                            while (i >= 0 && idx[i] == nb - k + i) i--;
-                            if (i < 0) break;
-                            idx[i]++;
-                            for (int tt = i + 1; tt < k; tt++) idx[tt] = idx[tt - 1] + 1;
-                        }
-                    }
-                }
-                for (int si = 0; si < nsub; si++) {
-                    for (int ti = -1; ti < nbr; ti++) {
-                        bool empty_sub = big ? (si == nb + 1) : (sub_mask[si] == 0);
-                        if (empty_sub && ti < 0) continue;
-                        if (ncd >= EMAXC) { atomicAdd(&A.overflow[0], 1ull); continue; }
-                        W->cd_edge[ncd] = e;
-                        W->cd_branch[ncd] = ti >= 0 ? W->tr[ti] : -1;
-                        W->cd_probe[ncd] = -1;
-                        int nf = 0;
-                        if (big) {
-                            if (si < nb) { W->cd_flip[ncd][0] = W->tb[si]; nf = 1; }
-                            else if (si == nb) { nf = -1; }   // all neuron bits of the edge
-                        } else {
-                            for (int i = 0; i < nb; i++)
-                                if (sub_mask[si] & (1 << i)) W->cd_flip[ncd][nf++] = W->tb[i];
-                        }
-                        W->cd_nflip[ncd] = nf;
-                        if (single) W->cd_probe[ncd] = e;   // the lone flip carries the probe record
-                        ncd++;
-                    }
-                }
-                // probe across crossable[0]: single-neuron edges -> probe record (resolved by the
-                // far cell's validation); anything else -> exact forward evaluation
-                double pn[3], po;
+                // probe across crossable[0] (reference marching.py:271-276) as a probe record:
+                // single-neuron edges point at their flip (resolved by that cell's mirrored
+                // validation); any other edge is a forced exact forward evaluation (cand = -1)
+                double pn[3], po_;
                 int pr = -1;
                 for (int r = 0; r < nC; r++)
                     if (W->cid[r] == first) { pr = r; break; }
                 if (pr >= 0) { pn[0] = W->cn[pr][0]; pn[1] = W->cn[pr][1]; pn[2] = W->cn[pr][2]; }
-                else get_row(c, first, pn, po);
-                const double* p = W->fv[e];
-                const double* q = W->fv[(e + 1) % nr];
-                double pt[3] = {0.5 * (p[0] + q[0]) + A.probe_delta * pn[0], 0.5 * (p[1] + q[1]) + A.probe_delta * pn[1],
-                                0.5 * (p[2] + q[2]) + A.probe_delta * pn[2]};
-                if (!single) {
-                    unsigned long long pi = atomicAdd(A.n_probe, 1ull);
-                    if ((int64_t)pi < A.cap_probe) {
-                        A.probe_pts[pi * 3 + 0] = pt[0]; A.probe_pts[pi * 3 + 1] = pt[1]; A.probe_pts[pi * 3 + 2] = pt[2];
-                    } else {
-                        atomicAdd(&A.overflow[1], 1ull);
-                    }
-                } else {
-                    W->qv[e][0] = pt[0]; W->qv[e][1] = pt[1]; W->qv[e][2] = pt[2];   // probe point of edge e
-                }
+                else get_row(c, first, pn, po_);
+                const double* p = W->u.pp.fv[e];
+                const double* q = W->u.pp.fv[(e + 1) % nr];
+                A.prec_pt[po * 3 + 0] = 0.5 * (p[0] + q[0]) + A.probe_delta * pn[0];
+                A.prec_pt[po * 3 + 1] = 0.5 * (p[1] + q[1]) + A.probe_delta * pn[1];
+                A.prec_pt[po * 3 + 2] = 0.5 * (p[2] + q[2]) + A.probe_delta * pn[2];
+                A.prec_k[po] = first;
+                A.prec_cand[po] = -1;
+                W->eprec[e] = (int)(po - (int64_t)r_prec);
+                po++;
             }
+            A.pool_voff[pidx] = vloff;
+            A.pool_vn[pidx] = nvalid;
             W->n_cd = ncd;
-            W->cbase = (long long)atomicAdd(A.n_cand, (unsigned long long)ncd);
+            W->cbase = (long long)r_cand;
+            W->pbase = (long long)r_prec;
         }
     }
     __syncwarp();
     const int ncd = W->n_cd;
     if (ncd < 0) return;
     const int64_t cbase = W->cbase;
-    // write candidate keys cooperatively: word w of candidate k
+    // candidate keys, cooperatively: word w of candidate k; lane 0 links single-edge probes
     for (int k = 0; k < ncd; k++) {
-        int64_t ci = cbase + k;
-        if (ci >= A.cap_cand) { if (lane == 0) atomicAdd(&A.overflow[1], 1ull); continue; }
+        const int64_t ci = cbase + k;
         uint64_t* dst = A.cand + ci * A.KW;
         for (int w = lane; w < A.KW; w += 32) {
             uint64_t word = c.key[w];
@@ -676,25 +999,20 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             if (A.ensemble && w == A.KW - 1 && W->cd_branch[k] >= 0) word = (uint64_t)W->cd_branch[k];
             dst[w] = word;
         }
-        // probe record: (emitted candidate index, neuron, point)
-        if (lane == 0 && W->cd_probe[k] >= 0) {
-            int e = W->cd_probe[k];
-            unsigned long long pi = atomicAdd(A.n_prec, 1ull);
-            if ((int64_t)pi < A.cap_prec) {
-                A.prec_cand[pi] = (int32_t)ci;
-                A.prec_k[pi] = W->cd_flip[k][0];
-                A.prec_pt[pi * 3 + 0] = W->qv[e][0];
-                A.prec_pt[pi * 3 + 1] = W->qv[e][1];
-                A.prec_pt[pi * 3 + 2] = W->qv[e][2];
-            } else {
-                atomicAdd(&A.overflow[1], 1ull);
-            }
+        if (lane == 0) {
+            const int e = W->cd_edge[k];
+            const double* p = W->u.pp.fv[e];
+            const double* q = W->u.pp.fv[(e + 1) % nr];
+            // hint for the neighbour: midpoint of the shared edge + search radius
+            reinterpret_cast<double4*>(A.emit_hint)[ci] =
+                make_double4(0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2]), 2.0 * W->diam + 1e-9);
+            if (W->cd_probe[k] >= 0) A.prec_cand[W->pbase + W->eprec[e]] = (int32_t)ci;
         }
     }
 }
 
 // persistent: each warp walks the device-resident frontier
-__global__ void __launch_bounds__(FW * 32) k_face(FaceArgs A) {
+__global__ void __launch_bounds__(FW * 32, 4) k_face(FaceArgs A) {
     extern __shared__ uint8_t smem_raw[];
     FaceWarp* W = reinterpret_cast<FaceWarp*>(smem_raw) + (threadIdx.x >> 5);
     const int64_t n = dev_count(A.n_dev, A.n_cap);

@@ -67,7 +67,7 @@ __global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx
 
 __global__ void k_hash_fixup(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                              int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag,
-                             int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail) {
+                             int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint) {
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(i, n) {
         const int64_t ci = idx ? idx[i] : i;
@@ -81,6 +81,9 @@ __global__ void k_hash_fixup(HashSet H, const uint64_t* src, const int32_t* idx,
         for (int w = 0; w < H.KW; w++) dst[w] = key[w];
         H.pool_flags[p] = flag;
         H.pool_vn[p] = -1;
+        double4 hint = src_hint ? reinterpret_cast<const double4*>(src_hint)[ci]
+                                : make_double4(0.0, 0.0, 0.0, __longlong_as_double(0x7ff0000000000000ll));
+        reinterpret_cast<double4*>(H.pool_hint)[p] = hint;
         uint64_t fp = key_hash(key, H.KW) >> 33;
         __threadfence();
         H.table[slot[ci]] = (fp << 33) | (uint64_t)(uint32_t)p;
@@ -124,8 +127,8 @@ void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* id
 }
 void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                        int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
-                       int32_t* queue, unsigned long long* q_tail, cudaStream_t s) {
-    if (n_cap > 0) { k_hash_fixup<<<grid_for(n_cap, 256), 256, 0, s>>>(H, src, idx, n_dev, n_cap, status, slot, flag, pool_idx, queue, q_tail); ++g_launch_count; }
+                       int32_t* queue, unsigned long long* q_tail, const double* src_hint, cudaStream_t s) {
+    if (n_cap > 0) { k_hash_fixup<<<grid_for(n_cap, 256), 256, 0, s>>>(H, src, idx, n_dev, n_cap, status, slot, flag, pool_idx, queue, q_tail, src_hint); ++g_launch_count; }
 }
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
     if (n_pool > 0) { k_hash_rebuild<<<grid_for(n_pool, 256), 256, 0, s>>>(H, n_pool); ++g_launch_count; }
@@ -179,14 +182,19 @@ __global__ void k_take(IterState I) {
 }
 
 // ckey[b] = pool[batch_pool[b]]; reset per-item flags
-__global__ void k_gather_batch(const uint64_t* pool, const int32_t* batch_pool, const unsigned long long* n_dev,
-                               int64_t n_cap, int KW, uint64_t* ckey, int32_t* changed, int32_t* canon_pos) {
+__global__ void k_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
+                               const unsigned long long* n_dev, int64_t n_cap, int KW, uint64_t* ckey,
+                               double* ckey_hint, int32_t* changed, int32_t* canon_pos) {
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(t, n * KW) {
         int64_t b = t / KW;
         int w = (int)(t - b * KW);
         ckey[t] = pool[(int64_t)batch_pool[b] * KW + w];
-        if (w == 0) { changed[b] = 0; canon_pos[b] = -1; }
+        if (w == 0) {
+            changed[b] = 0;
+            canon_pos[b] = -1;
+            reinterpret_cast<double4*>(ckey_hint)[b] = reinterpret_cast<const double4*>(pool_hint)[batch_pool[b]];
+        }
     }
 }
 
@@ -269,9 +277,11 @@ __global__ void k_route_emitted(const uint64_t* scratch, const unsigned long lon
 }
 
 void launch_take(const IterState& I, cudaStream_t s) { k_take<<<1, 1024, 0, s>>>(I); ++g_launch_count; }
-void launch_gather_batch(const uint64_t* pool, const int32_t* batch_pool, const unsigned long long* n_dev,
-                         int64_t n_cap, int KW, uint64_t* ckey, int32_t* changed, int32_t* canon_pos, cudaStream_t s) {
-    k_gather_batch<<<grid_for(n_cap * KW, 256), 256, 0, s>>>(pool, batch_pool, n_dev, n_cap, KW, ckey, changed, canon_pos);
+void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
+                         const unsigned long long* n_dev, int64_t n_cap, int KW, uint64_t* ckey, double* ckey_hint,
+                         int32_t* changed, int32_t* canon_pos, cudaStream_t s) {
+    k_gather_batch<<<grid_for(n_cap * KW, 256), 256, 0, s>>>(pool, pool_hint, batch_pool, n_dev, n_cap, KW, ckey,
+                                                              ckey_hint, changed, canon_pos);
     ++g_launch_count;
 }
 void launch_route_changed(const uint64_t* ckey, const int32_t* changed, const unsigned long long* n_dev, int64_t n_cap,
@@ -337,17 +347,11 @@ __global__ void k_prec_target(ProbeRecs R, const int32_t* status, const int32_t*
     const int par = (int)(ctr[C_PPAR] & 1ull);
     GRID_STRIDE(i, n) {
         const int32_t ci = R.cand[i];
-        const int32_t st = status[ci];
-        int32_t t = -1;
-        if (st == 1) t = pool_idx[ci];
-        else if (st == 0) t = dup_ref[ci] >= 0 ? dup_ref[ci] : pool_idx[-2 - dup_ref[ci]];
-        if (t < 0) {   // remote or unresolvable: exact forward evaluation
-            unsigned long long q = atomicAdd(ctr + C_NPROBE, 1ull);
-            if ((int64_t)q < cap_probe) {
-                probe_pts[q * 3 + 0] = R.pt[i * 3 + 0]; probe_pts[q * 3 + 1] = R.pt[i * 3 + 1];
-                probe_pts[q * 3 + 2] = R.pt[i * 3 + 2];
-            } else atomicAdd(ctr + C_OVF1, 1ull);
-            continue;
+        int32_t t = -1;   // -1: exact forward evaluation (no flip target, or owned by another rank)
+        if (ci >= 0) {
+            const int32_t st = status[ci];
+            if (st == 1) t = pool_idx[ci];
+            else if (st == 0) t = dup_ref[ci] >= 0 ? dup_ref[ci] : pool_idx[-2 - dup_ref[ci]];
         }
         unsigned long long j = atomicAdd(ctr + C_NPEND, 1ull);
         if ((int64_t)j >= R.cap_pend) { atomicAdd(ctr + C_OVF1, 1ull); continue; }
@@ -368,32 +372,39 @@ __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsign
     const int par = (int)(ctr[C_PPAR] & 1ull);
     GRID_STRIDE(i, n) {
         const int32_t t = R.pend_t[par][i];
-        const int32_t vn = H.pool_vn[t];
-        const uint32_t fl = H.pool_flags[t];
-        bool forward = false;
-        if (vn >= 0) {
-            const int32_t k = R.pend_k[par][i];
-            const int64_t off = H.pool_voff[t];
-            bool found = false;
-            for (int q = 0; q < vn; q++) found |= val_buf[off + q] == k;
-            forward = !found;
-        } else if (fl & 2u) {
-            forward = true;   // composed but no face (canonical elsewhere / capped): exact evaluation
+        bool forward = false, keep = false;
+        if (t < 0) {
+            forward = true;
         } else {
-            unsigned long long j = atomicAdd(ctr + C_NKEEP, 1ull);
-            R.pend_t[par ^ 1][j] = t;
-            R.pend_k[par ^ 1][j] = R.pend_k[par][i];
-            R.pend_pt[par ^ 1][j * 3 + 0] = R.pend_pt[par][i * 3 + 0];
-            R.pend_pt[par ^ 1][j * 3 + 1] = R.pend_pt[par][i * 3 + 1];
-            R.pend_pt[par ^ 1][j * 3 + 2] = R.pend_pt[par][i * 3 + 2];
-            continue;
+            const int32_t vn = H.pool_vn[t];
+            if (vn >= 0) {
+                const int32_t k = R.pend_k[par][i];
+                const int64_t off = H.pool_voff[t];
+                bool found = false;
+                for (int q = 0; q < vn; q++) found |= val_buf[off + q] == k;
+                forward = !found;
+            } else if (H.pool_flags[t] & 2u) {
+                forward = true;   // composed but no face (canonical elsewhere / capped): exact evaluation
+            } else {
+                keep = true;      // target still queued
+            }
         }
         if (forward) {
             unsigned long long q = atomicAdd(ctr + C_NPROBE, 1ull);
             if ((int64_t)q < cap_probe) {
                 probe_pts[q * 3 + 0] = R.pend_pt[par][i * 3 + 0]; probe_pts[q * 3 + 1] = R.pend_pt[par][i * 3 + 1];
                 probe_pts[q * 3 + 2] = R.pend_pt[par][i * 3 + 2];
-            } else atomicAdd(ctr + C_OVF1, 1ull);
+            } else {
+                keep = true;      // forward buffer full this iteration: retry next iteration
+            }
+        }
+        if (keep) {
+            unsigned long long j = atomicAdd(ctr + C_NKEEP, 1ull);
+            R.pend_t[par ^ 1][j] = t;
+            R.pend_k[par ^ 1][j] = R.pend_k[par][i];
+            R.pend_pt[par ^ 1][j * 3 + 0] = R.pend_pt[par][i * 3 + 0];
+            R.pend_pt[par ^ 1][j * 3 + 1] = R.pend_pt[par][i * 3 + 1];
+            R.pend_pt[par ^ 1][j * 3 + 2] = R.pend_pt[par][i * 3 + 2];
         }
     }
 }
@@ -401,7 +412,7 @@ __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsign
 __global__ void k_pend_finalize(unsigned long long* ctr) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         ctr[C_PREC_TOTAL] += ctr[C_NPREC];
-        ctr[C_PROBES_TOTAL] += ctr[C_NPROBE];
+        ctr[C_PROBES_TOTAL] += ctr[C_NPROBE];   // (may overshoot the buffer; capped where consumed)
         ctr[C_NPEND] = ctr[C_NKEEP];
         ctr[C_PPAR] ^= 1ull;
     }

@@ -69,6 +69,7 @@ struct LayerLaunch {
     const unsigned long long* key_off;  // optional device offset (items) into keys
     int64_t n_cap;        // capacity / grid sizing
     int KW, zs;           // key words, Z row count per item (>= NB)
+    int grid_cap;         // >0: persistent GEMM grid = grid_cap CTAs per SM
 };
 
 __device__ __forceinline__ int64_t dev_count(const unsigned long long* p, int64_t cap) {
@@ -101,6 +102,7 @@ struct HashSet {
     uint32_t* pool_flags; // bit0 visited cell, bit1 composed
     int32_t* pool_vn;     // validated-neuron count of a visited cell (-1: no face yet)
     int64_t* pool_voff;   // offset of its validated-neuron list
+    double* pool_hint;    // [cap][4] a point on the cell's face polygon + search radius (inf: none)
     unsigned long long* n_pool;  // device counter
     int64_t cap_pool;
     int KW;
@@ -111,7 +113,7 @@ void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* id
                         int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, cudaStream_t s);
 void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                        int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
-                       int32_t* queue, unsigned long long* q_tail, cudaStream_t s);
+                       int32_t* queue, unsigned long long* q_tail, const double* src_hint, cudaStream_t s);
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s);
 
 // per-iteration guard / queue state (am_hash.cu k_take)
@@ -139,8 +141,9 @@ void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf
                     int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s);
 void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s);
 void launch_take(const IterState& I, cudaStream_t s);
-void launch_gather_batch(const uint64_t* pool, const int32_t* batch_pool, const unsigned long long* n_dev,
-                         int64_t n_cap, int KW, uint64_t* ckey, int32_t* changed, int32_t* canon_pos, cudaStream_t s);
+void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
+                         const unsigned long long* n_dev, int64_t n_cap, int KW, uint64_t* ckey, double* ckey_hint,
+                         int32_t* changed, int32_t* canon_pos, cudaStream_t s);
 void launch_route_changed(const uint64_t* ckey, const int32_t* changed, const unsigned long long* n_dev, int64_t n_cap,
                           int KW, int rank, int world, int32_t* X, unsigned long long* nX, uint64_t* outbox,
                           unsigned long long* n_out, int32_t* canon_pos, cudaStream_t s);
@@ -170,6 +173,8 @@ struct FaceArgs {
     const uint64_t* keys;     // canonical keys [batch][KW]
     const int32_t* items;     // frontier: batch slots to process
     const int32_t* pool_idx;  // per frontier entry: pool index of the state
+    const double* hints;      // [batch][4] point on the face polygon + search radius (inf: none)
+    double* emit_hint;        // [cap_cand][4] hint of every emitted flip (edge midpoint + radius)
     const unsigned long long* n_dev;  // frontier size (device)
     int64_t n_cap;
     int NB, M, KW, zs, ensemble;
@@ -205,6 +210,7 @@ struct FaceArgs {
     int64_t cap_val;
     int32_t* pool_vn;
     int64_t* pool_voff;
+    unsigned long long* dbg;   // instrumentation (AM_FACE_STATS builds), may be null
 };
 constexpr int kEmitFlipsPerCell = 48;   // face kernel EMAXC
 constexpr int kVertsPerCell = 64;       // face kernel QMAX

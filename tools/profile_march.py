@@ -37,3 +37,13 @@ for _ in range(a.repeat):
     c = eng.counts()
     print(f"{a.net}: {c['cells']} cells, {it} iterations, {dt * 1e3:.1f} ms, {c['cells'] / dt:.0f} cells/s")
 print({k: round(v, 3) for k, v in eng.stats().items()})
+import numpy as np  # noqa: E402
+d = np.zeros(64, dtype=np.uint64)
+eng.lib.am_debug_counters(eng.h, d.ctypes.data)
+if d[0]:
+    n = float(d[0])
+    print(f"face stats: cells {int(n)} clips1 {d[1]/n:.2f} clips2 {d[2]/n:.2f} C' {d[3]/n:.2f} raw verts {d[4]/n:.2f} "
+          f"verts {d[5]/n:.2f} cycles {d[6]/n:.0f} (max {int(d[8])}) hinted {d[7]/n:.2f}")
+    print(f"hint: have {d[13]/n:.3f} x0-violates {d[9]/n:.3f} near>NMAX {d[10]/n:.3f} reach-fail {d[11]/n:.3f} "
+          f"near rows {d[12]/max(1, d[13]):.1f}")
+    print("cycle histogram (log2):", {int(2**i): int(d[16 + i]) for i in range(24) if d[16 + i]})
