@@ -25,7 +25,7 @@
 namespace am {
 
 constexpr int BM = 64, BN = 64, BK = 16, XLD = 20;  // XLD: padded k-stride of the X tile
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;   // 8 warps: 2 (rows) x 4 (columns), 32 x 16 outputs each
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -95,6 +95,7 @@ __device__ __forceinline__ void set_key_bit(uint64_t* key, int row, int bit) {
 // from the input), pre_c = (sc + 0) + b.
 template <int C>
 __global__ void k_input_step(LayerLaunch L) {
+    pdl_enter();
     const StepDev& st = L.st;
     const int64_t n = dev_count(L.n_dev, L.n_cap);
     uint64_t* keys = keys_at(L);
@@ -172,90 +173,70 @@ void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
     int64_t total = L.n_cap * L.st.n_out;
     if (total <= 0) return;
     int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : 8));
-    if (C == 4) { k_input_step<4><<<(unsigned)blocks, 256, 0, s>>>(L); ++g_launch_count; }
-    else { k_input_step<1><<<(unsigned)blocks, 256, 0, s>>>(L); ++g_launch_count; }
+    if (C == 4) { launch_k(k_input_step<4>, (unsigned)blocks, 256, 0, s, L); }
+    else { launch_k(k_input_step<1>, (unsigned)blocks, 256, 0, s, L); }
 }
 
 // ----------------------------------------------------------- GEMM step
+constexpr int NST = 4;     // pipeline stages (BK = 16 rows of K each)
+constexpr int XS4 = 64;    // compose stage: per-item stride (16 rows x 4 components, contiguous as in Z)
+constexpr int XS1 = 20;    // forward stage: per-point padded stride (bank-conflict free B fragments)
+
+template <int C>
 struct __align__(1024) GemmSmem {
-    double w[2][BM * BK];      // TMA destination, 128B-swizzled, 8 KB per stage
-    double x[2][BN * XLD];     // masked activation tile, [col][k] with padded stride
-    uint64_t bar[2];
+    static constexpr int XSZ = C == 4 ? 16 * XS4 : BN * XS1;
+    double w[NST][BM * BK];        // TMA destination, 128B-swizzled, 8 KB per stage
+    double x[NST][XSZ];            // raw activation tile
+    uint32_t mask[NST][BN];        // per item / point: the 16 state bits of the stage's K rows
+    uint64_t bar[NST];
     unsigned long long bits[BN][2];  // forward epilogue: per-column bit window
 };
 
-// stage one BK-chunk of the masked input tile for columns [n0, n0+BN) into registers
-template <int C>
-struct XStager {
-    double v[8];
-    __device__ __forceinline__ void load(const LayerLaunch& L, const uint64_t* keys, int64_t n, int64_t n0,
-                                         int src_row, int n_src, int k0) {
-        int tid = threadIdx.x;
-        if (C == 4) {
-            // 16 items x 16 rows x 4 comps: thread -> item tid/8, rows 2*(tid%8) .. +1
-            int it = tid >> 3, rr = (tid & 7) * 2;
-            int64_t item = n0 / 4 + it;
-            bool ok = item < n;
-            const uint64_t* key = keys + (ok ? item : 0) * L.KW;
-#pragma unroll
-            for (int q = 0; q < 2; q++) {
-                int k = k0 + rr + q;
-                double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
-                if (ok && k < n_src) {
-                    int grow = src_row + k;
-                    if (key_bit(key, grow)) {
-                        const double2* p = reinterpret_cast<const double2*>(L.Z + (item * L.zs + grow) * 4);
-                        a = __ldg(p);
-                        b = __ldg(p + 1);
-                    }
-                }
-                v[q * 4 + 0] = a.x; v[q * 4 + 1] = a.y; v[q * 4 + 2] = b.x; v[q * 4 + 3] = b.y;
-            }
-        } else {
-            // 64 points x 16 rows: thread -> point tid/2, rows 8*(tid%2) .. +7
-            int pt = tid >> 1, rr = (tid & 1) * 8;
-            int64_t item = n0 + pt;
-            bool ok = item < n;
-            const uint64_t* key = keys + (ok ? item : 0) * L.KW;
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                int k = k0 + rr + q;
-                double val = 0.0;
-                if (ok && k < n_src) {
-                    int grow = src_row + k;
-                    if (key_bit(key, grow)) val = __ldg(L.Z + item * L.zs + grow);
-                }
-                v[q] = val;
-            }
-        }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait(int pending) {
+    switch (pending) {
+        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
     }
-    __device__ __forceinline__ void store(double* xs) {
-        int tid = threadIdx.x;
-        if (C == 4) {
-            int it = tid >> 3, rr = (tid & 7) * 2;
+}
+// 16 state bits of rows [row, row + 16) (MSB-first key words), zero beyond `valid` rows
+__device__ __forceinline__ uint32_t bits16(const uint64_t* key, int row, int valid) {
+    if (valid <= 0) return 0u;
+    int w = row >> 6, off = row & 63;
+    uint64_t hi = key[w] << off;                        // bit 63 of hi = state bit of `row`
+    if (off > 48) hi |= key[w + 1] >> (64 - off);
+    uint32_t m = 0;
 #pragma unroll
-            for (int q = 0; q < 2; q++)
-#pragma unroll
-                for (int c = 0; c < 4; c++) xs[(it * 4 + c) * XLD + rr + q] = v[q * 4 + c];
-        } else {
-            int pt = tid >> 1, rr = (tid & 1) * 8;
-#pragma unroll
-            for (int q = 0; q < 8; q++) xs[pt * XLD + rr + q] = v[q];
-        }
-    }
-};
+    for (int j = 0; j < 16; j++) m |= (uint32_t)((hi >> (63 - j)) & 1ull) << j;
+    if (valid < 16) m &= (1u << valid) - 1u;
+    return m;
+}
 
-// Persistent: each CTA walks output tiles (64 neuron rows x 64 item columns) of
-// the device-resident item count, so the launch is graph-capturable.
+// Persistent: each CTA walks output tiles (64 neuron rows x 64 item columns) of the
+// device-resident item count (graph-capturable).  K is streamed in 16-row chunks through an
+// NST-stage ring: W by TMA (mbarrier), the raw activations by cp.async, the state mask of the
+// chunk as 16-bit words -- applied when the B fragments are read, so padding rows and
+// inactive neurons contribute exact zeros.
 template <int C>
 __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
                                                         const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
+    pdl_enter();
     extern __shared__ uint8_t smem_raw[];
-    GemmSmem& S = *reinterpret_cast<GemmSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    GemmSmem<C>& S = *reinterpret_cast<GemmSmem<C>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const StepDev& st = L.st;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wm = warp & 1, wn = warp >> 1;   // warp tile: rows wm*32 .. +31, columns wn*16 .. +15
     const int64_t n = dev_count(L.n_dev, L.n_cap);
     if (n <= 0) return;
     uint64_t* keys = keys_at(L);
@@ -268,9 +249,8 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
     const int nty = (st.n_out + BM - 1) / BM;
     const int64_t ntiles = ntx * nty;
 
+    if (tid < NST) mbar_init(&S.bar[tid], 1);
     if (tid == 0) {
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     }
@@ -281,51 +261,79 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
     const bool sc_input_id = sc_ident && (st.flags & AM_STEP_SC_FROM_INPUT);
     const bool has_sc = (st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR)) != 0;
 
-    uint32_t gchunk = 0;  // chunks consumed by this CTA so far (mbarrier phase tracking)
+    uint32_t gchunk = 0;  // chunks consumed by this CTA so far (stage ring + mbarrier phases)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int m0 = (int)(tile / ntx) * BM;
         const int64_t n0 = (tile % ntx) * BN;
         if (C == 1 && tid < BN) { S.bits[tid][0] = 0; S.bits[tid][1] = 0; }
 
-        auto issue_w = [&](int c, int stage) {
+        // issue chunk c of this tile into its ring stage
+        auto issue = [&](int c) {
+            const int stage = (gchunk + c) % NST;
+            const bool seg0 = c < kc0;
+            const int k0 = (seg0 ? c : c - kc0) * BK;
+            const int src_row = seg0 ? st.in_row_off : st.sin_row_off;
+            const int n_src = seg0 ? st.n_in : st.n_sin;
+            const int valid = n_src - k0;
             if (tid == 0) {
                 mbar_expect_tx(&S.bar[stage], BM * BK * sizeof(double));
-                if (c < kc0) tma_load_2d(S.w[stage], &tmW, &S.bar[stage], c * BK, m0);
-                else tma_load_2d(S.w[stage], &tmV, &S.bar[stage], (c - kc0) * BK, m0);
+                tma_load_2d(S.w[stage], seg0 ? &tmW : &tmV, &S.bar[stage], k0, m0);
             }
-        };
-        XStager<C> xs;
-        auto load_x = [&](int c) {
-            if (c < kc0) xs.load(L, keys, n, n0, st.in_row_off, st.n_in, c * BK);
-            else xs.load(L, keys, n, n0, st.sin_row_off, st.n_sin, (c - kc0) * BK);
+            if (C == 4) {
+                // 16 items x 512 B; 2 x 16-B pieces per thread
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    const int piece = tid * 2 + q;          // 0..511
+                    const int it = piece >> 5, j = piece & 31;   // item, 16-B piece within its 512 B
+                    const int64_t item = n0 / 4 + it;
+                    const int krow = j >> 1;                 // 2 pieces per row (4 doubles)
+                    if (item < n && krow < valid)
+                        cp_async16(&S.x[stage][it * XS4 + j * 2],
+                                   L.Z + (item * L.zs + src_row + k0) * 4 + j * 2);
+                }
+                if (tid < 16) {
+                    const int64_t item = n0 / 4 + tid;
+                    S.mask[stage][tid] = item < n ? bits16(keys + item * L.KW, src_row + k0, valid) : 0u;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int pt = tid >> 2, krow = (tid & 3) * 4 + q;
+                    const int64_t item = n0 + pt;
+                    if (item < n && krow < valid)
+                        cp_async8(&S.x[stage][pt * XS1 + krow], L.Z + item * L.zs + src_row + k0 + krow);
+                }
+                if (tid < BN) {
+                    const int64_t item = n0 + tid;
+                    S.mask[stage][tid] = item < n ? bits16(keys + item * L.KW, src_row + k0, valid) : 0u;
+                }
+            }
+            cp_async_commit();
         };
 
-        double acc[2][4][4];
+        double acc[2][2][4];
 #pragma unroll
         for (int i = 0; i < 2; i++)
 #pragma unroll
-            for (int j = 0; j < 4; j++)
+            for (int j = 0; j < 2; j++)
 #pragma unroll
                 for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
 
-        issue_w(0, gchunk & 1);
-        load_x(0);
-        xs.store(S.x[gchunk & 1]);
-        __syncthreads();
+        const int pro = nchunks < NST ? nchunks : NST;
+        for (int c = 0; c < pro; c++) issue(c);
 
         for (int c = 0; c < nchunks; c++) {
             const uint32_t gc = gchunk + c;
-            const int s = gc & 1;
-            if (c + 1 < nchunks) {
-                issue_w(c + 1, s ^ 1);
-                load_x(c + 1);
-            }
-            mbar_wait(&S.bar[s], (gc >> 1) & 1);
+            const int s = gc % NST;
+            const int committed = (c + NST < nchunks) ? c + NST : nchunks;
+            cp_async_wait(committed - c - 1);
+            mbar_wait(&S.bar[s], (gc / NST) & 1);
+            __syncthreads();
             const double* ws = S.w[s];
             const double* xsm = S.x[s];
 #pragma unroll
             for (int kk = 0; kk < BK; kk += 4) {
-                double a[2][2], b[4];
+                double a[2][2], b[2];
 #pragma unroll
                 for (int mi = 0; mi < 2; mi++) {
                     int r = wm * 32 + mi * 16 + g;
@@ -333,18 +341,30 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
                     a[mi][1] = ws[swz(r + 8, kk + t)];
                 }
 #pragma unroll
-                for (int nj = 0; nj < 4; nj++) b[nj] = xsm[(wn * 32 + nj * 8 + g) * XLD + kk + t];
+                for (int nj = 0; nj < 2; nj++) {
+                    const int col = wn * 16 + nj * 8 + g;
+                    double v;
+                    uint32_t mk;
+                    if (C == 4) {
+                        v = xsm[(col >> 2) * XS4 + (kk + t) * 4 + (col & 3)];
+                        mk = S.mask[s][col >> 2];
+                    } else {
+                        v = xsm[col * XS1 + kk + t];
+                        mk = S.mask[s][col];
+                    }
+                    b[nj] = ((mk >> (kk + t)) & 1u) ? v : 0.0;
+                }
 #pragma unroll
                 for (int mi = 0; mi < 2; mi++)
 #pragma unroll
-                    for (int nj = 0; nj < 4; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
+                    for (int nj = 0; nj < 2; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
             }
-            if (c + 1 < nchunks) xs.store(S.x[s ^ 1]);
-            __syncthreads();
+            __syncthreads();   // stage s free again
+            if (c + NST < nchunks) issue(c + NST);
         }
         gchunk += nchunks;
 
-        // ------------------------------------------------------ epilogue
+    // ------------------------------------------------------ epilogue
         const int wbase = (st.row_off + m0) >> 6;  // forward: first key word the tile touches
 #pragma unroll
         for (int mi = 0; mi < 2; mi++) {
@@ -355,8 +375,8 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
                 const bool rok = r < st.n_out;
                 const int row = st.row_off + r;
 #pragma unroll
-                for (int nj = 0; nj < 4; nj++) {
-                    const int64_t col = n0 + wn * 32 + nj * 8 + 2 * t;
+                for (int nj = 0; nj < 2; nj++) {
+                    const int64_t col = n0 + wn * 16 + nj * 8 + 2 * t;
                     double v0 = acc[mi][nj][half * 2], v1 = acc[mi][nj][half * 2 + 1];
                     if (C == 4) {
                         const int64_t item = col >> 2;
@@ -458,16 +478,16 @@ void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const
     if (L.n_cap <= 0) return;
     int64_t cols = L.n_cap * C;
     int64_t tiles = ((cols + BN - 1) / BN) * ((L.st.n_out + BM - 1) / BM);
-    int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : 5));
-    size_t smem = sizeof(GemmSmem) + 1024;
+    int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : 2));
+    size_t smem = (C == 4 ? sizeof(GemmSmem<4>) : sizeof(GemmSmem<1>)) + 1024;
     if (C == 4) {
         static bool init = false;
         if (!init) { cudaFuncSetAttribute(k_gemm_step<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
-        { k_gemm_step<4><<<(unsigned)grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L); ++g_launch_count; }
+        { launch_k(k_gemm_step<4>, (unsigned)grid, kThreads, smem, s, *tmW, tmV ? *tmV : *tmW, L); }
     } else {
         static bool init = false;
         if (!init) { cudaFuncSetAttribute(k_gemm_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
-        { k_gemm_step<1><<<(unsigned)grid, kThreads, smem, s>>>(*tmW, tmV ? *tmV : *tmW, L); ++g_launch_count; }
+        { launch_k(k_gemm_step<1>, (unsigned)grid, kThreads, smem, s, *tmW, tmV ? *tmV : *tmW, L); }
     }
 }
 
@@ -482,6 +502,7 @@ struct SubDev {
 // reference network.py:440-442
 __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
                             int64_t n_cap, int zs, int KW, const SubDev* subs, int n_subs) {
+    pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -517,6 +538,7 @@ __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces
 __global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsigned long long* key_off, double* vals,
                                const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const SubDev* subs,
                                int n_subs, int ensemble) {
+    pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     uint64_t* keys = key_off ? keys_base + (int64_t)(*key_off) * KW : keys_base;
     const int lane = threadIdx.x & 31;
@@ -549,16 +571,16 @@ void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, 
     int64_t warps = n_cap * n_subs;
     if (warps <= 0) return;
     int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)num_sms() * 8);
-    { k_face_head<<<(unsigned)blocks, 256, 0, s>>>(Z, keys, faces, n_dev, n_cap, zs, KW,
-                                                 static_cast<const SubDev*>(subs), n_subs); ++g_launch_count; }
+    { launch_k(k_face_head, (unsigned)blocks, 256, 0, s, Z, keys, faces, n_dev, n_cap, zs, KW,
+                                                 static_cast<const SubDev*>(subs), n_subs); }
 }
 void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
                              const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,
                              int n_subs, int ensemble, cudaStream_t s) {
     if (n_cap <= 0) return;
     int64_t blocks = std::min<int64_t>((n_cap * 32 + 255) / 256, (int64_t)num_sms() * 8);
-    { k_forward_head<<<(unsigned)blocks, 256, 0, s>>>(Z, keys, key_off, vals, n_dev, n_cap, zs, KW,
-                                                    static_cast<const SubDev*>(subs), n_subs, ensemble); ++g_launch_count; }
+    { launch_k(k_forward_head, (unsigned)blocks, 256, 0, s, Z, keys, key_off, vals, n_dev, n_cap, zs, KW,
+                                                    static_cast<const SubDev*>(subs), n_subs, ensemble); }
 }
 
 }  // namespace am

@@ -587,6 +587,7 @@ static int launch_iteration(am_engine* e) {
     a.val_buf = e->val_buf.p; a.n_val = c + C_NVAL; a.cap_val = e->val_buf.n;
     a.pool_vn = e->pool_vn.p; a.pool_voff = e->pool_voff.p;
     a.dbg = e->dbg.p;
+    a.cursor = c + C_FCURSOR;
     if (tm) cudaEventRecord(e->ev[2], s);
     launch_face(a, s);
     if (tm) cudaEventRecord(e->ev[3], s);

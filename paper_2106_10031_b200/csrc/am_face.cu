@@ -1013,11 +1013,17 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
 
 // persistent: each warp walks the device-resident frontier
 __global__ void __launch_bounds__(FW * 32, 4) k_face(FaceArgs A) {
+    pdl_enter();
     extern __shared__ uint8_t smem_raw[];
     FaceWarp* W = reinterpret_cast<FaceWarp*>(smem_raw) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     const int64_t n = dev_count(A.n_dev, A.n_cap);
-    const int64_t nw = (int64_t)gridDim.x * FW;
-    for (int64_t fi = (int64_t)blockIdx.x * FW + (threadIdx.x >> 5); fi < n; fi += nw) {
+    // dynamic work distribution: cell latencies vary by 10x, so warps pull cells from a cursor
+    for (;;) {
+        int64_t fi = 0;
+        if (lane == 0) fi = (int64_t)atomicAdd(A.cursor, 1ull);
+        fi = __shfl_sync(0xffffffffu, fi, 0);
+        if (fi >= n) break;
         face_cell(A, W, fi);
         __syncwarp();
     }
@@ -1038,7 +1044,7 @@ void launch_face(const FaceArgs& a, cudaStream_t s) {
         init = true;
     }
     int64_t need = (a.n_cap + FW - 1) / FW;
-    { k_face<<<(unsigned)(need < grid ? need : grid), FW * 32, smem, s>>>(a); ++g_launch_count; }
+    { launch_k(k_face, (unsigned)(need < grid ? need : grid), FW * 32, smem, s, a); }
 }
 
 }  // namespace am

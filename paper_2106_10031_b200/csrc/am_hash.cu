@@ -26,6 +26,7 @@ __device__ __forceinline__ bool keys_equal(const uint64_t* a, const uint64_t* b,
 
 __global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                               int64_t n_cap, int32_t* status, uint64_t* slot_out, int32_t* dup_ref) {
+    pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(i, n) {
         const int64_t ci = idx ? idx[i] : i;
@@ -68,6 +69,7 @@ __global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx
 __global__ void k_hash_fixup(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                              int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag,
                              int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint) {
+    pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(i, n) {
         const int64_t ci = idx ? idx[i] : i;
@@ -94,6 +96,7 @@ __global__ void k_hash_fixup(HashSet H, const uint64_t* src, const int32_t* idx,
 
 // rebuild the slot array from the pool (table growth)
 __global__ void k_hash_rebuild(HashSet H, int64_t n_pool) {
+    pdl_enter();
     GRID_STRIDE(p, n_pool) {
         const uint64_t* key = H.pool + p * H.KW;
         uint64_t h = key_hash(key, H.KW);
@@ -123,21 +126,22 @@ static unsigned grid_for(int64_t n, int b) {
 
 void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                         int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, cudaStream_t s) {
-    if (n_cap > 0) { k_hash_insert<<<grid_for(n_cap, 256), 256, 0, s>>>(H, src, idx, n_dev, n_cap, status, slot, dup_ref); ++g_launch_count; }
+    if (n_cap > 0) { launch_k(k_hash_insert, grid_for(n_cap, 256), 256, 0, s, H, src, idx, n_dev, n_cap, status, slot, dup_ref); }
 }
 void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                        int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
                        int32_t* queue, unsigned long long* q_tail, const double* src_hint, cudaStream_t s) {
-    if (n_cap > 0) { k_hash_fixup<<<grid_for(n_cap, 256), 256, 0, s>>>(H, src, idx, n_dev, n_cap, status, slot, flag, pool_idx, queue, q_tail, src_hint); ++g_launch_count; }
+    if (n_cap > 0) { launch_k(k_hash_fixup, grid_for(n_cap, 256), 256, 0, s, H, src, idx, n_dev, n_cap, status, slot, flag, pool_idx, queue, q_tail, src_hint); }
 }
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
-    if (n_pool > 0) { k_hash_rebuild<<<grid_for(n_pool, 256), 256, 0, s>>>(H, n_pool); ++g_launch_count; }
+    if (n_pool > 0) { launch_k(k_hash_rebuild, grid_for(n_pool, 256), 256, 0, s, H, n_pool); }
 }
 
 // ------------------------------------------------------------- iteration
 // take up to B queued states for this iteration, after checking that the
 // worst case of what the iteration can produce fits every buffer.
 __global__ void k_take(IterState I) {
+    pdl_enter();
     __shared__ long long s_nR;
     unsigned long long* c = I.ctr;
     if (threadIdx.x == 0) {
@@ -170,7 +174,7 @@ __global__ void k_take(IterState I) {
         c[C_STALL] = (want > 0 && nR == 0) ? 1ull : 0ull;
         c[C_NR] = (unsigned long long)nR;
         c[C_NX] = 0; c[C_NF] = 0; c[C_NPROBE] = 0; c[C_NEMIT] = 0; c[C_NLOCAL] = 0;
-        c[C_NPREC] = 0; c[C_NKEEP] = 0; c[C_NPLOCAL] = 0;
+        c[C_NPREC] = 0; c[C_NKEEP] = 0; c[C_NPLOCAL] = 0; c[C_FCURSOR] = 0;
         c[C_ITER] += nR > 0 ? 1ull : 0ull;
         s_nR = nR;
     }
@@ -185,6 +189,7 @@ __global__ void k_take(IterState I) {
 __global__ void k_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
                                const unsigned long long* n_dev, int64_t n_cap, int KW, uint64_t* ckey,
                                double* ckey_hint, int32_t* changed, int32_t* canon_pos) {
+    pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(t, n * KW) {
         int64_t b = t / KW;
@@ -202,6 +207,7 @@ __global__ void k_gather_batch(const uint64_t* pool, const double* pool_hint, co
 __global__ void k_route_changed(const uint64_t* ckey, const int32_t* changed, const unsigned long long* n_dev,
                                 int64_t n_cap, int KW, int rank, int world, int32_t* X, unsigned long long* nX,
                                 uint64_t* outbox, unsigned long long* n_out, int32_t* canon_pos) {
+    pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(b, n) {
         if (!changed[b]) continue;
@@ -225,6 +231,7 @@ __global__ void k_frontier(const unsigned long long* n_dev, int64_t n_cap, const
                            const int32_t* batch_pool, const int32_t* canon_pos, const int32_t* canon_status,
                            const int32_t* canon_pool, uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool,
                            unsigned long long* ctr, long long max_cells) {
+    pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(b, n) {
         int32_t p = -1;
@@ -249,6 +256,7 @@ __global__ void k_frontier(const unsigned long long* n_dev, int64_t n_cap, const
 
 // zero the key slots the probe forward pass ORs its bits into
 __global__ void k_zero_probe_keys(uint64_t* scratch, const unsigned long long* ctr, int KW) {
+    pdl_enter();
     const int64_t base = (int64_t)ctr[C_NEMIT] * KW;
     const int64_t n = (int64_t)ctr[C_NPROBE] * KW;
     GRID_STRIDE(i, n) scratch[base + i] = 0;
@@ -256,6 +264,7 @@ __global__ void k_zero_probe_keys(uint64_t* scratch, const unsigned long long* c
 
 // probes were appended after the flips: total emitted = flips + probes
 __global__ void k_emit_finalize(unsigned long long* ctr) {
+    pdl_enter();
     if (threadIdx.x == 0 && blockIdx.x == 0) ctr[C_NEMIT] += ctr[C_NPROBE];
 }
 
@@ -263,6 +272,7 @@ __global__ void k_emit_finalize(unsigned long long* ctr) {
 __global__ void k_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW,
                                 int rank, int world, int32_t* local_idx, unsigned long long* n_local,
                                 uint64_t* outbox, unsigned long long* n_out, int32_t* remote_status) {
+    pdl_enter();
     const int64_t n = dev_count(ctr_n, n_cap);
     GRID_STRIDE(i, n) {
         const uint64_t* k = scratch + i * KW;
@@ -276,44 +286,40 @@ __global__ void k_route_emitted(const uint64_t* scratch, const unsigned long lon
     }
 }
 
-void launch_take(const IterState& I, cudaStream_t s) { k_take<<<1, 1024, 0, s>>>(I); ++g_launch_count; }
+void launch_take(const IterState& I, cudaStream_t s) { launch_k(k_take, 1, 1024, 0, s, I); }
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
                          const unsigned long long* n_dev, int64_t n_cap, int KW, uint64_t* ckey, double* ckey_hint,
                          int32_t* changed, int32_t* canon_pos, cudaStream_t s) {
-    k_gather_batch<<<grid_for(n_cap * KW, 256), 256, 0, s>>>(pool, pool_hint, batch_pool, n_dev, n_cap, KW, ckey,
+    launch_k(k_gather_batch, grid_for(n_cap * KW, 256),  256,  0,  s, pool, pool_hint, batch_pool, n_dev, n_cap, KW, ckey,
                                                               ckey_hint, changed, canon_pos);
-    ++g_launch_count;
 }
 void launch_route_changed(const uint64_t* ckey, const int32_t* changed, const unsigned long long* n_dev, int64_t n_cap,
                           int KW, int rank, int world, int32_t* X, unsigned long long* nX, uint64_t* outbox,
                           unsigned long long* n_out, int32_t* canon_pos, cudaStream_t s) {
-    k_route_changed<<<grid_for(n_cap, 256), 256, 0, s>>>(ckey, changed, n_dev, n_cap, KW, rank, world, X, nX, outbox,
+    launch_k(k_route_changed, grid_for(n_cap, 256),  256,  0,  s, ckey, changed, n_dev, n_cap, KW, rank, world, X, nX, outbox,
                                                           n_out, canon_pos);
-    ++g_launch_count;
 }
 void launch_frontier(const unsigned long long* n_dev, int64_t n_cap, const int32_t* changed, const int32_t* batch_pool,
                      const int32_t* canon_pos, const int32_t* canon_status, const int32_t* canon_pool,
                      uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* ctr,
                      long long max_cells, cudaStream_t s) {
-    k_frontier<<<grid_for(n_cap, 256), 256, 0, s>>>(n_dev, n_cap, changed, batch_pool, canon_pos, canon_status,
+    launch_k(k_frontier, grid_for(n_cap, 256),  256,  0,  s, n_dev, n_cap, changed, batch_pool, canon_pos, canon_status,
                                                      canon_pool, pool_flags, f_items, f_pool, ctr, max_cells);
-    ++g_launch_count;
 }
 void launch_zero_probe_keys(uint64_t* scratch, const unsigned long long* ctr, int KW, int64_t cap, cudaStream_t s) {
-    k_zero_probe_keys<<<grid_for(cap * KW, 256), 256, 0, s>>>(scratch, ctr, KW);
-    ++g_launch_count;
+    launch_k(k_zero_probe_keys, grid_for(cap * KW, 256),  256,  0,  s, scratch, ctr, KW);
 }
-void launch_emit_finalize(unsigned long long* ctr, cudaStream_t s) { k_emit_finalize<<<1, 32, 0, s>>>(ctr); ++g_launch_count; }
+void launch_emit_finalize(unsigned long long* ctr, cudaStream_t s) { launch_k(k_emit_finalize, 1, 32, 0, s, ctr); }
 void launch_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW, int rank,
                           int world, int32_t* local_idx, unsigned long long* n_local, uint64_t* outbox,
                           unsigned long long* n_out, int32_t* remote_status, cudaStream_t s) {
-    k_route_emitted<<<grid_for(n_cap, 256), 256, 0, s>>>(scratch, ctr_n, n_cap, KW, rank, world, local_idx, n_local,
+    launch_k(k_route_emitted, grid_for(n_cap, 256),  256,  0,  s, scratch, ctr_n, n_cap, KW, rank, world, local_idx, n_local,
                                                           outbox, n_out, remote_status);
-    ++g_launch_count;
 }
 
 // dst[i] = src[idx[i]] (KW words each), host-sized
 __global__ void k_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst) {
+    pdl_enter();
     GRID_STRIDE(t, n * KW) {
         int64_t i = t / KW;
         int w = (int)(t - i * KW);
@@ -321,12 +327,13 @@ __global__ void k_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n
     }
 }
 void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int KW, uint64_t* dst, cudaStream_t s) {
-    if (n > 0) { k_gather_keys<<<grid_for(n * KW, 256), 256, 0, s>>>(src, idx, n, KW, dst); ++g_launch_count; }
+    if (n > 0) { launch_k(k_gather_keys, grid_for(n * KW, 256), 256, 0, s, src, idx, n, KW, dst); }
 }
 
 // open-edge count (edges with a box plane among their transition refs)
 __global__ void k_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
                              unsigned long long* out) {
+    pdl_enter();
     GRID_STRIDE(v, nv) {
         bool hit = false;
         for (int q = 0; q < enr[v]; q++) hit |= refs[roff[v] + q] >= box0;
@@ -335,7 +342,7 @@ __global__ void k_open_edges(const int32_t* enr, const int64_t* roff, const int3
 }
 void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
                        unsigned long long* out, cudaStream_t s) {
-    if (nv > 0) { k_open_edges<<<grid_for(nv, 256), 256, 0, s>>>(enr, roff, refs, nv, box0, out); ++g_launch_count; }
+    if (nv > 0) { launch_k(k_open_edges, grid_for(nv, 256), 256, 0, s, enr, roff, refs, nv, box0, out); }
 }
 
 // ------------------------------------------------------- probe records
@@ -343,6 +350,7 @@ void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* r
 // pending list (targets owned by another rank cannot be checked here: forward them)
 __global__ void k_prec_target(ProbeRecs R, const int32_t* status, const int32_t* dup_ref, const int32_t* pool_idx,
                               unsigned long long* ctr, int64_t cap, double* probe_pts, int64_t cap_probe) {
+    pdl_enter();
     const int64_t n = dev_count(ctr + C_NPREC, cap);
     const int par = (int)(ctr[C_PPAR] & 1ull);
     GRID_STRIDE(i, n) {
@@ -368,6 +376,7 @@ __global__ void k_prec_target(ProbeRecs R, const int32_t* status, const int32_t*
 // forward-evaluated; targets still queued keep the record for a later iteration
 __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsigned long long* ctr, int64_t cap,
                           double* probe_pts, int64_t cap_probe) {
+    pdl_enter();
     const int64_t n = dev_count(ctr + C_NPEND, cap);
     const int par = (int)(ctr[C_PPAR] & 1ull);
     GRID_STRIDE(i, n) {
@@ -410,6 +419,7 @@ __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsign
 }
 
 __global__ void k_pend_finalize(unsigned long long* ctr) {
+    pdl_enter();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         ctr[C_PREC_TOTAL] += ctr[C_NPREC];
         ctr[C_PROBES_TOTAL] += ctr[C_NPROBE];   // (may overshoot the buffer; capped where consumed)
@@ -419,41 +429,41 @@ __global__ void k_pend_finalize(unsigned long long* ctr) {
 }
 
 __global__ void k_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap) {
+    pdl_enter();
     const int64_t n = dev_count(n_dev, cap) * KW;
     GRID_STRIDE(i, n) keys[i] = 0;
 }
 
 void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t* dup_ref, const int32_t* pool_idx,
                         unsigned long long* ctr, int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s) {
-    k_prec_target<<<grid_for(cap, 256), 256, 0, s>>>(R, status, dup_ref, pool_idx, ctr, cap, probe_pts, cap_probe);
-    ++g_launch_count;
+    launch_k(k_prec_target, grid_for(cap, 256),  256,  0,  s, R, status, dup_ref, pool_idx, ctr, cap, probe_pts, cap_probe);
 }
 void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr, int64_t cap,
                     double* probe_pts, int64_t cap_probe, cudaStream_t s) {
-    k_resolve<<<grid_for(cap, 256), 256, 0, s>>>(R, H, val_buf, ctr, cap, probe_pts, cap_probe);
-    ++g_launch_count;
+    launch_k(k_resolve, grid_for(cap, 256),  256,  0,  s, R, H, val_buf, ctr, cap, probe_pts, cap_probe);
 }
-void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s) { k_pend_finalize<<<1, 32, 0, s>>>(ctr); ++g_launch_count; }
+void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s) { launch_k(k_pend_finalize, 1, 32, 0, s, ctr); }
 void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, cudaStream_t s) {
-    k_zero_keys<<<grid_for(cap * KW, 256), 256, 0, s>>>(keys, n_dev, KW, cap);
-    ++g_launch_count;
+    launch_k(k_zero_keys, grid_for(cap * KW, 256),  256,  0,  s, keys, n_dev, KW, cap);
 }
 
 // owner rank of each key (outbox grouping)
 __global__ void k_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner) {
+    pdl_enter();
     GRID_STRIDE(i, n) owner[i] = key_owner(keys + i * KW, KW, world);
 }
 void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s) {
-    if (n > 0) { k_owner<<<grid_for(n, 256), 256, 0, s>>>(keys, n, KW, world, owner); ++g_launch_count; }
+    if (n > 0) { launch_k(k_owner, grid_for(n, 256), 256, 0, s, keys, n, KW, world, owner); }
 }
 
 __global__ void k_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
                                unsigned long long* cnt) {
+    pdl_enter();
     GRID_STRIDE(i, n) if (key_owner(keys + i * KW, KW, world) == rank) idx[atomicAdd(cnt, 1ull)] = (int32_t)i;
 }
 void launch_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
                          unsigned long long* cnt, cudaStream_t s) {
-    if (n > 0) { k_filter_owned<<<grid_for(n, 256), 256, 0, s>>>(keys, n, KW, rank, world, idx, cnt); ++g_launch_count; }
+    if (n > 0) { launch_k(k_filter_owned, grid_for(n, 256), 256, 0, s, keys, n, KW, rank, world, idx, cnt); }
 }
 
 }  // namespace am

@@ -23,6 +23,32 @@ constexpr uint64_t kEmpty = ~0ull;
 // number of kernels this library launched (bench.py gpu_launches)
 extern unsigned long long g_launch_count;
 
+// Programmatic dependent launch: every kernel is launched with programmatic stream
+// serialization and starts with pdl_enter() -- it waits for the preceding kernel's memory
+// (griddepcontrol.wait) and immediately lets its own dependents begin launching, so the
+// ~30 kernels of a BFS iteration overlap their launch latency with the predecessor's tail
+// (also inside the captured CUDA graph).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ++g_launch_count;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ------------------------------------------------------------------ keys
 __host__ __device__ inline int key_bit(const uint64_t* k, int i) {
     return (int)((k[i >> 6] >> (63 - (i & 63))) & 1ull);
@@ -91,7 +117,7 @@ int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t col
 enum Ctr {
     C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_OVF0, C_OVF1, C_CAPPED, C_TOTAL, C_QHEAD, C_QTAIL, C_NR, C_NX,
     C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_NPREC, C_NPEND, C_PPAR,
-    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_N
+    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_N
 };
 
 // hash set (am_hash.cu)
@@ -211,6 +237,7 @@ struct FaceArgs {
     int32_t* pool_vn;
     int64_t* pool_voff;
     unsigned long long* dbg;   // instrumentation (AM_FACE_STATS builds), may be null
+    unsigned long long* cursor;   // work-distribution counter (zeroed by k_take each iteration)
 };
 constexpr int kEmitFlipsPerCell = 48;   // face kernel EMAXC
 constexpr int kVertsPerCell = 64;       // face kernel QMAX

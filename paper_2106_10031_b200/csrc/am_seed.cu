@@ -9,6 +9,7 @@ static inline unsigned nb(int64_t n) { return (unsigned)((n + 127) / 128); }
 // x_proj = x - (n.x + c)/nn * n on the face plane of canonical(s); nn <= 0 -> done
 __global__ void k_seed_project(const double* X, const double* faces, const uint64_t* keys, int KW, int M,
                                int ensemble, int64_t n, const int32_t* active, double* Xp, int32_t* done_flat) {
+    pdl_enter();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     done_flat[i] = 0;
@@ -28,6 +29,7 @@ __global__ void k_seed_project(const double* X, const double* faces, const uint6
 // with result = canon.  Otherwise: snew == canon -> result = canon, inactive; else x = xp, s = snew.
 __global__ void k_seed_check(const uint64_t* snew, const uint64_t* canon, int KW, int64_t n, int32_t* active,
                              double* X, const double* Xp, uint64_t* S, uint64_t* result, int32_t* done_flat) {
+    pdl_enter();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || !active[i]) return;
     if (!snew) {
@@ -49,16 +51,17 @@ __global__ void k_seed_check(const uint64_t* snew, const uint64_t* canon, int KW
 
 void launch_seed_project(const double* X, const double* faces, const uint64_t* keys, int KW, int M, int ensemble,
                          int64_t n, const int32_t* active, double* Xp, int32_t* done_flat, cudaStream_t s) {
-    if (n > 0) { k_seed_project<<<nb(n), 128, 0, s>>>(X, faces, keys, KW, M, ensemble, n, active, Xp, done_flat); ++g_launch_count; }
+    if (n > 0) { launch_k(k_seed_project, nb(n), 128, 0, s, X, faces, keys, KW, M, ensemble, n, active, Xp, done_flat); }
 }
 void launch_seed_check(const uint64_t* snew, const uint64_t* canon, int KW, int64_t n, int32_t* active, double* X,
                        const double* Xp, uint64_t* S, uint64_t* result, int32_t* done_flat, cudaStream_t s) {
-    if (n > 0) { k_seed_check<<<nb(n), 128, 0, s>>>(snew, canon, KW, n, active, X, Xp, S, result, done_flat); ++g_launch_count; }
+    if (n > 0) { launch_k(k_seed_check, nb(n), 128, 0, s, snew, canon, KW, n, active, X, Xp, S, result, done_flat); }
 }
 
 // one bisection step given F(mid) (reference seeding.py:96-112)
 __global__ void k_dichotomy_step(const double* vals, double* xp, double* xn, double* fp, double* fn, double* mid,
                                  int32_t* active, double* out, int64_t n, double eps, double seed_tol, int last) {
+    pdl_enter();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || !active[i]) return;
     double fm = vals[i];
@@ -83,24 +86,26 @@ __global__ void k_dichotomy_step(const double* vals, double* xp, double* xn, dou
 void launch_dichotomy_step(const double* vals, double* xp, double* xn, double* fp, double* fn, double* mid,
                            int32_t* active, double* out, int64_t n, double eps, double seed_tol, int last,
                            cudaStream_t s) {
-    if (n > 0) { k_dichotomy_step<<<nb(n), 128, 0, s>>>(vals, xp, xn, fp, fn, mid, active, out, n, eps, seed_tol, last); ++g_launch_count; }
+    if (n > 0) { launch_k(k_dichotomy_step, nb(n), 128, 0, s, vals, xp, xn, fp, fn, mid, active, out, n, eps, seed_tol, last); }
 }
 
 }  // namespace am
 
 namespace am {
 __global__ void k_midpoint(const double* a, const double* b, double* m, int64_t n) {
+    pdl_enter();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n * 3) m[i] = 0.5 * (a[i] + b[i]);
 }
 void launch_midpoint(const double* a, const double* b, double* m, int64_t n, cudaStream_t s) {
-    if (n > 0) { k_midpoint<<<(unsigned)((n * 3 + 127) / 128), 128, 0, s>>>(a, b, m, n); ++g_launch_count; }
+    if (n > 0) { launch_k(k_midpoint, (unsigned)((n * 3 + 127) / 128), 128, 0, s, a, b, m, n); }
 }
 __global__ void k_count_active(const int32_t* active, int64_t n, unsigned long long* cnt) {
+    pdl_enter();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n && active[i]) atomicAdd(cnt, 1ull);
 }
 void launch_count_active(const int32_t* active, int64_t n, unsigned long long* cnt, cudaStream_t s) {
-    if (n > 0) { k_count_active<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(active, n, cnt); ++g_launch_count; }
+    if (n > 0) { launch_k(k_count_active, (unsigned)((n + 127) / 128), 128, 0, s, active, n, cnt); }
 }
 }  // namespace am
