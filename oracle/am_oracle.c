@@ -1071,3 +1071,122 @@ void om_result_free(om_result *R) {
     if (!R) return;
     free(R->keys); free(R->nverts); free(R->verts); free(R->enr); free(R->erefs); free(R);
 }
+
+/* ------------------------------------------------ sharding / per-cell API */
+/* owner rank of a state: identical arithmetic to csrc/am_internal.h key_owner (GPU) */
+static uint64_t g_mix64(uint64_t x) {
+    x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27; x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+static uint64_t gpu_key_hash(const uint64_t *k, int kw) {
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ (uint64_t)kw;
+    for (int i = 0; i < kw; i++) {
+        uint64_t x = g_mix64(k[i] + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1));
+        h = (h ^ x) * 0x100000001B3ull;
+        h ^= h >> 29;
+    }
+    return g_mix64(h);
+}
+void om_key_owner(const uint64_t *keys, long n, int kw, int world, int32_t *out) {
+    for (long i = 0; i < n; i++)
+        out[i] = world <= 1 ? 0 : (int32_t)((gpu_key_hash(keys + i * kw, kw) >> 7) % (uint64_t)world);
+}
+
+/* canonical key of a raw state (reference network.py:446-489) */
+void om_canonical(const om_net *net, const uint64_t *key, uint64_t *canon) {
+    double *buf = alloc_buf(net);
+    om_maps m;
+    maps_alloc(net, &m);
+    affine_maps(net, key, &m, buf);
+    memcpy(canon, m.key, (size_t)net->kw * 8);
+    maps_free(&m);
+    free(buf);
+}
+
+/* face of one canonical state (naive enumeration, reference cells.py:337-362) and its
+ * neighbour candidates (transition states + probe states, reference marching.py:152-288).
+ * Returns the number of candidates written (<= max_out), -1 if the face is empty. */
+long om_cell_expand(const om_net *net, const uint64_t *key, const double *bbox6, uint64_t *out, long max_out) {
+    om_cfg cfg;
+    cfg.tol_cell = 1e-9; cfg.tol_weld = 1e-7; cfg.tol_onplane = 1e-9; cfg.probe_delta = 1e-7;
+    for (int k = 0; k < 3; k++) { cfg.lo[k] = bbox6[k]; cfg.hi[k] = bbox6[3 + k]; }
+    double *buf = alloc_buf(net);
+    om_maps m;
+    maps_alloc(net, &m);
+    affine_maps(net, key, &m, buf);
+    om_cell cl;
+    cell_alloc(net, &cl);
+    build_cell(net, &m, &cfg, &cl);
+    om_poly *P = extract_naive(&cl, &cfg);
+    long nout = -1;
+    if (P) {
+        nout = 0;
+        int kw = net->kw, off = 0;
+        for (int e = 0; e < P->nv; e++) {
+            const ref_t *er = P->erefs + off;
+            int ne = P->enr[e];
+            off += ne;
+            int bits[64], brs[64], nb = 0, nbr = 0;
+            ref_t first = {-1, -1};
+            for (int i = 0; i < ne; i++) {
+                if (er[i].kind == K_BBOX) continue;
+                if (first.kind < 0) first = er[i];
+                if (er[i].kind == K_NEURON && nb < 64) bits[nb++] = er[i].index;
+                else if (er[i].kind == K_BRANCH && nbr < 64) brs[nbr++] = er[i].index;
+            }
+            if (first.kind < 0) continue;
+            /* subsets exactly as process(): combinations (nb <= 3) or singles + full + () */
+            int big = nb > 3, nsub = 0, masks[16];
+            if (!big) {
+                for (int k = 0; k <= nb; k++) {
+                    int idx[4];
+                    for (int i = 0; i < k; i++) idx[i] = i;
+                    for (;;) {
+                        int mk = 0;
+                        for (int i = 0; i < k; i++) mk |= 1 << idx[i];
+                        masks[nsub++] = mk;
+                        int i = k - 1;
+                        while (i >= 0 && idx[i] == nb - k + i) i--;
+                        if (i < 0) break;
+                        idx[i]++;
+                        for (int t = i + 1; t < k; t++) idx[t] = idx[t - 1] + 1;
+                    }
+                }
+            } else {
+                nsub = nb + 2;
+            }
+            for (int si = 0; si < nsub; si++) {
+                for (int ti = -1; ti < nbr; ti++) {
+                    int empty = big ? si == nb + 1 : masks[si] == 0;
+                    if (empty && ti < 0) continue;
+                    if (nout >= max_out) continue;
+                    uint64_t *t = out + nout * kw;
+                    memcpy(t, m.key, (size_t)kw * 8);
+                    if (big) {
+                        if (si < nb) key_flip(t, bits[si]);
+                        else if (si == nb) for (int i = 0; i < nb; i++) key_flip(t, bits[i]);
+                    } else {
+                        for (int i = 0; i < nb; i++) if (masks[si] & (1 << i)) key_flip(t, bits[i]);
+                    }
+                    if (ti >= 0) t[kw - 1] = (uint64_t)brs[ti];
+                    nout++;
+                }
+            }
+            int prow = first.kind == K_NEURON ? cl.row_of[first.index] : cl.row_of[net->n_bits + first.index];
+            if (prow >= 0 && nout < max_out) {
+                const double *p0 = P->v + e * 3, *p1 = P->v + ((e + 1) % P->nv) * 3;
+                double pp[3];
+                for (int d = 0; d < 3; d++) pp[d] = 0.5 * (p0[d] + p1[d]) + cfg.probe_delta * cl.n[prow * 3 + d];
+                om_forward_state(net, pp, out + nout * kw, buf);
+                nout++;
+            }
+        }
+        poly_free(P);
+    }
+    cell_free(&cl);
+    maps_free(&m);
+    free(buf);
+    return nout;
+}

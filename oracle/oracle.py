@@ -56,6 +56,10 @@ def lib():
         L.om_result_counts.argtypes = [P, P]
         L.om_result_copy.argtypes = [P, P, P, P, P, P]
         L.om_result_free.argtypes = [P]
+        L.om_key_owner.argtypes = [P, ctypes.c_long, ctypes.c_int, ctypes.c_int, P]
+        L.om_canonical.argtypes = [P, P, P]
+        L.om_cell_expand.restype = ctypes.c_long
+        L.om_cell_expand.argtypes = [P, P, P, P, ctypes.c_long]
         _lib = L
     return _lib
 
@@ -257,3 +261,100 @@ def march(net: AnyNetwork, bbox=DEFAULT_BBOX, seeds: int = 64, scheme: str = "di
                   seeds_used=len(seed_pts), threads=threads)
     return OracleResult(kb, branch, keys, nverts > 0, nverts.astype(np.int64), verts,
                         enr.astype(np.int64), erefs.astype(np.int64), report, seed_pts)
+
+
+# ------------------------------------------------------- sharded-march stand-in
+
+def key_owner(keys: np.ndarray, world: int) -> np.ndarray:
+    """Owner rank per key (same hash as the GPU engine's key_owner)."""
+    k = np.ascontiguousarray(keys, dtype=np.uint64).reshape(len(keys), -1)
+    out = np.zeros(len(k), dtype=np.int32)
+    lib().om_key_owner(_ptr(k), len(k), k.shape[1], int(world), _ptr(out))
+    return out
+
+
+class OracleShardEngine:
+    """CPU stand-in with the GPU Engine's wave/outbox/push interface (tests of the sharded
+    driver over gloo).  Same semantics as the engine: a set of dispatched raw keys, a set
+    of visited canonical states, ownership owner(state) = hash % world."""
+
+    def __init__(self, net, bbox=DEFAULT_BBOX, max_cells=10_000_000, rank=0, world=1, **_):
+        self.on = OracleNet(net)
+        self.kw = self.on.kw
+        self.rank, self.world = rank, world
+        self.bbox = np.array(list(bbox[0]) + list(bbox[1]), dtype=np.float64)
+        self.net = net
+        self.reset()
+
+    def reset(self):
+        self.seen = set()
+        self.visited = set()
+        self.queue = []
+        self.out = []
+
+    def _owner(self, k):
+        return int(key_owner(np.asarray(k, dtype=np.uint64).reshape(1, -1), self.world)[0])
+
+    def _route(self, keys):
+        for k in keys:
+            k = np.asarray(k, dtype=np.uint64)
+            if self._owner(k) == self.rank:
+                t = k.tobytes()
+                if t not in self.seen:
+                    self.seen.add(t)
+                    self.queue.append(k)
+            else:
+                self.out.append(k)
+
+    def seed(self, pts):
+        from paper_2106_10031_b200 import network as _n  # noqa: F401
+        keys = []
+        for x in np.asarray(pts, dtype=np.float64).reshape(-1, 3):
+            # reference marching.py:201-213 via the oracle march of one seed with max_cells=1
+            r = march(self.net, bbox=(tuple(self.bbox[:3]), tuple(self.bbox[3:])), seed_points=x.reshape(1, 3),
+                      max_cells=1, oracle_net=self.on)
+            keys.append(r.key_words[0])
+        self._route(keys)
+
+    def wave(self):
+        todo, self.queue = self.queue, []
+        new = 0
+        buf = np.zeros((512, self.kw), dtype=np.uint64)
+        for r in todo:
+            canon = np.zeros(self.kw, dtype=np.uint64)
+            lib().om_canonical(self.on.h, _ptr(np.ascontiguousarray(r)), _ptr(canon))
+            if self._owner(canon) != self.rank:
+                self.out.append(canon)
+                continue
+            ct = canon.tobytes()
+            if ct in self.visited:
+                continue
+            self.visited.add(ct)
+            self.seen.add(ct)
+            new += 1
+            n = lib().om_cell_expand(self.on.h, _ptr(canon), _ptr(self.bbox), _ptr(buf), len(buf))
+            if n > 0:
+                self._route(list(buf[:n].copy()))
+        return new
+
+    def outbox(self):
+        import torch
+        counts = np.zeros(self.world, dtype=np.int64)
+        if not self.out:
+            return counts, torch.zeros((0, self.kw), dtype=torch.int64)
+        keys = np.stack(self.out)
+        self.out = []
+        own = key_owner(keys, self.world)
+        order = np.argsort(own, kind="stable")
+        for o in own:
+            counts[o] += 1
+        return counts, torch.from_numpy(keys[order].view(np.int64).copy())
+
+    def queue_size(self):
+        return len(self.queue)
+
+    def push(self, keys):
+        self._route([np.asarray(k).view(np.uint64) for k in keys.numpy()])
+
+    def visited_keys(self):
+        return sorted(self.visited)

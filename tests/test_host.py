@@ -1,0 +1,108 @@
+"""CPU-only checks of the host side and the C-ABI boundary (no GPU needed)."""
+
+import ctypes
+import json
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, REPO, load_golden
+
+from paper_2106_10031_b200 import network as N
+from paper_2106_10031_b200 import synth
+
+
+def header_functions():
+    src = open(os.path.join(REPO, "include", "am_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(am_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2106_10031_b200 import _native
+    lib = _native.load()          # loading needs no GPU
+    for name in header_functions():
+        assert hasattr(lib, name), f"{name} declared in include/am_b200.h but not exported"
+    assert set(_native.SIGNATURES) >= set(header_functions())
+
+
+def test_library_is_sm100a():
+    so = os.path.join(REPO, "paper_2106_10031_b200", "_lib", "libam_b200.so")
+    out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    assert "DMMA" in sass and "UTMALDG" in sass     # fp64 tensor cores + TMA in the composition GEMM
+
+
+def test_no_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2106_10031_b200 import marching, _native
+    with pytest.raises(_native.NativeUnavailable):
+        marching.march(N.octahedron_net(0.5), marching.MarchConfig(seeds=2))
+
+
+@pytest.mark.parametrize("name", ["oct", "cube", "res_linear", "deepsdf_small", "imnet_small"])
+def test_interchange_roundtrip(name, tmp_path):
+    net = N.load_network(os.path.join(GOLDEN, name + ".json"))
+    p = tmp_path / "n.json"
+    N.save_network(net, p)
+    net2 = N.load_network(p)
+    b1, b2 = N.to_blob(net), N.to_blob(net2)
+    np.testing.assert_array_equal(b1.params, b2.params)
+    np.testing.assert_array_equal(b1.steps, b2.steps)
+    assert json.load(open(p)) == json.load(open(os.path.join(GOLDEN, name + ".json"))) or name in ("res_linear",)
+
+
+def test_blob_layout_deepsdf():
+    net = synth.deepsdf_mlp(width=16, depth=6, skip_at=3, seed=0)
+    b = N.to_blob(net)
+    assert b.n_bits == 6 * 16 and b.n_subs == 1 and not b.ensemble
+    flags = b.steps[:, 4]
+    assert flags[0] & N.STEP_FIRST and flags[0] & N.STEP_SAVE_INPUT
+    assert flags[2] & N.STEP_SHORTCUT_LINEAR and flags[2] & N.STEP_SC_FROM_INPUT
+    assert list(b.steps[:, 7]) == [0, 16, 32, 48, 64, 80]          # row offsets in bit order
+    assert list(b.steps[:, 8]) == [-1, 0, 16, 32, 48, 64]
+
+
+def test_key_packing_matches_reference_packbits():
+    from paper_2106_10031_b200.marching import words_to_packbits
+    rng = np.random.default_rng(0)
+    for n_bits in (6, 64, 65, 540, 4096):
+        bits = rng.integers(0, 2, size=n_bits).astype(np.uint8)
+        kw = (n_bits + 63) // 64
+        words = np.zeros(kw, dtype=np.uint64)
+        for i, b in enumerate(bits):
+            if b:
+                words[i >> 6] |= np.uint64(1) << np.uint64(63 - (i & 63))
+        kb, br = words_to_packbits(words.reshape(1, -1), n_bits, False)
+        assert kb[0].tobytes() == N.StateVector.from_bits(bits).key
+        assert br[0] == -1
+
+
+def test_region_count_lower_bound():
+    assert N.region_count_lower_bound([3], 2) == 7
+    assert N.region_count_lower_bound([2, 2], 1) == 6
+    with pytest.raises(ValueError):
+        N.region_count_lower_bound([2], 3)
+
+
+def test_network_validation_errors():
+    with pytest.raises(N.NetworkFormatError):
+        N.NetworkSpec((N.DenseLayer(np.ones((6, 3)), np.zeros(6)),), np.ones(5), 0.0)
+    with pytest.raises(N.NetworkFormatError):
+        N.network_from_dict({"field_kind": "sdf", "subnetworks": []})
+    with pytest.raises(N.NetworkFormatError):
+        N.EnsembleSpec((N.octahedron_net(0.5), N.octahedron_net(0.5, field_kind="occupancy")))
+
+
+def test_golden_fixtures_are_self_consistent():
+    for name in ("oct", "geo_60x60"):
+        g = load_golden(name)
+        assert len(g["keys"]) == g["report"]["cells_visited"]
+        assert g["nverts"].sum() == len(g["verts"])
+        assert g["edge_nrefs"].sum() == len(g["edge_refs"])
