@@ -24,7 +24,7 @@
 
 namespace am {
 
-constexpr int BM = 64, BN = 64, BK = 16, XLD = 20;  // XLD: padded k-stride of the X tile
+constexpr int BM = 64, BN = 64, BK = 16;
 constexpr int kThreads = 256;   // 8 warps: 2 (rows) x 4 (columns), 32 x 16 outputs each
 
 // ------------------------------------------------------------ PTX helpers
@@ -93,68 +93,73 @@ __device__ __forceinline__ void set_key_bit(uint64_t* key, int row, int bit) {
 // ------------------------------------------------------ input step (l = 1)
 // reference network.py:398-443 with A = I, c = 0: pre_A = W[:, :3] (+ shortcut
 // from the input), pre_c = (sc + 0) + b.
+// reference network.py:398-443 with A = I, c = 0 for one (item, neuron)
+template <int C>
+__device__ __forceinline__ void input_elem(const LayerLaunch& L, uint64_t* keys, int64_t item, int r) {
+    const StepDev& st = L.st;
+    const double* w = st.W + (int64_t)r * st.ldw;
+    uint64_t* key = keys + item * L.KW;
+    int row = st.row_off + r;
+    double* z = L.Z + (item * L.zs + row) * C;
+    bool sc = st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR);
+    if (C == 4) {
+        double a0 = w[0], a1 = w[1], a2 = w[2], c = 0.0;
+        if (sc) {
+            double s0, s1, s2, sc_c = 0.0;
+            if (st.flags & AM_STEP_SHORTCUT_IDENT) {
+                s0 = r == 0; s1 = r == 1; s2 = r == 2;
+            } else {
+                const double* v = st.V + (int64_t)r * st.ldv;
+                s0 = v[0]; s1 = v[1]; s2 = v[2];
+                if (st.vb) sc_c = st.vb[r];
+            }
+            a0 = s0 + a0; a1 = s1 + a1; a2 = s2 + a2;
+            c = (sc_c + c) + st.b[r];
+        } else {
+            c = c + st.b[r];
+        }
+        double nrm = sqrt((a0 * a0 + a1 * a1) + a2 * a2);
+        if (!(nrm > kDegen)) {
+            int bit = c > 0.0;
+            if (bit != key_bit(key, row)) {
+                set_key_bit(key, row, bit);
+                if (L.changed) L.changed[item] = 1;
+            }
+        }
+        reinterpret_cast<double2*>(z)[0] = make_double2(a0, a1);
+        reinterpret_cast<double2*>(z)[1] = make_double2(a2, c);
+    } else {
+        const double* x = L.pts + item * 3;
+        double acc = (x[0] * w[0] + x[1] * w[1]) + x[2] * w[2];
+        double pre;
+        if (sc) {
+            double s;
+            if (st.flags & AM_STEP_SHORTCUT_IDENT) {
+                s = x[r];
+            } else {
+                const double* v = st.V + (int64_t)r * st.ldv;
+                s = (x[0] * v[0] + x[1] * v[1]) + x[2] * v[2];
+                if (st.vb) s = s + st.vb[r];
+            }
+            pre = (s + acc) + st.b[r];
+        } else {
+            pre = acc + st.b[r];
+        }
+        if (pre > 0.0) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)key_mask(row));
+        z[0] = pre;
+    }
+}
+
 template <int C>
 __global__ void k_input_step(LayerLaunch L) {
     pdl_enter();
-    const StepDev& st = L.st;
     const int64_t n = dev_count(L.n_dev, L.n_cap);
     uint64_t* keys = keys_at(L);
-    const int64_t total = n * st.n_out;
+    const int64_t total = n * L.st.n_out;
     for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
          gid += (int64_t)gridDim.x * blockDim.x) {
-        int64_t item = gid / st.n_out;
-        int r = (int)(gid - item * st.n_out);
-        const double* w = st.W + (int64_t)r * st.ldw;
-        uint64_t* key = keys + item * L.KW;
-        int row = st.row_off + r;
-        double* z = L.Z + (item * L.zs + row) * C;
-        bool sc = st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR);
-        if (C == 4) {
-            double a0 = w[0], a1 = w[1], a2 = w[2], c = 0.0;
-            if (sc) {
-                double s0, s1, s2, sc_c = 0.0;
-                if (st.flags & AM_STEP_SHORTCUT_IDENT) {
-                    s0 = r == 0; s1 = r == 1; s2 = r == 2;
-                } else {
-                    const double* v = st.V + (int64_t)r * st.ldv;
-                    s0 = v[0]; s1 = v[1]; s2 = v[2];
-                    if (st.vb) sc_c = st.vb[r];
-                }
-                a0 = s0 + a0; a1 = s1 + a1; a2 = s2 + a2;
-                c = (sc_c + c) + st.b[r];
-            } else {
-                c = c + st.b[r];
-            }
-            double nrm = sqrt((a0 * a0 + a1 * a1) + a2 * a2);
-            if (!(nrm > kDegen)) {
-                int bit = c > 0.0;
-                if (bit != key_bit(key, row)) {
-                    set_key_bit(key, row, bit);
-                    if (L.changed) L.changed[item] = 1;
-                }
-            }
-            reinterpret_cast<double2*>(z)[0] = make_double2(a0, a1);
-            reinterpret_cast<double2*>(z)[1] = make_double2(a2, c);
-        } else {
-            const double* x = L.pts + item * 3;
-            double acc = (x[0] * w[0] + x[1] * w[1]) + x[2] * w[2];
-            double pre;
-            if (sc) {
-                double s;
-                if (st.flags & AM_STEP_SHORTCUT_IDENT) {
-                    s = x[r];
-                } else {
-                    const double* v = st.V + (int64_t)r * st.ldv;
-                    s = (x[0] * v[0] + x[1] * v[1]) + x[2] * v[2];
-                    if (st.vb) s = s + st.vb[r];
-                }
-                pre = (s + acc) + st.b[r];
-            } else {
-                pre = acc + st.b[r];
-            }
-            if (pre > 0.0) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)key_mask(row));
-            z[0] = pre;
-        }
+        int64_t item = gid / L.st.n_out;
+        input_elem<C>(L, keys, item, (int)(gid - item * L.st.n_out));
     }
 }
 
@@ -178,16 +183,26 @@ void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
 }
 
 // ----------------------------------------------------------- GEMM step
+struct SubDev {
+    int last_row, last_n;
+    const double* hw;
+    double hb;
+};
+
 constexpr int NST = 4;     // pipeline stages (BK = 16 rows of K each)
 constexpr int XS4 = 64;    // compose stage: per-item stride (16 rows x 4 components, contiguous as in Z)
 constexpr int XS1 = 20;    // forward stage: per-point padded stride (bank-conflict free B fragments)
 
+constexpr int KCW = 10;    // cached state words per item and K segment (K rows <= 576)
+
 template <int C>
 struct __align__(1024) GemmSmem {
     static constexpr int XSZ = C == 4 ? 16 * XS4 : BN * XS1;
+    static constexpr int NI = C == 4 ? 16 : BN;   // items per tile
     double w[NST][BM * BK];        // TMA destination, 128B-swizzled, 8 KB per stage
     double x[NST][XSZ];            // raw activation tile
     uint32_t mask[NST][BN];        // per item / point: the 16 state bits of the stage's K rows
+    uint64_t kc[2][NI][KCW];       // the tile's state words covering each K segment
     uint64_t bar[NST];
     unsigned long long bits[BN][2];  // forward epilogue: per-column bit window
 };
@@ -222,50 +237,44 @@ __device__ __forceinline__ uint32_t bits16(const uint64_t* key, int row, int val
     return m;
 }
 
-// Persistent: each CTA walks output tiles (64 neuron rows x 64 item columns) of the
-// device-resident item count (graph-capturable).  K is streamed in 16-row chunks through an
-// NST-stage ring: W by TMA (mbarrier), the raw activations by cp.async, the state mask of the
-// chunk as 16-bit words -- applied when the B fragments are read, so padding rows and
-// inactive neurons contribute exact zeros.
+// One 64-row x 64-column output tile of layer L.st (all K chunks + epilogue).
 template <int C>
-__global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
-                                                        const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
-    pdl_enter();
-    extern __shared__ uint8_t smem_raw[];
-    GemmSmem<C>& S = *reinterpret_cast<GemmSmem<C>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+__device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, uint64_t* keys, int64_t n,
+                                          const CUtensorMap* tmWp, const CUtensorMap* tmVp, int m0, int64_t n0,
+                                          uint32_t& gchunk) {
     const StepDev& st = L.st;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp & 1, wn = warp >> 1;   // warp tile: rows wm*32 .. +31, columns wn*16 .. +15
-    const int64_t n = dev_count(L.n_dev, L.n_cap);
-    if (n <= 0) return;
-    uint64_t* keys = keys_at(L);
-
     const bool lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && !(st.flags & AM_STEP_SC_FROM_INPUT);
     const int kc0 = (st.n_in + BK - 1) / BK;
     const int kc1 = lin ? (st.n_sin + BK - 1) / BK : 0;
     const int nchunks = kc0 + kc1;
-    const int64_t ntx = (n * C + BN - 1) / BN;
-    const int nty = (st.n_out + BM - 1) / BM;
-    const int64_t ntiles = ntx * nty;
-
-    if (tid < NST) mbar_init(&S.bar[tid], 1);
-    if (tid == 0) {
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
-    }
-    __syncthreads();
-
     const bool sc_ident = st.flags & AM_STEP_SHORTCUT_IDENT;
     const bool sc_input_lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && (st.flags & AM_STEP_SC_FROM_INPUT);
     const bool sc_input_id = sc_ident && (st.flags & AM_STEP_SC_FROM_INPUT);
     const bool has_sc = (st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR)) != 0;
-
-    uint32_t gchunk = 0;  // chunks consumed by this CTA so far (stage ring + mbarrier phases)
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = (int)(tile / ntx) * BM;
-        const int64_t n0 = (tile % ntx) * BN;
+    {
         if (C == 1 && tid < BN) { S.bits[tid][0] = 0; S.bits[tid][1] = 0; }
+        // state words of the tile's items covering both K segments (no global reads in issue())
+        constexpr int NI = GemmSmem<C>::NI;
+        const int64_t item0 = C == 4 ? n0 / 4 : n0;
+        int wbeg[2], wcnt[2];
+        wbeg[0] = st.in_row_off >> 6;
+        wcnt[0] = ((st.in_row_off + st.n_in - 1) >> 6) - wbeg[0] + 1;
+        wbeg[1] = lin ? st.sin_row_off >> 6 : 0;
+        wcnt[1] = lin ? ((st.sin_row_off + st.n_sin - 1) >> 6) - wbeg[1] + 1 : 0;
+        const bool cache_ok = wcnt[0] <= KCW && wcnt[1] <= KCW;
+        if (cache_ok) {
+            for (int q = tid; q < 2 * NI * KCW; q += kThreads) {
+                const int sg = q / (NI * KCW), rem = q % (NI * KCW), il = rem / KCW, w = rem % KCW;
+                const int64_t item = item0 + il;
+                uint64_t v = 0;
+                if (item < n && w < wcnt[sg]) v = keys[item * L.KW + wbeg[sg] + w];
+                S.kc[sg][il][w] = v;
+            }
+        }
+        __syncthreads();
 
         // issue chunk c of this tile into its ring stage
         auto issue = [&](int c) {
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
             const int valid = n_src - k0;
             if (tid == 0) {
                 mbar_expect_tx(&S.bar[stage], BM * BK * sizeof(double));
-                tma_load_2d(S.w[stage], seg0 ? &tmW : &tmV, &S.bar[stage], k0, m0);
+                tma_load_2d(S.w[stage], seg0 ? tmWp : tmVp, &S.bar[stage], k0, m0);
             }
             if (C == 4) {
                 // 16 items x 512 B; 2 x 16-B pieces per thread
@@ -293,7 +302,10 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
                 }
                 if (tid < 16) {
                     const int64_t item = n0 / 4 + tid;
-                    S.mask[stage][tid] = item < n ? bits16(keys + item * L.KW, src_row + k0, valid) : 0u;
+                    const int sg = seg0 ? 0 : 1;
+                    S.mask[stage][tid] = item >= n ? 0u
+                        : cache_ok ? bits16(S.kc[sg][tid], src_row + k0 - wbeg[sg] * 64, valid)
+                                   : bits16(keys + item * L.KW, src_row + k0, valid);
                 }
             } else {
 #pragma unroll
@@ -305,7 +317,10 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
                 }
                 if (tid < BN) {
                     const int64_t item = n0 + tid;
-                    S.mask[stage][tid] = item < n ? bits16(keys + item * L.KW, src_row + k0, valid) : 0u;
+                    const int sg = seg0 ? 0 : 1;
+                    S.mask[stage][tid] = item >= n ? 0u
+                        : cache_ok ? bits16(S.kc[sg][tid], src_row + k0 - wbeg[sg] * 64, valid)
+                                   : bits16(keys + item * L.KW, src_row + k0, valid);
                 }
             }
             cp_async_commit();
@@ -319,16 +334,22 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
 #pragma unroll
                 for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
 
-        const int pro = nchunks < NST ? nchunks : NST;
+        // NST-1 chunks in flight; the stage refilled at iteration c is the one chunk c-1 used,
+        // which every warp has finished once it passes iteration c's barrier (one barrier per chunk)
+        const int pro = nchunks < NST - 1 ? nchunks : NST - 1;
         for (int c = 0; c < pro; c++) issue(c);
+        // fragment row g reads tile row pg: the 4 rows x 2 16-B chunks of a half-warp then fall on
+        // 8 distinct bank groups of the 128B-swizzled W stage
+        const int pg = ((g & 3) << 1) | (g >> 2);
 
         for (int c = 0; c < nchunks; c++) {
             const uint32_t gc = gchunk + c;
             const int s = gc % NST;
-            const int committed = (c + NST < nchunks) ? c + NST : nchunks;
-            cp_async_wait(committed - c - 1);
+            const int committed = (c + NST - 2 < nchunks - 1) ? c + NST - 2 : nchunks - 1;
+            cp_async_wait(committed - c);
             mbar_wait(&S.bar[s], (gc / NST) & 1);
             __syncthreads();
+            if (c + NST - 1 < nchunks) issue(c + NST - 1);
             const double* ws = S.w[s];
             const double* xsm = S.x[s];
 #pragma unroll
@@ -336,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
                 double a[2][2], b[2];
 #pragma unroll
                 for (int mi = 0; mi < 2; mi++) {
-                    int r = wm * 32 + mi * 16 + g;
+                    int r = wm * 32 + mi * 16 + pg;
                     a[mi][0] = ws[swz(r, kk + t)];
                     a[mi][1] = ws[swz(r + 8, kk + t)];
                 }
@@ -359,8 +380,6 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
 #pragma unroll
                     for (int nj = 0; nj < 2; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
             }
-            __syncthreads();   // stage s free again
-            if (c + NST < nchunks) issue(c + NST);
         }
         gchunk += nchunks;
 
@@ -370,7 +389,7 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
         for (int mi = 0; mi < 2; mi++) {
 #pragma unroll
             for (int half = 0; half < 2; half++) {
-                const int rl = wm * 32 + mi * 16 + g + half * 8;  // local row
+                const int rl = wm * 32 + mi * 16 + pg + half * 8;  // local row
                 const int r = m0 + rl;
                 const bool rok = r < st.n_out;
                 const int row = st.row_off + r;
@@ -474,6 +493,41 @@ __global__ void __launch_bounds__(kThreads) k_gemm_step(const __grid_constant__ 
     }
 }
 
+// Persistent: each CTA walks output tiles (64 neuron rows x 64 item columns) of the
+// device-resident item count (graph-capturable).  K is streamed in 16-row chunks through an
+// NST-stage ring: W by TMA (mbarrier), the raw activations by cp.async, the state mask of the
+// chunk as 16-bit words -- applied when the B fragments are read, so padding rows and
+// inactive neurons contribute exact zeros.
+template <int C>
+__global__ void __launch_bounds__(kThreads, 2) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
+                                                        const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
+    pdl_enter();
+    extern __shared__ uint8_t smem_raw[];
+    GemmSmem<C>& S = *reinterpret_cast<GemmSmem<C>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const StepDev& st = L.st;
+    const int tid = threadIdx.x;
+    const int64_t n = dev_count(L.n_dev, L.n_cap);
+    if (n <= 0) return;
+    uint64_t* keys = keys_at(L);
+    const int64_t ntx = (n * C + BN - 1) / BN;
+    const int nty = (st.n_out + BM - 1) / BM;
+    const int64_t ntiles = ntx * nty;
+
+    if (tid < NST) mbar_init(&S.bar[tid], 1);
+    if (tid == 0) {
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    }
+    __syncthreads();
+
+    uint32_t gchunk = 0;  // chunks consumed by this CTA so far (stage ring + mbarrier phases)
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = (int)(tile / ntx) * BM;
+        const int64_t n0 = (tile % ntx) * BN;
+        gemm_tile<C>(S, L, keys, n, &tmW, &tmV, m0, n0, gchunk);
+    }
+}
+
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV, cudaStream_t s) {
     if (L.n_cap <= 0) return;
     int64_t cols = L.n_cap * C;
@@ -492,11 +546,6 @@ void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const
 }
 
 // ------------------------------------------------------------ head kernels
-struct SubDev {
-    int last_row, last_n;
-    const double* hw;
-    double hb;
-};
 
 // face functional of every subnetwork: head_w @ (s ⊙ Z_last) (+ head_b on the offset)
 // reference network.py:440-442

@@ -357,7 +357,6 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     }
     CK(e->subdev.reserve((int64_t)(sizeof(SubDev) * e->M), e->stream));
     CK(cudaMemcpy(e->subdev.p, hsub.data(), sizeof(SubDev) * e->M, cudaMemcpyHostToDevice));
-
     // batch size from the per-iteration memory budget: compose planes + worst-case probe
     // activations + emitted keys per batch cell
     int64_t budget = e->P.mem_budget > 0 ? e->P.mem_budget : (int64_t)4 << 30;

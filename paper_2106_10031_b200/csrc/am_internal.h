@@ -107,6 +107,8 @@ __device__ __forceinline__ uint64_t* keys_at(const LayerLaunch& L) {
     return L.key_off ? L.keys + (int64_t)(*L.key_off) * L.KW : L.keys;
 }
 
+
+
 // kernels' host-side launchers (am_compose.cu)
 void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s);
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV,
