@@ -12,7 +12,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libam_b200.so")
+# AM_LIB_PATH: load an alternative in-tree build (tuning variants, tools/variants.sh)
+LIB_PATH = os.environ.get("AM_LIB_PATH") or os.path.join(HERE, "_lib", "libam_b200.so")
 
 STEP_FIELDS = 12
 SUB_FIELDS = 6

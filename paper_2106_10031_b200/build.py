@@ -14,7 +14,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "_lib", "libam_b200.so")
+OUT = os.environ.get("AM_BUILD_OUT") or os.path.join(HERE, "_lib", "libam_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=default"]
 SOURCES = {
@@ -42,7 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    objdir = os.path.join(HERE, "_lib", "obj")
+    objdir = os.path.join(os.path.dirname(OUT), "obj" if "AM_BUILD_OUT" not in os.environ
+                          else "obj_" + os.path.basename(OUT).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for name, extra in SOURCES.items():

@@ -24,7 +24,7 @@
 
 namespace am {
 
-constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int BM = 64, BN = 64, TB = 16, BK = 32;   // TB: K width of one TMA box (128 B)
 constexpr int kThreads = 256;   // 8 warps: 2 (rows) x 4 (columns), 32 x 16 outputs each
 
 // ------------------------------------------------------------ PTX helpers
@@ -75,7 +75,7 @@ int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t col
     }
     cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t gstride[1] = {(cuuint64_t)(ld_elems * sizeof(double))};
-    cuuint32_t box[2] = {BK, BM};
+    cuuint32_t box[2] = {TB, BM};
     cuuint32_t estride[2] = {1, 1};
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box,
                           estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -189,9 +189,12 @@ struct SubDev {
     double hb;
 };
 
-constexpr int NST = 4;     // pipeline stages (BK = 16 rows of K each)
-constexpr int XS4 = 64;    // compose stage: per-item stride (16 rows x 4 components, contiguous as in Z)
-constexpr int XS1 = 20;    // forward stage: per-point padded stride (bank-conflict free B fragments)
+#ifndef AM_NST
+#define AM_NST 3
+#endif
+constexpr int NST = AM_NST;   // pipeline stages (BK = 32 rows of K each)
+constexpr int XS4 = BK * 4;   // compose stage: per-item stride (32 rows x 4 components, contiguous as in Z)
+constexpr int XS1 = BK + 4;   // forward stage: per-point padded stride (bank-conflict free B fragments)
 
 constexpr int KCW = 10;    // cached state words per item and K segment (K rows <= 576)
 
@@ -199,9 +202,9 @@ template <int C>
 struct __align__(1024) GemmSmem {
     static constexpr int XSZ = C == 4 ? 16 * XS4 : BN * XS1;
     static constexpr int NI = C == 4 ? 16 : BN;   // items per tile
-    double w[NST][BM * BK];        // TMA destination, 128B-swizzled, 8 KB per stage
+    double w[NST][BK / TB][BM * TB];   // TMA destination: 2 boxes of 64 rows x 16 k, 128B-swizzled
     double x[NST][XSZ];            // raw activation tile
-    uint32_t mask[NST][BN];        // per item / point: the 16 state bits of the stage's K rows
+    uint32_t mask[NST][BN];        // per item / point: the 32 state bits of the stage's K rows
     uint64_t kc[2][NI][KCW];       // the tile's state words covering each K segment
     uint64_t bar[NST];
     unsigned long long bits[BN][2];  // forward epilogue: per-column bit window
@@ -224,16 +227,14 @@ __device__ __forceinline__ void cp_async_wait(int pending) {
         default: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
     }
 }
-// 16 state bits of rows [row, row + 16) (MSB-first key words), zero beyond `valid` rows
-__device__ __forceinline__ uint32_t bits16(const uint64_t* key, int row, int valid) {
+// 32 state bits of rows [row, row + 32) (MSB-first key words), bit j = row + j; zero beyond `valid`
+__device__ __forceinline__ uint32_t bits32(const uint64_t* key, int row, int valid) {
     if (valid <= 0) return 0u;
     int w = row >> 6, off = row & 63;
     uint64_t hi = key[w] << off;                        // bit 63 of hi = state bit of `row`
-    if (off > 48) hi |= key[w + 1] >> (64 - off);
-    uint32_t m = 0;
-#pragma unroll
-    for (int j = 0; j < 16; j++) m |= (uint32_t)((hi >> (63 - j)) & 1ull) << j;
-    if (valid < 16) m &= (1u << valid) - 1u;
+    if (off > 32 && valid > 64 - off) hi |= key[w + 1] >> (64 - off);
+    uint32_t m = __brev((uint32_t)(hi >> 32));
+    if (valid < 32) m &= (1u << valid) - 1u;
     return m;
 }
 
@@ -284,16 +285,18 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
             const int src_row = seg0 ? st.in_row_off : st.sin_row_off;
             const int n_src = seg0 ? st.n_in : st.n_sin;
             const int valid = n_src - k0;
-            if (tid == 0) {
+            if (tid == 0) {   // boxes past the K extent are zero-filled and still complete their bytes
                 mbar_expect_tx(&S.bar[stage], BM * BK * sizeof(double));
-                tma_load_2d(S.w[stage], seg0 ? tmWp : tmVp, &S.bar[stage], k0, m0);
+#pragma unroll
+                for (int bx = 0; bx < BK / TB; bx++)
+                    tma_load_2d(S.w[stage][bx], seg0 ? tmWp : tmVp, &S.bar[stage], k0 + bx * TB, m0);
             }
             if (C == 4) {
-                // 16 items x 512 B; 2 x 16-B pieces per thread
+                // 16 items x 1 KB; 4 x 16-B pieces per thread
 #pragma unroll
-                for (int q = 0; q < 2; q++) {
-                    const int piece = tid * 2 + q;          // 0..511
-                    const int it = piece >> 5, j = piece & 31;   // item, 16-B piece within its 512 B
+                for (int q = 0; q < 4; q++) {
+                    const int piece = q * kThreads + tid;    // 0..1023
+                    const int it = piece >> 6, j = piece & 63;   // item, 16-B piece within its 1 KB
                     const int64_t item = n0 / 4 + it;
                     const int krow = j >> 1;                 // 2 pieces per row (4 doubles)
                     if (item < n && krow < valid)
@@ -304,13 +307,13 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                     const int64_t item = n0 / 4 + tid;
                     const int sg = seg0 ? 0 : 1;
                     S.mask[stage][tid] = item >= n ? 0u
-                        : cache_ok ? bits16(S.kc[sg][tid], src_row + k0 - wbeg[sg] * 64, valid)
-                                   : bits16(keys + item * L.KW, src_row + k0, valid);
+                        : cache_ok ? bits32(S.kc[sg][tid], src_row + k0 - wbeg[sg] * 64, valid)
+                                   : bits32(keys + item * L.KW, src_row + k0, valid);
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const int pt = tid >> 2, krow = (tid & 3) * 4 + q;
+                for (int q = 0; q < 8; q++) {
+                    const int pt = tid >> 2, krow = (tid & 3) * 8 + q;
                     const int64_t item = n0 + pt;
                     if (item < n && krow < valid)
                         cp_async8(&S.x[stage][pt * XS1 + krow], L.Z + item * L.zs + src_row + k0 + krow);
@@ -319,8 +322,8 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                     const int64_t item = n0 + tid;
                     const int sg = seg0 ? 0 : 1;
                     S.mask[stage][tid] = item >= n ? 0u
-                        : cache_ok ? bits16(S.kc[sg][tid], src_row + k0 - wbeg[sg] * 64, valid)
-                                   : bits16(keys + item * L.KW, src_row + k0, valid);
+                        : cache_ok ? bits32(S.kc[sg][tid], src_row + k0 - wbeg[sg] * 64, valid)
+                                   : bits32(keys + item * L.KW, src_row + k0, valid);
                 }
             }
             cp_async_commit();
@@ -350,7 +353,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
             mbar_wait(&S.bar[s], (gc / NST) & 1);
             __syncthreads();
             if (c + NST - 1 < nchunks) issue(c + NST - 1);
-            const double* ws = S.w[s];
+            const double* ws = S.w[s][0];
             const double* xsm = S.x[s];
 #pragma unroll
             for (int kk = 0; kk < BK; kk += 4) {
@@ -358,8 +361,8 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
 #pragma unroll
                 for (int mi = 0; mi < 2; mi++) {
                     int r = wm * 32 + mi * 16 + pg;
-                    a[mi][0] = ws[swz(r, kk + t)];
-                    a[mi][1] = ws[swz(r + 8, kk + t)];
+                    a[mi][0] = ws[(kk / TB) * BM * TB + swz(r, (kk % TB) + t)];
+                    a[mi][1] = ws[(kk / TB) * BM * TB + swz(r + 8, (kk % TB) + t)];
                 }
 #pragma unroll
                 for (int nj = 0; nj < 2; nj++) {
@@ -503,7 +506,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemm_step(const __grid_constant
                                                         const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
     pdl_enter();
     extern __shared__ uint8_t smem_raw[];
-    GemmSmem<C>& S = *reinterpret_cast<GemmSmem<C>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KB-aligned view derived by pointer arithmetic on the shared array (keeps LDS addressing)
+    GemmSmem<C>& S = *reinterpret_cast<GemmSmem<C>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const StepDev& st = L.st;
     const int tid = threadIdx.x;
     const int64_t n = dev_count(L.n_dev, L.n_cap);

@@ -40,8 +40,15 @@ def main():
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, capture_output=True)
     cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
     dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
-    # locate the function
+    # locate the function: explicit mangled name, else the report's kernel name must be unique
     fn = sys.argv[4] if len(sys.argv) > 4 else None
+    if fn is None:
+        names = set(re.findall(r"\.text\.(\S+):", dis))
+        cands = [nm for nm in names if ksub in nm]
+        if len(cands) == 1:
+            fn = cands[0]
+        elif cands:
+            sys.exit("ambiguous kernel; pass the mangled name: " + " ".join(sorted(cands)))
     lines_by_off = {}
     cur_line = None
     in_fn = fn is None
@@ -50,9 +57,9 @@ def main():
         if m:
             in_fn = fn is None or m.group(1) == fn
             continue
-        m = re.search(r'//## File ".*?", line (\d+)', ln)
+        m = re.search(r'//## File "(.*?)", line (\d+)', ln)
         if m:
-            cur_line = int(m.group(1))
+            cur_line = f"{os.path.basename(m.group(1))}:{m.group(2)}"
             continue
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if m and in_fn:
@@ -65,7 +72,7 @@ def main():
         per_line_i[lines_by_off.get(off)] += insts.get(off, 0)
     src = None
     for ln, v in sorted(per_line.items(), key=lambda x: -x[1])[:40]:
-        print(f"{100 * v / tot:5.1f}%  inst {per_line_i[ln]:>12.0f}  line {ln}")
+        print(f"{100 * v / tot:5.1f}%  inst {per_line_i[ln]:>12.0f}  {ln}")
 
 
 if __name__ == "__main__":
