@@ -127,6 +127,20 @@ int am_result_counts(am_engine *e, int64_t *h_counts);
 int am_result_copy(am_engine *e, uint64_t *h_keys, int32_t *h_nverts, double *h_verts,
                    int32_t *h_edge_nrefs, int32_t *h_edge_refs);
 
+/* --- mesh assembly ------------------------------------------------------- */
+/* Weld the vertices of a polygon soup: reference meshes.py:89-148 weld(mesh, tol)
+ * (MarchResult.welded_mesh, reference marching.py:126-127), bit-identical output.
+ * Device inputs: d_verts [n_verts*3] fp64, loops as CSR d_loop_off [n_loops+1] /
+ * d_loop_idx [d_loop_off[n_loops]] (int64 vertex indices).  Device outputs (caller-sized):
+ * d_remap [n_verts] (vertex -> kept index), d_kept [n_verts*3] (first n_kept rows used),
+ * d_face_off [n_loops+1] / d_face_idx [d_loop_off[n_loops]] (kept faces, CSR; loops that
+ * collapse below 3 distinct vertices are dropped), d_face_src [n_loops] (source loop of each
+ * kept face, for carrying face planes).  h_counts[3] = {n_kept, n_faces, n_dropped}.
+ * stream: a cudaStream_t (null = legacy default stream); returns after synchronizing it. */
+int am_weld(const double *d_verts, int64_t n_verts, const int64_t *d_loop_off, const int64_t *d_loop_idx,
+            int64_t n_loops, double tol, void *stream, int64_t *d_remap, double *d_kept, int64_t *d_face_off,
+            int64_t *d_face_idx, int64_t *d_face_src, int64_t *h_counts);
+
 /* --- profiling hooks (bench.py roofline) --------------------------------- */
 /* cumulative device time (ms) of the compose (DMMA) kernels, of the face
  * kernel, and the algorithmic flop / byte counts they processed */

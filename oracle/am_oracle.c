@@ -1190,3 +1190,119 @@ long om_cell_expand(const om_net *net, const uint64_t *key, const double *bbox6,
     free(buf);
     return nout;
 }
+
+/* ------------------------------------------------------------------ mesh weld
+ * reference meshes.py:89-148 weld(mesh, tol).  Greedy over the vertices in order: a vertex
+ * merges into the FIRST kept vertex met while scanning the 27 grid cells of side tol (dx, dy,
+ * dz each in the order 0, -1, 1; reference meshes.py:112-126) and, inside a cell, the kept
+ * vertices in insertion order, at euclidean distance <= tol; otherwise it is kept and appended
+ * to its own cell.  tol == 0: exact-coordinate buckets (-0.0 == 0.0), merge into the first kept
+ * vertex with equal coordinates (reference meshes.py:104-110).  Loops are remapped, consecutive
+ * repeats and a closing repeat removed, and loops with < 3 distinct indices dropped
+ * (reference meshes.py:134-148).  Returns 0, or -1 on allocation failure.
+ * Outputs: remap[n], kept[n_kept*3], face_off[n_faces+1], face_idx[...], face_src[n_faces],
+ * counts3 = {n_kept, n_faces, n_dropped}. */
+typedef struct { int64_t k[3]; long *items; long n, cap; int used; } wcell;
+
+static uint64_t wkey_hash(const int64_t k[3]) {
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    for (int d = 0; d < 3; d++) {
+        h ^= (uint64_t)k[d] + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+        h *= 0xff51afd7ed558ccdull;
+    }
+    return h ^ (h >> 33);
+}
+static wcell *wfind(wcell *tab, uint64_t mask, const int64_t k[3], int create) {
+    for (uint64_t s = wkey_hash(k) & mask;; s = (s + 1) & mask) {
+        wcell *c = &tab[s];
+        if (!c->used) {
+            if (!create) return NULL;
+            c->used = 1;
+            memcpy(c->k, k, sizeof c->k);
+            return c;
+        }
+        if (c->k[0] == k[0] && c->k[1] == k[1] && c->k[2] == k[2]) return c;
+    }
+}
+static int64_t wbits(double x) {
+    int64_t b;
+    if (x == 0.0) x = 0.0;  /* -0.0 and 0.0 hash and compare equal in the reference's tuple keys */
+    memcpy(&b, &x, 8);
+    return b;
+}
+
+int om_weld(const double *v, long n, const long *loop_off, const long *loop_idx, long n_loops, double tol,
+            long *remap, double *kept, long *face_off, long *face_idx, long *face_src, long *counts3) {
+    uint64_t cap = 16;
+    while (cap < (uint64_t)(2 * n + 2)) cap <<= 1;
+    wcell *tab = calloc(cap, sizeof(wcell));
+    if (!tab) return -1;
+    const double inv = tol > 0 ? 1.0 / tol : 0.0;
+    static const int ord[3] = {0, -1, 1};
+    long nk = 0;
+    for (long i = 0; i < n; i++) {
+        const double *p = v + i * 3;
+        int64_t c[3];
+        long hit = -1;
+        if (tol > 0) {
+            for (int d = 0; d < 3; d++) c[d] = (int64_t)floor(p[d] * inv);
+            for (int a = 0; a < 3 && hit < 0; a++)
+                for (int b = 0; b < 3 && hit < 0; b++)
+                    for (int e = 0; e < 3 && hit < 0; e++) {
+                        int64_t q[3] = {c[0] + ord[a], c[1] + ord[b], c[2] + ord[e]};
+                        wcell *cl = wfind(tab, cap - 1, q, 0);
+                        if (!cl) continue;
+                        for (long m = 0; m < cl->n; m++) {
+                            const double *r = kept + cl->items[m] * 3;
+                            double d0 = r[0] - p[0], d1 = r[1] - p[1], d2 = r[2] - p[2];
+                            if (sqrt((d0 * d0 + d1 * d1) + d2 * d2) <= tol) { hit = cl->items[m]; break; }
+                        }
+                    }
+        } else {
+            for (int d = 0; d < 3; d++) c[d] = wbits(p[d]);
+            wcell *cl = wfind(tab, cap - 1, c, 0);
+            if (cl)
+                for (long m = 0; m < cl->n; m++) {
+                    const double *r = kept + cl->items[m] * 3;
+                    if (r[0] == p[0] && r[1] == p[1] && r[2] == p[2]) { hit = cl->items[m]; break; }
+                }
+        }
+        if (hit < 0) {
+            hit = nk++;
+            memcpy(kept + hit * 3, p, 24);
+            wcell *cl = wfind(tab, cap - 1, c, 1);
+            if (cl->n == cl->cap) {
+                cl->cap = cl->cap ? 2 * cl->cap : 4;
+                cl->items = realloc(cl->items, (size_t)cl->cap * sizeof(long));
+            }
+            cl->items[cl->n++] = hit;
+        }
+        remap[i] = hit;
+    }
+    for (uint64_t s = 0; s < cap; s++) free(tab[s].items);
+    free(tab);
+    long nf = 0, dropped = 0, w = 0;
+    face_off[0] = 0;
+    for (long l = 0; l < n_loops; l++) {
+        long a = loop_off[l], b = loop_off[l + 1];
+        if (b <= a) { dropped++; continue; }
+        long start = w;
+        face_idx[w++] = remap[loop_idx[a]];
+        for (long q = a + 1; q < b; q++) {
+            long x = remap[loop_idx[q]];
+            if (x != face_idx[w - 1]) face_idx[w++] = x;
+        }
+        if (w - start > 1 && face_idx[start] == face_idx[w - 1]) w--;
+        long distinct = 0;
+        for (long q = start; q < w; q++) {
+            int seen = 0;
+            for (long r = start; r < q; r++) if (face_idx[r] == face_idx[q]) { seen = 1; break; }
+            distinct += !seen;
+        }
+        if (distinct < 3) { dropped++; w = start; continue; }
+        face_src[nf] = l;
+        face_off[++nf] = w;
+    }
+    counts3[0] = nk; counts3[1] = nf; counts3[2] = dropped;
+    return 0;
+}

@@ -60,6 +60,8 @@ def lib():
         L.om_canonical.argtypes = [P, P, P]
         L.om_cell_expand.restype = ctypes.c_long
         L.om_cell_expand.argtypes = [P, P, P, P, ctypes.c_long]
+        L.om_weld.restype = ctypes.c_int
+        L.om_weld.argtypes = [P, ctypes.c_long, P, P, ctypes.c_long, ctypes.c_double, P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -358,3 +360,23 @@ class OracleShardEngine:
 
     def visited_keys(self):
         return sorted(self.visited)
+
+
+def weld(verts, loop_off, loop_idx, tol: float = TOL_WELD):
+    """reference meshes.py:89-148 on CSR loops.  Returns (kept (K,3), face_off (F+1,),
+    face_idx, face_src (F,) source loop of each kept face, remap (V,), n_dropped)."""
+    v = np.ascontiguousarray(verts, dtype=np.float64).reshape(-1, 3)
+    lo = np.ascontiguousarray(loop_off, dtype=np.int64)
+    li = np.ascontiguousarray(loop_idx, dtype=np.int64)
+    n, nl = len(v), len(lo) - 1
+    remap = np.empty(n, np.int64)
+    kept = np.empty((max(n, 1), 3), np.float64)
+    face_off = np.empty(nl + 1, np.int64)
+    face_idx = np.empty(max(len(li), 1), np.int64)
+    face_src = np.empty(max(nl, 1), np.int64)
+    counts = np.zeros(3, np.int64)
+    if lib().om_weld(_ptr(v), n, _ptr(lo), _ptr(li), nl, float(tol), _ptr(remap), _ptr(kept), _ptr(face_off),
+                     _ptr(face_idx), _ptr(face_src), _ptr(counts)) != 0:
+        raise MemoryError("om_weld")
+    nk, nf, nd = (int(x) for x in counts)
+    return kept[:nk].copy(), face_off[:nf + 1].copy(), face_idx[:face_off[nf]].copy(), face_src[:nf].copy(), remap, nd

@@ -24,6 +24,7 @@ SOURCES = {
     "am_engine.cu": [],
     "am_face.cu": ["-fmad=false"],
     "am_peak.cu": [],
+    "am_weld.cu": [],
 }
 
 

@@ -51,7 +51,8 @@ struct SubDev {
 using namespace am;
 
 static thread_local std::string g_err;
-static int fail(int code, const char* fmt, ...) {
+// records the message am_last_error() returns; shared by every C-ABI entry point
+int am::set_error(int code, const char* fmt, ...) {
     char buf[512];
     va_list ap;
     va_start(ap, fmt);
@@ -60,6 +61,7 @@ static int fail(int code, const char* fmt, ...) {
     g_err = buf;
     return code;
 }
+#define fail am::set_error
 #define CK(x)                                                                                  \
     do {                                                                                       \
         cudaError_t _e = (x);                                                                  \

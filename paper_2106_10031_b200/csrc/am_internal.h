@@ -16,6 +16,8 @@
 
 namespace am {
 
+int set_error(int code, const char* fmt, ...);   // am_engine.cu; returns code
+
 constexpr double kDegen = 1e-12;   // reference network.py:27 DEGENERATE_NORMAL_TOL
 constexpr double kTolDet = 1e-12;  // reference cells.py:32 TOL_DET
 constexpr uint64_t kEmpty = ~0ull;

@@ -181,8 +181,13 @@ class MarchResult:
         return PolygonMesh(self.verts.copy(), faces, None)
 
     def welded_mesh(self, tol: float = TOL_WELD):
-        from .meshes import weld
-        return weld(self.polygon_soup(), tol)
+        """reference marching.py:126-127 weld(polygon_soup(), tol), welded on the GPU straight
+        from the CSR soup (no per-loop Python objects on the way in)."""
+        from .meshes import PolygonMesh, weld_arrays
+        nv = self.nverts[self.nverts > 0].astype(np.int64)
+        off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
+        kept, foff, fidx, _, nd = weld_arrays(self.verts, off, np.arange(off[-1], dtype=np.int64), tol)
+        return PolygonMesh(kept, np.split(fidx, foff[1:-1]) if len(foff) > 1 else [], None, nd)
 
     def face_multiset(self, decimals: int = 10):
         """Order-independent fingerprint (reference marching.py:139-149)."""
