@@ -126,6 +126,10 @@ int am_result_counts(am_engine *e, int64_t *h_counts);
  * id < n_bits neuron, id < n_bits+n_subs branch target, else bbox face. */
 int am_result_copy(am_engine *e, uint64_t *h_keys, int32_t *h_nverts, double *h_verts,
                    int32_t *h_edge_nrefs, int32_t *h_edge_refs);
+/* the same sorted arrays into DEVICE buffers (sorting and gathering run on the GPU in both
+ * calls: LSD radix sort of the key words, CSR gathers); feeds am_weld without a host trip */
+int am_result_copy_device(am_engine *e, uint64_t *d_keys, int32_t *d_nverts, double *d_verts,
+                          int32_t *d_edge_nrefs, int32_t *d_edge_refs);
 
 /* --- mesh assembly ------------------------------------------------------- */
 /* Weld the vertices of a polygon soup: reference meshes.py:89-148 weld(mesh, tol)

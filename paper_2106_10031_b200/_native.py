@@ -70,6 +70,7 @@ SIGNATURES = {
     "am_queue_size": (ctypes.c_int, [P, P]),
     "am_result_counts": (ctypes.c_int, [P, P]),
     "am_result_copy": (ctypes.c_int, [P, P, P, P, P, P]),
+    "am_result_copy_device": (ctypes.c_int, [P, P, P, P, P, P]),
     "am_stats": (ctypes.c_int, [P, P]),
     "am_set_timing": (ctypes.c_int, [P, ctypes.c_int]),
     "am_bench_fp64_peak": (ctypes.c_int, [ctypes.c_int, P]),

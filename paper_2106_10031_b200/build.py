@@ -25,6 +25,7 @@ SOURCES = {
     "am_face.cu": ["-fmad=false"],
     "am_peak.cu": [],
     "am_weld.cu": [],
+    "am_result.cu": [],
 }
 
 

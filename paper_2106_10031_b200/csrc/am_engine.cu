@@ -62,6 +62,7 @@ int am::set_error(int code, const char* fmt, ...) {
     return code;
 }
 #define fail am::set_error
+#define fail am::set_error
 #define CK(x)                                                                                  \
     do {                                                                                       \
         cudaError_t _e = (x);                                                                  \
@@ -145,6 +146,9 @@ struct am_engine {
     DBuf<double> verts;
     // host-sized scratch (seeding, pushes, primitives)
     DBuf<uint64_t> hkeys;
+    DBuf<uint64_t> s_keys;   // sorted results (am_result_copy)
+    DBuf<int32_t> s_nv, s_enr, s_refs;
+    DBuf<double> s_verts;
     DBuf<int32_t> hstatus;
     DBuf<uint64_t> hslot;
     DBuf<double> sx, sxp, pvals;
@@ -413,16 +417,17 @@ extern "C" int am_engine_destroy(am_engine* e) {
     if (e->graph) cudaGraphDestroy(e->graph);
     DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx,
                            &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1], &e->pool_hint,
-                           &e->ckey_hint, &e->emit_hint};
+                           &e->ckey_hint, &e->emit_hint, &e->s_verts};
     for (auto* b : dbl) b->release();
     DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->ckey, &e->slot, &e->slot2, &e->scratch, &e->outbox,
-                             &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres, &e->pkeys, &e->pslot};
+                             &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres, &e->pkeys, &e->pslot, &e->s_keys};
     for (auto* b : u64) b->release();
     DBuf<int32_t>* i32[] = {&e->changed, &e->status, &e->status2, &e->canon_pos, &e->canon_pool, &e->X,
                             &e->f_items, &e->f_pool, &e->batch_pool, &e->local_idx, &e->queue, &e->cell_pool,
                             &e->cell_nv, &e->edge_nrefs, &e->edge_refs, &e->hstatus, &e->sact, &e->sdone,
                             &e->pool_vn, &e->pstatus, &e->emit_dup, &e->emit_pool, &e->prec_cand, &e->prec_k,
-                            &e->pend_t[0], &e->pend_t[1], &e->pend_k[0], &e->pend_k[1], &e->val_buf};
+                            &e->pend_t[0], &e->pend_t[1], &e->pend_k[0], &e->pend_k[1], &e->val_buf, &e->s_nv,
+                            &e->s_enr, &e->s_refs};
     for (auto* b : i32) b->release();
     e->pool_flags.release();
     e->pool_voff.release();
@@ -897,57 +902,50 @@ extern "C" int am_result_counts(am_engine* e, int64_t* h) {
     return AM_OK;
 }
 
+// sorted result arrays into device buffers -- see include/am_b200.h
+static int result_assemble(am_engine* e, uint64_t* d_keys, int32_t* d_nverts, double* d_verts,
+                           int32_t* d_edge_nrefs, int32_t* d_edge_refs) {
+    const int KW = e->KW;
+    const int64_t nc = (int64_t)e->hctr[C_CELLS], nvt = (int64_t)e->hctr[C_VERTS];
+    if (nc == 0) return AM_OK;
+    CK(e->hkeys.reserve(nc * KW, e->stream));
+    launch_gather_keys(e->pool.p, e->cell_pool.p, nc, KW, e->hkeys.p, e->stream);
+    return assemble_results(e->hkeys.p, e->cell_nv.p, e->cell_voff.p, e->verts.p, e->edge_nrefs.p, e->edge_roff.p,
+                            e->edge_refs.p, nc, nvt, KW, e->stream, d_keys, d_nverts, d_verts, d_edge_nrefs,
+                            d_edge_refs);
+}
+
+extern "C" int am_result_copy_device(am_engine* e, uint64_t* d_keys, int32_t* d_nverts, double* d_verts,
+                                     int32_t* d_edge_nrefs, int32_t* d_edge_refs) {
+    if (!e) return fail(AM_ERR_ARG, "null engine");
+    RC(sync_counters(e));
+    RC(result_assemble(e, d_keys, d_nverts, d_verts, d_edge_nrefs, d_edge_refs));
+    CK(cudaStreamSynchronize(e->stream));
+    return AM_OK;
+}
+
 extern "C" int am_result_copy(am_engine* e, uint64_t* h_keys, int32_t* h_nverts, double* h_verts,
                               int32_t* h_edge_nrefs, int32_t* h_edge_refs) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
     RC(sync_counters(e));
     const int KW = e->KW;
-    int64_t nc = (int64_t)e->hctr[C_CELLS], nvt = (int64_t)e->hctr[C_VERTS], nref = (int64_t)e->hctr[C_REFS];
+    const int64_t nc = (int64_t)e->hctr[C_CELLS], nvt = (int64_t)e->hctr[C_VERTS], nref = (int64_t)e->hctr[C_REFS];
     if (nc == 0) return AM_OK;
-    std::vector<int32_t> cp(nc), nv(nc);
-    std::vector<int64_t> voff(nc);
-    CK(cudaMemcpy(cp.data(), e->cell_pool.p, nc * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(nv.data(), e->cell_nv.p, nc * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(voff.data(), e->cell_voff.p, nc * 8, cudaMemcpyDeviceToHost));
-    CK(e->hkeys.reserve(nc * KW, e->stream));
-    launch_gather_keys(e->pool.p, e->cell_pool.p, nc, KW, e->hkeys.p, e->stream);
-    std::vector<uint64_t> keys((size_t)nc * KW);
-    CK(cudaMemcpyAsync(keys.data(), e->hkeys.p, nc * KW * 8, cudaMemcpyDeviceToHost, e->stream));
-    std::vector<double> verts((size_t)nvt * 3);
-    std::vector<int32_t> enr(nvt), refs(nref);
-    std::vector<int64_t> roff(nvt);
+    cudaStream_t s = e->stream;
+    CK(e->s_keys.reserve(nc * KW, s));
+    CK(e->s_nv.reserve(nc, s));
+    CK(e->s_verts.reserve(std::max<int64_t>(nvt, 1) * 3, s));
+    CK(e->s_enr.reserve(std::max<int64_t>(nvt, 1), s));
+    CK(e->s_refs.reserve(std::max<int64_t>(nref, 1), s));
+    RC(result_assemble(e, e->s_keys.p, e->s_nv.p, e->s_verts.p, e->s_enr.p, e->s_refs.p));
+    CK(cudaMemcpyAsync(h_keys, e->s_keys.p, (size_t)nc * KW * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_nverts, e->s_nv.p, (size_t)nc * 4, cudaMemcpyDeviceToHost, s));
     if (nvt) {
-        CK(cudaMemcpyAsync(verts.data(), e->verts.p, nvt * 24, cudaMemcpyDeviceToHost, e->stream));
-        CK(cudaMemcpyAsync(enr.data(), e->edge_nrefs.p, nvt * 4, cudaMemcpyDeviceToHost, e->stream));
-        CK(cudaMemcpyAsync(roff.data(), e->edge_roff.p, nvt * 8, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaMemcpyAsync(h_verts, e->s_verts.p, (size_t)nvt * 24, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_edge_nrefs, e->s_enr.p, (size_t)nvt * 4, cudaMemcpyDeviceToHost, s));
     }
-    if (nref) CK(cudaMemcpyAsync(refs.data(), e->edge_refs.p, nref * 4, cudaMemcpyDeviceToHost, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    std::vector<int64_t> order(nc);
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-        const uint64_t* ka = &keys[(size_t)a * KW];
-        const uint64_t* kb = &keys[(size_t)b * KW];
-        for (int w = 0; w < KW; w++)
-            if (ka[w] != kb[w]) return ka[w] < kb[w];
-        return false;
-    });
-    int64_t vo = 0, ro = 0;
-    for (int64_t i = 0; i < nc; i++) {
-        int64_t c = order[i];
-        memcpy(h_keys + i * KW, &keys[(size_t)c * KW], KW * 8);
-        int n = nv[c] > 0 ? nv[c] : 0;
-        h_nverts[i] = nv[c];
-        for (int v = 0; v < n; v++) {
-            int64_t src = voff[c] + v;
-            h_verts[(vo + v) * 3 + 0] = verts[src * 3 + 0];
-            h_verts[(vo + v) * 3 + 1] = verts[src * 3 + 1];
-            h_verts[(vo + v) * 3 + 2] = verts[src * 3 + 2];
-            h_edge_nrefs[vo + v] = enr[src];
-            for (int q = 0; q < enr[src]; q++) h_edge_refs[ro++] = refs[roff[src] + q];
-        }
-        vo += n;
-    }
+    if (nref) CK(cudaMemcpyAsync(h_edge_refs, e->s_refs.p, (size_t)nref * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     return AM_OK;
 }
 

@@ -111,6 +111,12 @@ __device__ __forceinline__ uint64_t* keys_at(const LayerLaunch& L) {
 
 
 
+// result assembly (am_result.cu): sorted cell order + gathered CSR face loops
+int assemble_results(const uint64_t* keys, const int32_t* cell_nv, const int64_t* cell_voff, const double* verts,
+                     const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nc, int64_t nvt, int KW,
+                     cudaStream_t s, uint64_t* s_keys, int32_t* s_nv, double* s_verts, int32_t* s_enr,
+                     int32_t* s_refs);
+
 // kernels' host-side launchers (am_compose.cu)
 void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s);
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV,

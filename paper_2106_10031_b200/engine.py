@@ -151,15 +151,34 @@ class Engine:
         return dict(zip(keys, (int(x) for x in c)))
 
     def results(self):
+        """Sorted results on the host (sorted and gathered on the GPU; pinned staging)."""
         c = self.counts()
-        keys = np.zeros((c["cells"], self.kw), dtype=np.uint64)
-        nverts = np.zeros(c["cells"], dtype=np.int32)
-        verts = np.zeros((c["verts"], 3))
-        enr = np.zeros(c["verts"], dtype=np.int32)
-        erefs = np.zeros(c["edge_refs"], dtype=np.int32)
+
+        def pinned(shape, dt):
+            return torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+        keys = pinned((c["cells"], self.kw), torch.int64).view(np.uint64)
+        nverts = pinned(c["cells"], torch.int32)
+        verts = pinned((c["verts"], 3), torch.float64)
+        enr = pinned(c["verts"], torch.int32)
+        erefs = pinned(c["edge_refs"], torch.int32)
         _native.check(self.lib.am_result_copy(self.h, keys.ctypes.data, nverts.ctypes.data, verts.ctypes.data,
                                               enr.ctypes.data, erefs.ctypes.data), "am_result_copy")
         return c, keys, nverts, verts, enr, erefs
+
+    def results_device(self):
+        """Sorted results as device tensors: (counts, keys (C, KW) int64, nverts (C,) int32,
+        verts (V, 3), edge_nrefs (V,), edge_refs (R,))."""
+        c = self.counts()
+        d = self.dev
+        keys = torch.empty((max(c["cells"], 1), self.kw), dtype=torch.int64, device=d)
+        nverts = torch.empty(max(c["cells"], 1), dtype=torch.int32, device=d)
+        verts = torch.empty((max(c["verts"], 1), 3), dtype=torch.float64, device=d)
+        enr = torch.empty(max(c["verts"], 1), dtype=torch.int32, device=d)
+        erefs = torch.empty(max(c["edge_refs"], 1), dtype=torch.int32, device=d)
+        _native.check(self.lib.am_result_copy_device(self.h, keys.data_ptr(), nverts.data_ptr(), verts.data_ptr(),
+                                                     enr.data_ptr(), erefs.data_ptr()), "am_result_copy_device")
+        return (c, keys[:c["cells"]], nverts[:c["cells"]], verts[:c["verts"]], enr[:c["verts"]],
+                erefs[:c["edge_refs"]])
 
     def set_timing(self, on: bool):
         _native.check(self.lib.am_set_timing(self.h, int(on)), "am_set_timing")
