@@ -79,26 +79,27 @@ template <class T>
 struct DBuf {
     T* p = nullptr;
     int64_t n = 0;  // capacity in elements
-    // grow to >= m elements (2x geometric); keep the first keep_n elements
+    // grow to >= m elements (2x geometric); keep the first keep_n elements.  Stream-ordered
+    // allocation from the device's default memory pool (kept resident, see pool_setup): no
+    // device-wide synchronisation, and a re-created engine reuses the pooled memory.
     cudaError_t reserve(int64_t m, cudaStream_t s, bool keep = false, int64_t keep_n = 0, bool* moved = nullptr) {
         if (m <= n) return cudaSuccess;
         int64_t cap = std::max<int64_t>(m, 2 * n);
         T* q = nullptr;
-        cudaError_t e = cudaMalloc(&q, (size_t)cap * sizeof(T));
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&q), (size_t)cap * sizeof(T), s);
         if (e != cudaSuccess) return e;
         if (keep && p && keep_n > 0) {
             e = cudaMemcpyAsync(q, p, (size_t)keep_n * sizeof(T), cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) return e;
         }
-        cudaStreamSynchronize(s);
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = q;
         n = cap;
         if (moved) *moved = true;
         return cudaSuccess;
     }
-    void release() {
-        if (p) cudaFree(p);
+    void release(cudaStream_t s) {
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
     }
@@ -164,6 +165,7 @@ struct am_engine {
     // stats
     bool timing = false;
     cudaEvent_t ev[6];
+    cudaEvent_t ev_join = nullptr;   // orders the caller's stream and the engine's own stream
     double t_compose = 0, t_face = 0, t_probe = 0, flops = 0, pflops = 0, face_bytes = 0;
     double n_comp_cells = 0, n_face_cells = 0, n_probes = 0;
     int64_t iters = 0;
@@ -228,7 +230,7 @@ static int ensure_hash(am_engine* e, int64_t extra) {
     if ((int64_t)e->tcap < 2 * need) {
         uint64_t cap = e->tcap ? e->tcap : 1024;
         while ((int64_t)cap < 2 * need) cap <<= 1;
-        e->table.release();
+        e->table.release(e->stream);
         CK(e->table.reserve((int64_t)cap, e->stream));
         e->tcap = cap;
         CK(cudaMemsetAsync(e->table.p, 0xff, cap * sizeof(uint64_t), e->stream));
@@ -278,6 +280,13 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device)
         return fail(AM_ERR_NO_DEVICE, "no CUDA device %d (found %d)", device, ndev);
     CK(cudaSetDevice(device));
+    {   // keep freed engine / weld / result memory in the device's default pool
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     am_engine* e = new am_engine();
     e->device = device;
     e->stream = (cudaStream_t)stream;
@@ -295,7 +304,8 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     e->steps.assign(net->h_steps, net->h_steps + (size_t)net->n_steps * AM_STEP_FIELDS);
     e->subs.assign(net->h_subs, net->h_subs + (size_t)net->n_subs * AM_SUB_FIELDS);
     CK(e->params.reserve(std::max<int64_t>(net->n_params, 1), e->stream));
-    CK(cudaMemcpy(e->params.p, net->h_params, (size_t)net->n_params * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(e->params.p, net->h_params, (size_t)net->n_params * sizeof(double), cudaMemcpyHostToDevice,
+                       e->stream));
 
     // padded weight copies (row stride multiple of 16 doubles) for TMA
     int ns = net->n_steps;
@@ -321,7 +331,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
         }
     }
     CK(e->wpad.reserve((int64_t)hw.size(), e->stream));
-    CK(cudaMemcpy(e->wpad.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(e->wpad.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, e->stream));
     e->sdev.resize(ns);
     e->tmW.resize(ns);
     e->tmV.resize(ns);
@@ -362,7 +372,8 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
         hsub[j].hb = net->h_params[sb[3]];
     }
     CK(e->subdev.reserve((int64_t)(sizeof(SubDev) * e->M), e->stream));
-    CK(cudaMemcpy(e->subdev.p, hsub.data(), sizeof(SubDev) * e->M, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(e->subdev.p, hsub.data(), sizeof(SubDev) * e->M, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));   // host staging vectors go out of scope
     // batch size from the per-iteration memory budget: compose planes + worst-case probe
     // activations + emitted keys per batch cell
     int64_t budget = e->P.mem_budget > 0 ? e->P.mem_budget : (int64_t)4 << 30;
@@ -399,10 +410,11 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->prec_pt.reserve(e->PR * 3, s));
     CK(e->outbox.reserve(e->KW, s));
     CK(e->ctr.reserve(C_N, s));
-    CK(cudaMemset(e->ctr.p, 0, C_N * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(e->ctr.p, 0, C_N * sizeof(unsigned long long), e->stream));
     CK(e->dbg.reserve(64, s));
-    CK(cudaMemset(e->dbg.p, 0, 64 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(e->dbg.p, 0, 64 * sizeof(unsigned long long), e->stream));
     for (int i = 0; i < 6; i++) cudaEventCreate(&e->ev[i]);
+    CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
     int rc = ensure_hash(e, 4 * e->B * (1 + emit_per_cell()));
     if (!rc) rc = ensure_results(e, 4 * e->B);
     if (rc) { delete e; return rc; }
@@ -418,24 +430,25 @@ extern "C" int am_engine_destroy(am_engine* e) {
     DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx,
                            &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1], &e->pool_hint,
                            &e->ckey_hint, &e->emit_hint, &e->s_verts};
-    for (auto* b : dbl) b->release();
+    for (auto* b : dbl) b->release(e->stream);
     DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->ckey, &e->slot, &e->slot2, &e->scratch, &e->outbox,
                              &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres, &e->pkeys, &e->pslot, &e->s_keys};
-    for (auto* b : u64) b->release();
+    for (auto* b : u64) b->release(e->stream);
     DBuf<int32_t>* i32[] = {&e->changed, &e->status, &e->status2, &e->canon_pos, &e->canon_pool, &e->X,
                             &e->f_items, &e->f_pool, &e->batch_pool, &e->local_idx, &e->queue, &e->cell_pool,
                             &e->cell_nv, &e->edge_nrefs, &e->edge_refs, &e->hstatus, &e->sact, &e->sdone,
                             &e->pool_vn, &e->pstatus, &e->emit_dup, &e->emit_pool, &e->prec_cand, &e->prec_k,
                             &e->pend_t[0], &e->pend_t[1], &e->pend_k[0], &e->pend_k[1], &e->val_buf, &e->s_nv,
                             &e->s_enr, &e->s_refs};
-    for (auto* b : i32) b->release();
-    e->pool_flags.release();
-    e->pool_voff.release();
-    e->cell_voff.release();
-    e->edge_roff.release();
-    e->subdev.release();
-    e->ctr.release();
+    for (auto* b : i32) b->release(e->stream);
+    e->pool_flags.release(e->stream);
+    e->pool_voff.release(e->stream);
+    e->cell_voff.release(e->stream);
+    e->edge_roff.release(e->stream);
+    e->subdev.release(e->stream);
+    e->ctr.release(e->stream);
     for (int i = 0; i < 6; i++) cudaEventDestroy(e->ev[i]);
+    if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->own_stream) cudaStreamDestroy(e->stream);
     delete e;
     return AM_OK;
@@ -506,9 +519,20 @@ static int forward_host(am_engine* e, const double* pts, int64_t n, double* vals
     return AM_OK;
 }
 
+// When the caller passed the legacy default stream (torch's default), the engine runs on a
+// stream of its own: the caller's pending work that produced our device inputs must come
+// first (the entry points end with a host sync, so outputs are complete on return).
+static int join_caller(am_engine* e) {
+    if (!e->own_stream) return AM_OK;   // caller's own stream: already ordered
+    CK(cudaEventRecord(e->ev_join, cudaStreamLegacy));
+    CK(cudaStreamWaitEvent(e->stream, e->ev_join, 0));
+    return AM_OK;
+}
+
 extern "C" int am_forward(am_engine* e, const double* d_pts, int64_t n, double* d_vals, uint64_t* d_keys) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
     if (n == 0) return AM_OK;
+    RC(join_caller(e));
     uint64_t* keys = d_keys;
     if (!keys) {
         CK(e->hkeys.reserve(n * e->KW, e->stream));
@@ -522,6 +546,7 @@ extern "C" int am_forward(am_engine* e, const double* d_pts, int64_t n, double* 
 extern "C" int am_affine_maps(am_engine* e, const uint64_t* d_keys, int64_t n, uint64_t* d_canon, double* d_planes,
                               double* d_faces) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
+    RC(join_caller(e));
     for (int64_t o = 0; o < n; o += e->B) {
         int64_t m = std::min<int64_t>(e->B, n - o);
         CK(cudaMemcpyAsync(e->ckey.p, d_keys + o * e->KW, m * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
@@ -739,6 +764,7 @@ static int push_keys(am_engine* e, const uint64_t* d_keys, int64_t n) {
 
 extern "C" int am_push_candidates(am_engine* e, const uint64_t* d_keys, int64_t n) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
+    RC(join_caller(e));
     return push_keys(e, d_keys, n);
 }
 
@@ -780,6 +806,7 @@ extern "C" int am_outbox_counts(am_engine* e, int64_t* h_total) {
 // move the outbox to d_out grouped by owner rank (h_counts[world] keys per owner) and clear it
 extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out, int64_t* h_counts) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
+    RC(join_caller(e));
     RC(sync_counters(e));
     const int world = e->P.world, KW = e->KW;
     int64_t n = (int64_t)e->hctr[C_NOUT];
@@ -799,8 +826,8 @@ extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out, int64_t* h_counts) 
         CK(cudaMemcpyAsync(idx.p, order.data(), n * 4, cudaMemcpyHostToDevice, e->stream));
         launch_gather_keys(e->outbox.p, idx.p, n, KW, d_out, e->stream);
         CK(cudaStreamSynchronize(e->stream));
-        own.release();
-        idx.release();
+        own.release(e->stream);
+        idx.release(e->stream);
     }
     RC(set_counter(e, C_NOUT, 0));
     return AM_OK;
@@ -811,6 +838,7 @@ extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out, int64_t* h_counts) 
 extern "C" int am_seed(am_engine* e, const double* d_pts, int64_t n) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
     if (n == 0) return AM_OK;
+    RC(join_caller(e));
     if (n > e->B) return fail(AM_ERR_ARG, "too many seeds for one batch (%lld > %lld)", (long long)n, (long long)e->B);
     cudaStream_t s = e->stream;
     int KW = e->KW;
@@ -849,6 +877,7 @@ extern "C" int am_dichotomy(am_engine* e, const double* d_xpos, const double* d_
                             double seed_tol, int max_iters, double* d_out) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
     if (n == 0) return AM_OK;
+    RC(join_caller(e));
     if (n > e->PB) return fail(AM_ERR_ARG, "too many dichotomy pairs (%lld)", (long long)n);
     cudaStream_t s = e->stream;
     DBuf<double> xp, xn, fp, fn, mid, vals;
@@ -875,7 +904,8 @@ extern "C" int am_dichotomy(am_engine* e, const double* d_xpos, const double* d_
         }
     }
     CK(cudaStreamSynchronize(s));
-    xp.release(); xn.release(); fp.release(); fn.release(); mid.release(); vals.release(); act.release();
+    for (auto* b : {&xp, &xn, &fp, &fn, &mid, &vals}) b->release(s);
+    act.release(s);
     return AM_OK;
 }
 
@@ -885,7 +915,10 @@ extern "C" int am_result_counts(am_engine* e, int64_t* h) {
     RC(sync_counters(e));
     int64_t nc = (int64_t)e->hctr[C_CELLS], nvt = (int64_t)e->hctr[C_VERTS];
     std::vector<int32_t> nv(nc);
-    if (nc) CK(cudaMemcpy(nv.data(), e->cell_nv.p, nc * 4, cudaMemcpyDeviceToHost));
+    if (nc) {
+        CK(cudaMemcpyAsync(nv.data(), e->cell_nv.p, nc * 4, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+    }
     int64_t faces = 0, empty = 0, verts = 0, ovf = 0;
     for (int64_t i = 0; i < nc; i++) {
         if (nv[i] > 0) { faces++; verts += nv[i]; }
@@ -918,6 +951,7 @@ static int result_assemble(am_engine* e, uint64_t* d_keys, int32_t* d_nverts, do
 extern "C" int am_result_copy_device(am_engine* e, uint64_t* d_keys, int32_t* d_nverts, double* d_verts,
                                      int32_t* d_edge_nrefs, int32_t* d_edge_refs) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
+    RC(join_caller(e));
     RC(sync_counters(e));
     RC(result_assemble(e, d_keys, d_nverts, d_verts, d_edge_nrefs, d_edge_refs));
     CK(cudaStreamSynchronize(e->stream));
@@ -952,8 +986,9 @@ extern "C" int am_result_copy(am_engine* e, uint64_t* h_keys, int32_t* h_nverts,
 // face-kernel instrumentation counters (non-zero only in AM_FACE_STATS builds); reset after read
 extern "C" int am_debug_counters(am_engine* e, uint64_t* h_out64) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
-    CK(cudaMemcpy(h_out64, e->dbg.p, 64 * 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemset(e->dbg.p, 0, 64 * 8));
+    CK(cudaMemcpyAsync(h_out64, e->dbg.p, 64 * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemsetAsync(e->dbg.p, 0, 64 * 8, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
     return AM_OK;
 }
 

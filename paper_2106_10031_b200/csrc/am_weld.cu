@@ -56,8 +56,8 @@ __device__ inline CellKey key_of(const double* v, double inv, bool exact) {
 struct Table {
     unsigned long long* tag;
     CellKey* key;
-    int* start;   // first sorted position of the cell's vertices
-    int* count;
+    int* start;   // the cell's vertices are sorted positions [start, end)
+    int* end;
     unsigned long long mask, seed;
 };
 
@@ -104,7 +104,7 @@ __global__ void k_weld_ranges(const unsigned long long* sorted, int n, Table T) 
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
         unsigned s = (unsigned)(sorted[p] >> 32);
         if (p == 0 || (unsigned)(sorted[p - 1] >> 32) != s) T.start[s] = p;
-        if (p == n - 1 || (unsigned)(sorted[p + 1] >> 32) != s) T.count[s] = p + 1 - T.start[s];
+        if (p == n - 1 || (unsigned)(sorted[p + 1] >> 32) != s) T.end[s] = p + 1;
     }
 }
 
@@ -128,7 +128,7 @@ __global__ void k_weld_cands(const double* v, int n, double tol, double inv, int
             }
             const long long s = table_find(T, c2);
             if (s < 0) continue;
-            const int b = T.start[s], e = b + T.count[s];
+            const int b = T.start[s], e = T.end[s];
             for (int r = b; r < e; r++) {
                 const int j = (int)(unsigned)(sorted[r] & 0xffffffffull);
                 if (j >= i) break;   // ascending: only earlier vertices exist at i's turn
@@ -286,14 +286,14 @@ extern "C" int am_weld(const double* d_verts, int64_t n_verts, const int64_t* d_
     while (cap < 2ull * (unsigned long long)n + 2) cap <<= 1;
     Tmp<unsigned long long> tag(s), sk(s), sk2(s);
     Tmp<CellKey> keys(s);
-    Tmp<int> start(s), count(s), slot(s), flag(s), status(s), hit(s), rank(s), oflag(s), orank(s), dev(s);
+    Tmp<int> start(s), endp(s), slot(s), flag(s), status(s), hit(s), rank(s), oflag(s), orank(s), dev(s);
     Tmp<long long> ncand(s), coff(s), outn(s), ooff(s);
     Tmp<int> cand(s);
-    WCK(tag.alloc(cap)); WCK(keys.alloc(cap)); WCK(start.alloc(cap)); WCK(count.alloc(cap));
+    WCK(tag.alloc(cap)); WCK(keys.alloc(cap)); WCK(start.alloc(cap)); WCK(endp.alloc(cap));
     WCK(slot.alloc(n)); WCK(sk.alloc(n)); WCK(sk2.alloc(n)); WCK(flag.alloc(n)); WCK(ncand.alloc(n + 1));
     WCK(status.alloc(n)); WCK(hit.alloc(n)); WCK(rank.alloc(n)); WCK(coff.alloc(n + 1)); WCK(dev.alloc(2));
     WCK(outn.alloc(nl + 1)); WCK(oflag.alloc(nl + 1)); WCK(orank.alloc(nl + 1)); WCK(ooff.alloc(nl + 1));
-    Table T{tag.p, keys.p, start.p, count.p, cap - 1, 0x243f6a8885a308d3ull};
+    Table T{tag.p, keys.p, start.p, endp.p, cap - 1, 0x243f6a8885a308d3ull};
     const unsigned G = grid_for(n);
     for (int attempt = 0;; attempt++) {
         WCK(cudaMemsetAsync(tag.p, 0, cap * 8, s));
