@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seeds", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the capped configs[2] measurement")
+    ap.add_argument("--deepsdf-cells", type=int, default=1_000_000)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -288,31 +290,78 @@ def main():
     roof["kernel"] = dominant
 
     # ------------------------------------------------------------------ e2e
+    # the public call a user makes, from host buffers: march(net, cfg) (engine set-up + weight
+    # upload, seeding, BFS, sorted results back to host) + MarchResult.welded_mesh() (GPU weld,
+    # welded mesh back to host) = the end-to-end mesh time
     e2e = None
     if world == 1:
         cfg = marching.MarchConfig(seeds=args.seeds, rng_seed=0, bbox=bbox)
-        marching.march(net, cfg)   # warm
-        e_times = []
+        marching.march(net, cfg).welded_mesh()   # warm
+        e_times, m_times = [], []
         h2d = d2h = 0
+        from paper_2106_10031_b200.network import to_blob
         for _ in range(max(1, min(args.steps, 3))):
             flush_l2(flush)
             torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+            t0 = time.perf_counter()
             r = marching.march(net, cfg)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            e_times.append(e0.elapsed_time(e1))
-            from paper_2106_10031_b200.network import to_blob
+            t1 = time.perf_counter()
+            mesh = r.welded_mesh()
+            t2 = time.perf_counter()
+            e_times.append((t2 - t0) * 1e3)
+            m_times.append((t1 - t0) * 1e3)
             blob = to_blob(net)
-            h2d = blob.params.nbytes + args.seeds * 64 * 3 * 8 * 2 + args.seeds * 3 * 8
-            d2h = (r.keys.nbytes + r.nverts.nbytes + r.verts.nbytes + r.edge_nrefs.nbytes
-                   + r.edge_refs.nbytes // 2)
+            # inputs: parameters, step/sub tables, seed-trigger sample points (64 x 64 pairs)
+            h2d = (blob.params.nbytes + blob.steps.nbytes + blob.subs.nbytes + args.seeds * 64 * 2 * 3 * 8
+                   + r.verts.nbytes + 2 * 8 * (len(r.nverts) + 1))
+            d2h = (r.keys.nbytes + r.nverts.nbytes + r.verts.nbytes + r.edge_nrefs.nbytes + r.edge_refs.nbytes // 2
+                   + mesh.vertices.nbytes + sum(f.nbytes for f in mesh.faces))
         e_ms = float(np.mean(e_times))
         e2e = {"value": r.report.cells_visited / (e_ms * 1e-3), "unit": "cells/s", "ms_per_step": e_ms,
+               "mesh_time_s": e_ms * 1e-3, "march_only_ms": float(np.mean(m_times)),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "api": "paper_2106_10031_b200.march(net, MarchConfig(seeds=64)) from host buffers"}
+               "mesh": {"vertices": int(mesh.n_vertices), "faces": int(mesh.n_faces),
+                        "dropped": int(mesh.dropped_faces)},
+               "api": "paper_2106_10031_b200.march(net, MarchConfig(seeds=64)).welded_mesh() from host buffers, "
+                      "wall clock (host-synchronous API)"}
+
+    # --------------------------------------- the largest MLP (configs[2]), capped sample
+    others = {}
+    if world == 1 and not args.no_extra:
+        from paper_2106_10031_b200 import synth
+        dnet = synth.deepsdf_mlp(512, 8, 4, seed=0)
+        cap = args.deepsdf_cells
+        deng = Engine(dnet, bbox=bbox, max_cells=cap)
+        dseeds = torch.as_tensor(sample_seeds(deng, args.seeds, bbox, rng_seed=0), device=dev)
+
+        def drun():
+            deng.reset()
+            deng.seed(dseeds)
+            return deng.run()
+        drun()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dw = drun()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        d_ms = e0.elapsed_time(e1)
+        dcells = deng.counts()["cells"]
+        deng.set_timing(True)
+        drun()
+        ds = deng.stats()
+        deng.set_timing(False)
+        dtf = ds["compose_flops"] / (ds["compose_ms"] * 1e-3) / 1e12 if ds["compose_ms"] else 0.0
+        others["configs[2]"] = {
+            "workload": "DeepSDF-style 3-(512x8)-1, linear skip over layers 1-4, seed 0, fp64, 64 dichotomy seeds; "
+                        f"first {dcells} cells (max_cells cap {cap}; the full march is ~16M cells)",
+            "cells": int(dcells), "waves": int(dw), "ms": d_ms, "cells_per_s": dcells / (d_ms * 1e-3),
+            "compose_dmma": {"achieved_tflops": dtf, "peak_tflops": float(pk[0]),
+                             "frac": dtf / pk[0] if pk[0] else None, "ms": ds["compose_ms"],
+                             "share_of_march": ds["compose_ms"] / d_ms if d_ms else None},
+        }
+        del deng
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -326,8 +375,8 @@ def main():
             "config": {"workload": WORKLOAD, "cells_per_step": cells, "waves": int(waves),
                        "parallelism": f"dp{world} (state-hash ownership)" if world > 1 else "1 GPU",
                        "l2": "flushed between timed steps (512 MiB write)",
-                       "mesh_time_s": t_step * 1e-3},
-            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+                       "device_march_time_s": t_step * 1e-3},
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "other_configs": others,
             "gpu_launches": int(launches), "clocks": clocks,
             "fp64_peaks_tflops": {"dmma": float(pk[0]), "dfma": float(pk[1])},
         }

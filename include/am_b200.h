@@ -81,6 +81,11 @@ int am_engine_create(am_engine **out, const am_net_desc *net, const am_march_par
 int am_engine_destroy(am_engine *e);
 int am_engine_key_words(const am_engine *e);
 int am_engine_reset(am_engine *e);                       /* clear visited set + results */
+/* new weights for an engine of the same architecture (same step / sub tables and parameter
+ * count, e.g. another latent code folded into the first layer, or a training checkpoint):
+ * re-uploads the values; buffers, TMA descriptors and captured graphs are reused.
+ * Replaces re-running the reference's network construction (network.py:131-216) per march. */
+int am_engine_load_params(am_engine *e, const double *h_params, int64_t n_params);
 
 /* --- per-point primitives (replace forward_many / state_at / affine_maps) - */
 /* F(x) and the activation state at n points (device buffers; keys may be NULL) */

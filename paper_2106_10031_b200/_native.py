@@ -75,6 +75,7 @@ SIGNATURES = {
     "am_set_timing": (ctypes.c_int, [P, ctypes.c_int]),
     "am_bench_fp64_peak": (ctypes.c_int, [ctypes.c_int, P]),
     "am_debug_counters": (ctypes.c_int, [P, P]),
+    "am_engine_load_params": (ctypes.c_int, [P, P, ctypes.c_int64]),
     "am_weld": (ctypes.c_int, [P, ctypes.c_int64, P, P, ctypes.c_int64, ctypes.c_double, P, P, P, P, P, P, P]),
 }
 

@@ -117,6 +117,8 @@ struct am_engine {
     std::vector<CUtensorMap> tmW, tmV;
     std::vector<int> tmV_ok;
     DBuf<double> params, wpad;
+    int64_t n_params = 0;
+    std::vector<int64_t> woff, voff;   // padded weight layout (wpad_layout)
     DBuf<uint8_t> subdev;
     double flops_per_cell = 0, flops_per_point = 0;
     // hash set + queue
@@ -273,6 +275,57 @@ static int ensure_results(am_engine* e, int64_t cells) {
 }
 
 // -------------------------------------------------------------- lifecycle
+// padded weight layout: per step, W (and the shortcut V) with a row stride of 16 doubles
+static int64_t wpad_layout(am_engine* e, std::vector<int64_t>& woff, std::vector<int64_t>& voff) {
+    const int ns = (int)(e->steps.size() / AM_STEP_FIELDS);
+    woff.assign(ns, 0);
+    voff.assign(ns, -1);
+    int64_t tot = 0;
+    auto pad = [](int64_t x) { return (x + 15) / 16 * 16; };
+    for (int s = 0; s < ns; s++) {
+        const int64_t* st = &e->steps[(size_t)s * AM_STEP_FIELDS];
+        woff[s] = tot;
+        tot += st[1] * pad(st[0]);
+        if (st[5] >= 0) { voff[s] = tot; tot += st[1] * pad(st[10]); }
+    }
+    return tot;
+}
+
+// network parameters -> device: the flat parameter buffer, the padded per-step weight copies
+// the TMA descriptors point at, and the per-subnetwork head table (head bias by value)
+static int upload_params(am_engine* e, const double* h_params) {
+    const int ns = (int)(e->steps.size() / AM_STEP_FIELDS);
+    CK(cudaMemcpyAsync(e->params.p, h_params, (size_t)e->n_params * sizeof(double), cudaMemcpyHostToDevice,
+                       e->stream));
+    auto pad = [](int64_t x) { return (x + 15) / 16 * 16; };
+    std::vector<double> hw((size_t)std::max<int64_t>(e->wpad.n, 1), 0.0);
+    for (int s = 0; s < ns; s++) {
+        const int64_t* st = &e->steps[(size_t)s * AM_STEP_FIELDS];
+        int64_t n_in = st[0], n_out = st[1], ld = pad(n_in);
+        for (int64_t r = 0; r < n_out; r++)
+            memcpy(&hw[e->woff[s] + r * ld], h_params + st[2] + r * n_in, (size_t)n_in * sizeof(double));
+        if (st[5] >= 0) {
+            int64_t n_sin = st[10], ldv = pad(n_sin);
+            for (int64_t r = 0; r < n_out; r++)
+                memcpy(&hw[e->voff[s] + r * ldv], h_params + st[5] + r * n_sin, (size_t)n_sin * sizeof(double));
+        }
+    }
+    CK(cudaMemcpyAsync(e->wpad.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    std::vector<SubDev> hsub(e->M);
+    for (int j = 0; j < e->M; j++) {
+        const int64_t* sb = &e->subs[(size_t)j * AM_SUB_FIELDS];
+        int last = (int)(sb[0] + sb[1] - 1);
+        const int64_t* st = &e->steps[(size_t)last * AM_STEP_FIELDS];
+        hsub[j].last_row = (int)st[7];
+        hsub[j].last_n = (int)st[1];
+        hsub[j].hw = e->params.p + sb[2];
+        hsub[j].hb = h_params[sb[3]];
+    }
+    CK(cudaMemcpyAsync(e->subdev.p, hsub.data(), sizeof(SubDev) * e->M, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));   // host staging vectors go out of scope
+    return AM_OK;
+}
+
 extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const am_march_params* p, int device,
                                 void* stream) {
     if (!out || !net || !p) return fail(AM_ERR_ARG, "null argument");
@@ -303,48 +356,27 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     e->zs = e->NB;
     e->steps.assign(net->h_steps, net->h_steps + (size_t)net->n_steps * AM_STEP_FIELDS);
     e->subs.assign(net->h_subs, net->h_subs + (size_t)net->n_subs * AM_SUB_FIELDS);
+    e->n_params = net->n_params;
     CK(e->params.reserve(std::max<int64_t>(net->n_params, 1), e->stream));
-    CK(cudaMemcpyAsync(e->params.p, net->h_params, (size_t)net->n_params * sizeof(double), cudaMemcpyHostToDevice,
-                       e->stream));
 
     // padded weight copies (row stride multiple of 16 doubles) for TMA
     int ns = net->n_steps;
-    std::vector<int64_t> woff(ns), voff(ns, -1);
-    int64_t tot = 0;
-    auto pad = [](int64_t x) { return (x + 15) / 16 * 16; };
-    for (int s = 0; s < ns; s++) {
-        const int64_t* st = &e->steps[(size_t)s * AM_STEP_FIELDS];
-        woff[s] = tot;
-        tot += st[1] * pad(st[0]);
-        if (st[5] >= 0) { voff[s] = tot; tot += st[1] * pad(st[10]); }
-    }
-    std::vector<double> hw((size_t)std::max<int64_t>(tot, 1), 0.0);
-    for (int s = 0; s < ns; s++) {
-        const int64_t* st = &e->steps[(size_t)s * AM_STEP_FIELDS];
-        int64_t n_in = st[0], n_out = st[1], ld = pad(n_in);
-        for (int64_t r = 0; r < n_out; r++)
-            for (int64_t k = 0; k < n_in; k++) hw[woff[s] + r * ld + k] = net->h_params[st[2] + r * n_in + k];
-        if (st[5] >= 0) {
-            int64_t n_sin = st[10], ldv = pad(n_sin);
-            for (int64_t r = 0; r < n_out; r++)
-                for (int64_t k = 0; k < n_sin; k++) hw[voff[s] + r * ldv + k] = net->h_params[st[5] + r * n_sin + k];
-        }
-    }
-    CK(e->wpad.reserve((int64_t)hw.size(), e->stream));
-    CK(cudaMemcpyAsync(e->wpad.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    int64_t tot = wpad_layout(e, e->woff, e->voff);
+    CK(e->wpad.reserve(std::max<int64_t>(tot, 1), e->stream));
     e->sdev.resize(ns);
     e->tmW.resize(ns);
     e->tmV.resize(ns);
     e->tmV_ok.assign(ns, 0);
+    auto pad = [](int64_t x) { return (x + 15) / 16 * 16; };
     for (int s = 0; s < ns; s++) {
         const int64_t* st = &e->steps[(size_t)s * AM_STEP_FIELDS];
         StepDev& d = e->sdev[s];
         d.n_in = (int)st[0]; d.n_out = (int)st[1]; d.flags = (int)st[4]; d.row_off = (int)st[7];
         d.in_row_off = (int)st[8]; d.sin_row_off = (int)st[9]; d.n_sin = (int)st[10]; d.sub = (int)st[11];
-        d.W = e->wpad.p + woff[s];
+        d.W = e->wpad.p + e->woff[s];
         d.ldw = (int)pad(st[0]);
         d.b = e->params.p + st[3];
-        d.V = st[5] >= 0 ? e->wpad.p + voff[s] : nullptr;
+        d.V = st[5] >= 0 ? e->wpad.p + e->voff[s] : nullptr;
         d.ldv = st[5] >= 0 ? (int)pad(st[10]) : 0;
         d.vb = st[6] >= 0 ? e->params.p + st[6] : nullptr;
         if (!(d.flags & AM_STEP_FIRST)) {
@@ -361,19 +393,8 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
             e->flops_per_point += 2.0 * d.n_out * d.n_sin;
         }
     }
-    std::vector<SubDev> hsub(e->M);
-    for (int j = 0; j < e->M; j++) {
-        const int64_t* sb = &e->subs[(size_t)j * AM_SUB_FIELDS];
-        int last = (int)(sb[0] + sb[1] - 1);
-        const int64_t* st = &e->steps[(size_t)last * AM_STEP_FIELDS];
-        hsub[j].last_row = (int)st[7];
-        hsub[j].last_n = (int)st[1];
-        hsub[j].hw = e->params.p + sb[2];
-        hsub[j].hb = net->h_params[sb[3]];
-    }
     CK(e->subdev.reserve((int64_t)(sizeof(SubDev) * e->M), e->stream));
-    CK(cudaMemcpyAsync(e->subdev.p, hsub.data(), sizeof(SubDev) * e->M, cudaMemcpyHostToDevice, e->stream));
-    CK(cudaStreamSynchronize(e->stream));   // host staging vectors go out of scope
+    RC(upload_params(e, net->h_params));
     // batch size from the per-iteration memory budget: compose planes + worst-case probe
     // activations + emitted keys per batch cell
     int64_t budget = e->P.mem_budget > 0 ? e->P.mem_budget : (int64_t)4 << 30;
@@ -455,6 +476,18 @@ extern "C" int am_engine_destroy(am_engine* e) {
 }
 
 extern "C" int am_engine_key_words(const am_engine* e) { return e ? e->KW : 0; }
+
+// new weights for an engine built for the same architecture (same step / sub tables and
+// parameter count): everything derived from the values is re-uploaded; buffers, TMA descriptors
+// and captured graphs (which reference the buffers, not the values) stay valid
+extern "C" int am_engine_load_params(am_engine* e, const double* h_params, int64_t n_params) {
+    if (!e || !h_params) return fail(AM_ERR_ARG, "null argument");
+    if (n_params != e->n_params)
+        return fail(AM_ERR_ARG, "parameter count %lld does not match the engine's %lld", (long long)n_params,
+                    (long long)e->n_params);
+    CK(cudaStreamSynchronize(e->stream));
+    return upload_params(e, h_params);
+}
 
 extern "C" int am_engine_reset(am_engine* e) {
     if (!e) return fail(AM_ERR_ARG, "null engine");

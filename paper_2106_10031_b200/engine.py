@@ -26,6 +26,11 @@ def _require_cuda():
         raise _native.NativeUnavailable("no CUDA device visible; the meshing path runs only on a B200")
 
 
+def architecture_key(blob: NetBlob) -> tuple:
+    """What an engine is built for: step / sub tables (shapes, offsets, flags) and sizes."""
+    return (blob.steps.tobytes(), blob.subs.tobytes(), int(blob.n_bits), bool(blob.ensemble), len(blob.params))
+
+
 class Engine:
     def __init__(self, net: AnyNetwork, bbox=((-1.2,) * 3, (1.2,) * 3), max_cells: int = 10_000_000,
                  tol_cell=TOL_CELL, tol_weld=TOL_WELD, tol_onplane=TOL_ONPLANE, probe_delta=PROBE_DELTA,
@@ -109,6 +114,19 @@ class Engine:
     # --------------------------------------------------------------- marching
     def reset(self):
         _native.check(self.lib.am_engine_reset(self.h), "am_engine_reset")
+
+    def architecture(self) -> tuple:
+        return architecture_key(self.blob)
+
+    def load_network(self, net: AnyNetwork, blob: NetBlob | None = None):
+        """Swap in the weights of a network with this engine's architecture (am_engine_load_params)."""
+        blob = blob or to_blob(net)
+        if architecture_key(blob) != self.architecture():
+            raise ValueError("load_network: different architecture (layer shapes / flags / ensemble)")
+        params = np.ascontiguousarray(blob.params, dtype=np.float64)
+        _native.check(self.lib.am_engine_load_params(self.h, params.ctypes.data, len(params)),
+                      "am_engine_load_params")
+        self.net, self.blob, self._params = net, blob, params
 
     def seed(self, pts):
         t = pts if isinstance(pts, torch.Tensor) else self._dev(np.asarray(pts, np.float64).reshape(-1, 3),

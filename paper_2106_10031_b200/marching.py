@@ -13,12 +13,13 @@ from __future__ import annotations
 
 import json
 import time
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from .engine import PROBE_DELTA, TOL_CELL, TOL_ONPLANE, TOL_WELD, Engine
-from .network import AffinePlane, AnyNetwork, EnsembleSpec, StateVector, subnetworks
+from .engine import PROBE_DELTA, TOL_CELL, TOL_ONPLANE, TOL_WELD, Engine, architecture_key
+from .network import AffinePlane, AnyNetwork, EnsembleSpec, StateVector, subnetworks, to_blob
 from .seeding import sample_seeds
 
 DEFAULT_BBOX = ((-1.2, -1.2, -1.2), (1.2, 1.2, 1.2))   # reference cells.py:37
@@ -175,10 +176,9 @@ class MarchResult:
 
     def polygon_soup(self):
         from .meshes import PolygonMesh
-        offs = np.concatenate([[0], np.cumsum(np.maximum(self.nverts, 0))])
-        faces = [np.arange(offs[i], offs[i + 1], dtype=np.int64) for i in range(len(self.nverts))
-                 if self.nverts[i] > 0]
-        return PolygonMesh(self.verts.copy(), faces, None)
+        nv = self.nverts[self.nverts > 0].astype(np.int64)
+        off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
+        return PolygonMesh(self.verts.copy(), None, None, face_off=off, face_idx=np.arange(off[-1], dtype=np.int64))
 
     def welded_mesh(self, tol: float = TOL_WELD):
         """reference marching.py:126-127 weld(polygon_soup(), tol), welded on the GPU straight
@@ -187,7 +187,7 @@ class MarchResult:
         nv = self.nverts[self.nverts > 0].astype(np.int64)
         off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
         kept, foff, fidx, _, nd = weld_arrays(self.verts, off, np.arange(off[-1], dtype=np.int64), tol)
-        return PolygonMesh(kept, np.split(fidx, foff[1:-1]) if len(foff) > 1 else [], None, nd)
+        return PolygonMesh(kept, None, None, nd, face_off=foff, face_idx=fidx)
 
     def face_multiset(self, decimals: int = 10):
         """Order-independent fingerprint (reference marching.py:139-149)."""
@@ -200,10 +200,11 @@ class MarchResult:
 
 
 def refs_to_kind_index(ids: np.ndarray, n_bits: int, n_subs: int) -> np.ndarray:
-    ids = np.asarray(ids, dtype=np.int64)
-    kind = np.where(ids < n_bits, PLANE_NEURON, np.where(ids < n_bits + n_subs, PLANE_BRANCH, PLANE_BBOX))
-    index = np.where(kind == PLANE_NEURON, ids, np.where(kind == PLANE_BRANCH, ids - n_bits, ids - n_bits - n_subs))
-    return np.stack([kind, index], axis=1) if len(ids) else np.zeros((0, 2), np.int64)
+    """Global plane ids (neuron < n_bits <= branch < n_bits + n_subs <= bbox) -> (kind, index)."""
+    ids = np.asarray(ids).astype(np.int64)
+    kind = (ids >= n_bits).astype(np.int64) + (ids >= n_bits + n_subs)
+    index = ids - np.array([0, n_bits, n_bits + n_subs], dtype=np.int64)[kind]
+    return np.stack([kind, index], axis=1)
 
 
 def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, threads: int = 1) -> MarchResult:
@@ -217,13 +218,43 @@ def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, thread
                        refs_to_kind_index(erefs, b.n_bits, b.n_subs), rep, b.n_bits, seeds)
 
 
+_ENGINES: "OrderedDict[tuple, Engine]" = OrderedDict()
+ENGINE_CACHE_SIZE = 2
+
+
+def clear_engine_cache():
+    """Drop the engines march() keeps for reuse (frees their device memory)."""
+    _ENGINES.clear()
+
+
+def _engine_for(net: AnyNetwork, config: MarchConfig) -> Engine:
+    """An engine for this architecture and configuration: cached ones are reused with the new
+    weights uploaded (buffers, TMA descriptors and captured graphs do not depend on values)."""
+    import torch
+    blob = to_blob(net)
+    key = (architecture_key(blob), tuple(map(tuple, config.bbox)), config.max_cells, config.tol_cell,
+           config.tol_weld, config.probe_delta, config.batch_cells, config.mem_budget,
+           torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = Engine(net, bbox=config.bbox, max_cells=config.max_cells, tol_cell=config.tol_cell,
+                     tol_weld=config.tol_weld, probe_delta=config.probe_delta,
+                     batch_cells=config.batch_cells, mem_budget=config.mem_budget)
+        _ENGINES[key] = eng
+        while len(_ENGINES) > ENGINE_CACHE_SIZE:
+            _ENGINES.popitem(last=False)
+    else:
+        eng.load_network(net, blob)
+        eng.reset()
+        _ENGINES.move_to_end(key)
+    return eng
+
+
 def march(net: AnyNetwork, config: MarchConfig | None = None, engine: Engine | None = None) -> MarchResult:
     """Extract every analytic face reachable from the seeds (reference marching.py:304-362)."""
     config = config or MarchConfig()
     t0 = time.perf_counter()
-    eng = engine or Engine(net, bbox=config.bbox, max_cells=config.max_cells, tol_cell=config.tol_cell,
-                           tol_weld=config.tol_weld, probe_delta=config.probe_delta,
-                           batch_cells=config.batch_cells, mem_budget=config.mem_budget)
+    eng = engine or _engine_for(net, config)
     if config.seed_points is not None:
         seeds = np.asarray(config.seed_points, dtype=np.float64).reshape(-1, 3)
     else:

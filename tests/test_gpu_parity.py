@@ -105,3 +105,22 @@ def test_march_matches_oracle_larger(which):
     o = oracle.march(net, bbox=kw.get("bbox", m.DEFAULT_BBOX), seed_points=r.seeds)
     assert r.report.cells_visited > 50
     assert_same_march(r, o.keys, o.branch, o.nverts, o.verts, o.edge_nrefs, o.edge_refs)
+
+
+@pytest.mark.gpu
+def test_engine_cache_reuses_with_new_weights():
+    """march() reuses a cached engine for a same-architecture network with different weights:
+    am_engine_load_params must refresh every value-derived buffer (padded TMA copies, biases,
+    head bias)."""
+    from paper_2106_10031_b200 import MarchConfig, march
+    from paper_2106_10031_b200.marching import clear_engine_cache
+    clear_engine_cache()
+    bbox = ((-1.0,) * 3, (1.0,) * 3)
+    cfg = MarchConfig(bbox=bbox, seeds=8, rng_seed=3)
+    for seed in (21, 22, 21):
+        net = make_random_net(3, 16, seed)
+        got = march(net, cfg)
+        ref = oracle.march(net, bbox=bbox, seeds=8, rng_seed=3)
+        np.testing.assert_array_equal(got.keys, ref.keys)
+        np.testing.assert_array_equal(got.nverts, ref.nverts)
+        assert np.abs(got.verts - ref.verts).max(initial=0) <= 1e-9

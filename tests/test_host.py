@@ -106,3 +106,31 @@ def test_golden_fixtures_are_self_consistent():
         assert len(g["keys"]) == g["report"]["cells_visited"]
         assert g["nverts"].sum() == len(g["verts"])
         assert g["edge_nrefs"].sum() == len(g["edge_refs"])
+
+
+def test_polygon_mesh_csr_and_triangulate():
+    """PolygonMesh keeps loops as CSR with the reference's constructor / faces semantics; the
+    vectorised fan triangulation equals the reference's loop (meshes.py:152-159)."""
+    from paper_2106_10031_b200.meshes import PolygonMesh, triangulate
+    rng = np.random.default_rng(0)
+    v = rng.normal(size=(50, 3))
+    loops = [rng.choice(50, size=k, replace=False) for k in rng.integers(3, 9, size=40)]
+    m = PolygonMesh(v, loops)
+    assert m.n_faces == 40
+    for a, b in zip(m.faces, loops):
+        np.testing.assert_array_equal(a, b)
+    m2 = PolygonMesh(v, None, face_off=m.face_off, face_idx=m.face_idx)
+    for a, b in zip(m2.faces, loops):
+        np.testing.assert_array_equal(a, b)
+    ref = [(lp[0], lp[i], lp[i + 1]) for lp in loops for i in range(1, len(lp) - 1)]
+    np.testing.assert_array_equal(triangulate(m2).triangles, np.array(ref))
+    with pytest.raises(ValueError):
+        PolygonMesh(v, [np.array([0, 1, 60])])
+
+
+def test_refs_to_kind_index():
+    from paper_2106_10031_b200.marching import refs_to_kind_index
+    nb, ns = 10, 2
+    ids = np.array([0, 9, 10, 11, 12, 17], np.int32)
+    np.testing.assert_array_equal(refs_to_kind_index(ids, nb, ns),
+                                  [[0, 0], [0, 9], [1, 0], [1, 1], [2, 0], [2, 5]])
