@@ -132,7 +132,7 @@ class MarchResult:
     keys (C, nbytes) packbits states of every visited cell (empty faces
     included), sorted by (key, branch) as the reference sorts; nverts (C,)
     (0 = empty face); verts (V, 3); edge_nrefs (V,); edge_refs (R, 2) as
-    (kind, index).
+    (kind, index).  Integer arrays are int32.
     """
 
     keys: np.ndarray
@@ -200,22 +200,42 @@ class MarchResult:
 
 
 def refs_to_kind_index(ids: np.ndarray, n_bits: int, n_subs: int) -> np.ndarray:
-    """Global plane ids (neuron < n_bits <= branch < n_bits + n_subs <= bbox) -> (kind, index)."""
-    ids = np.asarray(ids).astype(np.int64)
-    kind = (ids >= n_bits).astype(np.int64) + (ids >= n_bits + n_subs)
-    index = ids - np.array([0, n_bits, n_bits + n_subs], dtype=np.int64)[kind]
-    return np.stack([kind, index], axis=1)
+    """Global plane ids (neuron < n_bits <= branch < n_bits + n_subs <= bbox) -> (kind, index)
+    pairs, int32 (R, 2)."""
+    ids = np.asarray(ids, dtype=np.int32)
+    out = np.empty((len(ids), 2), dtype=np.int32)
+    g1, g2 = ids >= n_bits, ids >= n_bits + n_subs
+    out[:, 0] = g1
+    out[:, 0] += g2
+    out[:, 1] = ids
+    np.subtract(out[:, 1], n_bits, out=out[:, 1], where=g1)
+    np.subtract(out[:, 1], n_subs, out=out[:, 1], where=g2)
+    return out
 
 
 def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, threads: int = 1) -> MarchResult:
-    c, keys, nverts, verts, enr, erefs = eng.results()
+    """Sorted results (GPU sort + gathers, am_result_copy_device), converted to the reference's
+    representations on the device (edge refs -> (kind, index)), one pinned copy per array."""
+    import torch
+    c, keys, nverts, verts, enr, erefs = eng.results_device()
     b = eng.blob
-    kb, branch = words_to_packbits(keys, b.n_bits, b.ensemble)
+    nb, ns = b.n_bits, b.n_subs
+    g1, g2 = erefs >= nb, erefs >= nb + ns
+    kind = g1.to(torch.int32) + g2.to(torch.int32)
+    index = erefs - nb * g1.to(torch.int32) - ns * g2.to(torch.int32)
+    refs = torch.stack([kind, index], dim=1)
+
+    def host(t):
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        return out
+    hk, hn, hv, he, hr = (host(t) for t in (keys, nverts, verts, enr, refs))
+    torch.cuda.current_stream(eng.dev).synchronize()
+    kb, branch = words_to_packbits(hk.numpy().view(np.uint64), nb, b.ensemble)
     rep = MarchReport(cells_visited=c["cells"], faces_emitted=c["faces"], empty_faces=c["empty"],
                       open_edges=c["open_edges"], seconds=time.perf_counter() - t0, seeds_used=len(seeds),
                       capped=bool(c["capped"]), threads=threads, waves=waves, overflow=c["overflow"])
-    return MarchResult(kb, branch, nverts.astype(np.int64), verts, enr.astype(np.int64),
-                       refs_to_kind_index(erefs, b.n_bits, b.n_subs), rep, b.n_bits, seeds)
+    return MarchResult(kb, branch, hn.numpy(), hv.numpy(), he.numpy(), hr.numpy(), rep, nb, seeds)
 
 
 _ENGINES: "OrderedDict[tuple, Engine]" = OrderedDict()
