@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the capped configs[2] measurement")
     ap.add_argument("--deepsdf-cells", type=int, default=1_000_000)
+    ap.add_argument("--latent-cells", type=int, default=20_000)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -362,6 +363,29 @@ def main():
                              "share_of_march": ds["compose_ms"] / d_ms if d_ms else None},
         }
         del deng
+
+        # configs[4]: a batch of 64 latent-conditioned shapes (256-d code folded into the first
+        # layer and skip biases of one DeepSDF decoder), one reused engine, per-shape cap
+        from paper_2106_10031_b200.batch import march_batch
+        lnets, _ = synth.latent_batch(n_shapes=64, latent_dim=256, width=512, depth=8, skip_at=4, seed=0)
+        lcfg = marching.MarchConfig(seeds=args.seeds, rng_seed=0, bbox=bbox, max_cells=args.latent_cells)
+        march_batch(lnets[:2], lcfg)   # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        lres = march_batch(lnets, lcfg)
+        torch.cuda.synchronize()
+        l_s = time.perf_counter() - t0
+        lcells = sum(r.report.cells_visited for _, r in lres)
+        others["configs[4]"] = {
+            "workload": "64 latent-conditioned shapes: 256-d code (+) xyz into a DeepSDF 3-(512x8)-1 decoder "
+                        f"(code folded into first-layer / skip biases), fp64, 64 dichotomy seeds per shape, "
+                        f"first {args.latent_cells} cells per shape (max_cells cap)",
+            "shapes": len(lres), "cells": int(lcells), "seconds": l_s, "cells_per_s": lcells / l_s,
+            "per_shape_ms": 1e3 * l_s / len(lres),
+            "api": "paper_2106_10031_b200.batch.march_batch(nets, MarchConfig) -> MarchResults on host; "
+                   "one engine reused (am_engine_load_params), wall clock",
+        }
+        marching.clear_engine_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -68,6 +68,9 @@ typedef struct {
     int64_t batch_cells;  /* cells composed per batch (0 = size from mem_budget) */
     int64_t mem_budget;   /* bytes for per-batch plane buffers (0 = 2 GiB) */
     int32_t rank, world;  /* state ownership: owner(state) = hash(state) % world */
+    int32_t n_shapes;     /* > 1: batch of same-architecture shapes marched together (the key
+                           * gains a trailing shape word; see am_engine_set_shape_params) */
+    int32_t reserved;
 } am_march_params;
 
 typedef struct am_engine am_engine;
@@ -86,10 +89,22 @@ int am_engine_reset(am_engine *e);                       /* clear visited set + 
  * re-uploads the values; buffers, TMA descriptors and captured graphs are reused.
  * Replaces re-running the reference's network construction (network.py:131-216) per march. */
 int am_engine_load_params(am_engine *e, const double *h_params, int64_t n_params);
+/* Batch of shapes (n_shapes > 1): shape s uses the engine's parameters with the n_idx entries
+ * h_param_idx[j] replaced by h_values[s * n_idx + j].  Every replaced entry must lie in a bias
+ * vector (a layer bias, a shortcut bias or a head bias), so the shapes share every weight
+ * matrix and one DMMA contraction serves all of them -- e.g. latent-conditioned decoders with
+ * the code folded into the biases it enters (BASELINE configs[4]).  Each shape's march is the
+ * reference march (marching.py:304-362) of its own network. */
+int am_engine_set_shape_params(am_engine *e, const int64_t *h_param_idx, int64_t n_idx, const double *h_values);
+/* shape of the points given to later am_forward / am_dichotomy / am_seed calls */
+int am_engine_set_shape(am_engine *e, int32_t shape);
 
 /* --- per-point primitives (replace forward_many / state_at / affine_maps) - */
 /* F(x) and the activation state at n points (device buffers; keys may be NULL) */
 int am_forward(am_engine *e, const double *d_pts, int64_t n, double *d_vals, uint64_t *d_keys);
+/* the same for a batch-of-shapes engine with a per-point shape (device int32 [n]) */
+int am_forward_shapes(am_engine *e, const double *d_pts, const int32_t *d_shapes, int64_t n, double *d_vals,
+                      uint64_t *d_keys);
 /* canonical state, raw neuron planes (n_bits x 4: nx,ny,nz,c) and face planes
  * (n_subs x 4) of n states; device buffers */
 int am_affine_maps(am_engine *e, const uint64_t *d_keys, int64_t n, uint64_t *d_canon,
@@ -99,10 +114,13 @@ int am_affine_maps(am_engine *e, const uint64_t *d_keys, int64_t n, uint64_t *d_
 /* seed points -> refined canonical seed states queued as candidates
  * (reference marching.py:201-213 _refine_seed_state, 322-324) */
 int am_seed(am_engine *e, const double *d_pts, int64_t n);
+int am_seed_shapes(am_engine *e, const double *d_pts, const int32_t *d_shapes, int64_t n);
 /* batched bisection triggering between F>0 and F<0 samples (reference
  * seeding.py:84-112); writes n surface points to d_out */
 int am_dichotomy(am_engine *e, const double *d_xpos, const double *d_xneg, int64_t n, double eps,
                  double seed_tol, int max_iters, double *d_out);
+int am_dichotomy_shapes(am_engine *e, const double *d_xpos, const double *d_xneg, const int32_t *d_shapes,
+                        int64_t n, double eps, double seed_tol, int max_iters, double *d_out);
 /* queue n raw candidate states (device keys) for the next absorb */
 int am_push_candidates(am_engine *e, const uint64_t *d_keys, int64_t n);
 /* one BFS iteration: dequeue up to a batch of states, compose them,

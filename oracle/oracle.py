@@ -355,6 +355,14 @@ class OracleShardEngine:
     def queue_size(self):
         return len(self.queue)
 
+    def sample_seeds(self, count, bbox, scheme="dichotomy", rng_seed=0):
+        return sample_seeds(self.on, count, bbox, scheme=scheme, rng_seed=rng_seed)
+
+    def load_network(self, net):
+        """Next network of a same-architecture batch (the stand-in just rebuilds)."""
+        self.on = OracleNet(net)
+        self.net = net
+
     def push(self, keys):
         self._route([np.asarray(k).view(np.uint64) for k in keys.numpy()])
 

@@ -46,6 +46,7 @@ class MarchParams(ctypes.Structure):
         ("tol_onplane", ctypes.c_double), ("probe_delta", ctypes.c_double),
         ("max_cells", ctypes.c_int64), ("batch_cells", ctypes.c_int64),
         ("mem_budget", ctypes.c_int64), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("n_shapes", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 
@@ -76,6 +77,12 @@ SIGNATURES = {
     "am_bench_fp64_peak": (ctypes.c_int, [ctypes.c_int, P]),
     "am_debug_counters": (ctypes.c_int, [P, P]),
     "am_engine_load_params": (ctypes.c_int, [P, P, ctypes.c_int64]),
+    "am_engine_set_shape_params": (ctypes.c_int, [P, P, ctypes.c_int64, P]),
+    "am_engine_set_shape": (ctypes.c_int, [P, ctypes.c_int32]),
+    "am_forward_shapes": (ctypes.c_int, [P, P, P, ctypes.c_int64, P, P]),
+    "am_seed_shapes": (ctypes.c_int, [P, P, P, ctypes.c_int64]),
+    "am_dichotomy_shapes": (ctypes.c_int, [P, P, P, P, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_int, P]),
     "am_weld": (ctypes.c_int, [P, ctypes.c_int64, P, P, ctypes.c_int64, ctypes.c_double, P, P, P, P, P, P, P]),
 }
 

@@ -102,6 +102,8 @@ __device__ __forceinline__ void input_elem(const LayerLaunch& L, uint64_t* keys,
     int row = st.row_off + r;
     double* z = L.Z + (item * L.zs + row) * C;
     bool sc = st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR);
+    const bool has_vb = st.vb || st.vb_shape;
+    const int shp = item_shape(key, L.shape_w);
     if (C == 4) {
         double a0 = w[0], a1 = w[1], a2 = w[2], c = 0.0;
         if (sc) {
@@ -111,12 +113,12 @@ __device__ __forceinline__ void input_elem(const LayerLaunch& L, uint64_t* keys,
             } else {
                 const double* v = st.V + (int64_t)r * st.ldv;
                 s0 = v[0]; s1 = v[1]; s2 = v[2];
-                if (st.vb) sc_c = st.vb[r];
+                if (has_vb) sc_c = step_vbias(st, shp, r);
             }
             a0 = s0 + a0; a1 = s1 + a1; a2 = s2 + a2;
-            c = (sc_c + c) + st.b[r];
+            c = (sc_c + c) + step_bias(st, shp, r);
         } else {
-            c = c + st.b[r];
+            c = c + step_bias(st, shp, r);
         }
         double nrm = sqrt((a0 * a0 + a1 * a1) + a2 * a2);
         if (!(nrm > kDegen)) {
@@ -139,11 +141,11 @@ __device__ __forceinline__ void input_elem(const LayerLaunch& L, uint64_t* keys,
             } else {
                 const double* v = st.V + (int64_t)r * st.ldv;
                 s = (x[0] * v[0] + x[1] * v[1]) + x[2] * v[2];
-                if (st.vb) s = s + st.vb[r];
+                if (has_vb) s = s + step_vbias(st, shp, r);
             }
-            pre = (s + acc) + st.b[r];
+            pre = (s + acc) + step_bias(st, shp, r);
         } else {
-            pre = acc + st.b[r];
+            pre = acc + step_bias(st, shp, r);
         }
         if (pre > 0.0) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)key_mask(row));
         z[0] = pre;
@@ -183,11 +185,6 @@ void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
 }
 
 // ----------------------------------------------------------- GEMM step
-struct SubDev {
-    int last_row, last_n;
-    const double* hw;
-    double hb;
-};
 
 #ifndef AM_NST
 #define AM_NST 3
@@ -255,6 +252,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
     const bool sc_input_lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && (st.flags & AM_STEP_SC_FROM_INPUT);
     const bool sc_input_id = sc_ident && (st.flags & AM_STEP_SC_FROM_INPUT);
     const bool has_sc = (st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR)) != 0;
+    const bool has_vb = st.vb || st.vb_shape;
     {
         if (C == 1 && tid < BN) { S.bits[tid][0] = 0; S.bits[tid][1] = 0; }
         // state words of the tile's items covering both K segments (no global reads in issue())
@@ -404,6 +402,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                         const int64_t item = col >> 2;
                         const int comp = (int)(col & 3);  // 0 (even t) or 2 (odd t)
                         const bool ok = rok && item < n;
+                        const int shp = (ok && L.shape_w >= 0) ? item_shape(keys + item * L.KW, L.shape_w) : 0;
                         if (ok && has_sc) {
                             double s0 = 0.0, s1 = 0.0;
                             if (sc_input_id) {            // A_in = I, c_in = 0 (block starts at x)
@@ -412,7 +411,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                             } else if (sc_input_lin) {    // V @ I = V[:, :3], V @ 0 + vb
                                 const double* vr = st.V + (int64_t)r * st.ldv;
                                 s0 = vr[comp];
-                                s1 = comp == 0 ? vr[1] : (st.vb ? st.vb[r] : 0.0);
+                                s1 = comp == 0 ? vr[1] : (has_vb ? step_vbias(st, shp, r) : 0.0);
                             } else if (sc_ident) {        // masked block input rows
                                 const uint64_t* key = keys + item * L.KW;
                                 int srow = st.sin_row_off + r;
@@ -421,12 +420,12 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                                     s0 = p.x; s1 = p.y;
                                 }
                             } else {                      // V @ A_in is in acc (second K segment); add vb
-                                s1 = (comp == 2 && st.vb) ? st.vb[r] : 0.0;
+                                s1 = (comp == 2 && has_vb) ? step_vbias(st, shp, r) : 0.0;
                             }
                             v0 = s0 + v0;   // pre_A = sA + W A ; pre_c = (sc + W c) + b
                             v1 = s1 + v1;
                         }
-                        if (comp == 2) v1 = v1 + (ok ? st.b[r] : 0.0);
+                        if (comp == 2) v1 = v1 + (ok ? step_bias(st, shp, r) : 0.0);
                         // canonical bit: the pair (t, t^1) holds the 4 components of (item, row)
                         double p0 = __shfl_xor_sync(0xffffffffu, v0, 1);
                         double p1 = __shfl_xor_sync(0xffffffffu, v1, 1);
@@ -450,6 +449,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                             const int64_t item = col + e;
                             double v = e ? v1 : v0;
                             if (!(rok && item < n)) continue;
+                            const int shp = L.shape_w >= 0 ? item_shape(keys + item * L.KW, L.shape_w) : 0;
                             double pre;
                             if (has_sc) {
                                 double sc = 0.0;
@@ -459,16 +459,16 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                                 } else if (sc_input_lin) {
                                     const double* vr = st.V + (int64_t)r * st.ldv;
                                     sc = (x[0] * vr[0] + x[1] * vr[1]) + x[2] * vr[2];
-                                    if (st.vb) sc = sc + st.vb[r];
+                                    if (has_vb) sc = sc + step_vbias(st, shp, r);
                                 } else if (sc_ident) {
                                     int srow = st.sin_row_off + r;
                                     if (key_bit(keys + item * L.KW, srow)) sc = L.Z[item * L.zs + srow];
-                                } else if (st.vb) {
-                                    sc = st.vb[r];  // V h_in is in acc (second K segment)
+                                } else if (has_vb) {
+                                    sc = step_vbias(st, shp, r);  // V h_in is in acc (second K segment)
                                 }
-                                pre = (sc + v) + st.b[r];   // reference: shortcut(h_in) + h W^T + b
+                                pre = (sc + v) + step_bias(st, shp, r);   // reference: shortcut(h_in) + h W^T + b
                             } else {
-                                pre = v + st.b[r];
+                                pre = v + step_bias(st, shp, r);
                             }
                             L.Z[item * L.zs + row] = pre;
                             if (pre > 0.0) {
@@ -554,7 +554,7 @@ void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const
 // face functional of every subnetwork: head_w @ (s ⊙ Z_last) (+ head_b on the offset)
 // reference network.py:440-442
 __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
-                            int64_t n_cap, int zs, int KW, const SubDev* subs, int n_subs) {
+                            int64_t n_cap, int zs, int KW, const SubDev* subs, int n_subs, int shape_w) {
     pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     const int lane = threadIdx.x & 31;
@@ -582,7 +582,7 @@ __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces
         }
         if (lane == 0) {
             double* f = faces + (item * n_subs + j) * 4;
-            f[0] = a0; f[1] = a1; f[2] = a2; f[3] = a3 + sd.hb;
+            f[0] = a0; f[1] = a1; f[2] = a2; f[3] = a3 + head_bias(sd, item_shape(key, shape_w));
         }
     }
 }
@@ -590,7 +590,7 @@ __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces
 // F_j(x) = head_w @ relu(Z_last) + head_b; F = max_j (argmax lowest index) -- reference network.py:352-392
 __global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsigned long long* key_off, double* vals,
                                const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const SubDev* subs,
-                               int n_subs, int ensemble) {
+                               int n_subs, int ensemble, int shape_w) {
     pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     uint64_t* keys = key_off ? keys_base + (int64_t)(*key_off) * KW : keys_base;
@@ -609,7 +609,7 @@ __global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsig
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-            double f = a + sd.hb;
+            double f = a + head_bias(sd, item_shape(key, shape_w));
             if (j == 0 || f > best) { best = f; arg = j; }
         }
         if (lane == 0) {
@@ -620,20 +620,20 @@ __global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsig
 }
 
 void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
-                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, cudaStream_t s) {
+                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, int shape_w, cudaStream_t s) {
     int64_t warps = n_cap * n_subs;
     if (warps <= 0) return;
     int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)num_sms() * 8);
     { launch_k(k_face_head, (unsigned)blocks, 256, 0, s, Z, keys, faces, n_dev, n_cap, zs, KW,
-                                                 static_cast<const SubDev*>(subs), n_subs); }
+                                                 static_cast<const SubDev*>(subs), n_subs, shape_w); }
 }
 void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
                              const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,
-                             int n_subs, int ensemble, cudaStream_t s) {
+                             int n_subs, int ensemble, int shape_w, cudaStream_t s) {
     if (n_cap <= 0) return;
     int64_t blocks = std::min<int64_t>((n_cap * 32 + 255) / 256, (int64_t)num_sms() * 8);
     { launch_k(k_forward_head, (unsigned)blocks, 256, 0, s, Z, keys, key_off, vals, n_dev, n_cap, zs, KW,
-                                                    static_cast<const SubDev*>(subs), n_subs, ensemble); }
+                                                    static_cast<const SubDev*>(subs), n_subs, ensemble, shape_w); }
 }
 
 }  // namespace am

@@ -41,11 +41,6 @@ void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* o
 void launch_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
                          unsigned long long* cnt, cudaStream_t s);
 
-struct SubDev {
-    int last_row, last_n;
-    const double* hw;
-    double hb;
-};
 }  // namespace am
 
 using namespace am;
@@ -117,6 +112,11 @@ struct am_engine {
     std::vector<CUtensorMap> tmW, tmV;
     std::vector<int> tmV_ok;
     DBuf<double> params, wpad;
+    int n_shapes = 1, shape_w = -1, cur_shape = 0;   // batch of shapes (am_engine_set_shape_params)
+    DBuf<double> shape_tab;                          // per-shape bias tables
+    std::vector<int64_t> shp_idx;                    // overridden parameter entries ...
+    std::vector<double> shp_val;                     // ... and their per-shape values [S][n_idx]
+    DBuf<int32_t> probe_shape, prec_s, pend_s[2];    // shapes of probe points / records (batches)
     int64_t n_params = 0;
     std::vector<int64_t> woff, voff;   // padded weight layout (wpad_layout)
     DBuf<uint8_t> subdev;
@@ -265,6 +265,7 @@ static int ensure_results(am_engine* e, int64_t cells) {
         CK(e->pend_t[q].reserve(pcap, s, true, keep, &moved));
         CK(e->pend_k[q].reserve(pcap, s, true, keep, &moved));
         CK(e->pend_pt[q].reserve(pcap * 3, s, true, keep * 3, &moved));
+        if (e->shape_w >= 0) CK(e->pend_s[q].reserve(pcap, s, true, keep, &moved));
     }
     if (e->P.world > 1) {
         int64_t no = (int64_t)e->hctr[C_NOUT];
@@ -291,6 +292,64 @@ static int64_t wpad_layout(am_engine* e, std::vector<int64_t>& woff, std::vector
     return tot;
 }
 
+// per-shape bias tables of a batch of shapes: every overridden parameter must be a layer bias,
+// a shortcut bias or a head bias; each affected vector gets a [n_shapes][n] table holding the
+// base values with the shape's overrides applied
+static int build_shape_tables(am_engine* e, const double* h_params, std::vector<const double*>* hb_shape) {
+    const int ns = (int)(e->steps.size() / AM_STEP_FIELDS), S = e->n_shapes;
+    const int64_t n_idx = (int64_t)e->shp_idx.size();
+    for (int st = 0; st < ns; st++) { e->sdev[st].b_shape = nullptr; e->sdev[st].vb_shape = nullptr; }
+    hb_shape->assign(e->M, nullptr);
+    if (n_idx == 0) return AM_OK;
+    // (vector kind, owner, offset of the vector in params, length) for each overridden entry
+    struct Vec { int kind, owner; int64_t base, len, tab; };
+    std::vector<Vec> vecs;
+    std::vector<int> vec_of(n_idx, -1), pos_of(n_idx, 0);
+    for (int64_t j = 0; j < n_idx; j++) {
+        const int64_t ix = e->shp_idx[j];
+        int kind = -1, owner = -1;
+        int64_t base = 0, len = 0;
+        for (int st = 0; st < ns && kind < 0; st++) {
+            const int64_t* d = &e->steps[(size_t)st * AM_STEP_FIELDS];
+            if (ix >= d[3] && ix < d[3] + d[1]) { kind = 0; owner = st; base = d[3]; len = d[1]; }
+            else if (d[6] >= 0 && ix >= d[6] && ix < d[6] + d[1]) { kind = 1; owner = st; base = d[6]; len = d[1]; }
+        }
+        for (int sb = 0; sb < e->M && kind < 0; sb++)
+            if (ix == e->subs[(size_t)sb * AM_SUB_FIELDS + 3]) { kind = 2; owner = sb; base = ix; len = 1; }
+        if (kind < 0)
+            return fail(AM_ERR_ARG, "shape parameter %lld is not a bias: shapes of a batch must share every weight",
+                        (long long)ix);
+        int v = -1;
+        for (size_t q = 0; q < vecs.size(); q++)
+            if (vecs[q].kind == kind && vecs[q].owner == owner) v = (int)q;
+        if (v < 0) { vecs.push_back({kind, owner, base, len, 0}); v = (int)vecs.size() - 1; }
+        vec_of[j] = v;
+        pos_of[j] = (int)(ix - base);
+    }
+    int64_t tot = 0;
+    for (auto& v : vecs) { v.tab = tot; tot += (int64_t)S * v.len; }
+    std::vector<double> h(tot);
+    for (auto& v : vecs)
+        for (int sh = 0; sh < S; sh++)
+            memcpy(&h[v.tab + (int64_t)sh * v.len], h_params + v.base, (size_t)v.len * sizeof(double));
+    for (int sh = 0; sh < S; sh++)
+        for (int64_t j = 0; j < n_idx; j++) {
+            const Vec& v = vecs[vec_of[j]];
+            h[v.tab + (int64_t)sh * v.len + pos_of[j]] = e->shp_val[(size_t)sh * n_idx + j];
+        }
+    CK(e->shape_tab.reserve(std::max<int64_t>(tot, 1), e->stream));
+    CK(cudaMemcpyAsync(e->shape_tab.p, h.data(), (size_t)tot * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (auto& v : vecs) {
+        const double* p = e->shape_tab.p + v.tab;
+        if (v.kind == 0) e->sdev[v.owner].b_shape = p;
+        else if (v.kind == 1) e->sdev[v.owner].vb_shape = p;
+        else (*hb_shape)[v.owner] = p;
+    }
+    e->graph_valid = false;   // captured launches carry the table pointers
+    return AM_OK;
+}
+
 // network parameters -> device: the flat parameter buffer, the padded per-step weight copies
 // the TMA descriptors point at, and the per-subnetwork head table (head bias by value)
 static int upload_params(am_engine* e, const double* h_params) {
@@ -311,6 +370,8 @@ static int upload_params(am_engine* e, const double* h_params) {
         }
     }
     CK(cudaMemcpyAsync(e->wpad.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    std::vector<const double*> hb_shape;
+    RC(build_shape_tables(e, h_params, &hb_shape));
     std::vector<SubDev> hsub(e->M);
     for (int j = 0; j < e->M; j++) {
         const int64_t* sb = &e->subs[(size_t)j * AM_SUB_FIELDS];
@@ -320,6 +381,7 @@ static int upload_params(am_engine* e, const double* h_params) {
         hsub[j].last_n = (int)st[1];
         hsub[j].hw = e->params.p + sb[2];
         hsub[j].hb = h_params[sb[3]];
+        hsub[j].hb_shape = hb_shape[j];
     }
     CK(cudaMemcpyAsync(e->subdev.p, hsub.data(), sizeof(SubDev) * e->M, cudaMemcpyHostToDevice, e->stream));
     CK(cudaStreamSynchronize(e->stream));   // host staging vectors go out of scope
@@ -352,7 +414,10 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     e->NB = net->n_bits;
     e->M = net->n_subs;
     e->ensemble = net->ensemble;
-    e->KW = (e->NB + 63) / 64 + (e->ensemble ? 1 : 0);
+    e->n_shapes = e->P.n_shapes > 1 ? e->P.n_shapes : 1;
+    if (e->n_shapes > 1 && e->ensemble) return fail(AM_ERR_ARG, "a batch of shapes of max-pool ensembles is not supported");
+    e->KW = (e->NB + 63) / 64 + (e->ensemble ? 1 : 0) + (e->n_shapes > 1 ? 1 : 0);
+    e->shape_w = e->n_shapes > 1 ? e->KW - 1 : -1;
     e->zs = e->NB;
     e->steps.assign(net->h_steps, net->h_steps + (size_t)net->n_steps * AM_STEP_FIELDS);
     e->subs.assign(net->h_subs, net->h_subs + (size_t)net->n_subs * AM_SUB_FIELDS);
@@ -429,6 +494,10 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->prec_cand.reserve(e->PR, s));
     CK(e->prec_k.reserve(e->PR, s));
     CK(e->prec_pt.reserve(e->PR * 3, s));
+    if (e->shape_w >= 0) {
+        CK(e->prec_s.reserve(e->PR, s));
+        CK(e->probe_shape.reserve(e->PB, s));
+    }
     CK(e->outbox.reserve(e->KW, s));
     CK(e->ctr.reserve(C_N, s));
     CK(cudaMemsetAsync(e->ctr.p, 0, C_N * sizeof(unsigned long long), e->stream));
@@ -450,7 +519,7 @@ extern "C" int am_engine_destroy(am_engine* e) {
     if (e->graph) cudaGraphDestroy(e->graph);
     DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx,
                            &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1], &e->pool_hint,
-                           &e->ckey_hint, &e->emit_hint, &e->s_verts};
+                           &e->ckey_hint, &e->emit_hint, &e->s_verts, &e->shape_tab};
     for (auto* b : dbl) b->release(e->stream);
     DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->ckey, &e->slot, &e->slot2, &e->scratch, &e->outbox,
                              &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres, &e->pkeys, &e->pslot, &e->s_keys};
@@ -460,6 +529,7 @@ extern "C" int am_engine_destroy(am_engine* e) {
                             &e->cell_nv, &e->edge_nrefs, &e->edge_refs, &e->hstatus, &e->sact, &e->sdone,
                             &e->pool_vn, &e->pstatus, &e->emit_dup, &e->emit_pool, &e->prec_cand, &e->prec_k,
                             &e->pend_t[0], &e->pend_t[1], &e->pend_k[0], &e->pend_k[1], &e->val_buf, &e->s_nv,
+                            &e->probe_shape, &e->prec_s, &e->pend_s[0], &e->pend_s[1],
                             &e->s_enr, &e->s_refs};
     for (auto* b : i32) b->release(e->stream);
     e->pool_flags.release(e->stream);
@@ -487,6 +557,27 @@ extern "C" int am_engine_load_params(am_engine* e, const double* h_params, int64
                     (long long)e->n_params);
     CK(cudaStreamSynchronize(e->stream));
     return upload_params(e, h_params);
+}
+
+extern "C" int am_engine_set_shape_params(am_engine* e, const int64_t* h_param_idx, int64_t n_idx,
+                                          const double* h_values) {
+    if (!e || n_idx < 0 || (n_idx > 0 && (!h_param_idx || !h_values))) return fail(AM_ERR_ARG, "bad arguments");
+    if (e->n_shapes < 2) return fail(AM_ERR_ARG, "engine was created for a single shape (n_shapes < 2)");
+    for (int64_t j = 0; j < n_idx; j++)
+        if (h_param_idx[j] < 0 || h_param_idx[j] >= e->n_params) return fail(AM_ERR_ARG, "parameter index out of range");
+    e->shp_idx.assign(h_param_idx, h_param_idx + n_idx);
+    e->shp_val.assign(h_values, h_values + (size_t)n_idx * e->n_shapes);
+    std::vector<double> hp((size_t)e->n_params);
+    CK(cudaMemcpyAsync(hp.data(), e->params.p, (size_t)e->n_params * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return upload_params(e, hp.data());
+}
+
+extern "C" int am_engine_set_shape(am_engine* e, int32_t shape) {
+    if (!e) return fail(AM_ERR_ARG, "null engine");
+    if (shape < 0 || shape >= e->n_shapes) return fail(AM_ERR_ARG, "shape %d out of range [0, %d)", shape, e->n_shapes);
+    e->cur_shape = shape;
+    return AM_OK;
 }
 
 extern "C" int am_engine_reset(am_engine* e) {
@@ -518,6 +609,7 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsig
         L.KW = e->KW;
         L.zs = e->zs;
         L.grid_cap = e->grid_cap;
+        L.shape_w = e->shape_w;
         if (L.st.flags & AM_STEP_FIRST) launch_input_step(L, C, e->stream);
         else launch_gemm_step(L, C, &e->tmW[s], e->tmV_ok[s] ? &e->tmV[s] : nullptr, e->stream);
     }
@@ -528,7 +620,7 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsig
 static int compose(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, double* faces,
                    const unsigned long long* n_dev, int64_t n_cap) {
     RC(run_steps(e, 4, Z, keys, nullptr, changed, nullptr, n_dev, n_cap));
-    launch_face_head_dev(Z, keys, faces, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->stream);
+    launch_face_head_dev(Z, keys, faces, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->shape_w, e->stream);
     CK(cudaGetLastError());
     return AM_OK;
 }
@@ -537,16 +629,20 @@ static int forward(am_engine* e, const double* pts, double* vals, uint64_t* keys
                    double* Zw, const unsigned long long* n_dev, int64_t n_cap) {
     RC(run_steps(e, 1, Zw, keys, key_off, nullptr, pts, n_dev, n_cap));
     launch_forward_head_dev(Zw, keys, key_off, vals, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->ensemble,
+                            e->shape_w,
                             e->stream);
     CK(cudaGetLastError());
     return AM_OK;
 }
 
 // host-sized forward in chunks of the probe workspace
-static int forward_host(am_engine* e, const double* pts, int64_t n, double* vals, uint64_t* keys) {
+// shapes: per-point shape of a batch-of-shapes engine (device, may be null: the current shape)
+static int forward_host(am_engine* e, const double* pts, int64_t n, double* vals, uint64_t* keys,
+                        const int32_t* shapes = nullptr) {
     for (int64_t o = 0; o < n; o += e->PB) {
         int64_t m = std::min<int64_t>(e->PB, n - o);
-        CK(cudaMemsetAsync(keys + o * e->KW, 0, (size_t)m * e->KW * 8, e->stream));
+        launch_zero_keys(keys + o * e->KW, nullptr, e->KW, m, e->shape_w, shapes ? shapes + o : nullptr, e->cur_shape,
+                         e->stream);
         RC(forward(e, pts + o * 3, vals ? vals + o : nullptr, keys + o * e->KW, nullptr, e->pZ.p, nullptr, m));
     }
     return AM_OK;
@@ -562,7 +658,13 @@ static int join_caller(am_engine* e) {
     return AM_OK;
 }
 
+extern "C" int am_forward_shapes(am_engine* e, const double* d_pts, const int32_t* d_shapes, int64_t n,
+                                 double* d_vals, uint64_t* d_keys);
 extern "C" int am_forward(am_engine* e, const double* d_pts, int64_t n, double* d_vals, uint64_t* d_keys) {
+    return am_forward_shapes(e, d_pts, nullptr, n, d_vals, d_keys);
+}
+extern "C" int am_forward_shapes(am_engine* e, const double* d_pts, const int32_t* d_shapes, int64_t n,
+                                 double* d_vals, uint64_t* d_keys) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
     if (n == 0) return AM_OK;
     RC(join_caller(e));
@@ -571,7 +673,7 @@ extern "C" int am_forward(am_engine* e, const double* d_pts, int64_t n, double* 
         CK(e->hkeys.reserve(n * e->KW, e->stream));
         keys = e->hkeys.p;
     }
-    RC(forward_host(e, d_pts, n, d_vals, keys));
+    RC(forward_host(e, d_pts, n, d_vals, keys, d_shapes));
     CK(cudaStreamSynchronize(e->stream));
     return AM_OK;
 }
@@ -615,6 +717,9 @@ static int launch_iteration(am_engine* e) {
     ProbeRecs R;
     R.cand = e->prec_cand.p; R.k = e->prec_k.p; R.pt = e->prec_pt.p;
     for (int q = 0; q < 2; q++) { R.pend_t[q] = e->pend_t[q].p; R.pend_k[q] = e->pend_k[q].p; R.pend_pt[q] = e->pend_pt[q].p; }
+    const bool shapes = e->shape_w >= 0;
+    R.s = shapes ? e->prec_s.p : nullptr;
+    for (int q = 0; q < 2; q++) R.pend_s[q] = shapes ? e->pend_s[q].p : nullptr;
     R.cap_pend = e->pend_t[0].n;
     const bool multi = e->P.world > 1;
 
@@ -647,6 +752,7 @@ static int launch_iteration(am_engine* e) {
     a.probe_pts = e->probe_pts.p; a.n_probe = c + C_NPROBE; a.cap_probe = e->PB;
     a.overflow = c + C_OVF0;
     a.prec_cand = e->prec_cand.p; a.prec_k = e->prec_k.p; a.prec_pt = e->prec_pt.p; a.n_prec = c + C_NPREC;
+    a.prec_s = shapes ? e->prec_s.p : nullptr; a.shape_w = e->shape_w;
     a.cap_prec = e->PR;
     a.val_buf = e->val_buf.p; a.n_val = c + C_NVAL; a.cap_val = e->val_buf.n;
     a.pool_vn = e->pool_vn.p; a.pool_voff = e->pool_voff.p;
@@ -670,10 +776,10 @@ static int launch_iteration(am_engine* e) {
     }
     // probe records: target entries -> pending; pending with processed targets -> drop / forward
     launch_prec_target(R, e->status.p, e->emit_dup.p, e->emit_pool.p, c, e->PR, e->probe_pts.p, e->PB, s);
-    launch_resolve(R, H, e->val_buf.p, c, R.cap_pend, e->probe_pts.p, e->PB, s);
+    launch_resolve(R, H, e->val_buf.p, c, R.cap_pend, e->probe_pts.p, shapes ? e->probe_shape.p : nullptr, e->PB, s);
     launch_pend_finalize(c, s);
     // exact forward evaluation of the remaining probes
-    launch_zero_keys(e->pkeys.p, c + C_NPROBE, e->KW, e->PB, s);
+    launch_zero_keys(e->pkeys.p, c + C_NPROBE, e->KW, e->PB, e->shape_w, shapes ? e->probe_shape.p : nullptr, 0, s);
     e->grid_cap = 2;   // probes are rare after validation: a small persistent grid per layer
     int frc = forward(e, e->probe_pts.p, nullptr, e->pkeys.p, nullptr, e->pZ.p, c + C_NPROBE, e->PB);
     e->grid_cap = 0;
@@ -868,7 +974,9 @@ extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out, int64_t* h_counts) 
 
 // ------------------------------------------------------------------ seeding
 // reference marching.py:201-213 (_refine_seed_state), batched over seeds
-extern "C" int am_seed(am_engine* e, const double* d_pts, int64_t n) {
+extern "C" int am_seed_shapes(am_engine* e, const double* d_pts, const int32_t* d_shapes, int64_t n);
+extern "C" int am_seed(am_engine* e, const double* d_pts, int64_t n) { return am_seed_shapes(e, d_pts, nullptr, n); }
+extern "C" int am_seed_shapes(am_engine* e, const double* d_pts, const int32_t* d_shapes, int64_t n) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
     if (n == 0) return AM_OK;
     RC(join_caller(e));
@@ -883,7 +991,7 @@ extern "C" int am_seed(am_engine* e, const double* d_pts, int64_t n) {
     CK(e->sact.reserve(n, s));
     CK(e->sdone.reserve(n, s));
     CK(cudaMemcpyAsync(e->sx.p, d_pts, n * 24, cudaMemcpyDeviceToDevice, s));
-    RC(forward_host(e, e->sx.p, n, nullptr, e->ss.p));
+    RC(forward_host(e, e->sx.p, n, nullptr, e->ss.p, d_shapes));
     std::vector<int32_t> ones(n, 1);
     CK(cudaMemcpyAsync(e->sact.p, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
     for (int it = 0; it < 3; it++) {
@@ -893,7 +1001,7 @@ extern "C" int am_seed(am_engine* e, const double* d_pts, int64_t n) {
         launch_seed_project(e->sx.p, e->faces.p, e->ckey.p, KW, e->M, e->ensemble, n, e->sact.p, e->sxp.p,
                             e->sdone.p, s);
         launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, e->sdone.p, s);
-        RC(forward_host(e, e->sxp.p, n, nullptr, e->ssn.p));
+        RC(forward_host(e, e->sxp.p, n, nullptr, e->ssn.p, d_shapes));
         launch_seed_check(e->ssn.p, e->ckey.p, KW, n, e->sact.p, e->sx.p, e->sxp.p, e->ss.p, e->sres.p, nullptr, s);
         CK(cudaGetLastError());
     }
@@ -906,8 +1014,14 @@ extern "C" int am_seed(am_engine* e, const double* d_pts, int64_t n) {
 }
 
 // batched bisection between sign-opposite samples (reference seeding.py:84-112)
+extern "C" int am_dichotomy_shapes(am_engine* e, const double* d_xpos, const double* d_xneg, const int32_t* d_shapes,
+                                   int64_t n, double eps, double seed_tol, int max_iters, double* d_out);
 extern "C" int am_dichotomy(am_engine* e, const double* d_xpos, const double* d_xneg, int64_t n, double eps,
                             double seed_tol, int max_iters, double* d_out) {
+    return am_dichotomy_shapes(e, d_xpos, d_xneg, nullptr, n, eps, seed_tol, max_iters, d_out);
+}
+extern "C" int am_dichotomy_shapes(am_engine* e, const double* d_xpos, const double* d_xneg, const int32_t* d_shapes,
+                                   int64_t n, double eps, double seed_tol, int max_iters, double* d_out) {
     if (!e || n < 0) return fail(AM_ERR_ARG, "bad arguments");
     if (n == 0) return AM_OK;
     RC(join_caller(e));
@@ -920,13 +1034,13 @@ extern "C" int am_dichotomy(am_engine* e, const double* d_xpos, const double* d_
     CK(e->hkeys.reserve(n * e->KW, s));
     CK(cudaMemcpyAsync(xp.p, d_xpos, n * 24, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(xn.p, d_xneg, n * 24, cudaMemcpyDeviceToDevice, s));
-    RC(forward_host(e, xp.p, n, fp.p, e->hkeys.p));
-    RC(forward_host(e, xn.p, n, fn.p, e->hkeys.p));
+    RC(forward_host(e, xp.p, n, fp.p, e->hkeys.p, d_shapes));
+    RC(forward_host(e, xn.p, n, fn.p, e->hkeys.p, d_shapes));
     std::vector<int32_t> ones(n, 1);
     CK(cudaMemcpyAsync(act.p, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
     launch_midpoint(xp.p, xn.p, mid.p, n, s);
     for (int it = 1; it <= max_iters; it++) {
-        RC(forward_host(e, mid.p, n, vals.p, e->hkeys.p));
+        RC(forward_host(e, mid.p, n, vals.p, e->hkeys.p, d_shapes));
         launch_dichotomy_step(vals.p, xp.p, xn.p, fp.p, fn.p, mid.p, act.p, d_out, n, eps, seed_tol, it == max_iters, s);
         CK(cudaGetLastError());
         if ((it & 7) == 0 || it == max_iters) {
@@ -977,8 +1091,8 @@ static int result_assemble(am_engine* e, uint64_t* d_keys, int32_t* d_nverts, do
     CK(e->hkeys.reserve(nc * KW, e->stream));
     launch_gather_keys(e->pool.p, e->cell_pool.p, nc, KW, e->hkeys.p, e->stream);
     return assemble_results(e->hkeys.p, e->cell_nv.p, e->cell_voff.p, e->verts.p, e->edge_nrefs.p, e->edge_roff.p,
-                            e->edge_refs.p, nc, nvt, KW, e->stream, d_keys, d_nverts, d_verts, d_edge_nrefs,
-                            d_edge_refs);
+                            e->edge_refs.p, nc, nvt, KW, e->shape_w, e->stream, d_keys, d_nverts, d_verts,
+                            d_edge_nrefs, d_edge_refs);
 }
 
 extern "C" int am_result_copy_device(am_engine* e, uint64_t* d_keys, int32_t* d_nverts, double* d_verts,

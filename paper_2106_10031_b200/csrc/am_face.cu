@@ -961,6 +961,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
                 A.prec_pt[po * 3 + 2] = 0.5 * (p[2] + q[2]) + A.probe_delta * pn[2];
                 A.prec_k[po] = first;
                 A.prec_cand[po] = -1;
+                if (A.prec_s) A.prec_s[po] = item_shape(c.key, A.shape_w);
                 W->eprec[e] = (int)(po - (int64_t)r_prec);
                 po++;
             }

@@ -368,6 +368,7 @@ __global__ void k_prec_target(ProbeRecs R, const int32_t* status, const int32_t*
         R.pend_pt[par][j * 3 + 0] = R.pt[i * 3 + 0];
         R.pend_pt[par][j * 3 + 1] = R.pt[i * 3 + 1];
         R.pend_pt[par][j * 3 + 2] = R.pt[i * 3 + 2];
+        if (R.s) R.pend_s[par][j] = R.s[i];
     }
 }
 
@@ -375,7 +376,7 @@ __global__ void k_prec_target(ProbeRecs R, const int32_t* status, const int32_t*
 // mirrored probe of that neuron (the probe provably lands in the target cell), otherwise
 // forward-evaluated; targets still queued keep the record for a later iteration
 __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsigned long long* ctr, int64_t cap,
-                          double* probe_pts, int64_t cap_probe) {
+                          double* probe_pts, int32_t* probe_shape, int64_t cap_probe) {
     pdl_enter();
     const int64_t n = dev_count(ctr + C_NPEND, cap);
     const int par = (int)(ctr[C_PPAR] & 1ull);
@@ -403,6 +404,7 @@ __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsign
             if ((int64_t)q < cap_probe) {
                 probe_pts[q * 3 + 0] = R.pend_pt[par][i * 3 + 0]; probe_pts[q * 3 + 1] = R.pend_pt[par][i * 3 + 1];
                 probe_pts[q * 3 + 2] = R.pend_pt[par][i * 3 + 2];
+                if (R.s) probe_shape[q] = R.pend_s[par][i];
             } else {
                 keep = true;      // forward buffer full this iteration: retry next iteration
             }
@@ -414,6 +416,7 @@ __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsign
             R.pend_pt[par ^ 1][j * 3 + 0] = R.pend_pt[par][i * 3 + 0];
             R.pend_pt[par ^ 1][j * 3 + 1] = R.pend_pt[par][i * 3 + 1];
             R.pend_pt[par ^ 1][j * 3 + 2] = R.pend_pt[par][i * 3 + 2];
+            if (R.s) R.pend_s[par ^ 1][j] = R.pend_s[par][i];
         }
     }
 }
@@ -428,10 +431,18 @@ __global__ void k_pend_finalize(unsigned long long* ctr) {
     }
 }
 
-__global__ void k_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap) {
+__global__ void k_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, int shape_w,
+                            const int32_t* shapes, int value) {
     pdl_enter();
     const int64_t n = dev_count(n_dev, cap) * KW;
-    GRID_STRIDE(i, n) keys[i] = 0;
+    GRID_STRIDE(i, n) {
+        uint64_t v = 0;
+        if (shape_w >= 0) {
+            const int64_t item = i / KW;
+            if (i - item * KW == shape_w) v = (uint64_t)(shapes ? shapes[item] : value);
+        }
+        keys[i] = v;
+    }
 }
 
 void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t* dup_ref, const int32_t* pool_idx,
@@ -439,12 +450,13 @@ void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t
     launch_k(k_prec_target, grid_for(cap, 256),  256,  0,  s, R, status, dup_ref, pool_idx, ctr, cap, probe_pts, cap_probe);
 }
 void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr, int64_t cap,
-                    double* probe_pts, int64_t cap_probe, cudaStream_t s) {
-    launch_k(k_resolve, grid_for(cap, 256),  256,  0,  s, R, H, val_buf, ctr, cap, probe_pts, cap_probe);
+                    double* probe_pts, int32_t* probe_shape, int64_t cap_probe, cudaStream_t s) {
+    launch_k(k_resolve, grid_for(cap, 256),  256,  0,  s, R, H, val_buf, ctr, cap, probe_pts, probe_shape, cap_probe);
 }
 void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s) { launch_k(k_pend_finalize, 1, 32, 0, s, ctr); }
-void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, cudaStream_t s) {
-    launch_k(k_zero_keys, grid_for(cap * KW, 256),  256,  0,  s, keys, n_dev, KW, cap);
+void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, int shape_w,
+                      const int32_t* shapes, int value, cudaStream_t s) {
+    launch_k(k_zero_keys, grid_for(cap * KW, 256),  256,  0,  s, keys, n_dev, KW, cap, shape_w, shapes, value);
 }
 
 // owner rank of each key (outbox grouping)

@@ -85,7 +85,31 @@ struct StepDev {
     const double* V;   // padded copy, row stride ldv (or null)
     const double* vb;  // or null
     int ldw, ldv;
+    const double* b_shape;    // batch of shapes: per-shape bias [n_shapes][n_out] (null: b shared)
+    const double* vb_shape;   // per-shape shortcut bias [n_shapes][n_out] (null: vb shared)
 };
+
+// head of one subnetwork: F_j = hw . relu(z_last) + hb
+struct SubDev {
+    int last_row, last_n;
+    const double* hw;
+    double hb;
+    const double* hb_shape;   // batch of shapes: per-shape head bias [n_shapes] (null: hb shared)
+};
+
+// shape of an item (batch-of-shapes engines keep it in key word shape_w; -1: single shape)
+__device__ __forceinline__ int item_shape(const uint64_t* key, int shape_w) {
+    return shape_w < 0 ? 0 : (int)key[shape_w];
+}
+__device__ __forceinline__ double step_bias(const StepDev& st, int shape, int r) {
+    return st.b_shape ? st.b_shape[(int64_t)shape * st.n_out + r] : st.b[r];
+}
+__device__ __forceinline__ double head_bias(const SubDev& sd, int shape) {
+    return sd.hb_shape ? sd.hb_shape[shape] : sd.hb;
+}
+__device__ __forceinline__ double step_vbias(const StepDev& st, int shape, int r) {
+    return st.vb_shape ? st.vb_shape[(int64_t)shape * st.n_out + r] : (st.vb ? st.vb[r] : 0.0);
+}
 
 struct LayerLaunch {
     StepDev st;
@@ -98,6 +122,7 @@ struct LayerLaunch {
     int64_t n_cap;        // capacity / grid sizing
     int KW, zs;           // key words, Z row count per item (>= NB)
     int grid_cap;         // >0: persistent GEMM grid = grid_cap CTAs per SM
+    int shape_w;          // key word holding the item's shape (-1: single-shape engine)
 };
 
 __device__ __forceinline__ int64_t dev_count(const unsigned long long* p, int64_t cap) {
@@ -114,7 +139,7 @@ __device__ __forceinline__ uint64_t* keys_at(const LayerLaunch& L) {
 // result assembly (am_result.cu): sorted cell order + gathered CSR face loops
 int assemble_results(const uint64_t* keys, const int32_t* cell_nv, const int64_t* cell_voff, const double* verts,
                      const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nc, int64_t nvt, int KW,
-                     cudaStream_t s, uint64_t* s_keys, int32_t* s_nv, double* s_verts, int32_t* s_enr,
+                     int shape_w, cudaStream_t s, uint64_t* s_keys, int32_t* s_nv, double* s_verts, int32_t* s_enr,
                      int32_t* s_refs);
 
 // kernels' host-side launchers (am_compose.cu)
@@ -169,12 +194,14 @@ struct ProbeRecs {
     int32_t* pend_t[2];   // pending: target pool index
     int32_t* pend_k[2];
     double* pend_pt[2];
+    int32_t* s;           // batch of shapes: [cap] shape of the record (null: single shape)
+    int32_t* pend_s[2];
     int64_t cap_pend;
 };
 void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t* dup_ref, const int32_t* pool_idx,
                         unsigned long long* ctr, int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s);
 void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr,
-                    int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s);
+                    int64_t cap, double* probe_pts, int32_t* probe_shape, int64_t cap_probe, cudaStream_t s);
 void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s);
 void launch_take(const IterState& I, cudaStream_t s);
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
@@ -187,7 +214,9 @@ void launch_frontier(const unsigned long long* n_dev, int64_t n_cap, const int32
                      const int32_t* canon_pos, const int32_t* canon_status, const int32_t* canon_pool,
                      uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* ctr,
                      long long max_cells, cudaStream_t s);
-void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, cudaStream_t s);
+// zero n keys; with shape_w >= 0 word shape_w gets shapes[item] (or `value` when shapes is null)
+void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, int shape_w,
+                      const int32_t* shapes, int value, cudaStream_t s);
 void launch_zero_probe_keys(uint64_t* scratch, const unsigned long long* ctr, int KW, int64_t cap, cudaStream_t s);
 void launch_emit_finalize(unsigned long long* ctr, cudaStream_t s);
 void launch_route_emitted(const uint64_t* scratch, const unsigned long long* ctr_n, int64_t n_cap, int KW, int rank,
@@ -197,10 +226,10 @@ void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int 
 void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
                        unsigned long long* out, cudaStream_t s);
 void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
-                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, cudaStream_t s);
+                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, int shape_w, cudaStream_t s);
 void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
                              const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,
-                             int n_subs, int ensemble, cudaStream_t s);
+                             int n_subs, int ensemble, int shape_w, cudaStream_t s);
 
 // face extraction (am_face.cu)
 struct FaceArgs {
@@ -239,6 +268,8 @@ struct FaceArgs {
     int32_t* prec_cand;
     int32_t* prec_k;
     double* prec_pt;
+    int32_t* prec_s;          // batch of shapes: shape of the record's cell (null: single shape)
+    int shape_w;
     unsigned long long* n_prec;
     int64_t cap_prec;
     int32_t* val_buf;

@@ -84,7 +84,7 @@ struct Tmp {
 // s_verts [nvt*3], s_enr [nvt], s_refs [nref], all in sorted cell order.
 int assemble_results(const uint64_t* keys, const int32_t* cell_nv, const int64_t* cell_voff, const double* verts,
                      const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nc, int64_t nvt, int KW,
-                     cudaStream_t s, uint64_t* s_keys, int32_t* s_nv, double* s_verts, int32_t* s_enr,
+                     int shape_w, cudaStream_t s, uint64_t* s_keys, int32_t* s_nv, double* s_verts, int32_t* s_enr,
                      int32_t* s_refs) {
     if (nc <= 0) return AM_OK;
     if (nc >= ((int64_t)1 << 31)) return set_error(AM_ERR_ARG, "result assembly: more than 2^31 cells");
@@ -104,7 +104,10 @@ int assemble_results(const uint64_t* keys, const int32_t* cell_nv, const int64_t
     RCK(tmp.alloc((int64_t)tb));
     const unsigned G = blocks(nc);
     k_iota<<<G, 256, 0, s>>>(ord_a.p, nc);
-    for (int w = KW - 1; w >= 0; w--) {   // LSD: stable sort by each word, least significant first
+    // LSD: a stable sort by each word, least significant first; a batch of shapes is ordered by
+    // shape first (its shape word is the most significant), then like the reference
+    for (int q = KW - 1; q >= 0; q--) {
+        const int w = shape_w < 0 ? q : (q == 0 ? shape_w : q - 1 + (q - 1 >= shape_w ? 1 : 0));
         k_key_word<<<G, 256, 0, s>>>(keys, ord_a.p, nc, KW, w, w_a.p);
         size_t t = tb;
         RCK(cub::DeviceRadixSort::SortPairs(tmp.p, t, w_a.p, w_b.p, ord_a.p, ord_b.p, (int)nc, 0, 64, s));

@@ -60,8 +60,18 @@ class ShardedMarcher:
         self.engine = factory(net, bbox=bbox, max_cells=max_cells, rank=self.rank, world=self.world, **kw)
         self.waves = 0
 
+    def load_network(self, net: AnyNetwork):
+        """Next network of a same-architecture batch (weights re-uploaded, engine reused)."""
+        self.net = net
+        if hasattr(self.engine, "load_network"):
+            self.engine.load_network(net)
+        else:                                 # engines without a weight swap are rebuilt
+            self.engine = type(self.engine)(net, bbox=self.bbox, rank=self.rank, world=self.world)
+
     def sample_seeds(self, count: int, rng_seed: int = 0, scheme: str = "dichotomy") -> np.ndarray:
         """Same seeds on every rank (the trigger is deterministic given rng_seed)."""
+        if hasattr(self.engine, "sample_seeds"):   # CPU stand-in engines bring their own trigger
+            return self.engine.sample_seeds(count, self.bbox, scheme=scheme, rng_seed=rng_seed)
         return sample_seeds(self.engine, count, self.bbox, scheme=scheme, rng_seed=rng_seed)
 
     def run(self, seeds: np.ndarray, max_waves: int = 1_000_000) -> int:

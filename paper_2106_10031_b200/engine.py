@@ -35,7 +35,7 @@ class Engine:
     def __init__(self, net: AnyNetwork, bbox=((-1.2,) * 3, (1.2,) * 3), max_cells: int = 10_000_000,
                  tol_cell=TOL_CELL, tol_weld=TOL_WELD, tol_onplane=TOL_ONPLANE, probe_delta=PROBE_DELTA,
                  batch_cells: int = 0, mem_budget: int = 0, rank: int = 0, world: int = 1,
-                 device: int | None = None, stream: torch.cuda.Stream | None = None):
+                 device: int | None = None, stream: torch.cuda.Stream | None = None, n_shapes: int = 1):
         _require_cuda()
         self.lib = _native.load()
         self.device = torch.cuda.current_device() if device is None else device
@@ -56,6 +56,8 @@ class Engine:
         p.tol_cell, p.tol_weld, p.tol_onplane, p.probe_delta = tol_cell, tol_weld, tol_onplane, probe_delta
         p.max_cells, p.batch_cells, p.mem_budget = int(max_cells), int(batch_cells), int(mem_budget)
         p.rank, p.world = int(rank), int(world)
+        p.n_shapes = int(n_shapes)
+        self.n_shapes = max(1, int(n_shapes))
         self.params = p
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
@@ -81,15 +83,24 @@ class Engine:
         t = torch.as_tensor(np.ascontiguousarray(arr), device=self.dev)
         return t.to(dtype).contiguous()
 
-    def forward(self, pts, keys: bool = False):
-        """F(x) (and activation-state keys) at points; reference network.py:352-392."""
+    def _shapes(self, shapes, n):
+        if shapes is None:
+            return None
+        t = self._dev(np.broadcast_to(np.asarray(shapes, np.int32), (n,)), torch.int32)
+        return t
+
+    def forward(self, pts, keys: bool = False, shapes=None):
+        """F(x) (and activation-state keys) at points; reference network.py:352-392.  shapes:
+        per-point shape of a batch-of-shapes engine (default: the current shape)."""
         pts_t = pts if isinstance(pts, torch.Tensor) else self._dev(np.asarray(pts, np.float64).reshape(-1, 3),
                                                                    torch.float64)
         n = pts_t.shape[0]
         vals = torch.empty(n, dtype=torch.float64, device=self.dev)
         k = torch.empty((n, self.kw), dtype=torch.int64, device=self.dev) if keys else None
-        _native.check(self.lib.am_forward(self.h, pts_t.data_ptr(), n, vals.data_ptr(),
-                                          k.data_ptr() if k is not None else None), "am_forward")
+        sh = self._shapes(shapes, n)
+        _native.check(self.lib.am_forward_shapes(self.h, pts_t.data_ptr(), sh.data_ptr() if sh is not None else None,
+                                                 n, vals.data_ptr(), k.data_ptr() if k is not None else None),
+                      "am_forward")
         return (vals, k) if keys else vals
 
     def affine_maps(self, keys):
@@ -103,17 +114,48 @@ class Engine:
                                               faces.data_ptr()), "am_affine_maps")
         return canon, planes, faces
 
-    def dichotomy(self, xpos, xneg, eps, seed_tol, max_iters=200):
+    def dichotomy(self, xpos, xneg, eps, seed_tol, max_iters=200, shapes=None):
         a = self._dev(np.asarray(xpos, np.float64).reshape(-1, 3), torch.float64)
         b = self._dev(np.asarray(xneg, np.float64).reshape(-1, 3), torch.float64)
         out = torch.empty_like(a)
-        _native.check(self.lib.am_dichotomy(self.h, a.data_ptr(), b.data_ptr(), a.shape[0], eps, seed_tol,
-                                            max_iters, out.data_ptr()), "am_dichotomy")
+        sh = self._shapes(shapes, a.shape[0])
+        _native.check(self.lib.am_dichotomy_shapes(self.h, a.data_ptr(), b.data_ptr(),
+                                                   sh.data_ptr() if sh is not None else None, a.shape[0], eps,
+                                                   seed_tol, max_iters, out.data_ptr()), "am_dichotomy")
         return out
 
     # --------------------------------------------------------------- marching
     def reset(self):
         _native.check(self.lib.am_engine_reset(self.h), "am_engine_reset")
+
+    def set_shapes(self, nets):
+        """Batch of same-architecture shapes (engine created with n_shapes = len(nets)): shape s
+        marches nets[s].  Their parameters may differ only in bias vectors (checked by the
+        engine); nets[0] becomes the base parameter set."""
+        if len(nets) != self.n_shapes:
+            raise ValueError(f"engine holds {self.n_shapes} shapes, got {len(nets)} networks")
+        blobs = [to_blob(n) for n in nets]
+        self.load_network(nets[0], blobs[0])
+        base = np.asarray(blobs[0].params, dtype=np.float64)
+        diff = np.zeros(len(base), dtype=bool)
+        for b in blobs[1:]:
+            diff |= np.asarray(b.params, dtype=np.float64) != base
+        idx = np.flatnonzero(diff).astype(np.int64)
+        vals = np.ascontiguousarray(np.stack([np.asarray(b.params, dtype=np.float64)[idx] for b in blobs]))
+        _native.check(self.lib.am_engine_set_shape_params(self.h, idx.ctypes.data, len(idx), vals.ctypes.data),
+                      "am_engine_set_shape_params")
+        self.shape_nets = list(nets)
+
+    @property
+    def batch_size(self) -> int:
+        """Cells per BFS iteration (also the most seeds one am_seed call takes)."""
+        return int(self.stats()["batch"])
+
+    def set_shape(self, shape: int):
+        """Shape of the points of later forward / dichotomy / seed calls."""
+        _native.check(self.lib.am_engine_set_shape(self.h, int(shape)), "am_engine_set_shape")
+        if hasattr(self, "shape_nets"):
+            self.net = self.shape_nets[shape]
 
     def architecture(self) -> tuple:
         return architecture_key(self.blob)
@@ -128,10 +170,12 @@ class Engine:
                       "am_engine_load_params")
         self.net, self.blob, self._params = net, blob, params
 
-    def seed(self, pts):
+    def seed(self, pts, shapes=None):
         t = pts if isinstance(pts, torch.Tensor) else self._dev(np.asarray(pts, np.float64).reshape(-1, 3),
                                                                torch.float64)
-        _native.check(self.lib.am_seed(self.h, t.data_ptr(), t.shape[0]), "am_seed")
+        sh = self._shapes(shapes, t.shape[0])
+        _native.check(self.lib.am_seed_shapes(self.h, t.data_ptr(), sh.data_ptr() if sh is not None else None,
+                                              t.shape[0]), "am_seed")
 
     def push(self, keys: torch.Tensor):
         if keys.numel():

@@ -213,29 +213,49 @@ def refs_to_kind_index(ids: np.ndarray, n_bits: int, n_subs: int) -> np.ndarray:
     return out
 
 
-def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, threads: int = 1) -> MarchResult:
-    """Sorted results (GPU sort + gathers, am_result_copy_device), converted to the reference's
-    representations on the device (edge refs -> (kind, index)), one pinned copy per array."""
+def device_results_to_host(eng: Engine):
+    """Sorted device results in the reference's representations, converted on the GPU and copied
+    once into pinned host memory: (counts, packbits keys (C, nbytes) uint8, branch (C,), extra
+    key word (C,) or None, nverts, verts, edge_nrefs, edge_refs (R, 2) (kind, index))."""
     import torch
     c, keys, nverts, verts, enr, erefs = eng.results_device()
     b = eng.blob
     nb, ns = b.n_bits, b.n_subs
+    bw, nbytes = (nb + 63) // 64, (nb + 7) // 8
+    n = keys.shape[0]
+    # MSB-first words -> big-endian bytes == np.packbits of the state bits
+    kbytes = keys[:, :bw].contiguous().view(torch.uint8).view(n, bw, 8).flip(-1).reshape(n, bw * 8)[:, :nbytes]
     g1, g2 = erefs >= nb, erefs >= nb + ns
-    kind = g1.to(torch.int32) + g2.to(torch.int32)
-    index = erefs - nb * g1.to(torch.int32) - ns * g2.to(torch.int32)
-    refs = torch.stack([kind, index], dim=1)
+    refs = torch.stack([g1.to(torch.int32) + g2.to(torch.int32),
+                        erefs - nb * g1.to(torch.int32) - ns * g2.to(torch.int32)], dim=1)
+    branch = keys[:, bw] if b.ensemble else None
+    shape = keys[:, eng.kw - 1] if getattr(eng, "n_shapes", 1) > 1 else None
 
     def host(t):
+        # small arrays: pinned staging (fast async copy); large ones: pinning fresh memory costs
+        # more than the staged pageable copy (~0.5 s per GB), so copy straight to pageable memory
+        if t.numel() * t.element_size() > (64 << 20):
+            return t.cpu()
         out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         out.copy_(t, non_blocking=True)
         return out
-    hk, hn, hv, he, hr = (host(t) for t in (keys, nverts, verts, enr, refs))
+    arrs = [host(t.contiguous()) for t in (kbytes, nverts, verts, enr, refs)]
+    br = host(branch) if branch is not None else None
+    sh = host(shape) if shape is not None else None
     torch.cuda.current_stream(eng.dev).synchronize()
-    kb, branch = words_to_packbits(hk.numpy().view(np.uint64), nb, b.ensemble)
+    hk, hn, hv, he, hr = (a.numpy() for a in arrs)
+    hbr = br.numpy().astype(np.int64) if br is not None else np.full(n, -1, np.int64)
+    return c, hk, hbr, (sh.numpy() if sh is not None else None), hn, hv, he, hr
+
+
+def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, threads: int = 1) -> MarchResult:
+    """Sorted results (GPU sort + gathers, am_result_copy_device), converted to the reference's
+    representations on the device, one pinned copy per array."""
+    c, kb, branch, _, hn, hv, he, hr = device_results_to_host(eng)
     rep = MarchReport(cells_visited=c["cells"], faces_emitted=c["faces"], empty_faces=c["empty"],
                       open_edges=c["open_edges"], seconds=time.perf_counter() - t0, seeds_used=len(seeds),
                       capped=bool(c["capped"]), threads=threads, waves=waves, overflow=c["overflow"])
-    return MarchResult(kb, branch, hn.numpy(), hv.numpy(), he.numpy(), hr.numpy(), rep, nb, seeds)
+    return MarchResult(kb, branch, hn, hv, he, hr, rep, eng.blob.n_bits, seeds)
 
 
 _ENGINES: "OrderedDict[tuple, Engine]" = OrderedDict()

@@ -129,3 +129,55 @@ def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int
     if not seeds:
         raise SeedingError("no surface located in bbox")
     return np.array(seeds)
+
+
+def sample_seeds_batch(eng, nets, count: int, bbox, rng_seed: int = 0, eps: float = SEED_TOL,
+                       seed_tol: float = SEED_TOL, retry_budget: int = 200) -> list:
+    """sample_seeds (dichotomy trigger) of every shape of a batch-of-shapes engine at once.
+
+    Shape s's trigger is the reference's (seeding.py:123-162) on its own network: the sample
+    streams default_rng([rng_seed, index]) do not depend on the network, and a pending
+    (shape, index) pair draws its k-th block in retry round k exactly as the per-shape loop
+    would, so one forward evaluation per round and one bisection serve the whole batch."""
+    if count < 1:
+        raise ValueError("count must be >= 1")
+    for net in nets:
+        validate_scheme(net, "dichotomy")
+    S = len(nets)
+    lo = np.asarray(bbox[0], dtype=np.float64)
+    hi = np.asarray(bbox[1], dtype=np.float64)
+    rngs = [np.random.default_rng([rng_seed, index]) for index in range(count)]
+    blocks: list = [[] for _ in range(count)]      # k-th (64, 3) draw of stream i, shared by all shapes
+    pending = [(s, i) for s in range(S) for i in range(count)]
+    pairs: dict = {}
+    for k in range(retry_budget):
+        if not pending:
+            break
+        for _, i in pending:
+            while len(blocks[i]) <= k:
+                blocks[i].append(rngs[i].uniform(lo, hi, size=(64, 3)))
+        pts = np.stack([blocks[i][k] for _, i in pending])
+        shp = np.repeat(np.array([s for s, _ in pending], np.int32), 64)
+        vals = eng.forward(pts.reshape(-1, 3), shapes=shp).cpu().numpy().reshape(len(pending), 64)
+        still = []
+        for j, (s, i) in enumerate(pending):
+            pos = pts[j][vals[j] > 0.0]
+            neg = pts[j][vals[j] < 0.0]
+            if len(pos) and len(neg):
+                pairs[(s, i)] = (pos[0], neg[0])
+            else:
+                still.append((s, i))
+        pending = still
+    out = [np.zeros((0, 3)) for _ in range(S)]
+    if pairs:
+        order = sorted(pairs)
+        xp = np.stack([pairs[o][0] for o in order])
+        xn = np.stack([pairs[o][1] for o in order])
+        sh = np.array([o[0] for o in order], np.int32)
+        pts = eng.dichotomy(xp, xn, eps, seed_tol, shapes=sh).cpu().numpy()
+        for s in range(S):
+            out[s] = pts[sh == s]
+    for s in range(S):
+        if not len(out[s]):
+            raise SeedingError(f"no surface located in bbox (shape {s})")
+    return out
