@@ -70,7 +70,11 @@ typedef struct {
     int32_t rank, world;  /* state ownership: owner(state) = hash(state) % world */
     int32_t n_shapes;     /* > 1: batch of same-architecture shapes marched together (the key
                            * gains a trailing shape word; see am_engine_set_shape_params) */
-    int32_t reserved;
+    int32_t precision;    /* 0: fp64 (reference arithmetic); 1: fp32 mode -- weights and every
+                           * composed affine map / field value rounded to fp32 (products of fp32
+                           * operands are exact in the fp64 DMMA accumulation), faces solved from
+                           * those fp32-precision planes; pair with the looser tolerances of the
+                           * fp32-mode study */
 } am_march_params;
 
 typedef struct am_engine am_engine;

@@ -46,7 +46,7 @@ class MarchParams(ctypes.Structure):
         ("tol_onplane", ctypes.c_double), ("probe_delta", ctypes.c_double),
         ("max_cells", ctypes.c_int64), ("batch_cells", ctypes.c_int64),
         ("mem_budget", ctypes.c_int64), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-        ("n_shapes", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("n_shapes", ctypes.c_int32), ("precision", ctypes.c_int32),
     ]
 
 

@@ -56,12 +56,12 @@ def _fused_engine(nets, config: MarchConfig):
     import torch
     key = ("batch", len(nets), architecture_key(to_blob(nets[0])), tuple(map(tuple, config.bbox)),
            config.max_cells, config.tol_cell, config.tol_weld, config.probe_delta, config.batch_cells,
-           config.mem_budget, torch.cuda.current_device())
+           config.mem_budget, config.precision, torch.cuda.current_device())
     eng = _ENGINES.get(key)
     if eng is None:
         eng = Engine(nets[0], bbox=config.bbox, max_cells=config.max_cells * len(nets), tol_cell=config.tol_cell,
                      tol_weld=config.tol_weld, probe_delta=config.probe_delta, batch_cells=config.batch_cells,
-                     mem_budget=config.mem_budget, n_shapes=len(nets))
+                     mem_budget=config.mem_budget, n_shapes=len(nets), precision=config.precision)
         _ENGINES[key] = eng
         while len(_ENGINES) > ENGINE_CACHE_SIZE:
             _ENGINES.popitem(last=False)

@@ -120,6 +120,8 @@ __device__ __forceinline__ void input_elem(const LayerLaunch& L, uint64_t* keys,
         } else {
             c = c + step_bias(st, shp, r);
         }
+        a0 = prec_round(a0, L.fp32); a1 = prec_round(a1, L.fp32);
+        a2 = prec_round(a2, L.fp32); c = prec_round(c, L.fp32);
         double nrm = sqrt((a0 * a0 + a1 * a1) + a2 * a2);
         if (!(nrm > kDegen)) {
             int bit = c > 0.0;
@@ -147,6 +149,7 @@ __device__ __forceinline__ void input_elem(const LayerLaunch& L, uint64_t* keys,
         } else {
             pre = acc + step_bias(st, shp, r);
         }
+        pre = prec_round(pre, L.fp32);
         if (pre > 0.0) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)key_mask(row));
         z[0] = pre;
     }
@@ -426,6 +429,8 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                             v1 = s1 + v1;
                         }
                         if (comp == 2) v1 = v1 + (ok ? step_bias(st, shp, r) : 0.0);
+                        v0 = prec_round(v0, L.fp32);
+                        v1 = prec_round(v1, L.fp32);
                         // canonical bit: the pair (t, t^1) holds the 4 components of (item, row)
                         double p0 = __shfl_xor_sync(0xffffffffu, v0, 1);
                         double p1 = __shfl_xor_sync(0xffffffffu, v1, 1);
@@ -470,6 +475,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                             } else {
                                 pre = v + step_bias(st, shp, r);
                             }
+                            pre = prec_round(pre, L.fp32);
                             L.Z[item * L.zs + row] = pre;
                             if (pre > 0.0) {
                                 int lb = row - wbase * 64;
@@ -554,7 +560,7 @@ void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const
 // face functional of every subnetwork: head_w @ (s ⊙ Z_last) (+ head_b on the offset)
 // reference network.py:440-442
 __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
-                            int64_t n_cap, int zs, int KW, const SubDev* subs, int n_subs, int shape_w) {
+                            int64_t n_cap, int zs, int KW, const SubDev* subs, int n_subs, int shape_w, int fp32) {
     pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     const int lane = threadIdx.x & 31;
@@ -582,7 +588,8 @@ __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces
         }
         if (lane == 0) {
             double* f = faces + (item * n_subs + j) * 4;
-            f[0] = a0; f[1] = a1; f[2] = a2; f[3] = a3 + head_bias(sd, item_shape(key, shape_w));
+            f[0] = prec_round(a0, fp32); f[1] = prec_round(a1, fp32); f[2] = prec_round(a2, fp32);
+            f[3] = prec_round(a3 + head_bias(sd, item_shape(key, shape_w)), fp32);
         }
     }
 }
@@ -590,7 +597,7 @@ __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces
 // F_j(x) = head_w @ relu(Z_last) + head_b; F = max_j (argmax lowest index) -- reference network.py:352-392
 __global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsigned long long* key_off, double* vals,
                                const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const SubDev* subs,
-                               int n_subs, int ensemble, int shape_w) {
+                               int n_subs, int ensemble, int shape_w, int fp32) {
     pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     uint64_t* keys = key_off ? keys_base + (int64_t)(*key_off) * KW : keys_base;
@@ -609,7 +616,7 @@ __global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsig
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-            double f = a + head_bias(sd, item_shape(key, shape_w));
+            double f = prec_round(a + head_bias(sd, item_shape(key, shape_w)), fp32);
             if (j == 0 || f > best) { best = f; arg = j; }
         }
         if (lane == 0) {
@@ -620,20 +627,21 @@ __global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsig
 }
 
 void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
-                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, int shape_w, cudaStream_t s) {
+                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, int shape_w, int fp32,
+                          cudaStream_t s) {
     int64_t warps = n_cap * n_subs;
     if (warps <= 0) return;
     int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)num_sms() * 8);
     { launch_k(k_face_head, (unsigned)blocks, 256, 0, s, Z, keys, faces, n_dev, n_cap, zs, KW,
-                                                 static_cast<const SubDev*>(subs), n_subs, shape_w); }
+                                                 static_cast<const SubDev*>(subs), n_subs, shape_w, fp32); }
 }
 void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
                              const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,
-                             int n_subs, int ensemble, int shape_w, cudaStream_t s) {
+                             int n_subs, int ensemble, int shape_w, int fp32, cudaStream_t s) {
     if (n_cap <= 0) return;
     int64_t blocks = std::min<int64_t>((n_cap * 32 + 255) / 256, (int64_t)num_sms() * 8);
     { launch_k(k_forward_head, (unsigned)blocks, 256, 0, s, Z, keys, key_off, vals, n_dev, n_cap, zs, KW,
-                                                    static_cast<const SubDev*>(subs), n_subs, ensemble, shape_w); }
+                                                    static_cast<const SubDev*>(subs), n_subs, ensemble, shape_w, fp32); }
 }
 
 }  // namespace am

@@ -113,6 +113,7 @@ struct am_engine {
     std::vector<int> tmV_ok;
     DBuf<double> params, wpad;
     int n_shapes = 1, shape_w = -1, cur_shape = 0;   // batch of shapes (am_engine_set_shape_params)
+    int fp32 = 0;                                    // fp32 mode (am_march_params.precision)
     DBuf<double> shape_tab;                          // per-shape bias tables
     std::vector<int64_t> shp_idx;                    // overridden parameter entries ...
     std::vector<double> shp_val;                     // ... and their per-shape values [S][n_idx]
@@ -335,7 +336,8 @@ static int build_shape_tables(am_engine* e, const double* h_params, std::vector<
     for (int sh = 0; sh < S; sh++)
         for (int64_t j = 0; j < n_idx; j++) {
             const Vec& v = vecs[vec_of[j]];
-            h[v.tab + (int64_t)sh * v.len + pos_of[j]] = e->shp_val[(size_t)sh * n_idx + j];
+            h[v.tab + (int64_t)sh * v.len + pos_of[j]] =
+                e->fp32 ? (double)(float)e->shp_val[(size_t)sh * n_idx + j] : e->shp_val[(size_t)sh * n_idx + j];
         }
     CK(e->shape_tab.reserve(std::max<int64_t>(tot, 1), e->stream));
     CK(cudaMemcpyAsync(e->shape_tab.p, h.data(), (size_t)tot * sizeof(double), cudaMemcpyHostToDevice, e->stream));
@@ -352,8 +354,15 @@ static int build_shape_tables(am_engine* e, const double* h_params, std::vector<
 
 // network parameters -> device: the flat parameter buffer, the padded per-step weight copies
 // the TMA descriptors point at, and the per-subnetwork head table (head bias by value)
-static int upload_params(am_engine* e, const double* h_params) {
+static int upload_params(am_engine* e, const double* h_params_in) {
     const int ns = (int)(e->steps.size() / AM_STEP_FIELDS);
+    std::vector<double> rounded;          // fp32 mode: the network at fp32 precision
+    const double* h_params = h_params_in;
+    if (e->fp32) {
+        rounded.assign(h_params_in, h_params_in + e->n_params);
+        for (double& v : rounded) v = (double)(float)v;
+        h_params = rounded.data();
+    }
     CK(cudaMemcpyAsync(e->params.p, h_params, (size_t)e->n_params * sizeof(double), cudaMemcpyHostToDevice,
                        e->stream));
     auto pad = [](int64_t x) { return (x + 15) / 16 * 16; };
@@ -415,6 +424,8 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     e->M = net->n_subs;
     e->ensemble = net->ensemble;
     e->n_shapes = e->P.n_shapes > 1 ? e->P.n_shapes : 1;
+    if (e->P.precision != 0 && e->P.precision != 1) return fail(AM_ERR_ARG, "precision must be 0 (fp64) or 1 (fp32)");
+    e->fp32 = e->P.precision;
     if (e->n_shapes > 1 && e->ensemble) return fail(AM_ERR_ARG, "a batch of shapes of max-pool ensembles is not supported");
     e->KW = (e->NB + 63) / 64 + (e->ensemble ? 1 : 0) + (e->n_shapes > 1 ? 1 : 0);
     e->shape_w = e->n_shapes > 1 ? e->KW - 1 : -1;
@@ -610,6 +621,7 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsig
         L.zs = e->zs;
         L.grid_cap = e->grid_cap;
         L.shape_w = e->shape_w;
+        L.fp32 = e->fp32;
         if (L.st.flags & AM_STEP_FIRST) launch_input_step(L, C, e->stream);
         else launch_gemm_step(L, C, &e->tmW[s], e->tmV_ok[s] ? &e->tmV[s] : nullptr, e->stream);
     }
@@ -620,7 +632,7 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsig
 static int compose(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, double* faces,
                    const unsigned long long* n_dev, int64_t n_cap) {
     RC(run_steps(e, 4, Z, keys, nullptr, changed, nullptr, n_dev, n_cap));
-    launch_face_head_dev(Z, keys, faces, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->shape_w, e->stream);
+    launch_face_head_dev(Z, keys, faces, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->shape_w, e->fp32, e->stream);
     CK(cudaGetLastError());
     return AM_OK;
 }
@@ -629,7 +641,7 @@ static int forward(am_engine* e, const double* pts, double* vals, uint64_t* keys
                    double* Zw, const unsigned long long* n_dev, int64_t n_cap) {
     RC(run_steps(e, 1, Zw, keys, key_off, nullptr, pts, n_dev, n_cap));
     launch_forward_head_dev(Zw, keys, key_off, vals, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->ensemble,
-                            e->shape_w,
+                            e->shape_w, e->fp32,
                             e->stream);
     CK(cudaGetLastError());
     return AM_OK;

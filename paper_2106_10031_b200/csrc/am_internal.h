@@ -123,7 +123,11 @@ struct LayerLaunch {
     int KW, zs;           // key words, Z row count per item (>= NB)
     int grid_cap;         // >0: persistent GEMM grid = grid_cap CTAs per SM
     int shape_w;          // key word holding the item's shape (-1: single-shape engine)
+    int fp32;             // fp32 mode: round every composed value to fp32
 };
+
+// fp32 mode: values kept at fp32 precision (round-to-nearest), fp64 otherwise
+__device__ __forceinline__ double prec_round(double v, int fp32) { return fp32 ? (double)__double2float_rn(v) : v; }
 
 __device__ __forceinline__ int64_t dev_count(const unsigned long long* p, int64_t cap) {
     if (!p) return cap;
@@ -226,10 +230,11 @@ void launch_gather_keys(const uint64_t* src, const int32_t* idx, int64_t n, int 
 void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* refs, int64_t nv, int box0,
                        unsigned long long* out, cudaStream_t s);
 void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
-                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, int shape_w, cudaStream_t s);
+                          int64_t n_cap, int zs, int KW, const void* subs, int n_subs, int shape_w, int fp32,
+                          cudaStream_t s);
 void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
                              const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,
-                             int n_subs, int ensemble, int shape_w, cudaStream_t s);
+                             int n_subs, int ensemble, int shape_w, int fp32, cudaStream_t s);
 
 // face extraction (am_face.cu)
 struct FaceArgs {

@@ -35,7 +35,8 @@ class Engine:
     def __init__(self, net: AnyNetwork, bbox=((-1.2,) * 3, (1.2,) * 3), max_cells: int = 10_000_000,
                  tol_cell=TOL_CELL, tol_weld=TOL_WELD, tol_onplane=TOL_ONPLANE, probe_delta=PROBE_DELTA,
                  batch_cells: int = 0, mem_budget: int = 0, rank: int = 0, world: int = 1,
-                 device: int | None = None, stream: torch.cuda.Stream | None = None, n_shapes: int = 1):
+                 device: int | None = None, stream: torch.cuda.Stream | None = None, n_shapes: int = 1,
+                 precision: str = "fp64"):
         _require_cuda()
         self.lib = _native.load()
         self.device = torch.cuda.current_device() if device is None else device
@@ -57,6 +58,10 @@ class Engine:
         p.max_cells, p.batch_cells, p.mem_budget = int(max_cells), int(batch_cells), int(mem_budget)
         p.rank, p.world = int(rank), int(world)
         p.n_shapes = int(n_shapes)
+        if precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
+        p.precision = 1 if precision == "fp32" else 0
+        self.precision = precision
         self.n_shapes = max(1, int(n_shapes))
         self.params = p
         h = ctypes.c_void_p()

@@ -82,8 +82,11 @@ class MarchConfig:
     probe_delta: float = PROBE_DELTA
     batch_cells: int = 0        # GPU: cells composed per batch (0 = from memory budget)
     mem_budget: int = 0         # GPU: bytes for per-batch plane buffers (0 = 2 GiB)
+    precision: str = "fp64"     # "fp32": fp32-precision planes (pair with FP32_TOLERANCES)
 
     def __post_init__(self):
+        if self.precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
         if self.max_cells < 1:
             raise ValueError("max_cells must be >= 1")
         if self.threads < 1:
@@ -273,13 +276,13 @@ def _engine_for(net: AnyNetwork, config: MarchConfig) -> Engine:
     import torch
     blob = to_blob(net)
     key = (architecture_key(blob), tuple(map(tuple, config.bbox)), config.max_cells, config.tol_cell,
-           config.tol_weld, config.probe_delta, config.batch_cells, config.mem_budget,
+           config.tol_weld, config.probe_delta, config.batch_cells, config.mem_budget, config.precision,
            torch.cuda.current_device() if torch.cuda.is_available() else -1)
     eng = _ENGINES.get(key)
     if eng is None:
         eng = Engine(net, bbox=config.bbox, max_cells=config.max_cells, tol_cell=config.tol_cell,
                      tol_weld=config.tol_weld, probe_delta=config.probe_delta,
-                     batch_cells=config.batch_cells, mem_budget=config.mem_budget)
+                     batch_cells=config.batch_cells, mem_budget=config.mem_budget, precision=config.precision)
         _ENGINES[key] = eng
         while len(_ENGINES) > ENGINE_CACHE_SIZE:
             _ENGINES.popitem(last=False)

@@ -134,3 +134,13 @@ def test_refs_to_kind_index():
     ids = np.array([0, 9, 10, 11, 12, 17], np.int32)
     np.testing.assert_array_equal(refs_to_kind_index(ids, nb, ns),
                                   [[0, 0], [0, 9], [1, 0], [1, 1], [2, 0], [2, 5]])
+
+
+def test_topology_check_octahedron():
+    from paper_2106_10031_b200.meshes import TriangleMesh, topology_check
+    v = np.array([[1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]], float)
+    t = np.array([[0, 2, 4], [2, 1, 4], [1, 3, 4], [3, 0, 4], [2, 0, 5], [1, 2, 5], [3, 1, 5], [0, 3, 5]])
+    r = topology_check(TriangleMesh(v, t))
+    assert r["watertight"] and r["euler"] == 2 and r["components"] == 1 and r["open_edges"] == 0
+    r = topology_check(TriangleMesh(v, t[:-1]))
+    assert not r["watertight"] and r["open_edges"] == 3
