@@ -36,6 +36,7 @@ void launch_dichotomy_step(const double* vals, double* xp, double* xn, double* f
                            int32_t* active, double* out, int64_t n, double eps, double seed_tol, int last,
                            cudaStream_t s);
 void launch_midpoint(const double* a, const double* b, double* m, int64_t n, cudaStream_t s);
+void launch_point_hints(const double* X, int64_t n, double tau, double* hints, cudaStream_t s);
 void launch_count_active(const int32_t* active, int64_t n, unsigned long long* cnt, cudaStream_t s);
 void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s);
 void launch_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
@@ -155,7 +156,7 @@ struct am_engine {
     DBuf<double> s_verts;
     DBuf<int32_t> hstatus;
     DBuf<uint64_t> hslot;
-    DBuf<double> sx, sxp, pvals;
+    DBuf<double> sx, sxp, pvals, shint;
     DBuf<uint64_t> ss, ssn, sres;
     DBuf<int32_t> sact, sdone;
     // graph of one iteration
@@ -528,7 +529,7 @@ extern "C" int am_engine_destroy(am_engine* e) {
     cudaStreamSynchronize(e->stream);
     if (e->gexec) cudaGraphExecDestroy(e->gexec);
     if (e->graph) cudaGraphDestroy(e->graph);
-    DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx,
+    DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx, &e->shint,
                            &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1], &e->pool_hint,
                            &e->ckey_hint, &e->emit_hint, &e->s_verts, &e->shape_tab};
     for (auto* b : dbl) b->release(e->stream);
@@ -790,14 +791,31 @@ static int launch_iteration(am_engine* e) {
     launch_prec_target(R, e->status.p, e->emit_dup.p, e->emit_pool.p, c, e->PR, e->probe_pts.p, e->PB, s);
     launch_resolve(R, H, e->val_buf.p, c, R.cap_pend, e->probe_pts.p, shapes ? e->probe_shape.p : nullptr, e->PB, s);
     launch_pend_finalize(c, s);
-    // exact forward evaluation of the remaining probes
+    if (tm) cudaEventRecord(e->ev[4], s);
+    CK(cudaGetLastError());
+    return AM_OK;
+}
+
+// exact forward evaluation of the accumulated probe points (reference marching.py:271-276) and
+// insertion of their states.  Run by the host loop between graph batches whenever probes are
+// waiting: the visited set is the closure of the seeds and does not depend on when a probe's
+// state is inserted, and after probe validation only a handful of probes per march remain, so
+// keeping this stage out of the per-iteration graph saves ~10 launches per iteration.
+static int probe_flush(am_engine* e) {
+    cudaStream_t s = e->stream;
+    unsigned long long* c = e->ctr.p;
+    const bool shapes = e->shape_w >= 0;
+    const bool multi = e->P.world > 1;
+    RC(ensure_hash(e, e->PB));
+    HashSet H = hs(e);
+    if (e->timing) cudaEventRecord(e->ev[5], s);
     launch_zero_keys(e->pkeys.p, c + C_NPROBE, e->KW, e->PB, e->shape_w, shapes ? e->probe_shape.p : nullptr, 0, s);
-    e->grid_cap = 2;   // probes are rare after validation: a small persistent grid per layer
+    e->grid_cap = 2;   // a small persistent grid per layer
     int frc = forward(e, e->probe_pts.p, nullptr, e->pkeys.p, nullptr, e->pZ.p, c + C_NPROBE, e->PB);
     e->grid_cap = 0;
     RC(frc);
-    if (tm) cudaEventRecord(e->ev[4], s);
     if (multi) {
+        CK(cudaMemsetAsync(c + C_NPLOCAL, 0, sizeof(unsigned long long), s));
         launch_route_emitted(e->pkeys.p, c + C_NPROBE, e->PB, e->KW, e->P.rank, e->P.world, e->local_idx.p,
                              c + C_NPLOCAL, e->outbox.p, c + C_NOUT, nullptr, s);
         launch_hash_insert(H, e->pkeys.p, e->local_idx.p, c + C_NPLOCAL, e->PB, e->pstatus.p, e->pslot.p, nullptr, s);
@@ -808,7 +826,15 @@ static int launch_iteration(am_engine* e) {
         launch_hash_fixup(H, e->pkeys.p, nullptr, c + C_NPROBE, e->PB, e->pstatus.p, e->pslot.p, 0u, nullptr,
                           e->queue.p, c + C_QTAIL, nullptr, s);
     }
+    launch_probe_done(c, e->PB, s);
     CK(cudaGetLastError());
+    if (e->timing) {
+        cudaEventRecord(e->ev[4], s);
+        CK(cudaEventSynchronize(e->ev[4]));
+        float t = 0;
+        cudaEventElapsedTime(&t, e->ev[5], e->ev[4]);
+        e->t_probe += t;
+    }
     return AM_OK;
 }
 
@@ -867,7 +893,11 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
     while (n < max_iters) {
         RC(sync_counters(e));
         if (e->hctr[C_OVF1]) return fail(AM_ERR_OVERFLOW, "output capacity overflow (%llu events)", e->hctr[C_OVF1]);
-        if (e->hctr[C_QHEAD] >= e->hctr[C_QTAIL] && e->hctr[C_NPEND] == 0) break;
+        if (e->hctr[C_QHEAD] >= e->hctr[C_QTAIL] && e->hctr[C_NPEND] == 0) {
+            if (e->hctr[C_NPROBE] == 0) break;
+            RC(probe_flush(e));
+            continue;
+        }
         int k = (int)std::min<int64_t>(e->graph_batch, max_iters - n);
         RC(ensure_iter_room(e, k + 1));
         if (e->timing) {
@@ -880,6 +910,10 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
         n += k;
         RC(sync_counters(e));
         if (e->hctr[C_STALL]) e->graph_valid = false;  // guard fired: the next round grows buffers
+        if (e->hctr[C_NPROBE]) {
+            RC(probe_flush(e));
+            RC(sync_counters(e));
+        }
     }
     RC(sync_counters(e));
     e->iters = (int64_t)e->hctr[C_ITER];
@@ -889,7 +923,7 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
 
 // --------------------------------------------------------------- marching
 // insert host-sized keys and queue the new ones
-static int push_keys(am_engine* e, const uint64_t* d_keys, int64_t n) {
+static int push_keys(am_engine* e, const uint64_t* d_keys, int64_t n, const double* d_hints = nullptr) {
     if (n <= 0) return AM_OK;
     RC(ensure_hash(e, n));
     CK(e->hstatus.reserve(n, e->stream));
@@ -902,11 +936,11 @@ static int push_keys(am_engine* e, const uint64_t* d_keys, int64_t n) {
         launch_hash_insert(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, nullptr,
                            e->stream);
         launch_hash_fixup(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, 0u, nullptr,
-                          e->queue.p, e->ctr.p + C_QTAIL, nullptr, e->stream);
+                          e->queue.p, e->ctr.p + C_QTAIL, d_hints, e->stream);
     } else {
         launch_hash_insert(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, nullptr, e->stream);
         launch_hash_fixup(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, 0u, nullptr, e->queue.p,
-                          e->ctr.p + C_QTAIL, nullptr, e->stream);
+                          e->ctr.p + C_QTAIL, d_hints, e->stream);
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(e->stream));
@@ -1021,8 +1055,14 @@ extern "C" int am_seed_shapes(am_engine* e, const double* d_pts, const int32_t* 
     CK(cudaMemsetAsync(e->changed.p, 0, n * 4, s));
     RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n));
     launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, nullptr, s);
+    // the seed point (inside the seed's cell, on the surface up to seed_tol) is the face
+    // solver's hint, with a small initial reach that the solver widens as needed
+    double ext = 0.0;
+    for (int k = 0; k < 3; k++) ext = std::max(ext, e->P.bbox_hi[k] - e->P.bbox_lo[k]);
+    CK(e->shint.reserve(n * 4, s));
+    launch_point_hints(e->sx.p, n, ext / 256.0, e->shint.p, s);
     CK(cudaGetLastError());
-    return push_keys(e, e->sres.p, n);
+    return push_keys(e, e->sres.p, n, e->shint.p);
 }
 
 // batched bisection between sign-opposite samples (reference seeding.py:84-112)

@@ -42,14 +42,16 @@ namespace am {
 // and a log2 histogram of per-cell cycles in dbg[16..40)
 #ifdef AM_FACE_STATS
 #define FSTAT(i, v) do { if (lane == 0 && A.dbg) atomicAdd(&A.dbg[i], (unsigned long long)(v)); } while (0)
+// phase timers: clock cycles since the previous mark accumulate in dbg[40 + i]
+#define PMARK(i) do { long long now_ = clock64(); FSTAT(40 + (i), now_ - t_mark); t_mark = now_; } while (0)
 #else
 #define FSTAT(i, v) do { } while (0)
+#define PMARK(i) do { } while (0)
 #endif
 
 constexpr int VMAX = 32;   // clip polygon capacity (one lane per vertex)
 constexpr int CMAX = 64;   // candidate plane set capacity (uint64 masks)
 constexpr int QMAX = 64;   // accepted raw vertices
-constexpr int EMAXC = 32;  // candidate descriptors per cell
 constexpr int FW = 4;      // warps per CTA
 constexpr int NMAX = 96;   // hinted path: rows near the hint point
 constexpr double kCDelta = 1e-10;
@@ -89,11 +91,9 @@ struct FaceWarp {
     int eargmin[QMAX];              // per-edge global row when the mask is empty (argmin fallback)
     int eval[QMAX];                 // per edge: 1 if the mirrored probe validated
     int efirst[QMAX], eprec[QMAX];  // per edge: crossable[0], probe-record slot
-    // candidate descriptors: flip bits (<= 4, or -1 = "all bits of edge e") and branch target
-    int cd_edge[EMAXC], cd_nflip[EMAXC], cd_flip[EMAXC][4], cd_branch[EMAXC];
-    int cd_probe[EMAXC];            // >= 0: this flip carries the probe record of edge cd_probe
-    long long pbase;
-    long long cbase;
+    // per-edge emission: neuron / branch counts and output offsets (warp scans)
+    int e_nb[QMAX], e_nbr[QMAX], e_cdoff[QMAX + 1], e_refoff[QMAX], e_valoff[QMAX];
+    long long obase[5];             // reserved bases: verts, refs, validated, candidates, probe records
     double diam;                    // polygon diameter bound (hint radius for the neighbours)
     int n_cd;
     int status;
@@ -109,7 +109,7 @@ struct Ctx {
 
 // unit oriented constraint row of global plane id gr (reference cells.py:127-185); false if dropped.
 // *nrm receives the raw normal norm (neuron / branch rows) or 1 (box rows)
-__device__ __forceinline__ bool get_row(const Ctx& c, int gr, double n[3], double& o, double* nrm_out = nullptr) {
+__device__ __noinline__ bool get_row(const Ctx& c, int gr, double n[3], double& o, double* nrm_out = nullptr) {
     if (gr < c.NB) {
         const double2* p = reinterpret_cast<const double2*>(c.Z + (int64_t)gr * 4);
         double2 a = __ldg(p), b = __ldg(p + 1);
@@ -147,13 +147,10 @@ __device__ __forceinline__ double dot3(const double* a, const double* b) { retur
 // raw functional of global plane id gr (not normalised, not oriented); kind: 0 neuron,
 // 1 branch (valid unless it is the cell's own branch), 2 box, -1 none
 struct RawRow { double x, y, z, c; int kind; };
-__device__ __forceinline__ RawRow load_raw(const Ctx& c, int gr) {
+// branch-dominance, box and padding rows (a handful per cell): out of line
+__device__ __noinline__ RawRow load_raw_other(const Ctx& c, int gr) {
     RawRow r;
-    if (gr < c.NB) {
-        const double2* p = reinterpret_cast<const double2*>(c.Z + (int64_t)gr * 4);
-        double2 a = __ldg(p), b = __ldg(p + 1);
-        r.x = a.x; r.y = a.y; r.z = b.x; r.c = b.y; r.kind = 0;
-    } else if (gr < c.NB + c.M) {
+    if (gr < c.NB + c.M) {
         int t = gr - c.NB;
         r.kind = (!c.ensemble || t == c.branch) ? -1 : 1;
         if (r.kind == 1) {
@@ -175,6 +172,16 @@ __device__ __forceinline__ RawRow load_raw(const Ctx& c, int gr) {
         r.kind = -1;
     }
     return r;
+}
+__device__ __forceinline__ RawRow load_raw(const Ctx& c, int gr) {
+    if (gr < c.NB) {
+        RawRow r;
+        const double2* p = reinterpret_cast<const double2*>(c.Z + (int64_t)gr * 4);
+        double2 a = __ldg(p), b = __ldg(p + 1);
+        r.x = a.x; r.y = a.y; r.z = b.x; r.c = b.y; r.kind = 0;
+        return r;
+    }
+    return load_raw_other(c, gr);
 }
 // 2-D projection (a, b, g) of the oriented unit row in the face-plane frame, with one
 // reciprocal per row (the streaming passes only need it to ~1 ulp); *nrm = raw norm
@@ -232,12 +239,119 @@ __device__ __forceinline__ bool lex_less(const double* a, const double* b) {
     return a[2] < b[2];
 }
 
+// current clip polygon of a warp: vertex count, ring buffer index, status (0 ok, 1 empty,
+// 2 overflow) and the bounding circle (sc, tc, rho) used by the quick rejection tests
+struct Poly { int nv, cur, status; double sc, tc, rho; };
+
+// warp-parallel Sutherland-Hodgman step by (ca, cb, cg) (<= 0 inside), one lane per vertex;
+// keeps the bounding circle current.  Out of line so the three call sites share one copy.
+__device__ __noinline__ Poly clip_poly(FaceWarp* W, Poly P, double ca, double cb, double cg) {
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const int nv = P.nv, cur = P.cur;
+    double si = 0, ti = 0, di = 0;
+    if (lane < nv) { si = W->ps[cur][lane]; ti = W->pt[cur][lane]; di = ca * si + cb * ti + cg; }
+    int nx = lane + 1 == nv ? 0 : lane + 1;
+    double sj = __shfl_sync(full, si, nx & 31), tj = __shfl_sync(full, ti, nx & 31),
+           dj = __shfl_sync(full, di, nx & 31);
+    bool in_i = di <= 0.0, in_j = dj <= 0.0;
+    if (!__any_sync(full, lane < nv && !in_i)) return P;
+    int cnt = lane < nv ? (in_i ? 1 : 0) + (in_i != in_j ? 1 : 0) : 0;
+    int pre = cnt;
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        int y = __shfl_up_sync(full, pre, o2);
+        if (lane >= o2) pre += y;
+    }
+    int total = __shfl_sync(full, pre, 31);
+    pre -= cnt;
+    if (total > VMAX) { P.status = 2; return P; }
+    int dst = cur ^ 1;
+    double ns = 0.0, nt = 0.0;
+    if (lane < nv) {
+        int w = pre;
+        if (in_i) { W->ps[dst][w] = si; W->pt[dst][w] = ti; ns += si; nt += ti; w++; }
+        if (in_i != in_j) {
+            double lam = di / (di - dj);
+            double xs = si + lam * (sj - si), xt = ti + lam * (tj - ti);
+            W->ps[dst][w] = xs;
+            W->pt[dst][w] = xt;
+            ns += xs; nt += xt;
+        }
+    }
+    __syncwarp();
+    P.cur = dst;
+    P.nv = total;
+    if (total < 3) { P.status = 1; return P; }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) {
+        ns += __shfl_xor_sync(full, ns, o2);
+        nt += __shfl_xor_sync(full, nt, o2);
+    }
+    P.sc = ns / total; P.tc = nt / total;
+    double d2 = 0.0;
+    if (lane < total) {
+        double ds = W->ps[dst][lane] - P.sc, dt = W->pt[dst][lane] - P.tc;
+        d2 = ds * ds + dt * dt;
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) d2 = fmax(d2, __shfl_xor_sync(full, d2, o2));
+    P.rho = sqrt(d2) * (1.0 + 1e-9) + 1e-12;
+    return P;
+}
+
+// exclusive warp scan of v; *total = sum over the warp
+__device__ __forceinline__ int warp_excl_scan(int v, int& total) {
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+}
+
+// flip subsets of an edge with 3 neuron planes in the reference's order (itertools.combinations
+// by size 0..3): bit i = flip the i-th neuron plane of the edge
+__constant__ unsigned kComb3[8] = {0u, 1u, 2u, 4u, 3u, 5u, 6u, 7u};
+
+// polygons with more than 32 vertices: the serial ordering (lane 0)
+__device__ __noinline__ void order_serial(FaceWarp* W, int nr, const double* fu) {
+    for (int i = 0; i < nr; i++) W->u.pp.ord[i] = i;
+    for (int i = 1; i < nr; i++) {   // stable sort by angle (reference np.argsort kind="stable")
+        int tt = W->u.pp.ord[i], j = i - 1;
+        while (j >= 0 && W->u.pp.ang[W->u.pp.ord[j]] > W->u.pp.ang[tt]) { W->u.pp.ord[j + 1] = W->u.pp.ord[j]; j--; }
+        W->u.pp.ord[j + 1] = tt;
+    }
+    double tot[3] = {0, 0, 0};
+    for (int i = 0; i < nr; i++) {
+        const double* p = W->u.pp.rv[W->u.pp.ord[i]];
+        const double* q = W->u.pp.rv[W->u.pp.ord[(i + 1) % nr]];
+        tot[0] += p[1] * q[2] - p[2] * q[1];
+        tot[1] += p[2] * q[0] - p[0] * q[2];
+        tot[2] += p[0] * q[1] - p[1] * q[0];
+    }
+    double area = 0.5 * ((tot[0] * fu[0] + tot[1] * fu[1]) + tot[2] * fu[2]);
+    if (area < 0.0)
+        for (int i = 0, j = nr - 1; i < j; i++, j--) { int tt = W->u.pp.ord[i]; W->u.pp.ord[i] = W->u.pp.ord[j]; W->u.pp.ord[j] = tt; }
+    int start = 0;
+    for (int k = 1; k < nr; k++)
+        if (lex_less(W->u.pp.rv[W->u.pp.ord[k]], W->u.pp.rv[W->u.pp.ord[start]])) start = k;
+    for (int k = 0; k < nr; k++) {
+        int src = W->u.pp.ord[(k + start) % nr];
+        for (int d = 0; d < 3; d++) W->u.pp.fv[k][d] = W->u.pp.rv[src][d];
+        W->u.pp.fs[k] = W->u.pp.rs[src];
+    }
+}
+
 __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int item = A.items[fi];
 #ifdef AM_FACE_STATS
     const long long t_start = clock64();
+    long long t_mark = t_start;
     int n_clip1 = 0, n_clip2 = 0;
 #endif
     (void)0;
@@ -276,63 +390,17 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     int status = face_ok ? 0 : 1;  // 0 ok, 1 empty, 2 overflow
     double sc = 0.0, tc = 0.0, rho = 0.0;   // bounding circle of the current polygon
 
-    // warp-parallel Sutherland-Hodgman step by (ca, cb, cg) (<= 0 inside), one lane per vertex;
-    // keeps the bounding circle current.  Returns false if nothing was cut.
-    auto clip = [&](double ca, double cb, double cg) -> bool {
-        double si = 0, ti = 0, di = 0;
-        if (lane < nv) { si = W->ps[cur][lane]; ti = W->pt[cur][lane]; di = ca * si + cb * ti + cg; }
-        int nx = lane + 1 == nv ? 0 : lane + 1;
-        double sj = __shfl_sync(full, si, nx & 31), tj = __shfl_sync(full, ti, nx & 31),
-               dj = __shfl_sync(full, di, nx & 31);
-        bool in_i = di <= 0.0, in_j = dj <= 0.0;
-        if (!__any_sync(full, lane < nv && !in_i)) return false;
-        int cnt = lane < nv ? (in_i ? 1 : 0) + (in_i != in_j ? 1 : 0) : 0;
-        int pre = cnt;
-#pragma unroll
-        for (int o2 = 1; o2 < 32; o2 <<= 1) {
-            int y = __shfl_up_sync(full, pre, o2);
-            if (lane >= o2) pre += y;
-        }
-        int total = __shfl_sync(full, pre, 31);
-        pre -= cnt;
-        if (total > VMAX) { status = 2; return true; }
-        int dst = cur ^ 1;
-        double ns = 0.0, nt = 0.0;
-        if (lane < nv) {
-            int w = pre;
-            if (in_i) { W->ps[dst][w] = si; W->pt[dst][w] = ti; ns += si; nt += ti; w++; }
-            if (in_i != in_j) {
-                double lam = di / (di - dj);
-                double xs = si + lam * (sj - si), xt = ti + lam * (tj - ti);
-                W->ps[dst][w] = xs;
-                W->pt[dst][w] = xt;
-                ns += xs; nt += xt;
-            }
-        }
-        __syncwarp();
-        cur = dst;
-        nv = total;
-        if (nv < 3) { status = 1; return true; }
-#pragma unroll
-        for (int o2 = 16; o2; o2 >>= 1) {
-            ns += __shfl_xor_sync(full, ns, o2);
-            nt += __shfl_xor_sync(full, nt, o2);
-        }
-        sc = ns / nv; tc = nt / nv;
-        double d2 = 0.0;
-        if (lane < nv) {
-            double ds = W->ps[cur][lane] - sc, dt = W->pt[cur][lane] - tc;
-            d2 = ds * ds + dt * dt;
-        }
-#pragma unroll
-        for (int o2 = 16; o2; o2 >>= 1) d2 = fmax(d2, __shfl_xor_sync(full, d2, o2));
-        rho = sqrt(d2) * (1.0 + 1e-9) + 1e-12;
-        return true;
+    // warp-parallel Sutherland-Hodgman step (clip_poly, out of line: one copy of the code)
+    auto clip = [&](double ca, double cb, double cg) {
+        Poly P{nv, cur, status, sc, tc, rho};
+        P = clip_poly(W, P, ca, cb, cg);
+        nv = P.nv; cur = P.cur; status = P.status; sc = P.sc; tc = P.tc; rho = P.rho;
     };
     // does row (a2, b2, g2) (shifted by tol) cut the current polygon?
     auto cuts = [&](double a2, double b2, double g2) -> bool {
         if ((a2 * sc + b2 * tc + g2) + rho <= 0.0) return false;   // |(a2, b2)| <= 1 for a unit row
         double mx = -1e300;
+#pragma unroll 1
         for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
         return mx > 0.0;
     };
@@ -341,10 +409,14 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     // found: F is continuous across the shared plane, so it lies on this face plane too)
     // and a search radius.  Pass 1 clips only by rows within that radius, so the polygon
     // is (nearly) final before the full passes.
-    const double4 hint = reinterpret_cast<const double4*>(A.hints)[item];
-    const bool have_hint = isfinite(hint.w);
+    // Seeds carry their surface point as the hint; it is projected onto the face plane (a
+    // no-op up to rounding for edge midpoints) so the 3-D near test and the 2-D frame agree.
+    double4 hint = reinterpret_cast<const double4*>(A.hints)[item];
+    const bool have_hint = isfinite(hint.w) && face_ok;
     double s0 = 0.0, t0 = 0.0;
     if (have_hint) {
+        const double hd = ((fu[0] * hint.x + fu[1] * hint.y) + fu[2] * hint.z) + fo;
+        hint.x -= hd * fu[0]; hint.y -= hd * fu[1]; hint.z -= hd * fu[2];
         double dx[3] = {hint.x - P0[0], hint.y - P0[1], hint.z - P0[2]};
         s0 = dot3(dx, U);
         t0 = dot3(dx, Vv);
@@ -362,6 +434,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     int risky = 0;
     const double band = tol_max + 1.5 * A.probe_delta + 1e-9;
     double tau = hint.w;
+    PMARK(0);
     for (int attempt = 0; attempt < 5 && status == 0 && have_hint && !hinted_done; attempt++) {
         const double x0[3] = {hint.x, hint.y, hint.z};
         const double lim = tau + band + 1e-9;
@@ -394,6 +467,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             }
             nn += __popc(mask);
         }
+        PMARK(1);
         bool x0ok = __all_sync(full, ok);
         ok = x0ok && nn <= NMAX;
         FSTAT(9, x0ok ? 0 : 1);
@@ -424,30 +498,62 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             __syncwarp();
             for (int i = lane; i < nn; i += 32) {   // rank sort by distance (ties: lower id first)
                 int rk = 0;
+#pragma unroll 1
                 for (int j = 0; j < nn; j++) rk += (W->u.np.nd[j] < W->u.np.nd[i]) || (W->u.np.nd[j] == W->u.np.nd[i] && j < i);
                 W->u.np.nord[rk] = i;
             }
-            // start from the square of half-size tau around x0
+            PMARK(2);
+            // start from the square of half-size tau around x0.  The polygon lives in registers
+            // (lane v holds vertex v), mirrored in W->ps/pt[cur] for the C' pass below; each near
+            // row is one register test + ballot, and a cutting row is a Sutherland-Hodgman step
+            // whose output slots come from two ballots.
             const double hw = tau;
+            double vs = 0.0, vt = 0.0;
             if (lane < 4) {
-                W->ps[0][lane] = s0 + ((lane == 0 || lane == 3) ? -hw : hw);
-                W->pt[0][lane] = t0 + ((lane < 2) ? -hw : hw);
+                vs = s0 + ((lane == 0 || lane == 3) ? -hw : hw);
+                vt = t0 + ((lane < 2) ? -hw : hw);
+                W->ps[0][lane] = vs;
+                W->pt[0][lane] = vt;
             }
             nv = 4; cur = 0;
-            sc = s0; tc = t0; rho = hw * 1.4142135623730951 * (1.0 + 1e-12) + 1e-12;
             __syncwarp();
-            for (int q = 0; q < nn && status == 0; q++) {
-                int i = W->u.np.nord[q];
-                double a2 = W->u.np.na[i], b2 = W->u.np.nb[i], g2 = W->u.np.ng[i] - tol_c;
-                if ((a2 * sc + b2 * tc + g2) + rho <= 0.0) continue;
-                double dv = lane < nv ? a2 * W->ps[cur][lane] + b2 * W->pt[cur][lane] + g2 : -1.0;
-                if (!__any_sync(full, dv > 0.0)) continue;
-                clip(a2, b2, g2);
+            const unsigned lt = (1u << lane) - 1u;
+#pragma unroll 1
+            for (int q = 0; q < nn; q++) {
+                const int i = W->u.np.nord[q];
+                const double a2 = W->u.np.na[i], b2 = W->u.np.nb[i], g2 = W->u.np.ng[i] - tol_c;
+                const bool act = lane < nv;
+                const double di = act ? a2 * vs + b2 * vt + g2 : -1.0;
+                if (!__any_sync(full, di > 0.0)) continue;
+                const int nx = lane + 1 == nv ? 0 : lane + 1;
+                const double sj = __shfl_sync(full, vs, nx & 31), tj = __shfl_sync(full, vt, nx & 31),
+                             dj = __shfl_sync(full, di, nx & 31);
+                const bool in_i = di <= 0.0, in_j = dj <= 0.0;
+                const unsigned m_in = __ballot_sync(full, act && in_i), m_x = __ballot_sync(full, act && in_i != in_j);
+                const int total = __popc(m_in) + __popc(m_x);
+                if (total > VMAX) { status = 2; break; }
+                const int dst = cur ^ 1;
+                if (act) {
+                    int w = __popc(m_in & lt) + __popc(m_x & lt);
+                    if (in_i) { W->ps[dst][w] = vs; W->pt[dst][w] = vt; w++; }
+                    if (in_i != in_j) {
+                        const double lam = di / (di - dj);
+                        W->ps[dst][w] = vs + lam * (sj - vs);
+                        W->pt[dst][w] = vt + lam * (tj - vt);
+                    }
+                }
+                __syncwarp();
+                cur = dst;
+                nv = total;
 #ifdef AM_FACE_STATS
                 n_clip1++;
 #endif
+                if (nv < 3) { status = 1; break; }
+                vs = lane < nv ? W->ps[cur][lane] : 0.0;
+                vt = lane < nv ? W->pt[cur][lane] : 0.0;
             }
             if (status == 0) {
+                PMARK(3);
                 // acceptance: P_tol within tau - band of x0
                 double dmax = 0.0;
                 if (lane < nv) {
@@ -466,7 +572,9 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
                         if (i < nn) {
                             double a2 = W->u.np.na[i], b2 = W->u.np.nb[i], g2 = W->u.np.ng[i];
                             double mx = -1e300;
-                            for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+#pragma unroll 1
+            #pragma unroll 1
+                for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
                             in = mx >= -band;
                             is_core = mx >= -tol_max - kCDelta;
                         }
@@ -502,6 +610,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         tau = fmax(2.0 * tau, 2.5 * dmax_seen);   // the polygon reached the square: widen the reach
     }
 
+    PMARK(4);
     if (status == 0 && !hinted_done) {
         // initial square; then pass 1: box rows first, then neurons, then branch rows
         nC = 0; core = 0;
@@ -578,6 +687,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             bool in = false, is_core = false;
             if (kept && (a2 * sc + b2 * tc + g2) + rho >= -band) {
                 double mx = -1e300;
+#pragma unroll 1
                 for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
                 in = mx >= -band;
                 is_core = mx >= -tol_max - kCDelta;
@@ -607,6 +717,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         risky = __any_sync(full, risky);
         if (nC <= CMAX) break;   // else: late clips inflated C' -- once more against the final polygon
     }
+    PMARK(5);
     if (status == 0 && nC > CMAX) status = 2;
     __syncwarp();
 
@@ -639,6 +750,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
                 double det = solve3(Mx, rhs, x);
                 if (det >= kTolDet) {
                     valid = true;
+#pragma unroll 1
                     for (int r = 0; r < nC; r++) {
                         double val = dot3(W->cn[r], x) + W->cn[r][3];
                         if (!(val <= tol_c)) { valid = false; break; }
@@ -660,6 +772,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         __syncwarp();
     }
 
+    PMARK(6);
     // dedup + ordering (lane 0; a handful of vertices)
     int nr = 0;
     if (status == 0) {
@@ -689,6 +802,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         if (nr < 3) status = 1;
     }
     if (status == 0) {
+        PMARK(7);
         // centroid (reference cells.py:282: verts.mean), angles in the face frame -- lane per vertex
         double cen[3] = {0, 0, 0};
         for (int k = 0; k < nr; k++) { cen[0] += W->u.pp.rv[k][0]; cen[1] += W->u.pp.rv[k][1]; cen[2] += W->u.pp.rv[k][2]; }
@@ -698,41 +812,72 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             double r0 = W->u.pp.rv[k][0] - cen[0], r1 = W->u.pp.rv[k][1] - cen[1], r2 = W->u.pp.rv[k][2] - cen[2];
             rk = fmax(rk, sqrt((r0 * r0 + r1 * r1) + r2 * r2));
             W->u.pp.ang[k] = atan2((r0 * Vv[0] + r1 * Vv[1]) + r2 * Vv[2], (r0 * U[0] + r1 * U[1]) + r2 * U[2]);
-            W->u.pp.ord[k] = k;
         }
 #pragma unroll
         for (int o2 = 16; o2; o2 >>= 1) rk = fmax(rk, __shfl_xor_sync(full, rk, o2));
         __syncwarp();
-        if (lane == 0) {
-            for (int i = 1; i < nr; i++) {   // stable sort by angle (reference np.argsort kind="stable")
-                int tt = W->u.pp.ord[i], j = i - 1;
-                while (j >= 0 && W->u.pp.ang[W->u.pp.ord[j]] > W->u.pp.ang[tt]) { W->u.pp.ord[j + 1] = W->u.pp.ord[j]; j--; }
-                W->u.pp.ord[j + 1] = tt;
+        if (nr <= 32) {
+            // lane per vertex: stable rank by angle (reference np.argsort kind="stable"), the
+            // orientation sum in sorted order on lane 0 (same terms, same order as the serial
+            // loop), CCW reversal and rotation to the lexicographically smallest vertex
+            const int k = lane;
+            int pos = 0;
+            if (k < nr) {
+                const double ak = W->u.pp.ang[k];
+#pragma unroll 1
+                for (int j = 0; j < nr; j++) {
+                    const double aj = W->u.pp.ang[j];
+                    pos += (aj < ak) || (aj == ak && j < k);
+                }
+                W->u.pp.ord[pos] = k;
             }
+            __syncwarp();
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            if (k < nr) {
+                const double* pv = W->u.pp.rv[W->u.pp.ord[k]];
+                const double* qv = W->u.pp.rv[W->u.pp.ord[k + 1 == nr ? 0 : k + 1]];
+                t0 = pv[1] * qv[2] - pv[2] * qv[1];
+                t1 = pv[2] * qv[0] - pv[0] * qv[2];
+                t2 = pv[0] * qv[1] - pv[1] * qv[0];
+            }
+            // serial left-to-right sum (bit-identical sign decision)
             double tot[3] = {0, 0, 0};
+#pragma unroll 1
             for (int i = 0; i < nr; i++) {
-                const double* p = W->u.pp.rv[W->u.pp.ord[i]];
-                const double* q = W->u.pp.rv[W->u.pp.ord[(i + 1) % nr]];
-                tot[0] += p[1] * q[2] - p[2] * q[1];
-                tot[1] += p[2] * q[0] - p[0] * q[2];
-                tot[2] += p[0] * q[1] - p[1] * q[0];
+                tot[0] += __shfl_sync(full, t0, i);
+                tot[1] += __shfl_sync(full, t1, i);
+                tot[2] += __shfl_sync(full, t2, i);
             }
-            double area = 0.5 * ((tot[0] * fu[0] + tot[1] * fu[1]) + tot[2] * fu[2]);
-            if (area < 0.0)
-                for (int i = 0, j = nr - 1; i < j; i++, j--) { int tt = W->u.pp.ord[i]; W->u.pp.ord[i] = W->u.pp.ord[j]; W->u.pp.ord[j] = tt; }
-            int start = 0;
-            for (int k = 1; k < nr; k++)
-                if (lex_less(W->u.pp.rv[W->u.pp.ord[k]], W->u.pp.rv[W->u.pp.ord[start]])) start = k;
-            for (int k = 0; k < nr; k++) {
-                int src = W->u.pp.ord[(k + start) % nr];
-                for (int d = 0; d < 3; d++) W->u.pp.fv[k][d] = W->u.pp.rv[src][d];
-                W->u.pp.fs[k] = W->u.pp.rs[src];
+            const double area = 0.5 * ((tot[0] * fu[0] + tot[1] * fu[1]) + tot[2] * fu[2]);
+            if (area < 0.0) pos = nr - 1 - pos;
+            // lexicographic minimum (first in the final order on ties)
+            double m0 = 1e300, m1 = 1e300, m2 = 1e300;
+            int mp = 0x7fffffff;
+            if (k < nr) { m0 = W->u.pp.rv[k][0]; m1 = W->u.pp.rv[k][1]; m2 = W->u.pp.rv[k][2]; mp = pos; }
+#pragma unroll
+            for (int o2 = 16; o2; o2 >>= 1) {
+                double o0 = __shfl_xor_sync(full, m0, o2), o1 = __shfl_xor_sync(full, m1, o2),
+                       oz = __shfl_xor_sync(full, m2, o2);
+                int op = __shfl_xor_sync(full, mp, o2);
+                bool take = op != 0x7fffffff &&
+                            (mp == 0x7fffffff || o0 < m0 || (o0 == m0 && (o1 < m1 || (o1 == m1 && (oz < m2 || (oz == m2 && op < mp))))));
+                if (take) { m0 = o0; m1 = o1; m2 = oz; mp = op; }
             }
+            if (k < nr) {
+                int f = pos - mp;
+                if (f < 0) f += nr;
+                W->u.pp.fv[f][0] = W->u.pp.rv[k][0]; W->u.pp.fv[f][1] = W->u.pp.rv[k][1]; W->u.pp.fv[f][2] = W->u.pp.rv[k][2];
+                W->u.pp.fs[f] = W->u.pp.rs[k];
+            }
+            if (lane == 0) W->diam = 2.0 * rk;
+        } else if (lane == 0) {
+            order_serial(W, nr, fu);
             W->diam = 2.0 * rk;
         }
         __syncwarp();
     }
 
+    PMARK(8);
     // per-edge transition planes + mirrored-probe validation (lane per edge)
     if (status == 0) {
         bool need_argmin = false;
@@ -741,6 +886,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             const double* q = W->u.pp.fv[(e + 1) % nr];
             double mid[3] = {0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2])};
             unsigned long long on_mid = 0;
+#pragma unroll 1
             for (int r = 0; r < nC; r++)
                 if (((core >> r) & 1ull) && fabs(dot3(W->cn[r], mid) + W->cn[r][3]) <= tol_p) on_mid |= 1ull << r;
             unsigned long long shared = W->u.pp.fs[e] & W->u.pp.fs[(e + 1) % nr];
@@ -765,6 +911,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
                     double qp[3] = {mid[0] - A.probe_delta * W->cn[kr][0], mid[1] - A.probe_delta * W->cn[kr][1],
                                     mid[2] - A.probe_delta * W->cn[kr][2]};
                     ok = 1;
+#pragma unroll 1
                     for (int r = 0; r < nC && ok; r++) {
                         if (W->cid[r] >= box0) continue;
                         double v = dot3(W->cn[r], qp) + W->cn[r][3];
@@ -833,183 +980,188 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         }
         return;
     }
-    if (lane == 0) {
-        int nrefs_total = 0, nvalid = 0, nprec = 0, ncd = 0;
-        const int box0l = box0;
-        for (int e = 0; e < nr; e++) {
-            nrefs_total += W->erow[e] ? __popcll(W->erow[e]) : 1;
-            nvalid += W->eval[e];
-            int nb = 0, nbr = 0, first = -1;   // first: global id of crossable[0]
-            if (W->erow[e]) {
-                unsigned long long m = W->erow[e];
+    PMARK(9);
+    // lane per edge: transition refs, validated neuron, probe record and the neighbour states
+    // of reference marching.py:152-186, 262-288; warp scans give every output offset and lane 0
+    // reserves all ranges with one round of independent atomics
+    const int NBl = c.NB;
+    int tot_ref = 0, tot_val = 0, tot_cd = 0, tot_prec = 0;
+#pragma unroll 1
+    for (int eb = 0; eb < nr; eb += 32) {
+        const int e = eb + lane;
+        int nref = 0, nval = 0, ncd = 0, npr = 0;
+        if (e < nr) {
+            int first = -1, nb = 0, nbr = 0;   // first: global id of crossable[0]
+            unsigned long long m = W->erow[e];
+            if (m) {
+                nref = __popcll(m);
                 while (m) {
-                    int r = __ffsll((long long)m) - 1;
+                    const int r = __ffsll((long long)m) - 1;
                     m &= m - 1;
-                    int gid = W->cid[r];
-                    if (gid >= box0l) continue;
+                    const int gid = W->cid[r];
+                    if (gid >= box0) continue;
                     if (first < 0) first = gid;
-                    if (gid < c.NB) { if (nb < 32) W->tb[nb++] = gid; }
-                    else if (nbr < 32) W->tr[nbr++] = gid - c.NB;
+                    if (gid < NBl) nb++; else nbr++;
                 }
-            } else if (W->eargmin[e] < box0l) {
-                first = W->eargmin[e];
-                if (first < c.NB) W->tb[nb++] = first; else W->tr[nbr++] = first - c.NB;
-            }
-            W->efirst[e] = first;
-            if (first < 0) continue;
-            nprec++;
-            const bool single = (nb == 1 && nbr == 0);
-            // subsets: combinations of sizes 0..nb (nb <= 3) or singles + full + () (nb > 3)
-            int nsub = 0, sub_mask[8];
-            const bool big = nb > 3;
-            if (big) {
-                nsub = nb + 2;
             } else {
-                for (int k = 0; k <= nb; k++) {
-                    int idx[3] = {0, 1, 2};
-                    for (int i = 0; i < k; i++) idx[i] = i;
-                    for (;;) {
-                        int mk = 0;
-                        for (int i = 0; i < k; i++) mk |= 1 << idx[i];
-                        sub_mask[nsub++] = mk;
-                        int i = k - 1;
-                        while (i >= 0 && idx[i] == nb - k + i) i--;
-                        if (i < 0) break;
-                        idx[i]++;
-                        for (int tt = i + 1; tt < k; tt++) idx[tt] = idx[tt - 1] + 1;
-                    }
-                }
+                nref = 1;
+                const int g = W->eargmin[e];
+                if (g < box0) { first = g; if (g < NBl) nb = 1; else nbr = 1; }
             }
-            for (int si = 0; si < nsub; si++) {
-                for (int ti = -1; ti < nbr; ti++) {
-                    bool empty_sub = big ? (si == nb + 1) : (sub_mask[si] == 0);
-                    if (empty_sub && ti < 0) continue;
-                    if (ncd >= EMAXC) { atomicAdd(&A.overflow[0], 1ull); continue; }
-                    W->cd_edge[ncd] = e;
-                    W->cd_branch[ncd] = ti >= 0 ? W->tr[ti] : -1;
-                    W->cd_probe[ncd] = -1;
-                    int nf = 0;
-                    if (big) {
-                        if (si < nb) { W->cd_flip[ncd][0] = W->tb[si]; nf = 1; }
-                        else if (si == nb) { nf = -1; }   // all neuron bits of the edge
-                    } else {
-                        for (int i = 0; i < nb; i++)
-                            if (sub_mask[si] & (1 << i)) W->cd_flip[ncd][nf++] = W->tb[i];
-                    }
-                    W->cd_nflip[ncd] = nf;
-                    if (single) W->cd_probe[ncd] = e;   // the lone flip carries the probe record
-                    ncd++;
-                }
+            nval = W->eval[e];
+            if (first >= 0) {
+                // flip subsets: all combinations (nb <= 3) or singles + all + none (nb > 3),
+                // times (no branch change + each branch target), minus (none, no change)
+                npr = 1;
+                ncd = (nb > 3 ? nb + 2 : (1 << nb)) * (nbr + 1) - 1;
             }
+            W->efirst[e] = first; W->e_nb[e] = nb; W->e_nbr[e] = nbr;
         }
-        // one round of reservations
-        unsigned long long r_cell = atomicAdd(A.n_cells, 1ull);
-        unsigned long long r_vert = atomicAdd(A.n_verts, (unsigned long long)nr);
-        unsigned long long r_ref = atomicAdd(A.n_refs, (unsigned long long)nrefs_total);
-        unsigned long long r_val = nvalid ? atomicAdd(A.n_val, (unsigned long long)nvalid) : 0ull;
-        unsigned long long r_cand = ncd ? atomicAdd(A.n_cand, (unsigned long long)ncd) : 0ull;
-        unsigned long long r_prec = nprec ? atomicAdd(A.n_prec, (unsigned long long)nprec) : 0ull;
-        const int64_t cell = (int64_t)r_cell, voff = (int64_t)r_vert, roff = (int64_t)r_ref, vloff = (int64_t)r_val;
-        bool fits = cell < A.cap_cells && voff + nr <= A.cap_verts && roff + nrefs_total <= A.cap_refs &&
-                    vloff + nvalid <= A.cap_val && (int64_t)r_cand + ncd <= A.cap_cand &&
-                    (int64_t)r_prec + nprec <= A.cap_prec;
+        int t_ref, t_val, t_cd, t_pr;
+        const int o_ref = warp_excl_scan(nref, t_ref), o_val = warp_excl_scan(nval, t_val);
+        const int o_cd = warp_excl_scan(ncd, t_cd), o_pr = warp_excl_scan(npr, t_pr);
+        if (e < nr) {
+            W->e_refoff[e] = tot_ref + o_ref; W->e_valoff[e] = tot_val + o_val;
+            W->e_cdoff[e] = tot_cd + o_cd; W->eprec[e] = tot_prec + o_pr;
+        }
+        tot_ref += t_ref; tot_val += t_val; tot_cd += t_cd; tot_prec += t_pr;
+    }
+    if (lane == 0) {
+        W->e_cdoff[nr] = tot_cd;
+        const unsigned long long r_cell = atomicAdd(A.n_cells, 1ull);
+        const unsigned long long r_vert = atomicAdd(A.n_verts, (unsigned long long)nr);
+        const unsigned long long r_ref = atomicAdd(A.n_refs, (unsigned long long)tot_ref);
+        const unsigned long long r_val = tot_val ? atomicAdd(A.n_val, (unsigned long long)tot_val) : 0ull;
+        const unsigned long long r_cand = tot_cd ? atomicAdd(A.n_cand, (unsigned long long)tot_cd) : 0ull;
+        const unsigned long long r_prec = tot_prec ? atomicAdd(A.n_prec, (unsigned long long)tot_prec) : 0ull;
+        const int64_t cell = (int64_t)r_cell;
+        const bool fits = cell < A.cap_cells && (int64_t)r_vert + nr <= A.cap_verts &&
+                          (int64_t)r_ref + tot_ref <= A.cap_refs && (int64_t)r_val + tot_val <= A.cap_val &&
+                          (int64_t)r_cand + tot_cd <= A.cap_cand && (int64_t)r_prec + tot_prec <= A.cap_prec;
         if (!fits) {
             atomicAdd(&A.overflow[1], 1ull);
             if (cell < A.cap_cells) { A.cell_pool[cell] = pidx; A.cell_nv[cell] = -2; A.cell_voff[cell] = 0; }
             A.pool_vn[pidx] = 0;
-            W->n_cd = -1;
+            W->status = -1;
         } else {
             A.cell_pool[cell] = pidx;
             A.cell_nv[cell] = nr;
-            A.cell_voff[cell] = voff;
-            int64_t ro = roff, vo = vloff, po = (int64_t)r_prec;
-            for (int e = 0; e < nr; e++) {
-                A.verts[(voff + e) * 3 + 0] = W->u.pp.fv[e][0];
-                A.verts[(voff + e) * 3 + 1] = W->u.pp.fv[e][1];
-                A.verts[(voff + e) * 3 + 2] = W->u.pp.fv[e][2];
-                A.edge_roff[voff + e] = ro;
-                int cnt = 0;
-                if (W->erow[e]) {
-                    unsigned long long m = W->erow[e];
-                    while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; A.edge_refs[ro++] = W->cid[r]; cnt++; }
-                } else {
-                    A.edge_refs[ro++] = W->eargmin[e];
-                    cnt = 1;
-                }
-                A.edge_nrefs[voff + e] = cnt;
-                if (W->eval[e]) {   // validated neuron = the single crossable plane of edge e
-                    unsigned long long m = W->erow[e];
-                    int kn = -1;
-                    while (m) { int r = __ffsll((long long)m) - 1; m &= m - 1; if (W->cid[r] < box0l) kn = W->cid[r]; }
-                    A.val_buf[vo++] = kn;
-                }
-                const int first = W->efirst[e];
-                if (first < 0) continue;
-                // probe across crossable[0] (reference marching.py:271-276) as a probe record:
-                // single-neuron edges point at their flip (resolved by that cell's mirrored
-                // validation); any other edge is a forced exact forward evaluation (cand = -1)
-                double pn[3], po_;
-                int pr = -1;
-                for (int r = 0; r < nC; r++)
-                    if (W->cid[r] == first) { pr = r; break; }
-                if (pr >= 0) { pn[0] = W->cn[pr][0]; pn[1] = W->cn[pr][1]; pn[2] = W->cn[pr][2]; }
-                else get_row(c, first, pn, po_);
-                const double* p = W->u.pp.fv[e];
-                const double* q = W->u.pp.fv[(e + 1) % nr];
-                A.prec_pt[po * 3 + 0] = 0.5 * (p[0] + q[0]) + A.probe_delta * pn[0];
-                A.prec_pt[po * 3 + 1] = 0.5 * (p[1] + q[1]) + A.probe_delta * pn[1];
-                A.prec_pt[po * 3 + 2] = 0.5 * (p[2] + q[2]) + A.probe_delta * pn[2];
-                A.prec_k[po] = first;
-                A.prec_cand[po] = -1;
-                if (A.prec_s) A.prec_s[po] = item_shape(c.key, A.shape_w);
-                W->eprec[e] = (int)(po - (int64_t)r_prec);
-                po++;
-            }
-            A.pool_voff[pidx] = vloff;
-            A.pool_vn[pidx] = nvalid;
-            W->n_cd = ncd;
-            W->cbase = (long long)r_cand;
-            W->pbase = (long long)r_prec;
+            A.cell_voff[cell] = (int64_t)r_vert;
+            A.pool_voff[pidx] = (int64_t)r_val;
+            A.pool_vn[pidx] = tot_val;
+            W->status = 0;
+            W->obase[0] = (long long)r_vert; W->obase[1] = (long long)r_ref; W->obase[2] = (long long)r_val;
+            W->obase[3] = (long long)r_cand; W->obase[4] = (long long)r_prec;
         }
     }
     __syncwarp();
-    const int ncd = W->n_cd;
-    if (ncd < 0) return;
-    const int64_t cbase = W->cbase;
-    // candidate keys, cooperatively: word w of candidate k; lane 0 links single-edge probes
-    for (int k = 0; k < ncd; k++) {
-        const int64_t ci = cbase + k;
-        uint64_t* dst = A.cand + ci * A.KW;
-        for (int w = lane; w < A.KW; w += 32) {
-            uint64_t word = c.key[w];
-            int nf = W->cd_nflip[k];
-            if (nf >= 0) {
-                for (int f = 0; f < nf; f++) {
-                    int b = W->cd_flip[k][f];
-                    if ((b >> 6) == w) word ^= key_mask(b);
-                }
-            } else {
-                int e = W->cd_edge[k];
-                unsigned long long m = W->erow[e];
-                while (m) {
-                    int r = __ffsll((long long)m) - 1; m &= m - 1;
-                    int b = W->cid[r];
-                    if (b < c.NB && (b >> 6) == w) word ^= key_mask(b);
-                }
+    if (W->status < 0) return;
+    const int64_t voff = W->obase[0], roff = W->obase[1], vloff = W->obase[2], cbase = W->obase[3],
+                  pbase = W->obase[4];
+    PMARK(10);
+    // per-edge records (lane per edge)
+#pragma unroll 1
+    for (int e = lane; e < nr; e += 32) {
+        const double* p = W->u.pp.fv[e];
+        const double* q = W->u.pp.fv[e + 1 == nr ? 0 : e + 1];
+        A.verts[(voff + e) * 3 + 0] = p[0];
+        A.verts[(voff + e) * 3 + 1] = p[1];
+        A.verts[(voff + e) * 3 + 2] = p[2];
+        int64_t ro = roff + W->e_refoff[e];
+        A.edge_roff[voff + e] = ro;
+        int cnt = 0, kn = -1;
+        unsigned long long m = W->erow[e];
+        if (m) {
+            while (m) {
+                const int r = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const int gid = W->cid[r];
+                A.edge_refs[ro++] = gid;
+                cnt++;
+                if (gid < box0) kn = gid;
             }
-            if (A.ensemble && w == A.KW - 1 && W->cd_branch[k] >= 0) word = (uint64_t)W->cd_branch[k];
-            dst[w] = word;
+        } else {
+            A.edge_refs[ro++] = W->eargmin[e];
+            cnt = 1;
         }
-        if (lane == 0) {
-            const int e = W->cd_edge[k];
-            const double* p = W->u.pp.fv[e];
-            const double* q = W->u.pp.fv[(e + 1) % nr];
+        A.edge_nrefs[voff + e] = cnt;
+        if (W->eval[e]) A.val_buf[vloff + W->e_valoff[e]] = kn;   // the edge's single crossable neuron
+        const int first = W->efirst[e];
+        if (first < 0) continue;
+        // probe across crossable[0] (reference marching.py:271-276) as a probe record: a
+        // single-neuron edge points at its lone flip (resolved by that cell's mirrored
+        // validation); any other edge is a forced exact forward evaluation (cand = -1)
+        double pn[3], po_;
+        int pr = -1;
+#pragma unroll 1
+        for (int r = 0; r < nC; r++)
+            if (W->cid[r] == first) { pr = r; break; }
+        if (pr >= 0) { pn[0] = W->cn[pr][0]; pn[1] = W->cn[pr][1]; pn[2] = W->cn[pr][2]; }
+        else get_row(c, first, pn, po_);
+        const int64_t po = pbase + W->eprec[e];
+        A.prec_pt[po * 3 + 0] = 0.5 * (p[0] + q[0]) + A.probe_delta * pn[0];
+        A.prec_pt[po * 3 + 1] = 0.5 * (p[1] + q[1]) + A.probe_delta * pn[1];
+        A.prec_pt[po * 3 + 2] = 0.5 * (p[2] + q[2]) + A.probe_delta * pn[2];
+        A.prec_k[po] = first;
+        const bool single = W->e_nb[e] == 1 && W->e_nbr[e] == 0;
+        A.prec_cand[po] = single ? (int32_t)(cbase + W->e_cdoff[e]) : -1;
+        if (A.prec_s) A.prec_s[po] = item_shape(c.key, A.shape_w);
+    }
+    PMARK(11);
+    // neighbour keys, one (candidate, word) per thread: coalesced over the cell's candidates
+    const int KW = A.KW;
+    const int n_words = tot_cd * KW;
+#pragma unroll 1
+    for (int idx = lane; idx < n_words; idx += 32) {
+        const int k = idx / KW, w = idx - k * KW;
+        int lo = 0, hi = nr - 1;   // edge of candidate k: last e with e_cdoff[e] <= k
+        while (lo < hi) {
+            const int md = (lo + hi + 1) >> 1;
+            if (W->e_cdoff[md] <= k) lo = md; else hi = md - 1;
+        }
+        const int e = lo;
+        const int j = k - W->e_cdoff[e];
+        const int nb = W->e_nb[e], nbr = W->e_nbr[e];
+        const bool big = nb > 3;
+        // position in the (subset, branch target) enumeration with the skipped (none, no change)
+        const int pos = big ? (j < (nb + 1) * (nbr + 1) ? j : j + 1) : j + 1;
+        const int si = pos / (nbr + 1), ti = pos % (nbr + 1) - 1;
+        const unsigned sub = nb == 3 ? kComb3[si] : (unsigned)si;   // combination order for nb <= 3
+        uint64_t word = c.key[w];
+        int branch = -1, in_ = 0, ib = 0;
+        auto visit = [&](int gid) {
+            if (gid >= box0) return;
+            if (gid < NBl) {
+                const bool fl = big ? (si < nb ? in_ == si : si == nb) : ((sub >> in_) & 1u);
+                if (fl && (gid >> 6) == w) word ^= key_mask(gid);
+                in_++;
+            } else {
+                if (ib == ti) branch = gid - NBl;
+                ib++;
+            }
+        };
+        unsigned long long m = W->erow[e];
+        if (m) {
+            while (m) {
+                const int r = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                visit(W->cid[r]);
+            }
+        } else {
+            visit(W->eargmin[e]);
+        }
+        if (A.ensemble && w == KW - 1 && branch >= 0) word = (uint64_t)branch;
+        const int64_t ci = cbase + k;
+        A.cand[ci * KW + w] = word;
+        if (w == 0) {
             // hint for the neighbour: midpoint of the shared edge + search radius
+            const double* p = W->u.pp.fv[e];
+            const double* q = W->u.pp.fv[e + 1 == nr ? 0 : e + 1];
             reinterpret_cast<double4*>(A.emit_hint)[ci] =
                 make_double4(0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2]), 2.0 * W->diam + 1e-9);
-            if (W->cd_probe[k] >= 0) A.prec_cand[W->pbase + W->eprec[e]] = (int32_t)ci;
         }
     }
+    PMARK(12);
 }
 
 // persistent: each warp walks the device-resident frontier

@@ -173,7 +173,9 @@ __global__ void k_take(IterState I) {
         if (nR > lim) nR = lim;
         c[C_STALL] = (want > 0 && nR == 0) ? 1ull : 0ull;
         c[C_NR] = (unsigned long long)nR;
-        c[C_NX] = 0; c[C_NF] = 0; c[C_NPROBE] = 0; c[C_NEMIT] = 0; c[C_NLOCAL] = 0;
+        // C_NPROBE is not reset: exact probe evaluations accumulate across iterations and are
+        // flushed by the host loop (probe_flush) outside the per-iteration graph
+        c[C_NX] = 0; c[C_NF] = 0; c[C_NEMIT] = 0; c[C_NLOCAL] = 0;
         c[C_NPREC] = 0; c[C_NKEEP] = 0; c[C_NPLOCAL] = 0; c[C_FCURSOR] = 0;
         c[C_ITER] += nR > 0 ? 1ull : 0ull;
         s_nR = nR;
@@ -425,7 +427,6 @@ __global__ void k_pend_finalize(unsigned long long* ctr) {
     pdl_enter();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         ctr[C_PREC_TOTAL] += ctr[C_NPREC];
-        ctr[C_PROBES_TOTAL] += ctr[C_NPROBE];   // (may overshoot the buffer; capped where consumed)
         ctr[C_NPEND] = ctr[C_NKEEP];
         ctr[C_PPAR] ^= 1ull;
     }
@@ -454,6 +455,19 @@ void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf
     launch_k(k_resolve, grid_for(cap, 256),  256,  0,  s, R, H, val_buf, ctr, cap, probe_pts, probe_shape, cap_probe);
 }
 void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s) { launch_k(k_pend_finalize, 1, 32, 0, s, ctr); }
+
+// after a probe flush: the evaluated probes leave the buffer
+__global__ void k_probe_done(unsigned long long* ctr, long long cap_probe) {
+    pdl_enter();
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const unsigned long long n = ctr[C_NPROBE];
+        ctr[C_PROBES_TOTAL] += n < (unsigned long long)cap_probe ? n : (unsigned long long)cap_probe;
+        ctr[C_NPROBE] = 0;
+    }
+}
+void launch_probe_done(unsigned long long* ctr, int64_t cap_probe, cudaStream_t s) {
+    launch_k(k_probe_done, 1, 32, 0, s, ctr, (long long)cap_probe);
+}
 void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, int shape_w,
                       const int32_t* shapes, int value, cudaStream_t s) {
     launch_k(k_zero_keys, grid_for(cap * KW, 256),  256,  0,  s, keys, n_dev, KW, cap, shape_w, shapes, value);

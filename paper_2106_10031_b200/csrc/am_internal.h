@@ -207,6 +207,7 @@ void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t
 void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr,
                     int64_t cap, double* probe_pts, int32_t* probe_shape, int64_t cap_probe, cudaStream_t s);
 void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s);
+void launch_probe_done(unsigned long long* ctr, int64_t cap_probe, cudaStream_t s);
 void launch_take(const IterState& I, cudaStream_t s);
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
                          const unsigned long long* n_dev, int64_t n_cap, int KW, uint64_t* ckey, double* ckey_hint,

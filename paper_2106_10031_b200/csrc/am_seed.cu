@@ -100,6 +100,15 @@ __global__ void k_midpoint(const double* a, const double* b, double* m, int64_t 
 void launch_midpoint(const double* a, const double* b, double* m, int64_t n, cudaStream_t s) {
     if (n > 0) { launch_k(k_midpoint, (unsigned)((n * 3 + 127) / 128), 128, 0, s, a, b, m, n); }
 }
+// hint records (x, y, z, reach) of points that lie in their cells (seeds)
+__global__ void k_point_hints(const double* X, int64_t n, double tau, double* hints) {
+    pdl_enter();
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) reinterpret_cast<double4*>(hints)[i] = make_double4(X[i * 3], X[i * 3 + 1], X[i * 3 + 2], tau);
+}
+void launch_point_hints(const double* X, int64_t n, double tau, double* hints, cudaStream_t s) {
+    if (n > 0) { launch_k(k_point_hints, (unsigned)((n + 127) / 128), 128, 0, s, X, n, tau, hints); }
+}
 __global__ void k_count_active(const int32_t* active, int64_t n, unsigned long long* cnt) {
     pdl_enter();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -47,3 +47,9 @@ if d[0]:
     print(f"hint: have {d[13]/n:.3f} x0-violates {d[9]/n:.3f} near>NMAX {d[10]/n:.3f} reach-fail {d[11]/n:.3f} "
           f"near rows {d[12]/max(1, d[13]):.1f}")
     print("cycle histogram (log2):", {int(2**i): int(d[16 + i]) for i in range(24) if d[16 + i]})
+if d[0]:
+    names = ["setup", "stream", "near-rows", "clip", "accept+C'", "full-path", "pairs", "dedup", "order", "edges",
+             "emit-count", "emit-records", "emit-keys"]
+    tot = sum(float(d[40 + i]) for i in range(13))
+    print("phase cycles per cell:", {nm: round(float(d[40 + i]) / n) for i, nm in enumerate(names)},
+          f"sum {tot / n:.0f}")
