@@ -128,7 +128,10 @@ struct am_engine {
     DBuf<uint32_t> pool_flags;
     DBuf<int32_t> queue, pool_vn;
     DBuf<int64_t> pool_voff;
-    DBuf<double> pool_hint, ckey_hint, emit_hint;
+    DBuf<double> pool_hint, ckey_hint, emit_hint, near_row;
+    DBuf<int32_t> near_n, near_flags, near_id;   // k_near lists per frontier entry
+    int near_cap = 128;
+    double tau_mult = 1.0, near_reach = 4.0;   // face-solver reach (tuning: AM_TAU_MULT, AM_NEAR_REACH)
     DBuf<unsigned long long> dbg;   // face-kernel instrumentation counters (AM_FACE_STATS builds)
     uint64_t tcap = 0;
     // counters (device) + host mirror
@@ -503,6 +506,13 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->emit_pool.reserve(e->E, s));
     CK(e->emit_hint.reserve(e->E * 4, s));
     CK(e->ckey_hint.reserve(e->B * 4, s));
+    if (const char* v = getenv("AM_TAU_MULT")) e->tau_mult = atof(v);
+    if (const char* v = getenv("AM_NEAR_REACH")) e->near_reach = atof(v);
+    if (const char* v = getenv("AM_NEAR_CAP")) e->near_cap = atoi(v);
+    CK(e->near_n.reserve(e->B, s));
+    CK(e->near_flags.reserve(e->B, s));
+    CK(e->near_id.reserve(e->B * e->near_cap, s));
+    CK(e->near_row.reserve(e->B * e->near_cap * 4, s));
     CK(e->prec_cand.reserve(e->PR, s));
     CK(e->prec_k.reserve(e->PR, s));
     CK(e->prec_pt.reserve(e->PR * 3, s));
@@ -531,7 +541,7 @@ extern "C" int am_engine_destroy(am_engine* e) {
     if (e->graph) cudaGraphDestroy(e->graph);
     DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx, &e->shint,
                            &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1], &e->pool_hint,
-                           &e->ckey_hint, &e->emit_hint, &e->s_verts, &e->shape_tab};
+                           &e->ckey_hint, &e->emit_hint, &e->s_verts, &e->shape_tab, &e->near_row};
     for (auto* b : dbl) b->release(e->stream);
     DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->ckey, &e->slot, &e->slot2, &e->scratch, &e->outbox,
                              &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres, &e->pkeys, &e->pslot, &e->s_keys};
@@ -541,6 +551,7 @@ extern "C" int am_engine_destroy(am_engine* e) {
                             &e->cell_nv, &e->edge_nrefs, &e->edge_refs, &e->hstatus, &e->sact, &e->sdone,
                             &e->pool_vn, &e->pstatus, &e->emit_dup, &e->emit_pool, &e->prec_cand, &e->prec_k,
                             &e->pend_t[0], &e->pend_t[1], &e->pend_k[0], &e->pend_k[1], &e->val_buf, &e->s_nv,
+                            &e->near_n, &e->near_flags, &e->near_id,
                             &e->probe_shape, &e->prec_s, &e->pend_s[0], &e->pend_s[1],
                             &e->s_enr, &e->s_refs};
     for (auto* b : i32) b->release(e->stream);
@@ -771,7 +782,11 @@ static int launch_iteration(am_engine* e) {
     a.pool_vn = e->pool_vn.p; a.pool_voff = e->pool_voff.p;
     a.dbg = e->dbg.p;
     a.cursor = c + C_FCURSOR;
+    a.near_cap = e->near_cap; a.near_n = e->near_n.p; a.near_flags = e->near_flags.p;
+    a.near_id = e->near_id.p; a.near_row = e->near_row.p;
+    a.tau_mult = e->tau_mult; a.near_reach = e->near_reach;
     if (tm) cudaEventRecord(e->ev[2], s);
+    launch_near(a, s);
     launch_face(a, s);
     if (tm) cudaEventRecord(e->ev[3], s);
     // flips: insert (local) and queue the new states

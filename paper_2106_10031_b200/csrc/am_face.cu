@@ -57,6 +57,7 @@ constexpr int NMAX = 96;   // hinted path: rows near the hint point
 constexpr double kCDelta = 1e-10;
 constexpr double kValMargin = 1e-11;   // sign margin (unit and raw values) for probe validation
 constexpr double kTinyNorm = 1e-6;     // rows this thin make validation unreliable
+constexpr int kNearValid = 1, kNearX0Bad = 2, kNearRisky = 4, kNearOverflow = 8;
 
 // phase-private scratch: near rows (hinted clipping) and polygon assembly never overlap
 struct NearPhase {
@@ -433,7 +434,15 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     unsigned long long core = 0;
     int risky = 0;
     const double band = tol_max + 1.5 * A.probe_delta + 1e-9;
-    double tau = hint.w;
+    double tau = A.tau_mult * hint.w;
+    // near list from k_near (rows within `reach` of x0): attempts with tau <= reach filter it
+    // instead of streaming every row again
+    const int list_flags = (A.near_flags && have_hint) ? A.near_flags[fi] : 0;
+    const bool use_list = (list_flags & kNearValid) && !(list_flags & kNearOverflow);
+    const int n_list = use_list ? A.near_n[fi] : 0;
+    const double reach = A.near_reach * hint.w;
+    FSTAT(14, use_list ? 1 : 0);
+    FSTAT(15, (list_flags & kNearOverflow) ? 1 : 0);
     PMARK(0);
     for (int attempt = 0; attempt < 5 && status == 0 && have_hint && !hinted_done; attempt++) {
         const double x0[3] = {hint.x, hint.y, hint.z};
@@ -441,6 +450,34 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         double dmax_seen = 0.0;
         int nn = 0;
         bool ok = true;
+        if (use_list && tau <= reach) {
+            // the near kernel's list (rows within `reach` of x0, ascending ids): same test, tighter lim
+            const int64_t lb = fi * (int64_t)A.near_cap;
+#pragma unroll 1
+            for (int base = 0; base < n_list; base += 32) {
+                const int j = base + lane;
+                bool near = false;
+                int gr = 0;
+                double4 rr = make_double4(0.0, 0.0, 0.0, 0.0);
+                if (j < n_list) {
+                    gr = A.near_id[lb + j];
+                    rr = reinterpret_cast<const double4*>(A.near_row)[lb + j];
+                    const double n2 = (rr.x * rr.x + rr.y * rr.y) + rr.z * rr.z;
+                    double v = ((rr.x * x0[0] + rr.y * x0[1]) + rr.z * x0[2]) + rr.w;
+                    if (gr < c.NB && key_bit(c.key, gr)) v = -v;
+                    near = v >= 0.0 || v * v <= lim * lim * n2;
+                }
+                const unsigned mask = __ballot_sync(full, near);
+                const int pos = nn + __popc(mask & ((1u << lane) - 1u));
+                if (near && pos < NMAX) {
+                    W->u.np.nl[pos] = gr;
+                    W->cn[pos][0] = rr.x; W->cn[pos][1] = rr.y; W->cn[pos][2] = rr.z; W->cn[pos][3] = rr.w;
+                }
+                nn += __popc(mask);
+            }
+            ok = !(list_flags & kNearX0Bad);
+            risky = (list_flags & kNearRisky) ? 1 : 0;
+        } else {
         RawRow nx1 = load_raw(c, lane), nx2 = load_raw(c, lane + 32);
         for (int base = 0; base < c.K; base += 32) {
             const int gr = base + lane;
@@ -466,6 +503,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
                 W->cn[pos][0] = rr.x; W->cn[pos][1] = rr.y; W->cn[pos][2] = rr.z; W->cn[pos][3] = rr.c;
             }
             nn += __popc(mask);
+        }
         }
         PMARK(1);
         bool x0ok = __all_sync(full, ok);
@@ -1162,6 +1200,100 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         }
     }
     PMARK(12);
+}
+
+// Near lists: one warp per frontier cell streams every constraint row once (coalesced 32 B
+// rows of the composition buffer, the same test as the face solver's hinted pass) and keeps the
+// rows within reach = near_reach x the hint radius of the hint point, in ascending id order,
+// with their raw functionals.  Full-occupancy warps keep many row loads in flight; the face
+// solver then filters ~tens of listed rows per attempt instead of streaming all K rows.
+__global__ void __launch_bounds__(256) k_near(FaceArgs A) {
+    pdl_enter();
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const int64_t n = dev_count(A.n_dev, A.n_cap);
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t fi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; fi < n; fi += nw) {
+        const int item = A.items[fi];
+        Ctx c;
+        c.Z = A.Z + (int64_t)item * A.zs * 4;
+        c.faces = A.faces + (int64_t)item * A.M * 4;
+        c.key = A.keys + (int64_t)item * A.KW;
+        c.NB = A.NB; c.M = A.M; c.ensemble = A.ensemble;
+        c.branch = A.ensemble ? (int)c.key[A.KW - 1] : 0;
+        c.K = A.NB + A.M + 6;
+        for (int k = 0; k < 3; k++) { c.lo[k] = A.lo[k]; c.hi[k] = A.hi[k]; }
+        // face plane and projected hint point: the face solver's arithmetic
+        const double* fr = c.faces + c.branch * 4;
+        const double fn = sqrt((fr[0] * fr[0] + fr[1] * fr[1]) + fr[2] * fr[2]);
+        double fu[3] = {0, 0, 0}, fo = 0.0;
+        bool face_ok = fn > kDegen;
+        if (face_ok) {
+            fu[0] = fr[0] / fn; fu[1] = fr[1] / fn; fu[2] = fr[2] / fn; fo = fr[3] / fn;
+            face_ok = sqrt((fu[0] * fu[0] + fu[1] * fu[1]) + fu[2] * fu[2]) > kDegen;
+        }
+        double4 hint = reinterpret_cast<const double4*>(A.hints)[item];
+        if (!(isfinite(hint.w) && face_ok)) {
+            if (lane == 0) A.near_flags[fi] = 0;
+            continue;
+        }
+        const double hd = ((fu[0] * hint.x + fu[1] * hint.y) + fu[2] * hint.z) + fo;
+        hint.x -= hd * fu[0]; hint.y -= hd * fu[1]; hint.z -= hd * fu[2];
+        const double x0[3] = {hint.x, hint.y, hint.z};
+        const double band = fmax(A.tol_cell, A.tol_onplane) + 1.5 * A.probe_delta + 1e-9;
+        const double lim = A.near_reach * hint.w + band + 1e-9;
+        const int64_t lb = fi * (int64_t)A.near_cap;
+        int nn = 0, risky = 0;
+        bool ok = true;
+        RawRow nx1 = load_raw(c, lane), nx2 = load_raw(c, lane + 32);
+        for (int base = 0; base < c.K; base += 32) {
+            const int gr = base + lane;
+            const RawRow rr = nx1;
+            nx1 = nx2;
+            if (base + 64 < c.K) nx2 = load_raw(c, gr + 64);
+            bool near = false;
+            if (gr < c.K && rr.kind >= 0) {
+                const double n2 = (rr.x * rr.x + rr.y * rr.y) + rr.z * rr.z;
+                if (rr.kind == 0 && n2 > 0.0 && n2 < kTinyNorm * kTinyNorm) risky = 1;
+                if (rr.kind == 1 && n2 < kTinyNorm * kTinyNorm) risky = 1;
+                if (rr.kind == 2 || n2 > kDegen * kDegen) {
+                    double v = ((rr.x * x0[0] + rr.y * x0[1]) + rr.z * x0[2]) + rr.c;
+                    if (rr.kind == 0 && key_bit(c.key, gr)) v = -v;
+                    if (v > 0.0 && v * v > 1e-18 * n2) ok = false;   // x0 violates the row by > 1e-9
+                    near = v >= 0.0 || v * v <= lim * lim * n2;
+                }
+            }
+            const unsigned mask = __ballot_sync(full, near);
+            const int pos = nn + __popc(mask & ((1u << lane) - 1u));
+            if (near && pos < A.near_cap) {
+                A.near_id[lb + pos] = gr;
+                reinterpret_cast<double4*>(A.near_row)[lb + pos] = make_double4(rr.x, rr.y, rr.z, rr.c);
+            }
+            nn += __popc(mask);
+        }
+        ok = __all_sync(full, ok);
+        risky = __any_sync(full, risky);
+        if (lane == 0) {
+            A.near_n[fi] = nn < A.near_cap ? nn : A.near_cap;
+            A.near_flags[fi] = kNearValid | (ok ? 0 : kNearX0Bad) | (risky ? kNearRisky : 0) |
+                               (nn > A.near_cap ? kNearOverflow : 0);
+        }
+    }
+}
+
+void launch_near(const FaceArgs& a, cudaStream_t s) {
+    if (a.n_cap <= 0 || !a.near_flags) return;
+    int64_t warps = a.n_cap;
+    static int grid_max = 0;
+    if (!grid_max) {
+        int per_sm = 0, dev = 0, sms = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near, 256, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid_max = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    int64_t blocks = (warps + 7) / 8;
+    launch_k(k_near, (unsigned)(blocks < grid_max ? blocks : grid_max), 256, 0, s, a);
 }
 
 // persistent: each warp walks the device-resident frontier

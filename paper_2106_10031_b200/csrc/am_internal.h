@@ -285,10 +285,19 @@ struct FaceArgs {
     int64_t* pool_voff;
     unsigned long long* dbg;   // instrumentation (AM_FACE_STATS builds), may be null
     unsigned long long* cursor;   // work-distribution counter (zeroed by k_take each iteration)
+    // near lists (k_near -> k_face), per frontier entry: count, flags, ids and raw rows
+    int near_cap;
+    double tau_mult;          // first hinted attempt: reach = tau_mult x the hint radius
+    double near_reach;        // near lists cover near_reach x the hint radius
+    int32_t* near_n;
+    int32_t* near_flags;
+    int32_t* near_id;         // [n_cap][near_cap]
+    double* near_row;         // [n_cap][near_cap][4]
 };
 constexpr int kEmitFlipsPerCell = 48;   // face kernel EMAXC
 constexpr int kVertsPerCell = 64;       // face kernel QMAX
 constexpr int kRefsPerCell = 256;
 void launch_face(const FaceArgs& a, cudaStream_t s);
+void launch_near(const FaceArgs& a, cudaStream_t s);
 
 }  // namespace am

@@ -45,7 +45,7 @@ if d[0]:
     print(f"face stats: cells {int(n)} clips1 {d[1]/n:.2f} clips2 {d[2]/n:.2f} C' {d[3]/n:.2f} raw verts {d[4]/n:.2f} "
           f"verts {d[5]/n:.2f} cycles {d[6]/n:.0f} (max {int(d[8])}) hinted {d[7]/n:.2f}")
     print(f"hint: have {d[13]/n:.3f} x0-violates {d[9]/n:.3f} near>NMAX {d[10]/n:.3f} reach-fail {d[11]/n:.3f} "
-          f"near rows {d[12]/max(1, d[13]):.1f}")
+          f"near rows {d[12]/max(1, d[13]):.1f} | near list used {d[14]/n:.3f} overflow {d[15]/n:.4f}")
     print("cycle histogram (log2):", {int(2**i): int(d[16 + i]) for i in range(24) if d[16 + i]})
 if d[0]:
     names = ["setup", "stream", "near-rows", "clip", "accept+C'", "full-path", "pairs", "dedup", "order", "edges",
