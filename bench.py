@@ -312,11 +312,13 @@ def main():
             e_times.append((t2 - t0) * 1e3)
             m_times.append((t1 - t0) * 1e3)
             blob = to_blob(net)
-            # inputs: parameters, step/sub tables, seed-trigger sample points (64 x 64 pairs)
-            h2d = (blob.params.nbytes + blob.steps.nbytes + blob.subs.nbytes + args.seeds * 64 * 2 * 3 * 8
-                   + r.verts.nbytes + 2 * 8 * (len(r.nverts) + 1))
-            d2h = (r.keys.nbytes + r.nverts.nbytes + r.verts.nbytes + r.edge_nrefs.nbytes + r.edge_refs.nbytes // 2
-                   + mesh.vertices.nbytes + sum(f.nbytes for f in mesh.faces))
+            # inputs: parameters (weights + padded copies), step/sub tables, the trigger's sample
+            # points (64 per seed) and bisection pairs; the soup stays in HBM for the weld
+            h2d = (2 * blob.params.nbytes + blob.steps.nbytes + blob.subs.nbytes + args.seeds * 64 * 3 * 8
+                   + args.seeds * 2 * 3 * 8)
+            # outputs: the sorted march result and the welded mesh
+            d2h = (r.keys.nbytes + r.nverts.nbytes + r.verts.nbytes + r.edge_nrefs.nbytes + r.edge_refs.nbytes
+                   + mesh.vertices.nbytes + mesh.face_off.nbytes + mesh.face_idx.nbytes)
         e_ms = float(np.mean(e_times))
         e2e = {"value": r.report.cells_visited / (e_ms * 1e-3), "unit": "cells/s", "ms_per_step": e_ms,
                "mesh_time_s": e_ms * 1e-3, "march_only_ms": float(np.mean(m_times)),

@@ -20,6 +20,7 @@ import numpy as np
 
 from .engine import PROBE_DELTA, TOL_CELL, TOL_ONPLANE, TOL_WELD, Engine, architecture_key
 from .network import AffinePlane, AnyNetwork, EnsembleSpec, StateVector, subnetworks, to_blob
+from .meshes import to_host
 from .seeding import sample_seeds
 
 DEFAULT_BBOX = ((-1.2, -1.2, -1.2), (1.2, 1.2, 1.2))   # reference cells.py:37
@@ -148,6 +149,9 @@ class MarchResult:
     n_bits: int
     seeds: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
     _polys: list | None = None
+    # device copies of (nverts, verts) kept by march() so welded_mesh() welds in HBM without
+    # sending the soup back to the GPU (None: host arrays only)
+    _dev: tuple | None = field(default=None, repr=False)
 
     @property
     def has_face(self) -> np.ndarray:
@@ -185,8 +189,21 @@ class MarchResult:
 
     def welded_mesh(self, tol: float = TOL_WELD):
         """reference marching.py:126-127 weld(polygon_soup(), tol), welded on the GPU straight
-        from the CSR soup (no per-loop Python objects on the way in)."""
-        from .meshes import PolygonMesh, weld_arrays
+        from the CSR soup (no per-loop Python objects on the way in).  A result of march() still
+        holds its soup in HBM: the loops are formed and welded there and only the welded mesh
+        comes back."""
+        from .meshes import PolygonMesh, weld_arrays, weld_device, to_host
+        if self._dev is not None:
+            import torch
+            dn, dv = self._dev
+            nv = dn[dn > 0].to(torch.int64)
+            off = torch.zeros(nv.numel() + 1, dtype=torch.int64, device=dv.device)
+            torch.cumsum(nv, 0, out=off[1:])
+            idx = torch.arange(dv.shape[0], dtype=torch.int64, device=dv.device)
+            kept, foff, fidx, _, _, nd = weld_device(dv, off, idx, tol)
+            kept_h, foff_h = to_host([kept, foff])
+            (fidx_h,) = to_host([fidx[:int(foff_h[-1])]])
+            return PolygonMesh(kept_h, None, None, nd, face_off=foff_h, face_idx=fidx_h)
         nv = self.nverts[self.nverts > 0].astype(np.int64)
         off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
         kept, foff, fidx, _, nd = weld_arrays(self.verts, off, np.arange(off[-1], dtype=np.int64), tol)
@@ -222,6 +239,7 @@ def device_results_to_host(eng: Engine):
     key word (C,) or None, nverts, verts, edge_nrefs, edge_refs (R, 2) (kind, index))."""
     import torch
     c, keys, nverts, verts, enr, erefs = eng.results_device()
+    eng.last_results_device = (c, keys, nverts, verts, enr, erefs)
     b = eng.blob
     nb, ns = b.n_bits, b.n_subs
     bw, nbytes = (nb + 63) // 64, (nb + 7) // 8
@@ -234,31 +252,27 @@ def device_results_to_host(eng: Engine):
     branch = keys[:, bw] if b.ensemble else None
     shape = keys[:, eng.kw - 1] if getattr(eng, "n_shapes", 1) > 1 else None
 
-    def host(t):
-        # small arrays: pinned staging (fast async copy); large ones: pinning fresh memory costs
-        # more than the staged pageable copy (~0.5 s per GB), so copy straight to pageable memory
-        if t.numel() * t.element_size() > (64 << 20):
-            return t.cpu()
-        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-        out.copy_(t, non_blocking=True)
-        return out
-    arrs = [host(t.contiguous()) for t in (kbytes, nverts, verts, enr, refs)]
-    br = host(branch) if branch is not None else None
-    sh = host(shape) if shape is not None else None
-    torch.cuda.current_stream(eng.dev).synchronize()
-    hk, hn, hv, he, hr = (a.numpy() for a in arrs)
-    hbr = br.numpy().astype(np.int64) if br is not None else np.full(n, -1, np.int64)
-    return c, hk, hbr, (sh.numpy() if sh is not None else None), hn, hv, he, hr
+    ts = [kbytes, nverts, verts, enr, refs] + [t for t in (branch, shape) if t is not None]
+    hk, hn, hv, he, hr, *rest = to_host(ts)
+    br = rest.pop(0) if branch is not None else None
+    sh = rest.pop(0) if shape is not None else None
+    hbr = br.astype(np.int64) if br is not None else np.full(n, -1, np.int64)
+    return c, hk, hbr, sh, hn, hv, he, hr
 
 
-def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, threads: int = 1) -> MarchResult:
+def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, threads: int = 1,
+                   keep_device: bool = False) -> MarchResult:
     """Sorted results (GPU sort + gathers, am_result_copy_device), converted to the reference's
     representations on the device, one pinned copy per array."""
     c, kb, branch, _, hn, hv, he, hr = device_results_to_host(eng)
+    dev = None
+    if keep_device:
+        _, _, dn, dv, _, _ = eng.last_results_device
+        dev = (dn, dv)
     rep = MarchReport(cells_visited=c["cells"], faces_emitted=c["faces"], empty_faces=c["empty"],
                       open_edges=c["open_edges"], seconds=time.perf_counter() - t0, seeds_used=len(seeds),
                       capped=bool(c["capped"]), threads=threads, waves=waves, overflow=c["overflow"])
-    return MarchResult(kb, branch, hn, hv, he, hr, rep, eng.blob.n_bits, seeds)
+    return MarchResult(kb, branch, hn, hv, he, hr, rep, eng.blob.n_bits, seeds, _dev=dev)
 
 
 _ENGINES: "OrderedDict[tuple, Engine]" = OrderedDict()
@@ -304,7 +318,7 @@ def march(net: AnyNetwork, config: MarchConfig | None = None, engine: Engine | N
         seeds = sample_seeds(eng, config.seeds, config.bbox, scheme=config.scheme, rng_seed=config.rng_seed)
     eng.seed(seeds)
     waves = eng.run()
-    res = collect_result(eng, seeds, t0, waves, config.threads)
+    res = collect_result(eng, seeds, t0, waves, config.threads, keep_device=True)
     if res.report.faces_emitted <= config.unique_planes_limit:
         res.report.unique_plane_violations = None   # diagnostic not computed on the GPU path
     return res
