@@ -84,6 +84,11 @@ int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t col
 }
 
 // -------------------------------------------------------- bit utilities
+// state bit read through L2: the fused composition kernel updates canonical bits with atomics
+// (performed at L2) and reads them back in later layers of the same launch
+__device__ __forceinline__ int key_bit_cg(const uint64_t* k, int i) {
+    return (int)((__ldcg(k + (i >> 6)) >> (63 - (i & 63))) & 1ull);
+}
 __device__ __forceinline__ void set_key_bit(uint64_t* key, int row, int bit) {
     uint64_t m = key_mask(row);
     if (bit) atomicOr(reinterpret_cast<unsigned long long*>(key + (row >> 6)), (unsigned long long)m);
@@ -228,11 +233,13 @@ __device__ __forceinline__ void cp_async_wait(int pending) {
     }
 }
 // 32 state bits of rows [row, row + 32) (MSB-first key words), bit j = row + j; zero beyond `valid`
+// (G: key in global memory, read through L2; else the tile's shared-memory word cache)
+template <bool G = false>
 __device__ __forceinline__ uint32_t bits32(const uint64_t* key, int row, int valid) {
     if (valid <= 0) return 0u;
     int w = row >> 6, off = row & 63;
-    uint64_t hi = key[w] << off;                        // bit 63 of hi = state bit of `row`
-    if (off > 32 && valid > 64 - off) hi |= key[w + 1] >> (64 - off);
+    uint64_t hi = (G ? __ldcg(key + w) : key[w]) << off;   // bit 63 of hi = state bit of `row`
+    if (off > 32 && valid > 64 - off) hi |= (G ? __ldcg(key + w + 1) : key[w + 1]) >> (64 - off);
     uint32_t m = __brev((uint32_t)(hi >> 32));
     if (valid < 32) m &= (1u << valid) - 1u;
     return m;
@@ -272,7 +279,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                 const int sg = q / (NI * KCW), rem = q % (NI * KCW), il = rem / KCW, w = rem % KCW;
                 const int64_t item = item0 + il;
                 uint64_t v = 0;
-                if (item < n && w < wcnt[sg]) v = keys[item * L.KW + wbeg[sg] + w];
+                if (item < n && w < wcnt[sg]) v = __ldcg(keys + item * L.KW + wbeg[sg] + w);
                 S.kc[sg][il][w] = v;
             }
         }
@@ -309,7 +316,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                     const int sg = seg0 ? 0 : 1;
                     S.mask[stage][tid] = item >= n ? 0u
                         : cache_ok ? bits32(S.kc[sg][tid], src_row + k0 - wbeg[sg] * 64, valid)
-                                   : bits32(keys + item * L.KW, src_row + k0, valid);
+                                   : bits32<true>(keys + item * L.KW, src_row + k0, valid);
                 }
             } else {
 #pragma unroll
@@ -324,7 +331,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                     const int sg = seg0 ? 0 : 1;
                     S.mask[stage][tid] = item >= n ? 0u
                         : cache_ok ? bits32(S.kc[sg][tid], src_row + k0 - wbeg[sg] * 64, valid)
-                                   : bits32(keys + item * L.KW, src_row + k0, valid);
+                                   : bits32<true>(keys + item * L.KW, src_row + k0, valid);
                 }
             }
             cp_async_commit();
@@ -418,7 +425,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
                             } else if (sc_ident) {        // masked block input rows
                                 const uint64_t* key = keys + item * L.KW;
                                 int srow = st.sin_row_off + r;
-                                if (key_bit(key, srow)) {
+                                if (key_bit_cg(key, srow)) {
                                     double2 p = *reinterpret_cast<const double2*>(L.Z + (item * L.zs + srow) * 4 + comp);
                                     s0 = p.x; s1 = p.y;
                                 }
@@ -553,6 +560,87 @@ void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const
         if (!init) { cudaFuncSetAttribute(k_gemm_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
         { launch_k(k_gemm_step<1>, (unsigned)grid, kThreads, smem, s, *tmW, tmV ? *tmV : *tmW, L); }
     }
+}
+
+// ------------------------------------------------- fused composition (all steps)
+// One launch composes every step of a batch of cells and their face functionals: a CTA owns a
+// block of 16 cells (64 columns) and walks the steps in order -- the input step elementwise,
+// each hidden step as its 64-row output tiles (gemm_tile: TMA-staged W, DMMA, epilogue) -- with
+// a barrier between steps, then the heads.  Every step's K extent is the previous steps' rows of
+// the same cells, all produced by this CTA, so no grid-wide dependency exists and the ~L+2
+// per-layer launches of a BFS iteration (each paying its own pipeline fill) become one.
+__global__ void __launch_bounds__(kThreads, 2) k_compose_fused(const __grid_constant__ FusedCompose F) {
+    pdl_enter();
+    extern __shared__ uint8_t smem_raw[];
+    GemmSmem<4>& S = *reinterpret_cast<GemmSmem<4>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = dev_count(F.L.n_dev, F.L.n_cap);
+    if (n <= 0) return;
+    uint64_t* keys = keys_at(F.L);
+    if (tid < NST) mbar_init(&S.bar[tid], 1);
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const int64_t nblk = (n * 4 + BN - 1) / BN;
+    uint32_t gchunk = 0;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t n0 = blk * BN, item0 = n0 / 4;
+        for (int s = 0; s < F.nsteps; s++) {
+            LayerLaunch L = F.L;
+            L.st = F.st[s];
+            if (L.st.flags & AM_STEP_FIRST) {
+                const int no = L.st.n_out;
+                for (int idx = tid; idx < 16 * no; idx += kThreads) {
+                    const int64_t item = item0 + idx / no;
+                    if (item < n) input_elem<4>(L, keys, item, idx % no);
+                }
+            } else {
+                for (int m0 = 0; m0 < L.st.n_out; m0 += BM)
+                    gemm_tile<4>(S, L, keys, n, &F.tmW[s], F.tmV_ok[s] ? &F.tmV[s] : &F.tmW[s], m0, n0, gchunk);
+            }
+            __threadfence();
+            __syncthreads();
+        }
+        // face functional of every subnetwork (reference network.py:440-442), warp per (cell, sub)
+        for (int wid = warp; wid < 16 * F.n_subs; wid += kThreads / 32) {
+            const int64_t item = item0 + wid / F.n_subs;
+            const int j = wid % F.n_subs;
+            if (item >= n) continue;
+            const SubDev sd = F.subs[j];
+            const uint64_t* key = keys + item * F.L.KW;
+            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            for (int r = lane; r < sd.last_n; r += 32) {
+                const int row = sd.last_row + r;
+                if (!key_bit_cg(key, row)) continue;
+                const double2* p = reinterpret_cast<const double2*>(F.L.Z + (item * F.L.zs + row) * 4);
+                const double2 x = p[0], y = p[1];
+                const double w = sd.hw[r];
+                a0 += w * x.x; a1 += w * x.y; a2 += w * y.x; a3 += w * y.y;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+                a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+                a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+            }
+            if (lane == 0) {
+                double* f = F.faces + (item * F.n_subs + j) * 4;
+                f[0] = prec_round(a0, F.L.fp32); f[1] = prec_round(a1, F.L.fp32); f[2] = prec_round(a2, F.L.fp32);
+                f[3] = prec_round(a3 + head_bias(sd, item_shape(key, F.L.shape_w)), F.L.fp32);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+void launch_compose_fused(const FusedCompose& F, cudaStream_t s) {
+    if (F.L.n_cap <= 0) return;
+    const int64_t blocks = (F.L.n_cap * 4 + BN - 1) / BN;
+    const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms() * 2);
+    const size_t smem = sizeof(GemmSmem<4>) + 1024;
+    static bool init = false;
+    if (!init) { cudaFuncSetAttribute(k_compose_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
+    launch_k(k_compose_fused, (unsigned)grid, kThreads, smem, s, F);
 }
 
 // ------------------------------------------------------------ head kernels

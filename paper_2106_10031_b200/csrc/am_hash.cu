@@ -423,9 +423,11 @@ __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsign
     }
 }
 
-__global__ void k_pend_finalize(unsigned long long* ctr) {
+// (has_cond: also set the iteration graph's conditional probe stage: any probe to evaluate?)
+__global__ void k_pend_finalize(unsigned long long* ctr, cudaGraphConditionalHandle h, int has_cond) {
     pdl_enter();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
+        if (has_cond) cudaGraphSetConditional(h, ctr[C_NPROBE] ? 1u : 0u);
         ctr[C_PREC_TOTAL] += ctr[C_NPREC];
         ctr[C_NPEND] = ctr[C_NKEEP];
         ctr[C_PPAR] ^= 1ull;
@@ -454,17 +456,22 @@ void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf
                     double* probe_pts, int32_t* probe_shape, int64_t cap_probe, cudaStream_t s) {
     launch_k(k_resolve, grid_for(cap, 256),  256,  0,  s, R, H, val_buf, ctr, cap, probe_pts, probe_shape, cap_probe);
 }
-void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s) { launch_k(k_pend_finalize, 1, 32, 0, s, ctr); }
+void launch_pend_finalize(unsigned long long* ctr, const cudaGraphConditionalHandle* h, cudaStream_t s) {
+    launch_k(k_pend_finalize, 1, 32, 0, s, ctr, h ? *h : cudaGraphConditionalHandle{}, h ? 1 : 0);
+}
 
-// after a probe flush: the evaluated probes leave the buffer
+// after a probe stage: the evaluated probes leave the buffer
 __global__ void k_probe_done(unsigned long long* ctr, long long cap_probe) {
     pdl_enter();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         const unsigned long long n = ctr[C_NPROBE];
         ctr[C_PROBES_TOTAL] += n < (unsigned long long)cap_probe ? n : (unsigned long long)cap_probe;
+        ctr[C_NFLUSH] += n ? 1ull : 0ull;
         ctr[C_NPROBE] = 0;
     }
 }
+
+
 void launch_probe_done(unsigned long long* ctr, int64_t cap_probe, cudaStream_t s) {
     launch_k(k_probe_done, 1, 32, 0, s, ctr, (long long)cap_probe);
 }

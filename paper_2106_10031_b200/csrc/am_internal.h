@@ -148,6 +148,21 @@ int assemble_results(const uint64_t* keys, const int32_t* cell_nv, const int64_t
 
 // kernels' host-side launchers (am_compose.cu)
 void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s);
+
+// every step of a composition in one launch (k_compose_fused)
+constexpr int kMaxFusedSteps = 24;
+struct FusedCompose {
+    CUtensorMap tmW[kMaxFusedSteps];
+    CUtensorMap tmV[kMaxFusedSteps];
+    StepDev st[kMaxFusedSteps];
+    int tmV_ok[kMaxFusedSteps];
+    LayerLaunch L;          // common fields (L.st unused)
+    int nsteps;
+    double* faces;          // [items][n_subs][4]
+    const SubDev* subs;
+    int n_subs;
+};
+void launch_compose_fused(const FusedCompose& F, cudaStream_t s);
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV,
                       cudaStream_t s);
 int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld_elems);
@@ -156,7 +171,7 @@ int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t col
 enum Ctr {
     C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_OVF0, C_OVF1, C_CAPPED, C_TOTAL, C_QHEAD, C_QTAIL, C_NR, C_NX,
     C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_NPREC, C_NPEND, C_PPAR,
-    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_N
+    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_NFLUSH, C_N
 };
 
 // hash set (am_hash.cu)
@@ -206,7 +221,7 @@ void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t
                         unsigned long long* ctr, int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s);
 void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr,
                     int64_t cap, double* probe_pts, int32_t* probe_shape, int64_t cap_probe, cudaStream_t s);
-void launch_pend_finalize(unsigned long long* ctr, cudaStream_t s);
+void launch_pend_finalize(unsigned long long* ctr, const cudaGraphConditionalHandle* h, cudaStream_t s);
 void launch_probe_done(unsigned long long* ctr, int64_t cap_probe, cudaStream_t s);
 void launch_take(const IterState& I, cudaStream_t s);
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,

@@ -75,6 +75,27 @@ def _trace(eng, x0: np.ndarray, scheme: str, seed_tol: float):
     return out, iters
 
 
+_BLOCKS: dict = {}
+_BLOCKS_MAX = 1 << 16
+
+
+def _sample_block(rng_seed: int, index: int, rnd: int, lo: np.ndarray, hi: np.ndarray) -> np.ndarray:
+    """The rnd-th (64, 3) uniform draw of stream default_rng([rng_seed, index]) in [lo, hi)
+    (reference seeding.py:146-148).  The draws depend only on (rng_seed, index, rnd, box), not on
+    the network, so they are memoised: repeated marches with one configuration skip the
+    SeedSequence set-up of every stream."""
+    key = (int(rng_seed), int(index), lo.tobytes(), hi.tobytes())
+    ent = _BLOCKS.get(key)
+    if ent is None:
+        if len(_BLOCKS) >= _BLOCKS_MAX:
+            _BLOCKS.clear()
+        ent = _BLOCKS[key] = (np.random.default_rng([rng_seed, index]), [])
+    rng, blocks = ent
+    while len(blocks) <= rnd:
+        blocks.append(rng.uniform(lo, hi, size=(64, 3)))
+    return blocks[rnd]
+
+
 def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int = 0, eps: float = SEED_TOL,
                  seed_tol: float = SEED_TOL, retry_budget: int = 200, collect_iters: list | None = None) -> np.ndarray:
     """Up to ``count`` surface points, deterministic given rng_seed (reference seeding.py:123-162)."""
@@ -83,15 +104,14 @@ def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int
     validate_scheme(eng.net, scheme)
     lo = np.asarray(bbox[0], dtype=np.float64)
     hi = np.asarray(bbox[1], dtype=np.float64)
-    rngs = [np.random.default_rng([rng_seed, index]) for index in range(count)]
     found: list = [None] * count
     if scheme == "dichotomy":
         pairs: dict = {}
         pending = list(range(count))
-        for _ in range(retry_budget):
+        for rnd in range(retry_budget):
             if not pending:
                 break
-            pts = np.stack([rngs[i].uniform(lo, hi, size=(64, 3)) for i in pending])
+            pts = np.stack([_sample_block(rng_seed, i, rnd, lo, hi) for i in pending])
             vals = eng.forward(pts.reshape(-1, 3)).cpu().numpy().reshape(len(pending), 64)
             still = []
             for j, i in enumerate(pending):
@@ -110,6 +130,7 @@ def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int
             for i, p in zip(order, pts):
                 found[i] = p
     else:
+        rngs = [np.random.default_rng([rng_seed, index]) for index in range(count)]
         pending = list(range(count))
         for _ in range(retry_budget):
             if not pending:
