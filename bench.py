@@ -268,23 +268,33 @@ def main():
     pk = np.zeros(2)
     _native.check(lib.am_bench_fp64_peak(local_rank, pk.ctypes.data), "am_bench_fp64_peak")
     hbm, hbm_src = _peaks()
-    traffic = None
+    traffic = {}
     prof = os.path.join(HERE, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh)
+
+    def traffic_of(name):
+        t = traffic.get(name)
+        if not isinstance(t, dict):
+            return {"traffic": t}
+        return {"traffic": t.get("dram_bytes_per_launch"), "traffic_launch": t.get("launch"),
+                "traffic_algorithmic_bytes": t.get("algorithmic_bytes_per_launch")}
     kernels = {
         "compose_dmma": {"bound": "tensor", "achieved": comp_tf, "peak": float(pk[0]), "unit": "TFLOP/s",
                          "frac": comp_tf / pk[0] if pk[0] else None, "ms": comp_ms,
                          "peak_source": "measured fp64 DMMA microbenchmark (am_bench_fp64_peak)",
-                         "traffic": (traffic or {}).get("compose")},
+                         "kernels": "k_input_step + k_gemm_step<4> x L + k_face_head",
+                         "algorithmic": "sum_l 2 n_l n_(l-1) 4 FLOP per composed cell", **traffic_of("compose")},
         "face": {"bound": "hbm", "achieved": face_gbs, "peak": hbm, "unit": "GB/s",
                  "frac": face_gbs / hbm, "ms": face_ms, "peak_source": hbm_src,
-                 "traffic": (traffic or {}).get("face")},
+                 "kernels": "k_near + k_face (the face stage)",
+                 "algorithmic": "NB*32 + M*32 + KW*8 bytes per faced cell (planes, faces, key read once)",
+                 **traffic_of("face")},
         "probe_forward_dmma": {"bound": "tensor", "achieved": probe_tf, "peak": float(pk[0]), "unit": "TFLOP/s",
                                "frac": probe_tf / pk[0] if pk[0] else None, "ms": probe_ms,
                                "probes": s1["probes"], "peak_source": "measured fp64 DMMA microbenchmark",
-                               "traffic": (traffic or {}).get("probe")},
+                               **traffic_of("probe")},
     }
     dominant = max(kernels, key=lambda k: kernels[k]["ms"])
     roof = dict(kernels[dominant])
