@@ -307,7 +307,13 @@ def main():
     e2e = None
     if world == 1:
         cfg = marching.MarchConfig(seeds=args.seeds, rng_seed=0, bbox=bbox)
-        marching.march(net, cfg).welded_mesh()   # warm
+        # warm: engine cache and pinned host blocks, with the same result lifetimes as the timed
+        # loop (the previous step's result is alive while the next one is produced)
+        prev = None
+        for _ in range(max(args.warmup, 2)):
+            cur = marching.march(net, cfg)
+            prev = (cur, cur.welded_mesh())
+        del prev
         e_times, m_times = [], []
         h2d = d2h = 0
         from paper_2106_10031_b200.network import to_blob

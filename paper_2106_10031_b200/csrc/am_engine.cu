@@ -526,6 +526,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->ckey_hint.reserve(e->B * 4, s));
     if (const char* v = getenv("AM_TAU_MULT")) e->tau_mult = atof(v);
     if (const char* v = getenv("AM_COMPOSE_FUSED")) e->compose_fused = atoi(v) != 0;
+    if (const char* v = getenv("AM_PROBE_IN_GRAPH")) e->probe_in_graph = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_REACH")) e->near_reach = atof(v);
     if (const char* v = getenv("AM_NEAR_CAP")) e->near_cap = atoi(v);
     CK(e->near_n.reserve(e->B, s));

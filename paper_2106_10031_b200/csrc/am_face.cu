@@ -32,6 +32,7 @@
 //           (sign consistent with the canonical state, with margin); the
 //           validated neuron ids are published for the cell's pool entry.
 #include <cstdio>
+#include <cstdlib>
 
 #include "am_internal.h"
 
@@ -53,7 +54,8 @@ constexpr int VMAX = 32;   // clip polygon capacity (one lane per vertex)
 constexpr int CMAX = 64;   // candidate plane set capacity (uint64 masks)
 constexpr int QMAX = 64;   // accepted raw vertices
 constexpr int FW = 4;      // warps per CTA
-constexpr int NMAX = 96;   // hinted path: rows near the hint point
+constexpr int kFaceCtasPerSm = 3;
+constexpr int NMAX = 96;   // hinted path: rows near the hint point (more: the full path)
 constexpr double kCDelta = 1e-10;
 constexpr double kValMargin = 1e-11;   // sign margin (unit and raw values) for probe validation
 constexpr double kTinyNorm = 1e-6;     // rows this thin make validation unreliable
@@ -67,15 +69,20 @@ struct NearPhase {
     int nord[NMAX];                 // clipping order (by distance)
 };
 struct PolyPhase {
-    double qv[QMAX][3];             // accepted raw vertices (triu order)
-    unsigned long long qs[QMAX];    // their incident-plane sets (C-row masks)
+    // the raw vertices die with the dedup; the final loop (written by the ordering) reuses them
+    union {
+        double qv[QMAX][3];         // accepted raw vertices (triu order)
+        double fv[QMAX][3];         // final loop
+    };
+    union {
+        unsigned long long qs[QMAX];    // their incident-plane sets (C-row masks)
+        unsigned long long fs[QMAX];    // incident sets of the final loop
+    };
     double rv[QMAX][3];             // weld-cluster representatives (lexicographic minimum)
     int rfi[QMAX];                  // first member of each cluster (index into qv)
     unsigned long long rs[QMAX];
     double ang[QMAX];
     int ord[QMAX];
-    double fv[QMAX][3];             // final loop
-    unsigned long long fs[QMAX];
 };
 
 struct FaceWarp {
@@ -444,7 +451,14 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     FSTAT(14, use_list ? 1 : 0);
     FSTAT(15, (list_flags & kNearOverflow) ? 1 : 0);
     PMARK(0);
+#ifdef AM_FACE_STATS
+    int n_attempts = 0, n_streamed = 0, fp_reason = 3;   // 1 x0 violates, 2 near rows > NMAX, 3 attempts
+#endif
     for (int attempt = 0; attempt < 5 && status == 0 && have_hint && !hinted_done; attempt++) {
+#ifdef AM_FACE_STATS
+        n_attempts++;
+        if (!(use_list && tau <= reach)) n_streamed++;
+#endif
         const double x0[3] = {hint.x, hint.y, hint.z};
         const double lim = tau + band + 1e-9;
         double dmax_seen = 0.0;
@@ -644,6 +658,9 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
             }
             if (!hinted_done) status = 0;   // outside the hint's reach (or degenerate): retry / full path
         }
+#ifdef AM_FACE_STATS
+        if (!ok) fp_reason = !x0ok ? 1 : 2;
+#endif
         if (!ok) break;                    // x0 not on this polygon, or too many near rows: full path
         tau = fmax(2.0 * tau, 2.5 * dmax_seen);   // the polygon reached the square: widen the reach
     }
@@ -993,8 +1010,12 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         long long dt = clock64() - t_start;
         FSTAT(0, 1); FSTAT(1, n_clip1); FSTAT(2, n_clip2); FSTAT(3, nC); FSTAT(4, nq); FSTAT(5, nr);
         FSTAT(6, dt); FSTAT(7, hinted_done ? 1 : 0); FSTAT(13, have_hint ? 1 : 0);
-        int bkt = 0;
-        while ((1ll << (bkt + 1)) <= dt && bkt < 23) bkt++;
+        // path classes: 0 list, one attempt; 1 list, retries; 2 streamed an attempt; 3 full path
+        const int cls = !hinted_done ? 3 : n_streamed ? 2 : n_attempts > 1 ? 1 : 0;
+        FSTAT(24 + cls, 1); FSTAT(28 + cls, dt); FSTAT(32 + cls, dt > 100000 ? 1 : 0);
+        if (cls == 3) FSTAT(36 + (!have_hint ? 0 : fp_reason), 1);
+        int bkt = 0;   // log2 histogram from 2^14 cycles, 8 buckets
+        while ((1ll << (bkt + 15)) <= dt && bkt < 7) bkt++;
         FSTAT(16 + bkt, 1);
         if (lane == 0 && A.dbg) atomicMax(&A.dbg[8], (unsigned long long)dt);
     }
@@ -1325,6 +1346,11 @@ void launch_face(const FaceArgs& a, cudaStream_t s) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_face, FW * 32, smem);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // resident CTAs per SM: the per-cell latency chain, not issue throughput, bounds an
+        // iteration (waves of ~2.5 k cells on ~1.8 k warps), and more warps per SM lengthen it
+        int want = kFaceCtasPerSm;
+        if (const char* v = getenv("AM_FACE_CTAS")) want = atoi(v);
+        if (want > 0 && want < per_sm) per_sm = want;
         grid = sms * (per_sm > 0 ? per_sm : 1);
         init = true;
     }

@@ -113,15 +113,15 @@ def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int
                 break
             pts = np.stack([_sample_block(rng_seed, i, rnd, lo, hi) for i in pending])
             vals = eng.forward(pts.reshape(-1, 3)).cpu().numpy().reshape(len(pending), 64)
-            still = []
-            for j, i in enumerate(pending):
-                pos = pts[j][vals[j] > 0.0]
-                neg = pts[j][vals[j] < 0.0]
-                if len(pos) and len(neg):
-                    pairs[i] = (pos[0], neg[0])
-                else:
-                    still.append(i)
-            pending = still
+            # first positive / first negative sample of each stream (reference seeding.py:150-156)
+            pm, nm = vals > 0.0, vals < 0.0
+            ok = pm.any(axis=1) & nm.any(axis=1)
+            ip, ineg = pm.argmax(axis=1), nm.argmax(axis=1)
+            rows = np.arange(len(pending))
+            xp_all, xn_all = pts[rows, ip], pts[rows, ineg]
+            for j in np.flatnonzero(ok):
+                pairs[pending[j]] = (xp_all[j], xn_all[j])
+            pending = [pending[j] for j in np.flatnonzero(~ok)]
         if pairs:
             order = sorted(pairs)
             xp = np.stack([pairs[i][0] for i in order])

@@ -153,3 +153,33 @@ def test_fp32_mode_within_stated_tolerance():
     dev = np.array(dev)
     assert len(dev) > 0.99 * len(kb)
     assert np.quantile(dev, 0.99) <= 1e-5 and dev.max() <= 1e-3, (np.quantile(dev, 0.99), dev.max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("knob", [("AM_PROBE_IN_GRAPH", "1"), ("AM_COMPOSE_FUSED", "1"), ("AM_NEAR_CAP", "8"),
+                                  ("AM_TAU_MULT", "0.25"), ("AM_NEAR_REACH", "1")])
+def test_engine_paths_match_oracle(knob, monkeypatch):
+    """Every execution path of the engine is bit-exact, not only the default one: the probe stage
+    as a conditional graph node, the fused all-steps composition, near-list overflow (streaming
+    fallback), forced hint retries and attempts beyond the near list's reach."""
+    from paper_2106_10031_b200 import synth
+    from paper_2106_10031_b200.marching import clear_engine_cache
+    m = _gpu()
+    monkeypatch.setenv(*knob)
+    clear_engine_cache()
+    try:
+        for net, kw in ((synth.deepsdf_mlp(width=128, depth=8, skip_at=4, seed=2),
+                         dict(bbox=((0.0, 0.0, 0.0), (0.45, 0.45, 0.45)), seeds=4, rng_seed=2)),
+                        (synth.imnet_ensemble(widths=(32, 32, 32), n_parts=4, seed=3), dict(seeds=8, rng_seed=3))):
+            r = m.march(net, m.MarchConfig(**kw))
+            ck = (net.__class__.__name__, r.seeds.tobytes(), str(kw))
+            if ck not in _ORACLE_CACHE:   # same network and seeds for every knob: one oracle run
+                _ORACLE_CACHE[ck] = oracle.march(net, bbox=kw.get("bbox", m.DEFAULT_BBOX), seed_points=r.seeds)
+            o = _ORACLE_CACHE[ck]
+            assert r.report.cells_visited > 50
+            assert_same_march(r, o.keys, o.branch, o.nverts, o.verts, o.edge_nrefs, o.edge_refs)
+    finally:
+        clear_engine_cache()
+
+
+_ORACLE_CACHE: dict = {}

@@ -54,7 +54,10 @@ for name in ["seed", "run"]:
         return g
     setattr(engmod.Engine, name, mk(f, name))
 
-marching.march(net, cfg).welded_mesh()
+prev = None
+for _ in range(3):
+    cur = marching.march(net, cfg)
+    prev = (cur, cur.welded_mesh())
 for r in range(a.repeat):
     T.clear()
     flush.fill_(1)

@@ -46,10 +46,16 @@ if d[0]:
           f"verts {d[5]/n:.2f} cycles {d[6]/n:.0f} (max {int(d[8])}) hinted {d[7]/n:.2f}")
     print(f"hint: have {d[13]/n:.3f} x0-violates {d[9]/n:.3f} near>NMAX {d[10]/n:.3f} reach-fail {d[11]/n:.3f} "
           f"near rows {d[12]/max(1, d[13]):.1f} | near list used {d[14]/n:.3f} overflow {d[15]/n:.4f}")
-    print("cycle histogram (log2):", {int(2**i): int(d[16 + i]) for i in range(24) if d[16 + i]})
+    print("cycle histogram (log2, from 2^14):", {int(2**(i + 14)): int(d[16 + i]) for i in range(8) if d[16 + i]})
 if d[0]:
     names = ["setup", "stream", "near-rows", "clip", "accept+C'", "full-path", "pairs", "dedup", "order", "edges",
              "emit-count", "emit-records", "emit-keys"]
     tot = sum(float(d[40 + i]) for i in range(13))
     print("phase cycles per cell:", {nm: round(float(d[40 + i]) / n) for i, nm in enumerate(names)},
           f"sum {tot / n:.0f}")
+if d[0]:
+    cls = ["list-1", "list-retry", "streamed", "full-path"]
+    print("path classes (cells, mean cycles):", {c: (int(d[24 + i]), round(float(d[28 + i]) / max(1, int(d[24 + i]))))
+                                                for i, c in enumerate(cls)},
+          "| cells > 100k cycles:", {c: int(d[32 + i]) for i, c in enumerate(cls)},
+          "| full-path reasons (no hint, x0 violates, near > NMAX, attempts):", [int(d[36 + i]) for i in range(4)])
