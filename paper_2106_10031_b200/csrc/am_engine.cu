@@ -133,6 +133,7 @@ struct am_engine {
     DBuf<int32_t> near_n, near_flags, near_id;   // k_near lists per frontier entry
     int near_cap = 128;
     double tau_mult = 1.0, near_reach = 4.0;
+    int max_attempts = 5;                      // hinted attempts (AM_MAX_ATTEMPTS)
     // composition: per-step launches (AM_COMPOSE_FUSED=1: one fused launch for all steps; slower
     // on configs[1] and DeepSDF, kept for experiments)
     bool compose_fused = false;
@@ -529,6 +530,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_PROBE_IN_GRAPH")) e->probe_in_graph = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_REACH")) e->near_reach = atof(v);
     if (const char* v = getenv("AM_NEAR_CAP")) e->near_cap = atoi(v);
+    if (const char* v = getenv("AM_MAX_ATTEMPTS")) e->max_attempts = atoi(v);
     CK(e->near_n.reserve(e->B, s));
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
@@ -830,7 +832,7 @@ static int launch_iteration(am_engine* e) {
     a.cursor = c + C_FCURSOR;
     a.near_cap = e->near_cap; a.near_n = e->near_n.p; a.near_flags = e->near_flags.p;
     a.near_id = e->near_id.p; a.near_row = e->near_row.p;
-    a.tau_mult = e->tau_mult; a.near_reach = e->near_reach;
+    a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
     if (tm) cudaEventRecord(e->ev[2], s);
     launch_near(a, s);
     launch_face(a, s);
@@ -991,9 +993,15 @@ static int timed_iteration(am_engine* e) {
     e->flops += e->flops_per_cell * nR;
     e->n_comp_cells += nR;
     e->n_face_cells += nF;
-    if (getenv("AM_TRACE_ITERS"))
-        fprintf(stderr, "iter %lld nR %.0f nF %.0f compose %.1f us face %.1f us probe-stage %.1f us\n",
-                (long long)e->hctr[C_ITER], nR, nF, a * 1e3, b * 1e3, c * 1e3);
+    if (getenv("AM_TRACE_ITERS")) {
+        // AM_FACE_STATS builds: slowest face cell of the iteration (cycles) and full-path cells so far
+        unsigned long long dbg[64];
+        CK(cudaMemcpy(dbg, e->dbg.p, sizeof dbg, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "iter %lld nR %.0f nF %.0f compose %.1f us face %.1f us probe-stage %.1f us | max cell %llu cyc, "
+                "full-path %llu streamed %llu\n", (long long)e->hctr[C_ITER], nR, nF, a * 1e3, b * 1e3, c * 1e3,
+                dbg[8], dbg[27], dbg[26]);
+        CK(cudaMemset(e->dbg.p + 8, 0, 8));
+    }
     e->face_bytes += nF * (e->NB * 32.0 + e->M * 32.0 + e->KW * 8.0);
     return AM_OK;
 }

@@ -454,7 +454,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
 #ifdef AM_FACE_STATS
     int n_attempts = 0, n_streamed = 0, fp_reason = 3;   // 1 x0 violates, 2 near rows > NMAX, 3 attempts
 #endif
-    for (int attempt = 0; attempt < 5 && status == 0 && have_hint && !hinted_done; attempt++) {
+    for (int attempt = 0; attempt < A.max_attempts && status == 0 && have_hint && !hinted_done; attempt++) {
 #ifdef AM_FACE_STATS
         n_attempts++;
         if (!(use_list && tau <= reach)) n_streamed++;
@@ -656,6 +656,9 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
                     hinted_done = true;
                 }
             }
+#ifdef AM_FACE_STATS
+            if (!hinted_done) FSTAT(status == 1 ? 53 : status == 2 ? 54 : 55, 1);   // empty / overflow / reach
+#endif
             if (!hinted_done) status = 0;   // outside the hint's reach (or degenerate): retry / full path
         }
 #ifdef AM_FACE_STATS

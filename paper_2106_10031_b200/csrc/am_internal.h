@@ -304,6 +304,7 @@ struct FaceArgs {
     int near_cap;
     double tau_mult;          // first hinted attempt: reach = tau_mult x the hint radius
     double near_reach;        // near lists cover near_reach x the hint radius
+    int max_attempts;         // hinted attempts before the ring-ordered full path
     int32_t* near_n;
     int32_t* near_flags;
     int32_t* near_id;         // [n_cap][near_cap]

@@ -59,3 +59,5 @@ if d[0]:
                                                 for i, c in enumerate(cls)},
           "| cells > 100k cycles:", {c: int(d[32 + i]) for i, c in enumerate(cls)},
           "| full-path reasons (no hint, x0 violates, near > NMAX, attempts):", [int(d[36 + i]) for i in range(4)])
+if d[0]:
+    print("failed hinted attempts: empty", int(d[53]), "vertex overflow", int(d[54]), "reach", int(d[55]))
