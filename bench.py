@@ -150,7 +150,7 @@ def run_reference(args, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "cells/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample_cells": cells, "parallelism": f"{threads} host threads"},
         "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "port",
                          "sample": f"first {cells} cells of the march per step (max_cells cap)"},
@@ -180,9 +180,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # AM_BENCH_SHARE_GPU=1 / AM_DIST_BACKEND=gloo: functional check of the multi-rank path on a
+    # one-GPU box (ranks share the device; the timings of such a run are not measurements)
+    if os.environ.get("AM_BENCH_SHARE_GPU") == "1":
+        local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("AM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2106_10031_b200 import marching
     from paper_2106_10031_b200.engine import Engine
@@ -412,7 +420,7 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "cells_per_step": cells, "waves": int(waves),
                        "parallelism": f"dp{world} (state-hash ownership)" if world > 1 else "1 GPU",

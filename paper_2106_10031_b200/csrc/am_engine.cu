@@ -1104,7 +1104,9 @@ extern "C" int am_run(am_engine* e, int64_t* h_waves) {
 extern "C" int am_queue_size(am_engine* e, int64_t* h_n) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
     RC(sync_counters(e));
-    *h_n = (int64_t)(e->hctr[C_QTAIL] - e->hctr[C_QHEAD]);
+    // outstanding work: queued states, pending probe records and unevaluated probes (the
+    // sharded loop terminates when this is zero on every rank)
+    *h_n = (int64_t)(e->hctr[C_QTAIL] - e->hctr[C_QHEAD]) + (int64_t)e->hctr[C_NPEND] + (int64_t)e->hctr[C_NPROBE];
     return AM_OK;
 }
 

@@ -35,16 +35,19 @@ def exchange(send: torch.Tensor, counts: np.ndarray, kw: int, extra: int = 0):
     """
     world = dist.get_world_size()
     dev = send.device
-    meta = torch.tensor([[int(c), int(extra)] for c in counts], dtype=torch.int64, device=dev)
+    # gloo (CPU test runs) moves host tensors: device rows are staged through the host
+    stage = send.is_cuda and dist.get_backend() == "gloo"
+    cdev = torch.device("cpu") if stage else dev
+    meta = torch.tensor([[int(c), int(extra)] for c in counts], dtype=torch.int64, device=cdev)
     meta_in = torch.empty_like(meta)
     dist.all_to_all_single(meta_in, meta)
     recv_counts = meta_in[:, 0].tolist()
     total_pending = int(meta_in[:, 1].sum().item())
-    recv = torch.empty((sum(recv_counts), kw), dtype=send.dtype, device=dev)
+    recv = torch.empty((sum(recv_counts), kw), dtype=send.dtype, device=cdev)
     if world > 1:
-        dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=recv_counts,
+        dist.all_to_all_single(recv, (send.cpu() if stage else send).contiguous(), output_split_sizes=recv_counts,
                                input_split_sizes=[int(c) for c in counts])
-    return recv, total_pending
+    return (recv.to(dev) if stage else recv), total_pending
 
 
 class ShardedMarcher:
