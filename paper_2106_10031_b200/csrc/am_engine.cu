@@ -850,9 +850,7 @@ static int launch_iteration(am_engine* e) {
         launch_hash_fixup(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, 0u, e->emit_pool.p,
                           e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
     }
-    // probe records: target entries -> pending; pending with processed targets -> drop / forward
-    launch_prec_target(R, e->status.p, e->emit_dup.p, e->emit_pool.p, c, e->PR, e->probe_pts.p, e->PB, s);
-    launch_resolve(R, H, e->val_buf.p, c, R.cap_pend, e->probe_pts.p, shapes ? e->probe_shape.p : nullptr, e->PB, s);
+    // probe records (this iteration's and the pending ones): drop / forward / keep pending
     // This iteration's exact probe evaluations.  Probe-heavy marches (wide nets, batches of
     // shapes) capture them as a conditional node of the iteration graph whose predicate
     // k_pend_finalize sets, so probe-found states join the next wave.  Marches with only a
@@ -868,7 +866,8 @@ static int launch_iteration(am_engine* e) {
         CK(cudaStreamGetCaptureInfo_v3(s, &cs, nullptr, &g0, nullptr, nullptr, nullptr));
         CK(cudaGraphConditionalHandleCreate(&h, g0, 0, cudaGraphCondAssignDefault));
     }
-    launch_pend_finalize(c, capturing ? &h : nullptr, s);
+    launch_probe_records(R, H, e->status.p, e->emit_dup.p, e->emit_pool.p, e->val_buf.p, c, e->PR, e->probe_pts.p,
+                         shapes ? e->probe_shape.p : nullptr, e->PB, capturing ? &h : nullptr, s);
     if (capturing) {
         cudaGraph_t g = nullptr;
         const cudaGraphNode_t* deps = nullptr;

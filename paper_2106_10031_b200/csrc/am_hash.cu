@@ -424,6 +424,106 @@ __global__ void k_resolve(ProbeRecs R, HashSet H, const int32_t* val_buf, unsign
 }
 
 // (has_cond: also set the iteration graph's conditional probe stage: any probe to evaluate?)
+// Probe records of one iteration in one launch (k_prec_target + k_resolve + k_pend_finalize):
+// work item i < n_new is this iteration's record i (its target is resolved from the emitted
+// candidate's insert status), i >= n_new the pending record i - n_new of earlier iterations.
+// Either is dropped (the target validated the mirrored probe), queued for exact evaluation, or
+// kept pending (target not composed yet) in the other parity's list.  The last CTA to finish
+// updates the counters and, inside the captured graph, sets the probe stage's predicate.
+__device__ __forceinline__ void probe_decide(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf,
+                                             unsigned long long* ctr, int32_t t, int32_t k, const double* pt,
+                                             int32_t shp, double* probe_pts, int32_t* probe_shape,
+                                             int64_t cap_probe, int par) {
+    bool forward = false, keep = false;
+    if (t < 0) {
+        forward = true;
+    } else {
+        const int32_t vn = H.pool_vn[t];
+        if (vn >= 0) {
+            const int64_t off = H.pool_voff[t];
+            bool found = false;
+            for (int q = 0; q < vn; q++) found |= val_buf[off + q] == k;
+            forward = !found;
+        } else if (H.pool_flags[t] & 2u) {
+            forward = true;   // composed but no face (canonical elsewhere / capped): exact evaluation
+        } else {
+            keep = true;      // target still queued
+        }
+    }
+    if (forward) {
+        const unsigned long long q = atomicAdd(ctr + C_NPROBE, 1ull);
+        if ((int64_t)q < cap_probe) {
+            probe_pts[q * 3 + 0] = pt[0]; probe_pts[q * 3 + 1] = pt[1]; probe_pts[q * 3 + 2] = pt[2];
+            if (R.s) probe_shape[q] = shp;
+        } else {
+            keep = true;      // forward buffer full: retry next iteration
+        }
+    }
+    if (keep) {
+        const unsigned long long j = atomicAdd(ctr + C_NKEEP, 1ull);
+        if ((int64_t)j >= R.cap_pend) { atomicAdd(ctr + C_OVF1, 1ull); return; }
+        R.pend_t[par ^ 1][j] = t;
+        R.pend_k[par ^ 1][j] = k;
+        R.pend_pt[par ^ 1][j * 3 + 0] = pt[0];
+        R.pend_pt[par ^ 1][j * 3 + 1] = pt[1];
+        R.pend_pt[par ^ 1][j * 3 + 2] = pt[2];
+        if (R.s) R.pend_s[par ^ 1][j] = shp;
+    }
+}
+
+__global__ void k_probe_records(ProbeRecs R, HashSet H, const int32_t* status, const int32_t* dup_ref,
+                                const int32_t* pool_idx, const int32_t* val_buf, unsigned long long* ctr,
+                                int64_t cap_new, double* probe_pts, int32_t* probe_shape, int64_t cap_probe,
+                                cudaGraphConditionalHandle h, int has_cond) {
+    pdl_enter();
+    const int64_t n_new = dev_count(ctr + C_NPREC, cap_new);
+    const int64_t n_old = dev_count(ctr + C_NPEND, R.cap_pend);
+    const int par = (int)(ctr[C_PPAR] & 1ull);
+    GRID_STRIDE(i, n_new + n_old) {
+        if (i < n_new) {
+            const int32_t ci = R.cand[i];
+            int32_t t = -1;   // -1: exact forward evaluation (no flip target, or owned by another rank)
+            if (ci >= 0) {
+                const int32_t st = status[ci];
+                if (st == 1) t = pool_idx[ci];
+                else if (st == 0) t = dup_ref[ci] >= 0 ? dup_ref[ci] : pool_idx[-2 - dup_ref[ci]];
+            }
+            probe_decide(R, H, val_buf, ctr, t, R.k[i], R.pt + i * 3, R.s ? R.s[i] : 0, probe_pts, probe_shape,
+                         cap_probe, par);
+        } else {
+            const int64_t j = i - n_new;
+            probe_decide(R, H, val_buf, ctr, R.pend_t[par][j], R.pend_k[par][j], R.pend_pt[par] + j * 3,
+                         R.s ? R.pend_s[par][j] : 0, probe_pts, probe_shape, cap_probe, par);
+        }
+    }
+    // the last CTA to finish publishes the counters
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ctr + C_DONE, 1ull) == (unsigned long long)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        volatile unsigned long long* vc = ctr;
+        if (has_cond) cudaGraphSetConditional(h, vc[C_NPROBE] ? 1u : 0u);
+        vc[C_PREC_TOTAL] = vc[C_PREC_TOTAL] + vc[C_NPREC];
+        vc[C_NPEND] = vc[C_NKEEP];
+        vc[C_PPAR] = vc[C_PPAR] ^ 1ull;
+        vc[C_DONE] = 0;
+    }
+}
+
+void launch_probe_records(const ProbeRecs& R, const HashSet& H, const int32_t* status, const int32_t* dup_ref,
+                          const int32_t* pool_idx, const int32_t* val_buf, unsigned long long* ctr, int64_t cap_new,
+                          double* probe_pts, int32_t* probe_shape, int64_t cap_probe,
+                          const cudaGraphConditionalHandle* h, cudaStream_t s) {
+    launch_k(k_probe_records, grid_for(cap_new + R.cap_pend, 256), 256, 0, s, R, H, status, dup_ref, pool_idx,
+             val_buf, ctr, cap_new, probe_pts, probe_shape, cap_probe, h ? *h : cudaGraphConditionalHandle{},
+             h ? 1 : 0);
+}
+
 __global__ void k_pend_finalize(unsigned long long* ctr, cudaGraphConditionalHandle h, int has_cond) {
     pdl_enter();
     if (threadIdx.x == 0 && blockIdx.x == 0) {

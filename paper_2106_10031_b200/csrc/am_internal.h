@@ -171,7 +171,7 @@ int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t col
 enum Ctr {
     C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_OVF0, C_OVF1, C_CAPPED, C_TOTAL, C_QHEAD, C_QTAIL, C_NR, C_NX,
     C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_NPREC, C_NPEND, C_PPAR,
-    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_NFLUSH, C_N
+    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_NFLUSH, C_DONE, C_N
 };
 
 // hash set (am_hash.cu)
@@ -222,6 +222,10 @@ void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t
 void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr,
                     int64_t cap, double* probe_pts, int32_t* probe_shape, int64_t cap_probe, cudaStream_t s);
 void launch_pend_finalize(unsigned long long* ctr, const cudaGraphConditionalHandle* h, cudaStream_t s);
+void launch_probe_records(const ProbeRecs& R, const HashSet& H, const int32_t* status, const int32_t* dup_ref,
+                          const int32_t* pool_idx, const int32_t* val_buf, unsigned long long* ctr, int64_t cap_new,
+                          double* probe_pts, int32_t* probe_shape, int64_t cap_probe,
+                          const cudaGraphConditionalHandle* h, cudaStream_t s);
 void launch_probe_done(unsigned long long* ctr, int64_t cap_probe, cudaStream_t s);
 void launch_take(const IterState& I, cudaStream_t s);
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
