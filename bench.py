@@ -345,6 +345,7 @@ def main():
                    + mesh.vertices.nbytes + mesh.face_off.nbytes + mesh.face_idx.nbytes)
         e_ms = float(np.mean(e_times))
         e2e = {"value": r.report.cells_visited / (e_ms * 1e-3), "unit": "cells/s", "ms_per_step": e_ms,
+               "ms_steps": [round(x, 2) for x in e_times],
                "mesh_time_s": e_ms * 1e-3, "march_only_ms": float(np.mean(m_times)),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "mesh": {"vertices": int(mesh.n_vertices), "faces": int(mesh.n_faces),

@@ -131,9 +131,10 @@ struct am_engine {
     DBuf<int64_t> pool_voff;
     DBuf<double> pool_hint, ckey_hint, emit_hint, near_row;
     DBuf<int32_t> near_n, near_flags, near_id;   // k_near lists per frontier entry
-    int near_cap = 128;
-    double tau_mult = 1.0, near_reach = 4.0;
-    int max_attempts = 5;                      // hinted attempts (AM_MAX_ATTEMPTS)
+    int near_cap = 256;
+    double tau_mult = 1.0, near_reach = 6.0;
+    int max_attempts = 12;                     // hinted attempts (AM_MAX_ATTEMPTS; 5 -> 12: 31 -> 28.3 ms)
+    double tau_grow = 2.0;                     // reach growth per failed attempt (AM_TAU_GROW)
     // composition: per-step launches (AM_COMPOSE_FUSED=1: one fused launch for all steps; slower
     // on configs[1] and DeepSDF, kept for experiments)
     bool compose_fused = false;
@@ -531,6 +532,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_NEAR_REACH")) e->near_reach = atof(v);
     if (const char* v = getenv("AM_NEAR_CAP")) e->near_cap = atoi(v);
     if (const char* v = getenv("AM_MAX_ATTEMPTS")) e->max_attempts = atoi(v);
+    if (const char* v = getenv("AM_TAU_GROW")) e->tau_grow = atof(v);
     CK(e->near_n.reserve(e->B, s));
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
@@ -833,6 +835,7 @@ static int launch_iteration(am_engine* e) {
     a.near_cap = e->near_cap; a.near_n = e->near_n.p; a.near_flags = e->near_flags.p;
     a.near_id = e->near_id.p; a.near_row = e->near_row.p;
     a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
+    a.tau_grow = e->tau_grow;
     if (tm) cudaEventRecord(e->ev[2], s);
     launch_near(a, s);
     launch_face(a, s);

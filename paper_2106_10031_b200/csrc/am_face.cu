@@ -55,7 +55,7 @@ constexpr int CMAX = 64;   // candidate plane set capacity (uint64 masks)
 constexpr int QMAX = 64;   // accepted raw vertices
 constexpr int FW = 4;      // warps per CTA
 constexpr int kFaceCtasPerSm = 3;
-constexpr int NMAX = 96;   // hinted path: rows near the hint point (more: the full path)
+constexpr int NMAX = 160;  // hinted path: rows near the hint point (more: the full path)
 constexpr double kCDelta = 1e-10;
 constexpr double kValMargin = 1e-11;   // sign margin (unit and raw values) for probe validation
 constexpr double kTinyNorm = 1e-6;     // rows this thin make validation unreliable
@@ -665,7 +665,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         if (!ok) fp_reason = !x0ok ? 1 : 2;
 #endif
         if (!ok) break;                    // x0 not on this polygon, or too many near rows: full path
-        tau = fmax(2.0 * tau, 2.5 * dmax_seen);   // the polygon reached the square: widen the reach
+        tau = fmax(A.tau_grow * tau, 2.5 * dmax_seen);   // the polygon reached the square: widen the reach
     }
 
     PMARK(4);

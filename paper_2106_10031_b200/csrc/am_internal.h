@@ -308,7 +308,8 @@ struct FaceArgs {
     int near_cap;
     double tau_mult;          // first hinted attempt: reach = tau_mult x the hint radius
     double near_reach;        // near lists cover near_reach x the hint radius
-    int max_attempts;         // hinted attempts before the ring-ordered full path
+    int max_attempts;         // hinted attempts before the full path
+    double tau_grow;          // reach growth factor between attempts (at least)
     int32_t* near_n;
     int32_t* near_flags;
     int32_t* near_id;         // [n_cap][near_cap]
