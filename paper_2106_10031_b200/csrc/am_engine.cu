@@ -37,6 +37,13 @@ void launch_dichotomy_step(const double* vals, double* xp, double* xn, double* f
                            int32_t* active, double* out, int64_t n, double eps, double seed_tol, int last,
                            cudaStream_t s);
 void launch_midpoint(const double* a, const double* b, double* m, int64_t n, cudaStream_t s);
+void launch_bisect_tree(const double* xp, const double* xn, const int32_t* active, int64_t n, double* nodes,
+                        cudaStream_t s);
+void launch_bisect_replay(const double* vals, const double* nodes, double* xp, double* xn, double* fp, double* fn,
+                          int32_t* active, double* out, int64_t n, int it0, int max_iters, double eps,
+                          double seed_tol, cudaStream_t s);
+int bisect_tree_points();
+int bisect_tree_depth();
 void launch_point_hints(const double* X, int64_t n, double tau, double* hints, cudaStream_t s);
 void launch_count_active(const int32_t* active, int64_t n, unsigned long long* cnt, cudaStream_t s);
 void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s);
@@ -177,8 +184,9 @@ struct am_engine {
     bool probe_in_graph = false;             // probe stage inside the iteration graph (sticky)
     unsigned long long cond_kernels = 0;     // kernels in that body
     // bisection trigger: engine-owned buffers and a captured 8-step graph (am_dichotomy)
-    DBuf<double> dxp, dxn, dfp, dfn, dmid, dvals, dout;
-    DBuf<int32_t> dact, dshape;
+    DBuf<double> dxp, dxn, dfp, dfn, dmid, dvals, dout, dtree, dtvals;
+    DBuf<int32_t> dact, dshape, dtshape;
+    bool bisect_tree = true;   // speculative bisection tree (AM_BISECT_TREE=0: step by step)
     cudaGraphExec_t dgexec = nullptr;
     int64_t dg_n = -1;
     double dg_eps = 0, dg_tol = 0;
@@ -533,6 +541,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_NEAR_CAP")) e->near_cap = atoi(v);
     if (const char* v = getenv("AM_MAX_ATTEMPTS")) e->max_attempts = atoi(v);
     if (const char* v = getenv("AM_TAU_GROW")) e->tau_grow = atof(v);
+    if (const char* v = getenv("AM_BISECT_TREE")) e->bisect_tree = atoi(v) != 0;
     CK(e->near_n.reserve(e->B, s));
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
@@ -563,9 +572,11 @@ extern "C" int am_engine_destroy(am_engine* e) {
     cudaStreamSynchronize(e->stream);
     if (e->gexec) cudaGraphExecDestroy(e->gexec);
     if (e->dgexec) cudaGraphExecDestroy(e->dgexec);
-    for (auto* b : {&e->dxp, &e->dxn, &e->dfp, &e->dfn, &e->dmid, &e->dvals, &e->dout}) b->release(e->stream);
+    for (auto* b : {&e->dxp, &e->dxn, &e->dfp, &e->dfn, &e->dmid, &e->dvals, &e->dout, &e->dtree, &e->dtvals})
+        b->release(e->stream);
     e->dact.release(e->stream);
     e->dshape.release(e->stream);
+    e->dtshape.release(e->stream);
     if (e->graph) cudaGraphDestroy(e->graph);
     DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx, &e->shint,
                            &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1], &e->pool_hint,
@@ -1226,6 +1237,38 @@ extern "C" int am_dichotomy_shapes(am_engine* e, const double* d_xpos, const dou
     RC(forward_host(e, e->dxn.p, n, e->dfn.p, e->hkeys.p, shp));
     std::vector<int32_t> ones(n, 1);
     CK(cudaMemcpyAsync(e->dact.p, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
+    // speculative bisection tree: D exact steps per batched forward (k_bisect_tree / replay);
+    // the per-point shapes repeat over each pair's tree points
+    const int TN = bisect_tree_points(), TD = bisect_tree_depth();
+    if (e->bisect_tree && n * TN <= e->PB) {
+        CK(e->dtree.reserve(n * TN * 3, s));
+        CK(e->dtvals.reserve(n * TN, s));
+        CK(e->hkeys.reserve(n * TN * e->KW, s));
+        const int32_t* tshp = nullptr;
+        if (shp) {
+            std::vector<int32_t> hs(n), ht(n * TN);
+            CK(cudaMemcpyAsync(hs.data(), shp, n * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (int64_t i = 0; i < n; i++) for (int k = 0; k < TN; k++) ht[i * TN + k] = hs[i];
+            CK(e->dtshape.reserve(n * TN, s));
+            CK(cudaMemcpyAsync(e->dtshape.p, ht.data(), n * TN * 4, cudaMemcpyHostToDevice, s));
+            tshp = e->dtshape.p;
+        }
+        for (int it0 = 1; it0 <= max_iters; it0 += TD) {
+            launch_bisect_tree(e->dxp.p, e->dxn.p, e->dact.p, n, e->dtree.p, s);
+            RC(forward_host(e, e->dtree.p, n * TN, e->dtvals.p, e->hkeys.p, tshp));
+            launch_bisect_replay(e->dtvals.p, e->dtree.p, e->dxp.p, e->dxn.p, e->dfp.p, e->dfn.p, e->dact.p, e->dout.p, n,
+                                 it0, max_iters, eps, seed_tol, s);
+            CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, 8, s));
+            launch_count_active(e->dact.p, n, e->ctr.p + C_LIST, s);
+            RC(sync_counters(e));
+            if (e->hctr[C_LIST] == 0) break;
+        }
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(d_out, e->dout.p, n * 24, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        return AM_OK;
+    }
     launch_midpoint(e->dxp.p, e->dxn.p, e->dmid.p, n, s);
     // one bisection step: F(mid) (the forward kernels) + the step kernel; 8 steps are captured
     // once per (n, tolerances, buffers) and replayed, the host checks convergence between replays

@@ -89,6 +89,77 @@ void launch_dichotomy_step(const double* vals, double* xp, double* xn, double* f
     if (n > 0) { launch_k(k_dichotomy_step, nb(n), 128, 0, s, vals, xp, xn, fp, fn, mid, active, out, n, eps, seed_tol, last); }
 }
 
+// ---------------------------------------------- speculative bisection tree (exact)
+// The bisection's next D midpoints lie in a binary tree of 2^D - 1 points fixed by (xp, xn):
+// node 0 = 0.5 (xp + xn); the children of a node m of interval {a, b} are the midpoints of
+// {m, xn-side} (taken when F(m) > 0, xp := m) and {xp-side, m}.  Every node is formed with the
+// bisection's own arithmetic (0.5 (l + r); addition commutes, so the midpoint of an interval
+// does not depend on which end is xp), and F is evaluated per point, so replaying the
+// reference's step rule through the tree (k_bisect_replay) visits exactly the points and values
+// of D sequential steps -- with one batched forward instead of D.
+constexpr int kTreeD = 5, kTreeN = (1 << kTreeD) - 1;
+
+// node k (heap order: children of k are 2k+1 (F > 0: xp := m) and 2k+2 (F <= 0: xn := m))
+__global__ void k_bisect_tree(const double* xp, const double* xn, const int32_t* active, int64_t n, double* nodes) {
+    pdl_enter();
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double* out = nodes + i * kTreeN * 3;
+    double lp[kTreeN][3], ln[kTreeN][3];   // interval (xp side, xn side) of every node
+    for (int d = 0; d < 3; d++) { lp[0][d] = xp[i * 3 + d]; ln[0][d] = xn[i * 3 + d]; }
+    for (int k = 0; k < kTreeN; k++) {
+        double m[3];
+        for (int d = 0; d < 3; d++) { m[d] = 0.5 * (lp[k][d] + ln[k][d]); out[k * 3 + d] = m[d]; }
+        const int c0 = 2 * k + 1, c1 = 2 * k + 2;
+        if (c0 < kTreeN) for (int d = 0; d < 3; d++) { lp[c0][d] = m[d]; ln[c0][d] = ln[k][d]; }
+        if (c1 < kTreeN) for (int d = 0; d < 3; d++) { lp[c1][d] = lp[k][d]; ln[c1][d] = m[d]; }
+    }
+    (void)active;
+}
+
+// D steps of reference seeding.py:96-112 per active pair along the evaluated tree
+__global__ void k_bisect_replay(const double* vals, const double* nodes, double* xp, double* xn, double* fp,
+                                double* fn, int32_t* active, double* out, int64_t n, int it0, int max_iters,
+                                double eps, double seed_tol) {
+    pdl_enter();
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !active[i]) return;
+    int k = 0;
+    for (int lvl = 0; lvl < kTreeD; lvl++) {
+        const int it = it0 + lvl;
+        const double fm = vals[i * kTreeN + k];
+        const double* m = nodes + (i * kTreeN + k) * 3;
+        if (fabs(fm) <= seed_tol) {
+            out[i * 3 + 0] = m[0]; out[i * 3 + 1] = m[1]; out[i * 3 + 2] = m[2];
+            active[i] = 0;
+            return;
+        }
+        if (fm > 0.0) { xp[i * 3] = m[0]; xp[i * 3 + 1] = m[1]; xp[i * 3 + 2] = m[2]; fp[i] = fm; k = 2 * k + 1; }
+        else { xn[i * 3] = m[0]; xn[i * 3 + 1] = m[1]; xn[i * 3 + 2] = m[2]; fn[i] = fm; k = 2 * k + 2; }
+        if (fp[i] - fn[i] <= eps || it == max_iters) {
+            const double* src = fabs(fp[i]) <= fabs(fn[i]) ? xp + i * 3 : xn + i * 3;
+            out[i * 3 + 0] = src[0]; out[i * 3 + 1] = src[1]; out[i * 3 + 2] = src[2];
+            active[i] = 0;
+            return;
+        }
+    }
+}
+
+void launch_bisect_tree(const double* xp, const double* xn, const int32_t* active, int64_t n, double* nodes,
+                        cudaStream_t s) {
+    if (n > 0) { launch_k(k_bisect_tree, nb(n), 128, 0, s, xp, xn, active, n, nodes); }
+}
+void launch_bisect_replay(const double* vals, const double* nodes, double* xp, double* xn, double* fp, double* fn,
+                          int32_t* active, double* out, int64_t n, int it0, int max_iters, double eps,
+                          double seed_tol, cudaStream_t s) {
+    if (n > 0) {
+        launch_k(k_bisect_replay, nb(n), 128, 0, s, vals, nodes, xp, xn, fp, fn, active, out, n, it0, max_iters, eps,
+                 seed_tol);
+    }
+}
+int bisect_tree_points() { return kTreeN; }
+int bisect_tree_depth() { return kTreeD; }
+
 }  // namespace am
 
 namespace am {
