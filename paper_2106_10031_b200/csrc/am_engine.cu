@@ -816,9 +816,7 @@ static int launch_iteration(am_engine* e) {
     if (tm) cudaEventRecord(e->ev[1], s);
     launch_route_changed(e->ckey.p, e->changed.p, c + C_NR, B, e->KW, e->P.rank, e->P.world, e->X.p, c + C_NX,
                          e->outbox.p, c + C_NOUT, e->canon_pos.p, s);
-    launch_hash_insert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, nullptr, s);
-    launch_hash_fixup(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, 0u, e->canon_pool.p, nullptr,
-                      nullptr, e->ckey_hint.p, s);
+    launch_hash_upsert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, nullptr, 0u, e->canon_pool.p, nullptr, nullptr, e->ckey_hint.p, s);
     launch_frontier(c + C_NR, B, e->changed.p, e->batch_pool.p, e->canon_pos.p, e->status2.p, e->canon_pool.p,
                     e->pool_flags.p, e->f_items.p, e->f_pool.p, c, (long long)e->P.max_cells, s);
     FaceArgs a;
@@ -855,14 +853,9 @@ static int launch_iteration(am_engine* e) {
     if (multi) {
         launch_route_emitted(e->scratch.p, c + C_NEMIT, e->E, e->KW, e->P.rank, e->P.world, e->local_idx.p,
                              c + C_NLOCAL, e->outbox.p, c + C_NOUT, e->status.p, s);
-        launch_hash_insert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p,
-                           e->emit_dup.p, s);
-        launch_hash_fixup(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, 0u,
-                          e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
+        launch_hash_upsert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
     } else {
-        launch_hash_insert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, e->emit_dup.p, s);
-        launch_hash_fixup(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, 0u, e->emit_pool.p,
-                          e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
+        launch_hash_upsert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
     }
     // probe records (this iteration's and the pending ones): drop / forward / keep pending
     // This iteration's exact probe evaluations.  Probe-heavy marches (wide nets, batches of
@@ -933,13 +926,9 @@ static int launch_probe_stage(am_engine* e) {
         CK(cudaMemsetAsync(c + C_NPLOCAL, 0, sizeof(unsigned long long), s));
         launch_route_emitted(e->pkeys.p, c + C_NPROBE, e->PB, e->KW, e->P.rank, e->P.world, e->local_idx.p,
                              c + C_NPLOCAL, e->outbox.p, c + C_NOUT, nullptr, s);
-        launch_hash_insert(H, e->pkeys.p, e->local_idx.p, c + C_NPLOCAL, e->PB, e->pstatus.p, e->pslot.p, nullptr, s);
-        launch_hash_fixup(H, e->pkeys.p, e->local_idx.p, c + C_NPLOCAL, e->PB, e->pstatus.p, e->pslot.p, 0u, nullptr,
-                          e->queue.p, c + C_QTAIL, nullptr, s);
+        launch_hash_upsert(H, e->pkeys.p, e->local_idx.p, c + C_NPLOCAL, e->PB, e->pstatus.p, e->pslot.p, nullptr, 0u, nullptr, e->queue.p, c + C_QTAIL, nullptr, s);
     } else {
-        launch_hash_insert(H, e->pkeys.p, nullptr, c + C_NPROBE, e->PB, e->pstatus.p, e->pslot.p, nullptr, s);
-        launch_hash_fixup(H, e->pkeys.p, nullptr, c + C_NPROBE, e->PB, e->pstatus.p, e->pslot.p, 0u, nullptr,
-                          e->queue.p, c + C_QTAIL, nullptr, s);
+        launch_hash_upsert(H, e->pkeys.p, nullptr, c + C_NPROBE, e->PB, e->pstatus.p, e->pslot.p, nullptr, 0u, nullptr, e->queue.p, c + C_QTAIL, nullptr, s);
     }
     launch_probe_done(c, e->PB, s);
     CK(cudaGetLastError());
@@ -1073,14 +1062,9 @@ static int push_keys(am_engine* e, const uint64_t* d_keys, int64_t n, const doub
         CK(e->local_idx.reserve(n, e->stream));
         CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, 8, e->stream));
         launch_filter_owned(d_keys, n, e->KW, e->P.rank, e->P.world, e->local_idx.p, e->ctr.p + C_LIST, e->stream);
-        launch_hash_insert(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, nullptr,
-                           e->stream);
-        launch_hash_fixup(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, 0u, nullptr,
-                          e->queue.p, e->ctr.p + C_QTAIL, d_hints, e->stream);
+        launch_hash_upsert(H, d_keys, e->local_idx.p, e->ctr.p + C_LIST, n, e->hstatus.p, e->hslot.p, nullptr, 0u, nullptr, e->queue.p, e->ctr.p + C_QTAIL, d_hints, e->stream);
     } else {
-        launch_hash_insert(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, nullptr, e->stream);
-        launch_hash_fixup(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, 0u, nullptr, e->queue.p,
-                          e->ctr.p + C_QTAIL, d_hints, e->stream);
+        launch_hash_upsert(H, d_keys, nullptr, nullptr, n, e->hstatus.p, e->hslot.p, nullptr, 0u, nullptr, e->queue.p, e->ctr.p + C_QTAIL, d_hints, e->stream);
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(e->stream));

@@ -24,8 +24,16 @@ __device__ __forceinline__ bool keys_equal(const uint64_t* a, const uint64_t* b,
 
 #define GRID_STRIDE(i, n) for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
-__global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                              int64_t n_cap, int32_t* status, uint64_t* slot_out, int32_t* dup_ref) {
+// Insert a batch of keys (open addressing, linear probing).  A key that claims an empty slot
+// is new: the same thread appends it to the pool right away (key, flags, hint), publishes the
+// slot's final value (fingerprint | pool index) after a fence, and queues it.  Until then the
+// slot holds a candidate marker (fingerprint | cand bit | batch index) and concurrent inserters
+// of the same key compare against the batch copy, so duplicates inside a batch and against the
+// table resolve in this one launch (dup_ref: pool index, or -2 - batch index of the winner whose
+// pool index lands in pool_idx).
+__global__ void k_hash_upsert(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                              int64_t n_cap, int32_t* status, uint64_t* slot_out, int32_t* dup_ref, uint32_t flag,
+                              int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint) {
     pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(i, n) {
@@ -63,32 +71,20 @@ __global__ void k_hash_insert(HashSet H, const uint64_t* src, const int32_t* idx
         }
         status[ci] = st;
         if (dup_ref) dup_ref[ci] = dref;
-    }
-}
-
-__global__ void k_hash_fixup(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                             int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag,
-                             int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint) {
-    pdl_enter();
-    const int64_t n = dev_count(n_dev, n_cap);
-    GRID_STRIDE(i, n) {
-        const int64_t ci = idx ? idx[i] : i;
-        if (status[ci] != 1) {
+        if (st != 1) {
             if (pool_idx) pool_idx[ci] = -1;
             continue;
         }
-        const uint64_t* key = src + ci * H.KW;
-        unsigned long long p = atomicAdd(H.n_pool, 1ull);
+        const unsigned long long p = atomicAdd(H.n_pool, 1ull);
         uint64_t* dst = H.pool + (int64_t)p * H.KW;
         for (int w = 0; w < H.KW; w++) dst[w] = key[w];
         H.pool_flags[p] = flag;
         H.pool_vn[p] = -1;
-        double4 hint = src_hint ? reinterpret_cast<const double4*>(src_hint)[ci]
-                                : make_double4(0.0, 0.0, 0.0, __longlong_as_double(0x7ff0000000000000ll));
+        const double4 hint = src_hint ? reinterpret_cast<const double4*>(src_hint)[ci]
+                                      : make_double4(0.0, 0.0, 0.0, __longlong_as_double(0x7ff0000000000000ll));
         reinterpret_cast<double4*>(H.pool_hint)[p] = hint;
-        uint64_t fp = key_hash(key, H.KW) >> 33;
         __threadfence();
-        H.table[slot[ci]] = (fp << 33) | (uint64_t)(uint32_t)p;
+        H.table[pos] = (fp << 33) | (uint64_t)(uint32_t)p;
         if (pool_idx) pool_idx[ci] = (int32_t)p;
         if (queue) queue[atomicAdd(q_tail, 1ull)] = (int32_t)p;
     }
@@ -124,14 +120,14 @@ static unsigned grid_for(int64_t n, int b) {
     return (unsigned)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
 }
 
-void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                        int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, cudaStream_t s) {
-    if (n_cap > 0) { launch_k(k_hash_insert, grid_for(n_cap, 256), 256, 0, s, H, src, idx, n_dev, n_cap, status, slot, dup_ref); }
-}
-void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                       int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
-                       int32_t* queue, unsigned long long* q_tail, const double* src_hint, cudaStream_t s) {
-    if (n_cap > 0) { launch_k(k_hash_fixup, grid_for(n_cap, 256), 256, 0, s, H, src, idx, n_dev, n_cap, status, slot, flag, pool_idx, queue, q_tail, src_hint); }
+void launch_hash_upsert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                        int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, uint32_t flag,
+                        int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint,
+                        cudaStream_t s) {
+    if (n_cap > 0) {
+        launch_k(k_hash_upsert, grid_for(n_cap, 256), 256, 0, s, H, src, idx, n_dev, n_cap, status, slot, dup_ref, flag,
+                 pool_idx, queue, q_tail, src_hint);
+    }
 }
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
     if (n_pool > 0) { launch_k(k_hash_rebuild, grid_for(n_pool, 256), 256, 0, s, H, n_pool); }

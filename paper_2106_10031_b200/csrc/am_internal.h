@@ -189,11 +189,10 @@ struct HashSet {
 };
 // per-item outputs are indexed by source item ci (idx[i] or i): status 1 new / 0 present,
 // slot (new), dup_ref (present: pool index, or -2 - launch index of the in-flight winner)
-void launch_hash_insert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                        int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, cudaStream_t s);
-void launch_hash_fixup(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
-                       int64_t n_cap, const int32_t* status, const uint64_t* slot, uint32_t flag, int32_t* pool_idx,
-                       int32_t* queue, unsigned long long* q_tail, const double* src_hint, cudaStream_t s);
+void launch_hash_upsert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
+                        int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, uint32_t flag,
+                        int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint,
+                        cudaStream_t s);
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s);
 
 // per-iteration guard / queue state (am_hash.cu k_take)
