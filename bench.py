@@ -321,7 +321,7 @@ def main():
         for _ in range(max(args.warmup, 2)):
             cur = marching.march(net, cfg)
             prev = (cur, cur.welded_mesh())
-        del prev
+        del prev, cur
         e_times, m_times = [], []
         h2d = d2h = 0
         from paper_2106_10031_b200.network import to_blob

@@ -9,7 +9,7 @@ ncu --set full --clock-control none --import-source on -k regex:'^k_face$' -s 30
     python tools/profile_march.py > $O/ncu_face.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'^k_near$' -s 30 -c 1 -o $O/prof_near -f \
     python tools/profile_march.py > $O/ncu_near.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:'k_gemm_step<4>' -s 155 -c 1 -o $O/prof_gemm -f \
+ncu --set full --clock-control none --import-source on -k regex:k_gemm_step -s 400 -c 1 -o $O/prof_gemm -f \
     python tools/profile_march.py > $O/ncu_gemm.log 2>&1
 for r in prof_face prof_near prof_gemm; do ncu -i $O/$r.ncu-rep --page raw --csv > $O/$r.raw.csv 2>/dev/null; done
 AM_TRACE_ITERS=1 python tools/profile_march.py --timing > $O/trace_iters.log 2>&1

@@ -58,6 +58,7 @@ prev = None
 for _ in range(3):
     cur = marching.march(net, cfg)
     prev = (cur, cur.welded_mesh())
+del prev, cur
 for r in range(a.repeat):
     T.clear()
     flush.fill_(1)
@@ -67,5 +68,6 @@ for r in range(a.repeat):
     t1 = time.perf_counter()
     mesh = res.welded_mesh()
     t2 = time.perf_counter()
-    print(f"march {1e3 * (t1 - t0):.1f} ms  welded_mesh {1e3 * (t2 - t1):.1f} ms  total {1e3 * (t2 - t0):.1f} | "
+    import gc
+    print(f"gc counts {gc.get_count()} | march {1e3 * (t1 - t0):.1f} ms  welded_mesh {1e3 * (t2 - t1):.1f} ms  total {1e3 * (t2 - t0):.1f} | "
           + " ".join(f"{k} {v:.1f}" for k, v in T.items()))
