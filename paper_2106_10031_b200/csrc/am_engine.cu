@@ -46,7 +46,8 @@ int bisect_tree_points();
 int bisect_tree_depth();
 void launch_point_hints(const double* X, int64_t n, double tau, double* hints, cudaStream_t s);
 void launch_count_active(const int32_t* active, int64_t n, unsigned long long* cnt, cudaStream_t s);
-void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s);
+void launch_outbox_group(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner,
+                         unsigned long long* cnt, unsigned long long* cursor, uint64_t* dst, cudaStream_t s);
 void launch_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
                          unsigned long long* cnt, cudaStream_t s);
 
@@ -1123,22 +1124,19 @@ extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out, int64_t* h_counts) 
     int64_t n = (int64_t)e->hctr[C_NOUT];
     for (int r = 0; r < world; r++) h_counts[r] = 0;
     if (n > 0) {
-        DBuf<int32_t> own, idx;
+        if (world > 64) return fail(AM_ERR_ARG, "world size %d > 64", world);
+        DBuf<int32_t> own;
+        DBuf<unsigned long long> cnt;
         CK(own.reserve(n, e->stream));
-        CK(idx.reserve(n, e->stream));
-        launch_owner(e->outbox.p, n, KW, world, own.p, e->stream);
-        std::vector<int32_t> ho(n);
-        CK(cudaMemcpyAsync(ho.data(), own.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
+        CK(cnt.reserve(2 * world, e->stream));
+        CK(cudaMemsetAsync(cnt.p, 0, 2 * world * sizeof(unsigned long long), e->stream));
+        launch_outbox_group(e->outbox.p, n, KW, world, own.p, cnt.p, cnt.p + world, d_out, e->stream);
+        std::vector<unsigned long long> hc(world);
+        CK(cudaMemcpyAsync(hc.data(), cnt.p, world * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
-        std::vector<int32_t> order(n);
-        std::iota(order.begin(), order.end(), 0);
-        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return ho[a] < ho[b]; });
-        for (int64_t i = 0; i < n; i++) h_counts[ho[i]]++;
-        CK(cudaMemcpyAsync(idx.p, order.data(), n * 4, cudaMemcpyHostToDevice, e->stream));
-        launch_gather_keys(e->outbox.p, idx.p, n, KW, d_out, e->stream);
-        CK(cudaStreamSynchronize(e->stream));
+        for (int r = 0; r < world; r++) h_counts[r] = (int64_t)hc[r];
         own.release(e->stream);
-        idx.release(e->stream);
+        cnt.release(e->stream);
     }
     RC(set_counter(e, C_NOUT, 0));
     return AM_OK;

@@ -576,14 +576,40 @@ void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, i
     launch_k(k_zero_keys, grid_for(cap * KW, 256),  256,  0,  s, keys, n_dev, KW, cap, shape_w, shapes, value);
 }
 
-// owner rank of each key (outbox grouping)
-__global__ void k_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner) {
+// outbox grouped by owner rank on the device (counting sort over <= world buckets; the order
+// inside a bucket is free: the owner inserts the keys into an order-independent set)
+__global__ void k_outbox_hist(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner,
+                              unsigned long long* cnt) {
     pdl_enter();
-    GRID_STRIDE(i, n) owner[i] = key_owner(keys + i * KW, KW, world);
+    GRID_STRIDE(i, n) {
+        const int o = key_owner(keys + i * KW, KW, world);
+        owner[i] = o;
+        atomicAdd(cnt + o, 1ull);
+    }
 }
-void launch_owner(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner, cudaStream_t s) {
-    if (n > 0) { launch_k(k_owner, grid_for(n, 256), 256, 0, s, keys, n, KW, world, owner); }
+__global__ void k_outbox_scatter(const uint64_t* keys, int64_t n, int KW, int world, const int32_t* owner,
+                                 const unsigned long long* cnt, unsigned long long* cursor, uint64_t* dst) {
+    pdl_enter();
+    __shared__ unsigned long long base[64];
+    if (threadIdx.x == 0) {
+        unsigned long long b = 0;
+        for (int r = 0; r < world && r < 64; r++) { base[r] = b; b += cnt[r]; }
+    }
+    __syncthreads();
+    GRID_STRIDE(i, n) {
+        const int o = owner[i];
+        const unsigned long long p = base[o] + atomicAdd(cursor + o, 1ull);
+        for (int w = 0; w < KW; w++) dst[p * KW + w] = keys[i * KW + w];
+    }
 }
+void launch_outbox_group(const uint64_t* keys, int64_t n, int KW, int world, int32_t* owner,
+                         unsigned long long* cnt, unsigned long long* cursor, uint64_t* dst, cudaStream_t s) {
+    if (n <= 0) return;
+    launch_k(k_outbox_hist, grid_for(n, 256), 256, 0, s, keys, n, KW, world, owner, cnt);
+    launch_k(k_outbox_scatter, grid_for(n, 256), 256, 0, s, keys, n, KW, world, (const int32_t*)owner,
+             (const unsigned long long*)cnt, cursor, dst);
+}
+
 
 __global__ void k_filter_owned(const uint64_t* keys, int64_t n, int KW, int rank, int world, int32_t* idx,
                                unsigned long long* cnt) {
