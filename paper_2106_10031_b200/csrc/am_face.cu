@@ -353,6 +353,134 @@ __device__ __noinline__ void order_serial(FaceWarp* W, int nr, const double* fu)
     }
 }
 
+// Full path (cells whose hinted attempts did not converge, or without a hint): pass 1 clips a
+// large square by every row (box rows first), pass 2 collects C.  Out of line: rare, and its code
+// would otherwise sit between the hot phases in the instruction cache.
+struct FullOut { int nv, cur, status; double sc, tc, rho; int nC; unsigned long long core; int risky; };
+__device__ __noinline__ FullOut full_path(FaceWarp* W, const Ctx& c, const double* U, const double* Vv,
+                                          const double* P0, double tol_c, double tol_max, double band) {
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const int box0 = c.NB + c.M;
+    int nv = 0, cur = 0, status = 0;
+    double sc = 0.0, tc = 0.0, rho = 0.0;
+    int nC = 0, risky = 0;
+    unsigned long long core = 0;
+    auto clip = [&](double ca, double cb, double cg) {
+        Poly P{nv, cur, status, sc, tc, rho};
+        P = clip_poly(W, P, ca, cb, cg);
+        nv = P.nv; cur = P.cur; status = P.status; sc = P.sc; tc = P.tc; rho = P.rho;
+    };
+    auto cuts = [&](double a2, double b2, double g2) -> bool {
+        if ((a2 * sc + b2 * tc + g2) + rho <= 0.0) return false;   // |(a2, b2)| <= 1 for a unit row
+        double mx = -1e300;
+#pragma unroll 1
+        for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+        return mx > 0.0;
+    };
+    {
+        // initial square; then pass 1: box rows first, then neurons, then branch rows
+        nC = 0; core = 0;
+        double R = 64.0;
+        for (int k = 0; k < 3; k++) R = fmax(R, 64.0 * fmax(fabs(c.lo[k]), fabs(c.hi[k])));
+        if (lane < 4) {
+            W->ps[0][lane] = (lane == 0 || lane == 3) ? -R : R;
+            W->pt[0][lane] = (lane < 2) ? -R : R;
+        }
+        nv = 4; cur = 0; sc = 0.0; tc = 0.0;
+        rho = R * 1.4142135623730951 * (1.0 + 1e-12);
+        __syncwarp();
+        auto order = [&](int idx) { return idx < 6 ? box0 + idx : idx - 6; };
+        RawRow nxt = load_raw(c, lane < c.K ? order(lane) : c.K);
+        for (int base = 0; base < c.K && status == 0; base += 32) {
+            const int idx = base + lane;
+            const RawRow rr = nxt;
+            if (base + 32 < c.K) nxt = load_raw(c, idx + 32 < c.K ? order(idx + 32) : c.K);   // prefetch
+            double a2 = 0.0, b2 = 0.0, g2 = 0.0, nrm;
+            bool cut = false;
+            if (idx < c.K && row2d(c, order(idx), rr, U, Vv, P0, a2, b2, g2, nrm)) {
+                g2 -= tol_c;
+                cut = cuts(a2, b2, g2);
+            }
+            unsigned mask = __ballot_sync(full, cut);
+            while (mask && status == 0) {
+                int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                clip(__shfl_sync(full, a2, src), __shfl_sync(full, b2, src), __shfl_sync(full, g2, src));
+            }
+        }
+    }
+
+    // ------------------------------------------------ pass 2: remaining cuts + candidate set C'
+    // Every row: clip if it still cuts (rare after a good hint), then keep it in C' if it
+    // comes within the band of the current polygon.  Rows seen before a late clip were
+    // tested against a larger polygon -- a superset, which is still exact (C' only has to
+    // contain every row near the final P_tol).  core rows: within tol of P_tol (the only
+    // rows that can carry a vertex, an incident plane or an edge plane); the wider band up
+    // to 1.5 probe steps serves probe validation.  `risky` marks near-degenerate rows that
+    // make the validation margins meaningless (the cell then publishes nothing).
+    for (int attempt = 0; attempt < 2 && status == 0; attempt++) {
+        nC = 0;
+        core = 0;
+        risky = 0;
+        RawRow nx1 = load_raw(c, lane), nx2 = load_raw(c, lane + 32);
+        for (int base = 0; base < c.K && status == 0; base += 32) {
+            const int gr = base + lane;
+            const RawRow rr = nx1;
+            nx1 = nx2;
+            if (base + 64 < c.K) nx2 = load_raw(c, gr + 64);   // prefetch two batches ahead
+            double a2 = 0.0, b2 = 0.0, g2 = 0.0, nrm = 0.0;
+            bool kept = false;
+            if (gr < c.K) {
+                kept = row2d(c, gr, rr, U, Vv, P0, a2, b2, g2, nrm);
+                // near-degenerate neuron / branch functionals make the validation margins meaningless
+                if (rr.kind == 0 && nrm > 0.0 && nrm < kTinyNorm) risky = 1;
+                if (rr.kind == 1 && nrm < kTinyNorm) risky = 1;
+            }
+            bool cut = kept && cuts(a2, b2, g2 - tol_c);
+            unsigned cmask_cut = __ballot_sync(full, cut);
+            while (cmask_cut && status == 0) {
+                int src = __ffs(cmask_cut) - 1;
+                cmask_cut &= cmask_cut - 1;
+                clip(__shfl_sync(full, a2, src), __shfl_sync(full, b2, src), __shfl_sync(full, g2 - tol_c, src));
+            }
+            if (status != 0) break;
+            bool in = false, is_core = false;
+            if (kept && (a2 * sc + b2 * tc + g2) + rho >= -band) {
+                double mx = -1e300;
+#pragma unroll 1
+                for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
+                in = mx >= -band;
+                is_core = mx >= -tol_max - kCDelta;
+            }
+            unsigned mask = __ballot_sync(full, in);
+            unsigned cmask = __ballot_sync(full, is_core);
+            int pos = nC + __popc(mask & ((1u << lane) - 1u));
+            if (in && pos < CMAX) {
+                // exact unit row, same arithmetic as reference cells.py:146-160
+                double n[3], o;
+                get_row(c, gr, n, o);
+                W->cn[pos][0] = n[0]; W->cn[pos][1] = n[1]; W->cn[pos][2] = n[2]; W->cn[pos][3] = o;
+                W->cn[pos][4] = nrm;
+                W->cid[pos] = gr;
+            }
+            // core bits in C order
+            unsigned m = mask;
+            int k = nC;
+            while (m && k < CMAX) {
+                int l = __ffs(m) - 1;
+                m &= m - 1;
+                if ((cmask >> l) & 1u) core |= 1ull << k;
+                k++;
+            }
+            nC += __popc(mask);
+        }
+        risky = __any_sync(full, risky);
+        if (nC <= CMAX) break;   // else: late clips inflated C' -- once more against the final polygon
+    }
+    return FullOut{nv, cur, status, sc, tc, rho, nC, core, risky};
+}
+
 __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
@@ -396,22 +524,6 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
 
     int nv = 0, cur = 0;
     int status = face_ok ? 0 : 1;  // 0 ok, 1 empty, 2 overflow
-    double sc = 0.0, tc = 0.0, rho = 0.0;   // bounding circle of the current polygon
-
-    // warp-parallel Sutherland-Hodgman step (clip_poly, out of line: one copy of the code)
-    auto clip = [&](double ca, double cb, double cg) {
-        Poly P{nv, cur, status, sc, tc, rho};
-        P = clip_poly(W, P, ca, cb, cg);
-        nv = P.nv; cur = P.cur; status = P.status; sc = P.sc; tc = P.tc; rho = P.rho;
-    };
-    // does row (a2, b2, g2) (shifted by tol) cut the current polygon?
-    auto cuts = [&](double a2, double b2, double g2) -> bool {
-        if ((a2 * sc + b2 * tc + g2) + rho <= 0.0) return false;   // |(a2, b2)| <= 1 for a unit row
-        double mx = -1e300;
-#pragma unroll 1
-        for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
-        return mx > 0.0;
-    };
 
     // hint: a point on this cell's polygon (the edge midpoint through which the cell was
     // found: F is continuous across the shared plane, so it lies on this face plane too)
@@ -670,110 +782,9 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
 
     PMARK(4);
     if (status == 0 && !hinted_done) {
-        // initial square; then pass 1: box rows first, then neurons, then branch rows
-        nC = 0; core = 0;
-        double R = 64.0;
-        for (int k = 0; k < 3; k++) R = fmax(R, 64.0 * fmax(fabs(c.lo[k]), fabs(c.hi[k])));
-        if (lane < 4) {
-            W->ps[0][lane] = (lane == 0 || lane == 3) ? -R : R;
-            W->pt[0][lane] = (lane < 2) ? -R : R;
-        }
-        nv = 4; cur = 0; sc = 0.0; tc = 0.0;
-        rho = R * 1.4142135623730951 * (1.0 + 1e-12);
-        __syncwarp();
-        auto order = [&](int idx) { return idx < 6 ? box0 + idx : idx - 6; };
-        RawRow nxt = load_raw(c, lane < c.K ? order(lane) : c.K);
-        for (int base = 0; base < c.K && status == 0; base += 32) {
-            const int idx = base + lane;
-            const RawRow rr = nxt;
-            if (base + 32 < c.K) nxt = load_raw(c, idx + 32 < c.K ? order(idx + 32) : c.K);   // prefetch
-            double a2 = 0.0, b2 = 0.0, g2 = 0.0, nrm;
-            bool cut = false;
-            if (idx < c.K && row2d(c, order(idx), rr, U, Vv, P0, a2, b2, g2, nrm)) {
-                g2 -= tol_c;
-                cut = cuts(a2, b2, g2);
-            }
-            unsigned mask = __ballot_sync(full, cut);
-            while (mask && status == 0) {
-                int src = __ffs(mask) - 1;
-                mask &= mask - 1;
-                clip(__shfl_sync(full, a2, src), __shfl_sync(full, b2, src), __shfl_sync(full, g2, src));
-#ifdef AM_FACE_STATS
-                n_clip1++;
-#endif
-            }
-        }
-    }
-
-    // ------------------------------------------------ pass 2: remaining cuts + candidate set C'
-    // Every row: clip if it still cuts (rare after a good hint), then keep it in C' if it
-    // comes within the band of the current polygon.  Rows seen before a late clip were
-    // tested against a larger polygon -- a superset, which is still exact (C' only has to
-    // contain every row near the final P_tol).  core rows: within tol of P_tol (the only
-    // rows that can carry a vertex, an incident plane or an edge plane); the wider band up
-    // to 1.5 probe steps serves probe validation.  `risky` marks near-degenerate rows that
-    // make the validation margins meaningless (the cell then publishes nothing).
-    for (int attempt = 0; attempt < 2 && status == 0 && !hinted_done; attempt++) {
-        nC = 0;
-        core = 0;
-        risky = 0;
-        RawRow nx1 = load_raw(c, lane), nx2 = load_raw(c, lane + 32);
-        for (int base = 0; base < c.K && status == 0; base += 32) {
-            const int gr = base + lane;
-            const RawRow rr = nx1;
-            nx1 = nx2;
-            if (base + 64 < c.K) nx2 = load_raw(c, gr + 64);   // prefetch two batches ahead
-            double a2 = 0.0, b2 = 0.0, g2 = 0.0, nrm = 0.0;
-            bool kept = false;
-            if (gr < c.K) {
-                kept = row2d(c, gr, rr, U, Vv, P0, a2, b2, g2, nrm);
-                // near-degenerate neuron / branch functionals make the validation margins meaningless
-                if (rr.kind == 0 && nrm > 0.0 && nrm < kTinyNorm) risky = 1;
-                if (rr.kind == 1 && nrm < kTinyNorm) risky = 1;
-            }
-            bool cut = kept && cuts(a2, b2, g2 - tol_c);
-            unsigned cmask_cut = __ballot_sync(full, cut);
-            while (cmask_cut && status == 0) {
-                int src = __ffs(cmask_cut) - 1;
-                cmask_cut &= cmask_cut - 1;
-                clip(__shfl_sync(full, a2, src), __shfl_sync(full, b2, src), __shfl_sync(full, g2 - tol_c, src));
-#ifdef AM_FACE_STATS
-                n_clip2++;
-#endif
-            }
-            if (status != 0) break;
-            bool in = false, is_core = false;
-            if (kept && (a2 * sc + b2 * tc + g2) + rho >= -band) {
-                double mx = -1e300;
-#pragma unroll 1
-                for (int v = 0; v < nv; v++) mx = fmax(mx, a2 * W->ps[cur][v] + b2 * W->pt[cur][v] + g2);
-                in = mx >= -band;
-                is_core = mx >= -tol_max - kCDelta;
-            }
-            unsigned mask = __ballot_sync(full, in);
-            unsigned cmask = __ballot_sync(full, is_core);
-            int pos = nC + __popc(mask & ((1u << lane) - 1u));
-            if (in && pos < CMAX) {
-                // exact unit row, same arithmetic as reference cells.py:146-160
-                double n[3], o;
-                get_row(c, gr, n, o);
-                W->cn[pos][0] = n[0]; W->cn[pos][1] = n[1]; W->cn[pos][2] = n[2]; W->cn[pos][3] = o;
-                W->cn[pos][4] = nrm;
-                W->cid[pos] = gr;
-            }
-            // core bits in C order
-            unsigned m = mask;
-            int k = nC;
-            while (m && k < CMAX) {
-                int l = __ffs(m) - 1;
-                m &= m - 1;
-                if ((cmask >> l) & 1u) core |= 1ull << k;
-                k++;
-            }
-            nC += __popc(mask);
-        }
-        risky = __any_sync(full, risky);
-        if (nC <= CMAX) break;   // else: late clips inflated C' -- once more against the final polygon
+        const FullOut fo_ = full_path(W, c, U, Vv, P0, tol_c, tol_max, band);
+        nv = fo_.nv; cur = fo_.cur; status = fo_.status;
+        nC = fo_.nC; core = fo_.core; risky = fo_.risky;
     }
     PMARK(5);
     if (status == 0 && nC > CMAX) status = 2;
