@@ -65,7 +65,7 @@ __device__ __forceinline__ int swz(int row, int k) { return row * 16 + ((((k >> 
 // ----------------------------------------------------------- tensor maps
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld_elems) {
+int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld_elems, int box_rows) {
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -75,7 +75,7 @@ int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t col
     }
     cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t gstride[1] = {(cuuint64_t)(ld_elems * sizeof(double))};
-    cuuint32_t box[2] = {TB, BM};
+    cuuint32_t box[2] = {TB, (cuuint32_t)box_rows};
     cuuint32_t estride[2] = {1, 1};
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box,
                           estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -203,16 +203,30 @@ constexpr int XS1 = BK + 4;   // forward stage: per-point padded stride (bank-co
 
 constexpr int KCW = 10;    // cached state words per item and K segment (K rows <= 576)
 
-template <int C>
+// Tile shapes.  TM = 64: 8 warps (2 rows x 4 columns of 32 x 16 warp tiles), 64 x 64 outputs.
+// TM = 96 (compose steps with 64 < n_out <= 96, e.g. the 90-wide layers of configs[1]): 6 warps
+// (3 x 2), 96 x 32 outputs -- one row tile covers the layer, so the padding rows of a second
+// 64-row tile (26 of 64 useful) are not computed and the activation tile is staged once, not twice.
+template <int C, int TM>
+struct GT {
+    static constexpr int WM = TM / 32;                // warps along rows
+    static constexpr int WN = TM == 64 ? 4 : 2;       // warps along columns
+    static constexpr int NT = 32 * WM * WN;           // threads
+    static constexpr int TN = 16 * WN;                // columns per tile
+    static constexpr int NI = C == 4 ? TN / 4 : TN;   // items per tile
+};
+
+template <int C, int TM = BM>
 struct __align__(1024) GemmSmem {
-    static constexpr int XSZ = C == 4 ? 16 * XS4 : BN * XS1;
-    static constexpr int NI = C == 4 ? 16 : BN;   // items per tile
-    double w[NST][BK / TB][BM * TB];   // TMA destination: 2 boxes of 64 rows x 16 k, 128B-swizzled
+    static constexpr int NI = GT<C, TM>::NI;   // items per tile
+    static constexpr int TN = GT<C, TM>::TN;
+    static constexpr int XSZ = C == 4 ? NI * XS4 : TN * XS1;
+    double w[NST][BK / TB][TM * TB];   // TMA destination: 2 boxes of TM rows x 16 k, 128B-swizzled
     double x[NST][XSZ];            // raw activation tile
-    uint32_t mask[NST][BN];        // per item / point: the 32 state bits of the stage's K rows
+    uint32_t mask[NST][TN];        // per item / point: the 32 state bits of the stage's K rows
     uint64_t kc[2][NI][KCW];       // the tile's state words covering each K segment
     uint64_t bar[NST];
-    unsigned long long bits[BN][2];  // forward epilogue: per-column bit window
+    unsigned long long bits[TN][2];  // forward epilogue: per-column bit window
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -245,15 +259,17 @@ __device__ __forceinline__ uint32_t bits32(const uint64_t* key, int row, int val
     return m;
 }
 
-// One 64-row x 64-column output tile of layer L.st (all K chunks + epilogue).
-template <int C>
-__device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, uint64_t* keys, int64_t n,
+// One TM-row x TN-column output tile of layer L.st (all K chunks + epilogue).
+template <int C, int TM = BM>
+__device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch& L, uint64_t* keys, int64_t n,
                                           const CUtensorMap* tmWp, const CUtensorMap* tmVp, int m0, int64_t n0,
                                           uint32_t& gchunk) {
     const StepDev& st = L.st;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm = warp & 1, wn = warp >> 1;   // warp tile: rows wm*32 .. +31, columns wn*16 .. +15
+    using T = GT<C, TM>;
+    static_assert(C == 4 || TM == 64, "the forward stage uses 64-row tiles");
+    const int wm = warp % T::WM, wn = warp / T::WM;   // warp tile: rows wm*32 .. +31, columns wn*16 .. +15
     const bool lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && !(st.flags & AM_STEP_SC_FROM_INPUT);
     const int kc0 = (st.n_in + BK - 1) / BK;
     const int kc1 = lin ? (st.n_sin + BK - 1) / BK : 0;
@@ -266,7 +282,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
     {
         if (C == 1 && tid < BN) { S.bits[tid][0] = 0; S.bits[tid][1] = 0; }
         // state words of the tile's items covering both K segments (no global reads in issue())
-        constexpr int NI = GemmSmem<C>::NI;
+        constexpr int NI = GemmSmem<C, TM>::NI;
         const int64_t item0 = C == 4 ? n0 / 4 : n0;
         int wbeg[2], wcnt[2];
         wbeg[0] = st.in_row_off >> 6;
@@ -275,7 +291,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
         wcnt[1] = lin ? ((st.sin_row_off + st.n_sin - 1) >> 6) - wbeg[1] + 1 : 0;
         const bool cache_ok = wcnt[0] <= KCW && wcnt[1] <= KCW;
         if (cache_ok) {
-            for (int q = tid; q < 2 * NI * KCW; q += kThreads) {
+            for (int q = tid; q < 2 * NI * KCW; q += T::NT) {
                 const int sg = q / (NI * KCW), rem = q % (NI * KCW), il = rem / KCW, w = rem % KCW;
                 const int64_t item = item0 + il;
                 uint64_t v = 0;
@@ -294,24 +310,25 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
             const int n_src = seg0 ? st.n_in : st.n_sin;
             const int valid = n_src - k0;
             if (tid == 0) {   // boxes past the K extent are zero-filled and still complete their bytes
-                mbar_expect_tx(&S.bar[stage], BM * BK * sizeof(double));
+                mbar_expect_tx(&S.bar[stage], TM * BK * sizeof(double));
 #pragma unroll
                 for (int bx = 0; bx < BK / TB; bx++)
                     tma_load_2d(S.w[stage][bx], seg0 ? tmWp : tmVp, &S.bar[stage], k0 + bx * TB, m0);
             }
             if (C == 4) {
-                // 16 items x 1 KB; 4 x 16-B pieces per thread
+                // NI items x 1 KB in 16-B pieces
+                constexpr int NP = NI * 64;
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const int piece = q * kThreads + tid;    // 0..1023
+                for (int q = 0; q < (NP + T::NT - 1) / T::NT; q++) {
+                    const int piece = q * T::NT + tid;
                     const int it = piece >> 6, j = piece & 63;   // item, 16-B piece within its 1 KB
                     const int64_t item = n0 / 4 + it;
                     const int krow = j >> 1;                 // 2 pieces per row (4 doubles)
-                    if (item < n && krow < valid)
+                    if ((NP % T::NT == 0 || piece < NP) && item < n && krow < valid)
                         cp_async16(&S.x[stage][it * XS4 + j * 2],
                                    L.Z + (item * L.zs + src_row + k0) * 4 + j * 2);
                 }
-                if (tid < 16) {
+                if (tid < NI) {
                     const int64_t item = n0 / 4 + tid;
                     const int sg = seg0 ? 0 : 1;
                     S.mask[stage][tid] = item >= n ? 0u
@@ -369,8 +386,8 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
 #pragma unroll
                 for (int mi = 0; mi < 2; mi++) {
                     int r = wm * 32 + mi * 16 + pg;
-                    a[mi][0] = ws[(kk / TB) * BM * TB + swz(r, (kk % TB) + t)];
-                    a[mi][1] = ws[(kk / TB) * BM * TB + swz(r + 8, (kk % TB) + t)];
+                    a[mi][0] = ws[(kk / TB) * TM * TB + swz(r, (kk % TB) + t)];
+                    a[mi][1] = ws[(kk / TB) * TM * TB + swz(r + 8, (kk % TB) + t)];
                 }
 #pragma unroll
                 for (int nj = 0; nj < 2; nj++) {
@@ -514,20 +531,21 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C>& S, const LayerLaunch& L, 
 // NST-stage ring: W by TMA (mbarrier), the raw activations by cp.async, the state mask of the
 // chunk as 16-bit words -- applied when the B fragments are read, so padding rows and
 // inactive neurons contribute exact zeros.
-template <int C>
-__global__ void __launch_bounds__(kThreads, 2) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
+template <int C, int TM>
+__global__ void __launch_bounds__(GT<C, TM>::NT, 2) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
                                                         const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
     pdl_enter();
     extern __shared__ uint8_t smem_raw[];
     // 1 KB-aligned view derived by pointer arithmetic on the shared array (keeps LDS addressing)
-    GemmSmem<C>& S = *reinterpret_cast<GemmSmem<C>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    GemmSmem<C, TM>& S = *reinterpret_cast<GemmSmem<C, TM>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const StepDev& st = L.st;
     const int tid = threadIdx.x;
     const int64_t n = dev_count(L.n_dev, L.n_cap);
     if (n <= 0) return;
     uint64_t* keys = keys_at(L);
-    const int64_t ntx = (n * C + BN - 1) / BN;
-    const int nty = (st.n_out + BM - 1) / BM;
+    constexpr int TN = GT<C, TM>::TN;
+    const int64_t ntx = (n * C + TN - 1) / TN;
+    const int nty = (st.n_out + TM - 1) / TM;
     const int64_t ntiles = ntx * nty;
 
     if (tid < NST) mbar_init(&S.bar[tid], 1);
@@ -539,27 +557,33 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemm_step(const __grid_constant
 
     uint32_t gchunk = 0;  // chunks consumed by this CTA so far (stage ring + mbarrier phases)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = (int)(tile / ntx) * BM;
-        const int64_t n0 = (tile % ntx) * BN;
-        gemm_tile<C>(S, L, keys, n, &tmW, &tmV, m0, n0, gchunk);
+        const int m0 = (int)(tile / ntx) * TM;
+        const int64_t n0 = (tile % ntx) * TN;
+        gemm_tile<C, TM>(S, L, keys, n, &tmW, &tmV, m0, n0, gchunk);
     }
 }
 
-void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV, cudaStream_t s) {
-    if (L.n_cap <= 0) return;
-    int64_t cols = L.n_cap * C;
-    int64_t tiles = ((cols + BN - 1) / BN) * ((L.st.n_out + BM - 1) / BM);
-    int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : 2));
-    size_t smem = (C == 4 ? sizeof(GemmSmem<4>) : sizeof(GemmSmem<1>)) + 1024;
-    if (C == 4) {
-        static bool init = false;
-        if (!init) { cudaFuncSetAttribute(k_gemm_step<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
-        { launch_k(k_gemm_step<4>, (unsigned)grid, kThreads, smem, s, *tmW, tmV ? *tmV : *tmW, L); }
-    } else {
-        static bool init = false;
-        if (!init) { cudaFuncSetAttribute(k_gemm_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); init = true; }
-        { launch_k(k_gemm_step<1>, (unsigned)grid, kThreads, smem, s, *tmW, tmV ? *tmV : *tmW, L); }
+template <int C, int TM>
+static void launch_gemm_tm(const LayerLaunch& L, const CUtensorMap* tmW, const CUtensorMap* tmV, cudaStream_t s) {
+    using T = GT<C, TM>;
+    const int64_t cols = L.n_cap * C;
+    const int64_t tiles = ((cols + T::TN - 1) / T::TN) * ((L.st.n_out + TM - 1) / TM);
+    const int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : 2));
+    const size_t smem = sizeof(GemmSmem<C, TM>) + 1024;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_gemm_step<C, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init = true;
     }
+    launch_k(k_gemm_step<C, TM>, (unsigned)grid, T::NT, smem, s, *tmW, tmV ? *tmV : *tmW, L);
+}
+
+void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV, cudaStream_t s,
+                      const CUtensorMap* tmW96, const CUtensorMap* tmV96) {
+    if (L.n_cap <= 0) return;
+    if (C == 4 && tmW96) launch_gemm_tm<4, 96>(L, tmW96, tmV96, s);
+    else if (C == 4) launch_gemm_tm<4, 64>(L, tmW, tmV, s);
+    else launch_gemm_tm<1, 64>(L, tmW, tmV, s);
 }
 
 // ------------------------------------------------- fused composition (all steps)

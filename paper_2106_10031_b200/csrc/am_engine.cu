@@ -121,6 +121,8 @@ struct am_engine {
     std::vector<StepDev> sdev;
     std::vector<CUtensorMap> tmW, tmV;
     std::vector<int> tmV_ok;
+    std::vector<CUtensorMap> tmW96, tmV96;   // 96-row boxes of the compose steps with 64 < n_out <= 96
+    std::vector<int> narrow;
     DBuf<double> params, wpad;
     int n_shapes = 1, shape_w = -1, cur_shape = 0;   // batch of shapes (am_engine_set_shape_params)
     int fp32 = 0;                                    // fp32 mode (am_march_params.precision)
@@ -476,6 +478,11 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     e->tmW.resize(ns);
     e->tmV.resize(ns);
     e->tmV_ok.assign(ns, 0);
+    e->tmW96.resize(ns);
+    e->tmV96.resize(ns);
+    e->narrow.assign(ns, 0);
+    const char* nv = getenv("AM_NARROW96");
+    const bool use96 = !nv || atoi(nv) != 0;
     auto pad = [](int64_t x) { return (x + 15) / 16 * 16; };
     for (int s = 0; s < ns; s++) {
         const int64_t* st = &e->steps[(size_t)s * AM_STEP_FIELDS];
@@ -493,11 +500,18 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
                 return fail(AM_ERR_CUDA, "cuTensorMapEncodeTiled failed for step %d", s);
             e->flops_per_cell += 2.0 * d.n_out * d.n_in * 4;
             e->flops_per_point += 2.0 * d.n_out * d.n_in;
+            if (use96 && d.n_out > 64 && d.n_out <= 96) {
+                if (make_tmap_2d(&e->tmW96[s], d.W, d.n_out, d.n_in, d.ldw, 96) != 0)
+                    return fail(AM_ERR_CUDA, "cuTensorMapEncodeTiled failed for step %d", s);
+                e->narrow[s] = 1;
+            }
         }
         if (d.V && !(d.flags & AM_STEP_SC_FROM_INPUT)) {
             if (make_tmap_2d(&e->tmV[s], d.V, d.n_out, d.n_sin, d.ldv) != 0)
                 return fail(AM_ERR_CUDA, "cuTensorMapEncodeTiled failed for shortcut of step %d", s);
             e->tmV_ok[s] = 1;
+            if (e->narrow[s] && make_tmap_2d(&e->tmV96[s], d.V, d.n_out, d.n_sin, d.ldv, 96) != 0)
+                return fail(AM_ERR_CUDA, "cuTensorMapEncodeTiled failed for shortcut of step %d", s);
             e->flops_per_cell += 2.0 * d.n_out * d.n_sin * 4;
             e->flops_per_point += 2.0 * d.n_out * d.n_sin;
         }
@@ -676,7 +690,9 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsig
         L.shape_w = e->shape_w;
         L.fp32 = e->fp32;
         if (L.st.flags & AM_STEP_FIRST) launch_input_step(L, C, e->stream);
-        else launch_gemm_step(L, C, &e->tmW[s], e->tmV_ok[s] ? &e->tmV[s] : nullptr, e->stream);
+        else launch_gemm_step(L, C, &e->tmW[s], e->tmV_ok[s] ? &e->tmV[s] : nullptr, e->stream,
+                              e->narrow[s] ? &e->tmW96[s] : nullptr,
+                              e->narrow[s] && e->tmV_ok[s] ? &e->tmV96[s] : nullptr);
     }
     CK(cudaGetLastError());
     return AM_OK;

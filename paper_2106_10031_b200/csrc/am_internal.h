@@ -164,8 +164,9 @@ struct FusedCompose {
 };
 void launch_compose_fused(const FusedCompose& F, cudaStream_t s);
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV,
-                      cudaStream_t s);
-int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld_elems);
+                      cudaStream_t s, const CUtensorMap* tmW96 = nullptr, const CUtensorMap* tmV96 = nullptr);
+int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld_elems,
+                 int box_rows = 64);
 
 // device counters shared by the iteration kernels
 enum Ctr {
