@@ -353,6 +353,46 @@ def main():
                "api": "paper_2106_10031_b200.march(net, MarchConfig(seeds=64)).welded_mesh() from host buffers, "
                       "wall clock (host-synchronous API)"}
 
+    elif world > 1:
+        # the multi-GPU public call on every rank, from host buffers: march_sharded(net, cfg) =
+        # seeding, the sharded BFS with its all-to-all frontier exchange, and each rank's sorted
+        # share of the result (its owned cells with their polygons) back to host; mesh time =
+        # the slowest rank
+        from paper_2106_10031_b200.distributed import march_sharded
+        from paper_2106_10031_b200.network import to_blob
+        cfg = marching.MarchConfig(seeds=args.seeds, rng_seed=0, bbox=bbox)
+        for _ in range(max(args.warmup, 2)):
+            r = march_sharded(net, cfg)
+        del r
+        e_times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            r = march_sharded(net, cfg)
+            t1 = time.perf_counter()
+            barrier()
+            e_times.append((t1 - t0) * 1e3)
+        blob = to_blob(net)
+        h2d_l = (2 * blob.params.nbytes + blob.steps.nbytes + blob.subs.nbytes + args.seeds * 64 * 3 * 8
+                 + args.seeds * 2 * 3 * 8)
+        d2h_l = r.keys.nbytes + r.nverts.nbytes + r.verts.nbytes + r.edge_nrefs.nbytes + r.edge_refs.nbytes
+        agg = torch.tensor([float(np.mean(e_times)), float(r.report.cells_visited), float(h2d_l), float(d2h_l)],
+                           dtype=torch.float64, device=dev)
+        emax = agg[:1].clone()
+        dist.all_reduce(emax, op=dist.ReduceOp.MAX)
+        esum = agg[1:].clone()
+        dist.all_reduce(esum, op=dist.ReduceOp.SUM)
+        e_ms = float(emax.item())
+        e_cells, h2d, d2h = (float(x) for x in esum.tolist())
+        e2e = {"value": e_cells / (e_ms * 1e-3), "unit": "cells/s", "ms_per_step": e_ms,
+               "mesh_time_s": e_ms * 1e-3, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "cells": int(e_cells),
+               "api": "paper_2106_10031_b200.distributed.march_sharded(net, MarchConfig(seeds=64)) on every "
+                      "rank from host buffers (each rank's sorted owned cells + polygons to host; no weld), "
+                      "wall clock, max over ranks"}
+
     # --------------------------------------- the largest MLP (configs[2]), capped sample
     others = {}
     if world == 1 and not args.no_extra:

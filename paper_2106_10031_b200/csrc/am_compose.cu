@@ -207,8 +207,16 @@ constexpr int KCW = 10;    // cached state words per item and K segment (K rows 
 // TM = 96 (compose steps with 64 < n_out <= 96, e.g. the 90-wide layers of configs[1]): 6 warps
 // (3 x 2), 96 x 32 outputs -- one row tile covers the layer, so the padding rows of a second
 // 64-row tile (26 of 64 useful) are not computed and the activation tile is staged once, not twice.
+#ifndef AM_NST96
+#define AM_NST96 3
+#endif
+#ifndef AM_CPS96
+#define AM_CPS96 2
+#endif
 template <int C, int TM>
 struct GT {
+    static constexpr int NS = TM == 96 ? AM_NST96 : NST;   // pipeline stages
+    static constexpr int CPS = TM == 96 ? AM_CPS96 : 2;    // resident CTAs per SM
     static constexpr int WM = TM / 32;                // warps along rows
     static constexpr int WN = TM == 64 ? 4 : 2;       // warps along columns
     static constexpr int NT = 32 * WM * WN;           // threads
@@ -221,11 +229,12 @@ struct __align__(1024) GemmSmem {
     static constexpr int NI = GT<C, TM>::NI;   // items per tile
     static constexpr int TN = GT<C, TM>::TN;
     static constexpr int XSZ = C == 4 ? NI * XS4 : TN * XS1;
-    double w[NST][BK / TB][TM * TB];   // TMA destination: 2 boxes of TM rows x 16 k, 128B-swizzled
-    double x[NST][XSZ];            // raw activation tile
-    uint32_t mask[NST][TN];        // per item / point: the 32 state bits of the stage's K rows
+    static constexpr int NS = GT<C, TM>::NS;
+    double w[NS][BK / TB][TM * TB];   // TMA destination: 2 boxes of TM rows x 16 k, 128B-swizzled
+    double x[NS][XSZ];            // raw activation tile
+    uint32_t mask[NS][TN];        // per item / point: the 32 state bits of the stage's K rows
     uint64_t kc[2][NI][KCW];       // the tile's state words covering each K segment
-    uint64_t bar[NST];
+    uint64_t bar[NS];
     unsigned long long bits[TN][2];  // forward epilogue: per-column bit window
 };
 
@@ -303,7 +312,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
 
         // issue chunk c of this tile into its ring stage
         auto issue = [&](int c) {
-            const int stage = (gchunk + c) % NST;
+            const int stage = (gchunk + c) % T::NS;
             const bool seg0 = c < kc0;
             const int k0 = (seg0 ? c : c - kc0) * BK;
             const int src_row = seg0 ? st.in_row_off : st.sin_row_off;
@@ -364,6 +373,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
 
         // NST-1 chunks in flight; the stage refilled at iteration c is the one chunk c-1 used,
         // which every warp has finished once it passes iteration c's barrier (one barrier per chunk)
+        constexpr int NST = T::NS;
         const int pro = nchunks < NST - 1 ? nchunks : NST - 1;
         for (int c = 0; c < pro; c++) issue(c);
         // fragment row g reads tile row pg: the 4 rows x 2 16-B chunks of a half-warp then fall on
@@ -532,7 +542,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
 // chunk as 16-bit words -- applied when the B fragments are read, so padding rows and
 // inactive neurons contribute exact zeros.
 template <int C, int TM>
-__global__ void __launch_bounds__(GT<C, TM>::NT, 2) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
+__global__ void __launch_bounds__(GT<C, TM>::NT, GT<C, TM>::CPS) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
                                                         const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
     pdl_enter();
     extern __shared__ uint8_t smem_raw[];
@@ -548,7 +558,7 @@ __global__ void __launch_bounds__(GT<C, TM>::NT, 2) k_gemm_step(const __grid_con
     const int nty = (st.n_out + TM - 1) / TM;
     const int64_t ntiles = ntx * nty;
 
-    if (tid < NST) mbar_init(&S.bar[tid], 1);
+    if (tid < GT<C, TM>::NS) mbar_init(&S.bar[tid], 1);
     if (tid == 0) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
@@ -568,7 +578,7 @@ static void launch_gemm_tm(const LayerLaunch& L, const CUtensorMap* tmW, const C
     using T = GT<C, TM>;
     const int64_t cols = L.n_cap * C;
     const int64_t tiles = ((cols + T::TN - 1) / T::TN) * ((L.st.n_out + TM - 1) / TM);
-    const int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : 2));
+    const int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : T::CPS));
     const size_t smem = sizeof(GemmSmem<C, TM>) + 1024;
     static bool init = false;
     if (!init) {

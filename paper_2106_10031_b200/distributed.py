@@ -17,6 +17,8 @@ partitioned instead, and the union over ranks equals the single-GPU set.
 
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -96,3 +98,38 @@ class ShardedMarcher:
                 break
         self.waves = waves
         return waves
+
+
+_MARCHERS: dict = {}
+
+
+def march_sharded(net: AnyNetwork, config=None) -> "MarchResult":
+    """Multi-GPU ``march`` (call it on every rank, one process per GPU): this rank's share of the
+    march -- the visited cells it owns (hash(state) mod world), sorted in the reference's order
+    (marching.py:346-359), with their polygons, on the host.  The union of the ranks' results is
+    ``march(net, config)``'s result.  Marchers are kept per architecture and re-used with the new
+    weights uploaded, like ``march``'s engines."""
+    from .engine import architecture_key
+    from .marching import MarchConfig, collect_result
+    from .network import to_blob
+    config = config or MarchConfig()
+    t0 = time.perf_counter()
+    key = (architecture_key(to_blob(net)), tuple(map(tuple, config.bbox)), config.max_cells, config.tol_cell,
+           config.tol_weld, config.probe_delta, config.batch_cells, config.mem_budget, config.precision,
+           dist.get_rank(), dist.get_world_size(), torch.cuda.current_device())
+    sm = _MARCHERS.get(key)
+    if sm is None:
+        sm = ShardedMarcher(net, bbox=config.bbox, max_cells=config.max_cells, tol_cell=config.tol_cell,
+                            tol_weld=config.tol_weld, probe_delta=config.probe_delta,
+                            batch_cells=config.batch_cells, mem_budget=config.mem_budget,
+                            precision=config.precision)
+        _MARCHERS.clear()
+        _MARCHERS[key] = sm
+    else:
+        sm.load_network(net)
+    if config.seed_points is not None:
+        seeds = np.asarray(config.seed_points, dtype=np.float64).reshape(-1, 3)
+    else:
+        seeds = sm.sample_seeds(config.seeds, rng_seed=config.rng_seed, scheme=config.scheme)
+    waves = sm.run(seeds)
+    return collect_result(sm.engine, seeds, t0, waves, config.threads)
