@@ -208,7 +208,7 @@ constexpr int KCW = 10;    // cached state words per item and K segment (K rows 
 // (3 x 2), 96 x 32 outputs -- one row tile covers the layer, so the padding rows of a second
 // 64-row tile (26 of 64 useful) are not computed and the activation tile is staged once, not twice.
 #ifndef AM_NST96
-#define AM_NST96 3
+#define AM_NST96 2
 #endif
 #ifndef AM_CPS96
 #define AM_CPS96 2
