@@ -213,10 +213,17 @@ constexpr int KCW = 10;    // cached state words per item and K segment (K rows 
 #ifndef AM_CPS96
 #define AM_CPS96 2
 #endif
+// AM_WRES96 (off: measured neutral, 25.8-26.0 vs 25.8-25.9 ms): the 96-row tile keeps the whole layer's W (<= 3 K chunks) resident in shared memory,
+// loaded by TMA once per CTA (before the grid dependency wait), instead of re-streaming it per tile
+#ifndef AM_WRES96
+#define AM_WRES96 0
+#endif
 template <int C, int TM>
 struct GT {
     static constexpr int NS = TM == 96 ? AM_NST96 : NST;   // pipeline stages
     static constexpr int CPS = TM == 96 ? AM_CPS96 : 2;    // resident CTAs per SM
+    static constexpr bool WRES = TM == 96 && AM_WRES96;    // W resident for layers of <= WS chunks
+    static constexpr int WS = WRES ? (NS > 3 ? NS : 3) : NS;   // W slots
     static constexpr int WM = TM / 32;                // warps along rows
     static constexpr int WN = TM == 64 ? 4 : 2;       // warps along columns
     static constexpr int NT = 32 * WM * WN;           // threads
@@ -230,11 +237,12 @@ struct __align__(1024) GemmSmem {
     static constexpr int TN = GT<C, TM>::TN;
     static constexpr int XSZ = C == 4 ? NI * XS4 : TN * XS1;
     static constexpr int NS = GT<C, TM>::NS;
-    double w[NS][BK / TB][TM * TB];   // TMA destination: 2 boxes of TM rows x 16 k, 128B-swizzled
+    double w[GT<C, TM>::WS][BK / TB][TM * TB];   // TMA destination: 2 boxes of TM rows x 16 k, 128B-swizzled
     double x[NS][XSZ];            // raw activation tile
     uint32_t mask[NS][TN];        // per item / point: the 32 state bits of the stage's K rows
     uint64_t kc[2][NI][KCW];       // the tile's state words covering each K segment
     uint64_t bar[NS];
+    uint64_t wbar;                  // resident W loaded
     unsigned long long bits[TN][2];  // forward epilogue: per-column bit window
 };
 
@@ -272,7 +280,7 @@ __device__ __forceinline__ uint32_t bits32(const uint64_t* key, int row, int val
 template <int C, int TM = BM>
 __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch& L, uint64_t* keys, int64_t n,
                                           const CUtensorMap* tmWp, const CUtensorMap* tmVp, int m0, int64_t n0,
-                                          uint32_t& gchunk) {
+                                          uint32_t& gchunk, bool wres = false) {
     const StepDev& st = L.st;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -318,7 +326,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
             const int src_row = seg0 ? st.in_row_off : st.sin_row_off;
             const int n_src = seg0 ? st.n_in : st.n_sin;
             const int valid = n_src - k0;
-            if (tid == 0) {   // boxes past the K extent are zero-filled and still complete their bytes
+            if (tid == 0 && !wres) {   // boxes past the K extent are zero-filled and still complete their bytes
                 mbar_expect_tx(&S.bar[stage], TM * BK * sizeof(double));
 #pragma unroll
                 for (int bx = 0; bx < BK / TB; bx++)
@@ -385,10 +393,11 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
             const int s = gc % NST;
             const int committed = (c + NST - 2 < nchunks - 1) ? c + NST - 2 : nchunks - 1;
             cp_async_wait(committed - c);
-            mbar_wait(&S.bar[s], (gc / NST) & 1);
+            if (wres) mbar_wait(&S.wbar, 0);
+            else mbar_wait(&S.bar[s], (gc / NST) & 1);
             __syncthreads();
             if (c + NST - 1 < nchunks) issue(c + NST - 1);
-            const double* ws = S.w[s][0];
+            const double* ws = S.w[wres ? c : s][0];
             const double* xsm = S.x[s];
 #pragma unroll
             for (int kk = 0; kk < BK; kk += 4) {
@@ -544,33 +553,55 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
 template <int C, int TM>
 __global__ void __launch_bounds__(GT<C, TM>::NT, GT<C, TM>::CPS) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
                                                         const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
-    pdl_enter();
     extern __shared__ uint8_t smem_raw[];
     // 1 KB-aligned view derived by pointer arithmetic on the shared array (keeps LDS addressing)
     GemmSmem<C, TM>& S = *reinterpret_cast<GemmSmem<C, TM>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    using T = GT<C, TM>;
     const StepDev& st = L.st;
     const int tid = threadIdx.x;
-    const int64_t n = dev_count(L.n_dev, L.n_cap);
-    if (n <= 0) return;
-    uint64_t* keys = keys_at(L);
-    constexpr int TN = GT<C, TM>::TN;
-    const int64_t ntx = (n * C + TN - 1) / TN;
-    const int nty = (st.n_out + TM - 1) / TM;
-    const int64_t ntiles = ntx * nty;
+    const bool lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && !(st.flags & AM_STEP_SC_FROM_INPUT);
+    const int kc0 = (st.n_in + BK - 1) / BK;
+    const int nchunks = kc0 + (lin ? (st.n_sin + BK - 1) / BK : 0);
+    // W is a weight (not produced by the preceding kernels): its TMA is issued before the grid
+    // dependency wait, so it overlaps the predecessor's tail
+    const bool wres = T::WRES && st.n_out <= TM && nchunks <= T::WS;
 
-    if (tid < GT<C, TM>::NS) mbar_init(&S.bar[tid], 1);
+    if (tid < T::NS) mbar_init(&S.bar[tid], 1);
+    if (tid == T::NS) mbar_init(&S.wbar, 1);
     if (tid == 0) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     }
     __syncthreads();
+    if (wres && tid == 0) {
+        mbar_expect_tx(&S.wbar, (uint32_t)(nchunks * TM * BK * sizeof(double)));
+        for (int c = 0; c < nchunks; c++) {
+            const bool seg0 = c < kc0;
+            const int k0 = (seg0 ? c : c - kc0) * BK;
+#pragma unroll
+            for (int bx = 0; bx < BK / TB; bx++)
+                tma_load_2d(S.w[c][bx], seg0 ? &tmW : &tmV, &S.wbar, k0 + bx * TB, 0);
+        }
+    }
+    pdl_enter();
+    const int64_t n = dev_count(L.n_dev, L.n_cap);
+    if (n <= 0) {
+        if (wres) mbar_wait(&S.wbar, 0);   // no bulk copy may be in flight when the CTA exits
+        return;
+    }
+    uint64_t* keys = keys_at(L);
+    constexpr int TN = T::TN;
+    const int64_t ntx = (n * C + TN - 1) / TN;
+    const int nty = (st.n_out + TM - 1) / TM;
+    const int64_t ntiles = ntx * nty;
 
     uint32_t gchunk = 0;  // chunks consumed by this CTA so far (stage ring + mbarrier phases)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int m0 = (int)(tile / ntx) * TM;
         const int64_t n0 = (tile % ntx) * TN;
-        gemm_tile<C, TM>(S, L, keys, n, &tmW, &tmV, m0, n0, gchunk);
+        gemm_tile<C, TM>(S, L, keys, n, &tmW, &tmV, m0, n0, gchunk, wres);
     }
+    if (wres && blockIdx.x >= ntiles) mbar_wait(&S.wbar, 0);
 }
 
 template <int C, int TM>
