@@ -827,8 +827,8 @@ static int launch_iteration(am_engine* e) {
     const bool multi = e->P.world > 1;
 
     launch_take(I, s);
-    launch_gather_batch(e->pool.p, e->pool_hint.p, e->batch_pool.p, c + C_NR, B, e->KW, e->ckey.p, e->ckey_hint.p,
-                        e->changed.p, e->canon_pos.p, s);
+    launch_gather_batch(e->pool.p, e->pool_hint.p, e->queue.p, c, e->batch_pool.p, B, e->KW, e->ckey.p,
+                        e->ckey_hint.p, e->changed.p, e->canon_pos.p, s);
     if (tm) cudaEventRecord(e->ev[0], s);
     RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B));
     if (tm) cudaEventRecord(e->ev[1], s);

@@ -138,7 +138,6 @@ void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
 // worst case of what the iteration can produce fits every buffer.
 __global__ void k_take(IterState I) {
     pdl_enter();
-    __shared__ long long s_nR;
     unsigned long long* c = I.ctr;
     if (threadIdx.x == 0) {
         long long head = (long long)c[C_QHEAD], tail = (long long)c[C_QTAIL];
@@ -174,29 +173,29 @@ __global__ void k_take(IterState I) {
         c[C_NX] = 0; c[C_NF] = 0; c[C_NEMIT] = 0; c[C_NLOCAL] = 0;
         c[C_NPREC] = 0; c[C_NKEEP] = 0; c[C_NPLOCAL] = 0; c[C_FCURSOR] = 0;
         c[C_ITER] += nR > 0 ? 1ull : 0ull;
-        s_nR = nR;
+        // the batch is queue[head, head + nR): k_gather_batch copies it out (batch_pool)
+        c[C_QHEAD] = (unsigned long long)((long long)c[C_QHEAD] + nR);
     }
-    __syncthreads();
-    long long head = (long long)c[C_QHEAD];
-    for (long long b = threadIdx.x; b < s_nR; b += blockDim.x) I.batch_pool[b] = I.queue[head + b];
-    __syncthreads();
-    if (threadIdx.x == 0) c[C_QHEAD] = (unsigned long long)(head + s_nR);
 }
 
-// ckey[b] = pool[batch_pool[b]]; reset per-item flags
-__global__ void k_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
-                               const unsigned long long* n_dev, int64_t n_cap, int KW, uint64_t* ckey,
-                               double* ckey_hint, int32_t* changed, int32_t* canon_pos) {
+// batch_pool[b] = queue[head0 + b] (the batch k_take dequeued), ckey[b] = pool[batch_pool[b]];
+// reset per-item flags
+__global__ void k_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
+                               const unsigned long long* ctr, int32_t* batch_pool, int64_t n_cap, int KW,
+                               uint64_t* ckey, double* ckey_hint, int32_t* changed, int32_t* canon_pos) {
     pdl_enter();
-    const int64_t n = dev_count(n_dev, n_cap);
+    const int64_t n = dev_count(ctr + C_NR, n_cap);
+    const int64_t head0 = (int64_t)ctr[C_QHEAD] - n;
     GRID_STRIDE(t, n * KW) {
         int64_t b = t / KW;
         int w = (int)(t - b * KW);
-        ckey[t] = pool[(int64_t)batch_pool[b] * KW + w];
+        const int32_t p = queue[head0 + b];
+        ckey[t] = pool[(int64_t)p * KW + w];
         if (w == 0) {
+            batch_pool[b] = p;
             changed[b] = 0;
             canon_pos[b] = -1;
-            reinterpret_cast<double4*>(ckey_hint)[b] = reinterpret_cast<const double4*>(pool_hint)[batch_pool[b]];
+            reinterpret_cast<double4*>(ckey_hint)[b] = reinterpret_cast<const double4*>(pool_hint)[p];
         }
     }
 }
@@ -284,12 +283,12 @@ __global__ void k_route_emitted(const uint64_t* scratch, const unsigned long lon
     }
 }
 
-void launch_take(const IterState& I, cudaStream_t s) { launch_k(k_take, 1, 1024, 0, s, I); }
-void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* batch_pool,
-                         const unsigned long long* n_dev, int64_t n_cap, int KW, uint64_t* ckey, double* ckey_hint,
-                         int32_t* changed, int32_t* canon_pos, cudaStream_t s) {
-    launch_k(k_gather_batch, grid_for(n_cap * KW, 256),  256,  0,  s, pool, pool_hint, batch_pool, n_dev, n_cap, KW, ckey,
-                                                              ckey_hint, changed, canon_pos);
+void launch_take(const IterState& I, cudaStream_t s) { launch_k(k_take, 1, 32, 0, s, I); }
+void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
+                         const unsigned long long* ctr, int32_t* batch_pool, int64_t n_cap, int KW, uint64_t* ckey,
+                         double* ckey_hint, int32_t* changed, int32_t* canon_pos, cudaStream_t s) {
+    launch_k(k_gather_batch, grid_for(n_cap * KW, 256), 256, 0, s, pool, pool_hint, queue, ctr, batch_pool, n_cap, KW,
+             ckey, ckey_hint, changed, canon_pos);
 }
 void launch_route_changed(const uint64_t* ckey, const int32_t* changed, const unsigned long long* n_dev, int64_t n_cap,
                           int KW, int rank, int world, int32_t* X, unsigned long long* nX, uint64_t* outbox,
