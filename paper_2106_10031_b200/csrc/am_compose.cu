@@ -192,6 +192,45 @@ void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
     else { launch_k(k_input_step<1>, (unsigned)blocks, 256, 0, s, L); }
 }
 
+// ------------------------------------------- batch gather fused with the input step
+// One warp per batch item: the item's pool index is read from the queue slice k_take dequeued
+// (queue[QHEAD - nR + b]), its key words and hint are gathered (k_gather_batch's work), and the
+// warp's lanes then compute the item's layer-1 rows exactly as k_input_step does (input_elem),
+// so a BFS iteration launches one kernel less.  __syncwarp orders the gathered key and the reset
+// flags before the lanes' canonical-bit updates of the same item.
+__global__ void k_gather_input(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
+                               const unsigned long long* ctr, int32_t* batch_pool, double* ckey_hint,
+                               int32_t* canon_pos, LayerLaunch L) {
+    pdl_enter();
+    const int64_t n = dev_count(ctr + C_NR, L.n_cap);
+    const int64_t head0 = (int64_t)ctr[C_QHEAD] - n;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    uint64_t* keys = L.keys;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < n; b += nw) {
+        const int32_t p = queue[head0 + b];
+        for (int w = lane; w < L.KW; w += 32) keys[b * L.KW + w] = pool[(int64_t)p * L.KW + w];
+        if (lane == 0) {
+            batch_pool[b] = p;
+            L.changed[b] = 0;
+            canon_pos[b] = -1;
+            reinterpret_cast<double4*>(ckey_hint)[b] = reinterpret_cast<const double4*>(pool_hint)[p];
+        }
+        __syncwarp();
+        for (int r = lane; r < L.st.n_out; r += 32) input_elem<4>(L, keys, b, r);
+        __syncwarp();
+    }
+}
+
+void launch_gather_input(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
+                         const unsigned long long* ctr, int32_t* batch_pool, double* ckey_hint, int32_t* canon_pos,
+                         const LayerLaunch& L, cudaStream_t s) {
+    if (L.n_cap <= 0) return;
+    const int64_t blocks = std::min<int64_t>((L.n_cap + 7) / 8, (int64_t)num_sms() * 16);
+    launch_k(k_gather_input, (unsigned)blocks, 256, 0, s, pool, pool_hint, queue, ctr, batch_pool, ckey_hint,
+             canon_pos, L);
+}
+
 // ----------------------------------------------------------- GEMM step
 
 #ifndef AM_NST

@@ -196,6 +196,7 @@ struct am_engine {
     int dg_shapes = -3;   // -2: per-point shapes, else the engine's current shape at capture
     std::vector<const void*> dg_ptrs;
     unsigned long long dg_kernels = 0;
+    bool gather_input = true;   // k_gather_input: batch gather + input step in one launch
     int graph_batch = 16;   // iterations replayed per host synchronisation (A/B: 8 -> 25.7 ms, 16 -> 25.1, 24 -> 25.0)
     int grid_cap = 0;    // >0: CTAs per SM for persistent GEMM launches
     unsigned long long graph_kernels = 0;
@@ -558,6 +559,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_TAU_GROW")) e->tau_grow = atof(v);
     if (const char* v = getenv("AM_BISECT_TREE")) e->bisect_tree = atoi(v) != 0;
     if (const char* v = getenv("AM_GRAPH_BATCH")) e->graph_batch = std::max(1, atoi(v));
+    if (const char* v = getenv("AM_GATHER_INPUT")) e->gather_input = atoi(v) != 0;
     CK(e->near_n.reserve(e->B, s));
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
@@ -674,8 +676,9 @@ extern "C" int am_engine_reset(am_engine* e) {
 // ----------------------------------------------------- compose / forward
 // every hidden step for the items; C = 4 (cells) or 1 (points); n_dev null -> n_cap items
 static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsigned long long* key_off,
-                     int32_t* changed, const double* pts, const unsigned long long* n_dev, int64_t n_cap) {
-    for (size_t s = 0; s < e->sdev.size(); s++) {
+                     int32_t* changed, const double* pts, const unsigned long long* n_dev, int64_t n_cap,
+                     size_t first = 0) {
+    for (size_t s = first; s < e->sdev.size(); s++) {
         LayerLaunch L;
         L.st = e->sdev[s];
         L.Z = Z;
@@ -699,8 +702,25 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsig
     return AM_OK;
 }
 
+// step 0 launch of the compose path (input step: the caller may fuse it with its gather)
+static LayerLaunch first_step_launch(am_engine* e, uint64_t* keys, int32_t* changed, double* Z,
+                                     const unsigned long long* n_dev, int64_t n_cap) {
+    LayerLaunch L{};
+    L.st = e->sdev[0];
+    L.Z = Z; L.keys = keys; L.key_off = nullptr; L.changed = changed; L.pts = nullptr;
+    L.n_dev = n_dev; L.n_cap = n_cap; L.KW = e->KW; L.zs = e->zs; L.grid_cap = e->grid_cap;
+    L.shape_w = e->shape_w; L.fp32 = e->fp32;
+    return L;
+}
+
+static bool gather_fuses_input(const am_engine* e) {
+    const int ns = (int)e->sdev.size();
+    return e->gather_input && ns > 0 && (e->sdev[0].flags & AM_STEP_FIRST) &&
+           !(e->compose_fused && ns <= kMaxFusedSteps);
+}
+
 static int compose(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, double* faces,
-                   const unsigned long long* n_dev, int64_t n_cap) {
+                   const unsigned long long* n_dev, int64_t n_cap, size_t first = 0) {
     const int ns = (int)e->sdev.size();
     if (e->compose_fused && ns <= kMaxFusedSteps) {
         FusedCompose* F = e->fused.get();
@@ -720,7 +740,7 @@ static int compose(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, do
         CK(cudaGetLastError());
         return AM_OK;
     }
-    RC(run_steps(e, 4, Z, keys, nullptr, changed, nullptr, n_dev, n_cap));
+    RC(run_steps(e, 4, Z, keys, nullptr, changed, nullptr, n_dev, n_cap, first));
     launch_face_head_dev(Z, keys, faces, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->shape_w, e->fp32, e->stream);
     CK(cudaGetLastError());
     return AM_OK;
@@ -827,10 +847,17 @@ static int launch_iteration(am_engine* e) {
     const bool multi = e->P.world > 1;
 
     launch_take(I, s);
-    launch_gather_batch(e->pool.p, e->pool_hint.p, e->queue.p, c, e->batch_pool.p, B, e->KW, e->ckey.p,
-                        e->ckey_hint.p, e->changed.p, e->canon_pos.p, s);
-    if (tm) cudaEventRecord(e->ev[0], s);
-    RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B));
+    const bool fuse_in = gather_fuses_input(e);
+    if (fuse_in) {
+        if (tm) cudaEventRecord(e->ev[0], s);
+        launch_gather_input(e->pool.p, e->pool_hint.p, e->queue.p, c, e->batch_pool.p, e->ckey_hint.p,
+                            e->canon_pos.p, first_step_launch(e, e->ckey.p, e->changed.p, e->Z.p, c + C_NR, B), s);
+    } else {
+        launch_gather_batch(e->pool.p, e->pool_hint.p, e->queue.p, c, e->batch_pool.p, B, e->KW, e->ckey.p,
+                            e->ckey_hint.p, e->changed.p, e->canon_pos.p, s);
+        if (tm) cudaEventRecord(e->ev[0], s);
+    }
+    RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B, fuse_in ? 1 : 0));
     if (tm) cudaEventRecord(e->ev[1], s);
     launch_route_changed(e->ckey.p, e->changed.p, c + C_NR, B, e->KW, e->P.rank, e->P.world, e->X.p, c + C_NX,
                          e->outbox.p, c + C_NOUT, e->canon_pos.p, s);

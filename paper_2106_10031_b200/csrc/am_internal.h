@@ -228,6 +228,10 @@ void launch_probe_records(const ProbeRecs& R, const HashSet& H, const int32_t* s
                           const cudaGraphConditionalHandle* h, cudaStream_t s);
 void launch_probe_done(unsigned long long* ctr, int64_t cap_probe, cudaStream_t s);
 void launch_take(const IterState& I, cudaStream_t s);
+// k_gather_batch + the first (input) compose step of the batch in one launch (am_compose.cu)
+void launch_gather_input(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
+                         const unsigned long long* ctr, int32_t* batch_pool, double* ckey_hint, int32_t* canon_pos,
+                         const LayerLaunch& L, cudaStream_t s);
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                          const unsigned long long* ctr, int32_t* batch_pool, int64_t n_cap, int KW, uint64_t* ckey,
                          double* ckey_hint, int32_t* changed, int32_t* canon_pos, cudaStream_t s);
