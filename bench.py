@@ -468,7 +468,7 @@ def main():
             "config": {"workload": WORKLOAD, "cells_per_step": cells, "waves": int(waves),
                        "parallelism": f"dp{world} (state-hash ownership)" if world > 1 else "1 GPU",
                        "l2": "flushed between timed steps (512 MiB write)",
-                       "device_march_time_s": t_step * 1e-3},
+                       "device_march_time_s": t_step * 1e-3, "ms_steps": [round(x, 3) for x in times]},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "other_configs": others,
             "gpu_launches": int(launches), "clocks": clocks,
             "fp64_peaks_tflops": {"dmma": float(pk[0]), "dfma": float(pk[1])},

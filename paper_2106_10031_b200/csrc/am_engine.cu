@@ -197,7 +197,7 @@ struct am_engine {
     std::vector<const void*> dg_ptrs;
     unsigned long long dg_kernels = 0;
     bool gather_input = true;   // k_gather_input: batch gather + input step in one launch
-    int graph_batch = 16;   // iterations replayed per host synchronisation (A/B: 8 -> 25.7 ms, 16 -> 25.1, 24 -> 25.0)
+    int graph_batch = 32;   // iterations replayed per host synchronisation (A/B: 8 -> 25.7 ms, 16 -> 25.0, 32 -> 24.6)
     int grid_cap = 0;    // >0: CTAs per SM for persistent GEMM launches
     unsigned long long graph_kernels = 0;
     // stats
@@ -1017,9 +1017,17 @@ static int capture(am_engine* e) {
     return AM_OK;
 }
 
-// make room for `iters` more iterations of worst-case output
+// make room for `iters` more iterations: the key pool / hash set get one iteration's worst case
+// (the unit k_take's capacity guard checks before taking a batch) plus the pool growth per cell
+// observed so far (x2, >= 8 keys) for the round's other iterations -- an under-estimate only makes
+// the guard take smaller batches (or stall until the next host round grows the buffers), never
+// overflows; the worst case for every iteration of a round would reserve ~130 keys per cell
 static int ensure_iter_room(am_engine* e, int iters) {
-    RC(ensure_hash(e, (int64_t)iters * e->B * (1 + emit_per_cell())));
+    RC(sync_counters(e));
+    const int64_t per_cell = 1 + emit_per_cell();
+    const int64_t np = (int64_t)e->hctr[C_POOL], nc = (int64_t)e->hctr[C_CELLS];
+    const int64_t g = nc > 0 ? std::min<int64_t>(per_cell, std::max<int64_t>(8, 2 * ((np + nc - 1) / nc))) : 16;
+    RC(ensure_hash(e, e->B * per_cell + (int64_t)(iters - 1) * e->B * g));
     RC(ensure_results(e, (int64_t)iters * e->B));
     return AM_OK;
 }
