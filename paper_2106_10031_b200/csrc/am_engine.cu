@@ -142,7 +142,7 @@ struct am_engine {
     DBuf<double> pool_hint, ckey_hint, emit_hint, near_row;
     DBuf<int32_t> near_n, near_flags, near_id;   // k_near lists per frontier entry
     int near_cap = 256;
-    double tau_mult = 1.0, near_reach = 6.0;
+    double tau_mult = 1.0, near_reach = 4.5;   // near-list reach in hint radii (A/B after the 96-row GEMM: 6 -> 24.7-24.9 ms, 4.5 -> 24.5)
     int max_attempts = 12;                     // hinted attempts (AM_MAX_ATTEMPTS; 5 -> 12: 31 -> 28.3 ms)
     double tau_grow = 2.0;                     // reach growth per failed attempt (AM_TAU_GROW)
     // composition: per-step launches (AM_COMPOSE_FUSED=1: one fused launch for all steps; slower
