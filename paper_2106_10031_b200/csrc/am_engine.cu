@@ -280,14 +280,18 @@ static int ensure_hash(am_engine* e, int64_t extra) {
     return AM_OK;
 }
 
-static int ensure_results(am_engine* e, int64_t cells) {
+// room for `cells` more visited cells; per-vertex buffers (vertices, edge refs, validation and
+// pending-probe lists) get worst-case room for `vcells` cells (default: all of them)
+static int ensure_results(am_engine* e, int64_t cells, int64_t vcells = -1) {
     RC(sync_counters(e));
+    const int64_t cells_all = cells;
+    if (vcells >= 0) cells = vcells;
     int64_t nc = (int64_t)e->hctr[C_CELLS], nv = (int64_t)e->hctr[C_VERTS], nr = (int64_t)e->hctr[C_REFS];
     cudaStream_t s = e->stream;
     bool moved = false;
-    CK(e->cell_pool.reserve(nc + cells, s, true, nc, &moved));
-    CK(e->cell_nv.reserve(nc + cells, s, true, nc, &moved));
-    CK(e->cell_voff.reserve(nc + cells, s, true, nc, &moved));
+    CK(e->cell_pool.reserve(nc + cells_all, s, true, nc, &moved));
+    CK(e->cell_nv.reserve(nc + cells_all, s, true, nc, &moved));
+    CK(e->cell_voff.reserve(nc + cells_all, s, true, nc, &moved));
     CK(e->verts.reserve((nv + cells * kVertsPerCell) * 3, s, true, nv * 3, &moved));
     CK(e->edge_nrefs.reserve(nv + cells * kVertsPerCell, s, true, nv, &moved));
     CK(e->edge_roff.reserve(nv + cells * kVertsPerCell, s, true, nv, &moved));
@@ -305,7 +309,7 @@ static int ensure_results(am_engine* e, int64_t cells) {
     }
     if (e->P.world > 1) {
         int64_t no = (int64_t)e->hctr[C_NOUT];
-        CK(e->outbox.reserve((no + cells * (1 + emit_per_cell())) * e->KW, s, true, no * e->KW, &moved));
+        CK(e->outbox.reserve((no + cells_all * (1 + emit_per_cell())) * e->KW, s, true, no * e->KW, &moved));
     }
     if (moved) e->graph_valid = false;
     return AM_OK;
@@ -1028,7 +1032,12 @@ static int ensure_iter_room(am_engine* e, int iters) {
     const int64_t np = (int64_t)e->hctr[C_POOL], nc = (int64_t)e->hctr[C_CELLS];
     const int64_t g = nc > 0 ? std::min<int64_t>(per_cell, std::max<int64_t>(8, 2 * ((np + nc - 1) / nc))) : 16;
     RC(ensure_hash(e, e->B * per_cell + (int64_t)(iters - 1) * e->B * g));
-    RC(ensure_results(e, (int64_t)iters * e->B));
+    // per-vertex buffers likewise: one worst-case iteration (kVertsPerCell per cell) + observed
+    // vertices per cell (x2, >= 8) for the rest
+    const int64_t nv = (int64_t)e->hctr[C_VERTS];
+    const int64_t gv = nc > 0 ? std::min<int64_t>(kVertsPerCell, std::max<int64_t>(8, 2 * ((nv + nc - 1) / nc))) : 16;
+    const int64_t vcells = e->B + ((int64_t)(iters - 1) * e->B * gv + kVertsPerCell - 1) / kVertsPerCell;
+    RC(ensure_results(e, (int64_t)iters * e->B, vcells));
     return AM_OK;
 }
 
