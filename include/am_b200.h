@@ -172,6 +172,15 @@ int am_weld(const double *d_verts, int64_t n_verts, const int64_t *d_loop_off, c
             int64_t n_loops, double tol, void *stream, int64_t *d_remap, double *d_kept, int64_t *d_face_off,
             int64_t *d_face_idx, int64_t *d_face_src, int64_t *h_counts);
 
+/* --- diagnostics -------------------------------------------------------- */
+/* Pairs (i < j) of face planes proportional within chord tol (reference network.py:528-570
+ * check_unique_planes; MarchReport.unique_plane_violations, reference marching.py:361-363).
+ * d_planes: m rows (nx, ny, nz, d) fp64 on the device.  Up to cap pairs are written to d_pairs
+ * (int32 [cap][2], unordered); *h_count = the number of pairs found (may exceed cap: call
+ * again with a larger buffer).  stream: a cudaStream_t; returns after synchronizing it. */
+int am_unique_planes(const double *d_planes, int64_t m, double tol, int32_t *d_pairs, int64_t cap, void *stream,
+                     int64_t *h_count);
+
 /* --- profiling hooks (bench.py roofline) --------------------------------- */
 /* cumulative device time (ms) of the compose (DMMA) kernels, of the face
  * kernel, and the algorithmic flop / byte counts they processed */

@@ -35,7 +35,7 @@ from typing import Sequence
 import numpy as np
 
 from .engine import architecture_key
-from .marching import MarchConfig, MarchResult, _engine_for, collect_result, march
+from .marching import MarchConfig, MarchResult, _engine_for, collect_result, march, seed_engine
 from .network import AnyNetwork, to_blob
 
 
@@ -96,7 +96,9 @@ def split_batch_result(eng, seeds_per_shape, t0: float, waves: int) -> list[Marc
                           empty_faces=int((nv == 0).sum()), open_edges=int(bbox_edge[v0:v1].sum()),
                           seconds=time.perf_counter() - t0, seeds_used=len(seeds_per_shape[s]),
                           capped=bool(c["capped"]), threads=1, waves=waves, overflow=int((nv < 0).sum()))
-        out.append(MarchResult(kb, branch, nv, hv[v0:v1], he[v0:v1], hr[r0:r1], rep, nb, seeds_per_shape[s]))
+        nets = getattr(eng, "shape_nets", None)
+        out.append(MarchResult(kb, branch, nv, hv[v0:v1], he[v0:v1], hr[r0:r1], rep, nb, seeds_per_shape[s],
+                               net=nets[s] if nets else None))
     return out
 
 
@@ -119,8 +121,7 @@ def march_fused(nets: Sequence[AnyNetwork], config: MarchConfig | None = None) -
             seeds.append(sample_seeds(eng, config.seeds, config.bbox, scheme=config.scheme, rng_seed=config.rng_seed))
     pts = np.concatenate(seeds)
     shp = np.concatenate([np.full(len(x), s, np.int32) for s, x in enumerate(seeds)])
-    for o in range(0, len(pts), eng.batch_size):   # am_seed takes at most one batch of cells
-        eng.seed(pts[o:o + eng.batch_size], shapes=shp[o:o + eng.batch_size])
+    seed_engine(eng, pts, shp)
     waves = eng.run()
     return split_batch_result(eng, seeds, t0, waves)
 

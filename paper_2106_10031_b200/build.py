@@ -26,6 +26,7 @@ SOURCES = {
     "am_peak.cu": [],
     "am_weld.cu": [],
     "am_result.cu": [],
+    "am_diag.cu": ["-fmad=false"],
 }
 
 

@@ -11,7 +11,9 @@ reference's per-polygon objects lazily.
 
 from __future__ import annotations
 
+import itertools
 import json
+import logging
 import time
 from collections import OrderedDict
 from dataclasses import dataclass, field
@@ -19,9 +21,11 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .engine import PROBE_DELTA, TOL_CELL, TOL_ONPLANE, TOL_WELD, Engine, architecture_key
-from .network import AffinePlane, AnyNetwork, EnsembleSpec, StateVector, subnetworks, to_blob
+from .network import AffinePlane, AnyNetwork, StateVector, is_ensemble, subnetworks, to_blob
 from .meshes import to_host
 from .seeding import sample_seeds
+
+log = logging.getLogger(__name__)
 
 DEFAULT_BBOX = ((-1.2, -1.2, -1.2), (1.2, 1.2, 1.2))   # reference cells.py:37
 
@@ -66,8 +70,16 @@ class FacePolygon:
 
 @dataclass
 class MarchConfig:
-    """reference marching.py:52-75 (``threads`` is accepted for API compatibility;
-    the GPU engine's parallelism is the whole wave)."""
+    """reference marching.py:52-75.
+
+    ``threads`` is accepted for API compatibility (the GPU engine's parallelism is the whole
+    wave).  ``mode`` is validated like the reference's and recorded, but both values run the
+    same face solver: the reference's pivot walk (``extract_face_pivot_checked``) and naive
+    enumeration (``extract_face_naive``) define the same polygon -- the pivot walk falls back
+    to naive enumeration whenever its hint does not verify (reference marching.py:247-255,
+    cells.py:365-462) -- and the GPU solver computes the naive-enumeration result exactly on a
+    provably sufficient candidate set (face stage).  ``pivot_fallbacks`` is
+    therefore always 0."""
 
     bbox: tuple = DEFAULT_BBOX
     seeds: int = 64
@@ -98,7 +110,9 @@ class MarchConfig:
 
 @dataclass
 class MarchReport:
-    """reference marching.py:78-103; pivot_fallbacks is always 0 (no pivot walk on the GPU)."""
+    """reference marching.py:78-103; pivot_fallbacks is always 0 (no pivot walk on the GPU).
+    ``overflow``: cells whose face exceeded the register-resident solver's limits and were
+    solved by the out-of-line global-memory path (0 on every benchmark configuration)."""
 
     cells_visited: int = 0
     faces_emitted: int = 0
@@ -136,7 +150,10 @@ class MarchResult:
     keys (C, nbytes) packbits states of every visited cell (empty faces
     included), sorted by (key, branch) as the reference sorts; nverts (C,)
     (0 = empty face); verts (V, 3); edge_nrefs (V,); edge_refs (R, 2) as
-    (kind, index).  Integer arrays are int32.
+    (kind, index).  Integer arrays are int32.  ``polygons`` builds the
+    reference's FacePolygon list (with each face's raw functional as ``plane``)
+    on first access; ``polygon_soup`` / ``welded_mesh`` carry the face planes
+    lazily (computed on the GPU when ``face_planes`` is first read).
     """
 
     keys: np.ndarray
@@ -148,10 +165,12 @@ class MarchResult:
     report: MarchReport
     n_bits: int
     seeds: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    net: object = field(default=None, repr=False)
     _polys: list | None = None
     # device copies of (nverts, verts) kept by march() so welded_mesh() welds in HBM without
     # sending the soup back to the GPU (None: host arrays only)
     _dev: tuple | None = field(default=None, repr=False)
+    _planes: np.ndarray | None = field(default=None, repr=False)
 
     @property
     def has_face(self) -> np.ndarray:
@@ -161,6 +180,20 @@ class MarchResult:
         b = int(self.branch[i])
         return StateVector(self.keys[i].tobytes(), self.n_bits, None if b < 0 else b)
 
+    def face_plane_rows(self) -> np.ndarray:
+        """(F, 4) raw face functional (nx, ny, nz, d) of every face, in polygon order: the
+        affine map of F on the cell (reference cells.py:100 FacePolygon.plane), recomputed
+        from the canonical states by the engine's composition (am_affine_maps)."""
+        if self._planes is None:
+            if self.net is None:
+                raise ValueError("face planes need the marched network (MarchResult.net)")
+            from .evaluate import face_planes_words, packbits_to_words
+            sel = self.nverts > 0
+            ens = is_ensemble(self.net)
+            words = packbits_to_words(self.keys[sel], self.branch[sel] if ens else None, self.n_bits)
+            self._planes = face_planes_words(self.net, words)
+        return self._planes
+
     @property
     def polygons(self) -> list:
         """Reference-style FacePolygon list (built lazily; O(cells) Python objects)."""
@@ -168,6 +201,7 @@ class MarchResult:
             out = []
             offs = np.concatenate([[0], np.cumsum(np.maximum(self.nverts, 0))])
             roffs = np.concatenate([[0], np.cumsum(self.edge_nrefs)])
+            planes = self.face_plane_rows() if self.net is not None else None
             for i in range(len(self.nverts)):
                 n = int(self.nverts[i])
                 if n <= 0:
@@ -177,22 +211,30 @@ class MarchResult:
                 for e in range(n):
                     a, b = int(roffs[v0 + e]), int(roffs[v0 + e + 1])
                     trans.append(tuple(PlaneRef(int(k), int(x)) for k, x in self.edge_refs[a:b]))
-                out.append(FacePolygon(self.state(i), self.verts[v0:v0 + n], None, tuple(trans)))
+                plane = None if planes is None else AffinePlane(planes[len(out), :3], planes[len(out), 3])
+                out.append(FacePolygon(self.state(i), self.verts[v0:v0 + n], plane, tuple(trans)))
             self._polys = out
         return self._polys
 
+    def _plane_source(self):
+        return self.face_plane_rows if self.net is not None else None
+
     def polygon_soup(self):
+        """One loop per analytic face, vertices not yet shared (reference marching.py:111-124)."""
         from .meshes import PolygonMesh
         nv = self.nverts[self.nverts > 0].astype(np.int64)
         off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
-        return PolygonMesh(self.verts.copy(), None, None, face_off=off, face_idx=np.arange(off[-1], dtype=np.int64))
+        return PolygonMesh(self.verts.copy(), None, None, face_off=off, face_idx=np.arange(off[-1], dtype=np.int64),
+                           plane_rows=self._plane_source())
 
     def welded_mesh(self, tol: float = TOL_WELD):
         """reference marching.py:126-127 weld(polygon_soup(), tol), welded on the GPU straight
         from the CSR soup (no per-loop Python objects on the way in).  A result of march() still
         holds its soup in HBM: the loops are formed and welded there and only the welded mesh
         comes back."""
-        from .meshes import PolygonMesh, weld_arrays, weld_device, to_host
+        from .meshes import PolygonMesh, weld_arrays, weld_device, to_host, select_rows
+        if tol < 0:
+            raise ValueError("weld tolerance must be >= 0")
         if self._dev is not None:
             import torch
             dn, dv = self._dev
@@ -200,14 +242,16 @@ class MarchResult:
             off = torch.zeros(nv.numel() + 1, dtype=torch.int64, device=dv.device)
             torch.cumsum(nv, 0, out=off[1:])
             idx = torch.arange(dv.shape[0], dtype=torch.int64, device=dv.device)
-            kept, foff, fidx, _, _, nd = weld_device(dv, off, idx, tol)
-            kept_h, foff_h = to_host([kept, foff])
+            kept, foff, fidx, fsrc, _, nd = weld_device(dv, off, idx, tol)
+            kept_h, foff_h, fsrc_h = to_host([kept, foff, fsrc])
             (fidx_h,) = to_host([fidx[:int(foff_h[-1])]])
-            return PolygonMesh(kept_h, None, None, nd, face_off=foff_h, face_idx=fidx_h)
-        nv = self.nverts[self.nverts > 0].astype(np.int64)
-        off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
-        kept, foff, fidx, _, nd = weld_arrays(self.verts, off, np.arange(off[-1], dtype=np.int64), tol)
-        return PolygonMesh(kept, None, None, nd, face_off=foff, face_idx=fidx)
+        else:
+            nv = self.nverts[self.nverts > 0].astype(np.int64)
+            off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
+            kept_h, foff_h, fidx_h, fsrc_h, nd = weld_arrays(self.verts, off, np.arange(off[-1], dtype=np.int64), tol)
+        src = self._plane_source()
+        return PolygonMesh(kept_h, None, None, nd, face_off=foff_h, face_idx=fidx_h,
+                           plane_rows=None if src is None else select_rows(src, fsrc_h))
 
     def face_multiset(self, decimals: int = 10):
         """Order-independent fingerprint (reference marching.py:139-149)."""
@@ -217,6 +261,54 @@ class MarchResult:
             out.append((poly.state.key, poly.state.branch, vs))
         out.sort(key=lambda t: (t[0], -1 if t[1] is None else t[1], sorted(t[2])))
         return out
+
+
+def neighbor_state(s: StateVector, ref: PlaneRef) -> StateVector:
+    """State across one boundary plane (reference marching.py:152-165): flip the neuron's bit or
+    switch branch; box faces have no neighbour."""
+    if ref.kind == PLANE_NEURON:
+        return s.flip(ref.index)
+    if ref.kind == PLANE_BRANCH:
+        if s.branch is None:
+            raise ValueError("branch switch on a non-ensemble state")
+        return s.with_branch(ref.index)
+    raise ValueError(f"no neighbor beyond the bounding box (ref {ref})")
+
+
+def transition_states(s: StateVector, refs) -> list:
+    """Neighbour states of an edge on possibly coincident planes (reference marching.py:168-195):
+    every non-empty flip subset of the neuron planes (singles + the joint flip + the unchanged
+    state beyond 3 planes), each with every branch target.  This is the host restatement of what
+    the face kernel emits per edge (am_face.cu, emission)."""
+    bits = [r.index for r in refs if r.kind == PLANE_NEURON]
+    targets = [None] + [r.index for r in refs if r.kind == PLANE_BRANCH]
+    if len(bits) > 3:
+        log.warning("edge on %d coincident planes; enqueueing singles and the full flip", len(bits))
+        subsets = [(b,) for b in bits] + [tuple(bits), ()]
+    else:
+        subsets = [c for k in range(len(bits) + 1) for c in itertools.combinations(bits, k)]
+    out = []
+    for sub, tgt in itertools.product(subsets, targets):
+        if not sub and tgt is None:
+            continue
+        t = s
+        for b in sub:
+            t = t.flip(b)
+        out.append(t if tgt is None else t.with_branch(tgt))
+    return out
+
+
+def vertex_residuals(net: AnyNetwork, mesh_or_result) -> np.ndarray:
+    """|F| at every mesh vertex, evaluated on the GPU (reference marching.py:369-377); the
+    exactness claim is max residual <= 1e-6."""
+    from .evaluate import forward_many
+    if isinstance(mesh_or_result, MarchResult):
+        verts = mesh_or_result.verts
+    else:
+        verts = mesh_or_result.vertices
+    if len(verts) == 0:
+        return np.empty(0)
+    return np.abs(forward_many(net, verts))
 
 
 def refs_to_kind_index(ids: np.ndarray, n_bits: int, n_subs: int) -> np.ndarray:
@@ -261,7 +353,7 @@ def device_results_to_host(eng: Engine):
 
 
 def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, threads: int = 1,
-                   keep_device: bool = False) -> MarchResult:
+                   keep_device: bool = False, net=None) -> MarchResult:
     """Sorted results (GPU sort + gathers, am_result_copy_device), converted to the reference's
     representations on the device, one pinned copy per array."""
     c, kb, branch, _, hn, hv, he, hr = device_results_to_host(eng)
@@ -272,7 +364,8 @@ def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, thread
     rep = MarchReport(cells_visited=c["cells"], faces_emitted=c["faces"], empty_faces=c["empty"],
                       open_edges=c["open_edges"], seconds=time.perf_counter() - t0, seeds_used=len(seeds),
                       capped=bool(c["capped"]), threads=threads, waves=waves, overflow=c["overflow"])
-    return MarchResult(kb, branch, hn, hv, he, hr, rep, eng.blob.n_bits, seeds, _dev=dev)
+    return MarchResult(kb, branch, hn, hv, he, hr, rep, eng.blob.n_bits, seeds, net=net if net is not None else eng.net,
+                       _dev=dev)
 
 
 _ENGINES: "OrderedDict[tuple, Engine]" = OrderedDict()
@@ -307,18 +400,49 @@ def _engine_for(net: AnyNetwork, config: MarchConfig) -> Engine:
     return eng
 
 
+def seed_engine(eng: Engine, seeds: np.ndarray, shapes=None):
+    """Queue the refined seed states; am_seed takes at most one batch of cells per call."""
+    bs = max(1, eng.batch_size)
+    for o in range(0, len(seeds), bs):
+        eng.seed(seeds[o:o + bs], shapes=None if shapes is None else shapes[o:o + bs])
+
+
+def unique_plane_violations(res: MarchResult, tol: float = 1e-9) -> int:
+    """Proportional face-plane pairs among the result's faces (reference marching.py:361-363 via
+    check_unique_planes), counted on the GPU (am_unique_planes)."""
+    from .evaluate import unique_plane_pairs
+    if res.report.faces_emitted < 2:
+        return 0
+    return len(unique_plane_pairs(res.face_plane_rows(), tol))
+
+
 def march(net: AnyNetwork, config: MarchConfig | None = None, engine: Engine | None = None) -> MarchResult:
-    """Extract every analytic face reachable from the seeds (reference marching.py:304-362)."""
+    """Extract every analytic face reachable from the seeds (reference marching.py:304-366).
+
+    Returns the face polygons plus a report; raises SeedingError ("no surface located in
+    bbox") if no seed can be found; hitting ``max_cells`` returns the partial mesh with
+    ``report.capped`` set.  ``engine``: an Engine of this network's architecture to march on
+    (its weights are replaced by ``net``'s and its visited set cleared)."""
     config = config or MarchConfig()
     t0 = time.perf_counter()
-    eng = engine or _engine_for(net, config)
+    if engine is not None:
+        engine.load_network(net)
+        engine.reset()
+        eng = engine
+    else:
+        eng = _engine_for(net, config)
     if config.seed_points is not None:
         seeds = np.asarray(config.seed_points, dtype=np.float64).reshape(-1, 3)
     else:
         seeds = sample_seeds(eng, config.seeds, config.bbox, scheme=config.scheme, rng_seed=config.rng_seed)
-    eng.seed(seeds)
+    seed_engine(eng, seeds)
     waves = eng.run()
-    res = collect_result(eng, seeds, t0, waves, config.threads, keep_device=True)
+    res = collect_result(eng, seeds, t0, waves, config.threads, keep_device=True, net=net)
+    if res.report.overflow:
+        log.warning("%d cells exceeded the face solver's fast-path limits", res.report.overflow)
     if res.report.faces_emitted <= config.unique_planes_limit:
-        res.report.unique_plane_violations = None   # diagnostic not computed on the GPU path
+        res.report.unique_plane_violations = unique_plane_violations(res)
+    if res.report.capped:
+        log.warning("max_cells=%d reached; mesh is partial", config.max_cells)
+    res.report.seconds = time.perf_counter() - t0
     return res

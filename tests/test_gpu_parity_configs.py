@@ -1,0 +1,95 @@
+"""GPU parity on the BENCHMARKED configurations themselves (BASELINE.json configs[1..3]).
+
+* configs[1] -- the headline march (3-(90x6)-1 geometric init, 64 dichotomy seeds, full
+  default box, 234 k cells): GPU == CPU oracle bit-exactly over the whole visited set, and
+  both == the digest of the UNMODIFIED reference's own march (tests/golden/make_digest.py,
+  committed as tests/golden/digest_configs1.json once the ~1 h CPU reference run is done).
+* configs[2] -- DeepSDF 3-(512x8)-1 with the skip at layer 4, in a sub-box around a surface
+  point (tens of thousands of cells, the oracle's C restatement finishes in ~1 min).
+* configs[3] -- IM-NET-style occupancy ensemble 4 x 3-(128x3)-1 merged by max-pooling, in a
+  sub-box.
+
+Bar (north_star): visited set, polygons and edge refs identical; vertices within 1e-9.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN
+from test_gpu_parity import assert_same_march
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 8
+DEEPSDF_HALF = 0.035    # sub-box half-sizes: tens of thousands of cells (tools/calib_subbox.py)
+IMNET_HALF = 0.1
+
+
+def _surface_box(net, direction, half):
+    """Box of half-size ``half`` around the surface point on the ray from the origin (GPU
+    forward + bisection, only used to place the box)."""
+    from paper_2106_10031_b200.evaluate import forward_many
+    d = np.asarray(direction, dtype=np.float64)
+    d /= np.linalg.norm(d)
+    ts = np.linspace(0.0, 1.1, 1101)
+    f = forward_many(net, ts[:, None] * d)
+    i = int(np.flatnonzero(np.sign(f[1:]) != np.sign(f[:-1]))[0])
+    a, b = ts[i], ts[i + 1]
+    for _ in range(60):
+        m = 0.5 * (a + b)
+        if np.sign(forward_many(net, (m * d)[None])[0]) == np.sign(f[i]):
+            a = m
+        else:
+            b = m
+    p = 0.5 * (a + b) * d
+    return (tuple(p - half), tuple(p + half)), p
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_configs1_full_march_matches_oracle_and_reference_digest():
+    from paper_2106_10031_b200 import MarchConfig, march, synth
+    net = synth.geometric_mlp([90] * 6, seed=0)
+    r = march(net, MarchConfig(seeds=64, rng_seed=0))
+    assert r.report.cells_visited > 200_000 and not r.report.capped
+    o = oracle.march(net, seed_points=r.seeds, threads=THREADS)
+    assert_same_march(r, o.keys, o.branch, o.nverts, o.verts, o.edge_nrefs, o.edge_refs)
+    path = os.path.join(GOLDEN, "digest_configs1.json")
+    if not os.path.exists(path):
+        pytest.skip("reference digest of configs[1] not generated yet (tests/golden/make_digest.py)")
+    d = json.load(open(path))
+    np.testing.assert_allclose(r.seeds, np.asarray(d["seeds"]), atol=1e-12, rtol=0)
+    assert r.report.cells_visited == d["cells"] and r.report.faces_emitted == d["faces"]
+    assert _sha(r.keys) == d["keys_sha256"]
+    assert _sha(r.nverts.astype(np.int64)) == d["nverts_sha256"]
+    assert _sha(r.edge_nrefs.astype(np.int64)) == d["edge_nrefs_sha256"]
+    assert _sha(r.edge_refs.astype(np.int64)) == d["edge_refs_sha256"]
+    assert len(r.verts) == d["n_verts"]
+    np.testing.assert_allclose(r.verts.sum(axis=0), d["vert_sum"], atol=1e-9 * len(r.verts), rtol=0)
+
+
+def test_configs2_deepsdf_512x8_subbox_matches_oracle():
+    from paper_2106_10031_b200 import MarchConfig, march, synth
+    net = synth.deepsdf_mlp(width=512, depth=8, skip_at=4, seed=0)
+    bbox, p = _surface_box(net, (0.3, 0.5, 0.8), DEEPSDF_HALF)
+    r = march(net, MarchConfig(bbox=bbox, seed_points=p[None]))
+    assert r.report.cells_visited > 5_000 and not r.report.capped
+    o = oracle.march(net, bbox=bbox, seed_points=r.seeds, threads=THREADS)
+    assert_same_march(r, o.keys, o.branch, o.nverts, o.verts, o.edge_nrefs, o.edge_refs)
+
+
+def test_configs3_imnet_128x3_ensemble_subbox_matches_oracle():
+    from paper_2106_10031_b200 import MarchConfig, march, synth
+    net = synth.imnet_ensemble(widths=(128, 128, 128), n_parts=4, seed=0)
+    bbox, p = _surface_box(net, (0.3, 0.5, 0.8), IMNET_HALF)
+    r = march(net, MarchConfig(bbox=bbox, seed_points=p[None]))
+    assert r.report.cells_visited > 5_000 and not r.report.capped
+    o = oracle.march(net, bbox=bbox, seed_points=r.seeds, threads=THREADS)
+    assert_same_march(r, o.keys, o.branch, o.nverts, o.verts, o.edge_nrefs, o.edge_refs)
