@@ -21,46 +21,12 @@
 #include <cstdio>
 
 #include "am_internal.h"
+#include "am_ptx.cuh"
 
 namespace am {
 
 constexpr int BM = 64, BN = 64, TB = 16, BK = 32;   // TB: K width of one TMA box (128 B)
 constexpr int kThreads = 256;   // 8 warps: 2 (rows) x 4 (columns), 32 x 16 outputs each
-
-// ------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
-        "[%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
-    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
-                 : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-                 : "d"(a0), "d"(a1), "d"(b0));
-}
-// element (row, k) of a [64][16] fp64 tile written by TMA with CU_TENSOR_MAP_SWIZZLE_128B
-__device__ __forceinline__ int swz(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7)) << 1) | (k & 1)); }
 
 // ----------------------------------------------------------- tensor maps
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -285,23 +251,6 @@ struct __align__(1024) GemmSmem {
     unsigned long long bits[TN][2];  // forward epilogue: per-column bit window
 };
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait(int pending) {
-    switch (pending) {
-        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-        case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-        case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
-        default: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
-    }
-}
 // 32 state bits of rows [row, row + 32) (MSB-first key words), bit j = row + j; zero beyond `valid`
 // (G: key in global memory, read through L2; else the tile's shared-memory word cache)
 template <bool G = false>
@@ -434,6 +383,9 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
             cp_async_wait(committed - c);
             if (wres) mbar_wait(&S.wbar, 0);
             else mbar_wait(&S.bar[s], (gc / NST) & 1);
+            // the stage refilled below (by TMA, async proxy) was read through the generic proxy
+            // in the previous chunk: order those reads before the refill
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
             if (c + NST - 1 < nchunks) issue(c + NST - 1);
             const double* ws = S.w[wres ? c : s][0];

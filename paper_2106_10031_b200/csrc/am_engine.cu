@@ -148,7 +148,15 @@ struct am_engine {
     // composition: per-step launches (AM_COMPOSE_FUSED=1: one fused launch for all steps; slower
     // on configs[1] and DeepSDF, kept for experiments)
     bool compose_fused = false;
-    std::unique_ptr<FusedCompose> fused{new FusedCompose()};   // face-solver reach (tuning: AM_TAU_MULT, AM_NEAR_REACH)
+    std::unique_ptr<FusedCompose> fused{new FusedCompose()};
+    // narrow plain networks (every hidden width <= 96): gather + composition + face head of an
+    // iteration in one launch (am_narrow.cu; AM_NARROW=0 selects the per-step kernels)
+    bool narrow_fused = false;
+    bool narrow_check = false;   // AM_NARROW_CHECK=1: also run the per-step path into shadow buffers and compare
+    DBuf<double> Z2, faces2;
+    DBuf<uint64_t> ckey2;
+    DBuf<int32_t> changed2;
+    std::unique_ptr<NarrowCompose> ncomp{new NarrowCompose()};   // face-solver reach (tuning: AM_TAU_MULT, AM_NEAR_REACH)
     DBuf<unsigned long long> dbg;   // face-kernel instrumentation counters (AM_FACE_STATS builds)
     uint64_t tcap = 0;
     // counters (device) + host mirror
@@ -523,6 +531,22 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     }
     CK(e->subdev.reserve((int64_t)(sizeof(SubDev) * e->M), e->stream));
     RC(upload_params(e, net->h_params));
+    {
+        const char* nv = getenv("AM_NARROW");
+        const int KWk = (e->NB + 63) / 64 + (e->ensemble ? 1 : 0) + (e->n_shapes > 1 ? 1 : 0);
+        if ((!nv || atoi(nv) != 0) && narrow_compose_ok(e->sdev.data(), ns, e->M, KWk)) {
+            NarrowCompose& N = *e->ncomp;
+            N.nsteps = ns;
+            for (int s = 0; s < ns; s++) {
+                const StepDev& d = e->sdev[s];
+                if (s > 0 && make_tmap_2d(&N.tm[s], d.W, d.n_out, d.n_in, d.ldw, 96) != 0)
+                    return fail(AM_ERR_CUDA, "cuTensorMapEncodeTiled failed for narrow step %d", s);
+            }
+            e->narrow_fused = true;
+            if (const char* v = getenv("AM_NARROW_CHECK")) e->narrow_check = atoi(v) != 0;
+            if (const char* v = getenv("AM_NARROW_DBG")) N.dbg = atoi(v);
+        }
+    }
     // batch size from the per-iteration memory budget: compose planes + worst-case probe
     // activations + emitted keys per batch cell
     int64_t budget = e->P.mem_budget > 0 ? e->P.mem_budget : (int64_t)4 << 30;
@@ -564,6 +588,10 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_BISECT_TREE")) e->bisect_tree = atoi(v) != 0;
     if (const char* v = getenv("AM_GRAPH_BATCH")) e->graph_batch = std::max(1, atoi(v));
     if (const char* v = getenv("AM_GATHER_INPUT")) e->gather_input = atoi(v) != 0;
+    if (e->narrow_check) {
+        CK(e->Z2.reserve(e->Z.n, s)); CK(e->faces2.reserve(e->faces.n, s));
+        CK(e->ckey2.reserve(e->ckey.n, s)); CK(e->changed2.reserve(e->changed.n, s));
+    }
     CK(e->near_n.reserve(e->B, s));
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
@@ -852,7 +880,25 @@ static int launch_iteration(am_engine* e) {
 
     launch_take(I, s);
     const bool fuse_in = gather_fuses_input(e);
-    if (fuse_in) {
+    if (e->narrow_fused) {
+        if (tm) cudaEventRecord(e->ev[0], s);
+        NarrowCompose& N = *e->ncomp;
+        for (int q = 0; q < N.nsteps; q++) N.st[q] = e->sdev[q];
+        N.subs = reinterpret_cast<const SubDev*>(e->subdev.p);
+        N.pool = e->pool.p; N.pool_hint = e->pool_hint.p; N.queue = e->queue.p; N.ctr = c;
+        N.batch_pool = e->batch_pool.p; N.canon_pos = e->canon_pos.p; N.ckey_hint = e->ckey_hint.p;
+        N.Z = e->Z.p; N.keys = e->ckey.p; N.faces = e->faces.p; N.changed = e->changed.p;
+        N.n_dev = c + C_NR; N.n_cap = B; N.KW = e->KW; N.zs = e->zs; N.shape_w = e->shape_w; N.fp32 = e->fp32;
+        launch_compose_narrow(N, s);
+        CK(cudaGetLastError());
+        if (e->narrow_check) {
+            launch_gather_input(e->pool.p, e->pool_hint.p, e->queue.p, c, e->batch_pool.p, e->ckey_hint.p,
+                                e->canon_pos.p, first_step_launch(e, e->ckey2.p, e->changed2.p, e->Z2.p, c + C_NR, B), s);
+            RC(compose(e, e->ckey2.p, e->changed2.p, e->Z2.p, e->faces2.p, c + C_NR, B, 1));
+            launch_narrow_check(e->Z.p, e->Z2.p, e->faces.p, e->faces2.p, e->ckey.p, e->ckey2.p, e->changed.p,
+                                e->changed2.p, c + C_NR, B, e->NB, e->zs, e->KW, e->dbg.p, s);
+        }
+    } else if (fuse_in) {
         if (tm) cudaEventRecord(e->ev[0], s);
         launch_gather_input(e->pool.p, e->pool_hint.p, e->queue.p, c, e->batch_pool.p, e->ckey_hint.p,
                             e->canon_pos.p, first_step_launch(e, e->ckey.p, e->changed.p, e->Z.p, c + C_NR, B), s);
@@ -861,7 +907,7 @@ static int launch_iteration(am_engine* e) {
                             e->ckey_hint.p, e->changed.p, e->canon_pos.p, s);
         if (tm) cudaEventRecord(e->ev[0], s);
     }
-    RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B, fuse_in ? 1 : 0));
+    if (!e->narrow_fused) RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B, fuse_in ? 1 : 0));
     if (tm) cudaEventRecord(e->ev[1], s);
     launch_route_changed(e->ckey.p, e->changed.p, c + C_NR, B, e->KW, e->P.rank, e->P.world, e->X.p, c + C_NX,
                          e->outbox.p, c + C_NOUT, e->canon_pos.p, s);

@@ -163,6 +163,37 @@ struct FusedCompose {
     int n_subs;
 };
 void launch_compose_fused(const FusedCompose& F, cudaStream_t s);
+// whole composition of an iteration (gather + every step + face head) in one launch, for plain
+// dense networks of width <= 96 (am_narrow.cu k_compose_narrow)
+constexpr int kMaxNarrowSteps = 12;
+struct NarrowCompose {
+    CUtensorMap tm[kMaxNarrowSteps];   // 96-row W boxes of steps >= 1
+    StepDev st[kMaxNarrowSteps];
+    int nsteps;
+    const SubDev* subs;                // device head table (one subnetwork)
+    // iteration state (k_gather_batch's inputs and outputs)
+    const uint64_t* pool;
+    const double* pool_hint;
+    const int32_t* queue;
+    const unsigned long long* ctr;
+    int32_t* batch_pool;
+    int32_t* canon_pos;
+    double* ckey_hint;
+    // composition outputs
+    double* Z;
+    uint64_t* keys;
+    double* faces;
+    int32_t* changed;
+    const unsigned long long* n_dev;
+    int64_t n_cap;
+    int KW, zs, shape_w, fp32;
+    int dbg;                           // AM_NARROW_DBG bits (experiments)
+};
+bool narrow_compose_ok(const StepDev* st, int nsteps, int n_subs, int KW);
+void launch_compose_narrow(const NarrowCompose& P, cudaStream_t s);
+void launch_narrow_check(const double* Z, const double* Z2, const double* F, const double* F2, const uint64_t* K,
+                         const uint64_t* K2, const int32_t* ch, const int32_t* ch2, const unsigned long long* n_dev,
+                         int64_t n_cap, int NB, int zs, int KW, unsigned long long* dbg, cudaStream_t s);
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV,
                       cudaStream_t s, const CUtensorMap* tmW96 = nullptr, const CUtensorMap* tmV96 = nullptr);
 int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld_elems,
