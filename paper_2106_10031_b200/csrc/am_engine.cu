@@ -889,6 +889,7 @@ static int launch_iteration(am_engine* e) {
         N.batch_pool = e->batch_pool.p; N.canon_pos = e->canon_pos.p; N.ckey_hint = e->ckey_hint.p;
         N.Z = e->Z.p; N.keys = e->ckey.p; N.faces = e->faces.p; N.changed = e->changed.p;
         N.n_dev = c + C_NR; N.n_cap = B; N.KW = e->KW; N.zs = e->zs; N.shape_w = e->shape_w; N.fp32 = e->fp32;
+        N.prof = e->dbg.p + 32;
         launch_compose_narrow(N, s);
         CK(cudaGetLastError());
         if (e->narrow_check) {

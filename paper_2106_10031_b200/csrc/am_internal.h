@@ -187,7 +187,8 @@ struct NarrowCompose {
     const unsigned long long* n_dev;
     int64_t n_cap;
     int KW, zs, shape_w, fp32;
-    int dbg;                           // AM_NARROW_DBG bits (experiments)
+    int dbg;                           // AM_NARROW_DBG bits (experiments; 8: phase cycle counters)
+    unsigned long long* prof;          // [8] phase cycles of thread 0 of every CTA (dbg & 8)
 };
 bool narrow_compose_ok(const StepDev* st, int nsteps, int n_subs, int KW);
 void launch_compose_narrow(const NarrowCompose& P, cudaStream_t s);

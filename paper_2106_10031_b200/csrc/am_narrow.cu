@@ -40,16 +40,30 @@ constexpr int NCELL = 8;        // cells per tile
 constexpr int NCOL = NCELL * 4; // columns
 constexpr int AS = NCOL + 4;    // act row stride (doubles): conflict-free B fragments
 constexpr int KB = 16;          // K per W box (128 B rows)
-constexpr int NSB = 4;          // W ring boxes
+#ifndef AM_NARROW_NSB
+#define AM_NARROW_NSB 4
+#endif
+#ifndef AM_NARROW_NACT
+#define AM_NARROW_NACT 2
+#endif
+#ifndef AM_NARROW_CPS
+#define AM_NARROW_CPS 2
+#endif
+constexpr int NSB = AM_NARROW_NSB;    // W ring boxes
+constexpr int NACT = AM_NARROW_NACT;  // act buffers: 2 = ping-pong (one barrier per layer), 1 = in place (two)
+constexpr int CPS = AM_NARROW_CPS;    // resident CTAs per SM
 constexpr int NCW = 6;          // consumer warps
 constexpr int NCT = NCW * 32;   // consumer threads
 constexpr int NT = NCT + 32;    // + producer warp
-constexpr int KWMAX = 40;       // key words per cell held in shared memory
+constexpr int KWMAX = 20;       // key words per cell held in shared memory (<= 1280 state bits)
 
 struct __align__(1024) NarrowSmem {
     double w[NSB][NR * KB];       // TMA destinations (1 KB aligned for the 128B swizzle)
-    double act[2][NR * AS];       // masked layer outputs [row][col], ping-pong
+    double act[NACT][NR * AS];    // masked layer outputs [row][col]
     uint64_t key[NCELL][KWMAX];   // the tile's state keys (canonical bits updated in place)
+    double p1[NR * 4];            // step 0's planes (W_1[:, :3], b_1) per row, staged once per CTA
+    double hw[NR];                // head weights
+    uint32_t deg1[NR / 32];       // step-0 rows with a degenerate (zero) normal
     uint64_t full[NSB], empty[NSB];
     int changed[NCELL];
 };
@@ -64,7 +78,25 @@ __device__ __forceinline__ void skey_set(uint64_t* k, int i, int bit) {
     else atomicAnd(w, ~m);
 }
 
-__global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant__ NarrowCompose P) {
+// !(|(x, y, z)| > 1e-12) -- the reference's constant-functional test (network.py:421-428) -- with
+// the square root taken only near the threshold: a squared norm far from 1e-24 decides it alone
+__device__ __forceinline__ bool degenerate3(double x, double y, double z) {
+    const double ss = (x * x + y * y) + z * z;
+    if (ss > 2.0e-24) return false;
+    if (ss < 0.5e-24) return true;
+    return !(sqrt(ss) > kDegen);
+}
+
+// |x| > t (t > 0) on the integer pipe; NaN counts as not greater, so a NaN normal takes the exact
+// norm test like every small one
+constexpr double kBig = 2e-12;
+__device__ __forceinline__ bool fabs_gt(double x, double t) {
+    const unsigned long long ax = (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+    return ax > (unsigned long long)__double_as_longlong(t) && ax <= 0x7ff0000000000000ull;
+}
+
+template <int FP32>
+__global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constant__ NarrowCompose P) {
     extern __shared__ uint8_t smem_raw[];
     NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -78,7 +110,21 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < 2 * NR * AS; i += NT) (&S.act[0][0])[i] = 0.0;
+    for (int i = tid; i < NACT * NR * AS; i += NT) (&S.act[0][0])[i] = 0.0;
+    if (tid < NR / 32) S.deg1[tid] = 0u;
+    __syncthreads();
+    {   // constants of step 0 and the head (weights: not produced by the preceding kernels)
+        const StepDev& s0 = P.st[0];
+        for (int r = tid; r < s0.n_out; r += NT) {
+            const double* w = s0.W + (int64_t)r * s0.ldw;
+            const double a0 = prec_round(w[0], FP32), a1 = prec_round(w[1], FP32), a2 = prec_round(w[2], FP32);
+            S.p1[r * 4 + 0] = a0; S.p1[r * 4 + 1] = a1; S.p1[r * 4 + 2] = a2;
+            S.p1[r * 4 + 3] = s0.b ? prec_round(0.0 + s0.b[r], FP32) : 0.0;
+            if (degenerate3(a0, a1, a2)) atomicOr(&S.deg1[r >> 5], 1u << (r & 31));
+        }
+        const SubDev* sd = P.subs;
+        for (int r = tid; r < sd->last_n; r += NT) S.hw[r] = sd->hw[r];
+    }
     __syncthreads();
 
     // boxes per tile: every GEMM step's K extent in 16-wide boxes
@@ -138,8 +184,12 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
     const int g = lane >> 2, tq = lane & 3;
     const int wm = warp % 3, wn = warp / 3;
     const int pg = ((g & 3) << 1) | (g >> 2);   // fragment row permutation (bank-conflict-free W reads)
-    const int fp32 = P.fp32;
+    constexpr int fp32 = FP32;
+    const bool shaped = P.shape_w >= 0;   // batch of shapes: biases per cell's shape
     uint32_t gbox = 0;
+    const bool prof = (P.dbg & 8) && P.prof && threadIdx.x == 0;
+    unsigned long long tprev = prof ? clock64() : 0;
+#define PROF(i) do { if (prof) { unsigned long long tn = clock64(); atomicAdd(&P.prof[i], tn - tprev); tprev = tn; } } while (0)
 
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t item0 = t * NCELL;
@@ -161,6 +211,7 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
         }
         if (tid < NCELL) S.changed[tid] = 0;
         bar_sync(1, NCT);
+        PROF(0);
 
         // ---- step 0: A_1 = W_1[:, :3], c_1 = b_1 (reference network.py:398-443 with A = I, c = 0)
         {
@@ -171,26 +222,24 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
                 const int64_t item = item0 + c;
                 uint64_t* key = S.key[c];
                 const int row = st.row_off + r;
-                const double* w = st.W + (int64_t)r * st.ldw;
-                double a0 = w[0], a1 = w[1], a2 = w[2];
-                double cc = 0.0;
-                cc = cc + step_bias(st, item_shape(key, P.shape_w), r);
-                a0 = prec_round(a0, fp32); a1 = prec_round(a1, fp32);
-                a2 = prec_round(a2, fp32); cc = prec_round(cc, fp32);
-                const double nrm = sqrt((a0 * a0 + a1 * a1) + a2 * a2);
+                const double2 pa = *reinterpret_cast<const double2*>(&S.p1[r * 4]);
+                const double a2 = S.p1[r * 4 + 2];
+                double cc = S.p1[r * 4 + 3];
+                if (shaped) cc = prec_round(0.0 + step_bias(st, item_shape(key, P.shape_w), r), fp32);
                 int bit = skey_bit(key, row);
-                if (!(nrm > kDegen)) {
+                if ((S.deg1[r >> 5] >> (r & 31)) & 1u) {
                     const int cb = cc > 0.0;
                     if (cb != bit) { skey_set(key, row, cb); S.changed[c] = 1; bit = cb; }
                 }
                 double* z = P.Z + (item * P.zs + row) * 4;
-                reinterpret_cast<double2*>(z)[0] = make_double2(a0, a1);
+                reinterpret_cast<double2*>(z)[0] = pa;
                 reinterpret_cast<double2*>(z)[1] = make_double2(a2, cc);
                 double* ao = &S.act[0][r * AS + c * 4];
-                reinterpret_cast<double2*>(ao)[0] = bit ? make_double2(a0, a1) : make_double2(0.0, 0.0);
+                reinterpret_cast<double2*>(ao)[0] = bit ? pa : make_double2(0.0, 0.0);
                 reinterpret_cast<double2*>(ao)[1] = bit ? make_double2(a2, cc) : make_double2(0.0, 0.0);
             }
             bar_sync(1, NCT);
+            PROF(1);
         }
 
         // ---- GEMM steps
@@ -205,10 +254,20 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
                 for (int j = 0; j < 2; j++)
 #pragma unroll
                     for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+            double bias[2][2];   // this thread's 4 output rows (loads overlap the K loop)
+#pragma unroll
+            for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+                for (int half = 0; half < 2; half++) {
+                    const int r = wm * 32 + mi * 16 + pg + half * 8;
+                    bias[mi][half] = (r < st.n_out && !shaped) ? st.b[r] : 0.0;
+                }
             const double* xs = S.act[cur];
             for (int b = 0; b < nb; b++, gbox++) {
                 const int slot = gbox % NSB;
+                const unsigned long long tw = prof ? clock64() : 0ull;
                 mbar_wait(&S.full[slot], (gbox / NSB) & 1);
+                if (prof) atomicAdd(&P.prof[8], clock64() - tw);
                 const double* ws = S.w[slot];
 #pragma unroll
                 for (int kk = 0; kk < KB; kk += 4) {
@@ -234,8 +293,10 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.empty[slot]);
             }
+            PROF(2);
             // epilogue
-            double* xo = S.act[cur ^ 1];
+            if (NACT == 1) bar_sync(1, NCT);   // in place: every warp has read the layer's input
+            double* xo = S.act[NACT == 1 ? 0 : cur ^ 1];
 #pragma unroll
             for (int mi = 0; mi < 2; mi++) {
 #pragma unroll
@@ -249,32 +310,51 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
                         const int c = col >> 2, comp = col & 3;   // comp 0 or 2
                         const bool ok = rok && c < ncell;
                         double v0 = acc[mi][nj][half * 2], v1 = acc[mi][nj][half * 2 + 1];
-                        if (comp == 2) v1 = v1 + (ok ? step_bias(st, item_shape(S.key[c], P.shape_w), r) : 0.0);
+                        if (comp == 2)
+                            v1 = v1 + (!ok ? 0.0 : shaped ? step_bias(st, item_shape(S.key[c], P.shape_w), r) : bias[mi][half]);
                         v0 = prec_round(v0, fp32);
                         v1 = prec_round(v1, fp32);
-                        // the pair of lanes (tq, tq ^ 1) holds the 4 components of (cell, row)
-                        const double p0 = __shfl_xor_sync(0xffffffffu, v0, 1);
-                        const double p1 = __shfl_xor_sync(0xffffffffu, v1, 1);
-                        if (ok) {
-                            const double nx = comp == 0 ? v0 : p0, ny = comp == 0 ? v1 : p1;
-                            const double nz = comp == 0 ? p0 : v0, cc = comp == 0 ? p1 : v1;
-                            const double nrm = sqrt((nx * nx + ny * ny) + nz * nz);
-                            int bit = skey_bit(S.key[c], row);
-                            if (!(nrm > kDegen)) {
-                                const int cb = cc > 0.0;
-                                if (cb != bit) {
-                                    if (comp == 0) { skey_set(S.key[c], row, cb); S.changed[c] = 1; }
-                                    bit = cb;
-                                }
+                        // Constant-functional test of (cell, row), whose 4 components sit in the lane
+                        // pair (tq, tq ^ 1): a normal component above 2e-12 settles it without fp64
+                        // math (|n| >= that component); only pairs with every component below run
+                        // the reference's norm test (uniform branch, rare).
+                        const bool big = (comp == 0) ? (fabs_gt(v0, kBig) || fabs_gt(v1, kBig)) : fabs_gt(v0, kBig);
+                        const unsigned bal = __ballot_sync(0xffffffffu, big);
+                        bool deg = !((bal >> lane) & 1u) && !((bal >> (lane ^ 1)) & 1u);
+                        if (__any_sync(0xffffffffu, deg && ok)) {
+                            const double p0 = __shfl_xor_sync(0xffffffffu, v0, 1);
+                            const double p1 = __shfl_xor_sync(0xffffffffu, v1, 1);
+                            if (deg) {
+                                const double nx = comp == 0 ? v0 : p0, ny = comp == 0 ? v1 : p1;
+                                const double nz = comp == 0 ? p0 : v0;
+                                deg = degenerate3(nx, ny, nz);
                             }
+                            // the sign of the offset decides a constant neuron's bit
+                            const double cc = comp == 0 ? p1 : v1;
+                            if (ok) {
+                                int bit = skey_bit(S.key[c], row);
+                                if (deg) {
+                                    const int cb = cc > 0.0;
+                                    if (cb != bit) {
+                                        if (comp == 0) { skey_set(S.key[c], row, cb); S.changed[c] = 1; }
+                                        bit = cb;
+                                    }
+                                }
+                                *reinterpret_cast<double2*>(P.Z + ((item0 + c) * P.zs + row) * 4 + comp) = make_double2(v0, v1);
+                                *reinterpret_cast<double2*>(xo + r * AS + col) = bit ? make_double2(v0, v1) : make_double2(0.0, 0.0);
+                            }
+                        } else if (ok) {
+                            const int bit = skey_bit(S.key[c], row);
                             *reinterpret_cast<double2*>(P.Z + ((item0 + c) * P.zs + row) * 4 + comp) = make_double2(v0, v1);
                             *reinterpret_cast<double2*>(xo + r * AS + col) = bit ? make_double2(v0, v1) : make_double2(0.0, 0.0);
                         }
                     }
                 }
             }
+            PROF(3);
             bar_sync(1, NCT);
-            cur ^= 1;
+            PROF(6);
+            if (NACT == 2) cur ^= 1;
         }
 
         // ---- face functional: head . (s_L (.) Z_L) (+ head bias on the offset)
@@ -286,7 +366,7 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
                 for (int r = lane; r < sd.last_n; r += 32) {
                     const double2 x = *reinterpret_cast<const double2*>(xs + r * AS + c * 4);
                     const double2 y = *reinterpret_cast<const double2*>(xs + r * AS + c * 4 + 2);
-                    const double w = sd.hw[r];
+                    const double w = S.hw[r];
                     a0 += w * x.x; a1 += w * x.y; a2 += w * y.x; a3 += w * y.y;
                 }
 #pragma unroll
@@ -303,6 +383,7 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
                 }
             }
         }
+        PROF(4);
         // ---- canonical keys + changed flags out
         for (int q = tid; q < ncell * KW; q += NCT) {
             const int c = q / KW, w = q - c * KW;
@@ -310,6 +391,8 @@ __global__ void __launch_bounds__(NT, 2) k_compose_narrow(const __grid_constant_
         }
         if (tid < ncell) P.changed[item0 + tid] = S.changed[tid];
         bar_sync(1, NCT);
+        PROF(5);
+        if (prof) atomicAdd(&P.prof[7], 1ull);
     }
 }
 
@@ -367,15 +450,17 @@ void launch_compose_narrow(const NarrowCompose& P, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = (P.dbg & 4) ? tiles : std::min<int64_t>(tiles, (int64_t)sms * 2);
+    const int64_t grid = (P.dbg & 4) ? tiles : std::min<int64_t>(tiles, (int64_t)sms * CPS);
     const size_t smem = sizeof(NarrowSmem) + 1024;
     // per device: the attribute is a property of the function on the current device
     static bool init[64] = {};
     if (dev < 64 && !init[dev]) {
-        cudaFuncSetAttribute(k_compose_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_compose_narrow<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_compose_narrow<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init[dev] = true;
     }
-    launch_k(k_compose_narrow, (unsigned)grid, NT, smem, s, P);
+    if (P.fp32) launch_k(k_compose_narrow<1>, (unsigned)grid, NT, smem, s, P);
+    else launch_k(k_compose_narrow<0>, (unsigned)grid, NT, smem, s, P);
 }
 
 }  // namespace am
