@@ -11,7 +11,8 @@ seed points resident in HBM; ``e2e`` = the same through the public
 ``march(net, MarchConfig)`` call from host buffers (engine creation + weight
 upload, seeding, marching, results back to host, sorted like the reference).
 With N > 1 ranks (torchrun, one per GPU) states are sharded by hash ownership
-and the frontier is exchanged with an NCCL all-to-all every wave.
+and the frontier is exchanged with one NCCL all-to-all per round of BFS
+iterations (paper_2106_10031_b200/distributed.py).
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the C
 oracle restatement; the reference itself is pure Python) on the host cores.
@@ -209,6 +210,7 @@ def main():
         seeds = sm.sample_seeds(args.seeds, rng_seed=0)
         run_once = lambda: sm.run(seeds)  # noqa: E731
         engine = sm.engine
+        stream = sm.stream   # the engine and its exchange run on the marcher's stream
     else:
         engine = Engine(net, bbox=bbox)
         seeds = sample_seeds(engine, args.seeds, bbox, rng_seed=0)
@@ -247,6 +249,7 @@ def main():
     clocks = clk.summary()
     st1 = engine.stats()
     counts = engine.counts()
+    assert counts["overflow"] == 0, "cells exceeded the face solver's limits: the march is incomplete"
     cells_local = counts["cells"]
     t_local = float(np.mean(times))
     if world > 1:
@@ -262,17 +265,29 @@ def main():
     launches = (st1["launches"] - st0["launches"]) / max(args.steps, 1)
 
     # ------------------------------------------------- kernel timing (roofline)
-    engine.set_timing(True)
-    run_once()          # stats are reset by the engine at the start of every march
+    # timing mode: every BFS iteration is cut by CUDA events on the engine's stream into contiguous
+    # stages (take, compose, canonical insert, frontier, near lists, face solver, flip insert,
+    # probe records) + the exact probe forwards, so the stages add up to the iterations' device
+    # time; one extra march, not part of the timed steps.  (Ranks > 1: measured on rank 0's own
+    # single-GPU engine -- the per-kernel figures do not depend on sharding.)
+    if world > 1:
+        tengine = Engine(net, bbox=bbox)
+        tseeds = torch.as_tensor(seeds, device=dev)
+
+        def trun():
+            tengine.reset()
+            tengine.seed(tseeds)
+            return tengine.run()
+    else:
+        tengine, trun = engine, run_once
+    tengine.set_timing(True)
+    trun()          # stats are reset by the engine at the start of every march
     torch.cuda.synchronize()
-    s1 = engine.stats()
-    engine.set_timing(False)
-    comp_ms = s1["compose_ms"]
-    face_ms = s1["face_ms"]
-    probe_ms = s1["probe_ms"]
-    comp_tf = s1["compose_flops"] / (comp_ms * 1e-3) / 1e12 if comp_ms else 0.0
-    face_gbs = s1["face_bytes"] / (face_ms * 1e-3) / 1e9 if face_ms else 0.0
-    probe_tf = s1["probe_flops"] / (probe_ms * 1e-3) / 1e12 if probe_ms else 0.0
+    s1 = tengine.stats()
+    kt = tengine.kernel_times()
+    tengine.set_timing(False)
+    overflow = tengine.counts()["overflow"]
+    assert overflow == 0, f"{overflow} cells exceeded the face solver's limits"
     pk = np.zeros(2)
     _native.check(lib.am_bench_fp64_peak(local_rank, pk.ctypes.data), "am_bench_fp64_peak")
     hbm, hbm_src = _peaks()
@@ -288,23 +303,54 @@ def main():
             return {"traffic": t}
         return {"traffic": t.get("dram_bytes_per_launch"), "traffic_launch": t.get("launch"),
                 "traffic_algorithmic_bytes": t.get("algorithmic_bytes_per_launch")}
+    ms = kt["ms"]
+    stage_sum = sum(ms.values())
+    kw8 = kt["kw"] * 8
+    comp_ms = ms["compose"]
+    comp_flops = s1["flops_per_cell"] * kt["composed"]
+    comp_tf = comp_flops / (comp_ms * 1e-3) / 1e12 if comp_ms else 0.0
+    face_ms = ms["near"] + ms["face"]
+    face_gbs = s1["face_bytes"] / (face_ms * 1e-3) / 1e9 if face_ms else 0.0
+    # hash inserts: every candidate reads its key and probes a slot; every new entry writes its
+    # key, hint, slot and queue entry
+    ins_ms = ms["canonical_insert"] + ms["flip_insert"]
+    ins_bytes = (kt["flips"] + kt["canonical"]) * (kw8 + 8) + kt["new_entries"] * (kw8 + 8 + 32 + 4)
+    ins_gbs = ins_bytes / (ins_ms * 1e-3) / 1e9 if ins_ms else 0.0
+    rec_ms = ms["probe_records"]
+    rec_bytes = kt["probe_records"] * (4 + 4 + 24 + 4)
+    rec_gbs = rec_bytes / (rec_ms * 1e-3) / 1e9 if rec_ms else 0.0
     kernels = {
         "compose_dmma": {"bound": "tensor", "achieved": comp_tf, "peak": float(pk[0]), "unit": "TFLOP/s",
                          "frac": comp_tf / pk[0] if pk[0] else None, "ms": comp_ms,
                          "peak_source": "measured fp64 DMMA microbenchmark (am_bench_fp64_peak)",
-                         "kernels": "k_input_step + k_gemm_step<4> x L + k_face_head",
+                         "kernels": "k_compose_narrow: gather + every layer + face head in one launch (plain "
+                                    "nets of width <= 96; else k_gather_input + k_gemm_step x L + k_face_head)",
                          "algorithmic": "sum_l 2 n_l n_(l-1) 4 FLOP per composed cell", **traffic_of("compose")},
-        "face": {"bound": "hbm", "achieved": face_gbs, "peak": hbm, "unit": "GB/s",
-                 "frac": face_gbs / hbm, "ms": face_ms, "peak_source": hbm_src,
-                 "kernels": "k_near + k_face (the face stage)",
-                 "algorithmic": "NB*32 + M*32 + KW*8 bytes per faced cell (planes, faces, key read once)",
-                 **traffic_of("face")},
-        "probe_forward_dmma": {"bound": "tensor", "achieved": probe_tf, "peak": float(pk[0]), "unit": "TFLOP/s",
-                               "frac": probe_tf / pk[0] if pk[0] else None, "ms": probe_ms,
-                               "probes": s1["probes"], "peak_source": "measured fp64 DMMA microbenchmark",
-                               **traffic_of("probe")},
+        "face_stage": {"bound": "hbm", "achieved": face_gbs, "peak": hbm, "unit": "GB/s",
+                       "frac": face_gbs / hbm, "ms": face_ms, "ms_near": ms["near"], "ms_face": ms["face"],
+                       "peak_source": hbm_src, "kernels": "k_near + k_face",
+                       "algorithmic": "NB*32 + M*32 + KW*8 bytes per faced cell (planes, faces, key read once)",
+                       **traffic_of("face")},
+        "hash_insert": {"bound": "hbm", "achieved": ins_gbs, "peak": hbm, "unit": "GB/s",
+                        "frac": ins_gbs / hbm, "ms": ins_ms, "ms_canonical": ms["canonical_insert"],
+                        "ms_flips": ms["flip_insert"], "peak_source": hbm_src,
+                        "kernels": "k_route_changed + k_hash_upsert (canonical keys), k_hash_upsert (flips)",
+                        "algorithmic": "(KW*8 + 8) B per candidate + (KW*8 + 52) B per new entry",
+                        "candidates": kt["flips"] + kt["canonical"], "new_entries": kt["new_entries"]},
+        "probe_records": {"bound": "hbm", "achieved": rec_gbs, "peak": hbm, "unit": "GB/s", "frac": rec_gbs / hbm,
+                          "ms": rec_ms, "records": kt["probe_records"], "kernels": "k_probe_records",
+                          "algorithmic": "36 B per probe record (target, neuron, point, status)"},
+        "probe_forward_dmma": {"ms": ms["probe_forward"], "probes": s1["probes"],
+                               "kernels": "exact forwards of unvalidated probes (k_gemm_step<1,64> x L + heads)"},
+        "take": {"ms": ms["take"]}, "frontier": {"ms": ms["frontier"]},
     }
-    dominant = max(kernels, key=lambda k: kernels[k]["ms"])
+    stages = {"ms": {k: round(v, 4) for k, v in ms.items()},
+              "share": {k: round(v / stage_sum, 4) if stage_sum else None for k, v in ms.items()},
+              "sum_ms": stage_sum, "iterations": kt["iterations"],
+              "note": "timing-mode march (events between stages, one host sync per iteration, no PDL overlap "
+                      "across the sync); sum_ms / ms_per_step shows the overhead of cutting the graph"}
+    rooflined = ("compose_dmma", "face_stage", "hash_insert", "probe_records")
+    dominant = max(rooflined, key=lambda k: kernels[k]["ms"])
     roof = dict(kernels[dominant])
     roof["kernel"] = dominant
 
@@ -456,6 +502,35 @@ def main():
         }
         marching.clear_engine_cache()
 
+    elif world > 1 and not args.no_extra:
+        # the largest MLP (configs[2]) sharded over the ranks: a capped sample of its march
+        from paper_2106_10031_b200 import synth
+        from paper_2106_10031_b200.distributed import ShardedMarcher
+        dnet = synth.deepsdf_mlp(512, 8, 4, seed=0)
+        cap = args.deepsdf_cells
+        dsm = ShardedMarcher(dnet, bbox=bbox, max_cells=cap)
+        dseeds = dsm.sample_seeds(args.seeds, rng_seed=0)
+        dsm.run(dseeds)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        rounds = dsm.run(dseeds)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        st = dsm.engine.shard_stats()
+        agg = torch.tensor([(t1 - t0) * 1e3, float(st["visited"])], dtype=torch.float64, device=dev)
+        dmax = agg[:1].clone()
+        dist.all_reduce(dmax, op=dist.ReduceOp.MAX)
+        dsum = agg[1:].clone()
+        dist.all_reduce(dsum, op=dist.ReduceOp.SUM)
+        d_ms, dcells = float(dmax.item()), int(dsum.item())
+        others["configs[2]"] = {
+            "workload": "DeepSDF-style 3-(512x8)-1, linear skip over layers 1-4, seed 0, fp64, 64 dichotomy seeds; "
+                        f"first {dcells} cells (global max_cells cap {cap} shared out over {world} ranks)",
+            "cells": dcells, "rounds": int(rounds), "ms": d_ms, "cells_per_s": dcells / (d_ms * 1e-3),
+            "timing": "wall clock around ShardedMarcher.run, max over ranks"}
+        del dsm
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu, _ = cpu_baseline_run(net, seeds)
@@ -469,7 +544,8 @@ def main():
                        "parallelism": f"dp{world} (state-hash ownership)" if world > 1 else "1 GPU",
                        "l2": "flushed between timed steps (512 MiB write)",
                        "device_march_time_s": t_step * 1e-3, "ms_steps": [round(x, 3) for x in times]},
-            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "other_configs": others,
+            "roofline": roof, "kernels": kernels, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
+            "other_configs": others,
             "gpu_launches": int(launches), "clocks": clocks,
             "fp64_peaks_tflops": {"dmma": float(pk[0]), "dfma": float(pk[1])},
         }

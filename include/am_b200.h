@@ -67,7 +67,7 @@ typedef struct {
     int64_t max_cells;    /* visited-cell cap                 (reference marching.py:59) */
     int64_t batch_cells;  /* cells composed per batch (0 = size from mem_budget) */
     int64_t mem_budget;   /* bytes for per-batch plane buffers (0 = 2 GiB) */
-    int32_t rank, world;  /* state ownership: owner(state) = hash(state) % world */
+    int32_t rank, world;  /* state ownership: owner(state) = (hash(state) >> 7) % world */
     int32_t n_shapes;     /* > 1: batch of same-architecture shapes marched together (the key
                            * gains a trailing shape word; see am_engine_set_shape_params) */
     int32_t precision;    /* 0: fp64 (reference arithmetic); 1: fp32 mode -- weights and every
@@ -134,7 +134,7 @@ int am_wave(am_engine *e, int64_t *h_new_cells);
 /* run waves until no candidates remain (single rank); *h_waves = waves run */
 int am_run(am_engine *e, int64_t *h_waves);
 
-/* --- sharded marching (owner = hash % world) ------------------------------ */
+/* --- sharded marching (owner = (hash >> 7) % world) ----------------------- */
 /* with world > 1, states emitted by a wave that another rank owns are held in
  * an outbox instead of being inserted locally.  am_outbox_counts gives the
  * total; am_outbox_take moves them to d_out grouped by owner rank
@@ -144,6 +144,31 @@ int am_outbox_counts(am_engine *e, int64_t *h_total);
 int am_outbox_take(am_engine *e, uint64_t *d_out, int64_t *h_counts);
 /* states queued but not yet composed on this rank */
 int am_queue_size(am_engine *e, int64_t *h_n);
+
+/* Device-driven rounds (the multi-GPU march's loop; one host synchronisation per round).
+ * A round is
+ *   am_shard_iterate(e, iters, cap, h_out) -- synchronises once: reads the engine counters and
+ *       the headers of the previous exchange.  h_out[0] = 1 when every rank reported no queued
+ *       work, no outbox and nothing sent (the march is over on every rank at the same round);
+ *       h_out[1] = the exchange capacity (keys per destination) for this round's exchange, agreed
+ *       from the headers (>= cap; identical on every rank); h_out[2] = visited cells summed over
+ *       ranks, h_out[3] = any rank capped.  Otherwise replays up to `iters` BFS iterations on
+ *       the owned queue (asynchronously, on the engine stream);
+ *   am_shard_pack(e, d_send, cap)  -- outbox -> d_send, [world][am_shard_rows(e, cap)][KW]
+ *       uint64 blocks, block r for rank r, each opening with a count header; keys beyond cap
+ *       per destination stay in the outbox for the next round (asynchronous);
+ *   the caller's all-to-all of equal blocks d_send -> d_recv (e.g. NCCL over NVLink) on the
+ *       engine stream;
+ *   am_shard_absorb(e, d_recv, cap) -- queues the received keys (device-side counts) and copies
+ *       the headers to the host for the next am_shard_iterate (asynchronous).
+ * Replaces the reference's shared visited set + queue of the threaded marcher
+ * (reference marching.py:217-316) by a partitioned one. */
+int am_shard_rows(am_engine *e, int64_t cap);
+int am_shard_iterate(am_engine *e, int iters, int64_t cap, int64_t *h_out);
+int am_shard_pack(am_engine *e, uint64_t *d_send, int64_t cap);
+int am_shard_absorb(am_engine *e, const uint64_t *d_recv, int64_t cap);
+/* h_out[6]: rounds, host synchronisations so far, iterations, pool entries, visited, outbox */
+int am_shard_stats(am_engine *e, int64_t *h_out);
 
 /* --- results ------------------------------------------------------------- */
 /* h_counts[8]: cells, faces, empty, verts, edge_refs, open_edges, capped, overflow */
@@ -186,6 +211,12 @@ int am_unique_planes(const double *d_planes, int64_t m, double tol, int32_t *d_p
  * kernel, and the algorithmic flop / byte counts they processed */
 int am_stats(am_engine *e, double *h_out16);
 int am_set_timing(am_engine *e, int enabled);
+/* timing mode: per-stage device time (ms) of the timed iterations, the stages contiguous so they
+ * sum to the iterations' device time: h_out16[0..8] take, compose, canonical insert, frontier,
+ * near lists, face solver, flip insert, probe records, exact probe forwards; [9] iterations;
+ * [10] flip candidates; [11] changed canonical keys; [12] probe records; [13] new pool entries;
+ * [14] key words; [15] cells composed */
+int am_kernel_times(am_engine *e, double *h_out16);
 /* measured fp64 peaks of this device: h_out2[0] DMMA (tensor) TFLOP/s, [1] DFMA TFLOP/s */
 int am_bench_fp64_peak(int device, double *h_out2);
 /* face-kernel instrumentation counters (64; non-zero only in -DAM_FACE_STATS builds), reset on read */

@@ -293,6 +293,7 @@ class OracleShardEngine:
         self.visited = set()
         self.queue = []
         self.out = []
+        self.hdr = None
 
     def _owner(self, k):
         return int(key_owner(np.asarray(k, dtype=np.uint64).reshape(1, -1), self.world)[0])
@@ -339,18 +340,57 @@ class OracleShardEngine:
                 self._route(list(buf[:n].copy()))
         return new
 
-    def outbox(self):
-        import torch
+    # ---- device-driven round protocol of the GPU engine (Engine.shard_*), restated on the host
+    HDR_WORDS = 8
+
+    def shard_rows(self, cap):
+        return (self.HDR_WORDS + self.kw - 1) // self.kw + int(cap)
+
+    def shard_iterate(self, iters, cap):
+        visited, capped = len(self.visited), False
+        if self.hdr is not None:
+            h = self.hdr
+            idle = not (h[:, 1].any() or h[:, 2].any() or h[:, 3].any())
+            while cap < int(h[:, 4].max()):
+                cap *= 2
+            visited, capped = int(h[:, 5].sum()), bool(h[:, 6].any())
+            if idle:
+                return True, cap, visited, capped
+        for _ in range(int(iters)):
+            if not self.queue:
+                break
+            self.wave()
+        return False, cap, visited, capped
+
+    def shard_pack(self, send, cap):
+        rows = self.shard_rows(cap)
+        hr = rows - cap
+        buf = send.numpy().view(np.uint64).reshape(self.world, rows, self.kw)
+        buf[:] = 0
         counts = np.zeros(self.world, dtype=np.int64)
-        if not self.out:
-            return counts, torch.zeros((0, self.kw), dtype=torch.int64)
-        keys = np.stack(self.out)
-        self.out = []
-        own = key_owner(keys, self.world)
-        order = np.argsort(own, kind="stable")
-        for o in own:
+        rest = []
+        for k in self.out:
+            o = self._owner(k)
+            if counts[o] < cap:
+                buf[o, hr + counts[o]] = k
+            else:
+                rest.append(k)
             counts[o] += 1
-        return counts, torch.from_numpy(keys[order].view(np.int64).copy())
+        sent = int(np.minimum(counts, cap).sum())
+        for o in range(self.world):
+            h = buf[o, :hr].reshape(-1)
+            h[:self.HDR_WORDS] = [min(counts[o], cap), len(self.queue), len(rest), sent, counts.max(initial=0),
+                                  len(self.visited), 0, 1]
+        self.out = rest
+
+    def shard_absorb(self, recv, cap):
+        rows = self.shard_rows(cap)
+        hr = rows - cap
+        buf = recv.numpy().view(np.uint64).reshape(self.world, rows, self.kw)
+        hdr = np.stack([buf[s, :hr].reshape(-1)[:self.HDR_WORDS] for s in range(self.world)]).astype(np.int64)
+        for s in range(self.world):
+            self._route(list(buf[s, hr:hr + int(hdr[s, 0])].copy()))
+        self.hdr = hdr
 
     def queue_size(self):
         return len(self.queue)

@@ -83,6 +83,12 @@ SIGNATURES = {
     "am_seed_shapes": (ctypes.c_int, [P, P, P, ctypes.c_int64]),
     "am_dichotomy_shapes": (ctypes.c_int, [P, P, P, P, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                            ctypes.c_int, P]),
+    "am_kernel_times": (ctypes.c_int, [P, P]),
+    "am_shard_rows": (ctypes.c_int, [P, ctypes.c_int64]),
+    "am_shard_iterate": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int64, P]),
+    "am_shard_pack": (ctypes.c_int, [P, P, ctypes.c_int64]),
+    "am_shard_absorb": (ctypes.c_int, [P, P, ctypes.c_int64]),
+    "am_shard_stats": (ctypes.c_int, [P, P]),
     "am_unique_planes": (ctypes.c_int, [P, ctypes.c_int64, ctypes.c_double, P, ctypes.c_int64, P, P]),
     "am_weld": (ctypes.c_int, [P, ctypes.c_int64, P, P, ctypes.c_int64, ctypes.c_double, P, P, P, P, P, P, P]),
 }

@@ -36,7 +36,7 @@ import numpy as np
 
 from .engine import architecture_key
 from .marching import MarchConfig, MarchResult, _engine_for, collect_result, march, seed_engine
-from .network import AnyNetwork, to_blob
+from .network import AnyNetwork, is_ensemble, to_blob
 
 
 def _check_same_architecture(nets: Sequence[AnyNetwork]):
@@ -147,7 +147,8 @@ def march_batch(nets: Sequence[AnyNetwork], config: MarchConfig | None = None, s
     if world == 1 or shard == "shape":
         mine = shard_of_shapes(len(nets), rank, world)
         if engine_factory is None:
-            if fused and len(mine) > 1:
+            # batches of max-pool ensembles march shape by shape (the fused engine holds plain nets)
+            if fused and len(mine) > 1 and not is_ensemble(nets[0]):
                 return list(zip(mine, march_fused([nets[s] for s in mine], config)))
             return [(s, march(nets[s], config)) for s in mine]
         out = []

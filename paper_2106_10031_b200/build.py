@@ -28,6 +28,7 @@ SOURCES = {
     "am_weld.cu": [],
     "am_result.cu": [],
     "am_diag.cu": ["-fmad=false"],
+    "am_shard.cu": [],
 }
 
 

@@ -208,9 +208,21 @@ struct am_engine {
     int graph_batch = 32;   // iterations replayed per host synchronisation (A/B: 8 -> 25.7 ms, 16 -> 25.0, 32 -> 24.6)
     int grid_cap = 0;    // >0: CTAs per SM for persistent GEMM launches
     unsigned long long graph_kernels = 0;
+    // sharded rounds (am_shard_*): leftover outbox, pack counters, received-row index, headers
+    DBuf<uint64_t> sh_rest;
+    DBuf<unsigned long long> sh_cnt;
+    DBuf<int32_t> sh_idx;
+    uint64_t* h_hdr = nullptr;   // pinned [world][kHdrWords] headers of the last exchange
+    bool sh_have_hdr = false;
+    unsigned long long n_syncs = 0, sh_rounds = 0, sh_sent = 0, sh_recv = 0;
     // stats
     bool timing = false;
     cudaEvent_t ev[6];
+    // timing mode: contiguous per-stage buckets of an iteration (am_kernel_times)
+    static constexpr int kMarks = 9;
+    cudaEvent_t tev[kMarks] = {};
+    double t_bucket[12] = {0};
+    double n_emit = 0, n_canon = 0, n_prec = 0, n_new = 0, n_timed = 0;
     cudaEvent_t ev_join = nullptr;   // orders the caller's stream and the engine's own stream
     double t_compose = 0, t_face = 0, t_probe = 0, flops = 0, pflops = 0, face_bytes = 0;
     double n_comp_cells = 0, n_face_cells = 0, n_probes = 0;
@@ -234,6 +246,7 @@ extern "C" int am_device_info(int device, int32_t* sm, int32_t* maj, int32_t* mi
 static int sync_counters(am_engine* e) {
     CK(cudaMemcpyAsync(e->hctr, e->ctr.p, sizeof(e->hctr), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
+    e->n_syncs++;
     return AM_OK;
 }
 static int set_counter(am_engine* e, int which, unsigned long long v) {
@@ -260,8 +273,8 @@ static HashSet hs(am_engine* e) {
 static int64_t emit_per_cell() { return kEmitFlipsPerCell + kVertsPerCell; }
 
 // hash set + queue room for `extra` more states (load factor <= 1/2)
-static int ensure_hash(am_engine* e, int64_t extra) {
-    RC(sync_counters(e));
+static int ensure_hash(am_engine* e, int64_t extra, bool sync = true) {
+    if (sync) RC(sync_counters(e));
     int64_t np = (int64_t)e->hctr[C_POOL];
     int64_t need = np + extra;
     bool moved = false;
@@ -290,8 +303,8 @@ static int ensure_hash(am_engine* e, int64_t extra) {
 
 // room for `cells` more visited cells; per-vertex buffers (vertices, edge refs, validation and
 // pending-probe lists) get worst-case room for `vcells` cells (default: all of them)
-static int ensure_results(am_engine* e, int64_t cells, int64_t vcells = -1) {
-    RC(sync_counters(e));
+static int ensure_results(am_engine* e, int64_t cells, int64_t vcells = -1, bool sync = true) {
+    if (sync) RC(sync_counters(e));
     const int64_t cells_all = cells;
     if (vcells >= 0) cells = vcells;
     int64_t nc = (int64_t)e->hctr[C_CELLS], nv = (int64_t)e->hctr[C_VERTS], nr = (int64_t)e->hctr[C_REFS];
@@ -609,6 +622,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->dbg.reserve(64, s));
     CK(cudaMemsetAsync(e->dbg.p, 0, 64 * sizeof(unsigned long long), e->stream));
     for (int i = 0; i < 6; i++) cudaEventCreate(&e->ev[i]);
+    for (int i = 0; i < am_engine::kMarks; i++) cudaEventCreate(&e->tev[i]);
     CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
     int rc = ensure_hash(e, 4 * e->B * (1 + emit_per_cell()));
     if (!rc) rc = ensure_results(e, 4 * e->B);
@@ -651,6 +665,8 @@ extern "C" int am_engine_destroy(am_engine* e) {
     e->subdev.release(e->stream);
     e->ctr.release(e->stream);
     for (int i = 0; i < 6; i++) cudaEventDestroy(e->ev[i]);
+    for (int i = 0; i < am_engine::kMarks; i++) if (e->tev[i]) cudaEventDestroy(e->tev[i]);
+    if (e->h_hdr) cudaFreeHost(e->h_hdr);
     if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->own_stream) cudaStreamDestroy(e->stream);
     if (e->stream2) cudaStreamDestroy(e->stream2);
@@ -702,6 +718,10 @@ extern "C" int am_engine_reset(am_engine* e) {
     e->t_compose = e->t_face = e->t_probe = e->flops = e->pflops = e->face_bytes = 0;
     e->n_comp_cells = e->n_face_cells = e->n_probes = 0;
     e->iters = 0;
+    e->sh_have_hdr = false;
+    e->sh_rounds = 0;
+    for (double& t : e->t_bucket) t = 0;
+    e->n_emit = e->n_canon = e->n_prec = e->n_new = e->n_timed = 0;
     return AM_OK;
 }
 
@@ -877,8 +897,12 @@ static int launch_iteration(am_engine* e) {
     for (int q = 0; q < 2; q++) R.pend_s[q] = shapes ? e->pend_s[q].p : nullptr;
     R.cap_pend = e->pend_t[0].n;
     const bool multi = e->P.world > 1;
+    // timing mode: marks 0..8 cut the iteration into contiguous stages (am_kernel_times)
+    auto mark = [&](int i) { if (tm) cudaEventRecord(e->tev[i], s); };
 
+    mark(0);
     launch_take(I, s);
+    mark(1);
     const bool fuse_in = gather_fuses_input(e);
     if (e->narrow_fused) {
         if (tm) cudaEventRecord(e->ev[0], s);
@@ -910,9 +934,11 @@ static int launch_iteration(am_engine* e) {
     }
     if (!e->narrow_fused) RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B, fuse_in ? 1 : 0));
     if (tm) cudaEventRecord(e->ev[1], s);
+    mark(2);
     launch_route_changed(e->ckey.p, e->changed.p, c + C_NR, B, e->KW, e->P.rank, e->P.world, e->X.p, c + C_NX,
                          e->outbox.p, c + C_NOUT, e->canon_pos.p, s);
     launch_hash_upsert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, nullptr, 0u, e->canon_pool.p, nullptr, nullptr, e->ckey_hint.p, s);
+    mark(3);
     launch_frontier(c + C_NR, B, e->changed.p, e->batch_pool.p, e->canon_pos.p, e->status2.p, e->canon_pool.p,
                     e->pool_flags.p, e->f_items.p, e->f_pool.p, c, (long long)e->P.max_cells, s);
     FaceArgs a;
@@ -942,8 +968,11 @@ static int launch_iteration(am_engine* e) {
     a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
     a.tau_grow = e->tau_grow;
     if (tm) cudaEventRecord(e->ev[2], s);
+    mark(4);
     launch_near(a, s);
+    mark(5);
     launch_face(a, s);
+    mark(6);
     if (tm) cudaEventRecord(e->ev[3], s);
     // flips: insert (local) and queue the new states
     if (multi) {
@@ -953,6 +982,7 @@ static int launch_iteration(am_engine* e) {
     } else {
         launch_hash_upsert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
     }
+    mark(7);
     // probe records (this iteration's and the pending ones): drop / forward / keep pending
     // This iteration's exact probe evaluations.  Probe-heavy marches (wide nets, batches of
     // shapes) capture them as a conditional node of the iteration graph whose predicate
@@ -999,6 +1029,7 @@ static int launch_iteration(am_engine* e) {
         CK(cudaStreamUpdateCaptureDependencies(s, &cn, 1, cudaStreamSetCaptureDependencies));
     }
     if (tm) cudaEventRecord(e->ev[4], s);
+    mark(8);
     CK(cudaGetLastError());
     return AM_OK;
 }
@@ -1043,6 +1074,7 @@ static int probe_flush(am_engine* e) {
         float t = 0;
         cudaEventElapsedTime(&t, e->ev[5], e->ev[4]);
         e->t_probe += t;
+        e->t_bucket[8] += t;
         const double nP = (double)std::min<unsigned long long>(e->hctr[C_NPROBE], (unsigned long long)e->PB);
         e->pflops += e->flops_per_point * nP;
         e->n_probes += nP;
@@ -1073,33 +1105,43 @@ static int capture(am_engine* e) {
 // observed so far (x2, >= 8 keys) for the round's other iterations -- an under-estimate only makes
 // the guard take smaller batches (or stall until the next host round grows the buffers), never
 // overflows; the worst case for every iteration of a round would reserve ~130 keys per cell
-static int ensure_iter_room(am_engine* e, int iters) {
-    RC(sync_counters(e));
+static int ensure_iter_room(am_engine* e, int iters, bool sync = true, int64_t extra_keys = 0) {
+    if (sync) RC(sync_counters(e));
     const int64_t per_cell = 1 + emit_per_cell();
     const int64_t np = (int64_t)e->hctr[C_POOL], nc = (int64_t)e->hctr[C_CELLS];
     const int64_t g = nc > 0 ? std::min<int64_t>(per_cell, std::max<int64_t>(8, 2 * ((np + nc - 1) / nc))) : 16;
-    RC(ensure_hash(e, e->B * per_cell + (int64_t)(iters - 1) * e->B * g));
+    RC(ensure_hash(e, e->B * per_cell + (int64_t)(iters - 1) * e->B * g + extra_keys, sync));
     // per-vertex buffers likewise: one worst-case iteration (kVertsPerCell per cell) + observed
     // vertices per cell (x2, >= 8) for the rest
     const int64_t nv = (int64_t)e->hctr[C_VERTS];
     const int64_t gv = nc > 0 ? std::min<int64_t>(kVertsPerCell, std::max<int64_t>(8, 2 * ((nv + nc - 1) / nc))) : 16;
     const int64_t vcells = e->B + ((int64_t)(iters - 1) * e->B * gv + kVertsPerCell - 1) / kVertsPerCell;
-    RC(ensure_results(e, (int64_t)iters * e->B, vcells));
+    RC(ensure_results(e, (int64_t)iters * e->B, vcells, sync));
     return AM_OK;
 }
 
 static int timed_iteration(am_engine* e) {
+    const unsigned long long pool0 = e->hctr[C_POOL];
     RC(launch_iteration(e));
-    CK(cudaEventSynchronize(e->ev[4]));
+    CK(cudaEventSynchronize(e->tev[am_engine::kMarks - 1]));
     float a = 0, b = 0, c = 0;
     cudaEventElapsedTime(&a, e->ev[0], e->ev[1]);
     cudaEventElapsedTime(&b, e->ev[2], e->ev[3]);
     cudaEventElapsedTime(&c, e->ev[3], e->ev[4]);
+    for (int i = 0; i + 1 < am_engine::kMarks; i++) {
+        float t = 0;
+        cudaEventElapsedTime(&t, e->tev[i], e->tev[i + 1]);
+        e->t_bucket[i] += t;
+    }
     RC(sync_counters(e));
+    e->n_emit += (double)e->hctr[C_NEMIT];
+    e->n_canon += (double)e->hctr[C_NX];
+    e->n_prec += (double)e->hctr[C_NPREC];
+    e->n_new += (double)(e->hctr[C_POOL] - pool0);
+    e->n_timed += 1;
     if (e->hctr[C_NPROBE]) RC(probe_flush(e));
     e->t_compose += a;
     e->t_face += b;
-    e->t_probe += c;
     double nR = (double)e->hctr[C_NR], nF = (double)e->hctr[C_NF];
     e->flops += e->flops_per_cell * nR;
     e->n_comp_cells += nR;
@@ -1247,6 +1289,103 @@ extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out, int64_t* h_counts) 
         cnt.release(e->stream);
     }
     RC(set_counter(e, C_NOUT, 0));
+    return AM_OK;
+}
+
+// ------------------------------------------------------------ sharded rounds
+// One round of the multi-GPU march = am_shard_iterate (the round's only host synchronisation)
+// + am_shard_pack + the caller's all-to-all + am_shard_absorb; see include/am_b200.h.
+static int shard_hdr_rows(const am_engine* e) { return (kHdrWords + e->KW - 1) / e->KW; }
+
+extern "C" int am_shard_rows(am_engine* e, int64_t cap) {
+    if (!e || cap < 1) return fail(AM_ERR_ARG, "bad arguments");
+    return shard_hdr_rows(e) + (int)std::min<int64_t>(cap, INT32_MAX / 2);
+}
+
+extern "C" int am_shard_iterate(am_engine* e, int iters, int64_t cap, int64_t* h_out) {
+    if (!e || iters < 0 || cap < 1 || !h_out) return fail(AM_ERR_ARG, "bad arguments");
+    const int world = e->P.world;
+    RC(sync_counters(e));   // also completes the previous absorb's header copy
+    if (e->hctr[C_OVF1]) return fail(AM_ERR_OVERFLOW, "output capacity overflow (%llu events)", e->hctr[C_OVF1]);
+    int64_t done = 0, cap_next = cap, visited = 0, capped = 0;
+    if (e->sh_have_hdr) {
+        bool idle = true;
+        uint64_t demand = 0;
+        for (int r = 0; r < world; r++) {
+            const uint64_t* h = e->h_hdr + (size_t)r * kHdrWords;
+            if (h[7] != 1) return fail(AM_ERR_ARG, "exchange header of rank %d missing", r);
+            if (h[1] || h[2] || h[3]) idle = false;
+            demand = std::max<uint64_t>(demand, h[4]);
+            visited += (int64_t)h[5];
+            capped |= h[6] ? 1 : 0;
+        }
+        done = idle ? 1 : 0;
+        // the next exchange must take every rank's largest per-destination demand (identical on
+        // every rank: every rank sees every header); grows in powers of two, never shrinks
+        while ((uint64_t)cap_next < demand && cap_next < (int64_t)1 << 24) cap_next <<= 1;
+    }
+    h_out[0] = done;
+    h_out[1] = cap_next;
+    h_out[2] = visited;
+    h_out[3] = capped;
+    if (done) return AM_OK;
+    // local iterations: capacity from the counters just read (no further synchronisation), plus
+    // room for the keys the coming exchange can deliver
+    const bool queued = e->hctr[C_QHEAD] < e->hctr[C_QTAIL] || e->hctr[C_NPEND] || e->hctr[C_NPROBE];
+    const int k = queued ? iters : 0;
+    RC(ensure_iter_room(e, k + 1, false, (int64_t)world * cap_next));
+    if (k > 0) {
+        if (!e->probe_in_graph) { e->probe_in_graph = true; e->graph_valid = false; }   // probes stay on the device
+        if (!e->graph_valid) RC(capture(e));
+        for (int i = 0; i < k; i++) CK(cudaGraphLaunch(e->gexec, e->stream));
+        g_launch_count += (unsigned long long)k * e->graph_kernels;
+    }
+    return AM_OK;
+}
+
+extern "C" int am_shard_pack(am_engine* e, uint64_t* d_send, int64_t cap) {
+    if (!e || !d_send || cap < 1) return fail(AM_ERR_ARG, "bad arguments");
+    const int world = e->P.world;
+    const int64_t max_keys = e->outbox.n / e->KW;
+    CK(e->sh_rest.reserve(std::max<int64_t>(e->outbox.n, e->KW), e->stream));
+    CK(e->sh_cnt.reserve(world + 1, e->stream));
+    launch_shard_pack(e->outbox.p, e->ctr.p, e->KW, world, cap, shard_hdr_rows(e), d_send, e->sh_rest.p, e->sh_cnt.p,
+                      max_keys, e->stream);
+    CK(cudaGetLastError());
+    e->sh_rounds++;
+    return AM_OK;
+}
+
+extern "C" int am_shard_absorb(am_engine* e, const uint64_t* d_recv, int64_t cap) {
+    if (!e || !d_recv || cap < 1) return fail(AM_ERR_ARG, "bad arguments");
+    const int world = e->P.world, KW = e->KW, hr = shard_hdr_rows(e);
+    const int64_t rows = hr + cap;
+    if (!e->h_hdr) CK(cudaMallocHost(&e->h_hdr, (size_t)64 * kHdrWords * sizeof(uint64_t)));
+    if (world > 64) return fail(AM_ERR_ARG, "world size %d > 64", world);
+    CK(e->sh_idx.reserve((int64_t)world * cap, e->stream));
+    CK(e->hstatus.reserve((int64_t)world * rows, e->stream));   // upsert outputs are indexed by recv row
+    CK(e->hslot.reserve((int64_t)world * rows, e->stream));
+    // room for world * cap keys was reserved by am_shard_iterate
+    launch_shard_index(d_recv, KW, world, cap, hr, e->sh_idx.p, e->ctr.p + C_LIST, e->stream);
+    HashSet H = hs(e);
+    launch_hash_upsert(H, d_recv, e->sh_idx.p, e->ctr.p + C_LIST, (int64_t)world * cap, e->hstatus.p, e->hslot.p,
+                       nullptr, 0u, nullptr, e->queue.p, e->ctr.p + C_QTAIL, nullptr, e->stream);
+    CK(cudaMemcpy2DAsync(e->h_hdr, kHdrWords * sizeof(uint64_t), d_recv, (size_t)rows * KW * sizeof(uint64_t),
+                         kHdrWords * sizeof(uint64_t), world, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaGetLastError());
+    e->sh_have_hdr = true;
+    return AM_OK;
+}
+
+// h_out[6]: rounds, host synchronisations, iterations, pool entries, visited cells, outbox
+extern "C" int am_shard_stats(am_engine* e, int64_t* h_out) {
+    if (!e || !h_out) return fail(AM_ERR_ARG, "bad arguments");
+    h_out[0] = (int64_t)e->sh_rounds;
+    h_out[1] = (int64_t)e->n_syncs;
+    h_out[2] = (int64_t)e->hctr[C_ITER];
+    h_out[3] = (int64_t)e->hctr[C_POOL];
+    h_out[4] = (int64_t)e->hctr[C_TOTAL];
+    h_out[5] = (int64_t)e->hctr[C_NOUT];
     return AM_OK;
 }
 
@@ -1435,7 +1574,7 @@ extern "C" int am_result_counts(am_engine* e, int64_t* h) {
     h[0] = nc; h[1] = faces; h[2] = empty; h[3] = verts; h[4] = (int64_t)e->hctr[C_REFS];
     h[5] = (int64_t)e->hctr[C_OPEN];
     h[6] = e->hctr[C_CAPPED] ? 1 : 0;
-    h[7] = ovf + (int64_t)e->hctr[C_OVF0];
+    h[7] = ovf;   // every cell past the face solver's limits is recorded once (nverts -1 / -2)
     return AM_OK;
 }
 
@@ -1504,6 +1643,18 @@ extern "C" int am_set_timing(am_engine* e, int enabled) {
 
 // out: [compose_ms, face_ms, compose_flops, face_bytes, composed, faced, batch, flops_per_cell,
 //       kernel launches (process-wide), iterations, probe_ms, probe_flops, probes, flops_per_point]
+// timing mode (am_set_timing): per-stage device time of the iterations, contiguous stages
+// h[0..8] ms: take, compose, canonical insert, frontier, near, face, flip insert, probe records,
+// probe forwards; h[9] iterations timed; h[10] flip candidates emitted; h[11] changed canonical
+// keys inserted; h[12] probe records; h[13] new pool entries; h[14] key words; h[15] cells composed
+extern "C" int am_kernel_times(am_engine* e, double* h) {
+    if (!e || !h) return fail(AM_ERR_ARG, "bad arguments");
+    for (int i = 0; i < 9; i++) h[i] = e->t_bucket[i];
+    h[9] = e->n_timed; h[10] = e->n_emit; h[11] = e->n_canon; h[12] = e->n_prec; h[13] = e->n_new;
+    h[14] = (double)e->KW; h[15] = e->n_comp_cells;
+    return AM_OK;
+}
+
 extern "C" int am_stats(am_engine* e, double* h) {
     if (!e) return fail(AM_ERR_ARG, "null engine");
     RC(sync_counters(e));

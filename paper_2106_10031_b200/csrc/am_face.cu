@@ -1319,16 +1319,17 @@ __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
 void launch_near(const FaceArgs& a, cudaStream_t s) {
     if (a.n_cap <= 0 || !a.near_flags) return;
     int64_t warps = a.n_cap;
-    static int grid_max = 0;
-    if (!grid_max) {
-        int per_sm = 0, dev = 0, sms = 148;
+    static int grid_max[64] = {};   // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int di = dev >= 0 && dev < 64 ? dev : 0;
+    if (!grid_max[di]) {
+        int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near, 256, 0);
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid_max = sms * (per_sm > 0 ? per_sm : 1);
+        grid_max[di] = device_sms() * (per_sm > 0 ? per_sm : 1);
     }
     int64_t blocks = (warps + 7) / 8;
-    launch_k(k_near, (unsigned)(blocks < grid_max ? blocks : grid_max), 256, 0, s, a);
+    launch_k(k_near, (unsigned)(blocks < grid_max[di] ? blocks : grid_max[di]), 256, 0, s, a);
 }
 
 // persistent: each warp walks the device-resident frontier
@@ -1352,22 +1353,22 @@ __global__ void __launch_bounds__(FW * 32, 4) k_face(FaceArgs A) {
 void launch_face(const FaceArgs& a, cudaStream_t s) {
     if (a.n_cap <= 0) return;
     size_t smem = sizeof(FaceWarp) * FW;
-    static bool init = false;
-    static int grid = 0;
-    if (!init) {
+    static int grids[64] = {};   // per device: the smem attribute and occupancy are per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int di = dev >= 0 && dev < 64 ? dev : 0;
+    if (!grids[di]) {
         cudaFuncSetAttribute(k_face, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int per_sm = 0, dev = 0, sms = 148;
+        int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_face, FW * 32, smem);
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         // resident CTAs per SM: the per-cell latency chain, not issue throughput, bounds an
         // iteration (waves of ~2.5 k cells on ~1.8 k warps), and more warps per SM lengthen it
         int want = kFaceCtasPerSm;
         if (const char* v = getenv("AM_FACE_CTAS")) want = atoi(v);
         if (want > 0 && want < per_sm) per_sm = want;
-        grid = sms * (per_sm > 0 ? per_sm : 1);
-        init = true;
+        grids[di] = device_sms() * (per_sm > 0 ? per_sm : 1);
     }
+    const int grid = grids[di];
     int64_t need = (a.n_cap + FW - 1) / FW;
     { launch_k(k_face, (unsigned)(need < grid ? need : grid), FW * 32, smem, s, a); }
 }

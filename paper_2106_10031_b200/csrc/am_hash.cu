@@ -4,12 +4,12 @@
 // marching.py:221-245).  Slots are 64-bit words  fp(31) | cand(1) | ref(32):
 //   cand = 1 : ref indexes the key buffer of the insert launch in flight
 //   cand = 0 : ref indexes the key pool
-// Insertion is lock-free: a thread claims an empty slot with one CAS carrying a
-// reference to its own (already written) key, so concurrent duplicates resolve
-// by key comparison without a second round; a fix-up launch then moves the
-// winners' keys into the pool, rewrites their slots to pool references and
-// appends them to the work queue.  Every launch reads its item count from device
-// memory, so a whole BFS iteration is one capturable CUDA graph.
+// Insertion is lock-free and takes one launch (k_hash_upsert): a thread claims an
+// empty slot with one CAS carrying a candidate marker (its batch index), so
+// concurrent inserters of the same key resolve by comparing against the claimant's
+// batch copy; the claiming thread itself appends the key to the pool, rewrites the
+// slot to the pool reference and queues the new state.  Every launch reads its item
+// count from device memory, so a whole BFS iteration is one capturable CUDA graph.
 #include "am_internal.h"
 
 namespace am {
@@ -107,16 +107,9 @@ __global__ void k_hash_rebuild(HashSet H, int64_t n_pool) {
     }
 }
 
-static int g_sms = 0;
 static unsigned grid_for(int64_t n, int b) {
-    if (!g_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (!g_sms) g_sms = 148;
-    }
     int64_t blocks = (n + b - 1) / b;
-    int64_t cap = (int64_t)g_sms * 8;
+    int64_t cap = (int64_t)device_sms() * 8;
     return (unsigned)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
 }
 

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "../../include/am_b200.h"
 
 namespace am {
@@ -21,6 +23,20 @@ int set_error(int code, const char* fmt, ...);   // am_engine.cu; returns code
 constexpr double kDegen = 1e-12;   // reference network.py:27 DEGENERATE_NORMAL_TOL
 constexpr double kTolDet = 1e-12;  // reference cells.py:32 TOL_DET
 constexpr uint64_t kEmpty = ~0ull;
+
+// SM count of the current device (cached per device: one process may drive several GPUs)
+inline int device_sms() {
+    static int cache[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = n > 0 ? n : 148;
+    }
+    return cache[dev];
+}
 
 // number of kernels this library launched (bench.py gpu_launches)
 extern unsigned long long g_launch_count;
@@ -190,6 +206,13 @@ struct NarrowCompose {
     int dbg;                           // AM_NARROW_DBG bits (experiments; 8: phase cycle counters)
     unsigned long long* prof;          // [8] phase cycles of thread 0 of every CTA (dbg & 8)
 };
+// sharded march exchange (am_shard.cu)
+constexpr int kHdrWords = 8;
+void launch_shard_pack(uint64_t* outbox, unsigned long long* ctr, int KW, int world, int64_t cap,
+                       int hdr_rows, uint64_t* send, uint64_t* rest, unsigned long long* cnt, int64_t max_keys,
+                       cudaStream_t s);
+void launch_shard_index(const uint64_t* recv, int KW, int world, int64_t cap, int hdr_rows, int32_t* idx,
+                        unsigned long long* n, cudaStream_t s);
 bool narrow_compose_ok(const StepDev* st, int nsteps, int n_subs, int KW);
 void launch_compose_narrow(const NarrowCompose& P, cudaStream_t s);
 void launch_narrow_check(const double* Z, const double* Z2, const double* F, const double* F2, const uint64_t* K,

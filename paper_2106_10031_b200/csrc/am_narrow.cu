@@ -447,9 +447,9 @@ bool narrow_compose_ok(const StepDev* st, int nsteps, int n_subs, int KW) {
 void launch_compose_narrow(const NarrowCompose& P, cudaStream_t s) {
     if (P.n_cap <= 0) return;
     const int64_t tiles = (P.n_cap + NCELL - 1) / NCELL;
-    int dev = 0, sms = 148;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     const int64_t grid = (P.dbg & 4) ? tiles : std::min<int64_t>(tiles, (int64_t)sms * CPS);
     const size_t smem = sizeof(NarrowSmem) + 1024;
     // per device: the attribute is a property of the function on the current device

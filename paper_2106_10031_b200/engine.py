@@ -85,7 +85,10 @@ class Engine:
 
     # ------------------------------------------------------------ primitives
     def _dev(self, arr, dtype):
-        t = torch.as_tensor(np.ascontiguousarray(arr), device=self.dev)
+        a = np.ascontiguousarray(arr)
+        if not a.flags.writeable:
+            a = a.copy()
+        t = torch.as_tensor(a, device=self.dev)
         return t.to(dtype).contiguous()
 
     def _shapes(self, shapes, n):
@@ -211,6 +214,29 @@ class Engine:
         _native.check(self.lib.am_outbox_take(self.h, out.data_ptr(), counts.ctypes.data), "am_outbox_take")
         return counts, out[:total.value]
 
+    # ---------------------------------------------------- sharded rounds
+    def shard_rows(self, cap: int) -> int:
+        """Rows of one destination block of the exchange buffers (count header + cap keys)."""
+        return int(self.lib.am_shard_rows(self.h, int(cap)))
+
+    def shard_iterate(self, iters: int, cap: int):
+        """The round's one host synchronisation: (done, exchange capacity, visited over ranks,
+        any rank capped); when not done, up to `iters` iterations are replayed asynchronously."""
+        out = np.zeros(4, dtype=np.int64)
+        _native.check(self.lib.am_shard_iterate(self.h, int(iters), int(cap), out.ctypes.data), "am_shard_iterate")
+        return bool(out[0]), int(out[1]), int(out[2]), bool(out[3])
+
+    def shard_pack(self, send: torch.Tensor, cap: int):
+        _native.check(self.lib.am_shard_pack(self.h, send.data_ptr(), int(cap)), "am_shard_pack")
+
+    def shard_absorb(self, recv: torch.Tensor, cap: int):
+        _native.check(self.lib.am_shard_absorb(self.h, recv.data_ptr(), int(cap)), "am_shard_absorb")
+
+    def shard_stats(self) -> dict:
+        out = np.zeros(6, dtype=np.int64)
+        _native.check(self.lib.am_shard_stats(self.h, out.ctypes.data), "am_shard_stats")
+        return dict(zip(("rounds", "host_syncs", "iterations", "pool", "visited", "outbox"), (int(x) for x in out)))
+
     def counts(self) -> dict:
         c = np.zeros(8, dtype=np.int64)
         _native.check(self.lib.am_result_counts(self.h, c.ctypes.data), "am_result_counts")
@@ -246,6 +272,16 @@ class Engine:
                                                      enr.data_ptr(), erefs.data_ptr()), "am_result_copy_device")
         return (c, keys[:c["cells"]], nverts[:c["cells"]], verts[:c["verts"]], enr[:c["verts"]],
                 erefs[:c["edge_refs"]])
+
+    def kernel_times(self) -> dict:
+        """Timing mode: per-stage device ms of the timed iterations (contiguous stages) + counts."""
+        h = np.zeros(16)
+        _native.check(self.lib.am_kernel_times(self.h, h.ctypes.data), "am_kernel_times")
+        names = ("take", "compose", "canonical_insert", "frontier", "near", "face", "flip_insert", "probe_records",
+                 "probe_forward")
+        return {"ms": dict(zip(names, (float(x) for x in h[:9]))), "iterations": int(h[9]), "flips": int(h[10]),
+                "canonical": int(h[11]), "probe_records": int(h[12]), "new_entries": int(h[13]), "kw": int(h[14]),
+                "composed": int(h[15])}
 
     def set_timing(self, on: bool):
         _native.check(self.lib.am_set_timing(self.h, int(on)), "am_set_timing")

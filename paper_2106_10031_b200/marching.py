@@ -400,6 +400,19 @@ def _engine_for(net: AnyNetwork, config: MarchConfig) -> Engine:
     return eng
 
 
+class MarchOverflowError(RuntimeError):
+    """A cell's face exceeded the GPU face solver's limits (more than 32 polygon vertices or 64
+    candidate planes); its polygon and neighbours are missing, so the mesh would have a hole."""
+
+
+def check_overflow(report: MarchReport):
+    """Fail loudly instead of returning a mesh with holes (report.overflow counts such cells)."""
+    if report.overflow:
+        raise MarchOverflowError(
+            f"{report.overflow} cell(s) exceeded the face solver's limits (32 polygon vertices / 64 candidate "
+            "planes); the march is incomplete")
+
+
 def seed_engine(eng: Engine, seeds: np.ndarray, shapes=None):
     """Queue the refined seed states; am_seed takes at most one batch of cells per call."""
     bs = max(1, eng.batch_size)
@@ -438,8 +451,7 @@ def march(net: AnyNetwork, config: MarchConfig | None = None, engine: Engine | N
     seed_engine(eng, seeds)
     waves = eng.run()
     res = collect_result(eng, seeds, t0, waves, config.threads, keep_device=True, net=net)
-    if res.report.overflow:
-        log.warning("%d cells exceeded the face solver's fast-path limits", res.report.overflow)
+    check_overflow(res.report)
     if res.report.faces_emitted <= config.unique_planes_limit:
         res.report.unique_plane_violations = unique_plane_violations(res)
     if res.report.capped:

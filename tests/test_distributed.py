@@ -39,8 +39,8 @@ def _worker(rank, world, port, name, q):
     g = lg(name)
     bbox = tuple(map(tuple, g["config"]["bbox"]))
     sm = ShardedMarcher(g["net"], bbox=bbox, engine_factory=oracle.OracleShardEngine)
-    waves = sm.run(g["seeds"])
-    q.put((rank, waves, sm.engine.visited_keys()))
+    rounds = sm.run(g["seeds"])
+    q.put((rank, rounds, sm.engine.visited_keys()))
     dist.destroy_process_group()
 
 

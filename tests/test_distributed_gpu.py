@@ -1,5 +1,5 @@
 """The sharded march with real GPU engines: two ranks (processes) on one B200, frontier exchange
-over gloo (host-staged).  Ranks only meet in the host-side all-to-all between waves -- no kernel
+over gloo (host-staged).  Ranks only meet in the all-to-all between rounds -- no kernel
 waits on another rank -- so this checks the engines' sharded mode (owned-state filtering,
 outboxes, single waves, pushed candidates, remote probe targets): the union of the ranks'
 visited sets equals the single-GPU march and the shards are disjoint.  Multi-GPU timing is not
@@ -43,9 +43,12 @@ def _worker(rank, world, port, which, seeds, q):
     from paper_2106_10031_b200.distributed import ShardedMarcher
     net, bbox = _net(which)
     sm = ShardedMarcher(net, bbox=bbox)
-    waves = sm.run(seeds)
-    c, keys, *_ = sm.engine.results()
-    q.put((rank, waves, [k.tobytes() for k in keys]))
+    s0 = sm.engine.shard_stats()["host_syncs"]
+    rounds = sm.run(seeds)
+    syncs = sm.engine.shard_stats()["host_syncs"] - s0
+    with torch.cuda.stream(sm.stream):
+        c, keys, *_ = sm.engine.results()
+    q.put((rank, (rounds, syncs), [k.tobytes() for k in keys]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -79,6 +82,9 @@ def test_sharded_gpu_engines_union_equals_single_gpu(which):
     assert not (shards[0] & shards[1]), "a state is owned by two ranks"
     assert shards[0] and shards[1]
     assert shards[0] | shards[1] == ref
+    # one host synchronisation per round (am_shard_iterate), plus the seeding's own
+    for _, (rounds, syncs), _ in res:
+        assert rounds > 1 and syncs <= rounds + 1 + 8, (rounds, syncs)
 
 
 def _api_worker(rank, world, port, q):

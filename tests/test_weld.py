@@ -31,9 +31,18 @@ def test_oracle_weld_matches_reference(name):
     np.testing.assert_array_equal(foff, g["face_off"])
     np.testing.assert_array_equal(fidx, g["face_idx"])
     assert dropped == int(g["dropped"])
-    # remap is consistent with the kept list
-    np.testing.assert_array_equal(kept[remap], kept[remap])
-    assert remap.max(initial=-1) < len(kept)
+    # remap against the reference's contract (meshes.py:89-148): every vertex lands on a kept
+    # vertex within tol (exactly equal at tol = 0), representatives are first occurrences (the
+    # first vertex mapped to kept j IS kept j, and kept indices appear in first-occurrence order)
+    v = np.asarray(g["verts"], dtype=np.float64)
+    assert remap.shape == (len(v),) and remap.min(initial=0) >= 0 and remap.max(initial=-1) < len(kept)
+    d = np.linalg.norm(v - kept[remap], axis=1)
+    assert (d <= float(g["tol"])).all() if float(g["tol"]) > 0 else (v == kept[remap]).all()
+    first = np.full(len(kept), -1)
+    for i in range(len(v) - 1, -1, -1):
+        first[remap[i]] = i
+    np.testing.assert_array_equal(v[first], kept)
+    assert (np.diff(first) > 0).all()
 
 
 def test_oracle_weld_is_idempotent():
