@@ -125,6 +125,14 @@ int am_dichotomy(am_engine *e, const double *d_xpos, const double *d_xneg, int64
                  double seed_tol, int max_iters, double *d_out);
 int am_dichotomy_shapes(am_engine *e, const double *d_xpos, const double *d_xneg, const int32_t *d_shapes,
                         int64_t n, double eps, double seed_tol, int max_iters, double *d_out);
+/* iterative triggers from n start points (device, all in lockstep; reference seeding.py:35-77):
+ * scheme 0 = sgd on |F| (param = initial step 0.05), 1 = sphere tracing (param = eta 1.0,
+ * escape = 12 x the unit box), at most max_iters steps (1000 / 50).  d_out [n*3] final iterate,
+ * d_status [n]: 1 converged, 2 diverged (sphere tracing; the reference raises), 3 not converged
+ * (zero gradient / out of iterations); d_iters [n] iterations to convergence.  n <= the
+ * engine's batch size. */
+int am_trace(am_engine *e, const double *d_x0, int64_t n, int scheme, double seed_tol, int max_iters, double param,
+             double escape, double *d_out, int32_t *d_status, int32_t *d_iters);
 /* queue n raw candidate states (device keys) for the next absorb */
 int am_push_candidates(am_engine *e, const uint64_t *d_keys, int64_t n);
 /* one BFS iteration: dequeue up to a batch of states, compose them,

@@ -83,6 +83,8 @@ SIGNATURES = {
     "am_seed_shapes": (ctypes.c_int, [P, P, P, ctypes.c_int64]),
     "am_dichotomy_shapes": (ctypes.c_int, [P, P, P, P, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                            ctypes.c_int, P]),
+    "am_trace": (ctypes.c_int, [P, P, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                ctypes.c_double, P, P, P]),
     "am_kernel_times": (ctypes.c_int, [P, P]),
     "am_shard_rows": (ctypes.c_int, [P, ctypes.c_int64]),
     "am_shard_iterate": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int64, P]),

@@ -29,6 +29,7 @@ SOURCES = {
     "am_result.cu": [],
     "am_diag.cu": ["-fmad=false"],
     "am_shard.cu": [],
+    "am_trace.cu": ["-fmad=false"],
 }
 
 

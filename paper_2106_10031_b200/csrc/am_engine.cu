@@ -208,6 +208,10 @@ struct am_engine {
     int graph_batch = 32;   // iterations replayed per host synchronisation (A/B: 8 -> 25.7 ms, 16 -> 25.0, 32 -> 24.6)
     int grid_cap = 0;    // >0: CTAs per SM for persistent GEMM launches
     unsigned long long graph_kernels = 0;
+    // iterative trigger schemes (am_trace): per-start state
+    DBuf<double> tx, tf, txn, tfn, tcur;
+    DBuf<uint64_t> tk, tkn;
+    DBuf<unsigned long long> trun;
     // sharded rounds (am_shard_*): leftover outbox, pack counters, received-row index, headers
     DBuf<uint64_t> sh_rest;
     DBuf<unsigned long long> sh_cnt;
@@ -1289,6 +1293,61 @@ extern "C" int am_outbox_take(am_engine* e, uint64_t* d_out, int64_t* h_counts) 
         cnt.release(e->stream);
     }
     RC(set_counter(e, C_NOUT, 0));
+    return AM_OK;
+}
+
+// ------------------------------------------------------------ trigger schemes
+// sgd (scheme 0) and sphere tracing (scheme 1) from n start points, all in lockstep on the device
+// (reference seeding.py:35-77); the host looks at the running count every 8 steps only.
+extern "C" int am_trace(am_engine* e, const double* d_x0, int64_t n, int scheme, double seed_tol, int max_iters,
+                        double param, double escape, double* d_out, int32_t* d_status, int32_t* d_iters) {
+    if (!e || n < 0 || (scheme != 0 && scheme != 1) || max_iters < 0) return fail(AM_ERR_ARG, "bad arguments");
+    if (n == 0) return AM_OK;
+    if (n > e->B || n > e->PB) return fail(AM_ERR_ARG, "am_trace: at most %lld start points per call",
+                                           (long long)std::min(e->B, e->PB));
+    RC(join_caller(e));
+    cudaStream_t s = e->stream;
+    const int KW = e->KW;
+    CK(e->tx.reserve(n * 3, s)); CK(e->txn.reserve(n * 3, s));
+    CK(e->tf.reserve(n, s)); CK(e->tfn.reserve(n, s)); CK(e->tcur.reserve(n, s));
+    CK(e->tk.reserve(n * KW, s)); CK(e->tkn.reserve(n * KW, s));
+    CK(e->trun.reserve(1, s));
+    const int bw_branch = e->ensemble ? (e->NB + 63) / 64 : -1;
+    launch_trace_init(n, d_x0, e->tx.p, e->tcur.p, param, d_status, d_iters, s);
+    auto grad = [&]() -> int {   // face planes of the current states -> e->faces
+        CK(cudaMemcpyAsync(e->ckey.p, e->tk.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemsetAsync(e->changed.p, 0, n * sizeof(int32_t), s));
+        return compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n);
+    };
+    if (scheme == 0) RC(forward_host(e, e->tx.p, n, e->tf.p, e->tk.p));
+    for (int it = 0; it <= max_iters; it++) {
+        CK(cudaMemsetAsync(e->trun.p, 0, sizeof(unsigned long long), s));
+        if (scheme == 0) {
+            launch_sgd_check(n, e->tf.p, d_status, d_iters, it, seed_tol, e->trun.p, s);
+        } else {
+            RC(forward_host(e, e->tx.p, n, e->tf.p, e->tk.p));
+            launch_sphere_check(n, e->tx.p, e->tf.p, d_status, d_iters, it, seed_tol, escape, e->trun.p, s);
+        }
+        if (it % 8 == 7) {
+            unsigned long long running = 0;
+            CK(cudaMemcpyAsync(&running, e->trun.p, sizeof running, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (!running) break;
+        }
+        RC(grad());
+        if (scheme == 0) {
+            launch_sgd_propose(n, e->tx.p, e->tf.p, e->faces.p, e->ckey.p, KW, e->M, bw_branch, e->tcur.p, d_status,
+                               e->txn.p, s);
+            RC(forward_host(e, e->txn.p, n, e->tfn.p, e->tkn.p));
+            launch_sgd_accept(n, e->tx.p, e->tf.p, e->tk.p, e->txn.p, e->tfn.p, e->tkn.p, KW, e->tcur.p, d_status, s);
+        } else {
+            launch_sphere_step(n, e->tx.p, e->tf.p, e->faces.p, e->ckey.p, KW, e->M, bw_branch, param, d_status, s);
+        }
+        CK(cudaGetLastError());
+    }
+    launch_trace_finish(n, e->tx.p, d_status, d_out, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
     return AM_OK;
 }
 

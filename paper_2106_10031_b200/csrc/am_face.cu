@@ -55,7 +55,10 @@ constexpr int CMAX = 64;   // candidate plane set capacity (uint64 masks)
 constexpr int QMAX = 64;   // accepted raw vertices
 constexpr int FW = 4;      // warps per CTA
 constexpr int kFaceCtasPerSm = 3;
-constexpr int NMAX = 160;  // hinted path: rows near the hint point (more: the full path)
+#ifndef AM_NMAX
+#define AM_NMAX 160
+#endif
+constexpr int NMAX = AM_NMAX;  // hinted path: rows near the hint point (more: the full path)
 constexpr double kCDelta = 1e-10;
 constexpr double kValMargin = 1e-11;   // sign margin (unit and raw values) for probe validation
 constexpr double kTinyNorm = 1e-6;     // rows this thin make validation unreliable

@@ -213,6 +213,20 @@ void launch_shard_pack(uint64_t* outbox, unsigned long long* ctr, int KW, int wo
                        cudaStream_t s);
 void launch_shard_index(const uint64_t* recv, int KW, int world, int64_t cap, int hdr_rows, int32_t* idx,
                         unsigned long long* n, cudaStream_t s);
+// iterative trigger schemes (am_trace.cu)
+void launch_trace_init(int64_t n, const double* x0, double* x, double* cur, double step, int32_t* status,
+                       int32_t* iters, cudaStream_t s);
+void launch_sgd_check(int64_t n, const double* f, int32_t* status, int32_t* iters, int it, double tol,
+                      unsigned long long* running, cudaStream_t s);
+void launch_sgd_propose(int64_t n, const double* x, const double* f, const double* faces, const uint64_t* keys, int KW,
+                        int M, int bw_branch, const double* cur, int32_t* status, double* xn, cudaStream_t s);
+void launch_sgd_accept(int64_t n, double* x, double* f, uint64_t* keys, const double* xn, const double* fn,
+                       const uint64_t* keysn, int KW, double* cur, const int32_t* status, cudaStream_t s);
+void launch_sphere_check(int64_t n, const double* x, const double* f, int32_t* status, int32_t* iters, int it,
+                         double tol, double escape, unsigned long long* running, cudaStream_t s);
+void launch_sphere_step(int64_t n, double* x, const double* f, const double* faces, const uint64_t* keys, int KW,
+                        int M, int bw_branch, double eta, const int32_t* status, cudaStream_t s);
+void launch_trace_finish(int64_t n, const double* x, int32_t* status, double* out, cudaStream_t s);
 bool narrow_compose_ok(const StepDev* st, int nsteps, int n_subs, int KW);
 void launch_compose_narrow(const NarrowCompose& P, cudaStream_t s);
 void launch_narrow_check(const double* Z, const double* Z2, const double* F, const double* F2, const uint64_t* K,

@@ -132,6 +132,21 @@ class Engine:
                                                    seed_tol, max_iters, out.data_ptr()), "am_dichotomy")
         return out
 
+    def trace(self, x0, scheme: str, seed_tol: float, max_iters: int | None = None):
+        """sgd / sphere tracing from start points (reference seeding.py:35-77), on the device:
+        (final points (n, 3), status (n,) 1 converged / 2 diverged / 3 not converged, iterations)."""
+        x = self._dev(np.asarray(x0, np.float64).reshape(-1, 3), torch.float64)
+        n = x.shape[0]
+        sch = {"sgd": 0, "sphere_trace": 1}[scheme]
+        mi = (1000 if sch == 0 else 50) if max_iters is None else int(max_iters)
+        param = 0.05 if sch == 0 else 1.0
+        out = torch.empty_like(x)
+        status = torch.empty(n, dtype=torch.int32, device=self.dev)
+        iters = torch.empty(n, dtype=torch.int32, device=self.dev)
+        _native.check(self.lib.am_trace(self.h, x.data_ptr(), n, sch, float(seed_tol), mi, param, 12.0, out.data_ptr(),
+                                        status.data_ptr(), iters.data_ptr()), "am_trace")
+        return out, status, iters
+
     # --------------------------------------------------------------- marching
     def reset(self):
         _native.check(self.lib.am_engine_reset(self.h), "am_engine_reset")

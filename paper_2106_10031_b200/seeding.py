@@ -2,8 +2,9 @@
 
 The random sampling keeps the reference's per-index streams
 (``np.random.default_rng([rng_seed, index])``, reference seeding.py:146) so the
-same seeds come out; every field evaluation and the bisection itself run on the
-GPU (``Engine.forward`` / ``Engine.dichotomy``).
+same seeds come out; every field evaluation, the bisection and the sgd / sphere
+tracing iterations run on the GPU (``Engine.forward`` / ``Engine.dichotomy`` /
+``Engine.trace``).
 """
 
 from __future__ import annotations
@@ -26,52 +27,20 @@ def validate_scheme(net, scheme: str) -> None:
         raise SeedingError(f"scheme {scheme!r} does not trigger on occupancy fields; use 'dichotomy'")
 
 
-def _grad(eng, x: np.ndarray) -> np.ndarray:
-    """Face-plane normals of the regions containing x (reference network.py:492-499)."""
-    _, keys = eng.forward(x, keys=True)
-    _, _, faces = eng.affine_maps(keys)
-    f = faces.cpu().numpy()
-    if eng.blob.ensemble:
-        br = keys[:, -1].cpu().numpy()
-        return f[np.arange(len(x)), br, :3]
-    return f[:, 0, :3]
-
-
 def _trace(eng, x0: np.ndarray, scheme: str, seed_tol: float):
-    """Batched sphere tracing (reference seeding.py:60-81) or SGD on |F| (seeding.py:33-57)."""
-    x = x0.copy()
-    n = len(x)
-    out = [None] * n
-    iters = np.zeros(n, dtype=np.int64)
-    active = np.ones(n, dtype=bool)
-    step = np.full(n, 0.05)
-    f = eng.forward(x).cpu().numpy()
-    max_iters = 50 if scheme == "sphere_trace" else 1000
-    for it in range(max_iters + 1):
-        done = active & (np.abs(f) <= seed_tol)
-        for i in np.nonzero(done)[0]:
-            out[i] = x[i].copy()
-            iters[i] = it
-        active &= ~done
-        if not active.any() or it == max_iters:
-            break
-        idx = np.nonzero(active)[0]
-        g = _grad(eng, x[idx])
-        if scheme == "sphere_trace":
-            if np.any(np.abs(x[idx]).max(axis=1) > 12.0):
-                raise SeedingError(f"sphere tracing diverged after {it} iterations")
-            x[idx] = x[idx] - 1.0 * f[idx, None] * g
-            f[idx] = eng.forward(x[idx]).cpu().numpy()
-        else:
-            gn = np.linalg.norm(g, axis=1)
-            dead = gn == 0.0
-            active[idx[dead]] = False
-            idx, g, gn = idx[~dead], g[~dead], gn[~dead]
-            x_new = x[idx] - step[idx, None] * np.sign(f[idx])[:, None] * g / gn[:, None]
-            f_new = eng.forward(x_new).cpu().numpy()
-            flip = np.sign(f_new) != np.sign(f[idx])
-            step[idx[flip]] *= 0.5
-            x[idx], f[idx] = x_new, f_new
+    """Batched sphere tracing (reference seeding.py:60-81) or SGD on |F| (seeding.py:33-57) from
+    every start point at once, on the device (Engine.trace: forwards, gradients and updates stay in
+    HBM; no host round trip per step).  Returns (converged point or None per start, iterations)."""
+    out, iters = [None] * len(x0), np.zeros(len(x0), dtype=np.int64)
+    step = max(1, min(eng.batch_size, 4096))
+    for o in range(0, len(x0), step):
+        pts, status, it = (t.cpu().numpy() for t in eng.trace(x0[o:o + step], scheme, seed_tol))
+        if scheme == "sphere_trace" and (status == 2).any():
+            j = int(np.flatnonzero(status == 2)[0])
+            raise SeedingError(f"sphere tracing diverged after {int(it[j])} iterations")
+        for j in np.flatnonzero(status == 1):
+            out[o + j] = pts[j].copy()
+            iters[o + j] = it[j]
     return out, iters
 
 

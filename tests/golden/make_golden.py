@@ -134,6 +134,11 @@ def cases():
     # configs[0]: 3-60-60-1 geometric (sphere-SDF) init, single seed point
     out["geo_60x60"] = (lambda p: via_json(synth.geometric_mlp([60, 60], seed=0), p),
                         dict(seeds=1, rng_seed=0))
+    # the other two trigger schemes (reference seeding.py:35-77)
+    out["rand_3x10_s42_sgd"] = (lambda p: _save_ref(make_random_net(3, 10, 42), p),
+                                dict(seeds=6, rng_seed=7, scheme="sgd"))
+    out["geo_24x24_sphere"] = (lambda p: via_json(synth.geometric_mlp([24, 24], seed=1), p),
+                               dict(seeds=6, rng_seed=2, scheme="sphere_trace"))
     # configs[1] network (3-(90x6)-1) restricted to a sub-box around one surface point
     out["geo_90x6_box"] = (lambda p: via_json(synth.geometric_mlp([90] * 6, seed=0), p),
                            dict(box_around=(0.3, 0.5, 0.8), box_half=0.05))
