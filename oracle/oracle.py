@@ -410,6 +410,67 @@ class OracleShardEngine:
         return sorted(self.visited)
 
 
+class OracleBatchShardEngine(OracleShardEngine):
+    """Stand-in for a batch-of-shapes engine (n_shapes > 1): every key carries a trailing shape
+    word (hashed into the owner like the GPU engine's), and a state of shape s is canonicalised
+    and expanded with shape s's network."""
+
+    def __init__(self, nets, bbox=DEFAULT_BBOX, max_cells=10_000_000, rank=0, world=1, **_):
+        self.nets = list(nets)
+        self.ons = [OracleNet(n) for n in self.nets]
+        self.on = self.ons[0]
+        self.kw = self.on.kw + 1
+        self.rank, self.world = rank, world
+        self.bbox = np.array(list(bbox[0]) + list(bbox[1]), dtype=np.float64)
+        self.net = self.nets[0]
+        self.reset()
+
+    def seed(self, pts, shapes=None):
+        pts = np.asarray(pts, dtype=np.float64).reshape(-1, 3)
+        shapes = np.zeros(len(pts), np.int64) if shapes is None else np.asarray(shapes).reshape(-1)
+        keys = []
+        for x, sh in zip(pts, shapes):
+            r = march(self.nets[int(sh)], bbox=(tuple(self.bbox[:3]), tuple(self.bbox[3:])),
+                      seed_points=x.reshape(1, 3), max_cells=1, oracle_net=self.ons[int(sh)])
+            keys.append(np.append(r.key_words[0], np.uint64(sh)))
+        self._route(keys)
+
+    def wave(self):
+        todo, self.queue = self.queue, []
+        new = 0
+        kw = self.kw - 1
+        buf = np.zeros((512, kw), dtype=np.uint64)
+        for r in todo:
+            sh = int(r[-1])
+            on = self.ons[sh]
+            base = np.zeros(kw, dtype=np.uint64)
+            lib().om_canonical(on.h, _ptr(np.ascontiguousarray(r[:-1])), _ptr(base))
+            canon = np.append(base, np.uint64(sh))
+            if self._owner(canon) != self.rank:
+                self.out.append(canon)
+                continue
+            ct = canon.tobytes()
+            if ct in self.visited:
+                continue
+            self.visited.add(ct)
+            self.seen.add(ct)
+            new += 1
+            n = lib().om_cell_expand(on.h, _ptr(base), _ptr(self.bbox), _ptr(buf), len(buf))
+            if n > 0:
+                self._route([np.append(k, np.uint64(sh)) for k in buf[:n].copy()])
+        return new
+
+    def sample_seeds_batch(self, count, bbox, rng_seed=0):
+        return [sample_seeds(on, count, bbox, "dichotomy", rng_seed) for on in self.ons]
+
+    def visited_by_shape(self):
+        out = {s: [] for s in range(len(self.nets))}
+        for t in self.visited:
+            w = np.frombuffer(t, dtype=np.uint64)
+            out[int(w[-1])].append(w[:-1].tobytes())
+        return {s: sorted(v) for s, v in out.items()}
+
+
 def weld(verts, loop_off, loop_idx, tol: float = TOL_WELD):
     """reference meshes.py:89-148 on CSR loops.  Returns (kept (K,3), face_off (F+1,),
     face_idx, face_src (F,) source loop of each kept face, remap (V,), n_dropped)."""

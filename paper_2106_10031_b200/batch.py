@@ -20,9 +20,10 @@ reused engine (exact per-shape caps).
 
 Across ranks (one process per GPU, torch.distributed initialised):
 
-* ``shard="hash"``: every shape is marched by all ranks together, states owned by
-  hash(state) mod P, one NCCL all-to-all per wave (``distributed.ShardedMarcher``); each rank
-  returns its owned part of every shape, and the union over ranks is the shape's full result.
+* ``shard="hash"``: ONE fused BFS over every shape of the batch on all ranks together: the
+  batch engine's keys carry the shape word, states are owned by hash(state) mod P and exchanged
+  in device-driven rounds (``distributed.ShardedMarcher``); each rank returns its owned part of
+  every shape, and the union over ranks is the shape's full result.
 * ``shard="shape"``: rank r marches shapes s with s % P == r alone (no collective; weak
   scaling over shapes).
 """
@@ -35,7 +36,7 @@ from typing import Sequence
 import numpy as np
 
 from .engine import architecture_key
-from .marching import MarchConfig, MarchResult, _engine_for, collect_result, march, seed_engine
+from .marching import MarchConfig, MarchResult, _engine_for, check_overflow, collect_result, march, seed_engine
 from .network import AnyNetwork, is_ensemble, to_blob
 
 
@@ -165,6 +166,29 @@ def march_batch(nets: Sequence[AnyNetwork], config: MarchConfig | None = None, s
         return out
 
     from .distributed import ShardedMarcher
+    if not is_ensemble(nets[0]):
+        # one fused BFS over every shape, states owned by hash(state incl. shape word) mod P
+        t0 = time.perf_counter()
+        sm = ShardedMarcher(list(nets), bbox=config.bbox, max_cells=config.max_cells * len(nets),
+                            engine_factory=engine_factory)
+        if config.seed_points is not None:
+            seeds = [np.asarray(config.seed_points, dtype=np.float64).reshape(-1, 3)] * len(nets)
+        else:
+            seeds = sm.sample_seeds_batch(config.seeds, rng_seed=config.rng_seed)
+        pts = np.concatenate(seeds)
+        shp = np.concatenate([np.full(len(x), s, np.int32) for s, x in enumerate(seeds)])
+        rounds = sm.run(pts, shapes=shp)
+        if engine_factory is not None:
+            vis = sm.engine.visited_by_shape()
+            return [(s, vis[s]) for s in range(len(nets))]
+        import torch
+        with torch.cuda.stream(sm.stream):
+            res = split_batch_result(sm.engine, seeds, t0, rounds)
+        for r in res:
+            r.report.capped = sm.capped
+            check_overflow(r.report)
+        return list(enumerate(res))
+    # batches of max-pool ensembles: shape by shape, each hash-sharded
     sm = None
     out = []
     for s, net in enumerate(nets):
@@ -177,9 +201,11 @@ def march_batch(nets: Sequence[AnyNetwork], config: MarchConfig | None = None, s
             seeds = np.asarray(config.seed_points, dtype=np.float64).reshape(-1, 3)
         else:
             seeds = sm.sample_seeds(config.seeds, rng_seed=config.rng_seed, scheme=config.scheme)
-        waves = sm.run(seeds)
+        rounds = sm.run(seeds)
         if engine_factory is None:
-            out.append((s, collect_result(sm.engine, seeds, t0, waves)))
+            import torch
+            with torch.cuda.stream(sm.stream):
+                out.append((s, collect_result(sm.engine, seeds, t0, rounds, net=net)))
         else:
             out.append((s, sm.engine.visited_keys()))
     return out

@@ -79,9 +79,14 @@ class ShardedMarcher:
 
     def __init__(self, net, bbox=((-1.2,) * 3, (1.2,) * 3), max_cells: int = 10_000_000, engine_factory=None,
                  iters_per_round: int = ITERS_PER_ROUND, **kw):
+        """``net``: one network, or a list of same-architecture networks marched as ONE fused BFS
+        (a batch of shapes: the shape word is part of every key, so ownership and dedup are
+        per shape; ``max_cells`` then caps the batch total)."""
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
-        self.net = net
+        self.batch = isinstance(net, (list, tuple))
+        self.nets = list(net) if self.batch else [net]
+        self.net = self.nets[0]
         self.bbox = bbox
         self.iters = int(iters_per_round)
         self.max_cells = int(max_cells)
@@ -89,14 +94,24 @@ class ShardedMarcher:
         if engine_factory is None:
             # the engine runs on a stream of its own; the exchange is enqueued on the same stream
             self.stream = torch.cuda.Stream()
-            self.engine = Engine(net, bbox=bbox, max_cells=share, rank=self.rank, world=self.world,
-                                 stream=self.stream, **kw)
+            self.engine = Engine(self.net, bbox=bbox, max_cells=share, rank=self.rank, world=self.world,
+                                 stream=self.stream, n_shapes=len(self.nets) if self.batch else 1, **kw)
+            if self.batch:
+                self.engine.set_shapes(self.nets)
         else:
             self.stream = None
-            self.engine = engine_factory(net, bbox=bbox, max_cells=share, rank=self.rank, world=self.world, **kw)
+            self.engine = engine_factory(self.nets if self.batch else self.net, bbox=bbox, max_cells=share,
+                                         rank=self.rank, world=self.world, **kw)
         self.rounds = 0
         self.capped = False
         self._bufs = (0, None, None)
+
+    def sample_seeds_batch(self, count: int, rng_seed: int = 0) -> list:
+        """Every shape's dichotomy seeds (identical on every rank)."""
+        if hasattr(self.engine, "sample_seeds_batch"):
+            return self.engine.sample_seeds_batch(count, self.bbox, rng_seed=rng_seed)
+        from .seeding import sample_seeds_batch
+        return sample_seeds_batch(self.engine, self.nets, count, self.bbox, rng_seed=rng_seed)
 
     def load_network(self, net):
         """Next network of a same-architecture batch (weights re-uploaded, engine reused)."""
@@ -118,16 +133,18 @@ class ShardedMarcher:
                           torch.zeros(shape, dtype=torch.int64, device=dev))
         return self._bufs[1], self._bufs[2]
 
-    def run(self, seeds: np.ndarray, max_rounds: int = 1_000_000) -> int:
-        """March from the seeds (every rank passes the same seeds; each keeps the states it owns).
-        Returns the number of rounds."""
+    def run(self, seeds: np.ndarray, shapes=None, max_rounds: int = 1_000_000) -> int:
+        """March from the seeds (every rank passes the same seeds; each keeps the states it owns;
+        ``shapes``: the shape of every seed of a batch).  Returns the number of rounds."""
         eng = self.engine
         ctx = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
         with ctx:
             eng.reset()
             if self.stream is not None:
                 from .marching import seed_engine
-                seed_engine(eng, np.asarray(seeds, dtype=np.float64).reshape(-1, 3))
+                seed_engine(eng, np.asarray(seeds, dtype=np.float64).reshape(-1, 3), shapes)
+            elif self.batch:
+                eng.seed(seeds, shapes)
             else:
                 eng.seed(seeds)
             cap, rounds = INITIAL_CAP, 0

@@ -45,8 +45,8 @@ def _worker(rank, world, port, shard, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import datetime
     dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
-    res = march_batch(mk(), MarchConfig(bbox=bbox, seeds=4, rng_seed=1), shard=shard,
-                      engine_factory=oracle.OracleShardEngine)
+    factory = oracle.OracleBatchShardEngine if shard == "hash" else oracle.OracleShardEngine
+    res = march_batch(mk(), MarchConfig(bbox=bbox, seeds=4, rng_seed=1), shard=shard, engine_factory=factory)
     q.put((rank, [(s, list(v)) for s, v in res]))
     dist.destroy_process_group()
 

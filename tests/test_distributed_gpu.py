@@ -136,3 +136,55 @@ def test_march_sharded_api_union_equals_march():
     for k, v in ref.items():
         assert merged[k].shape == v.shape
         assert np.abs(merged[k] - v).max(initial=0.0) <= 1e-9
+
+
+def _batch_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, REPO)
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from test_batch import BBOX, small_latent_batch
+    from paper_2106_10031_b200.batch import march_batch
+    from paper_2106_10031_b200.marching import MarchConfig
+    res = march_batch(small_latent_batch(4), MarchConfig(bbox=BBOX, seeds=4, rng_seed=1), shard="hash")
+    out = []
+    for s, r in res:
+        off = np.concatenate([[0], np.cumsum(r.nverts)])
+        out.append((s, {r.keys[i].tobytes(): r.verts[off[i]:off[i + 1]].copy() for i in range(len(r.keys))}))
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_hash_sharded_fused_batch_union_equals_single_gpu():
+    """configs[4]'s multi-GPU form: ONE fused BFS over a batch of latent shapes, states owned by
+    hash (shape word included) across 2 ranks; per shape, the disjoint union of the ranks' cells
+    (with polygons) equals the single-GPU fused batch march."""
+    from test_batch import BBOX, small_latent_batch
+    from paper_2106_10031_b200.batch import march_fused
+    from paper_2106_10031_b200.marching import MarchConfig
+    single = march_fused(small_latent_batch(4), MarchConfig(bbox=BBOX, seeds=4, rng_seed=1))
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for s, ref in enumerate(single):
+        parts = [dict(items)[s] for _, items in res]
+        assert not (parts[0].keys() & parts[1].keys())
+        merged = {**parts[0], **parts[1]}
+        off = np.concatenate([[0], np.cumsum(ref.nverts)])
+        want = {ref.keys[i].tobytes(): ref.verts[off[i]:off[i + 1]] for i in range(len(ref.keys))}
+        assert merged.keys() == want.keys(), f"shape {s}"
+        for k, v in want.items():
+            assert merged[k].shape == v.shape and np.abs(merged[k] - v).max(initial=0.0) <= 1e-9
