@@ -34,12 +34,23 @@ PLANE_BRANCH = 1
 PLANE_BBOX = 2
 
 
-@dataclass(frozen=True)
+@dataclass(frozen=True, eq=False)
 class PlaneRef:
-    """Cell boundary plane: neuron (global bit), branch target, or box face (reference cells.py:44)."""
+    """Cell boundary plane: neuron (global bit), branch target, or box face (reference cells.py:44).
+    Equal to / hashed like any plane reference with the same (kind, index), the reference's
+    own PlaneRef included, so the two can be looked up in each other's cells."""
 
     kind: int
     index: int
+
+    def __eq__(self, other):
+        try:
+            return (self.kind, self.index) == (other.kind, other.index)
+        except AttributeError:
+            return NotImplemented
+
+    def __hash__(self):
+        return hash((self.kind, self.index))
 
     def __repr__(self) -> str:
         tag = {PLANE_NEURON: "neuron", PLANE_BRANCH: "branch", PLANE_BBOX: "bbox"}[self.kind]

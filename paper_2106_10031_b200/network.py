@@ -252,6 +252,21 @@ class StateVector(NamedTuple):
         body = "".join("1" if x else "0" for x in self.bits())
         return f"StateVector({body}{'' if self.branch is None else f'|b{self.branch}'})"
 
+    # equal to (and hashed like) any state object with the same (key, n_bits, branch) -- e.g. the
+    # reference's own StateVector, so states from either side index the same sets and dicts
+    def __eq__(self, other):
+        try:
+            return (self.key, self.n_bits, self.branch) == (other.key, other.n_bits, other.branch)
+        except AttributeError:
+            return NotImplemented
+
+    def __ne__(self, other):
+        eq = self.__eq__(other)
+        return eq if eq is NotImplemented else not eq
+
+    def __hash__(self):
+        return hash((self.key, self.n_bits, self.branch))
+
 
 class AffinePlane:
     """Affine functional x -> normal . x + offset (its zero set is a plane when normal != 0)."""

@@ -61,21 +61,49 @@ def patch():
     sys.path.insert(0, REPO)
     import exactmesh
     import exactmesh.marching as rm
+    import exactmesh.meshes as rmesh
+    import exactmesh.network as rnet
 
     from paper_2106_10031_b200 import marching as mm
 
     fields = [f.name for f in dataclasses.fields(mm.MarchConfig) if f.name in
               {g.name for g in dataclasses.fields(rm.MarchConfig)}]
 
+    def to_ref_mesh(m):
+        """This package's PolygonMesh -> the reference's (its utilities type-check their own
+        class): the conversion a binding of the reference to this engine performs."""
+        planes = None if m.face_planes is None else [rnet.AffinePlane(p.normal, p.offset) for p in m.face_planes]
+        return rmesh.PolygonMesh(m.vertices, m.faces, planes, m.dropped_faces)
+
+    class Result:
+        """The GPU MarchResult, meshes handed out as the reference's PolygonMesh."""
+
+        def __init__(self, r):
+            self.gpu = r
+
+        def __getattr__(self, name):
+            return getattr(self.gpu, name)
+
+        def polygon_soup(self):
+            return to_ref_mesh(self.gpu.polygon_soup())
+
+        def welded_mesh(self, tol=rmesh.TOL_WELD):
+            return to_ref_mesh(self.gpu.welded_mesh(tol))
+
     def march(net, config=None):
         cfg = config or rm.MarchConfig()
-        return mm.march(net, mm.MarchConfig(**{k: getattr(cfg, k) for k in fields}))
+        return Result(mm.march(net, mm.MarchConfig(**{k: getattr(cfg, k) for k in fields})))
+
+    def vertex_residuals(net, mesh_or_result):
+        if isinstance(mesh_or_result, Result):
+            mesh_or_result = mesh_or_result.gpu
+        return mm.vertex_residuals(net, mesh_or_result)
 
     rm.march = march
-    rm.vertex_residuals = mm.vertex_residuals
+    rm.vertex_residuals = vertex_residuals
     exactmesh.march = march
     if hasattr(exactmesh, "vertex_residuals"):
-        exactmesh.vertex_residuals = mm.vertex_residuals
+        exactmesh.vertex_residuals = vertex_residuals
     return march
 
 
