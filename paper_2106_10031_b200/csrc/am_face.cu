@@ -31,6 +31,7 @@
 //           is checked against every neuron / branch functional of this cell
 //           (sign consistent with the canonical state, with margin); the
 //           validated neuron ids are published for the cell's pool entry.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1329,6 +1330,7 @@ void launch_near(const FaceArgs& a, cudaStream_t s) {
     if (!grid_max[di]) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near, 256, 0);
+        if (const char* v = getenv("AM_NEAR_CTAS")) per_sm = std::min(per_sm, std::max(1, atoi(v)));
         grid_max[di] = device_sms() * (per_sm > 0 ? per_sm : 1);
     }
     int64_t blocks = (warps + 7) / 8;

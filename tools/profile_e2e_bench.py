@@ -37,10 +37,11 @@ def wrap(mod, name):
 
 
 for mod, name in [(marching, "_engine_for"), (marching, "sample_seeds"), (marching, "collect_result"),
-                  (meshes, "weld_arrays"), (meshes, "weld_device")]:
+                  (marching, "unique_plane_violations"), (marching, "device_results_to_host"),
+                  (meshes, "weld_arrays"), (meshes, "weld_device"), (meshes, "to_host")]:
     wrap(mod, name)
 from paper_2106_10031_b200 import engine as engmod  # noqa: E402
-for name in ["seed", "run"]:
+for name in ["seed", "run", "results_device", "forward", "dichotomy"]:
     f = getattr(engmod.Engine, name)
 
     def mk(f, name):
