@@ -562,6 +562,10 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
             e->narrow_fused = true;
             if (const char* v = getenv("AM_NARROW_CHECK")) e->narrow_check = atoi(v) != 0;
             if (const char* v = getenv("AM_NARROW_DBG")) N.dbg = atoi(v);
+            N.thr8 = 12; N.thr4 = 4; N.tile_cells = 0;
+            if (const char* v = getenv("AM_NARROW_THR8")) N.thr8 = atoi(v);
+            if (const char* v = getenv("AM_NARROW_THR4")) N.thr4 = atoi(v);
+            if (const char* v = getenv("AM_NARROW_TILE")) N.tile_cells = atoi(v);
         }
     }
     // batch size from the per-iteration memory budget: compose planes + worst-case probe

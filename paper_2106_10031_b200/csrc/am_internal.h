@@ -204,6 +204,9 @@ struct NarrowCompose {
     int64_t n_cap;
     int KW, zs, shape_w, fp32;
     int dbg;                           // AM_NARROW_DBG bits (experiments; 8: phase cycle counters)
+    int thr8, thr4;                    // tile width by wave size: 8 cells when n >= grid * thr8, 4 when
+                                       // n >= grid * thr4, else 2 (AM_NARROW_THR8 / AM_NARROW_THR4)
+    int tile_cells;                    // > 0: fixed tile width (AM_NARROW_TILE)
     unsigned long long* prof;          // [8] phase cycles of thread 0 of every CTA (dbg & 8)
 };
 // sharded march exchange (am_shard.cu)

@@ -95,107 +95,32 @@ __device__ __forceinline__ bool fabs_gt(double x, double t) {
     return ax > (unsigned long long)__double_as_longlong(t) && ax <= 0x7ff0000000000000ull;
 }
 
-template <int FP32>
-__global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constant__ NarrowCompose P) {
-    extern __shared__ uint8_t smem_raw[];
-    NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+// The consumer warps' tile loop for one tile width: MI 16-row fragments x NJ 8-column fragments
+// per warp; 6 warps = WR row blocks x WC column blocks; a tile is NC = WC * NJ * 2 cells.
+//   MI 2, NJ 2: 3 x 2 warps of 32 x 16, 8 cells (wide waves)
+//   MI 1, NJ 2: 6 x 1 warps of 16 x 16, 4 cells
+//   MI 1, NJ 1: 6 x 1 warps of 16 x 8,  2 cells (narrow waves: spread over more SMs)
+template <int FP32, int MI, int NJ>
+__device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, int64_t n, int64_t head0,
+                                        uint32_t& gbox, bool prof, unsigned long long& tprev) {
+    constexpr int WR = MI == 2 ? 3 : 6, WC = NCW / WR, RB = 16 * MI, CB = 8 * NJ;
+    constexpr int NC = WC * NJ * 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ns = P.nsteps;
     const int KW = P.KW;
-
-    if (tid == 0) {   // one thread initialises every barrier, then makes the inits visible to the async proxy
-        for (int i = 0; i < NSB; i++) {
-            mbar_init(&S.full[i], 1);
-            mbar_init(&S.empty[i], NCW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (int i = tid; i < NACT * NR * AS; i += NT) (&S.act[0][0])[i] = 0.0;
-    if (tid < NR / 32) S.deg1[tid] = 0u;
-    __syncthreads();
-    {   // constants of step 0 and the head (weights: not produced by the preceding kernels)
-        const StepDev& s0 = P.st[0];
-        for (int r = tid; r < s0.n_out; r += NT) {
-            const double* w = s0.W + (int64_t)r * s0.ldw;
-            const double a0 = prec_round(w[0], FP32), a1 = prec_round(w[1], FP32), a2 = prec_round(w[2], FP32);
-            S.p1[r * 4 + 0] = a0; S.p1[r * 4 + 1] = a1; S.p1[r * 4 + 2] = a2;
-            S.p1[r * 4 + 3] = s0.b ? prec_round(0.0 + s0.b[r], FP32) : 0.0;
-            if (degenerate3(a0, a1, a2)) atomicOr(&S.deg1[r >> 5], 1u << (r & 31));
-        }
-        const SubDev* sd = P.subs;
-        for (int r = tid; r < sd->last_n; r += NT) S.hw[r] = sd->hw[r];
-    }
-    __syncthreads();
-
-    // boxes per tile: every GEMM step's K extent in 16-wide boxes
-    int tile_boxes = 0;
-    for (int s = 1; s < ns; s++) tile_boxes += (P.st[s].n_in + KB - 1) / KB;
-
-    if (warp == NCW) {
-        // ---------------------------------------------------------------- producer warp
-        if (lane != 0) return;
-        for (int s = 1; s < ns; s++) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm[s])) : "memory");
-        // the weights are not produced by the preceding kernels: the first boxes are requested
-        // before the grid-dependency wait
-        uint32_t g = 0;
-        auto issue = [&](int s, int b) {
-            const int slot = g % NSB;
-            if (g >= NSB) mbar_wait(&S.empty[slot], ((g / NSB) - 1) & 1);
-            mbar_expect_tx(&S.full[slot], NR * KB * sizeof(double));
-            tma_load_2d(S.w[slot], &P.tm[s], &S.full[slot], b * KB, 0);
-            g++;
-        };
-        int ps = 1, pb = 0;   // next (step, box) of the first tile
-        const int pre = (P.dbg & 1) ? 0 : (NSB < tile_boxes ? NSB : tile_boxes);
-        for (int i = 0; i < pre; i++) {
-            issue(ps, pb);
-            if (++pb == (P.st[ps].n_in + KB - 1) / KB) { pb = 0; ps++; }
-        }
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-        const int64_t n = dev_count(P.n_dev, P.n_cap);
-        const int64_t ntiles = (n + NCELL - 1) / NCELL;
-        if ((int64_t)blockIdx.x >= ntiles) {
-            // no tile for this CTA: let the prefetched boxes land before exiting
-            for (uint32_t i = 0; i < g; i++) mbar_wait(&S.full[i % NSB], (i / NSB) & 1);
-            return;
-        }
-        bool first = true;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            for (int s = 1; s < ns; s++) {
-                const int nb = (P.st[s].n_in + KB - 1) / KB;
-                for (int b = 0; b < nb; b++) {
-                    if (first && (s < ps || (s == ps && b < pb))) continue;   // prefetched
-                    issue(s, b);
-                }
-            }
-            first = false;
-        }
-        return;
-    }
-
-    // -------------------------------------------------------------------- consumers
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const unsigned long long* ctr = P.ctr;
-    const int64_t n = dev_count(P.n_dev, P.n_cap);
-    const int64_t ntiles = (n + NCELL - 1) / NCELL;
-    const int64_t head0 = (int64_t)ctr[C_QHEAD] - n;
+    const int64_t ntiles = (n + NC - 1) / NC;
     const int g = lane >> 2, tq = lane & 3;
-    const int wm = warp % 3, wn = warp / 3;
+    const int wm = warp % WR, wn = warp / WR;
     const int pg = ((g & 3) << 1) | (g >> 2);   // fragment row permutation (bank-conflict-free W reads)
     constexpr int fp32 = FP32;
     const bool shaped = P.shape_w >= 0;   // batch of shapes: biases per cell's shape
-    uint32_t gbox = 0;
-    const bool prof = (P.dbg & 8) && P.prof && threadIdx.x == 0;
-    unsigned long long tprev = prof ? clock64() : 0;
 #define PROF(i) do { if (prof) { unsigned long long tn = clock64(); atomicAdd(&P.prof[i], tn - tprev); tprev = tn; } } while (0)
 
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t item0 = t * NCELL;
-        const int ncell = (int)(n - item0 < NCELL ? n - item0 : NCELL);
+        const int64_t item0 = t * NC;
+        const int ncell = (int)(n - item0 < NC ? n - item0 : NC);
         // ---- gather (reference order: the BFS queue slice k_take dequeued)
-        for (int q = tid; q < NCELL * KW; q += NCT) {
+        for (int q = tid; q < NC * KW; q += NCT) {
             const int c = q / KW, w = q - c * KW;
             uint64_t v = 0;
             if (c < ncell) {
@@ -247,19 +172,19 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
         for (int s = 1; s < ns; s++) {
             const StepDev& st = P.st[s];
             const int nb = (st.n_in + KB - 1) / KB;
-            double acc[2][2][4];
+            double acc[MI][NJ][4];
 #pragma unroll
-            for (int i = 0; i < 2; i++)
+            for (int i = 0; i < MI; i++)
 #pragma unroll
-                for (int j = 0; j < 2; j++)
+                for (int j = 0; j < NJ; j++)
 #pragma unroll
                     for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
-            double bias[2][2];   // this thread's 4 output rows (loads overlap the K loop)
+            double bias[MI][2];   // this thread's output rows (loads overlap the K loop)
 #pragma unroll
-            for (int mi = 0; mi < 2; mi++)
+            for (int mi = 0; mi < MI; mi++)
 #pragma unroll
                 for (int half = 0; half < 2; half++) {
-                    const int r = wm * 32 + mi * 16 + pg + half * 8;
+                    const int r = wm * RB + mi * 16 + pg + half * 8;
                     bias[mi][half] = (r < st.n_out && !shaped) ? st.b[r] : 0.0;
                 }
             const double* xs = S.act[cur];
@@ -271,20 +196,20 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
                 const double* ws = S.w[slot];
 #pragma unroll
                 for (int kk = 0; kk < KB; kk += 4) {
-                    double a[2][2], bf[2];
+                    double a[MI][2], bf[NJ];
 #pragma unroll
-                    for (int mi = 0; mi < 2; mi++) {
-                        const int r = wm * 32 + mi * 16 + pg;
+                    for (int mi = 0; mi < MI; mi++) {
+                        const int r = wm * RB + mi * 16 + pg;
                         a[mi][0] = ws[swz(r, kk + tq)];
                         a[mi][1] = ws[swz(r + 8, kk + tq)];
                     }
                     const int k = b * KB + kk + tq;
 #pragma unroll
-                    for (int nj = 0; nj < 2; nj++) bf[nj] = xs[k * AS + wn * 16 + nj * 8 + g];
+                    for (int nj = 0; nj < NJ; nj++) bf[nj] = xs[k * AS + wn * CB + nj * 8 + g];
 #pragma unroll
-                    for (int mi = 0; mi < 2; mi++)
+                    for (int mi = 0; mi < MI; mi++)
 #pragma unroll
-                        for (int nj = 0; nj < 2; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], bf[nj]);
+                        for (int nj = 0; nj < NJ; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], bf[nj]);
                 }
                 // release the slot: the generic-proxy reads of this box must be ordered before the
                 // TMA (async proxy) that will overwrite it -- without the proxy fence a refill was
@@ -298,15 +223,15 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
             if (NACT == 1) bar_sync(1, NCT);   // in place: every warp has read the layer's input
             double* xo = S.act[NACT == 1 ? 0 : cur ^ 1];
 #pragma unroll
-            for (int mi = 0; mi < 2; mi++) {
+            for (int mi = 0; mi < MI; mi++) {
 #pragma unroll
                 for (int half = 0; half < 2; half++) {
-                    const int r = wm * 32 + mi * 16 + pg + half * 8;
+                    const int r = wm * RB + mi * 16 + pg + half * 8;
                     const bool rok = r < st.n_out;
                     const int row = st.row_off + r;
 #pragma unroll
-                    for (int nj = 0; nj < 2; nj++) {
-                        const int col = wn * 16 + nj * 8 + 2 * tq;
+                    for (int nj = 0; nj < NJ; nj++) {
+                        const int col = wn * CB + nj * 8 + 2 * tq;
                         const int c = col >> 2, comp = col & 3;   // comp 0 or 2
                         const bool ok = rok && c < ncell;
                         double v0 = acc[mi][nj][half * 2], v1 = acc[mi][nj][half * 2 + 1];
@@ -394,6 +319,109 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
         PROF(5);
         if (prof) atomicAdd(&P.prof[7], 1ull);
     }
+#undef PROF
+}
+
+// cells per tile for a wave of n cells: the widest tile that still gives every CTA slot work
+__device__ __forceinline__ int tile_cells(int64_t n, const NarrowCompose& P, int grid) {
+    if (P.tile_cells) return P.tile_cells;
+    if (n >= (int64_t)grid * P.thr8) return 8;
+    if (n >= (int64_t)grid * P.thr4) return 4;
+    return 2;
+}
+
+template <int FP32>
+__global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constant__ NarrowCompose P) {
+    extern __shared__ uint8_t smem_raw[];
+    NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ns = P.nsteps;
+    const int KW = P.KW;
+
+    if (tid == 0) {   // one thread initialises every barrier, then makes the inits visible to the async proxy
+        for (int i = 0; i < NSB; i++) {
+            mbar_init(&S.full[i], 1);
+            mbar_init(&S.empty[i], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < NACT * NR * AS; i += NT) (&S.act[0][0])[i] = 0.0;
+    if (tid < NR / 32) S.deg1[tid] = 0u;
+    __syncthreads();
+    {   // constants of step 0 and the head (weights: not produced by the preceding kernels)
+        const StepDev& s0 = P.st[0];
+        for (int r = tid; r < s0.n_out; r += NT) {
+            const double* w = s0.W + (int64_t)r * s0.ldw;
+            const double a0 = prec_round(w[0], FP32), a1 = prec_round(w[1], FP32), a2 = prec_round(w[2], FP32);
+            S.p1[r * 4 + 0] = a0; S.p1[r * 4 + 1] = a1; S.p1[r * 4 + 2] = a2;
+            S.p1[r * 4 + 3] = s0.b ? prec_round(0.0 + s0.b[r], FP32) : 0.0;
+            if (degenerate3(a0, a1, a2)) atomicOr(&S.deg1[r >> 5], 1u << (r & 31));
+        }
+        const SubDev* sd = P.subs;
+        for (int r = tid; r < sd->last_n; r += NT) S.hw[r] = sd->hw[r];
+    }
+    __syncthreads();
+
+    // boxes per tile: every GEMM step's K extent in 16-wide boxes
+    int tile_boxes = 0;
+    for (int s = 1; s < ns; s++) tile_boxes += (P.st[s].n_in + KB - 1) / KB;
+
+    if (warp == NCW) {
+        // ---------------------------------------------------------------- producer warp
+        if (lane != 0) return;
+        for (int s = 1; s < ns; s++) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm[s])) : "memory");
+        // the weights are not produced by the preceding kernels: the first boxes are requested
+        // before the grid-dependency wait
+        uint32_t g = 0;
+        auto issue = [&](int s, int b) {
+            const int slot = g % NSB;
+            if (g >= NSB) mbar_wait(&S.empty[slot], ((g / NSB) - 1) & 1);
+            mbar_expect_tx(&S.full[slot], NR * KB * sizeof(double));
+            tma_load_2d(S.w[slot], &P.tm[s], &S.full[slot], b * KB, 0);
+            g++;
+        };
+        int ps = 1, pb = 0;   // next (step, box) of the first tile
+        const int pre = (P.dbg & 1) ? 0 : (NSB < tile_boxes ? NSB : tile_boxes);
+        for (int i = 0; i < pre; i++) {
+            issue(ps, pb);
+            if (++pb == (P.st[ps].n_in + KB - 1) / KB) { pb = 0; ps++; }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        const int64_t n = dev_count(P.n_dev, P.n_cap);
+        const int nc = tile_cells(n, P, gridDim.x);
+        const int64_t ntiles = (n + nc - 1) / nc;
+        if ((int64_t)blockIdx.x >= ntiles) {
+            // no tile for this CTA: let the prefetched boxes land before exiting
+            for (uint32_t i = 0; i < g; i++) mbar_wait(&S.full[i % NSB], (i / NSB) & 1);
+            return;
+        }
+        bool first = true;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int s = 1; s < ns; s++) {
+                const int nb = (P.st[s].n_in + KB - 1) / KB;
+                for (int b = 0; b < nb; b++) {
+                    if (first && (s < ps || (s == ps && b < pb))) continue;   // prefetched
+                    issue(s, b);
+                }
+            }
+            first = false;
+        }
+        return;
+    }
+
+    // -------------------------------------------------------------------- consumers
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int64_t n = dev_count(P.n_dev, P.n_cap);
+    const int64_t head0 = (int64_t)P.ctr[C_QHEAD] - n;
+    uint32_t gbox = 0;
+    const bool prof = (P.dbg & 8) && P.prof && threadIdx.x == 0;
+    unsigned long long tprev = prof ? clock64() : 0;
+    const int nc = tile_cells(n, P, gridDim.x);
+    if (nc == 8) consume<FP32, 2, 2>(S, P, n, head0, gbox, prof, tprev);
+    else if (nc == 4) consume<FP32, 1, 2>(S, P, n, head0, gbox, prof, tprev);
+    else consume<FP32, 1, 1>(S, P, n, head0, gbox, prof, tprev);
 }
 
 // debug (AM_NARROW_CHECK=1): compare the fused kernel's outputs with the per-step path's
