@@ -141,6 +141,8 @@ struct am_engine {
     DBuf<int64_t> pool_voff;
     DBuf<double> pool_hint, ckey_hint, emit_hint, near_row;
     DBuf<int32_t> near_n, near_flags, near_id;   // k_near lists per frontier entry
+    DBuf<int32_t> f_order;                        // face work order (heavy cells first)
+    bool face_order = false;                      // AM_FACE_ORDER=1: heavy cells first (A/B: 20.15 vs 19.95 ms, off)
     int near_cap = 256;
     double tau_mult = 1.0, near_reach = 4.5;   // near-list reach in hint radii (A/B after the 96-row GEMM: 6 -> 24.7-24.9 ms, 4.5 -> 24.5)
     int max_attempts = 12;                     // hinted attempts (AM_MAX_ATTEMPTS; 5 -> 12: 31 -> 28.3 ms)
@@ -614,6 +616,8 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
         CK(e->ckey2.reserve(e->ckey.n, s)); CK(e->changed2.reserve(e->changed.n, s));
     }
     CK(e->near_n.reserve(e->B, s));
+    CK(e->f_order.reserve(e->B, s));
+    if (const char* v = getenv("AM_FACE_ORDER")) e->face_order = atoi(v) != 0;
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
     CK(e->near_row.reserve(e->B * e->near_cap * 4, s));
@@ -973,6 +977,7 @@ static int launch_iteration(am_engine* e) {
     a.cursor = c + C_FCURSOR;
     a.near_cap = e->near_cap; a.near_n = e->near_n.p; a.near_flags = e->near_flags.p;
     a.near_id = e->near_id.p; a.near_row = e->near_row.p;
+    a.order = e->face_order ? e->f_order.p : nullptr; a.order_ctr = c + C_NHEAVY;
     a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
     a.tau_grow = e->tau_grow;
     if (tm) cudaEventRecord(e->ev[2], s);

@@ -1246,6 +1246,13 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
 // rows within reach = near_reach x the hint radius of the hint point, in ascending id order,
 // with their raw functionals.  Full-occupancy warps keep many row loads in flight; the face
 // solver then filters ~tens of listed rows per attempt instead of streaming all K rows.
+// face work order: heavy cells from the front, light ones from the back (longest chains first)
+__device__ __forceinline__ void place_cell(const FaceArgs& A, int64_t n, int64_t fi, bool heavy) {
+    if (!A.order) return;
+    if (heavy) A.order[atomicAdd(&A.order_ctr[0], 1ull)] = (int32_t)fi;
+    else A.order[n - 1 - (int64_t)atomicAdd(&A.order_ctr[1], 1ull)] = (int32_t)fi;
+}
+
 __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
     pdl_enter();
     const int lane = threadIdx.x & 31;
@@ -1273,7 +1280,10 @@ __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
         }
         double4 hint = reinterpret_cast<const double4*>(A.hints)[item];
         if (!(isfinite(hint.w) && face_ok)) {
-            if (lane == 0) A.near_flags[fi] = 0;
+            if (lane == 0) {
+                A.near_flags[fi] = 0;
+                place_cell(A, n, fi, face_ok);   // no hint: the full two-pass path; empty face: quick
+            }
             continue;
         }
         const double hd = ((fu[0] * hint.x + fu[1] * hint.y) + fu[2] * hint.z) + fo;
@@ -1316,6 +1326,7 @@ __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
             A.near_n[fi] = nn < A.near_cap ? nn : A.near_cap;
             A.near_flags[fi] = kNearValid | (ok ? 0 : kNearX0Bad) | (risky ? kNearRisky : 0) |
                                (nn > A.near_cap ? kNearOverflow : 0);
+            place_cell(A, n, fi, !ok || nn > A.near_cap);
         }
     }
 }
@@ -1347,7 +1358,11 @@ __global__ void __launch_bounds__(FW * 32, 4) k_face(FaceArgs A) {
     // dynamic work distribution: cell latencies vary by 10x, so warps pull cells from a cursor
     for (;;) {
         int64_t fi = 0;
-        if (lane == 0) fi = (int64_t)atomicAdd(A.cursor, 1ull);
+        if (lane == 0) {
+            fi = (int64_t)atomicAdd(A.cursor, 1ull);
+            if (fi < n && A.order) fi = A.order[fi];
+            else if (fi >= n) fi = n;
+        }
         fi = __shfl_sync(0xffffffffu, fi, 0);
         if (fi >= n) break;
         face_cell(A, W, fi);

@@ -175,6 +175,7 @@ __global__ void k_take(IterState I) {
         // flushed by the host loop (probe_flush) outside the per-iteration graph
         c[C_NX] = 0; c[C_NF] = 0; c[C_NEMIT] = 0; c[C_NLOCAL] = 0;
         c[C_NPREC] = 0; c[C_NKEEP] = 0; c[C_NPLOCAL] = 0; c[C_FCURSOR] = 0;
+        c[C_NHEAVY] = 0; c[C_NLIGHT] = 0;
         c[C_ITER] += nR > 0 ? 1ull : 0ull;
         // the batch is queue[head, head + nR): k_gather_batch copies it out (batch_pool)
         c[C_QHEAD] = (unsigned long long)((long long)c[C_QHEAD] + nR);

@@ -244,7 +244,8 @@ int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t col
 enum Ctr {
     C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_OVF0, C_OVF1, C_CAPPED, C_TOTAL, C_QHEAD, C_QTAIL, C_NR, C_NX,
     C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_NPREC, C_NPEND, C_PPAR,
-    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_NFLUSH, C_DONE, C_N
+    C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_NFLUSH, C_DONE, C_NHEAVY, C_NLIGHT,
+    C_N
 };
 
 // hash set (am_hash.cu)
@@ -388,6 +389,11 @@ struct FaceArgs {
     double tau_grow;          // reach growth factor between attempts (at least)
     int32_t* near_n;
     int32_t* near_flags;
+    // face work order (k_near -> k_face): cells known to take the slow paths (near list overflow,
+    // hint point outside the cell, no hint) first, so their long chains start with the wave
+    // instead of trailing it; null: frontier order
+    int32_t* order;
+    unsigned long long* order_ctr;   // [0] heavy cells placed from the front, [1] light from the back
     int32_t* near_id;         // [n_cap][near_cap]
     double* near_row;         // [n_cap][near_cap][4]
 };

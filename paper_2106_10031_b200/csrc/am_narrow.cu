@@ -336,7 +336,6 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
     NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ns = P.nsteps;
-    const int KW = P.KW;
 
     if (tid == 0) {   // one thread initialises every barrier, then makes the inits visible to the async proxy
         for (int i = 0; i < NSB; i++) {
