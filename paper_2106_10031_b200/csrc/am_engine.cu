@@ -142,6 +142,7 @@ struct am_engine {
     DBuf<double> pool_hint, ckey_hint, emit_hint, near_row;
     DBuf<int32_t> near_n, near_flags, near_id;   // k_near lists per frontier entry
     DBuf<int32_t> f_order;                        // face work order (heavy cells first)
+    bool canon_fused = true;    // k_canon_frontier (AM_CANON_FUSED=0: the three separate kernels)
     bool face_order = false;                      // AM_FACE_ORDER=1: heavy cells first (A/B: 20.15 vs 19.95 ms, off)
     int near_cap = 256;
     double tau_mult = 1.0, near_reach = 4.5;   // near-list reach in hint radii (A/B after the 96-row GEMM: 6 -> 24.7-24.9 ms, 4.5 -> 24.5)
@@ -618,6 +619,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->near_n.reserve(e->B, s));
     CK(e->f_order.reserve(e->B, s));
     if (const char* v = getenv("AM_FACE_ORDER")) e->face_order = atoi(v) != 0;
+    if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
     CK(e->near_row.reserve(e->B * e->near_cap * 4, s));
@@ -947,12 +949,19 @@ static int launch_iteration(am_engine* e) {
     if (!e->narrow_fused) RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B, fuse_in ? 1 : 0));
     if (tm) cudaEventRecord(e->ev[1], s);
     mark(2);
-    launch_route_changed(e->ckey.p, e->changed.p, c + C_NR, B, e->KW, e->P.rank, e->P.world, e->X.p, c + C_NX,
-                         e->outbox.p, c + C_NOUT, e->canon_pos.p, s);
-    launch_hash_upsert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, nullptr, 0u, e->canon_pool.p, nullptr, nullptr, e->ckey_hint.p, s);
-    mark(3);
-    launch_frontier(c + C_NR, B, e->changed.p, e->batch_pool.p, e->canon_pos.p, e->status2.p, e->canon_pool.p,
-                    e->pool_flags.p, e->f_items.p, e->f_pool.p, c, (long long)e->P.max_cells, s);
+    if (e->canon_fused) {
+        launch_canon_frontier(H, e->ckey.p, e->changed.p, e->batch_pool.p, c + C_NR, B, e->P.rank, e->P.world,
+                              e->outbox.p, c + C_NOUT, e->canon_pos.p, e->status2.p, e->slot2.p, e->canon_pool.p,
+                              e->ckey_hint.p, e->f_items.p, e->f_pool.p, c, (long long)e->P.max_cells, s);
+        mark(3);
+    } else {
+        launch_route_changed(e->ckey.p, e->changed.p, c + C_NR, B, e->KW, e->P.rank, e->P.world, e->X.p, c + C_NX,
+                             e->outbox.p, c + C_NOUT, e->canon_pos.p, s);
+        launch_hash_upsert(H, e->ckey.p, e->X.p, c + C_NX, B, e->status2.p, e->slot2.p, nullptr, 0u, e->canon_pool.p, nullptr, nullptr, e->ckey_hint.p, s);
+        mark(3);
+        launch_frontier(c + C_NR, B, e->changed.p, e->batch_pool.p, e->canon_pos.p, e->status2.p, e->canon_pool.p,
+                        e->pool_flags.p, e->f_items.p, e->f_pool.p, c, (long long)e->P.max_cells, s);
+    }
     FaceArgs a;
     a.Z = e->Z.p; a.faces = e->faces.p; a.keys = e->ckey.p; a.items = e->f_items.p; a.pool_idx = e->f_pool.p;
     a.hints = e->ckey_hint.p; a.emit_hint = e->emit_hint.p;

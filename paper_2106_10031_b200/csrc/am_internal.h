@@ -315,6 +315,12 @@ void launch_frontier(const unsigned long long* n_dev, int64_t n_cap, const int32
                      const int32_t* canon_pos, const int32_t* canon_status, const int32_t* canon_pool,
                      uint32_t* pool_flags, int32_t* f_items, int32_t* f_pool, unsigned long long* ctr,
                      long long max_cells, cudaStream_t s);
+// k_route_changed + canonical k_hash_upsert + k_frontier fused (one launch per iteration)
+void launch_canon_frontier(const HashSet& H, const uint64_t* ckey, const int32_t* changed, const int32_t* batch_pool,
+                           const unsigned long long* n_dev, int64_t n_cap, int rank, int world, uint64_t* outbox,
+                           unsigned long long* n_out, int32_t* canon_pos, int32_t* status2, uint64_t* slot2,
+                           int32_t* canon_pool, const double* ckey_hint, int32_t* f_items, int32_t* f_pool,
+                           unsigned long long* ctr, long long max_cells, cudaStream_t s);
 // zero n keys; with shape_w >= 0 word shape_w gets shapes[item] (or `value` when shapes is null)
 void launch_zero_keys(uint64_t* keys, const unsigned long long* n_dev, int KW, int64_t cap, int shape_w,
                       const int32_t* shapes, int value, cudaStream_t s);
