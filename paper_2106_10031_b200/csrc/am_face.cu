@@ -89,7 +89,11 @@ struct PolyPhase {
     int ord[QMAX];
 };
 
+constexpr int KWF = 72;     // key words of a cell held in shared memory (larger keys: read from HBM)
+
 struct FaceWarp {
+    uint64_t key[KWF];              // the cell's state key: every orientation / bit lookup of the
+                                    // solver reads it here instead of from global memory
     double ps[2][VMAX], pt[2][VMAX];
     double cn[NMAX][5];             // unit row (n, o) + raw normal norm (near rows, then C')
     int cid[NMAX];
@@ -500,6 +504,11 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     c.Z = A.Z + (int64_t)item * A.zs * 4;
     c.faces = A.faces + (int64_t)item * A.M * 4;
     c.key = A.keys + (int64_t)item * A.KW;
+    if (A.KW <= KWF) {   // stage the key: one coalesced load instead of a dependent round trip per lookup
+        for (int w = lane; w < A.KW; w += 32) W->key[w] = c.key[w];
+        __syncwarp();
+        c.key = W->key;
+    }
     c.NB = A.NB; c.M = A.M; c.ensemble = A.ensemble;
     c.branch = A.ensemble ? (int)c.key[A.KW - 1] : 0;
     c.K = A.NB + A.M + 6;
