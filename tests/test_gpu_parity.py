@@ -157,7 +157,8 @@ def test_fp32_mode_within_stated_tolerance():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("knob", [("AM_PROBE_IN_GRAPH", "1"), ("AM_COMPOSE_FUSED", "1"), ("AM_NEAR_CAP", "8"),
-                                  ("AM_TAU_MULT", "0.25"), ("AM_NEAR_REACH", "1")])
+                                  ("AM_TAU_MULT", "0.25"), ("AM_NEAR_REACH", "1"), ("AM_NARROW", "0"),
+                                  ("AM_NARROW_TILE", "2"), ("AM_CANON_FUSED", "0"), ("AM_FACE_ORDER", "1")])
 def test_engine_paths_match_oracle(knob, monkeypatch):
     """Every execution path of the engine is bit-exact, not only the default one: the probe stage
     as a conditional graph node, the fused all-steps composition, near-list overflow (streaming
@@ -170,7 +171,9 @@ def test_engine_paths_match_oracle(knob, monkeypatch):
     try:
         for net, kw in ((synth.deepsdf_mlp(width=128, depth=8, skip_at=4, seed=2),
                          dict(bbox=((0.0, 0.0, 0.0), (0.45, 0.45, 0.45)), seeds=4, rng_seed=2)),
-                        (synth.imnet_ensemble(widths=(32, 32, 32), n_parts=4, seed=3), dict(seeds=8, rng_seed=3))):
+                        (synth.imnet_ensemble(widths=(32, 32, 32), n_parts=4, seed=3), dict(seeds=8, rng_seed=3)),
+                        (synth.geometric_mlp([90] * 4, seed=1), dict(bbox=((0.0, 0.0, 0.0), (0.5, 0.5, 0.5)), seeds=4,
+                                                                     rng_seed=5))):
             r = m.march(net, m.MarchConfig(**kw))
             ck = (net.__class__.__name__, r.seeds.tobytes(), str(kw))
             if ck not in _ORACLE_CACHE:   # same network and seeds for every knob: one oracle run
@@ -183,3 +186,55 @@ def test_engine_paths_match_oracle(knob, monkeypatch):
 
 
 _ORACLE_CACHE: dict = {}
+
+
+def _bias_batch(n=3):
+    """Same-weight plain narrow nets that differ only in their bias vectors (a batch of shapes
+    on the fused narrow composition path, per-shape bias tables)."""
+    from paper_2106_10031_b200 import synth
+    from paper_2106_10031_b200.network import DenseLayer, NetworkSpec
+    base = synth.geometric_mlp([24, 24], seed=3, bias_std=0.05)
+    rng = np.random.default_rng(11)
+    out = []
+    for _ in range(n):
+        layers = [DenseLayer(l.weight, l.bias + rng.normal(0.0, 0.02, size=l.bias.shape)) for l in base.layers]
+        out.append(NetworkSpec(layers, base.head_weight, base.head_bias + rng.normal(0.0, 0.02)))
+    return out
+
+
+@pytest.mark.gpu
+def test_narrow_path_batch_of_shapes_matches_oracle():
+    """k_compose_narrow with per-shape biases (a fused batch of plain narrow nets) == the oracle
+    march of every shape."""
+    from paper_2106_10031_b200.batch import march_fused
+    m = _gpu()
+    nets = _bias_batch(3)
+    cfg = m.MarchConfig(seeds=6, rng_seed=4)
+    for s, r in enumerate(march_fused(nets, cfg)):
+        o = oracle.march(nets[s], seed_points=r.seeds)
+        assert r.report.cells_visited > 100
+        assert_same_march(r, o.keys, o.branch, o.nverts, o.verts, o.edge_nrefs, o.edge_refs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_narrow_and_per_layer_composition_agree_bitwise(precision, monkeypatch):
+    """The fused narrow composition and the per-layer DMMA kernels produce the same march, bit
+    for bit, in both precisions (AM_NARROW=0 selects the per-layer path)."""
+    from paper_2106_10031_b200 import synth
+    from paper_2106_10031_b200.marching import clear_engine_cache
+    m = _gpu()
+    net = synth.geometric_mlp([60, 60], seed=0)
+    cfg = m.MarchConfig(seeds=4, rng_seed=0, precision=precision)
+    clear_engine_cache()
+    a = m.march(net, cfg)
+    monkeypatch.setenv("AM_NARROW", "0")
+    clear_engine_cache()
+    try:
+        b = m.march(net, cfg)
+    finally:
+        clear_engine_cache()
+    np.testing.assert_array_equal(a.keys, b.keys)
+    np.testing.assert_array_equal(a.nverts, b.nverts)
+    np.testing.assert_array_equal(a.verts, b.verts)
+    np.testing.assert_array_equal(a.edge_refs, b.edge_refs)
