@@ -638,8 +638,12 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     for (int i = 0; i < 6; i++) cudaEventCreate(&e->ev[i]);
     for (int i = 0; i < am_engine::kMarks; i++) cudaEventCreate(&e->tev[i]);
     CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
-    int rc = ensure_hash(e, 4 * e->B * (1 + emit_per_cell()));
-    if (!rc) rc = ensure_results(e, 4 * e->B);
+    // initial room: the trigger's and one iteration's worth; the march grows it from the observed
+    // per-cell growth before every batch of graph replays (ensure_iter_room)
+    int64_t init_keys = e->B * 8;
+    if (const char* v = getenv("AM_INIT_KEYS")) init_keys = std::max<int64_t>(1024, atoll(v));
+    int rc = ensure_hash(e, init_keys);
+    if (!rc) rc = ensure_results(e, e->B, std::min<int64_t>(e->B, 4096));
     if (rc) { delete e; return rc; }
     *out = e;
     return AM_OK;
