@@ -188,3 +188,38 @@ def test_hash_sharded_fused_batch_union_equals_single_gpu():
         assert merged.keys() == want.keys(), f"shape {s}"
         for k, v in want.items():
             assert merged[k].shape == v.shape and np.abs(merged[k] - v).max(initial=0.0) <= 1e-9
+
+
+def _nccl_worker(port, q):
+    import sys
+    sys.path.insert(0, REPO)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    from paper_2106_10031_b200 import marching
+    from paper_2106_10031_b200.distributed import march_sharded
+    net, bbox = _net("geo_60x2")
+    r = march_sharded(net, marching.MarchConfig(bbox=bbox, seeds=16, rng_seed=0))
+    q.put((r.keys.tobytes(), r.nverts.tobytes(), r.verts.tobytes(), r.report.cells_visited))
+    dist.destroy_process_group()
+
+
+def test_sharded_rounds_over_nccl_single_rank():
+    """The NCCL path of the round protocol (fixed-block all_to_all_single on the marcher's stream,
+    device-side pack / absorb, header-driven termination) with one rank: the result equals
+    march()'s exactly."""
+    from paper_2106_10031_b200 import marching
+    net, bbox = _net("geo_60x2")
+    single = marching.march(net, marching.MarchConfig(bbox=bbox, seeds=16, rng_seed=0))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    keys, nv, verts, cells = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert cells == single.report.cells_visited
+    assert keys == single.keys.tobytes() and nv == single.nverts.tobytes()
+    assert np.abs(np.frombuffer(verts) - single.verts.reshape(-1)).max(initial=0.0) <= 1e-9
