@@ -194,6 +194,8 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
                 mbar_wait(&S.full[slot], (gbox / NSB) & 1);
                 if (prof) atomicAdd(&P.prof[8], clock64() - tw);
                 const double* ws = S.w[slot];
+                // (skipping the all-zero k-steps past the layer's K extent measured slower: 20.0 vs
+                // 19.65 ms -- the fully unrolled box schedules its fragment loads better)
 #pragma unroll
                 for (int kk = 0; kk < KB; kk += 4) {
                     double a[MI][2], bf[NJ];
