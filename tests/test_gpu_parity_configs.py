@@ -4,8 +4,8 @@
   default box, 234 k cells): GPU == CPU oracle bit-exactly over the whole visited set, and
   both == the digest of the UNMODIFIED reference's own march (tests/golden/make_digest.py,
   committed as tests/golden/digest_configs1.json once the ~1 h CPU reference run is done).
-* configs[2] -- DeepSDF 3-(512x8)-1 with the skip at layer 4, in a sub-box around a surface
-  point (tens of thousands of cells, the oracle's C restatement finishes in ~1 min).
+* configs[2] -- DeepSDF 3-(512x8)-1 with the skip at layer 4, in sub-boxes around a surface
+  point (67 k and ~260 k cells; the oracle's C restatement takes ~30 s / ~110 s on the box).
 * configs[3] -- IM-NET-style occupancy ensemble 4 x 3-(128x3)-1 merged by max-pooling, in a
   sub-box.
 
@@ -75,10 +75,12 @@ def test_configs1_full_march_matches_oracle_and_reference_digest():
     np.testing.assert_allclose(r.verts.sum(axis=0), d["vert_sum"], atol=1e-9 * len(r.verts), rtol=0)
 
 
-def test_configs2_deepsdf_512x8_subbox_matches_oracle():
+@pytest.mark.parametrize("half", [DEEPSDF_HALF, 0.07])
+def test_configs2_deepsdf_512x8_subbox_matches_oracle(half):
+    """67 k cells (half-size 0.035) and ~260 k cells (0.07) of the DeepSDF march."""
     from paper_2106_10031_b200 import MarchConfig, march, synth
     net = synth.deepsdf_mlp(width=512, depth=8, skip_at=4, seed=0)
-    bbox, p = _surface_box(net, (0.3, 0.5, 0.8), DEEPSDF_HALF)
+    bbox, p = _surface_box(net, (0.3, 0.5, 0.8), half)
     r = march(net, MarchConfig(bbox=bbox, seed_points=p[None]))
     assert r.report.cells_visited > 5_000 and not r.report.capped
     o = oracle.march(net, bbox=bbox, seed_points=r.seeds, threads=THREADS)
