@@ -142,6 +142,7 @@ struct am_engine {
     DBuf<double> pool_hint, ckey_hint, emit_hint, near_row;
     DBuf<int32_t> near_n, near_flags, near_id;   // k_near lists per frontier entry
     DBuf<int32_t> f_order;                        // face work order (heavy cells first)
+    bool defer = true;          // deferral of cells that outgrow their near list (AM_DEFER=0: stream them)
     bool canon_fused = true;    // k_canon_frontier (AM_CANON_FUSED=0: the three separate kernels)
     bool face_order = false;                      // AM_FACE_ORDER=1: heavy cells first (A/B: 20.15 vs 19.95 ms, off)
     int near_cap = 256;
@@ -292,7 +293,8 @@ static int ensure_hash(am_engine* e, int64_t extra, bool sync = true) {
         CK(e->pool_voff.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
         CK(e->pool_hint.reserve(e->pool.n / e->KW * 4, e->stream, true, np * 4, &moved));
     }
-    CK(e->queue.reserve(e->pool.n / e->KW, e->stream, true, (int64_t)e->hctr[C_QTAIL], &moved));
+    // a cell is queued once, plus at most once more when deferred (face solver, status 3)
+    CK(e->queue.reserve(2 * (e->pool.n / e->KW), e->stream, true, (int64_t)e->hctr[C_QTAIL], &moved));
     if ((int64_t)e->tcap < 2 * need) {
         uint64_t cap = e->tcap ? e->tcap : 1024;
         while ((int64_t)cap < 2 * need) cap <<= 1;
@@ -620,6 +622,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->f_order.reserve(e->B, s));
     if (const char* v = getenv("AM_FACE_ORDER")) e->face_order = atoi(v) != 0;
     if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
+    if (const char* v = getenv("AM_DEFER")) e->defer = atoi(v) != 0;
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
     CK(e->near_row.reserve(e->B * e->near_cap * 4, s));
@@ -986,6 +989,8 @@ static int launch_iteration(am_engine* e) {
     a.cap_prec = e->PR;
     a.val_buf = e->val_buf.p; a.n_val = c + C_NVAL; a.cap_val = e->val_buf.n;
     a.pool_vn = e->pool_vn.p; a.pool_voff = e->pool_voff.p;
+    a.queue = e->defer ? e->queue.p : nullptr; a.q_tail = c + C_QTAIL;
+    a.pool_flags = e->pool_flags.p; a.pool_hint = e->pool_hint.p;
     a.dbg = e->dbg.p;
     a.cursor = c + C_FCURSOR;
     a.near_cap = e->near_cap; a.near_n = e->near_n.p; a.near_flags = e->near_flags.p;

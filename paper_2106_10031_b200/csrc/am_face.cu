@@ -536,7 +536,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     double P0[3] = {-fo * fu[0], -fo * fu[1], -fo * fu[2]};
 
     int nv = 0, cur = 0;
-    int status = face_ok ? 0 : 1;  // 0 ok, 1 empty, 2 overflow
+    int status = face_ok ? 0 : 1;  // 0 ok, 1 empty, 2 overflow, 3 deferred
 
     // hint: a point on this cell's polygon (the edge midpoint through which the cell was
     // found: F is continuous across the shared plane, so it lies on this face plane too)
@@ -562,6 +562,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     // square of half-size tau around x0, take C' from them, and accept the result iff
     // every vertex of P_tol lies within tau - band of x0 (else: the full two-pass path).
     bool hinted_done = false;
+    double defer_w = 0.0;   // status 3: the widened hint radius of a deferred cell
     int nC = 0;
     unsigned long long core = 0;
     int risky = 0;
@@ -584,6 +585,16 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         n_attempts++;
         if (!(use_list && tau <= reach)) n_streamed++;
 #endif
+        if (attempt > 0 && use_list && !(tau <= reach) && A.queue) {
+            // the polygon outgrew the near list: defer the cell (queued again with a hint radius
+            // whose near list covers this reach) rather than stream every row in this iteration
+            const int32_t pq = A.pool_idx[fi];
+            if (!(A.pool_flags[pq] & kPoolWasDeferred)) {
+                status = 3;
+                defer_w = tau / A.tau_mult;
+                break;
+            }
+        }
         const double x0[3] = {hint.x, hint.y, hint.z};
         const double lim = tau + band + 1e-9;
         double dmax_seen = 0.0;
@@ -1051,6 +1062,15 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
     // lane 0 builds the neighbour descriptors (reference marching.py:152-186, 262-288), then
     // every output range is reserved with one round of independent atomics
     const int32_t pidx = A.pool_idx[fi];
+    if (status == 3) {   // deferred: queued again, no record, nothing emitted or validated yet
+        if (lane == 0) {
+            A.pool_hint[(int64_t)pidx * 4 + 3] = defer_w;
+            atomicOr(&A.pool_flags[pidx], kPoolDeferred | kPoolWasDeferred);
+            __threadfence();
+            A.queue[atomicAdd(A.q_tail, 1ull)] = pidx;
+        }
+        return;
+    }
     if (status != 0) {
         if (lane == 0) {
             int64_t cell = (int64_t)atomicAdd(A.n_cells, 1ull);

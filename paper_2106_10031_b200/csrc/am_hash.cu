@@ -245,7 +245,14 @@ __global__ void k_frontier(const unsigned long long* n_dev, int64_t n_cap, const
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(b, n) {
         int32_t p = -1;
-        pool_flags[batch_pool[b]] |= 2u;   // composed (probe records aimed at it can resolve)
+        const uint32_t fl = pool_flags[batch_pool[b]];
+        pool_flags[batch_pool[b]] = (fl | 2u) & ~kPoolDeferred;   // composed (probe records can resolve)
+        if (fl & kPoolDeferred) {   // a deferred cell solved again: visited and counted already
+            const unsigned long long kf = atomicAdd(ctr + C_NF, 1ull);
+            f_items[kf] = (int32_t)b;
+            f_pool[kf] = batch_pool[b];
+            continue;
+        }
         if (!changed[b]) {
             p = batch_pool[b];
         } else if (canon_pos[b] == 1 && canon_status[b] == 1) {
@@ -278,7 +285,14 @@ __global__ void k_canon_frontier(HashSet H, const uint64_t* ckey, const int32_t*
     const int KW = H.KW;
     GRID_STRIDE(b, n) {
         int32_t p = -1;
-        H.pool_flags[batch_pool[b]] |= 2u;   // composed (probe records aimed at it can resolve)
+        const uint32_t fl = H.pool_flags[batch_pool[b]];
+        H.pool_flags[batch_pool[b]] = (fl | 2u) & ~kPoolDeferred;   // composed (probe records can resolve)
+        if (fl & kPoolDeferred) {   // a deferred cell solved again: visited and counted already
+            const unsigned long long kf = atomicAdd(ctr + C_NF, 1ull);
+            f_items[kf] = (int32_t)b;
+            f_pool[kf] = batch_pool[b];
+            continue;
+        }
         if (!changed[b]) {
             p = batch_pool[b];
         } else {
@@ -508,10 +522,10 @@ __device__ __forceinline__ void probe_decide(const ProbeRecs& R, const HashSet& 
             bool found = false;
             for (int q = 0; q < vn; q++) found |= val_buf[off + q] == k;
             forward = !found;
-        } else if (H.pool_flags[t] & 2u) {
+        } else if ((H.pool_flags[t] & 2u) && !(H.pool_flags[t] & kPoolDeferred)) {
             forward = true;   // composed but no face (canonical elsewhere / capped): exact evaluation
         } else {
-            keep = true;      // target still queued
+            keep = true;      // target still queued (or deferred: it is solved in a later iteration)
         }
     }
     if (forward) {

@@ -253,7 +253,8 @@ struct HashSet {
     uint64_t* table;      // slots
     uint64_t mask;        // capacity - 1
     uint64_t* pool;       // [cap_pool][KW]
-    uint32_t* pool_flags; // bit0 visited cell, bit1 composed
+    uint32_t* pool_flags; // bit0 visited cell, bit1 composed, bit2 deferred (queued again, already
+                          // counted as visited), bit3 was deferred once
     int32_t* pool_vn;     // validated-neuron count of a visited cell (-1: no face yet)
     int64_t* pool_voff;   // offset of its validated-neuron list
     double* pool_hint;    // [cap][4] a point on the cell's face polygon + search radius (inf: none)
@@ -385,6 +386,14 @@ struct FaceArgs {
     int64_t cap_val;
     int32_t* pool_vn;
     int64_t* pool_voff;
+    // deferral of cells whose polygon outgrows the near list's reach: instead of the slow
+    // streaming attempts, the cell is queued again with its hint radius widened (so the next
+    // near list covers it) and solved in a later iteration -- the visited set and every result
+    // are order independent.  Once per cell.  null queue: never defer.
+    int32_t* queue;
+    unsigned long long* q_tail;
+    uint32_t* pool_flags;
+    double* pool_hint;
     unsigned long long* dbg;   // instrumentation (AM_FACE_STATS builds), may be null
     unsigned long long* cursor;   // work-distribution counter (zeroed by k_take each iteration)
     // near lists (k_near -> k_face), per frontier entry: count, flags, ids and raw rows
@@ -403,6 +412,7 @@ struct FaceArgs {
     int32_t* near_id;         // [n_cap][near_cap]
     double* near_row;         // [n_cap][near_cap][4]
 };
+constexpr uint32_t kPoolDeferred = 4u, kPoolWasDeferred = 8u;
 constexpr int kEmitFlipsPerCell = 48;   // face kernel EMAXC
 constexpr int kVertsPerCell = 64;       // face kernel QMAX
 constexpr int kRefsPerCell = 256;
