@@ -622,6 +622,10 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->f_order.reserve(e->B, s));
     if (const char* v = getenv("AM_FACE_ORDER")) e->face_order = atoi(v) != 0;
     if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
+    // deferral re-composes the deferred cells: worth it where the face solve dominates (narrow
+    // nets; configs[1] 19.75 -> 18.85 ms), not where composition does (DeepSDF 512x8: 0.724 ->
+    // 0.747 s for the first 1 M cells)
+    e->defer = e->flops_per_cell < 2.0e6;
     if (const char* v = getenv("AM_DEFER")) e->defer = atoi(v) != 0;
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
