@@ -1186,8 +1186,9 @@ static int timed_iteration(am_engine* e) {
         unsigned long long dbg[64];
         CK(cudaMemcpy(dbg, e->dbg.p, sizeof dbg, cudaMemcpyDeviceToHost));
         fprintf(stderr, "iter %lld nR %.0f nF %.0f compose %.1f us face %.1f us probe-stage %.1f us | max cell %llu cyc, "
-                "full-path %llu streamed %llu\n", (long long)e->hctr[C_ITER], nR, nF, a * 1e3, b * 1e3, c * 1e3,
-                dbg[8], dbg[27], dbg[26]);
+                "full-path %llu streamed %llu | emit %llu prec %llu pend %llu\n", (long long)e->hctr[C_ITER], nR, nF,
+                a * 1e3, b * 1e3, c * 1e3, dbg[8], dbg[27], dbg[26], e->hctr[C_NEMIT], e->hctr[C_NPREC],
+                e->hctr[C_NPEND]);
         CK(cudaMemset(e->dbg.p + 8, 0, 8));
     }
     e->face_bytes += nF * (e->NB * 32.0 + e->M * 32.0 + e->KW * 8.0);
