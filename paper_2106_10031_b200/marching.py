@@ -236,7 +236,7 @@ class MarchResult:
         nv = self.nverts[self.nverts > 0].astype(np.int64)
         off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
         return PolygonMesh(self.verts.copy(), None, None, face_off=off, face_idx=np.arange(off[-1], dtype=np.int64),
-                           plane_rows=self._plane_source())
+                           plane_rows=self._plane_source(), _checked=True)
 
     def welded_mesh(self, tol: float = TOL_WELD):
         """reference marching.py:126-127 weld(polygon_soup(), tol), welded on the GPU straight
@@ -262,7 +262,7 @@ class MarchResult:
             kept_h, foff_h, fidx_h, fsrc_h, nd = weld_arrays(self.verts, off, np.arange(off[-1], dtype=np.int64), tol)
         src = self._plane_source()
         return PolygonMesh(kept_h, None, None, nd, face_off=foff_h, face_idx=fidx_h,
-                           plane_rows=None if src is None else select_rows(src, fsrc_h))
+                           plane_rows=None if src is None else select_rows(src, fsrc_h), _checked=True)
 
     def face_multiset(self, decimals: int = 10):
         """Order-independent fingerprint (reference marching.py:139-149)."""
