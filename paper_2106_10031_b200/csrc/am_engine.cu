@@ -142,6 +142,7 @@ struct am_engine {
     DBuf<double> pool_hint, ckey_hint, emit_hint, near_row;
     DBuf<int32_t> near_n, near_flags, near_id;   // k_near lists per frontier entry
     DBuf<int32_t> f_order;                        // face work order (heavy cells first)
+    int64_t defer_min = 0;      // AM_DEFER_MIN: smallest wave that defers
     bool defer = true;          // deferral of cells that outgrow their near list (AM_DEFER=0: stream them)
     bool canon_fused = true;    // k_canon_frontier (AM_CANON_FUSED=0: the three separate kernels)
     bool face_order = false;                      // AM_FACE_ORDER=1: heavy cells first (A/B: 20.15 vs 19.95 ms, off)
@@ -627,6 +628,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // 0.747 s for the first 1 M cells)
     e->defer = e->flops_per_cell < 2.0e6;
     if (const char* v = getenv("AM_DEFER")) e->defer = atoi(v) != 0;
+    if (const char* v = getenv("AM_DEFER_MIN")) e->defer_min = atoll(v);
     CK(e->near_flags.reserve(e->B, s));
     CK(e->near_id.reserve(e->B * e->near_cap, s));
     CK(e->near_row.reserve(e->B * e->near_cap * 4, s));
@@ -993,7 +995,7 @@ static int launch_iteration(am_engine* e) {
     a.cap_prec = e->PR;
     a.val_buf = e->val_buf.p; a.n_val = c + C_NVAL; a.cap_val = e->val_buf.n;
     a.pool_vn = e->pool_vn.p; a.pool_voff = e->pool_voff.p;
-    a.queue = e->defer ? e->queue.p : nullptr; a.q_tail = c + C_QTAIL;
+    a.queue = e->defer ? e->queue.p : nullptr; a.q_tail = c + C_QTAIL; a.defer_min = e->defer_min;
     a.pool_flags = e->pool_flags.p; a.pool_hint = e->pool_hint.p;
     a.dbg = e->dbg.p;
     a.cursor = c + C_FCURSOR;

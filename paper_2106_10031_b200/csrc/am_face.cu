@@ -489,7 +489,7 @@ __device__ __noinline__ FullOut full_path(FaceWarp* W, const Ctx& c, const doubl
     return FullOut{nv, cur, status, sc, tc, rho, nC, core, risky};
 }
 
-__device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
+__device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_wave) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int item = A.items[fi];
@@ -585,7 +585,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi) {
         n_attempts++;
         if (!(use_list && tau <= reach)) n_streamed++;
 #endif
-        if (attempt > 0 && use_list && !(tau <= reach) && A.queue) {
+        if (attempt > 0 && use_list && !(tau <= reach) && A.queue && n_wave >= A.defer_min) {
             // the polygon outgrew the near list: defer the cell (queued again with a hint radius
             // whose near list covers this reach) rather than stream every row in this iteration
             const int32_t pq = A.pool_idx[fi];
@@ -1394,7 +1394,7 @@ __global__ void __launch_bounds__(FW * 32, 4) k_face(FaceArgs A) {
         }
         fi = __shfl_sync(0xffffffffu, fi, 0);
         if (fi >= n) break;
-        face_cell(A, W, fi);
+        face_cell(A, W, fi, n);
         __syncwarp();
     }
 }

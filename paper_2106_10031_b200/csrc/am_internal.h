@@ -392,6 +392,8 @@ struct FaceArgs {
     // are order independent.  Once per cell.  null queue: never defer.
     int32_t* queue;
     unsigned long long* q_tail;
+    int64_t defer_min;        // defer only in waves of at least this many cells (a lone deferred cell
+                              // costs a whole extra iteration at the end of a march)
     uint32_t* pool_flags;
     double* pool_hint;
     unsigned long long* dbg;   // instrumentation (AM_FACE_STATS builds), may be null
