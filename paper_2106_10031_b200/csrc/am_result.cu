@@ -2,13 +2,16 @@
 //
 // The reference returns its polygons sorted by (state key bytes, branch) (marching.py:356-359);
 // packbits key bytes compare like the MSB-first key words, and the ensemble branch is the last
-// word, so the order is the word-lexicographic order of the KW-word keys.  It is produced by an
-// LSD radix sort: one stable (word, index) pair sort per word, last word first.  The cells' face
+// word, so the order is the word-lexicographic order of the KW-word keys.  It is produced by a
+// stable merge sort of the cell indices comparing the KW-word keys most significant word first
+// (keys resident in L2; most comparisons resolve in the first words), or with AM_RESULT_RADIX=1
+// by an LSD radix sort: one stable (word, index) pair sort per word, last word first.  The cells' face
 // loops (vertices, per-edge transition refs) are then gathered into that order as CSR, ready for
 // one device->host copy per array or for the GPU weld.
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "am_internal.h"
 
@@ -58,6 +61,27 @@ __global__ void k_sorted_refs(const int64_t* vsrc, const int64_t* s_enr, const i
     }
 }
 
+// word q of the sort order -> key word: a batch of shapes is ordered by shape first (its shape
+// word is the most significant), then like the reference
+__host__ __device__ __forceinline__ int order_word(int q, int shape_w) {
+    return shape_w < 0 ? q : (q == 0 ? shape_w : q - 1 + (q - 1 >= shape_w ? 1 : 0));
+}
+
+struct KeyLess {
+    const uint64_t* keys;
+    int KW, shape_w;
+    __device__ bool operator()(int32_t a, int32_t b) const {
+        const uint64_t* ka = keys + (int64_t)a * KW;
+        const uint64_t* kb = keys + (int64_t)b * KW;
+        for (int q = 0; q < KW; q++) {
+            const int w = order_word(q, shape_w);
+            const uint64_t x = __ldg(ka + w), y = __ldg(kb + w);
+            if (x != y) return x < y;
+        }
+        return false;
+    }
+};
+
 inline unsigned blocks(int64_t n) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
 }
@@ -94,8 +118,11 @@ int assemble_results(const uint64_t* keys, const int32_t* cell_nv, const int64_t
     RCK(ord_a.alloc(nc)); RCK(ord_b.alloc(nc)); RCK(w_a.alloc(nc)); RCK(w_b.alloc(nc));
     RCK(cnt.alloc(nc + 1)); RCK(svoff.alloc(nc + 1)); RCK(senr.alloc(nvt + 1)); RCK(sroff.alloc(nvt + 1));
     RCK(vsrc.alloc(nvt));
+    static const bool radix = [] { const char* v = getenv("AM_RESULT_RADIX"); return v && atoi(v) != 0; }();
+    const KeyLess less{keys, KW, shape_w};
     size_t tb = 0, t2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, w_a.p, w_b.p, ord_a.p, ord_b.p, (int)nc, 0, 64, s);
+    if (radix) cub::DeviceRadixSort::SortPairs(nullptr, tb, w_a.p, w_b.p, ord_a.p, ord_b.p, (int)nc, 0, 64, s);
+    else cub::DeviceMergeSort::StableSortKeys(nullptr, tb, ord_a.p, (int)nc, less, s);
     cub::DeviceScan::ExclusiveSum(nullptr, t2, cnt.p, svoff.p, nc + 1, s);
     tb = std::max(tb, t2);
     cub::DeviceScan::ExclusiveSum(nullptr, t2, senr.p, sroff.p, nvt + 1, s);
@@ -104,14 +131,17 @@ int assemble_results(const uint64_t* keys, const int32_t* cell_nv, const int64_t
     RCK(tmp.alloc((int64_t)tb));
     const unsigned G = blocks(nc);
     k_iota<<<G, 256, 0, s>>>(ord_a.p, nc);
-    // LSD: a stable sort by each word, least significant first; a batch of shapes is ordered by
-    // shape first (its shape word is the most significant), then like the reference
-    for (int q = KW - 1; q >= 0; q--) {
-        const int w = shape_w < 0 ? q : (q == 0 ? shape_w : q - 1 + (q - 1 >= shape_w ? 1 : 0));
-        k_key_word<<<G, 256, 0, s>>>(keys, ord_a.p, nc, KW, w, w_a.p);
+    if (radix) {
+        // LSD: a stable sort by each word, least significant first
+        for (int q = KW - 1; q >= 0; q--) {
+            k_key_word<<<G, 256, 0, s>>>(keys, ord_a.p, nc, KW, order_word(q, shape_w), w_a.p);
+            size_t t = tb;
+            RCK(cub::DeviceRadixSort::SortPairs(tmp.p, t, w_a.p, w_b.p, ord_a.p, ord_b.p, (int)nc, 0, 64, s));
+            std::swap(ord_a.p, ord_b.p);
+        }
+    } else {
         size_t t = tb;
-        RCK(cub::DeviceRadixSort::SortPairs(tmp.p, t, w_a.p, w_b.p, ord_a.p, ord_b.p, (int)nc, 0, 64, s));
-        std::swap(ord_a.p, ord_b.p);
+        RCK(cub::DeviceMergeSort::StableSortKeys(tmp.p, t, ord_a.p, (int)nc, less, s));
     }
     k_sorted_cells<<<G, 256, 0, s>>>(keys, ord_a.p, cell_nv, nc, KW, s_keys, s_nv, cnt.p);
     RCK(cudaMemsetAsync(cnt.p + nc, 0, 8, s));

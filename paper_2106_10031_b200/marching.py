@@ -182,6 +182,9 @@ class MarchResult:
     # sending the soup back to the GPU (None: host arrays only)
     _dev: tuple | None = field(default=None, repr=False)
     _planes: np.ndarray | None = field(default=None, repr=False)
+    # (tol, future) of the weld march() started on a side stream while the soup was copied to the
+    # host (welded_mesh(tol) with the same tolerance takes its result)
+    _weld: tuple | None = field(default=None, repr=False)
 
     @property
     def has_face(self) -> np.ndarray:
@@ -243,19 +246,13 @@ class MarchResult:
         from the CSR soup (no per-loop Python objects on the way in).  A result of march() still
         holds its soup in HBM: the loops are formed and welded there and only the welded mesh
         comes back."""
-        from .meshes import PolygonMesh, weld_arrays, weld_device, to_host, select_rows
+        from .meshes import PolygonMesh, weld_arrays, select_rows
         if tol < 0:
             raise ValueError("weld tolerance must be >= 0")
-        if self._dev is not None:
-            import torch
-            dn, dv = self._dev
-            nv = dn[dn > 0].to(torch.int64)
-            off = torch.zeros(nv.numel() + 1, dtype=torch.int64, device=dv.device)
-            torch.cumsum(nv, 0, out=off[1:])
-            idx = torch.arange(dv.shape[0], dtype=torch.int64, device=dv.device)
-            kept, foff, fidx, fsrc, _, nd = weld_device(dv, off, idx, tol)
-            kept_h, foff_h, fsrc_h = to_host([kept, foff, fsrc])
-            (fidx_h,) = to_host([fidx[:int(foff_h[-1])]])
+        if self._weld is not None and self._weld[0] == tol:
+            kept_h, foff_h, fidx_h, fsrc_h, nd = self._weld[1].result()
+        elif self._dev is not None:
+            kept_h, foff_h, fidx_h, fsrc_h, nd = _weld_soup_device(*self._dev, tol)
         else:
             nv = self.nverts[self.nverts > 0].astype(np.int64)
             off = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
@@ -272,6 +269,56 @@ class MarchResult:
             out.append((poly.state.key, poly.state.branch, vs))
         out.sort(key=lambda t: (t[0], -1 if t[1] is None else t[1], sorted(t[2])))
         return out
+
+
+def _weld_soup_device(dn, dv, tol: float, after=None):
+    """Weld the device-resident soup (sorted per-cell vertex counts dn, vertices dv) on the GPU
+    and copy the welded mesh to the host: (kept, face_off, face_idx, face_src, n_dropped).  With
+    ``after`` (a stream) the work runs on a side stream ordered after it."""
+    import torch
+    from .meshes import weld_device
+    dev = dv.device
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev)
+        if after is not None:
+            st = _side_stream(dev)
+            st.wait_stream(after)
+        with torch.cuda.stream(st):
+            nv = dn[dn > 0].to(torch.int64)
+            off = torch.zeros(nv.numel() + 1, dtype=torch.int64, device=dev)
+            torch.cumsum(nv, 0, out=off[1:])
+            idx = torch.arange(dv.shape[0], dtype=torch.int64, device=dev)
+            kept, foff, fidx, fsrc, _, nd = weld_device(dv, off, idx, tol, stream=st)
+            kept_h, foff_h, fsrc_h = to_host([kept, foff, fsrc])
+            (fidx_h,) = to_host([fidx[:int(foff_h[-1])]])
+    return kept_h, foff_h, fidx_h, fsrc_h, nd
+
+
+_SIDE: dict = {}
+_WELD_POOL = None
+
+
+def _side_stream(dev):
+    import torch
+    st = _SIDE.get(dev.index)
+    if st is None:
+        st = _SIDE[dev.index] = torch.cuda.Stream(device=dev)
+    return st
+
+
+def _start_weld(dn, dv, tol: float):
+    """Start the default-tolerance weld of a march's soup on a side stream from a worker thread,
+    so that it overlaps the soup's device->host copies (AM_WELD_PREFETCH=0 disables)."""
+    import os
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    global _WELD_POOL
+    if os.environ.get("AM_WELD_PREFETCH", "1") == "0":
+        return None
+    if _WELD_POOL is None:
+        _WELD_POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="am-weld")
+    main = torch.cuda.current_stream(dv.device)
+    return (tol, _WELD_POOL.submit(_weld_soup_device, dn, dv, tol, main))
 
 
 def neighbor_state(s: StateVector, ref: PlaneRef) -> StateVector:
@@ -336,13 +383,15 @@ def refs_to_kind_index(ids: np.ndarray, n_bits: int, n_subs: int) -> np.ndarray:
     return out
 
 
-def device_results_to_host(eng: Engine):
+def device_results_to_host(eng: Engine, on_device=None):
     """Sorted device results in the reference's representations, converted on the GPU and copied
     once into pinned host memory: (counts, packbits keys (C, nbytes) uint8, branch (C,), extra
     key word (C,) or None, nverts, verts, edge_nrefs, edge_refs (R, 2) (kind, index))."""
     import torch
     c, keys, nverts, verts, enr, erefs = eng.results_device()
     eng.last_results_device = (c, keys, nverts, verts, enr, erefs)
+    if on_device is not None:
+        on_device(nverts, verts)
     b = eng.blob
     nb, ns = b.n_bits, b.n_subs
     bw, nbytes = (nb + 63) // 64, (nb + 7) // 8
@@ -367,16 +416,18 @@ def collect_result(eng: Engine, seeds: np.ndarray, t0: float, waves: int, thread
                    keep_device: bool = False, net=None) -> MarchResult:
     """Sorted results (GPU sort + gathers, am_result_copy_device), converted to the reference's
     representations on the device, one pinned copy per array."""
-    c, kb, branch, _, hn, hv, he, hr = device_results_to_host(eng)
-    dev = None
+    dev = weld = None
     if keep_device:
-        _, _, dn, dv, _, _ = eng.last_results_device
-        dev = (dn, dv)
+        def on_device(dn, dv):
+            nonlocal dev, weld
+            dev = (dn, dv)
+            weld = _start_weld(dn, dv, TOL_WELD)
+    c, kb, branch, _, hn, hv, he, hr = device_results_to_host(eng, on_device if keep_device else None)
     rep = MarchReport(cells_visited=c["cells"], faces_emitted=c["faces"], empty_faces=c["empty"],
                       open_edges=c["open_edges"], seconds=time.perf_counter() - t0, seeds_used=len(seeds),
                       capped=bool(c["capped"]), threads=threads, waves=waves, overflow=c["overflow"])
     return MarchResult(kb, branch, hn, hv, he, hr, rep, eng.blob.n_bits, seeds, net=net if net is not None else eng.net,
-                       _dev=dev)
+                       _dev=dev, _weld=weld)
 
 
 _ENGINES: "OrderedDict[tuple, Engine]" = OrderedDict()
