@@ -216,8 +216,10 @@ int am_unique_planes(const double *d_planes, int64_t m, double tol, int32_t *d_p
 
 /* --- profiling hooks (bench.py roofline) --------------------------------- */
 /* cumulative device time (ms) of the compose (DMMA) kernels, of the face
- * kernel, and the algorithmic flop / byte counts they processed */
-int am_stats(am_engine *e, double *h_out16);
+ * kernel, and the algorithmic flop / byte counts they processed; h_out[16] = composition
+ * flops taken from parents' rows instead of executed (prefix reuse), h_out[17] = 1 when prefix
+ * reuse is on (18 doubles) */
+int am_stats(am_engine *e, double *h_out18);
 int am_set_timing(am_engine *e, int enabled);
 /* timing mode: per-stage device time (ms) of the timed iterations, the stages contiguous so they
  * sum to the iterations' device time: h_out16[0..8] take, compose, canonical insert, frontier,

@@ -161,6 +161,13 @@ struct am_engine {
     DBuf<double> Z2, faces2;
     DBuf<uint64_t> ckey2;
     DBuf<int32_t> changed2;
+    // prefix reuse of the narrow composition (AM_PREFIX=0: off): the iterations' Z rows in two
+    // halves by iteration parity, each pool entry's / emitted flip's parent word, and the batch
+    // listed per shared-step bucket
+    bool prefix = false;
+    DBuf<double> Zi;
+    DBuf<int64_t> pool_par, emit_par;
+    DBuf<int32_t> blist;
     std::unique_ptr<NarrowCompose> ncomp{new NarrowCompose()};   // face-solver reach (tuning: AM_TAU_MULT, AM_NEAR_REACH)
     DBuf<unsigned long long> dbg;   // face-kernel instrumentation counters (AM_FACE_STATS builds)
     uint64_t tcap = 0;
@@ -274,6 +281,7 @@ static HashSet hs(am_engine* e) {
     H.pool_vn = e->pool_vn.p;
     H.pool_voff = e->pool_voff.p;
     H.pool_hint = e->pool_hint.p;
+    H.pool_par = e->prefix ? e->pool_par.p : nullptr;
     H.n_pool = e->ctr.p + C_POOL;
     H.cap_pool = e->pool.n / e->KW;
     H.KW = e->KW;
@@ -293,6 +301,7 @@ static int ensure_hash(am_engine* e, int64_t extra, bool sync = true) {
         CK(e->pool_vn.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
         CK(e->pool_voff.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
         CK(e->pool_hint.reserve(e->pool.n / e->KW * 4, e->stream, true, np * 4, &moved));
+        if (e->prefix) CK(e->pool_par.reserve(e->pool.n / e->KW, e->stream, true, np, &moved));
     }
     // a cell is queued once, plus at most once more when deferred (face solver, status 3)
     CK(e->queue.reserve(2 * (e->pool.n / e->KW), e->stream, true, (int64_t)e->hctr[C_QTAIL], &moved));
@@ -619,6 +628,14 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
         CK(e->Z2.reserve(e->Z.n, s)); CK(e->faces2.reserve(e->faces.n, s));
         CK(e->ckey2.reserve(e->ckey.n, s)); CK(e->changed2.reserve(e->changed.n, s));
     }
+    e->prefix = e->narrow_fused && !e->narrow_check && e->ncomp->nsteps <= kMaxPrefixBuckets &&
+                e->B < (INT64_C(1) << 27);
+    if (const char* v = getenv("AM_PREFIX")) e->prefix = e->prefix && atoi(v) != 0;
+    if (e->prefix) {
+        CK(e->Zi.reserve(2 * e->B * e->zs * 4, s));
+        CK(e->emit_par.reserve(e->E, s));
+        CK(e->blist.reserve(kMaxPrefixBuckets * e->B, s));
+    }
     CK(e->near_n.reserve(e->B, s));
     CK(e->f_order.reserve(e->B, s));
     if (const char* v = getenv("AM_FACE_ORDER")) e->face_order = atoi(v) != 0;
@@ -671,7 +688,8 @@ extern "C" int am_engine_destroy(am_engine* e) {
     if (e->graph) cudaGraphDestroy(e->graph);
     DBuf<double>* dbl[] = {&e->params, &e->wpad, &e->Z, &e->faces, &e->probe_pts, &e->pZ, &e->verts, &e->sx, &e->shint,
                            &e->sxp, &e->pvals, &e->prec_pt, &e->pend_pt[0], &e->pend_pt[1], &e->pool_hint,
-                           &e->ckey_hint, &e->emit_hint, &e->s_verts, &e->shape_tab, &e->near_row};
+                           &e->ckey_hint, &e->emit_hint, &e->s_verts, &e->shape_tab, &e->near_row, &e->Zi,
+                           &e->Z2, &e->faces2};
     for (auto* b : dbl) b->release(e->stream);
     DBuf<uint64_t>* u64[] = {&e->table, &e->pool, &e->ckey, &e->slot, &e->slot2, &e->scratch, &e->outbox,
                              &e->hkeys, &e->hslot, &e->ss, &e->ssn, &e->sres, &e->pkeys, &e->pslot, &e->s_keys};
@@ -687,6 +705,11 @@ extern "C" int am_engine_destroy(am_engine* e) {
     for (auto* b : i32) b->release(e->stream);
     e->pool_flags.release(e->stream);
     e->pool_voff.release(e->stream);
+    e->pool_par.release(e->stream);
+    e->emit_par.release(e->stream);
+    e->blist.release(e->stream);
+    e->ckey2.release(e->stream);
+    e->changed2.release(e->stream);
     e->cell_voff.release(e->stream);
     e->edge_roff.release(e->stream);
     e->subdev.release(e->stream);
@@ -916,6 +939,9 @@ static int launch_iteration(am_engine* e) {
     I.cap_pend = e->pend_t[0].n; I.cap_val = e->val_buf.n;
     I.emit_per_cell = emit_per_cell(); I.verts_per_cell = kVertsPerCell; I.refs_per_cell = kRefsPerCell;
     I.world = e->P.world;
+    I.pool_par = e->prefix ? e->pool_par.p : nullptr;
+    I.blist = e->blist.p;
+    I.max_share = e->ncomp->nsteps - 1;
     ProbeRecs R;
     R.cand = e->prec_cand.p; R.k = e->prec_k.p; R.pt = e->prec_pt.p;
     for (int q = 0; q < 2; q++) { R.pend_t[q] = e->pend_t[q].p; R.pend_k[q] = e->pend_k[q].p; R.pend_pt[q] = e->pend_pt[q].p; }
@@ -938,7 +964,8 @@ static int launch_iteration(am_engine* e) {
         N.subs = reinterpret_cast<const SubDev*>(e->subdev.p);
         N.pool = e->pool.p; N.pool_hint = e->pool_hint.p; N.queue = e->queue.p; N.ctr = c;
         N.batch_pool = e->batch_pool.p; N.canon_pos = e->canon_pos.p; N.ckey_hint = e->ckey_hint.p;
-        N.Z = e->Z.p; N.keys = e->ckey.p; N.faces = e->faces.p; N.changed = e->changed.p;
+        N.Z = e->prefix ? e->Zi.p : e->Z.p; N.keys = e->ckey.p; N.faces = e->faces.p; N.changed = e->changed.p;
+        N.prefix = e->prefix; N.zstride = e->B * e->zs * 4; N.pool_par = e->pool_par.p; N.blist = e->blist.p;
         N.n_dev = c + C_NR; N.n_cap = B; N.KW = e->KW; N.zs = e->zs; N.shape_w = e->shape_w; N.fp32 = e->fp32;
         N.prof = e->dbg.p + 32;
         launch_compose_narrow(N, s);
@@ -1004,6 +1031,13 @@ static int launch_iteration(am_engine* e) {
     a.order = e->face_order ? e->f_order.p : nullptr; a.order_ctr = c + C_NHEAVY;
     a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
     a.tau_grow = e->tau_grow;
+    a.zpar = nullptr; a.zstride = 0; a.emit_par = nullptr; a.nsteps = 0;
+    if (e->prefix) {
+        a.Z = e->Zi.p;
+        a.zpar = c + C_ITER; a.zstride = e->B * e->zs * 4; a.emit_par = e->emit_par.p;
+        a.nsteps = e->ncomp->nsteps;
+        for (int q = 0; q < a.nsteps; q++) a.step_end[q] = e->sdev[q].row_off + e->sdev[q].n_out;
+    }
     if (tm) cudaEventRecord(e->ev[2], s);
     mark(4);
     launch_near(a, s);
@@ -1015,9 +1049,9 @@ static int launch_iteration(am_engine* e) {
     if (multi) {
         launch_route_emitted(e->scratch.p, c + C_NEMIT, e->E, e->KW, e->P.rank, e->P.world, e->local_idx.p,
                              c + C_NLOCAL, e->outbox.p, c + C_NOUT, e->status.p, s);
-        launch_hash_upsert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
+        launch_hash_upsert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s, a.emit_par);
     } else {
-        launch_hash_upsert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s);
+        launch_hash_upsert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s, a.emit_par);
     }
     mark(7);
     // probe records (this iteration's and the pending ones): drop / forward / keep pending
@@ -1756,5 +1790,13 @@ extern "C" int am_stats(am_engine* e, double* h) {
     h[8] = (double)g_launch_count; h[9] = (double)e->iters; h[10] = e->t_probe; h[11] = e->pflops;
     h[12] = e->n_probes; h[13] = e->flops_per_point;
     h[14] = (double)e->hctr[C_PROBES_TOTAL]; h[15] = (double)e->hctr[C_PREC_TOTAL];
+    // prefix reuse: composition flops not executed (cells x the DMMA steps taken from parents)
+    double skipped = 0, step_flops = 0;
+    if (e->prefix)
+        for (int f = 1; f < e->ncomp->nsteps; f++) {
+            step_flops += 2.0 * e->sdev[f].n_out * e->sdev[f].n_in * 4;
+            skipped += (double)e->hctr[C_BKT0 + f] * step_flops;
+        }
+    h[16] = skipped; h[17] = e->prefix ? 1.0 : 0.0;
     return AM_OK;
 }

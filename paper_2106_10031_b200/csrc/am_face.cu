@@ -123,6 +123,11 @@ struct Ctx {
     double lo[3], hi[3];
 };
 
+// this iteration's half of the (prefix-reuse double-buffered) composition rows
+__device__ __forceinline__ const double* zbase(const FaceArgs& A) {
+    return A.zpar ? A.Z + (int64_t)(*A.zpar & 1ull) * A.zstride : A.Z;
+}
+
 // unit oriented constraint row of global plane id gr (reference cells.py:127-185); false if dropped.
 // *nrm receives the raw normal norm (neuron / branch rows) or 1 (box rows)
 __device__ __noinline__ bool get_row(const Ctx& c, int gr, double n[3], double& o, double* nrm_out = nullptr) {
@@ -501,7 +506,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
     (void)0;
 
     Ctx c;
-    c.Z = A.Z + (int64_t)item * A.zs * 4;
+    c.Z = zbase(A) + (int64_t)item * A.zs * 4;
     c.faces = A.faces + (int64_t)item * A.M * 4;
     c.key = A.keys + (int64_t)item * A.KW;
     if (A.KW <= KWF) {   // stage the key: one coalesced load instead of a dependent round trip per lookup
@@ -1234,12 +1239,13 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
         const int si = pos / (nbr + 1), ti = pos % (nbr + 1) - 1;
         const unsigned sub = nb == 3 ? kComb3[si] : (unsigned)si;   // combination order for nb <= 3
         uint64_t word = c.key[w];
-        int branch = -1, in_ = 0, ib = 0;
+        int branch = -1, in_ = 0, ib = 0, gmin = NBl;
         auto visit = [&](int gid) {
             if (gid >= box0) return;
             if (gid < NBl) {
                 const bool fl = big ? (si < nb ? in_ == si : si == nb) : ((sub >> in_) & 1u);
                 if (fl && (gid >> 6) == w) word ^= key_mask(gid);
+                if (fl && gid < gmin) gmin = gid;
                 in_++;
             } else {
                 if (ib == ti) branch = gid - NBl;
@@ -1265,6 +1271,15 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
             const double* q = W->u.pp.fv[e + 1 == nr ? 0 : e + 1];
             reinterpret_cast<double4*>(A.emit_hint)[ci] =
                 make_double4(0.5 * (p[0] + q[0]), 0.5 * (p[1] + q[1]), 0.5 * (p[2] + q[2]), 2.0 * W->diam + 1e-9);
+            if (A.emit_par) {
+                // prefix reuse: the child shares Z rows of steps 0..f with this cell (f: step of
+                // its first flipped neuron; a branch-only change shares nothing)
+                int f = 0;
+                if (gmin < NBl && branch < 0) {
+                    while (f + 1 < A.nsteps && A.step_end[f] <= gmin) f++;
+                }
+                A.emit_par[ci] = f ? prefix_word(*A.zpar, item, f) : 0;
+            }
         }
     }
     PMARK(12);
@@ -1291,7 +1306,7 @@ __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
     for (int64_t fi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; fi < n; fi += nw) {
         const int item = A.items[fi];
         Ctx c;
-        c.Z = A.Z + (int64_t)item * A.zs * 4;
+        c.Z = zbase(A) + (int64_t)item * A.zs * 4;
         c.faces = A.faces + (int64_t)item * A.M * 4;
         c.key = A.keys + (int64_t)item * A.KW;
         c.NB = A.NB; c.M = A.M; c.ensemble = A.ensemble;

@@ -38,7 +38,7 @@ __device__ __forceinline__ bool keys_equal(const uint64_t* a, const uint64_t* b,
 __device__ __forceinline__ int32_t upsert_one(const HashSet& H, const uint64_t* src, const int32_t* idx, int64_t i,
                                               int64_t ci, uint64_t* slot_out, int32_t* dup_ref, uint32_t flag,
                                               int32_t* queue, unsigned long long* q_tail, const double* src_hint,
-                                              int32_t* pidx) {
+                                              int32_t* pidx, const int64_t* src_par = nullptr) {
     const uint64_t* key = src + ci * H.KW;
     uint64_t h = key_hash(key, H.KW);
     uint64_t fp = h >> 33;
@@ -81,6 +81,7 @@ __device__ __forceinline__ int32_t upsert_one(const HashSet& H, const uint64_t* 
     const double4 hint = src_hint ? reinterpret_cast<const double4*>(src_hint)[ci]
                                   : make_double4(0.0, 0.0, 0.0, __longlong_as_double(0x7ff0000000000000ll));
     reinterpret_cast<double4*>(H.pool_hint)[p] = hint;
+    if (H.pool_par) H.pool_par[p] = src_par ? src_par[ci] : 0;
     __threadfence();
     H.table[pos] = (fp << 33) | (uint64_t)(uint32_t)p;
     *pidx = (int32_t)p;
@@ -90,13 +91,14 @@ __device__ __forceinline__ int32_t upsert_one(const HashSet& H, const uint64_t* 
 
 __global__ void k_hash_upsert(HashSet H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                               int64_t n_cap, int32_t* status, uint64_t* slot_out, int32_t* dup_ref, uint32_t flag,
-                              int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint) {
+                              int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint,
+                              const int64_t* src_par) {
     pdl_enter();
     const int64_t n = dev_count(n_dev, n_cap);
     GRID_STRIDE(i, n) {
         const int64_t ci = idx ? idx[i] : i;
         int32_t p;
-        status[ci] = upsert_one(H, src, idx, i, ci, slot_out, dup_ref, flag, queue, q_tail, src_hint, &p);
+        status[ci] = upsert_one(H, src, idx, i, ci, slot_out, dup_ref, flag, queue, q_tail, src_hint, &p, src_par);
         if (pool_idx) pool_idx[ci] = p;
     }
 }
@@ -135,10 +137,10 @@ static unsigned grid_for(int64_t n, int b) {
 void launch_hash_upsert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                         int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, uint32_t flag,
                         int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint,
-                        cudaStream_t s) {
+                        cudaStream_t s, const int64_t* src_par) {
     if (n_cap > 0) {
         launch_k(k_hash_upsert, grid_for(n_cap, 256), 256, 0, s, H, src, idx, n_dev, n_cap, status, slot, dup_ref, flag,
-                 pool_idx, queue, q_tail, src_hint);
+                 pool_idx, queue, q_tail, src_hint, src_par);
     }
 }
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
@@ -151,7 +153,12 @@ void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
 __global__ void k_take(IterState I) {
     pdl_enter();
     unsigned long long* c = I.ctr;
+    __shared__ long long s_head, s_n;
+    __shared__ unsigned long long s_iter;
+    __shared__ unsigned s_cnt[kMaxPrefixBuckets];
+    if (threadIdx.x < kMaxPrefixBuckets) s_cnt[threadIdx.x] = 0u;
     if (threadIdx.x == 0) {
+        s_head = (long long)c[C_QHEAD];
         long long head = (long long)c[C_QHEAD], tail = (long long)c[C_QTAIL];
         long long want = tail - head;
         if (want > I.B) want = I.B;
@@ -188,6 +195,29 @@ __global__ void k_take(IterState I) {
         c[C_ITER] += nR > 0 ? 1ull : 0ull;
         // the batch is queue[head, head + nR): k_gather_batch copies it out (batch_pool)
         c[C_QHEAD] = (unsigned long long)((long long)c[C_QHEAD] + nR);
+        s_n = nR;
+        s_iter = c[C_ITER];
+    }
+    if (!I.pool_par) return;
+    // prefix reuse: bucket the batch by the number of composition steps its cells can take from
+    // their parents (emitted in the previous iteration; anything else composes in full)
+    __syncthreads();
+    const long long n = s_n, head = s_head;
+    const unsigned long long it = s_iter;
+    for (long long b = threadIdx.x; b < n; b += blockDim.x) {
+        const long long w = I.pool_par[I.queue[head + b]];
+        int f = 0;
+        if (w != 0 && ((unsigned long long)w >> 32) + 1ull == it) {
+            f = (int)(w & 31);
+            if (f > I.max_share) f = I.max_share;
+        }
+        const unsigned pos = atomicAdd(&s_cnt[f], 1u);
+        I.blist[(long long)f * I.B + pos] = (int32_t)b;
+    }
+    __syncthreads();
+    if (threadIdx.x < kMaxPrefixBuckets) {
+        c[C_BK0 + threadIdx.x] = s_cnt[threadIdx.x];
+        c[C_BKT0 + threadIdx.x] += s_cnt[threadIdx.x];
     }
 }
 
@@ -366,7 +396,7 @@ __global__ void k_route_emitted(const uint64_t* scratch, const unsigned long lon
     }
 }
 
-void launch_take(const IterState& I, cudaStream_t s) { launch_k(k_take, 1, 32, 0, s, I); }
+void launch_take(const IterState& I, cudaStream_t s) { launch_k(k_take, 1, I.pool_par ? 1024 : 32, 0, s, I); }
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                          const unsigned long long* ctr, int32_t* batch_pool, int64_t n_cap, int KW, uint64_t* ckey,
                          double* ckey_hint, int32_t* changed, int32_t* canon_pos, cudaStream_t s) {

@@ -208,6 +208,13 @@ struct NarrowCompose {
                                        // n >= grid * thr4, else 2 (AM_NARROW_THR8 / AM_NARROW_THR4)
     int tile_cells;                    // > 0: fixed tile width (AM_NARROW_TILE)
     unsigned long long* prof;          // [8] phase cycles of thread 0 of every CTA (dbg & 8)
+    // prefix reuse (prefix != 0): Z is double-buffered by iteration parity (zstride doubles per
+    // half), tiles are formed per bucket of blist (IterState), parents' rows read from the
+    // other half
+    int prefix;
+    int64_t zstride;
+    const int64_t* pool_par;
+    const int32_t* blist;
 };
 // sharded march exchange (am_shard.cu)
 constexpr int kHdrWords = 8;
@@ -245,8 +252,21 @@ enum Ctr {
     C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_OVF0, C_OVF1, C_CAPPED, C_TOTAL, C_QHEAD, C_QTAIL, C_NR, C_NX,
     C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_NPREC, C_NPEND, C_PPAR,
     C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_NFLUSH, C_DONE, C_NHEAVY, C_NLIGHT,
-    C_N
+    C_BK0,               // [kMaxPrefixBuckets] cells of this iteration's batch per shared-step count
+    C_BKT0 = C_BK0 + 12, // [kMaxPrefixBuckets] the same, summed over the march's iterations
+    C_N = C_BKT0 + 12
 };
+constexpr int kMaxPrefixBuckets = 12;
+
+// Prefix reuse of the narrow composition.  A cell emitted by the face stage differs from its
+// parent only in the flipped neuron(s): with the first flip in step f, Z rows of steps 0..f are
+// the parent's (they depend on the state bits of earlier layers only).  A child composed in the
+// iteration right after its parent's copies those rows from the parent's slot of the other
+// half of the double-buffered Z and runs the DMMA chain from step f + 1.
+//   pool_par / emit_par word: iteration (bits 32..63) | parent batch item (5..31) | f (0..4)
+__host__ __device__ __forceinline__ long long prefix_word(unsigned long long iter, long long item, int f) {
+    return (long long)((iter << 32) | ((unsigned long long)item << 5) | (unsigned long long)f);
+}
 
 // hash set (am_hash.cu)
 struct HashSet {
@@ -258,6 +278,7 @@ struct HashSet {
     int32_t* pool_vn;     // validated-neuron count of a visited cell (-1: no face yet)
     int64_t* pool_voff;   // offset of its validated-neuron list
     double* pool_hint;    // [cap][4] a point on the cell's face polygon + search radius (inf: none)
+    int64_t* pool_par;    // [cap] prefix_word of the emitting parent (0: none); null: not kept
     unsigned long long* n_pool;  // device counter
     int64_t cap_pool;
     int KW;
@@ -267,7 +288,7 @@ struct HashSet {
 void launch_hash_upsert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,
                         int64_t n_cap, int32_t* status, uint64_t* slot, int32_t* dup_ref, uint32_t flag,
                         int32_t* pool_idx, int32_t* queue, unsigned long long* q_tail, const double* src_hint,
-                        cudaStream_t s);
+                        cudaStream_t s, const int64_t* src_par = nullptr);
 void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s);
 
 // per-iteration guard / queue state (am_hash.cu k_take)
@@ -278,6 +299,11 @@ struct IterState {
     long long B, cap_pool, tcap, cap_cells, cap_verts, cap_refs, cap_outbox, cap_pend, cap_val;
     long long emit_per_cell, verts_per_cell, refs_per_cell;
     int world;
+    // prefix reuse (null pool_par: off): the batch's cells are listed per shared-step count
+    // (blist[f * B + i], counts in ctr[C_BK0 + f]) for the narrow composition's tiles
+    const int64_t* pool_par;
+    int32_t* blist;
+    int max_share;            // largest usable f (nsteps - 1)
 };
 // probe records: (target pool entry, neuron, point); double-buffered by parity counter
 struct ProbeRecs {
@@ -413,6 +439,13 @@ struct FaceArgs {
     unsigned long long* order_ctr;   // [0] heavy cells placed from the front, [1] light from the back
     int32_t* near_id;         // [n_cap][near_cap]
     double* near_row;         // [n_cap][near_cap][4]
+    // prefix reuse: Z half of this iteration (parity of *zpar), and every emitted flip's
+    // prefix_word (first flipped step: step_end[f] > its row) -- null zpar / emit_par: off
+    const unsigned long long* zpar;
+    int64_t zstride;
+    int64_t* emit_par;
+    int nsteps;
+    int step_end[12];
 };
 constexpr uint32_t kPoolDeferred = 4u, kPoolWasDeferred = 8u;
 constexpr int kEmitFlipsPerCell = 48;   // face kernel EMAXC

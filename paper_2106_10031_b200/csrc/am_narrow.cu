@@ -66,6 +66,38 @@ struct __align__(1024) NarrowSmem {
     uint32_t deg1[NR / 32];       // step-0 rows with a degenerate (zero) normal
     uint64_t full[NSB], empty[NSB];
     int changed[NCELL];
+    int32_t bidx[NCELL];          // batch item of each tile cell
+    int32_t pitem[NCELL];         // prefix reuse: the parent's batch item (previous iteration)
+};
+
+// Tiles of an iteration.  Without prefix reuse: consecutive batch items.  With it: per bucket f
+// (cells sharing steps 0..f with their parents, ascending f), each bucket cut into tiles of nc
+// cells of blist.  Producer and consumers derive the same (f, cells) from the bucket counts.
+struct Tiling {
+    int nb;                        // buckets (1 without prefix reuse)
+    long long cnt[kMaxPrefixBuckets];
+    long long ntiles;
+    __device__ void init(const NarrowCompose& P, int64_t n, int nc) {
+        if (!P.prefix) { nb = 1; cnt[0] = n; ntiles = (n + nc - 1) / nc; return; }
+        nb = P.nsteps < kMaxPrefixBuckets ? P.nsteps : kMaxPrefixBuckets;
+        ntiles = 0;
+        for (int f = 0; f < nb; f++) {
+            cnt[f] = (long long)P.ctr[C_BK0 + f];
+            ntiles += (cnt[f] + nc - 1) / nc;
+        }
+    }
+    // tile t -> (bucket f, first position in the bucket, cells)
+    __device__ void locate(long long t, int nc, int& f, long long& pos, int& ncell) const {
+        f = 0;
+        for (; f < nb - 1; f++) {
+            const long long tf = (cnt[f] + nc - 1) / nc;
+            if (t < tf) break;
+            t -= tf;
+        }
+        pos = t * nc;
+        const long long left = cnt[f] - pos;
+        ncell = (int)(left < nc ? left : nc);
+    }
 };
 
 __device__ __forceinline__ int skey_bit(const uint64_t* k, int i) {
@@ -102,13 +134,16 @@ __device__ __forceinline__ bool fabs_gt(double x, double t) {
 //   MI 1, NJ 1: 6 x 1 warps of 16 x 8,  2 cells (narrow waves: spread over more SMs)
 template <int FP32, int MI, int NJ>
 __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, int64_t n, int64_t head0,
-                                        uint32_t& gbox, bool prof, unsigned long long& tprev) {
+                                        uint32_t& gbox, bool prof, unsigned long long& tprev, double* Zc,
+                                        const double* Zp) {
     constexpr int WR = MI == 2 ? 3 : 6, WC = NCW / WR, RB = 16 * MI, CB = 8 * NJ;
     constexpr int NC = WC * NJ * 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ns = P.nsteps;
     const int KW = P.KW;
-    const int64_t ntiles = (n + NC - 1) / NC;
+    Tiling T;
+    T.init(P, n, NC);
+    const int64_t ntiles = T.ntiles;
     const int g = lane >> 2, tq = lane & 3;
     const int wm = warp % WR, wn = warp / WR;
     const int pg = ((g & 3) << 1) | (g >> 2);   // fragment row permutation (bank-conflict-free W reads)
@@ -117,19 +152,23 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
 #define PROF(i) do { if (prof) { unsigned long long tn = clock64(); atomicAdd(&P.prof[i], tn - tprev); tprev = tn; } } while (0)
 
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t item0 = t * NC;
-        const int ncell = (int)(n - item0 < NC ? n - item0 : NC);
+        int fsh, ncell;
+        long long pos0;
+        T.locate(t, NC, fsh, pos0, ncell);
         // ---- gather (reference order: the BFS queue slice k_take dequeued)
         for (int q = tid; q < NC * KW; q += NCT) {
             const int c = q / KW, w = q - c * KW;
             uint64_t v = 0;
             if (c < ncell) {
-                const int32_t p = P.queue[head0 + item0 + c];
+                const int64_t b = P.prefix ? (int64_t)P.blist[(int64_t)fsh * P.n_cap + pos0 + c] : pos0 + c;
+                const int32_t p = P.queue[head0 + b];
                 v = P.pool[(int64_t)p * KW + w];
                 if (w == 0) {
-                    P.batch_pool[item0 + c] = p;
-                    P.canon_pos[item0 + c] = -1;
-                    reinterpret_cast<double4*>(P.ckey_hint)[item0 + c] = reinterpret_cast<const double4*>(P.pool_hint)[p];
+                    S.bidx[c] = (int32_t)b;
+                    if (fsh) S.pitem[c] = (int32_t)(((unsigned long long)P.pool_par[p] >> 5) & 0x7ffffffull);
+                    P.batch_pool[b] = p;
+                    P.canon_pos[b] = -1;
+                    reinterpret_cast<double4*>(P.ckey_hint)[b] = reinterpret_cast<const double4*>(P.pool_hint)[p];
                 }
             }
             S.key[c][w] = v;
@@ -144,7 +183,7 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
             const int no = st.n_out;
             for (int idx = tid; idx < ncell * no; idx += NCT) {
                 const int c = idx / no, r = idx - c * no;
-                const int64_t item = item0 + c;
+                const int64_t item = S.bidx[c];
                 uint64_t* key = S.key[c];
                 const int row = st.row_off + r;
                 const double2 pa = *reinterpret_cast<const double2*>(&S.p1[r * 4]);
@@ -156,7 +195,7 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
                     const int cb = cc > 0.0;
                     if (cb != bit) { skey_set(key, row, cb); S.changed[c] = 1; bit = cb; }
                 }
-                double* z = P.Z + (item * P.zs + row) * 4;
+                double* z = Zc + (item * P.zs + row) * 4;
                 reinterpret_cast<double2*>(z)[0] = pa;
                 reinterpret_cast<double2*>(z)[1] = make_double2(a2, cc);
                 double* ao = &S.act[0][r * AS + c * 4];
@@ -167,9 +206,36 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
             PROF(1);
         }
 
+        // ---- prefix reuse: Z rows of steps 1..fsh are the parent's (same bits in every earlier
+        // layer); the masked rows of step fsh (own bits, canonical test of the flipped neuron)
+        // feed step fsh + 1
+        if (fsh) {
+            const StepDev& sf = P.st[fsh];
+            const int r0 = P.st[1].row_off, rf = sf.row_off, nrow = rf + sf.n_out - r0;
+            for (int idx = tid; idx < ncell * nrow; idx += NCT) {
+                const int c = idx / nrow, row = r0 + (idx - c * nrow);
+                const double2* src = reinterpret_cast<const double2*>(Zp + ((int64_t)S.pitem[c] * P.zs + row) * 4);
+                const double2 v0 = src[0], v1 = src[1];
+                double2* dst = reinterpret_cast<double2*>(Zc + ((int64_t)S.bidx[c] * P.zs + row) * 4);
+                dst[0] = v0;
+                dst[1] = v1;
+                if (row >= rf) {
+                    int bit = skey_bit(S.key[c], row);
+                    if (degenerate3(v0.x, v0.y, v1.x)) {
+                        const int cb = v1.y > 0.0;
+                        if (cb != bit) { skey_set(S.key[c], row, cb); S.changed[c] = 1; bit = cb; }
+                    }
+                    double* ao = &S.act[0][(row - rf) * AS + c * 4];
+                    reinterpret_cast<double2*>(ao)[0] = bit ? v0 : make_double2(0.0, 0.0);
+                    reinterpret_cast<double2*>(ao)[1] = bit ? v1 : make_double2(0.0, 0.0);
+                }
+            }
+            bar_sync(1, NCT);
+        }
+
         // ---- GEMM steps
         int cur = 0;
-        for (int s = 1; s < ns; s++) {
+        for (int s = fsh + 1; s < ns; s++) {
             const StepDev& st = P.st[s];
             const int nb = (st.n_in + KB - 1) / KB;
             double acc[MI][NJ][4];
@@ -267,12 +333,12 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
                                         bit = cb;
                                     }
                                 }
-                                *reinterpret_cast<double2*>(P.Z + ((item0 + c) * P.zs + row) * 4 + comp) = make_double2(v0, v1);
+                                *reinterpret_cast<double2*>(Zc + ((int64_t)S.bidx[c] * P.zs + row) * 4 + comp) = make_double2(v0, v1);
                                 *reinterpret_cast<double2*>(xo + r * AS + col) = bit ? make_double2(v0, v1) : make_double2(0.0, 0.0);
                             }
                         } else if (ok) {
                             const int bit = skey_bit(S.key[c], row);
-                            *reinterpret_cast<double2*>(P.Z + ((item0 + c) * P.zs + row) * 4 + comp) = make_double2(v0, v1);
+                            *reinterpret_cast<double2*>(Zc + ((int64_t)S.bidx[c] * P.zs + row) * 4 + comp) = make_double2(v0, v1);
                             *reinterpret_cast<double2*>(xo + r * AS + col) = bit ? make_double2(v0, v1) : make_double2(0.0, 0.0);
                         }
                     }
@@ -304,7 +370,7 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
                     a3 += __shfl_xor_sync(0xffffffffu, a3, o);
                 }
                 if (lane == 0) {
-                    double* f = P.faces + (item0 + c) * 4;
+                    double* f = P.faces + (int64_t)S.bidx[c] * 4;
                     f[0] = prec_round(a0, fp32); f[1] = prec_round(a1, fp32); f[2] = prec_round(a2, fp32);
                     f[3] = prec_round(a3 + head_bias(sd, item_shape(S.key[c], P.shape_w)), fp32);
                 }
@@ -314,9 +380,9 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
         // ---- canonical keys + changed flags out
         for (int q = tid; q < ncell * KW; q += NCT) {
             const int c = q / KW, w = q - c * KW;
-            P.keys[(item0 + c) * KW + w] = S.key[c][w];
+            P.keys[(int64_t)S.bidx[c] * KW + w] = S.key[c][w];
         }
-        if (tid < ncell) P.changed[item0 + tid] = S.changed[tid];
+        if (tid < ncell) P.changed[S.bidx[tid]] = S.changed[tid];
         bar_sync(1, NCT);
         PROF(5);
         if (prof) atomicAdd(&P.prof[7], 1ull);
@@ -391,15 +457,25 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         const int64_t n = dev_count(P.n_dev, P.n_cap);
         const int nc = tile_cells(n, P, gridDim.x);
-        const int64_t ntiles = (n + nc - 1) / nc;
+        Tiling T;
+        T.init(P, n, nc);
+        const int64_t ntiles = T.ntiles;
         if ((int64_t)blockIdx.x >= ntiles) {
             // no tile for this CTA: let the prefetched boxes land before exiting
             for (uint32_t i = 0; i < g; i++) mbar_wait(&S.full[i % NSB], (i / NSB) & 1);
             return;
         }
-        bool first = true;
+        // a first tile that starts past step 1 (prefix reuse) does not use the prefetched boxes:
+        // the consumers drain them and the tile's own sequence follows
+        int f0, nc0;
+        long long pos0;
+        T.locate(blockIdx.x, nc, f0, pos0, nc0);
+        bool first = f0 == 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            for (int s = 1; s < ns; s++) {
+            int f, ncell;
+            long long pos;
+            T.locate(t, nc, f, pos, ncell);
+            for (int s = f + 1; s < ns; s++) {
                 const int nb = (P.st[s].n_in + KB - 1) / KB;
                 for (int b = 0; b < nb; b++) {
                     if (first && (s < ps || (s == ps && b < pb))) continue;   // prefetched
@@ -420,9 +496,29 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
     const bool prof = (P.dbg & 8) && P.prof && threadIdx.x == 0;
     unsigned long long tprev = prof ? clock64() : 0;
     const int nc = tile_cells(n, P, gridDim.x);
-    if (nc == 8) consume<FP32, 2, 2>(S, P, n, head0, gbox, prof, tprev);
-    else if (nc == 4) consume<FP32, 1, 2>(S, P, n, head0, gbox, prof, tprev);
-    else consume<FP32, 1, 1>(S, P, n, head0, gbox, prof, tprev);
+    double* Zc = P.Z;
+    const double* Zp = P.Z;
+    if (P.prefix) {
+        const unsigned long long par = P.ctr[C_ITER] & 1ull;
+        Zc = P.Z + (int64_t)par * P.zstride;
+        Zp = P.Z + (int64_t)(par ^ 1ull) * P.zstride;
+        Tiling T;
+        T.init(P, n, nc);
+        int f0, nc0;
+        long long pos0;
+        T.locate(blockIdx.x, nc, f0, pos0, nc0);
+        if ((int64_t)blockIdx.x < T.ntiles && f0 > 0) {   // drain the prefetched boxes (see the producer)
+            const uint32_t pre = (P.dbg & 1) ? 0u : (uint32_t)(NSB < tile_boxes ? NSB : tile_boxes);
+            for (; gbox < pre; gbox++) {
+                mbar_wait(&S.full[gbox % NSB], (gbox / NSB) & 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.empty[gbox % NSB]);
+            }
+        }
+    }
+    if (nc == 8) consume<FP32, 2, 2>(S, P, n, head0, gbox, prof, tprev, Zc, Zp);
+    else if (nc == 4) consume<FP32, 1, 2>(S, P, n, head0, gbox, prof, tprev, Zc, Zp);
+    else consume<FP32, 1, 1>(S, P, n, head0, gbox, prof, tprev, Zc, Zp);
 }
 
 // debug (AM_NARROW_CHECK=1): compare the fused kernel's outputs with the per-step path's

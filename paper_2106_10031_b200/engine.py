@@ -302,9 +302,9 @@ class Engine:
         _native.check(self.lib.am_set_timing(self.h, int(on)), "am_set_timing")
 
     def stats(self) -> dict:
-        s = np.zeros(16)
+        s = np.zeros(18)
         _native.check(self.lib.am_stats(self.h, s.ctypes.data), "am_stats")
         keys = ("compose_ms", "face_ms", "compose_flops", "face_bytes", "composed", "faced", "batch",
                 "flops_per_cell", "launches", "iterations", "probe_ms", "probe_flops", "probes",
-                "flops_per_point", "probes_forwarded", "probe_records")
+                "flops_per_point", "probes_forwarded", "probe_records", "prefix_skipped_flops", "prefix")
         return dict(zip(keys, (float(x) for x in s)))
