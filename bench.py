@@ -373,6 +373,7 @@ def main():
         from paper_2106_10031_b200 import seeding
         marching.clear_engine_cache()
         seeding._BLOCKS.clear()
+        seeding._ROUNDS.clear()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         cold = marching.march(net, cfg)

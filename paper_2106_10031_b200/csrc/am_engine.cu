@@ -216,6 +216,20 @@ struct am_engine {
     int dg_shapes = -3;   // -2: per-point shapes, else the engine's current shape at capture
     std::vector<const void*> dg_ptrs;
     unsigned long long dg_kernels = 0;
+    // speculative-tree bisection graph (all rounds), keyed like the step graph
+    cudaGraphExec_t tgexec = nullptr;
+    int64_t tg_n = -1;
+    double tg_eps = 0, tg_tol = 0;
+    int tg_iters = -1, tg_shapes = -3;
+    std::vector<const void*> tg_ptrs;
+    unsigned long long tg_kernels = 0;
+    // seed refinement graph (am_seed_shapes), keyed like the bisection's
+    cudaGraphExec_t sgexec = nullptr;
+    int64_t sg_n = -1;
+    int sg_shape = -3;
+    std::vector<const void*> sg_ptrs;
+    unsigned long long sg_kernels = 0;
+    DBuf<int32_t> sshape;
     bool gather_input = true;   // k_gather_input: batch gather + input step in one launch
     int graph_batch = 32;   // iterations replayed per host synchronisation (A/B: 8 -> 25.7 ms, 16 -> 25.0, 32 -> 24.6)
     int grid_cap = 0;    // >0: CTAs per SM for persistent GEMM launches
@@ -680,6 +694,9 @@ extern "C" int am_engine_destroy(am_engine* e) {
     cudaStreamSynchronize(e->stream);
     if (e->gexec) cudaGraphExecDestroy(e->gexec);
     if (e->dgexec) cudaGraphExecDestroy(e->dgexec);
+    if (e->sgexec) cudaGraphExecDestroy(e->sgexec);
+    if (e->tgexec) cudaGraphExecDestroy(e->tgexec);
+    e->sshape.release(e->stream);
     for (auto* b : {&e->dxp, &e->dxn, &e->dfp, &e->dfn, &e->dmid, &e->dvals, &e->dout, &e->dtree, &e->dtvals})
         b->release(e->stream);
     e->dact.release(e->stream);
@@ -1535,31 +1552,61 @@ extern "C" int am_seed_shapes(am_engine* e, const double* d_pts, const int32_t* 
     CK(e->sact.reserve(n, s));
     CK(e->sdone.reserve(n, s));
     CK(cudaMemcpyAsync(e->sx.p, d_pts, n * 24, cudaMemcpyDeviceToDevice, s));
-    RC(forward_host(e, e->sx.p, n, nullptr, e->ss.p, d_shapes));
-    std::vector<int32_t> ones(n, 1);
-    CK(cudaMemcpyAsync(e->sact.p, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
-    for (int it = 0; it < 3; it++) {
+    const int32_t* shp = nullptr;
+    if (d_shapes) {
+        CK(e->sshape.reserve(n, s));
+        CK(cudaMemcpyAsync(e->sshape.p, d_shapes, n * 4, cudaMemcpyDeviceToDevice, s));
+        shp = e->sshape.p;
+    }
+    CK(e->shint.reserve(n * 4, s));
+    double ext = 0.0;
+    for (int k = 0; k < 3; k++) ext = std::max(ext, e->P.bbox_hi[k] - e->P.bbox_lo[k]);
+    // the refinement (3 project / re-evaluate rounds + the final composition) is a fixed
+    // sequence of ~50 small launches: captured once per (n, buffers) and replayed
+    auto body = [&]() -> int {
+        RC(forward_host(e, e->sx.p, n, nullptr, e->ss.p, shp));
+        CK(cudaMemsetAsync(e->sact.p, 1, n * 4, s));   // active: any non-zero word
+        for (int it = 0; it < 3; it++) {
+            CK(cudaMemcpyAsync(e->ckey.p, e->ss.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemsetAsync(e->changed.p, 0, n * 4, s));
+            RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n));
+            launch_seed_project(e->sx.p, e->faces.p, e->ckey.p, KW, e->M, e->ensemble, n, e->sact.p, e->sxp.p,
+                                e->sdone.p, s);
+            launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, e->sdone.p, s);
+            RC(forward_host(e, e->sxp.p, n, nullptr, e->ssn.p, shp));
+            launch_seed_check(e->ssn.p, e->ckey.p, KW, n, e->sact.p, e->sx.p, e->sxp.p, e->ss.p, e->sres.p, nullptr, s);
+            CK(cudaGetLastError());
+        }
         CK(cudaMemcpyAsync(e->ckey.p, e->ss.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemsetAsync(e->changed.p, 0, n * 4, s));
         RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n));
-        launch_seed_project(e->sx.p, e->faces.p, e->ckey.p, KW, e->M, e->ensemble, n, e->sact.p, e->sxp.p,
-                            e->sdone.p, s);
-        launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, e->sdone.p, s);
-        RC(forward_host(e, e->sxp.p, n, nullptr, e->ssn.p, d_shapes));
-        launch_seed_check(e->ssn.p, e->ckey.p, KW, n, e->sact.p, e->sx.p, e->sxp.p, e->ss.p, e->sres.p, nullptr, s);
+        launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, nullptr, s);
+        // the seed point (inside the seed's cell, on the surface up to seed_tol) is the face
+        // solver's hint, with a small initial reach that the solver widens as needed
+        launch_point_hints(e->sx.p, n, ext / 256.0, e->shint.p, s);
         CK(cudaGetLastError());
+        return AM_OK;
+    };
+    std::vector<const void*> ptrs = {e->sx.p, e->sxp.p, e->ss.p, e->ssn.p, e->sres.p, e->sact.p, e->sdone.p,
+                                     e->ckey.p, e->changed.p, e->Z.p, e->faces.p, e->pZ.p, e->shint.p, shp};
+    if (!e->sgexec || e->sg_n != n || e->sg_shape != (shp ? -2 : e->cur_shape) || e->sg_ptrs != ptrs) {
+        if (e->sgexec) { cudaGraphExecDestroy(e->sgexec); e->sgexec = nullptr; }
+        unsigned long long before = g_launch_count;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const int rc = body();
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(s, &g);
+        if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+        CK(ce);
+        e->sg_kernels = g_launch_count - before;
+        g_launch_count = before;
+        cudaError_t ie = cudaGraphInstantiate(&e->sgexec, g, 0);
+        cudaGraphDestroy(g);
+        CK(ie);
+        e->sg_n = n; e->sg_shape = shp ? -2 : e->cur_shape; e->sg_ptrs = ptrs;
     }
-    CK(cudaMemcpyAsync(e->ckey.p, e->ss.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemsetAsync(e->changed.p, 0, n * 4, s));
-    RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n));
-    launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, nullptr, s);
-    // the seed point (inside the seed's cell, on the surface up to seed_tol) is the face
-    // solver's hint, with a small initial reach that the solver widens as needed
-    double ext = 0.0;
-    for (int k = 0; k < 3; k++) ext = std::max(ext, e->P.bbox_hi[k] - e->P.bbox_lo[k]);
-    CK(e->shint.reserve(n * 4, s));
-    launch_point_hints(e->sx.p, n, ext / 256.0, e->shint.p, s);
-    CK(cudaGetLastError());
+    CK(cudaGraphLaunch(e->sgexec, s));
+    g_launch_count += e->sg_kernels;
     return push_keys(e, e->sres.p, n, e->shint.p);
 }
 
@@ -1610,15 +1657,48 @@ extern "C" int am_dichotomy_shapes(am_engine* e, const double* d_xpos, const dou
             CK(cudaMemcpyAsync(e->dtshape.p, ht.data(), n * TN * 4, cudaMemcpyHostToDevice, s));
             tshp = e->dtshape.p;
         }
-        for (int it0 = 1; it0 <= max_iters; it0 += TD) {
+        // the first kGraphRounds rounds of the tree (25 bisection steps: what a pair between
+        // sample points needs to reach eps) as one graph, captured per (n, tolerances, buffers),
+        // then one host check; any pair still open continues round by round
+        constexpr int kGraphRounds = 5;
+        auto round = [&](int it0) -> int {
             launch_bisect_tree(e->dxp.p, e->dxn.p, e->dact.p, n, e->dtree.p, s);
             RC(forward_host(e, e->dtree.p, n * TN, e->dtvals.p, e->hkeys.p, tshp));
-            launch_bisect_replay(e->dtvals.p, e->dtree.p, e->dxp.p, e->dxn.p, e->dfp.p, e->dfn.p, e->dact.p, e->dout.p, n,
-                                 it0, max_iters, eps, seed_tol, s);
+            launch_bisect_replay(e->dtvals.p, e->dtree.p, e->dxp.p, e->dxn.p, e->dfp.p, e->dfn.p, e->dact.p,
+                                 e->dout.p, n, it0, max_iters, eps, seed_tol, s);
+            return AM_OK;
+        };
+        int it0 = 1;
+        std::vector<const void*> tptrs = {e->dxp.p, e->dxn.p, e->dfp.p, e->dfn.p, e->dact.p, e->dout.p, e->dtree.p,
+                                          e->dtvals.p, e->hkeys.p, e->pZ.p, tshp};
+        if (!e->tgexec || e->tg_n != n || e->tg_eps != eps || e->tg_tol != seed_tol || e->tg_iters != max_iters ||
+            e->tg_shapes != (tshp ? -2 : e->cur_shape) || e->tg_ptrs != tptrs) {
+            if (e->tgexec) { cudaGraphExecDestroy(e->tgexec); e->tgexec = nullptr; }
+            unsigned long long before = g_launch_count;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            int rc = AM_OK;
+            for (int r = 0, i0 = 1; r < kGraphRounds && i0 <= max_iters && !rc; r++, i0 += TD) rc = round(i0);
+            cudaGraph_t g = nullptr;
+            cudaError_t ce = cudaStreamEndCapture(s, &g);
+            if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+            CK(ce);
+            e->tg_kernels = g_launch_count - before;
+            g_launch_count = before;
+            cudaError_t ie = cudaGraphInstantiate(&e->tgexec, g, 0);
+            cudaGraphDestroy(g);
+            CK(ie);
+            e->tg_n = n; e->tg_eps = eps; e->tg_tol = seed_tol; e->tg_iters = max_iters;
+            e->tg_shapes = tshp ? -2 : e->cur_shape; e->tg_ptrs = tptrs;
+        }
+        CK(cudaGraphLaunch(e->tgexec, s));
+        g_launch_count += e->tg_kernels;
+        it0 += kGraphRounds * TD;
+        for (; it0 <= max_iters; it0 += TD) {
             CK(cudaMemsetAsync(e->ctr.p + C_LIST, 0, 8, s));
             launch_count_active(e->dact.p, n, e->ctr.p + C_LIST, s);
             RC(sync_counters(e));
             if (e->hctr[C_LIST] == 0) break;
+            RC(round(it0));
         }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(d_out, e->dout.p, n * 24, cudaMemcpyDeviceToDevice, s));

@@ -65,6 +65,22 @@ def _sample_block(rng_seed: int, index: int, rnd: int, lo: np.ndarray, hi: np.nd
     return blocks[rnd]
 
 
+_ROUNDS: dict = {}
+
+
+def _sample_round(rng_seed: int, pending: np.ndarray, rnd: int, lo: np.ndarray, hi: np.ndarray) -> np.ndarray:
+    """(len(pending), 64, 3): the rnd-th draw of every pending stream, stacked (memoised like the
+    blocks themselves, so a repeated trigger is one dictionary lookup per round)."""
+    key = (int(rng_seed), int(rnd), pending.tobytes(), lo.tobytes(), hi.tobytes())
+    arr = _ROUNDS.get(key)
+    if arr is None:
+        if len(_ROUNDS) >= 256:
+            _ROUNDS.clear()
+        arr = _ROUNDS[key] = np.stack([_sample_block(rng_seed, int(i), rnd, lo, hi) for i in pending])
+        arr.setflags(write=False)
+    return arr
+
+
 def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int = 0, eps: float = SEED_TOL,
                  seed_tol: float = SEED_TOL, retry_budget: int = 200, collect_iters: list | None = None) -> np.ndarray:
     """Up to ``count`` surface points, deterministic given rng_seed (reference seeding.py:123-162)."""
@@ -75,27 +91,27 @@ def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int
     hi = np.asarray(bbox[1], dtype=np.float64)
     found: list = [None] * count
     if scheme == "dichotomy":
-        pairs: dict = {}
-        pending = list(range(count))
+        xp_f = np.zeros((count, 3))
+        xn_f = np.zeros((count, 3))
+        have = np.zeros(count, dtype=bool)
+        pending = np.arange(count)
         for rnd in range(retry_budget):
-            if not pending:
+            if not len(pending):
                 break
-            pts = np.stack([_sample_block(rng_seed, i, rnd, lo, hi) for i in pending])
+            pts = _sample_round(rng_seed, pending, rnd, lo, hi)
             vals = eng.forward(pts.reshape(-1, 3)).cpu().numpy().reshape(len(pending), 64)
             # first positive / first negative sample of each stream (reference seeding.py:150-156)
             pm, nm = vals > 0.0, vals < 0.0
             ok = pm.any(axis=1) & nm.any(axis=1)
-            ip, ineg = pm.argmax(axis=1), nm.argmax(axis=1)
-            rows = np.arange(len(pending))
-            xp_all, xn_all = pts[rows, ip], pts[rows, ineg]
-            for j in np.flatnonzero(ok):
-                pairs[pending[j]] = (xp_all[j], xn_all[j])
-            pending = [pending[j] for j in np.flatnonzero(~ok)]
-        if pairs:
-            order = sorted(pairs)
-            xp = np.stack([pairs[i][0] for i in order])
-            xn = np.stack([pairs[i][1] for i in order])
-            pts = eng.dichotomy(xp, xn, eps, seed_tol).cpu().numpy()
+            rows = np.flatnonzero(ok)
+            idx = pending[rows]
+            xp_f[idx] = pts[rows, pm.argmax(axis=1)[rows]]
+            xn_f[idx] = pts[rows, nm.argmax(axis=1)[rows]]
+            have[idx] = True
+            pending = pending[~ok]
+        order = np.flatnonzero(have)
+        if len(order):
+            pts = eng.dichotomy(xp_f[order], xn_f[order], eps, seed_tol).cpu().numpy()
             for i, p in zip(order, pts):
                 found[i] = p
     else:
