@@ -43,7 +43,7 @@ def nvcc() -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     """AM_BUILD_FLAGS (space-separated) are appended to every nvcc compile (e.g. -DAM_FACE_STATS)."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "am_internal.h"), os.path.join(CSRC, "am_ptx.cuh"),
+    deps = srcs + [os.path.join(CSRC, "am_internal.h"), os.path.join(CSRC, "am_ptx.cuh"), os.path.join(CSRC, "am_near.cuh"),
                    os.path.join(os.path.dirname(HERE), "include", "am_b200.h")]
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
         return OUT

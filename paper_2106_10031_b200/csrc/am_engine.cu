@@ -165,6 +165,7 @@ struct am_engine {
     // halves by iteration parity, each pool entry's / emitted flip's parent word, and the batch
     // listed per shared-step bucket
     bool prefix = false;
+    bool near_fused = false;    // near lists built by k_compose_narrow (AM_NEAR_FUSED=1; default: k_near)
     DBuf<double> Zi;
     DBuf<int64_t> pool_par, emit_par;
     DBuf<int32_t> blist;
@@ -653,6 +654,11 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     CK(e->near_n.reserve(e->B, s));
     CK(e->f_order.reserve(e->B, s));
     if (const char* v = getenv("AM_FACE_ORDER")) e->face_order = atoi(v) != 0;
+    // near lists inside k_compose_narrow (AM_NEAR_FUSED=1): correct, but slower on configs[1]
+    // (BFS 18.58 vs 18.27 ms): 12 warps per SM stream the tile's rows at the end of every tile,
+    // where k_near keeps 32 warps per SM of row loads in flight
+    if (const char* v = getenv("AM_NEAR_FUSED"))
+        e->near_fused = e->narrow_fused && !e->face_order && !e->narrow_check && atoi(v) != 0;
     if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
     // deferral re-composes the deferred cells: worth it where the face solve dominates (narrow
     // nets; configs[1] 19.75 -> 18.85 ms), not where composition does (DeepSDF 512x8: 0.724 ->
@@ -983,6 +989,11 @@ static int launch_iteration(am_engine* e) {
         N.batch_pool = e->batch_pool.p; N.canon_pos = e->canon_pos.p; N.ckey_hint = e->ckey_hint.p;
         N.Z = e->prefix ? e->Zi.p : e->Z.p; N.keys = e->ckey.p; N.faces = e->faces.p; N.changed = e->changed.p;
         N.prefix = e->prefix; N.zstride = e->B * e->zs * 4; N.pool_par = e->pool_par.p; N.blist = e->blist.p;
+        N.near_fused = e->near_fused; N.NB = e->NB;
+        N.near_n = e->near_n.p; N.near_flags = e->near_flags.p; N.near_id = e->near_id.p; N.near_row = e->near_row.p;
+        N.near_cap = e->near_cap; N.near_reach = e->near_reach; N.tol_cell = e->P.tol_cell;
+        N.tol_onplane = e->P.tol_onplane; N.probe_delta = e->P.probe_delta;
+        for (int k = 0; k < 3; k++) { N.lo[k] = e->P.bbox_lo[k]; N.hi[k] = e->P.bbox_hi[k]; }
         N.n_dev = c + C_NR; N.n_cap = B; N.KW = e->KW; N.zs = e->zs; N.shape_w = e->shape_w; N.fp32 = e->fp32;
         N.prof = e->dbg.p + 32;
         launch_compose_narrow(N, s);
@@ -1044,7 +1055,7 @@ static int launch_iteration(am_engine* e) {
     a.dbg = e->dbg.p;
     a.cursor = c + C_FCURSOR;
     a.near_cap = e->near_cap; a.near_n = e->near_n.p; a.near_flags = e->near_flags.p;
-    a.near_id = e->near_id.p; a.near_row = e->near_row.p;
+    a.near_id = e->near_id.p; a.near_row = e->near_row.p; a.near_by_item = e->near_fused ? 1 : 0;
     a.order = e->face_order ? e->f_order.p : nullptr; a.order_ctr = c + C_NHEAVY;
     a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
     a.tau_grow = e->tau_grow;
@@ -1057,7 +1068,7 @@ static int launch_iteration(am_engine* e) {
     }
     if (tm) cudaEventRecord(e->ev[2], s);
     mark(4);
-    launch_near(a, s);
+    if (!e->near_fused) launch_near(a, s);
     mark(5);
     launch_face(a, s);
     mark(6);

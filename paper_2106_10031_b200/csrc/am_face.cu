@@ -36,6 +36,7 @@
 #include <cstdlib>
 
 #include "am_internal.h"
+#include "am_near.cuh"
 
 namespace am {
 
@@ -62,8 +63,6 @@ constexpr int kFaceCtasPerSm = 3;
 constexpr int NMAX = AM_NMAX;  // hinted path: rows near the hint point (more: the full path)
 constexpr double kCDelta = 1e-10;
 constexpr double kValMargin = 1e-11;   // sign margin (unit and raw values) for probe validation
-constexpr double kTinyNorm = 1e-6;     // rows this thin make validation unreliable
-constexpr int kNearValid = 1, kNearX0Bad = 2, kNearRisky = 4, kNearOverflow = 8;
 
 // phase-private scratch: near rows (hinted clipping) and polygon assembly never overlap
 struct NearPhase {
@@ -115,14 +114,6 @@ struct FaceWarp {
     int status;
 };
 
-struct Ctx {
-    const double* Z;   // this item's rows
-    const double* faces;
-    const uint64_t* key;
-    int NB, M, branch, ensemble, K;
-    double lo[3], hi[3];
-};
-
 // this iteration's half of the (prefix-reuse double-buffered) composition rows
 __device__ __forceinline__ const double* zbase(const FaceArgs& A) {
     return A.zpar ? A.Z + (int64_t)(*A.zpar & 1ull) * A.zstride : A.Z;
@@ -165,45 +156,6 @@ __device__ __noinline__ bool get_row(const Ctx& c, int gr, double n[3], double& 
 
 __device__ __forceinline__ double dot3(const double* a, const double* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
 
-// raw functional of global plane id gr (not normalised, not oriented); kind: 0 neuron,
-// 1 branch (valid unless it is the cell's own branch), 2 box, -1 none
-struct RawRow { double x, y, z, c; int kind; };
-// branch-dominance, box and padding rows (a handful per cell): out of line
-__device__ __noinline__ RawRow load_raw_other(const Ctx& c, int gr) {
-    RawRow r;
-    if (gr < c.NB + c.M) {
-        int t = gr - c.NB;
-        r.kind = (!c.ensemble || t == c.branch) ? -1 : 1;
-        if (r.kind == 1) {
-            const double* ft = c.faces + t * 4;
-            const double* fj = c.faces + c.branch * 4;
-            r.x = ft[0] - fj[0]; r.y = ft[1] - fj[1]; r.z = ft[2] - fj[2]; r.c = ft[3] - fj[3];
-        } else {
-            r.x = r.y = r.z = r.c = 0.0;
-        }
-    } else if (gr < c.K) {
-        int k = gr - c.NB - c.M, ax = k >> 1;
-        r.x = r.y = r.z = 0.0;
-        double sg = (k & 1) ? -1.0 : 1.0;
-        if (ax == 0) r.x = sg; else if (ax == 1) r.y = sg; else r.z = sg;
-        r.c = (k & 1) ? c.lo[ax] : -c.hi[ax];
-        r.kind = 2;
-    } else {
-        r.x = r.y = r.z = r.c = 0.0;
-        r.kind = -1;
-    }
-    return r;
-}
-__device__ __forceinline__ RawRow load_raw(const Ctx& c, int gr) {
-    if (gr < c.NB) {
-        RawRow r;
-        const double2* p = reinterpret_cast<const double2*>(c.Z + (int64_t)gr * 4);
-        double2 a = __ldg(p), b = __ldg(p + 1);
-        r.x = a.x; r.y = a.y; r.z = b.x; r.c = b.y; r.kind = 0;
-        return r;
-    }
-    return load_raw_other(c, gr);
-}
 // 2-D projection (a, b, g) of the oriented unit row in the face-plane frame, with one
 // reciprocal per row (the streaming passes only need it to ~1 ulp); *nrm = raw norm
 __device__ __forceinline__ bool row2d(const Ctx& c, int gr, const RawRow& r, const double U[3], const double V[3],
@@ -575,9 +527,10 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
     double tau = A.tau_mult * hint.w;
     // near list from k_near (rows within `reach` of x0): attempts with tau <= reach filter it
     // instead of streaming every row again
-    const int list_flags = (A.near_flags && have_hint) ? A.near_flags[fi] : 0;
+    const int64_t nslot = A.near_by_item ? (int64_t)item : fi;   // near lists built by the composition: per item
+    const int list_flags = (A.near_flags && have_hint) ? A.near_flags[nslot] : 0;
     const bool use_list = (list_flags & kNearValid) && !(list_flags & kNearOverflow);
-    const int n_list = use_list ? A.near_n[fi] : 0;
+    const int n_list = use_list ? A.near_n[nslot] : 0;
     const double reach = A.near_reach * hint.w;
     FSTAT(14, use_list ? 1 : 0);
     FSTAT(15, (list_flags & kNearOverflow) ? 1 : 0);
@@ -607,7 +560,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
         bool ok = true;
         if (use_list && tau <= reach) {
             // the near kernel's list (rows within `reach` of x0, ascending ids): same test, tighter lim
-            const int64_t lb = fi * (int64_t)A.near_cap;
+            const int64_t lb = nslot * (int64_t)A.near_cap;
 #pragma unroll 1
             for (int base = 0; base < n_list; base += 32) {
                 const int j = base + lane;
@@ -1300,7 +1253,6 @@ __device__ __forceinline__ void place_cell(const FaceArgs& A, int64_t n, int64_t
 __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
     pdl_enter();
     const int lane = threadIdx.x & 31;
-    const unsigned full = 0xffffffffu;
     const int64_t n = dev_count(A.n_dev, A.n_cap);
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t fi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; fi < n; fi += nw) {
@@ -1313,65 +1265,11 @@ __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
         c.branch = A.ensemble ? (int)c.key[A.KW - 1] : 0;
         c.K = A.NB + A.M + 6;
         for (int k = 0; k < 3; k++) { c.lo[k] = A.lo[k]; c.hi[k] = A.hi[k]; }
-        // face plane and projected hint point: the face solver's arithmetic
-        const double* fr = c.faces + c.branch * 4;
-        const double fn = sqrt((fr[0] * fr[0] + fr[1] * fr[1]) + fr[2] * fr[2]);
-        double fu[3] = {0, 0, 0}, fo = 0.0;
-        bool face_ok = fn > kDegen;
-        if (face_ok) {
-            fu[0] = fr[0] / fn; fu[1] = fr[1] / fn; fu[2] = fr[2] / fn; fo = fr[3] / fn;
-            face_ok = sqrt((fu[0] * fu[0] + fu[1] * fu[1]) + fu[2] * fu[2]) > kDegen;
-        }
-        double4 hint = reinterpret_cast<const double4*>(A.hints)[item];
-        if (!(isfinite(hint.w) && face_ok)) {
-            if (lane == 0) {
-                A.near_flags[fi] = 0;
-                place_cell(A, n, fi, face_ok);   // no hint: the full two-pass path; empty face: quick
-            }
-            continue;
-        }
-        const double hd = ((fu[0] * hint.x + fu[1] * hint.y) + fu[2] * hint.z) + fo;
-        hint.x -= hd * fu[0]; hint.y -= hd * fu[1]; hint.z -= hd * fu[2];
-        const double x0[3] = {hint.x, hint.y, hint.z};
-        const double band = fmax(A.tol_cell, A.tol_onplane) + 1.5 * A.probe_delta + 1e-9;
-        const double lim = A.near_reach * hint.w + band + 1e-9;
-        const int64_t lb = fi * (int64_t)A.near_cap;
-        int nn = 0, risky = 0;
-        bool ok = true;
-        RawRow nx1 = load_raw(c, lane), nx2 = load_raw(c, lane + 32);
-        for (int base = 0; base < c.K; base += 32) {
-            const int gr = base + lane;
-            const RawRow rr = nx1;
-            nx1 = nx2;
-            if (base + 64 < c.K) nx2 = load_raw(c, gr + 64);
-            bool near = false;
-            if (gr < c.K && rr.kind >= 0) {
-                const double n2 = (rr.x * rr.x + rr.y * rr.y) + rr.z * rr.z;
-                if (rr.kind == 0 && n2 > 0.0 && n2 < kTinyNorm * kTinyNorm) risky = 1;
-                if (rr.kind == 1 && n2 < kTinyNorm * kTinyNorm) risky = 1;
-                if (rr.kind == 2 || n2 > kDegen * kDegen) {
-                    double v = ((rr.x * x0[0] + rr.y * x0[1]) + rr.z * x0[2]) + rr.c;
-                    if (rr.kind == 0 && key_bit(c.key, gr)) v = -v;
-                    if (v > 0.0 && v * v > 1e-18 * n2) ok = false;   // x0 violates the row by > 1e-9
-                    near = v >= 0.0 || v * v <= lim * lim * n2;
-                }
-            }
-            const unsigned mask = __ballot_sync(full, near);
-            const int pos = nn + __popc(mask & ((1u << lane) - 1u));
-            if (near && pos < A.near_cap) {
-                A.near_id[lb + pos] = gr;
-                reinterpret_cast<double4*>(A.near_row)[lb + pos] = make_double4(rr.x, rr.y, rr.z, rr.c);
-            }
-            nn += __popc(mask);
-        }
-        ok = __all_sync(full, ok);
-        risky = __any_sync(full, risky);
-        if (lane == 0) {
-            A.near_n[fi] = nn < A.near_cap ? nn : A.near_cap;
-            A.near_flags[fi] = kNearValid | (ok ? 0 : kNearX0Bad) | (risky ? kNearRisky : 0) |
-                               (nn > A.near_cap ? kNearOverflow : 0);
-            place_cell(A, n, fi, !ok || nn > A.near_cap);
-        }
+        NearOut o{A.near_n, A.near_flags, A.near_id, A.near_row, A.near_cap};
+        bool heavy = false;
+        near_list<true>(c, reinterpret_cast<const double4*>(A.hints)[item], A.tol_cell, A.tol_onplane, A.probe_delta,
+                        A.near_reach, o, fi, heavy);
+        if (lane == 0) place_cell(A, n, fi, heavy);
     }
 }
 

@@ -215,6 +215,16 @@ struct NarrowCompose {
     int64_t zstride;
     const int64_t* pool_par;
     const int32_t* blist;
+    // near lists of the tile's cells (near_fused != 0; am_near.cuh), indexed by batch item
+    int near_fused;
+    int NB;
+    int32_t* near_n;
+    int32_t* near_flags;
+    int32_t* near_id;
+    double* near_row;
+    int near_cap;
+    double near_reach, tol_cell, tol_onplane, probe_delta;
+    double lo[3], hi[3];
 };
 // sharded march exchange (am_shard.cu)
 constexpr int kHdrWords = 8;
@@ -439,6 +449,7 @@ struct FaceArgs {
     unsigned long long* order_ctr;   // [0] heavy cells placed from the front, [1] light from the back
     int32_t* near_id;         // [n_cap][near_cap]
     double* near_row;         // [n_cap][near_cap][4]
+    int near_by_item;         // 1: lists indexed by batch item (built by k_compose_narrow), 0: by frontier entry
     // prefix reuse: Z half of this iteration (parity of *zpar), and every emitted flip's
     // prefix_word (first flipped step: step_end[f] > its row) -- null zpar / emit_par: off
     const unsigned long long* zpar;

@@ -29,6 +29,7 @@
 #include <algorithm>
 
 #include "am_internal.h"
+#include "am_near.cuh"
 #include "am_ptx.cuh"
 
 namespace am {
@@ -385,6 +386,25 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
         if (tid < ncell) P.changed[S.bidx[tid]] = S.changed[tid];
         bar_sync(1, NCT);
         PROF(5);
+        if (P.near_fused) {
+            // ---- near lists of the tile's cells (the face solver's k_near), while their rows are
+            // in L2: warp per cell, the same warp that wrote the cell's face plane
+            for (int c = warp; c < ncell; c += NCW) {
+                const int64_t b = S.bidx[c];
+                Ctx cx;
+                cx.Z = Zc + b * P.zs * 4;
+                cx.faces = P.faces + b * 4;
+                cx.key = S.key[c];
+                cx.NB = P.NB; cx.M = 1; cx.branch = 0; cx.ensemble = 0; cx.K = P.NB + 1 + 6;
+                for (int k = 0; k < 3; k++) { cx.lo[k] = P.lo[k]; cx.hi[k] = P.hi[k]; }
+                const NearOut o{P.near_n, P.near_flags, P.near_id, P.near_row, P.near_cap};
+                bool heavy = false;
+                near_list<false>(cx, reinterpret_cast<const double4*>(P.ckey_hint)[b], P.tol_cell, P.tol_onplane,
+                                 P.probe_delta, P.near_reach, o, b, heavy);
+            }
+            bar_sync(1, NCT);
+            PROF(9);
+        }
         if (prof) atomicAdd(&P.prof[7], 1ull);
     }
 #undef PROF
