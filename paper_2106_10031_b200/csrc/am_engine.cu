@@ -165,6 +165,7 @@ struct am_engine {
     // halves by iteration parity, each pool entry's / emitted flip's parent word, and the batch
     // listed per shared-step bucket
     bool prefix = false;
+    int near_depth = 2;         // AM_NEAR_DEPTH
     bool near_fused = false;    // near lists built by k_compose_narrow (AM_NEAR_FUSED=1; default: k_near)
     DBuf<double> Zi;
     DBuf<int64_t> pool_par, emit_par;
@@ -657,6 +658,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // near lists inside k_compose_narrow (AM_NEAR_FUSED=1): correct, but slower on configs[1]
     // (BFS 18.58 vs 18.27 ms): 12 warps per SM stream the tile's rows at the end of every tile,
     // where k_near keeps 32 warps per SM of row loads in flight
+    if (const char* v = getenv("AM_NEAR_DEPTH")) e->near_depth = atoi(v);
     if (const char* v = getenv("AM_NEAR_FUSED"))
         e->near_fused = e->narrow_fused && !e->face_order && !e->narrow_check && atoi(v) != 0;
     if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
@@ -1056,6 +1058,7 @@ static int launch_iteration(am_engine* e) {
     a.cursor = c + C_FCURSOR;
     a.near_cap = e->near_cap; a.near_n = e->near_n.p; a.near_flags = e->near_flags.p;
     a.near_id = e->near_id.p; a.near_row = e->near_row.p; a.near_by_item = e->near_fused ? 1 : 0;
+    a.near_depth = e->near_depth;
     a.order = e->face_order ? e->f_order.p : nullptr; a.order_ctr = c + C_NHEAVY;
     a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
     a.tau_grow = e->tau_grow;

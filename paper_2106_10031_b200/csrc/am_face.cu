@@ -1250,6 +1250,7 @@ __device__ __forceinline__ void place_cell(const FaceArgs& A, int64_t n, int64_t
     else A.order[n - 1 - (int64_t)atomicAdd(&A.order_ctr[1], 1ull)] = (int32_t)fi;
 }
 
+template <int D>
 __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
     pdl_enter();
     const int lane = threadIdx.x & 31;
@@ -1267,27 +1268,32 @@ __global__ void __launch_bounds__(256) k_near(FaceArgs A) {
         for (int k = 0; k < 3; k++) { c.lo[k] = A.lo[k]; c.hi[k] = A.hi[k]; }
         NearOut o{A.near_n, A.near_flags, A.near_id, A.near_row, A.near_cap};
         bool heavy = false;
-        near_list<true>(c, reinterpret_cast<const double4*>(A.hints)[item], A.tol_cell, A.tol_onplane, A.probe_delta,
-                        A.near_reach, o, fi, heavy);
+        near_list<true, D>(c, reinterpret_cast<const double4*>(A.hints)[item], A.tol_cell, A.tol_onplane,
+                           A.probe_delta, A.near_reach, o, fi, heavy);
         if (lane == 0) place_cell(A, n, fi, heavy);
     }
 }
 
-void launch_near(const FaceArgs& a, cudaStream_t s) {
-    if (a.n_cap <= 0 || !a.near_flags) return;
-    int64_t warps = a.n_cap;
+template <int D>
+static void launch_near_d(const FaceArgs& a, cudaStream_t s) {
     static int grid_max[64] = {};   // per device
     int dev = 0;
     cudaGetDevice(&dev);
     const int di = dev >= 0 && dev < 64 ? dev : 0;
     if (!grid_max[di]) {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near<D>, 256, 0);
         if (const char* v = getenv("AM_NEAR_CTAS")) per_sm = std::min(per_sm, std::max(1, atoi(v)));
         grid_max[di] = device_sms() * (per_sm > 0 ? per_sm : 1);
     }
-    int64_t blocks = (warps + 7) / 8;
-    launch_k(k_near, (unsigned)(blocks < grid_max[di] ? blocks : grid_max[di]), 256, 0, s, a);
+    const int64_t blocks = (a.n_cap + 7) / 8;   // a warp per frontier entry
+    launch_k(k_near<D>, (unsigned)(blocks < grid_max[di] ? blocks : grid_max[di]), 256, 0, s, a);
+}
+
+void launch_near(const FaceArgs& a, cudaStream_t s) {
+    if (a.n_cap <= 0 || !a.near_flags) return;
+    if (a.near_depth >= 4) launch_near_d<4>(a, s);
+    else launch_near_d<2>(a, s);
 }
 
 // persistent: each warp walks the device-resident frontier

@@ -450,6 +450,7 @@ struct FaceArgs {
     int32_t* near_id;         // [n_cap][near_cap]
     double* near_row;         // [n_cap][near_cap][4]
     int near_by_item;         // 1: lists indexed by batch item (built by k_compose_narrow), 0: by frontier entry
+    int near_depth;           // k_near: 32-row batches in flight per warp (2 or 4; AM_NEAR_DEPTH)
     // prefix reuse: Z half of this iteration (parity of *zpar), and every emitted flip's
     // prefix_word (first flipped step: step_end[f] > its row) -- null zpar / emit_par: off
     const unsigned long long* zpar;

@@ -78,7 +78,7 @@ struct NearOut {
 // Warp-collective: the near list of the cell in c, written at `slot`.  heavy (lane-uniform):
 // the face solver's slow paths are certain (no usable hint with a face, x0 outside the cell, or
 // a list overflow).
-template <bool NC>
+template <bool NC, int D = 2>   // D: row batches of 32 in flight per warp
 __device__ __forceinline__ void near_list(const Ctx& c, double4 hint, double tol_cell, double tol_onplane,
                                           double probe_delta, double near_reach, const NearOut& o, int64_t slot,
                                           bool& heavy) {
@@ -106,12 +106,15 @@ __device__ __forceinline__ void near_list(const Ctx& c, double4 hint, double tol
     const int64_t lb = slot * (int64_t)o.cap;
     int nn = 0, risky = 0;
     bool ok = true;
-    RawRow nx1 = load_raw<NC>(c, lane), nx2 = load_raw<NC>(c, lane + 32);
+    RawRow nx[D];
+#pragma unroll
+    for (int d = 0; d < D; d++) nx[d] = load_raw<NC>(c, lane + 32 * d);
     for (int base = 0; base < c.K; base += 32) {
         const int gr = base + lane;
-        const RawRow rr = nx1;
-        nx1 = nx2;
-        if (base + 64 < c.K) nx2 = load_raw<NC>(c, gr + 64);
+        const RawRow rr = nx[0];
+#pragma unroll
+        for (int d = 0; d + 1 < D; d++) nx[d] = nx[d + 1];
+        if (base + 32 * D < c.K) nx[D - 1] = load_raw<NC>(c, gr + 32 * D);
         bool near = false;
         if (gr < c.K && rr.kind >= 0) {
             const double n2 = (rr.x * rr.x + rr.y * rr.y) + rr.z * rr.z;
