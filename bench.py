@@ -312,7 +312,8 @@ def main():
     stage_sum = sum(ms.values())
     kw8 = kt["kw"] * 8
     comp_ms = ms["compose"]
-    comp_flops = s1["flops_per_cell"] * kt["composed"]
+    # executed DMMA work: the composition steps taken from parents' rows (prefix reuse) excluded
+    comp_flops = s1["flops_per_cell"] * kt["composed"] - s1.get("prefix_skipped_flops", 0.0)
     comp_tf = comp_flops / (comp_ms * 1e-3) / 1e12 if comp_ms else 0.0
     face_ms = ms["near"] + ms["face"]
     face_gbs = s1["face_bytes"] / (face_ms * 1e-3) / 1e9 if face_ms else 0.0
@@ -485,7 +486,8 @@ def main():
         drun()
         ds = deng.stats()
         deng.set_timing(False)
-        dtf = ds["compose_flops"] / (ds["compose_ms"] * 1e-3) / 1e12 if ds["compose_ms"] else 0.0
+        dtf = ((ds["compose_flops"] - ds.get("prefix_skipped_flops", 0.0)) / (ds["compose_ms"] * 1e-3) / 1e12
+               if ds["compose_ms"] else 0.0)
         others["configs[2]"] = {
             "workload": "DeepSDF-style 3-(512x8)-1, linear skip over layers 1-4, seed 0, fp64, 64 dichotomy seeds; "
                         f"first {dcells} cells (max_cells cap {cap}; the full march is ~16M cells)",

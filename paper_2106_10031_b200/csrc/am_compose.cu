@@ -71,7 +71,7 @@ __device__ __forceinline__ void input_elem(const LayerLaunch& L, uint64_t* keys,
     const double* w = st.W + (int64_t)r * st.ldw;
     uint64_t* key = keys + item * L.KW;
     int row = st.row_off + r;
-    double* z = L.Z + (item * L.zs + row) * C;
+    double* z = zbase(L) + (item * L.zs + row) * C;
     bool sc = st.flags & (AM_STEP_SHORTCUT_IDENT | AM_STEP_SHORTCUT_LINEAR);
     const bool has_vb = st.vb || st.vb_shape;
     const int shp = item_shape(key, L.shape_w);
@@ -155,9 +155,23 @@ void launch_input_step(const LayerLaunch& L, int C, cudaStream_t s) {
 // warp's lanes then compute the item's layer-1 rows exactly as k_input_step does (input_elem),
 // so a BFS iteration launches one kernel less.  __syncwarp orders the gathered key and the reset
 // flags before the lanes' canonical-bit updates of the same item.
+// batch item b -> (bucket f, position) of the prefix-reuse bucketing (k_take): items are laid out
+// bucket after bucket, ascending f
+__device__ __forceinline__ int bucket_of(const unsigned long long* ctr, int nb, int64_t b, int64_t& pos) {
+    int f = 0;
+    int64_t off = 0;
+    for (; f < nb - 1; f++) {
+        const int64_t c = (int64_t)ctr[C_BK0 + f];
+        if (b < off + c) break;
+        off += c;
+    }
+    pos = b - off;
+    return f;
+}
+
 __global__ void k_gather_input(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                                const unsigned long long* ctr, int32_t* batch_pool, double* ckey_hint,
-                               int32_t* canon_pos, LayerLaunch L) {
+                               int32_t* canon_pos, LayerLaunch L, const int32_t* blist, int nb) {
     pdl_enter();
     const int64_t n = dev_count(ctr + C_NR, L.n_cap);
     const int64_t head0 = (int64_t)ctr[C_QHEAD] - n;
@@ -165,7 +179,13 @@ __global__ void k_gather_input(const uint64_t* pool, const double* pool_hint, co
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     uint64_t* keys = L.keys;
     for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < n; b += nw) {
-        const int32_t p = queue[head0 + b];
+        int64_t q = b;
+        if (blist) {   // prefix reuse: bucket order (cells sharing fewer steps first)
+            int64_t pos;
+            const int f = bucket_of(ctr, nb, b, pos);
+            q = blist[(int64_t)f * L.n_cap + pos];
+        }
+        const int32_t p = queue[head0 + q];
         for (int w = lane; w < L.KW; w += 32) keys[b * L.KW + w] = pool[(int64_t)p * L.KW + w];
         if (lane == 0) {
             batch_pool[b] = p;
@@ -181,11 +201,58 @@ __global__ void k_gather_input(const uint64_t* pool, const double* pool_hint, co
 
 void launch_gather_input(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                          const unsigned long long* ctr, int32_t* batch_pool, double* ckey_hint, int32_t* canon_pos,
-                         const LayerLaunch& L, cudaStream_t s) {
+                         const LayerLaunch& L, cudaStream_t s, const int32_t* blist, int nb) {
     if (L.n_cap <= 0) return;
     const int64_t blocks = std::min<int64_t>((L.n_cap + 7) / 8, (int64_t)num_sms() * 16);
     launch_k(k_gather_input, (unsigned)blocks, 256, 0, s, pool, pool_hint, queue, ctr, batch_pool, ckey_hint,
-             canon_pos, L);
+             canon_pos, L, blist, nb);
+}
+
+// Prefix reuse on the per-step path: the items of buckets f >= 1 take the Z rows of steps 1..f
+// from their parents (the previous iteration's half of Z) instead of composing them, with the
+// canonical test of step f's rows (its flipped neuron: the parent's bits hold for every earlier
+// step); the GEMM of step s then runs over the items of buckets f < s only (C_PRE0 + s).  Warp
+// per item.
+__global__ void k_prefix_rows(PrefixRows R, LayerLaunch L, const int32_t* batch_pool, const int64_t* pool_par) {
+    pdl_enter();
+    const int64_t n = dev_count(R.ctr + C_NR, L.n_cap);
+    const int64_t n0 = (int64_t)R.ctr[C_BK0];
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const unsigned long long par = *L.zpar & 1ull;
+    double* Zc = L.Z + (int64_t)par * L.zstride;
+    const double* Zp = L.Z + (int64_t)(par ^ 1ull) * L.zstride;
+    for (int64_t b = n0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); b < n; b += nw) {
+        int64_t pos;
+        const int f = bucket_of(R.ctr, R.nb, b, pos);
+        const int64_t pi = (int64_t)(((unsigned long long)pool_par[batch_pool[b]] >> 5) & 0x7ffffffull);
+        const int r0 = R.row_off[1], rf = R.row_off[f], r1 = rf + R.n_out[f];
+        uint64_t* key = L.keys + b * L.KW;
+        for (int row = r0 + lane; row < r1; row += 32) {
+            const double2* src = reinterpret_cast<const double2*>(Zp + (pi * L.zs + row) * 4);
+            const double2 v0 = src[0], v1 = src[1];
+            double2* dst = reinterpret_cast<double2*>(Zc + (b * L.zs + row) * 4);
+            dst[0] = v0;
+            dst[1] = v1;
+            if (row >= rf) {
+                const double nrm = sqrt((v0.x * v0.x + v0.y * v0.y) + v1.x * v1.x);
+                if (!(nrm > kDegen)) {
+                    const int bit = v1.y > 0.0;
+                    if (bit != key_bit(key, row)) {
+                        set_key_bit(key, row, bit);
+                        if (L.changed) L.changed[b] = 1;
+                    }
+                }
+            }
+        }
+    }
+}
+
+void launch_prefix_rows(const PrefixRows& R, const LayerLaunch& L, const int32_t* batch_pool, const int64_t* pool_par,
+                        cudaStream_t s) {
+    if (L.n_cap <= 0) return;
+    const int64_t blocks = std::min<int64_t>((L.n_cap + 7) / 8, (int64_t)num_sms() * 16);
+    launch_k(k_prefix_rows, (unsigned)blocks, 256, 0, s, R, L, batch_pool, pool_par);
 }
 
 // ----------------------------------------------------------- GEMM step
@@ -261,6 +328,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                                           const CUtensorMap* tmWp, const CUtensorMap* tmVp, int m0, int64_t n0,
                                           uint32_t& gchunk, bool wres = false) {
     const StepDev& st = L.st;
+    double* const Zb = zbase(L);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     using T = GT<C, TM>;
@@ -322,7 +390,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                     const int krow = j >> 1;                 // 2 pieces per row (4 doubles)
                     if ((NP % T::NT == 0 || piece < NP) && item < n && krow < valid)
                         cp_async16(&S.x[stage][it * XS4 + j * 2],
-                                   L.Z + (item * L.zs + src_row + k0) * 4 + j * 2);
+                                   Zb + (item * L.zs + src_row + k0) * 4 + j * 2);
                 }
                 if (tid < NI) {
                     const int64_t item = n0 / 4 + tid;
@@ -337,7 +405,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                     const int pt = tid >> 2, krow = (tid & 3) * 8 + q;
                     const int64_t item = n0 + pt;
                     if (item < n && krow < valid)
-                        cp_async8(&S.x[stage][pt * XS1 + krow], L.Z + item * L.zs + src_row + k0 + krow);
+                        cp_async8(&S.x[stage][pt * XS1 + krow], Zb + item * L.zs + src_row + k0 + krow);
                 }
                 if (tid < BN) {
                     const int64_t item = n0 + tid;
@@ -444,7 +512,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                                 const uint64_t* key = keys + item * L.KW;
                                 int srow = st.sin_row_off + r;
                                 if (key_bit_cg(key, srow)) {
-                                    double2 p = *reinterpret_cast<const double2*>(L.Z + (item * L.zs + srow) * 4 + comp);
+                                    double2 p = *reinterpret_cast<const double2*>(Zb + (item * L.zs + srow) * 4 + comp);
                                     s0 = p.x; s1 = p.y;
                                 }
                             } else {                      // V @ A_in is in acc (second K segment); add vb
@@ -471,7 +539,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                                     }
                                 }
                             }
-                            *reinterpret_cast<double2*>(L.Z + (item * L.zs + row) * 4 + comp) = make_double2(v0, v1);
+                            *reinterpret_cast<double2*>(Zb + (item * L.zs + row) * 4 + comp) = make_double2(v0, v1);
                         }
                     } else {
 #pragma unroll
@@ -492,7 +560,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                                     if (has_vb) sc = sc + step_vbias(st, shp, r);
                                 } else if (sc_ident) {
                                     int srow = st.sin_row_off + r;
-                                    if (key_bit(keys + item * L.KW, srow)) sc = L.Z[item * L.zs + srow];
+                                    if (key_bit(keys + item * L.KW, srow)) sc = Zb[item * L.zs + srow];
                                 } else if (has_vb) {
                                     sc = step_vbias(st, shp, r);  // V h_in is in acc (second K segment)
                                 }
@@ -501,7 +569,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                                 pre = v + step_bias(st, shp, r);
                             }
                             pre = prec_round(pre, L.fp32);
-                            L.Z[item * L.zs + row] = pre;
+                            Zb[item * L.zs + row] = pre;
                             if (pre > 0.0) {
                                 int lb = row - wbase * 64;
                                 atomicOr(&S.bits[(int)(item - n0)][lb >> 6], (unsigned long long)key_mask(lb));
@@ -705,8 +773,10 @@ void launch_compose_fused(const FusedCompose& F, cudaStream_t s) {
 // face functional of every subnetwork: head_w @ (s ⊙ Z_last) (+ head_b on the offset)
 // reference network.py:440-442
 __global__ void k_face_head(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
-                            int64_t n_cap, int zs, int KW, const SubDev* subs, int n_subs, int shape_w, int fp32) {
+                            int64_t n_cap, int zs, int KW, const SubDev* subs, int n_subs, int shape_w, int fp32,
+                            const unsigned long long* zpar, int64_t zstride) {
     pdl_enter();
+    if (zpar) Z += (int64_t)(*zpar & 1ull) * zstride;
     const int64_t n = dev_count(n_dev, n_cap);
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -773,12 +843,12 @@ __global__ void k_forward_head(const double* Z, uint64_t* keys_base, const unsig
 
 void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
                           int64_t n_cap, int zs, int KW, const void* subs, int n_subs, int shape_w, int fp32,
-                          cudaStream_t s) {
+                          cudaStream_t s, const unsigned long long* zpar, int64_t zstride) {
     int64_t warps = n_cap * n_subs;
     if (warps <= 0) return;
     int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)num_sms() * 8);
     { launch_k(k_face_head, (unsigned)blocks, 256, 0, s, Z, keys, faces, n_dev, n_cap, zs, KW,
-                                                 static_cast<const SubDev*>(subs), n_subs, shape_w, fp32); }
+                                                 static_cast<const SubDev*>(subs), n_subs, shape_w, fp32, zpar, zstride); }
 }
 void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
                              const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,

@@ -288,6 +288,8 @@ static int set_counter(am_engine* e, int which, unsigned long long v) {
     CK(cudaStreamSynchronize(e->stream));
     return AM_OK;
 }
+static bool gather_fuses_input(const am_engine* e);
+
 static HashSet hs(am_engine* e) {
     HashSet H;
     H.table = e->table.p;
@@ -644,8 +646,9 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
         CK(e->Z2.reserve(e->Z.n, s)); CK(e->faces2.reserve(e->faces.n, s));
         CK(e->ckey2.reserve(e->ckey.n, s)); CK(e->changed2.reserve(e->changed.n, s));
     }
-    e->prefix = e->narrow_fused && !e->narrow_check && e->ncomp->nsteps <= kMaxPrefixBuckets &&
-                e->B < (INT64_C(1) << 27);
+    // narrow path, or the per-step path with the gather fused into the input step
+    e->prefix = (e->narrow_fused ? !e->narrow_check : gather_fuses_input(e)) &&
+                (int)e->sdev.size() <= kMaxPrefixBuckets && e->B < (INT64_C(1) << 27);
     if (const char* v = getenv("AM_PREFIX")) e->prefix = e->prefix && atoi(v) != 0;
     if (e->prefix) {
         CK(e->Zi.reserve(2 * e->B * e->zs * 4, s));
@@ -804,16 +807,19 @@ extern "C" int am_engine_reset(am_engine* e) {
 // every hidden step for the items; C = 4 (cells) or 1 (points); n_dev null -> n_cap items
 static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsigned long long* key_off,
                      int32_t* changed, const double* pts, const unsigned long long* n_dev, int64_t n_cap,
-                     size_t first = 0) {
+                     size_t first = 0, const unsigned long long* zpar = nullptr, int64_t zstride = 0,
+                     const unsigned long long* n_step = nullptr) {
     for (size_t s = first; s < e->sdev.size(); s++) {
-        LayerLaunch L;
+        LayerLaunch L{};
+        L.zpar = zpar;
+        L.zstride = zstride;
         L.st = e->sdev[s];
         L.Z = Z;
         L.keys = keys;
         L.key_off = key_off;
         L.changed = changed;
         L.pts = pts;
-        L.n_dev = n_dev;
+        L.n_dev = n_step ? n_step + s : n_dev;
         L.n_cap = n_cap;
         L.KW = e->KW;
         L.zs = e->zs;
@@ -966,7 +972,7 @@ static int launch_iteration(am_engine* e) {
     I.world = e->P.world;
     I.pool_par = e->prefix ? e->pool_par.p : nullptr;
     I.blist = e->blist.p;
-    I.max_share = e->ncomp->nsteps - 1;
+    I.max_share = (int)e->sdev.size() - 1;
     ProbeRecs R;
     R.cand = e->prec_cand.p; R.k = e->prec_k.p; R.pt = e->prec_pt.p;
     for (int q = 0; q < 2; q++) { R.pend_t[q] = e->pend_t[q].p; R.pend_k[q] = e->pend_k[q].p; R.pend_pt[q] = e->pend_pt[q].p; }
@@ -1007,6 +1013,25 @@ static int launch_iteration(am_engine* e) {
             launch_narrow_check(e->Z.p, e->Z2.p, e->faces.p, e->faces2.p, e->ckey.p, e->ckey2.p, e->changed.p,
                                 e->changed2.p, c + C_NR, B, e->NB, e->zs, e->KW, e->dbg.p, s);
         }
+    } else if (fuse_in && e->prefix) {
+        // prefix reuse on the per-step path: gather in bucket order + input step, parents' rows,
+        // then each GEMM step over the items that need it (buckets f < s) and the heads
+        if (tm) cudaEventRecord(e->ev[0], s);
+        LayerLaunch L0 = first_step_launch(e, e->ckey.p, e->changed.p, e->Zi.p, c + C_NR, B);
+        L0.zpar = c + C_ITER;
+        L0.zstride = B * e->zs * 4;
+        launch_gather_input(e->pool.p, e->pool_hint.p, e->queue.p, c, e->batch_pool.p, e->ckey_hint.p,
+                            e->canon_pos.p, L0, s, e->blist.p, (int)e->sdev.size());
+        PrefixRows R{};
+        R.ctr = c;
+        R.nb = (int)e->sdev.size();
+        for (int q = 0; q < R.nb; q++) { R.row_off[q] = e->sdev[q].row_off; R.n_out[q] = e->sdev[q].n_out; }
+        launch_prefix_rows(R, L0, e->batch_pool.p, e->pool_par.p, s);
+        RC(run_steps(e, 4, e->Zi.p, e->ckey.p, nullptr, e->changed.p, nullptr, c + C_NR, B, 1, c + C_ITER, L0.zstride,
+                     c + C_PRE0));
+        launch_face_head_dev(e->Zi.p, e->ckey.p, e->faces.p, c + C_NR, B, e->zs, e->KW, e->subdev.p, e->M,
+                             e->shape_w, e->fp32, s, c + C_ITER, L0.zstride);
+        CK(cudaGetLastError());
     } else if (fuse_in) {
         if (tm) cudaEventRecord(e->ev[0], s);
         launch_gather_input(e->pool.p, e->pool_hint.p, e->queue.p, c, e->batch_pool.p, e->ckey_hint.p,
@@ -1016,7 +1041,8 @@ static int launch_iteration(am_engine* e) {
                             e->ckey_hint.p, e->changed.p, e->canon_pos.p, s);
         if (tm) cudaEventRecord(e->ev[0], s);
     }
-    if (!e->narrow_fused) RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B, fuse_in ? 1 : 0));
+    if (!e->narrow_fused && !(fuse_in && e->prefix))
+        RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B, fuse_in ? 1 : 0));
     if (tm) cudaEventRecord(e->ev[1], s);
     mark(2);
     if (e->canon_fused) {
@@ -1066,7 +1092,7 @@ static int launch_iteration(am_engine* e) {
     if (e->prefix) {
         a.Z = e->Zi.p;
         a.zpar = c + C_ITER; a.zstride = e->B * e->zs * 4; a.emit_par = e->emit_par.p;
-        a.nsteps = e->ncomp->nsteps;
+        a.nsteps = (int)e->sdev.size();
         for (int q = 0; q < a.nsteps; q++) a.step_end[q] = e->sdev[q].row_off + e->sdev[q].n_out;
     }
     if (tm) cudaEventRecord(e->ev[2], s);
@@ -1887,8 +1913,9 @@ extern "C" int am_stats(am_engine* e, double* h) {
     // prefix reuse: composition flops not executed (cells x the DMMA steps taken from parents)
     double skipped = 0, step_flops = 0;
     if (e->prefix)
-        for (int f = 1; f < e->ncomp->nsteps; f++) {
-            step_flops += 2.0 * e->sdev[f].n_out * e->sdev[f].n_in * 4;
+        for (int f = 1; f < (int)e->sdev.size(); f++) {
+            const StepDev& d = e->sdev[f];
+            step_flops += 2.0 * d.n_out * d.n_in * 4 + (d.V && !(d.flags & AM_STEP_SC_FROM_INPUT) ? 2.0 * d.n_out * d.n_sin * 4 : 0.0);
             skipped += (double)e->hctr[C_BKT0 + f] * step_flops;
         }
     h[16] = skipped; h[17] = e->prefix ? 1.0 : 0.0;

@@ -218,6 +218,9 @@ __global__ void k_take(IterState I) {
     if (threadIdx.x < kMaxPrefixBuckets) {
         c[C_BK0 + threadIdx.x] = s_cnt[threadIdx.x];
         c[C_BKT0 + threadIdx.x] += s_cnt[threadIdx.x];
+        unsigned long long pre = 0;   // items of buckets below this one
+        for (int f = 0; f < (int)threadIdx.x; f++) pre += s_cnt[f];
+        c[C_PRE0 + threadIdx.x] = pre;
     }
 }
 

@@ -140,7 +140,13 @@ struct LayerLaunch {
     int grid_cap;         // >0: persistent GEMM grid = grid_cap CTAs per SM
     int shape_w;          // key word holding the item's shape (-1: single-shape engine)
     int fp32;             // fp32 mode: round every composed value to fp32
+    // prefix reuse: Z double-buffered by iteration parity (*zpar & 1) x zstride doubles (null: Z)
+    const unsigned long long* zpar;
+    int64_t zstride;
 };
+__device__ __forceinline__ double* zbase(const LayerLaunch& L) {
+    return L.zpar ? L.Z + (int64_t)(*L.zpar & 1ull) * L.zstride : L.Z;
+}
 
 // fp32 mode: values kept at fp32 precision (round-to-nearest), fp64 otherwise
 __device__ __forceinline__ double prec_round(double v, int fp32) { return fp32 ? (double)__double2float_rn(v) : v; }
@@ -264,7 +270,8 @@ enum Ctr {
     C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_NFLUSH, C_DONE, C_NHEAVY, C_NLIGHT,
     C_BK0,               // [kMaxPrefixBuckets] cells of this iteration's batch per shared-step count
     C_BKT0 = C_BK0 + 12, // [kMaxPrefixBuckets] the same, summed over the march's iterations
-    C_N = C_BKT0 + 12
+    C_PRE0 = C_BKT0 + 12,// [kMaxPrefixBuckets] items of buckets f < s (the items step s composes)
+    C_N = C_PRE0 + 12
 };
 constexpr int kMaxPrefixBuckets = 12;
 
@@ -341,7 +348,15 @@ void launch_take(const IterState& I, cudaStream_t s);
 // k_gather_batch + the first (input) compose step of the batch in one launch (am_compose.cu)
 void launch_gather_input(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                          const unsigned long long* ctr, int32_t* batch_pool, double* ckey_hint, int32_t* canon_pos,
-                         const LayerLaunch& L, cudaStream_t s);
+                         const LayerLaunch& L, cudaStream_t s, const int32_t* blist = nullptr, int nb = 0);
+// prefix reuse on the per-step path (k_prefix_rows): step row table + the bucket counters
+struct PrefixRows {
+    const unsigned long long* ctr;
+    int nb;                       // buckets (= steps)
+    int row_off[12], n_out[12];
+};
+void launch_prefix_rows(const PrefixRows& R, const LayerLaunch& L, const int32_t* batch_pool, const int64_t* pool_par,
+                        cudaStream_t s);
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                          const unsigned long long* ctr, int32_t* batch_pool, int64_t n_cap, int KW, uint64_t* ckey,
                          double* ckey_hint, int32_t* changed, int32_t* canon_pos, cudaStream_t s);
@@ -371,7 +386,7 @@ void launch_open_edges(const int32_t* enr, const int64_t* roff, const int32_t* r
                        unsigned long long* out, cudaStream_t s);
 void launch_face_head_dev(const double* Z, const uint64_t* keys, double* faces, const unsigned long long* n_dev,
                           int64_t n_cap, int zs, int KW, const void* subs, int n_subs, int shape_w, int fp32,
-                          cudaStream_t s);
+                          cudaStream_t s, const unsigned long long* zpar = nullptr, int64_t zstride = 0);
 void launch_forward_head_dev(const double* Z, uint64_t* keys, const unsigned long long* key_off, double* vals,
                              const unsigned long long* n_dev, int64_t n_cap, int zs, int KW, const void* subs,
                              int n_subs, int ensemble, int shape_w, int fp32, cudaStream_t s);

@@ -22,10 +22,15 @@ ap.add_argument("variants", nargs="+")
 ap.add_argument("--repeat", type=int, default=10)
 ap.add_argument("--net", default="90x6")
 ap.add_argument("--seeds", type=int, default=64)
+ap.add_argument("--max-cells", type=int, default=0)
 a = ap.parse_args()
-w, d = (int(x) for x in a.net.split("x"))
-net = synth.geometric_mlp([w] * d, seed=0)
-cfg = marching.MarchConfig(seeds=a.seeds, rng_seed=0, bbox=((-1.2,) * 3, (1.2,) * 3))
+if a.net == "deepsdf":
+    net = synth.deepsdf_mlp(512, 8, 4, seed=0)
+else:
+    w, d = (int(x) for x in a.net.split("x"))
+    net = synth.geometric_mlp([w] * d, seed=0)
+cfg = marching.MarchConfig(seeds=a.seeds, rng_seed=0, bbox=((-1.2,) * 3, (1.2,) * 3),
+                           **({"max_cells": a.max_cells} if a.max_cells else {}))
 T = []
 orig_run = engmod.Engine.run
 
@@ -63,7 +68,9 @@ for rep in range(a.repeat + 1):
             if ref is None:
                 ref = arrs
             same = all(np.array_equal(x, y) for x, y in zip(arrs, ref))
-            print(f"{a.variants[i]}: cells {r.report.cells_visited} bitwise equal to first: {same}", flush=True)
+            st = eng.stats()
+            print(f"{a.variants[i]}: cells {r.report.cells_visited} bitwise equal to first: {same}  "
+                  f"prefix {st['prefix']:.0f} skipped flops {st['prefix_skipped_flops']:.3e}", flush=True)
         else:
             times[i].append(T[-1])
 for v, t in zip(a.variants, times):
