@@ -646,8 +646,11 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
         CK(e->Z2.reserve(e->Z.n, s)); CK(e->faces2.reserve(e->faces.n, s));
         CK(e->ckey2.reserve(e->ckey.n, s)); CK(e->changed2.reserve(e->changed.n, s));
     }
-    // narrow path, or the per-step path with the gather fused into the input step
-    e->prefix = (e->narrow_fused ? !e->narrow_check : gather_fuses_input(e)) &&
+    // narrow path, or the per-step path with the gather fused into the input step where the
+    // composition is heavy enough to repay the extra launch (A/B, BFS ms off -> on: DeepSDF
+    // 512x8 first 1M cells 722 -> 545, 128-wide 108.8 -> 98.5, 64-wide 19.7 -> 21.5, configs[1]
+    // per-step 22.3 -> 23.1)
+    e->prefix = (e->narrow_fused ? !e->narrow_check : gather_fuses_input(e) && e->flops_per_cell >= 5.0e5) &&
                 (int)e->sdev.size() <= kMaxPrefixBuckets && e->B < (INT64_C(1) << 27);
     if (const char* v = getenv("AM_PREFIX")) e->prefix = e->prefix && atoi(v) != 0;
     if (e->prefix) {

@@ -24,8 +24,8 @@ ap.add_argument("--net", default="90x6")
 ap.add_argument("--seeds", type=int, default=64)
 ap.add_argument("--max-cells", type=int, default=0)
 a = ap.parse_args()
-if a.net == "deepsdf":
-    net = synth.deepsdf_mlp(512, 8, 4, seed=0)
+if a.net.startswith("deepsdf"):   # deepsdf (512 wide) or deepsdf:W
+    net = synth.deepsdf_mlp(int(a.net.split(":")[1]) if ":" in a.net else 512, 8, 4, seed=0)
 else:
     w, d = (int(x) for x in a.net.split("x"))
     net = synth.geometric_mlp([w] * d, seed=0)
