@@ -158,7 +158,8 @@ def test_fp32_mode_within_stated_tolerance():
 @pytest.mark.gpu
 @pytest.mark.parametrize("knob", [("AM_PROBE_IN_GRAPH", "1"), ("AM_COMPOSE_FUSED", "1"), ("AM_NEAR_CAP", "8"),
                                   ("AM_TAU_MULT", "0.25"), ("AM_NEAR_REACH", "1"), ("AM_NARROW", "0"),
-                                  ("AM_NARROW_TILE", "2"), ("AM_CANON_FUSED", "0"), ("AM_FACE_ORDER", "1")])
+                                  ("AM_NARROW_TILE", "2"), ("AM_CANON_FUSED", "0"), ("AM_FACE_ORDER", "1"),
+                                  ("AM_PREFIX", "0"), ("AM_NEAR_FUSED", "1")])
 def test_engine_paths_match_oracle(knob, monkeypatch):
     """Every execution path of the engine is bit-exact, not only the default one: the probe stage
     as a conditional graph node, the fused all-steps composition, near-list overflow (streaming
@@ -238,3 +239,38 @@ def test_narrow_and_per_layer_composition_agree_bitwise(precision, monkeypatch):
     np.testing.assert_array_equal(a.nverts, b.nverts)
     np.testing.assert_array_equal(a.verts, b.verts)
     np.testing.assert_array_equal(a.edge_refs, b.edge_refs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["narrow-fp64", "narrow-fp32", "per-step-deepsdf"])
+def test_prefix_reuse_is_bitwise_neutral(case, monkeypatch):
+    """Children composed from their parents' Z rows (prefix reuse, on the narrow and on the
+    per-step path) give the same march, bit for bit, as composing every step; and the reuse
+    really engaged (composition flops skipped)."""
+    from paper_2106_10031_b200 import synth
+    from paper_2106_10031_b200.marching import _ENGINES, clear_engine_cache
+    m = _gpu()
+    if case.startswith("narrow"):
+        net = synth.geometric_mlp([90] * 4, seed=1)
+        cfg = m.MarchConfig(bbox=((0.0, 0.0, 0.0), (0.5, 0.5, 0.5)), seeds=4, rng_seed=5,
+                            precision=case.split("-")[1])
+    else:
+        net = synth.deepsdf_mlp(width=128, depth=8, skip_at=4, seed=2)
+        cfg = m.MarchConfig(bbox=((0.0, 0.0, 0.0), (0.45, 0.45, 0.45)), seeds=4, rng_seed=2)
+    out = {}
+    try:
+        for mode in ("1", "0"):
+            monkeypatch.setenv("AM_PREFIX", mode)
+            clear_engine_cache()
+            out[mode] = m.march(net, cfg)
+            st = next(iter(_ENGINES.values())).stats()
+            if mode == "1":
+                assert st["prefix"] == 1 and st["prefix_skipped_flops"] > 0
+            else:
+                assert st["prefix"] == 0
+    finally:
+        clear_engine_cache()
+    a, b = out["1"], out["0"]
+    assert a.report.cells_visited > 1000
+    for f in ("keys", "nverts", "verts", "edge_nrefs", "edge_refs"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
