@@ -168,7 +168,7 @@ struct am_engine {
     int near_depth = 2;         // AM_NEAR_DEPTH
     bool near_fused = false;    // near lists built by k_compose_narrow (AM_NEAR_FUSED=1; default: k_near)
     DBuf<double> Zi;
-    DBuf<int64_t> pool_par, emit_par;
+    DBuf<int64_t> pool_par, emit_par, queue_par;
     DBuf<int32_t> blist;
     std::unique_ptr<NarrowCompose> ncomp{new NarrowCompose()};   // face-solver reach (tuning: AM_TAU_MULT, AM_NEAR_REACH)
     DBuf<unsigned long long> dbg;   // face-kernel instrumentation counters (AM_FACE_STATS builds)
@@ -300,6 +300,7 @@ static HashSet hs(am_engine* e) {
     H.pool_voff = e->pool_voff.p;
     H.pool_hint = e->pool_hint.p;
     H.pool_par = e->prefix ? e->pool_par.p : nullptr;
+    H.queue_par = e->prefix ? e->queue_par.p : nullptr;
     H.n_pool = e->ctr.p + C_POOL;
     H.cap_pool = e->pool.n / e->KW;
     H.KW = e->KW;
@@ -323,6 +324,7 @@ static int ensure_hash(am_engine* e, int64_t extra, bool sync = true) {
     }
     // a cell is queued once, plus at most once more when deferred (face solver, status 3)
     CK(e->queue.reserve(2 * (e->pool.n / e->KW), e->stream, true, (int64_t)e->hctr[C_QTAIL], &moved));
+    if (e->prefix) CK(e->queue_par.reserve(e->queue.n, e->stream, true, (int64_t)e->hctr[C_QTAIL], &moved));
     if ((int64_t)e->tcap < 2 * need) {
         uint64_t cap = e->tcap ? e->tcap : 1024;
         while ((int64_t)cap < 2 * need) cap <<= 1;
@@ -738,6 +740,7 @@ extern "C" int am_engine_destroy(am_engine* e) {
     e->pool_voff.release(e->stream);
     e->pool_par.release(e->stream);
     e->emit_par.release(e->stream);
+    e->queue_par.release(e->stream);
     e->blist.release(e->stream);
     e->ckey2.release(e->stream);
     e->changed2.release(e->stream);
@@ -973,7 +976,7 @@ static int launch_iteration(am_engine* e) {
     I.cap_pend = e->pend_t[0].n; I.cap_val = e->val_buf.n;
     I.emit_per_cell = emit_per_cell(); I.verts_per_cell = kVertsPerCell; I.refs_per_cell = kRefsPerCell;
     I.world = e->P.world;
-    I.pool_par = e->prefix ? e->pool_par.p : nullptr;
+    I.queue_par = e->prefix ? e->queue_par.p : nullptr;
     I.blist = e->blist.p;
     I.max_share = (int)e->sdev.size() - 1;
     ProbeRecs R;
@@ -1091,10 +1094,10 @@ static int launch_iteration(am_engine* e) {
     a.order = e->face_order ? e->f_order.p : nullptr; a.order_ctr = c + C_NHEAVY;
     a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
     a.tau_grow = e->tau_grow;
-    a.zpar = nullptr; a.zstride = 0; a.emit_par = nullptr; a.nsteps = 0;
+    a.zpar = nullptr; a.zstride = 0; a.emit_par = nullptr; a.queue_par = nullptr; a.nsteps = 0;
     if (e->prefix) {
         a.Z = e->Zi.p;
-        a.zpar = c + C_ITER; a.zstride = e->B * e->zs * 4; a.emit_par = e->emit_par.p;
+        a.zpar = c + C_ITER; a.zstride = e->B * e->zs * 4; a.emit_par = e->emit_par.p; a.queue_par = e->queue_par.p;
         a.nsteps = (int)e->sdev.size();
         for (int q = 0; q < a.nsteps; q++) a.step_end[q] = e->sdev[q].row_off + e->sdev[q].n_out;
     }

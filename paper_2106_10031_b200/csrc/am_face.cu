@@ -1025,7 +1025,9 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
             A.pool_hint[(int64_t)pidx * 4 + 3] = defer_w;
             atomicOr(&A.pool_flags[pidx], kPoolDeferred | kPoolWasDeferred);
             __threadfence();
-            A.queue[atomicAdd(A.q_tail, 1ull)] = pidx;
+            const unsigned long long qi = atomicAdd(A.q_tail, 1ull);
+            A.queue[qi] = pidx;
+            if (A.queue_par) A.queue_par[qi] = 0;
         }
         return;
     }

@@ -85,7 +85,11 @@ __device__ __forceinline__ int32_t upsert_one(const HashSet& H, const uint64_t* 
     __threadfence();
     H.table[pos] = (fp << 33) | (uint64_t)(uint32_t)p;
     *pidx = (int32_t)p;
-    if (queue) queue[atomicAdd(q_tail, 1ull)] = (int32_t)p;
+    if (queue) {
+        const unsigned long long qi = atomicAdd(q_tail, 1ull);
+        queue[qi] = (int32_t)p;
+        if (H.queue_par) H.queue_par[qi] = src_par ? src_par[ci] : 0;
+    }
     return st;
 }
 
@@ -198,14 +202,14 @@ __global__ void k_take(IterState I) {
         s_n = nR;
         s_iter = c[C_ITER];
     }
-    if (!I.pool_par) return;
+    if (!I.queue_par) return;
     // prefix reuse: bucket the batch by the number of composition steps its cells can take from
     // their parents (emitted in the previous iteration; anything else composes in full)
     __syncthreads();
     const long long n = s_n, head = s_head;
     const unsigned long long it = s_iter;
     for (long long b = threadIdx.x; b < n; b += blockDim.x) {
-        const long long w = I.pool_par[I.queue[head + b]];
+        const long long w = I.queue_par[head + b];
         int f = 0;
         if (w != 0 && ((unsigned long long)w >> 32) + 1ull == it) {
             f = (int)(w & 31);
@@ -399,7 +403,7 @@ __global__ void k_route_emitted(const uint64_t* scratch, const unsigned long lon
     }
 }
 
-void launch_take(const IterState& I, cudaStream_t s) { launch_k(k_take, 1, I.pool_par ? 1024 : 32, 0, s, I); }
+void launch_take(const IterState& I, cudaStream_t s) { launch_k(k_take, 1, I.queue_par ? 1024 : 32, 0, s, I); }
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                          const unsigned long long* ctr, int32_t* batch_pool, int64_t n_cap, int KW, uint64_t* ckey,
                          double* ckey_hint, int32_t* changed, int32_t* canon_pos, cudaStream_t s) {

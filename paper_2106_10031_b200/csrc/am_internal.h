@@ -296,6 +296,8 @@ struct HashSet {
     int64_t* pool_voff;   // offset of its validated-neuron list
     double* pool_hint;    // [cap][4] a point on the cell's face polygon + search radius (inf: none)
     int64_t* pool_par;    // [cap] prefix_word of the emitting parent (0: none); null: not kept
+    int64_t* queue_par;   // [queue cap] the same word per queue entry (k_take's bucketing reads it
+                          // coalesced); null: not kept
     unsigned long long* n_pool;  // device counter
     int64_t cap_pool;
     int KW;
@@ -318,7 +320,7 @@ struct IterState {
     int world;
     // prefix reuse (null pool_par: off): the batch's cells are listed per shared-step count
     // (blist[f * B + i], counts in ctr[C_BK0 + f]) for the narrow composition's tiles
-    const int64_t* pool_par;
+    const int64_t* queue_par;   // prefix_word per queue entry (HashSet::queue_par)
     int32_t* blist;
     int max_share;            // largest usable f (nsteps - 1)
 };
@@ -471,6 +473,7 @@ struct FaceArgs {
     const unsigned long long* zpar;
     int64_t zstride;
     int64_t* emit_par;
+    int64_t* queue_par;       // deferral re-queues a cell with no parent word (full composition)
     int nsteps;
     int step_end[12];
 };
