@@ -169,6 +169,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the capped configs[2] measurement")
     ap.add_argument("--deepsdf-cells", type=int, default=1_000_000)
+    ap.add_argument("--no-deepsdf-full", dest="deepsdf_full", action="store_false",
+                    help="skip the complete (uncapped) configs[2] march line in other_configs")
     ap.add_argument("--latent-cells", type=int, default=20_000)
     args = ap.parse_args()
 
@@ -497,6 +499,33 @@ def main():
                              "share_of_march": ds["compose_ms"] / d_ms if d_ms else None},
         }
         del deng
+
+        # configs[2] at full size: the whole ~16 M-cell march (device time, one warm-up march)
+        if args.deepsdf_full:
+            feng = Engine(dnet, bbox=bbox, max_cells=40_000_000)
+
+            def frun():
+                feng.reset()
+                feng.seed(dseeds)
+                return feng.run()
+            frun()
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(feng.stream)
+            fw = frun()
+            f1.record(feng.stream)
+            torch.cuda.synchronize()
+            f_ms = f0.elapsed_time(f1)
+            fc = feng.counts()
+            assert fc["overflow"] == 0 and not fc["capped"], "full DeepSDF march incomplete"
+            fs = feng.stats()
+            others["configs[2]_full"] = {
+                "workload": "DeepSDF-style 3-(512x8)-1, linear skip over layers 1-4, seed 0, fp64, 64 dichotomy "
+                            "seeds; the complete march (no cap)",
+                "cells": int(fc["cells"]), "waves": int(fw), "ms": f_ms, "cells_per_s": fc["cells"] / (f_ms * 1e-3),
+                "prefix_skipped_flops": fs["prefix_skipped_flops"],
+                "timing": "CUDA events on the engine stream around reset + seed + run, after one warm-up march"}
+            del feng
 
         # configs[4]: a batch of 64 latent-conditioned shapes (256-d code folded into the first
         # layer and skip biases of one DeepSDF decoder), one reused engine, per-shape cap

@@ -174,7 +174,6 @@ __global__ void k_gather_input(const uint64_t* pool, const double* pool_hint, co
                                int32_t* canon_pos, LayerLaunch L, const int32_t* blist, int nb) {
     pdl_enter();
     const int64_t n = dev_count(ctr + C_NR, L.n_cap);
-    const int64_t head0 = (int64_t)ctr[C_QHEAD] - n;
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     uint64_t* keys = L.keys;
@@ -185,7 +184,7 @@ __global__ void k_gather_input(const uint64_t* pool, const double* pool_hint, co
             const int f = bucket_of(ctr, nb, b, pos);
             q = blist[(int64_t)f * L.n_cap + pos];
         }
-        const int32_t p = queue[head0 + q];
+        const int32_t p = queue[batch_queue_index(ctr, q)];
         for (int w = lane; w < L.KW; w += 32) keys[b * L.KW + w] = pool[(int64_t)p * L.KW + w];
         if (lane == 0) {
             batch_pool[b] = p;

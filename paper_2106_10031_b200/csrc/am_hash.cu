@@ -157,12 +157,11 @@ void launch_hash_rebuild(const HashSet& H, int64_t n_pool, cudaStream_t s) {
 __global__ void k_take(IterState I) {
     pdl_enter();
     unsigned long long* c = I.ctr;
-    __shared__ long long s_head, s_n;
+    __shared__ long long s_n;
     __shared__ unsigned long long s_iter;
     __shared__ unsigned s_cnt[kMaxPrefixBuckets];
     if (threadIdx.x < kMaxPrefixBuckets) s_cnt[threadIdx.x] = 0u;
     if (threadIdx.x == 0) {
-        s_head = (long long)c[C_QHEAD];
         long long head = (long long)c[C_QHEAD], tail = (long long)c[C_QTAIL];
         long long want = tail - head;
         if (want > I.B) want = I.B;
@@ -197,8 +196,21 @@ __global__ void k_take(IterState I) {
         c[C_NPREC] = 0; c[C_NKEEP] = 0; c[C_NPLOCAL] = 0; c[C_FCURSOR] = 0;
         c[C_NHEAVY] = 0; c[C_NLIGHT] = 0;
         c[C_ITER] += nR > 0 ? 1ull : 0ull;
-        // the batch is queue[head, head + nR): k_gather_batch copies it out (batch_pool)
-        c[C_QHEAD] = (unsigned long long)((long long)c[C_QHEAD] + nR);
+        // the batch: queue[head, head + a) + queue[tail - t, tail) (batch_queue_index); prefix
+        // reuse takes the entries queued since the previous take (children of its batch) from the
+        // tail first, FIFO otherwise
+        long long t = 0;
+        if (I.queue_par) {
+            t = tail - (long long)c[C_QMARK];
+            if (t < 0) t = 0;
+            if (t > nR) t = nR;
+        }
+        const long long a = nR - t;
+        c[C_QA] = (unsigned long long)a;
+        c[C_QB] = (unsigned long long)(tail - t);
+        c[C_QHEAD] = (unsigned long long)(head + a);
+        c[C_QTAIL] = (unsigned long long)(tail - t);
+        c[C_QMARK] = (unsigned long long)(tail - t);
         s_n = nR;
         s_iter = c[C_ITER];
     }
@@ -206,10 +218,10 @@ __global__ void k_take(IterState I) {
     // prefix reuse: bucket the batch by the number of composition steps its cells can take from
     // their parents (emitted in the previous iteration; anything else composes in full)
     __syncthreads();
-    const long long n = s_n, head = s_head;
+    const long long n = s_n;
     const unsigned long long it = s_iter;
     for (long long b = threadIdx.x; b < n; b += blockDim.x) {
-        const long long w = I.queue_par[head + b];
+        const long long w = I.queue_par[batch_queue_index(c, b)];
         int f = 0;
         if (w != 0 && ((unsigned long long)w >> 32) + 1ull == it) {
             f = (int)(w & 31);
@@ -228,18 +240,17 @@ __global__ void k_take(IterState I) {
     }
 }
 
-// batch_pool[b] = queue[head0 + b] (the batch k_take dequeued), ckey[b] = pool[batch_pool[b]];
+// batch_pool[b] = queue[batch_queue_index(b)] (the batch k_take dequeued), ckey[b] = pool[batch_pool[b]];
 // reset per-item flags
 __global__ void k_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                                const unsigned long long* ctr, int32_t* batch_pool, int64_t n_cap, int KW,
                                uint64_t* ckey, double* ckey_hint, int32_t* changed, int32_t* canon_pos) {
     pdl_enter();
     const int64_t n = dev_count(ctr + C_NR, n_cap);
-    const int64_t head0 = (int64_t)ctr[C_QHEAD] - n;
     GRID_STRIDE(t, n * KW) {
         int64_t b = t / KW;
         int w = (int)(t - b * KW);
-        const int32_t p = queue[head0 + b];
+        const int32_t p = queue[batch_queue_index(ctr, b)];
         ckey[t] = pool[(int64_t)p * KW + w];
         if (w == 0) {
             batch_pool[b] = p;

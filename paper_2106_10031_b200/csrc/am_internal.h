@@ -268,12 +268,21 @@ enum Ctr {
     C_POOL = 0, C_CELLS, C_VERTS, C_REFS, C_OVF0, C_OVF1, C_CAPPED, C_TOTAL, C_QHEAD, C_QTAIL, C_NR, C_NX,
     C_NF, C_NPROBE, C_NEMIT, C_NLOCAL, C_NOUT, C_STALL, C_ITER, C_LIST, C_OPEN, C_NPREC, C_NPEND, C_PPAR,
     C_NKEEP, C_NVAL, C_NPLOCAL, C_PROBES_TOTAL, C_PREC_TOTAL, C_FCURSOR, C_NFLUSH, C_DONE, C_NHEAVY, C_NLIGHT,
+    // the batch k_take dequeued: batch items [0, QA) = queue[QHEAD - QA ..), items [QA, nR) =
+    // queue[QB ..) (prefix reuse takes the entries queued since the previous take from the
+    // tail, so children meet their parents' rows; QMARK = the tail after that take)
+    C_QA, C_QB, C_QMARK,
     C_BK0,               // [kMaxPrefixBuckets] cells of this iteration's batch per shared-step count
     C_BKT0 = C_BK0 + 12, // [kMaxPrefixBuckets] the same, summed over the march's iterations
     C_PRE0 = C_BKT0 + 12,// [kMaxPrefixBuckets] items of buckets f < s (the items step s composes)
     C_N = C_PRE0 + 12
 };
 constexpr int kMaxPrefixBuckets = 12;
+// queue index of batch item b of the current iteration (see C_QA)
+__device__ __forceinline__ int64_t batch_queue_index(const unsigned long long* ctr, int64_t b) {
+    const int64_t A = (int64_t)ctr[C_QA];
+    return b < A ? (int64_t)ctr[C_QHEAD] - A + b : (int64_t)ctr[C_QB] + (b - A);
+}
 
 // Prefix reuse of the narrow composition.  A cell emitted by the face stage differs from its
 // parent only in the flipped neuron(s): with the first flip in step f, Z rows of steps 0..f are

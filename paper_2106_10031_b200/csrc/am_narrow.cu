@@ -134,7 +134,7 @@ __device__ __forceinline__ bool fabs_gt(double x, double t) {
 //   MI 1, NJ 2: 6 x 1 warps of 16 x 16, 4 cells
 //   MI 1, NJ 1: 6 x 1 warps of 16 x 8,  2 cells (narrow waves: spread over more SMs)
 template <int FP32, int MI, int NJ>
-__device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, int64_t n, int64_t head0,
+__device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, int64_t n,
                                         uint32_t& gbox, bool prof, unsigned long long& tprev, double* Zc,
                                         const double* Zp) {
     constexpr int WR = MI == 2 ? 3 : 6, WC = NCW / WR, RB = 16 * MI, CB = 8 * NJ;
@@ -162,7 +162,7 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
             uint64_t v = 0;
             if (c < ncell) {
                 const int64_t b = P.prefix ? (int64_t)P.blist[(int64_t)fsh * P.n_cap + pos0 + c] : pos0 + c;
-                const int32_t p = P.queue[head0 + b];
+                const int32_t p = P.queue[batch_queue_index(P.ctr, b)];
                 v = P.pool[(int64_t)p * KW + w];
                 if (w == 0) {
                     S.bidx[c] = (int32_t)b;
@@ -511,7 +511,6 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t n = dev_count(P.n_dev, P.n_cap);
-    const int64_t head0 = (int64_t)P.ctr[C_QHEAD] - n;
     uint32_t gbox = 0;
     const bool prof = (P.dbg & 8) && P.prof && threadIdx.x == 0;
     unsigned long long tprev = prof ? clock64() : 0;
@@ -536,9 +535,9 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
             }
         }
     }
-    if (nc == 8) consume<FP32, 2, 2>(S, P, n, head0, gbox, prof, tprev, Zc, Zp);
-    else if (nc == 4) consume<FP32, 1, 2>(S, P, n, head0, gbox, prof, tprev, Zc, Zp);
-    else consume<FP32, 1, 1>(S, P, n, head0, gbox, prof, tprev, Zc, Zp);
+    if (nc == 8) consume<FP32, 2, 2>(S, P, n, gbox, prof, tprev, Zc, Zp);
+    else if (nc == 4) consume<FP32, 1, 2>(S, P, n, gbox, prof, tprev, Zc, Zp);
+    else consume<FP32, 1, 1>(S, P, n, gbox, prof, tprev, Zc, Zp);
 }
 
 // debug (AM_NARROW_CHECK=1): compare the fused kernel's outputs with the per-step path's
