@@ -66,7 +66,7 @@ typedef struct {
     double probe_delta;   /* 1e-7  neighbour probe step       (reference marching.py:67) */
     int64_t max_cells;    /* visited-cell cap                 (reference marching.py:59) */
     int64_t batch_cells;  /* cells composed per batch (0 = size from mem_budget) */
-    int64_t mem_budget;   /* bytes for per-batch plane buffers (0 = 2 GiB) */
+    int64_t mem_budget;   /* bytes for per-batch buffers (0 = 4 GiB; 32 GiB when a cell composes >= 2 MFLOP) */
     int32_t rank, world;  /* state ownership: owner(state) = (hash(state) >> 7) % world */
     int32_t n_shapes;     /* > 1: batch of same-architecture shapes marched together (the key
                            * gains a trailing shape word; see am_engine_set_shape_params) */

@@ -105,7 +105,7 @@ class MarchConfig:
     unique_planes_limit: int = 3000
     probe_delta: float = PROBE_DELTA
     batch_cells: int = 0        # GPU: cells composed per batch (0 = from memory budget)
-    mem_budget: int = 0         # GPU: bytes for per-batch plane buffers (0 = 2 GiB)
+    mem_budget: int = 0         # GPU: bytes for per-batch buffers (0 = 4 GiB; 32 GiB for >= 2 MFLOP/cell nets)
     precision: str = "fp64"     # "fp32": fp32-precision planes (pair with FP32_TOLERANCES)
 
     def __post_init__(self):
