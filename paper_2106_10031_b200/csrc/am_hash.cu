@@ -220,15 +220,26 @@ __global__ void k_take(IterState I) {
     __syncthreads();
     const long long n = s_n;
     const unsigned long long it = s_iter;
-    for (long long b = threadIdx.x; b < n; b += blockDim.x) {
-        const long long w = I.queue_par[batch_queue_index(c, b)];
-        int f = 0;
-        if (w != 0 && ((unsigned long long)w >> 32) + 1ull == it) {
-            f = (int)(w & 31);
-            if (f > I.max_share) f = I.max_share;
+    const long long qa = (long long)c[C_QA], q0 = (long long)c[C_QHEAD] - qa, qb = (long long)c[C_QB];
+    const int lane = threadIdx.x & 31;
+    for (long long b0 = threadIdx.x - lane; b0 < n; b0 += blockDim.x) {   // warp-uniform trip count
+        const long long b = b0 + lane;
+        int f = -1;
+        if (b < n) {
+            const long long w = I.queue_par[b < qa ? q0 + b : qb + (b - qa)];
+            f = 0;
+            if (w != 0 && ((unsigned long long)w >> 32) + 1ull == it) {
+                f = (int)(w & 31);
+                if (f > I.max_share) f = I.max_share;
+            }
         }
-        const unsigned pos = atomicAdd(&s_cnt[f], 1u);
-        I.blist[(long long)f * I.B + pos] = (int32_t)b;
+        // one shared-memory atomic per distinct bucket of the warp
+        const unsigned peers = __match_any_sync(0xffffffffu, f);
+        const int leader = __ffs(peers) - 1;
+        unsigned base = 0;
+        if (lane == leader && f >= 0) base = atomicAdd(&s_cnt[f], (unsigned)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (f >= 0) I.blist[(long long)f * I.B + base + __popc(peers & ((1u << lane) - 1u))] = (int32_t)b;
     }
     __syncthreads();
     if (threadIdx.x < kMaxPrefixBuckets) {
