@@ -166,6 +166,7 @@ struct am_engine {
     // listed per shared-step bucket
     bool prefix = false;
     int near_depth = 2;         // AM_NEAR_DEPTH
+    bool narrow_snake = true;   // AM_NARROW_SNAKE
     bool near_fused = false;    // near lists built by k_compose_narrow (AM_NEAR_FUSED=1; default: k_near)
     DBuf<double> Zi;
     DBuf<int64_t> pool_par, emit_par, queue_par;
@@ -674,6 +675,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // (BFS 18.58 vs 18.27 ms): 12 warps per SM stream the tile's rows at the end of every tile,
     // where k_near keeps 32 warps per SM of row loads in flight
     if (const char* v = getenv("AM_NEAR_DEPTH")) e->near_depth = atoi(v);
+    if (const char* v = getenv("AM_NARROW_SNAKE")) e->narrow_snake = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_FUSED"))
         e->near_fused = e->narrow_fused && !e->face_order && !e->narrow_check && atoi(v) != 0;
     if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
@@ -1011,6 +1013,7 @@ static int launch_iteration(am_engine* e) {
         N.Z = e->prefix ? e->Zi.p : e->Z.p; N.keys = e->ckey.p; N.faces = e->faces.p; N.changed = e->changed.p;
         N.prefix = e->prefix; N.zstride = e->B * e->zs * 4; N.pool_par = e->pool_par.p; N.blist = e->blist.p;
         N.near_fused = e->near_fused; N.NB = e->NB;
+        N.snake = e->prefix && e->narrow_snake;
         N.near_n = e->near_n.p; N.near_flags = e->near_flags.p; N.near_id = e->near_id.p; N.near_row = e->near_row.p;
         N.near_cap = e->near_cap; N.near_reach = e->near_reach; N.tol_cell = e->P.tol_cell;
         N.tol_onplane = e->P.tol_onplane; N.probe_delta = e->P.probe_delta;

@@ -218,6 +218,7 @@ struct NarrowCompose {
     // half), tiles are formed per bucket of blist (IterState), parents' rows read from the
     // other half
     int prefix;
+    int snake;                         // boustrophedon tile order (AM_NARROW_SNAKE; with prefix)
     int64_t zstride;
     const int64_t* pool_par;
     const int32_t* blist;

@@ -128,6 +128,14 @@ __device__ __forceinline__ bool fabs_gt(double x, double t) {
     return ax > (unsigned long long)__double_as_longlong(t) && ax <= 0x7ff0000000000000ull;
 }
 
+// the CTA's k-th tile: round-robin, or (P.snake, with the tiles ordered costliest first by the
+// prefix buckets) boustrophedon -- odd rounds run backwards, so the CTAs that drew the full-chain
+// tiles of bucket 0 draw the cheapest ones next
+__device__ __forceinline__ int64_t tile_of(const NarrowCompose& P, int64_t k) {
+    const int64_t g = gridDim.x;
+    return k * g + ((P.snake && (k & 1)) ? g - 1 - (int64_t)blockIdx.x : (int64_t)blockIdx.x);
+}
+
 // The consumer warps' tile loop for one tile width: MI 16-row fragments x NJ 8-column fragments
 // per warp; 6 warps = WR row blocks x WC column blocks; a tile is NC = WC * NJ * 2 cells.
 //   MI 2, NJ 2: 3 x 2 warps of 32 x 16, 8 cells (wide waves)
@@ -152,7 +160,9 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
     const bool shaped = P.shape_w >= 0;   // batch of shapes: biases per cell's shape
 #define PROF(i) do { if (prof) { unsigned long long tn = clock64(); atomicAdd(&P.prof[i], tn - tprev); tprev = tn; } } while (0)
 
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int64_t k = 0; k * gridDim.x < ntiles; k++) {
+        const int64_t t = tile_of(P, k);
+        if (t >= ntiles) continue;
         int fsh, ncell;
         long long pos0;
         T.locate(t, NC, fsh, pos0, ncell);
@@ -491,7 +501,9 @@ __global__ void __launch_bounds__(NT, CPS) k_compose_narrow(const __grid_constan
         long long pos0;
         T.locate(blockIdx.x, nc, f0, pos0, nc0);
         bool first = f0 == 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int64_t k = 0; k * gridDim.x < ntiles; k++) {
+            const int64_t t = tile_of(P, k);
+            if (t >= ntiles) continue;
             int f, ncell;
             long long pos;
             T.locate(t, nc, f, pos, ncell);
