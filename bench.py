@@ -393,7 +393,7 @@ def main():
         e_times, m_times = [], []
         h2d = d2h = 0
         from paper_2106_10031_b200.network import to_blob
-        for _ in range(max(1, min(args.steps, 3))):
+        for _ in range(max(3, min(args.steps, 10))):
             flush_l2(flush)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
