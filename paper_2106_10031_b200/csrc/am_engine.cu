@@ -167,6 +167,7 @@ struct am_engine {
     bool prefix = false;
     int near_depth = 2;         // AM_NEAR_DEPTH
     bool narrow_snake = true;   // AM_NARROW_SNAKE
+    bool canon_in_narrow = false;   // canonical insert + frontier in k_compose_narrow (AM_CANON_IN_NARROW)
     bool near_fused = false;    // near lists built by k_compose_narrow (AM_NEAR_FUSED=1; default: k_near)
     DBuf<double> Zi;
     DBuf<int64_t> pool_par, emit_par, queue_par;
@@ -679,6 +680,10 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_NEAR_FUSED"))
         e->near_fused = e->narrow_fused && !e->face_order && !e->narrow_check && atoi(v) != 0;
     if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
+    // canonical insert + frontier in k_compose_narrow's tile epilogue (AM_CANON_IN_NARROW=1):
+    // correct, but slower on configs[1] (BFS 18.48 vs 17.99 ms)
+    if (const char* v = getenv("AM_CANON_IN_NARROW"))
+        e->canon_in_narrow = e->narrow_fused && e->canon_fused && atoi(v) != 0;
     // deferral re-composes the deferred cells: worth it where the face solve dominates (narrow
     // nets; configs[1] 19.75 -> 18.85 ms), not where composition does (DeepSDF 512x8: 0.724 ->
     // 0.747 s for the first 1 M cells)
@@ -1014,6 +1019,10 @@ static int launch_iteration(am_engine* e) {
         N.prefix = e->prefix; N.zstride = e->B * e->zs * 4; N.pool_par = e->pool_par.p; N.blist = e->blist.p;
         N.near_fused = e->near_fused; N.NB = e->NB;
         N.snake = e->prefix && e->narrow_snake;
+        N.canon_fused = e->canon_in_narrow;
+        N.H = H; N.rank = e->P.rank; N.world = e->P.world; N.outbox = e->outbox.p; N.n_out = c + C_NOUT;
+        N.status2 = e->status2.p; N.slot2 = e->slot2.p; N.canon_pool = e->canon_pool.p; N.f_items = e->f_items.p;
+        N.f_pool = e->f_pool.p; N.max_cells = (long long)e->P.max_cells;
         N.near_n = e->near_n.p; N.near_flags = e->near_flags.p; N.near_id = e->near_id.p; N.near_row = e->near_row.p;
         N.near_cap = e->near_cap; N.near_reach = e->near_reach; N.tol_cell = e->P.tol_cell;
         N.tol_onplane = e->P.tol_onplane; N.probe_delta = e->P.probe_delta;
@@ -1061,7 +1070,9 @@ static int launch_iteration(am_engine* e) {
         RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, c + C_NR, B, fuse_in ? 1 : 0));
     if (tm) cudaEventRecord(e->ev[1], s);
     mark(2);
-    if (e->canon_fused) {
+    if (e->narrow_fused && e->canon_in_narrow) {
+        mark(3);   // done in k_compose_narrow's tile epilogue
+    } else if (e->canon_fused) {
         launch_canon_frontier(H, e->ckey.p, e->changed.p, e->batch_pool.p, c + C_NR, B, e->P.rank, e->P.world,
                               e->outbox.p, c + C_NOUT, e->canon_pos.p, e->status2.p, e->slot2.p, e->canon_pool.p,
                               e->ckey_hint.p, e->f_items.p, e->f_pool.p, c, (long long)e->P.max_cells, s);

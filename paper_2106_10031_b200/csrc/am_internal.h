@@ -185,6 +185,24 @@ struct FusedCompose {
     int n_subs;
 };
 void launch_compose_fused(const FusedCompose& F, cudaStream_t s);
+// hash set (am_hash.cu)
+struct HashSet {
+    uint64_t* table;      // slots
+    uint64_t mask;        // capacity - 1
+    uint64_t* pool;       // [cap_pool][KW]
+    uint32_t* pool_flags; // bit0 visited cell, bit1 composed, bit2 deferred (queued again, already
+                          // counted as visited), bit3 was deferred once
+    int32_t* pool_vn;     // validated-neuron count of a visited cell (-1: no face yet)
+    int64_t* pool_voff;   // offset of its validated-neuron list
+    double* pool_hint;    // [cap][4] a point on the cell's face polygon + search radius (inf: none)
+    int64_t* pool_par;    // [cap] prefix_word of the emitting parent (0: none); null: not kept
+    int64_t* queue_par;   // [queue cap] the same word per queue entry (k_take's bucketing reads it
+                          // coalesced); null: not kept
+    unsigned long long* n_pool;  // device counter
+    int64_t cap_pool;
+    int KW;
+};
+
 // whole composition of an iteration (gather + every step + face head) in one launch, for plain
 // dense networks of width <= 96 (am_narrow.cu k_compose_narrow)
 constexpr int kMaxNarrowSteps = 12;
@@ -232,6 +250,19 @@ struct NarrowCompose {
     int near_cap;
     double near_reach, tol_cell, tol_onplane, probe_delta;
     double lo[3], hi[3];
+    // canonical insert + frontier of the tile's cells in its epilogue (canon_fused != 0;
+    // am_hashset.cuh canon_frontier_one: k_canon_frontier's work without its launch)
+    int canon_fused;
+    HashSet H;
+    int rank, world;
+    uint64_t* outbox;
+    unsigned long long* n_out;
+    int32_t* status2;
+    uint64_t* slot2;
+    int32_t* canon_pool;
+    int32_t* f_items;
+    int32_t* f_pool;
+    long long max_cells;
 };
 // sharded march exchange (am_shard.cu)
 constexpr int kHdrWords = 8;
@@ -295,23 +326,6 @@ __host__ __device__ __forceinline__ long long prefix_word(unsigned long long ite
     return (long long)((iter << 32) | ((unsigned long long)item << 5) | (unsigned long long)f);
 }
 
-// hash set (am_hash.cu)
-struct HashSet {
-    uint64_t* table;      // slots
-    uint64_t mask;        // capacity - 1
-    uint64_t* pool;       // [cap_pool][KW]
-    uint32_t* pool_flags; // bit0 visited cell, bit1 composed, bit2 deferred (queued again, already
-                          // counted as visited), bit3 was deferred once
-    int32_t* pool_vn;     // validated-neuron count of a visited cell (-1: no face yet)
-    int64_t* pool_voff;   // offset of its validated-neuron list
-    double* pool_hint;    // [cap][4] a point on the cell's face polygon + search radius (inf: none)
-    int64_t* pool_par;    // [cap] prefix_word of the emitting parent (0: none); null: not kept
-    int64_t* queue_par;   // [queue cap] the same word per queue entry (k_take's bucketing reads it
-                          // coalesced); null: not kept
-    unsigned long long* n_pool;  // device counter
-    int64_t cap_pool;
-    int KW;
-};
 // per-item outputs are indexed by source item ci (idx[i] or i): status 1 new / 0 present,
 // slot (new), dup_ref (present: pool index, or -2 - launch index of the in-flight winner)
 void launch_hash_upsert(const HashSet& H, const uint64_t* src, const int32_t* idx, const unsigned long long* n_dev,

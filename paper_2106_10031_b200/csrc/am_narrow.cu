@@ -29,6 +29,7 @@
 #include <algorithm>
 
 #include "am_internal.h"
+#include "am_hashset.cuh"
 #include "am_near.cuh"
 #include "am_ptx.cuh"
 
@@ -394,7 +395,22 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
             P.keys[(int64_t)S.bidx[c] * KW + w] = S.key[c][w];
         }
         if (tid < ncell) P.changed[S.bidx[tid]] = S.changed[tid];
+        // canonical insert + frontier (k_canon_frontier's work): another CTA's inserter may compare
+        // against this tile's key rows as soon as a slot marker is published, so they are made
+        // visible device-wide first; the per-cell values are read before the barrier (the next
+        // tile's gather rewrites them)
+        int32_t cf_b = 0, cf_ch = 0;
+        if (P.canon_fused) {
+            bool anych = false;   // only a changed key is inserted (and read by other CTAs)
+            for (int c = 0; c < ncell; c++) anych |= S.changed[c] != 0;
+            if (anych) __threadfence();
+            if (tid < ncell) { cf_b = S.bidx[tid]; cf_ch = S.changed[tid]; }
+        }
         bar_sync(1, NCT);
+        if (P.canon_fused && tid < ncell)
+            canon_frontier_one(P.H, P.keys, cf_ch, P.batch_pool[cf_b], cf_b, P.rank, P.world, P.outbox, P.n_out,
+                               P.canon_pos, P.status2, P.slot2, P.canon_pool, P.ckey_hint, P.f_items, P.f_pool,
+                               const_cast<unsigned long long*>(P.ctr), P.max_cells);
         PROF(5);
         if (P.near_fused) {
             // ---- near lists of the tile's cells (the face solver's k_near), while their rows are
