@@ -95,20 +95,27 @@ def sample_seeds(eng, count: int, bbox, scheme: str = "dichotomy", rng_seed: int
         xn_f = np.zeros((count, 3))
         have = np.zeros(count, dtype=bool)
         pending = np.arange(count)
-        for rnd in range(retry_budget):
-            if not len(pending):
-                break
-            pts = _sample_round(rng_seed, pending, rnd, lo, hi)
-            vals = eng.forward(pts.reshape(-1, 3)).cpu().numpy().reshape(len(pending), 64)
-            # first positive / first negative sample of each stream (reference seeding.py:150-156)
-            pm, nm = vals > 0.0, vals < 0.0
-            ok = pm.any(axis=1) & nm.any(axis=1)
-            rows = np.flatnonzero(ok)
-            idx = pending[rows]
-            xp_f[idx] = pts[rows, pm.argmax(axis=1)[rows]]
-            xn_f[idx] = pts[rows, nm.argmax(axis=1)[rows]]
-            have[idx] = True
-            pending = pending[~ok]
+        rnd = 0
+        while rnd < retry_budget and len(pending):
+            # the next S retry rounds of every pending stream in one forward: a stream's k-th block
+            # is fixed by (rng_seed, stream, k), so evaluating blocks a stream will not need
+            # changes nothing, and the rounds are then replayed in order on the host
+            S = min(4 if rnd == 0 else 8, retry_budget - rnd)
+            blocks = [_sample_round(rng_seed, pending, rnd + k, lo, hi) for k in range(S)]
+            vals = eng.forward(np.concatenate(blocks).reshape(-1, 3)).cpu().numpy().reshape(S, len(pending), 64)
+            still = np.ones(len(pending), dtype=bool)
+            for k in range(S):
+                # first positive / first negative sample of each stream (reference seeding.py:150-156)
+                pm, nm = vals[k] > 0.0, vals[k] < 0.0
+                ok = still & pm.any(axis=1) & nm.any(axis=1)
+                rows = np.flatnonzero(ok)
+                idx = pending[rows]
+                xp_f[idx] = blocks[k][rows, pm.argmax(axis=1)[rows]]
+                xn_f[idx] = blocks[k][rows, nm.argmax(axis=1)[rows]]
+                have[idx] = True
+                still &= ~ok
+            pending = pending[still]
+            rnd += S
         order = np.flatnonzero(have)
         if len(order):
             pts = eng.dichotomy(xp_f[order], xn_f[order], eps, seed_tol).cpu().numpy()
