@@ -167,6 +167,11 @@ struct am_engine {
     bool prefix = false;
     int near_depth = 2;         // AM_NEAR_DEPTH
     bool narrow_snake = true;   // AM_NARROW_SNAKE
+    // point forwards through k_forward_narrow on the narrow path (AM_FORWARD_NARROW=1): bitwise
+    // equal to the per-layer kernels but not faster (4096 trigger samples 0.114 vs 0.123 ms, the
+    // configs[1] BFS with its probe forwards 17.90 vs 17.71 ms): a 32-point tile walking every
+    // layer is as long a chain as the per-layer launches
+    bool forward_narrow = false;
     bool canon_in_narrow = false;   // canonical insert + frontier in k_compose_narrow (AM_CANON_IN_NARROW)
     bool near_fused = false;    // near lists built by k_compose_narrow (AM_NEAR_FUSED=1; default: k_near)
     DBuf<double> Zi;
@@ -677,6 +682,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // where k_near keeps 32 warps per SM of row loads in flight
     if (const char* v = getenv("AM_NEAR_DEPTH")) e->near_depth = atoi(v);
     if (const char* v = getenv("AM_NARROW_SNAKE")) e->narrow_snake = atoi(v) != 0;
+    if (const char* v = getenv("AM_FORWARD_NARROW")) e->forward_narrow = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_FUSED"))
         e->near_fused = e->narrow_fused && !e->face_order && !e->narrow_check && atoi(v) != 0;
     if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
@@ -901,6 +907,17 @@ static int compose(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, do
 
 static int forward(am_engine* e, const double* pts, double* vals, uint64_t* keys, const unsigned long long* key_off,
                    double* Zw, const unsigned long long* n_dev, int64_t n_cap) {
+    if (e->narrow_fused && e->forward_narrow && !key_off) {
+        // narrow plain nets: every layer + head in one launch (bitwise equal to the per-layer path)
+        NarrowCompose& N = *e->ncomp;
+        for (int q = 0; q < N.nsteps; q++) N.st[q] = e->sdev[q];
+        N.subs = reinterpret_cast<const SubDev*>(e->subdev.p);
+        N.KW = e->KW; N.shape_w = e->shape_w; N.fp32 = e->fp32;
+        ForwardArgs F{pts, vals, keys, n_dev, n_cap};
+        launch_forward_narrow(N, F, e->stream);
+        CK(cudaGetLastError());
+        return AM_OK;
+    }
     RC(run_steps(e, 1, Zw, keys, key_off, nullptr, pts, n_dev, n_cap));
     launch_forward_head_dev(Zw, keys, key_off, vals, n_dev, n_cap, e->zs, e->KW, e->subdev.p, e->M, e->ensemble,
                             e->shape_w, e->fp32,

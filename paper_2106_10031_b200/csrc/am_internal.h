@@ -264,6 +264,15 @@ struct NarrowCompose {
     int32_t* f_pool;
     long long max_cells;
 };
+// point forward on the narrow path (am_narrow.cu k_forward_narrow)
+struct ForwardArgs {
+    const double* pts;                 // [n][3]
+    double* vals;                      // [n] (may be null)
+    uint64_t* keys;                    // [n][KW]: in, the shape word (zeroed keys); out, the state bits
+    const unsigned long long* n_dev;   // device count (null: n_cap)
+    int64_t n_cap;
+};
+void launch_forward_narrow(const NarrowCompose& P, const ForwardArgs& F, cudaStream_t s);
 // sharded march exchange (am_shard.cu)
 constexpr int kHdrWords = 8;
 void launch_shard_pack(uint64_t* outbox, unsigned long long* ctr, int KW, int world, int64_t cap,

@@ -616,6 +616,216 @@ bool narrow_compose_ok(const StepDev* st, int nsteps, int n_subs, int KW) {
     return true;
 }
 
+// ---------------------------------------------------------------------------------------
+// Point forward of the same narrow networks in one launch (the trigger's samples, bisection
+// midpoints, seed refinement and the BFS's exact probe evaluations): a CTA walks tiles of 32
+// points (32 columns) through every layer with the activations in shared memory, W streamed by
+// the same producer-warp TMA ring.  Per element the arithmetic is the per-layer path's
+// (k_input_step<1> / k_gemm_step<1, 64> / k_forward_head: DMMA accumulation in the same K order,
+// + bias, relu by the sign bit, the head's lane-strided sums and shuffle tree), so values and
+// state bits agree bit for bit with it.
+constexpr int FP = 32;   // points per tile
+struct __align__(1024) ForwardSmem {
+    double w[NSB][NR * KB];
+    double act[2][NR * AS];
+    double x[FP][3];
+    uint64_t key[FP][KWMAX];
+    double hw[NR];
+    uint64_t full[NSB], empty[NSB];
+};
+
+template <int FP32>
+__global__ void __launch_bounds__(NT, CPS) k_forward_narrow(const __grid_constant__ NarrowCompose P,
+                                                            const __grid_constant__ ForwardArgs F) {
+    extern __shared__ uint8_t smem_raw[];
+    ForwardSmem& S = *reinterpret_cast<ForwardSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ns = P.nsteps, KW = P.KW;
+    if (tid == 0) {
+        for (int i = 0; i < NSB; i++) {
+            mbar_init(&S.full[i], 1);
+            mbar_init(&S.empty[i], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < 2 * NR * AS; i += NT) (&S.act[0][0])[i] = 0.0;
+    for (int r = tid; r < P.subs->last_n; r += NT) S.hw[r] = P.subs->hw[r];
+    __syncthreads();
+    int tile_boxes = 0;
+    for (int s = 1; s < ns; s++) tile_boxes += (P.st[s].n_in + KB - 1) / KB;
+
+    if (warp == NCW) {   // producer: every tile streams the W boxes of steps 1..ns-1
+        if (lane != 0) return;
+        uint32_t g = 0;
+        auto issue = [&](int s, int b) {
+            const int slot = g % NSB;
+            if (g >= NSB) mbar_wait(&S.empty[slot], ((g / NSB) - 1) & 1);
+            mbar_expect_tx(&S.full[slot], NR * KB * sizeof(double));
+            tma_load_2d(S.w[slot], &P.tm[s], &S.full[slot], b * KB, 0);
+            g++;
+        };
+        int ps = 1, pb = 0;
+        const int pre = NSB < tile_boxes ? NSB : tile_boxes;
+        for (int i = 0; i < pre; i++) {
+            issue(ps, pb);
+            if (++pb == (P.st[ps].n_in + KB - 1) / KB) { pb = 0; ps++; }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        const int64_t n = dev_count(F.n_dev, F.n_cap);
+        const int64_t ntiles = (n + FP - 1) / FP;
+        if ((int64_t)blockIdx.x >= ntiles) {
+            for (uint32_t i = 0; i < g; i++) mbar_wait(&S.full[i % NSB], (i / NSB) & 1);
+            return;
+        }
+        bool first = true;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int s = 1; s < ns; s++) {
+                const int nb = (P.st[s].n_in + KB - 1) / KB;
+                for (int b = 0; b < nb; b++) {
+                    if (first && (s < ps || (s == ps && b < pb))) continue;
+                    issue(s, b);
+                }
+            }
+            first = false;
+        }
+        return;
+    }
+
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int64_t n = dev_count(F.n_dev, F.n_cap);
+    const int64_t ntiles = (n + FP - 1) / FP;
+    constexpr int MI = 2, NJ = 2, WR = 3, RB = 32, CB = 16;
+    const int g = lane >> 2, tq = lane & 3;
+    const int wm = warp % WR, wn = warp / WR;
+    const int pg = ((g & 3) << 1) | (g >> 2);
+    uint32_t gbox = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t p0 = t * FP;
+        const int np = (int)(n - p0 < FP ? n - p0 : FP);
+        // ---- points and key rows (the shape word, if any, comes with the zeroed keys)
+        for (int q = tid; q < FP * 3; q += NCT) {
+            const int c = q / 3;
+            S.x[c][q - c * 3] = c < np ? F.pts[(p0 + c) * 3 + (q - c * 3)] : 0.0;
+        }
+        for (int q = tid; q < FP * KW; q += NCT) {
+            const int c = q / KW, w = q - c * KW;
+            S.key[c][w] = (c < np && w == P.shape_w) ? F.keys[(p0 + c) * KW + w] : 0ull;
+        }
+        bar_sync(1, NCT);
+        // ---- step 0 (k_input_step<1>'s input_elem): pre = x . W_1[r] + b_1[r]
+        {
+            const StepDev& st = P.st[0];
+            for (int idx = tid; idx < np * st.n_out; idx += NCT) {
+                const int c = idx / st.n_out, r = idx - c * st.n_out;
+                const double* w = st.W + (int64_t)r * st.ldw;
+                const double acc = (S.x[c][0] * w[0] + S.x[c][1] * w[1]) + S.x[c][2] * w[2];
+                const double pre = prec_round(acc + step_bias(st, item_shape(S.key[c], P.shape_w), r), FP32);
+                const int row = st.row_off + r;
+                if (pre > 0.0) atomicOr(reinterpret_cast<unsigned long long*>(&S.key[c][row >> 6]), key_mask(row));
+                S.act[0][r * AS + c] = pre > 0.0 ? pre : 0.0;
+            }
+            bar_sync(1, NCT);
+        }
+        int cur = 0;
+        for (int s = 1; s < ns; s++) {
+            const StepDev& st = P.st[s];
+            const int nb = (st.n_in + KB - 1) / KB;
+            double acc[MI][NJ][4];
+#pragma unroll
+            for (int i = 0; i < MI; i++)
+#pragma unroll
+                for (int j = 0; j < NJ; j++)
+#pragma unroll
+                    for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+            const double* xs = S.act[cur];
+            for (int b = 0; b < nb; b++, gbox++) {
+                const int slot = gbox % NSB;
+                mbar_wait(&S.full[slot], (gbox / NSB) & 1);
+                const double* ws = S.w[slot];
+#pragma unroll
+                for (int kk = 0; kk < KB; kk += 4) {
+                    double a[MI][2], bf[NJ];
+#pragma unroll
+                    for (int mi = 0; mi < MI; mi++) {
+                        const int r = wm * RB + mi * 16 + pg;
+                        a[mi][0] = ws[swz(r, kk + tq)];
+                        a[mi][1] = ws[swz(r + 8, kk + tq)];
+                    }
+                    const int k = b * KB + kk + tq;
+#pragma unroll
+                    for (int nj = 0; nj < NJ; nj++) bf[nj] = xs[k * AS + wn * CB + nj * 8 + g];
+#pragma unroll
+                    for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+                        for (int nj = 0; nj < NJ; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], bf[nj]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.empty[slot]);
+            }
+            double* xo = S.act[cur ^ 1];
+#pragma unroll
+            for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+                for (int half = 0; half < 2; half++) {
+                    const int r = wm * RB + mi * 16 + pg + half * 8;
+                    if (r >= st.n_out) continue;
+                    const int row = st.row_off + r;
+#pragma unroll
+                    for (int nj = 0; nj < NJ; nj++)
+#pragma unroll
+                        for (int e = 0; e < 2; e++) {
+                            const int c = wn * CB + nj * 8 + 2 * tq + e;
+                            if (c >= np) continue;
+                            const double pre = prec_round(
+                                acc[mi][nj][half * 2 + e] + step_bias(st, item_shape(S.key[c], P.shape_w), r), FP32);
+                            if (pre > 0.0)
+                                atomicOr(reinterpret_cast<unsigned long long*>(&S.key[c][row >> 6]), key_mask(row));
+                            xo[r * AS + c] = pre > 0.0 ? pre : 0.0;
+                        }
+                }
+            bar_sync(1, NCT);
+            cur ^= 1;
+        }
+        // ---- head (k_forward_head): per point, lane-strided sums over the active rows + tree
+        const SubDev sd = *P.subs;
+        for (int c = warp; c < np; c += NCW) {
+            double a = 0.0;
+            for (int r = lane; r < sd.last_n; r += 32) {
+                const int row = sd.last_row + r;
+                if ((S.key[c][row >> 6] >> (63 - (row & 63))) & 1ull) a += S.act[cur][r * AS + c] * S.hw[r];
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (lane == 0 && F.vals) F.vals[p0 + c] = prec_round(a + head_bias(sd, item_shape(S.key[c], P.shape_w)), FP32);
+        }
+        for (int q = tid; q < np * KW; q += NCT) {
+            const int c = q / KW, w = q - c * KW;
+            F.keys[(p0 + c) * KW + w] = S.key[c][w];
+        }
+        bar_sync(1, NCT);
+    }
+}
+
+void launch_forward_narrow(const NarrowCompose& P, const ForwardArgs& F, cudaStream_t s) {
+    if (F.n_cap <= 0) return;
+    const int64_t tiles = (F.n_cap + FP - 1) / FP;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int64_t grid = std::min<int64_t>(tiles, (int64_t)device_sms() * CPS);
+    const size_t smem = sizeof(ForwardSmem) + 1024;
+    static bool init[64] = {};
+    if (dev < 64 && !init[dev]) {
+        cudaFuncSetAttribute(k_forward_narrow<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_forward_narrow<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init[dev] = true;
+    }
+    if (P.fp32) launch_k(k_forward_narrow<1>, (unsigned)grid, NT, smem, s, P, F);
+    else launch_k(k_forward_narrow<0>, (unsigned)grid, NT, smem, s, P, F);
+}
+
 void launch_compose_narrow(const NarrowCompose& P, cudaStream_t s) {
     if (P.n_cap <= 0) return;
     const int64_t tiles = (P.n_cap + NCELL - 1) / NCELL;

@@ -274,3 +274,40 @@ def test_prefix_reuse_is_bitwise_neutral(case, monkeypatch):
     assert a.report.cells_visited > 1000
     for f in ("keys", "nverts", "verts", "edge_nrefs", "edge_refs"):
         np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_narrow_point_forward_matches_per_layer_bitwise(precision, monkeypatch):
+    """k_forward_narrow (every layer + head of a narrow net in one launch) returns the values and
+    state keys of the per-layer forward kernels bit for bit, also for a batch of shapes."""
+    import torch
+    from paper_2106_10031_b200 import synth
+    from paper_2106_10031_b200.engine import Engine
+    _gpu()
+    rng = np.random.default_rng(7)
+    pts = rng.uniform(-1.2, 1.2, size=(5000, 3))
+    nets = [synth.geometric_mlp([90] * 6, seed=0), synth.geometric_mlp([60, 60], seed=3)]
+    for net in nets:
+        out = {}
+        for mode in ("1", "0"):
+            monkeypatch.setenv("AM_FORWARD_NARROW", mode)
+            eng = Engine(net, precision=precision)
+            v, k = eng.forward(pts, keys=True)
+            out[mode] = (v.cpu().numpy(), k.cpu().numpy())
+            del eng
+        np.testing.assert_array_equal(out["1"][0], out["0"][0])
+        np.testing.assert_array_equal(out["1"][1], out["0"][1])
+    # batch of shapes: per-shape biases, per-point shapes
+    bnets = _bias_batch(3)
+    shapes = rng.integers(0, 3, size=len(pts)).astype(np.int32)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("AM_FORWARD_NARROW", mode)
+        eng = Engine(bnets[0], n_shapes=3)
+        eng.set_shapes(bnets)
+        v, k = eng.forward(pts, keys=True, shapes=shapes)
+        out[mode] = (v.cpu().numpy(), k.cpu().numpy())
+        del eng
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_array_equal(out["1"][1], out["0"][1])
