@@ -1253,7 +1253,10 @@ __device__ __forceinline__ void place_cell(const FaceArgs& A, int64_t n, int64_t
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_near(FaceArgs A) {
+#ifndef AM_NEAR_MINB
+#define AM_NEAR_MINB 1
+#endif
+__global__ void __launch_bounds__(256, AM_NEAR_MINB) k_near(FaceArgs A) {
     pdl_enter();
     const int lane = threadIdx.x & 31;
     const int64_t n = dev_count(A.n_dev, A.n_cap);

@@ -4,6 +4,6 @@
 for flags in "$@"; do
   AM_BUILD_FLAGS="$flags" python -c "from paper_2106_10031_b200 import build; build.build(force=True)" > /dev/null 2>&1 || { echo "build failed: $flags"; continue; }
   echo "== flags: [$flags]"
-  python tools/env_ab.py --repeat 10 "AM_PREFIX=1" 2>&1 | tail -1
+  python tools/env_ab.py --repeat 10 ${AB_VARIANT:-"AM_PREFIX=1"} 2>&1 | tail -1
 done
 AM_BUILD_FLAGS="" python -c "from paper_2106_10031_b200 import build; build.build(force=True)" > /dev/null 2>&1
