@@ -242,6 +242,30 @@ def test_narrow_and_per_layer_composition_agree_bitwise(precision, monkeypatch):
 
 
 @pytest.mark.gpu
+def test_prefix_reuse_per_step_batch_of_shapes_is_bitwise_neutral(monkeypatch):
+    """Prefix reuse on the per-step path of a fused batch of latent shapes (per-shape biases; a
+    child's parent is always of its own shape) gives every shape's march bit for bit."""
+    from paper_2106_10031_b200 import synth
+    from paper_2106_10031_b200.batch import march_fused
+    from paper_2106_10031_b200.marching import clear_engine_cache
+    m = _gpu()
+    nets, _ = synth.latent_batch(n_shapes=3, latent_dim=8, width=160, depth=5, skip_at=3, seed=5, code_std=0.05)
+    cfg = m.MarchConfig(bbox=((0.0, 0.0, 0.0), (0.5, 0.5, 0.5)), seeds=4, rng_seed=1)
+    out = {}
+    try:
+        for mode in ("1", "0"):
+            monkeypatch.setenv("AM_PREFIX", mode)
+            clear_engine_cache()
+            out[mode] = march_fused(nets, cfg)
+    finally:
+        clear_engine_cache()
+    for a, b in zip(out["1"], out["0"]):
+        assert a.report.cells_visited > 200
+        for f in ("keys", "nverts", "verts", "edge_nrefs", "edge_refs"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("case", ["narrow-fp64", "narrow-fp32", "per-step-deepsdf"])
 def test_prefix_reuse_is_bitwise_neutral(case, monkeypatch):
     """Children composed from their parents' Z rows (prefix reuse, on the narrow and on the
