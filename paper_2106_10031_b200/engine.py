@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .network import AnyNetwork, NetBlob, to_blob
+from .network import AnyNetwork, NetBlob, NetworkFormatError, to_blob
 
 TOL_CELL = 1e-9      # reference cells.py:33
 TOL_WELD = 1e-7      # reference cells.py:35
@@ -157,14 +157,39 @@ class Engine:
         engine); nets[0] becomes the base parameter set."""
         if len(nets) != self.n_shapes:
             raise ValueError(f"engine holds {self.n_shapes} shapes, got {len(nets)} networks")
-        blobs = [to_blob(n) for n in nets]
-        self.load_network(nets[0], blobs[0])
-        base = np.asarray(blobs[0].params, dtype=np.float64)
-        diff = np.zeros(len(base), dtype=bool)
-        for b in blobs[1:]:
-            diff |= np.asarray(b.params, dtype=np.float64) != base
+        from .network import param_chunks, subnetworks
+        blob0 = to_blob(nets[0])
+        kind0 = getattr(subnetworks(nets[0])[0], "field_kind", "sdf")
+        self.load_network(nets[0], blob0)
+        base = param_chunks(nets[0])
+        per_net = [base]
+        diff = np.zeros(len(blob0.params), dtype=bool)
+        for n in nets[1:]:
+            ch = param_chunks(n)
+            if len(ch) != len(base):
+                raise NetworkFormatError("batch of shapes: the networks differ in structure")
+            if getattr(subnetworks(n)[0], "field_kind", "sdf") != kind0:
+                raise NetworkFormatError("batch of shapes: the networks differ in field kind")
+            for (off, a0), (off1, a) in zip(base, ch):
+                if a is a0:
+                    continue      # shared array (e.g. one decoder's weights): equal by identity
+                a = np.asarray(a, dtype=np.float64)
+                if off1 != off or a.shape != np.shape(a0):
+                    raise NetworkFormatError("batch of shapes: the networks differ in structure")
+                if not np.isfinite(a).all():
+                    raise NetworkFormatError("batch of shapes: non-finite parameters")
+                diff[off:off + a.size] |= a.reshape(-1) != np.asarray(a0, dtype=np.float64).reshape(-1)
+            per_net.append(ch)
         idx = np.flatnonzero(diff).astype(np.int64)
-        vals = np.ascontiguousarray(np.stack([np.asarray(b.params, dtype=np.float64)[idx] for b in blobs]))
+
+        def gather(ch):
+            flat = np.empty(len(idx), dtype=np.float64)
+            for off, a in ch:
+                lo, hi = np.searchsorted(idx, [off, off + np.size(a)])
+                if hi > lo:
+                    flat[lo:hi] = np.asarray(a, dtype=np.float64).reshape(-1)[idx[lo:hi] - off]
+            return flat
+        vals = np.ascontiguousarray(np.stack([gather(ch) for ch in per_net]))
         _native.check(self.lib.am_engine_set_shape_params(self.h, idx.ctypes.data, len(idx), vals.ctypes.data),
                       "am_engine_set_shape_params")
         self.shape_nets = list(nets)

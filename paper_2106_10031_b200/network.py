@@ -463,11 +463,29 @@ class NetBlob:
 def to_blob(net) -> NetBlob:
     """Flatten any reference-shaped network (validated with ``check_network``)."""
     check_network(net)
+    return _walk_blob(net, None)
+
+
+def param_chunks(net) -> list:
+    """The parameter arrays of ``net`` in descriptor order, as given (no copies): [(offset, array)].
+    A batch of shapes compares these against the base network's to find the per-shape entries
+    (arrays shared by identity are skipped without a comparison)."""
+    out: list = []
+    _walk_blob(net, out)
+    return out
+
+
+def _walk_blob(net, record):
     chunks: list = []
     size = 0
 
     def put(arr) -> int:
         nonlocal size
+        if record is not None:
+            a = arr if isinstance(arr, np.ndarray) else np.asarray(arr, dtype=np.float64)
+            record.append((size, a))
+            size += a.size
+            return size - a.size
         a = np.asarray(arr, dtype=np.float64).reshape(-1)
         chunks.append(a)
         size += a.size
@@ -509,6 +527,8 @@ def to_blob(net) -> NetBlob:
                 widest = max(widest, w.shape[0])
         subs.append([first_step, len(steps) - first_step, put(sub.head_weight), put([float(sub.head_bias)]),
                      row_begin, row - row_begin])
+    if record is not None:
+        return None
     return NetBlob(
         params=np.concatenate(chunks) if chunks else np.zeros(0),
         steps=np.asarray(steps, dtype=np.int64).reshape(-1, STEP_FIELDS),

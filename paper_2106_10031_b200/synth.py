@@ -53,30 +53,46 @@ def deepsdf_mlp(width: int = 512, depth: int = 8, skip_at: int = 4, radius: floa
                 seed: int = 0, bias_std: float = 0.0, latent_dim: int = 0,
                 latent: np.ndarray | None = None) -> NetworkSpec:
     """DeepSDF decoder with x (and the latent code) re-entering at hidden layer ``skip_at``."""
+    return _deepsdf_assemble(_deepsdf_parts(width, depth, skip_at, radius, seed, bias_std, latent_dim), latent)
+
+
+def _deepsdf_parts(width, depth, skip_at, radius, seed, bias_std, latent_dim):
+    """The decoder's arrays (drawn once): the code only enters the first-layer and skip biases."""
     if not 1 <= skip_at < depth:
         raise ValueError("skip_at must be in [1, depth)")
     rng = np.random.default_rng(seed)
     in_dim = 3 + latent_dim
-    z = np.zeros(latent_dim) if latent is None else np.asarray(latent, dtype=np.float64)
     inner = []
     n_in = in_dim
     for k in range(skip_at):
         w = _geo_hidden(rng, n_in, width)
         b = rng.normal(0.0, bias_std, size=width) if bias_std > 0 else np.zeros(width)
-        if k == 0 and latent_dim:
-            # x-part keeps its columns; the code part folds into the bias
-            b = b + w[:, 3:] @ z
-            w = w[:, :3]
-        inner.append(DenseLayer(w, b))
+        inner.append((w, b))
         n_in = width
     v_full = _geo_hidden(rng, in_dim, width) / np.sqrt(2.0)
-    vb = v_full[:, 3:] @ z if latent_dim else np.zeros(width)
-    block = ResidualBlock(tuple(inner), v_full[:, :3], vb)
-    layers = [block]
+    later = []
     for _ in range(depth - skip_at):
         b = rng.normal(0.0, bias_std, size=width) if bias_std > 0 else np.zeros(width)
-        layers.append(DenseLayer(_geo_hidden(rng, width, width), b))
-    return NetworkSpec(tuple(layers), _geo_head(rng, width), -radius)
+        later.append(DenseLayer(_geo_hidden(rng, width, width), b))
+    w0 = inner[0][0]
+    return {"latent_dim": latent_dim, "inner": inner, "w0x": w0[:, :3] if latent_dim else w0, "v_full": v_full,
+            "vx": v_full[:, :3], "later": tuple(later), "head": _geo_head(rng, width), "radius": radius}
+
+
+def _deepsdf_assemble(parts, latent):
+    latent_dim = parts["latent_dim"]
+    z = np.zeros(latent_dim) if latent is None else np.asarray(latent, dtype=np.float64)
+    inner = []
+    for k, (w, b) in enumerate(parts["inner"]):
+        if k == 0 and latent_dim:
+            # x-part keeps its columns (one shared array); the code part folds into the bias
+            inner.append(DenseLayer(parts["w0x"], b + w[:, 3:] @ z))
+        else:
+            inner.append(DenseLayer(w, b))
+    v_full = parts["v_full"]
+    vb = v_full[:, 3:] @ z if latent_dim else np.zeros(v_full.shape[0])
+    block = ResidualBlock(tuple(inner), parts["vx"], vb)
+    return NetworkSpec((block,) + parts["later"], parts["head"], -parts["radius"])
 
 
 def imnet_ensemble(widths=(64, 64, 64), n_parts: int = 4, seed: int = 0,
@@ -105,8 +121,11 @@ def imnet_ensemble(widths=(64, 64, 64), n_parts: int = 4, seed: int = 0,
 
 def latent_batch(n_shapes: int = 64, latent_dim: int = 256, width: int = 512, depth: int = 8,
                  skip_at: int = 4, seed: int = 0, code_std: float = 0.01):
-    """One shared DeepSDF decoder, ``n_shapes`` codes z_i ~ N(0, code_std): list of networks."""
+    """One shared DeepSDF decoder, ``n_shapes`` codes z_i ~ N(0, code_std): list of networks (the
+    decoder's weight arrays are shared by every network; only the code-folded biases differ)."""
     rng = np.random.default_rng([seed, 1])
     codes = rng.normal(0.0, code_std, size=(n_shapes, latent_dim))
-    return [deepsdf_mlp(width, depth, skip_at, seed=seed, latent_dim=latent_dim, latent=z)
-            for z in codes], codes
+    parts = _deepsdf_parts(width, depth, skip_at, 0.5, seed, 0.0, latent_dim)
+    return [_deepsdf_assemble(parts, z) for z in codes], codes
+
+
