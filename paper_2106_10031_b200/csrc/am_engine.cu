@@ -1010,6 +1010,8 @@ static int launch_iteration(am_engine* e) {
     I.queue_par = e->prefix ? e->queue_par.p : nullptr;
     I.blist = e->blist.p;
     I.max_share = (int)e->sdev.size() - 1;
+    I.max_cells = (long long)e->P.max_cells;
+    I.cap_drop = e->defer ? 0 : 1;
     ProbeRecs R;
     R.cand = e->prec_cand.p; R.k = e->prec_k.p; R.pt = e->prec_pt.p;
     for (int q = 0; q < 2; q++) { R.pend_t[q] = e->pend_t[q].p; R.pend_k[q] = e->pend_k[q].p; R.pend_pt[q] = e->pend_pt[q].p; }

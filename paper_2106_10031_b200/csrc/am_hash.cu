@@ -112,7 +112,19 @@ __global__ void k_take(IterState I) {
         if (room_val < lim) lim = room_val;
         if (lim < 0) lim = 0;
         if (nR > lim) nR = lim;
-        c[C_STALL] = (want > 0 && nR == 0) ? 1ull : 0ull;
+        // max_cells (reference marching.py:240-242 ends the walk there): a batch item becomes at
+        // most one visited cell, so no more than the remaining allowance is composed; once it is
+        // used up and no cell can be waiting for a deferred face, the queue, the pending probe
+        // records and the queued probe evaluations are dropped instead of composed and discarded
+        bool drop = false;
+        const long long rem = I.max_cells - (long long)c[C_TOTAL];
+        if (rem <= 0 && I.cap_drop) {
+            drop = want > 0 || c[C_NPEND] || c[C_NPROBE];
+            nR = 0;
+        } else if (rem > 0 && nR > rem) {
+            nR = rem;
+        }
+        c[C_STALL] = (!drop && want > 0 && nR == 0) ? 1ull : 0ull;
         c[C_NR] = (unsigned long long)nR;
         // C_NPROBE is not reset: exact probe evaluations accumulate across iterations and are
         // flushed by the host loop (probe_flush) outside the per-iteration graph
@@ -135,6 +147,13 @@ __global__ void k_take(IterState I) {
         c[C_QHEAD] = (unsigned long long)(head + a);
         c[C_QTAIL] = (unsigned long long)(tail - t);
         c[C_QMARK] = (unsigned long long)(tail - t);
+        if (drop) {
+            c[C_CAPPED] += (unsigned long long)(want > 0 ? want : 1);
+            c[C_QHEAD] = (unsigned long long)tail;
+            c[C_QMARK] = (unsigned long long)tail;
+            c[C_NPEND] = 0;
+            c[C_NPROBE] = 0;
+        }
         s_n = nR;
         s_iter = c[C_ITER];
     }

@@ -356,6 +356,8 @@ struct IterState {
     const int64_t* queue_par;   // prefix_word per queue entry (HashSet::queue_par)
     int32_t* blist;
     int max_share;            // largest usable f (nsteps - 1)
+    long long max_cells;      // visited-cell cap (this rank's share)
+    int cap_drop;             // no deferral: the cap ends the walk (drop what is queued)
 };
 // probe records: (target pool entry, neuron, point); double-buffered by parity counter
 struct ProbeRecs {
