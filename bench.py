@@ -544,7 +544,8 @@ def main():
         others["configs[4]"] = {
             "workload": "64 latent-conditioned shapes: 256-d code (+) xyz into a DeepSDF 3-(512x8)-1 decoder "
                         f"(code folded into first-layer / skip biases), fp64, 64 dichotomy seeds per shape, "
-                        f"first {args.latent_cells} cells per shape (max_cells cap)",
+                        f"max_cells {args.latent_cells} per shape (the fused batch caps the total at "
+                        f"{len(lnets)} x {args.latent_cells} cells)",
             "shapes": len(lres), "cells": int(lcells), "seconds": l_s, "cells_per_s": lcells / l_s,
             "per_shape_ms": 1e3 * l_s / len(lres),
             "api": "paper_2106_10031_b200.batch.march_batch(nets, MarchConfig) -> MarchResults on host; "
