@@ -461,6 +461,14 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
     c.Z = zbase(A) + (int64_t)item * A.zs * 4;
     c.faces = A.faces + (int64_t)item * A.M * 4;
     c.key = A.keys + (int64_t)item * A.KW;
+    // the cell's independent inputs are requested together, ahead of their first use: hint,
+    // near-list header and (single-subnetwork nets) the face row
+    const int64_t nslot = A.near_by_item ? (int64_t)item : fi;   // near lists built by the composition: per item
+    const double4 hint_in = reinterpret_cast<const double4*>(A.hints)[item];
+    const int nflags_in = A.near_flags ? A.near_flags[nslot] : 0;
+    const int nn_in = A.near_flags ? A.near_n[nslot] : 0;
+    double4 face_in = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (!A.ensemble) face_in = *reinterpret_cast<const double4*>(c.faces);
     if (A.KW <= KWF) {   // stage the key: one coalesced load instead of a dependent round trip per lookup
         for (int w = lane; w < A.KW; w += 32) W->key[w] = c.key[w];
         __syncwarp();
@@ -475,7 +483,8 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
     const int box0 = c.NB + c.M;
 
     // ------------------------------------------------------ face plane
-    const double* fr = c.faces + c.branch * 4;
+    if (A.ensemble) face_in = *reinterpret_cast<const double4*>(c.faces + c.branch * 4);
+    const double fr[4] = {face_in.x, face_in.y, face_in.z, face_in.w};
     double fn = sqrt((fr[0] * fr[0] + fr[1] * fr[1]) + fr[2] * fr[2]);
     double fu[3] = {0, 0, 0}, fo = 0.0;
     bool face_ok = fn > kDegen;
@@ -501,7 +510,7 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
     // is (nearly) final before the full passes.
     // Seeds carry their surface point as the hint; it is projected onto the face plane (a
     // no-op up to rounding for edge midpoints) so the 3-D near test and the 2-D frame agree.
-    double4 hint = reinterpret_cast<const double4*>(A.hints)[item];
+    double4 hint = hint_in;
     const bool have_hint = isfinite(hint.w) && face_ok;
     double s0 = 0.0, t0 = 0.0;
     if (have_hint) {
@@ -527,10 +536,9 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
     double tau = A.tau_mult * hint.w;
     // near list from k_near (rows within `reach` of x0): attempts with tau <= reach filter it
     // instead of streaming every row again
-    const int64_t nslot = A.near_by_item ? (int64_t)item : fi;   // near lists built by the composition: per item
-    const int list_flags = (A.near_flags && have_hint) ? A.near_flags[nslot] : 0;
+    const int list_flags = have_hint ? nflags_in : 0;
     const bool use_list = (list_flags & kNearValid) && !(list_flags & kNearOverflow);
-    const int n_list = use_list ? A.near_n[nslot] : 0;
+    const int n_list = use_list ? nn_in : 0;
     const double reach = A.near_reach * hint.w;
     FSTAT(14, use_list ? 1 : 0);
     FSTAT(15, (list_flags & kNearOverflow) ? 1 : 0);

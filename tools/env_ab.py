@@ -69,7 +69,7 @@ for rep in range(a.repeat + 1):
                 ref = arrs
             same = all(np.array_equal(x, y) for x, y in zip(arrs, ref))
             st = eng.stats()
-            print(f"{a.variants[i]}: cells {r.report.cells_visited} bitwise equal to first: {same}  "
+            print(f"{a.variants[i]}: cells {r.report.cells_visited} waves {r.report.waves} bitwise equal to first: {same}  "
                   f"prefix {st['prefix']:.0f} skipped flops {st['prefix_skipped_flops']:.3e}", flush=True)
         else:
             times[i].append(T[-1])
