@@ -617,7 +617,9 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // previous batch's children all fit the next batch (prefix reuse).  Complete DeepSDF march:
     // 16 k -> 8.07 s, 24 k -> 7.55, 32 k -> 7.24, 48 k -> 6.74, 64 k -> 6.74 s (waves 1002 -> 818).
     // Light ones keep 16 k cells in 4 GB (configs[1]'s waves stay below 6 k cells).
-    const bool heavy = e->flops_per_cell >= 2.0e6;
+    // (sharded engines keep 16 k: the exchange buffers are reserved for a whole round's worst-case
+    // emissions, and several ranks may share a device in functional checks)
+    const bool heavy = e->flops_per_cell >= 2.0e6 && e->P.world <= 1;
     int64_t budget = e->P.mem_budget > 0 ? e->P.mem_budget : (int64_t)(heavy ? 32 : 4) << 30;
     int64_t per = (int64_t)e->zs * 32 * 3 + (int64_t)e->zs * 8 + emit_per_cell() * e->KW * 8 * 2 +
                   (int64_t)kVertsPerCell * 40 + e->M * 32 + 256;   // Z + both prefix halves
