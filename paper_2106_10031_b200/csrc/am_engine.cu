@@ -167,6 +167,10 @@ struct am_engine {
     bool prefix = false;
     int near_depth = 2;         // AM_NEAR_DEPTH
     bool narrow_snake = true;   // AM_NARROW_SNAKE
+    // flips inserted by the face warps themselves (AM_FACE_UPSERT=1; single rank): bitwise-equal
+    // marches but slower (configs[1] BFS 18.55 vs 17.76 ms, a 48-wave small net 3.78 vs 3.57):
+    // the hash probes lengthen every cell's chain more than the separate launch costs
+    bool face_upsert = false;
     // point forwards through k_forward_narrow on the narrow path (AM_FORWARD_NARROW=1): bitwise
     // equal to the per-layer kernels but not faster (4096 trigger samples 0.114 vs 0.123 ms, the
     // configs[1] BFS with its probe forwards 17.90 vs 17.71 ms): a 32-point tile walking every
@@ -684,6 +688,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // where k_near keeps 32 warps per SM of row loads in flight
     if (const char* v = getenv("AM_NEAR_DEPTH")) e->near_depth = atoi(v);
     if (const char* v = getenv("AM_NARROW_SNAKE")) e->narrow_snake = atoi(v) != 0;
+    if (const char* v = getenv("AM_FACE_UPSERT")) e->face_upsert = atoi(v) != 0;
     if (const char* v = getenv("AM_FORWARD_NARROW")) e->forward_narrow = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_FUSED"))
         e->near_fused = e->narrow_fused && !e->face_order && !e->narrow_check && atoi(v) != 0;
@@ -1137,6 +1142,9 @@ static int launch_iteration(am_engine* e) {
     a.tau_mult = e->tau_mult; a.near_reach = e->near_reach; a.max_attempts = e->max_attempts;
     a.tau_grow = e->tau_grow;
     a.zpar = nullptr; a.zstride = 0; a.emit_par = nullptr; a.queue_par = nullptr; a.nsteps = 0;
+    a.fused_upsert = (e->face_upsert && !multi) ? 1 : 0;
+    a.H = H; a.cand_status = e->status.p; a.cand_slot = e->slot.p; a.cand_dup = e->emit_dup.p;
+    a.cand_pool = e->emit_pool.p; a.ins_queue = e->queue.p;
     if (e->prefix) {
         a.Z = e->Zi.p;
         a.zpar = c + C_ITER; a.zstride = e->B * e->zs * 4; a.emit_par = e->emit_par.p; a.queue_par = e->queue_par.p;
@@ -1155,7 +1163,7 @@ static int launch_iteration(am_engine* e) {
         launch_route_emitted(e->scratch.p, c + C_NEMIT, e->E, e->KW, e->P.rank, e->P.world, e->local_idx.p,
                              c + C_NLOCAL, e->outbox.p, c + C_NOUT, e->status.p, s);
         launch_hash_upsert(H, e->scratch.p, e->local_idx.p, c + C_NLOCAL, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s, a.emit_par);
-    } else {
+    } else if (!a.fused_upsert) {
         launch_hash_upsert(H, e->scratch.p, nullptr, c + C_NEMIT, e->E, e->status.p, e->slot.p, e->emit_dup.p, 0u, e->emit_pool.p, e->queue.p, c + C_QTAIL, e->emit_hint.p, s, a.emit_par);
     }
     mark(7);

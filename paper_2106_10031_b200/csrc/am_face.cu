@@ -36,6 +36,7 @@
 #include <cstdlib>
 
 #include "am_internal.h"
+#include "am_hashset.cuh"
 #include "am_near.cuh"
 
 namespace am {
@@ -1243,6 +1244,20 @@ __device__ void face_cell(const FaceArgs& A, FaceWarp* W, int64_t fi, int64_t n_
                 }
                 A.emit_par[ci] = f ? prefix_word(*A.zpar, item, f) : 0;
             }
+        }
+    }
+    if (A.fused_upsert && tot_cd) {
+        // the flips go straight into the state set (k_hash_upsert's work, one candidate per
+        // lane): their key rows must be visible device-wide before a slot marker can point at them
+        __threadfence();
+        __syncwarp();
+#pragma unroll 1
+        for (int k = lane; k < tot_cd; k += 32) {
+            const int64_t ci = cbase + k;
+            int32_t p;
+            A.cand_status[ci] = upsert_one(A.H, A.cand, nullptr, ci, ci, A.cand_slot, A.cand_dup, 0u, A.ins_queue,
+                                           A.q_tail, A.emit_hint, &p, A.emit_par);
+            A.cand_pool[ci] = p;
         }
     }
     PMARK(12);

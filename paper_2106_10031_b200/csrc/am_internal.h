@@ -509,6 +509,15 @@ struct FaceArgs {
     int64_t zstride;
     int64_t* emit_par;
     int64_t* queue_par;       // deferral re-queues a cell with no parent word (full composition)
+    // flips inserted by the face warps themselves (fused_upsert; single rank): per candidate
+    // status / slot / dup_ref / pool index, as k_hash_upsert writes them
+    int fused_upsert;
+    HashSet H;
+    int32_t* cand_status;
+    uint64_t* cand_slot;
+    int32_t* cand_dup;
+    int32_t* cand_pool;
+    int32_t* ins_queue;
     int nsteps;
     int step_end[12];
 };
