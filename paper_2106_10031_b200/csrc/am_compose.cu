@@ -280,26 +280,34 @@ constexpr int KCW = 10;    // cached state words per item and K segment (K rows 
 #ifndef AM_WRES96
 #define AM_WRES96 0
 #endif
-template <int C, int TM>
+// NJ: 8-column fragments per warp (2: 32 x 16 warp tiles; 4: 32 x 32 warp tiles, half the warps
+// per CTA for the same 64 x 64 output tile -- twice the DMMAs per A-fragment load, AM_GEMM_NJ4)
+#ifndef AM_NJ4_NST
+#define AM_NJ4_NST 2
+#endif
+#ifndef AM_NJ4_CPS
+#define AM_NJ4_CPS 3
+#endif
+template <int C, int TM, int NJ = 2>
 struct GT {
-    static constexpr int NS = TM == 96 ? AM_NST96 : NST;   // pipeline stages
-    static constexpr int CPS = TM == 96 ? AM_CPS96 : 2;    // resident CTAs per SM
+    static constexpr int NS = TM == 96 ? AM_NST96 : (NJ == 4 ? AM_NJ4_NST : NST);   // pipeline stages
+    static constexpr int CPS = TM == 96 ? AM_CPS96 : (NJ == 4 ? AM_NJ4_CPS : 2);    // resident CTAs per SM
     static constexpr bool WRES = TM == 96 && AM_WRES96;    // W resident for layers of <= WS chunks
     static constexpr int WS = WRES ? (NS > 3 ? NS : 3) : NS;   // W slots
     static constexpr int WM = TM / 32;                // warps along rows
-    static constexpr int WN = TM == 64 ? 4 : 2;       // warps along columns
+    static constexpr int WN = TM == 64 ? 8 / NJ : 2;  // warps along columns
     static constexpr int NT = 32 * WM * WN;           // threads
-    static constexpr int TN = 16 * WN;                // columns per tile
+    static constexpr int TN = 8 * NJ * WN;            // columns per tile
     static constexpr int NI = C == 4 ? TN / 4 : TN;   // items per tile
 };
 
-template <int C, int TM = BM>
+template <int C, int TM = BM, int NJ = 2>
 struct __align__(1024) GemmSmem {
-    static constexpr int NI = GT<C, TM>::NI;   // items per tile
-    static constexpr int TN = GT<C, TM>::TN;
+    static constexpr int NI = GT<C, TM, NJ>::NI;   // items per tile
+    static constexpr int TN = GT<C, TM, NJ>::TN;
     static constexpr int XSZ = C == 4 ? NI * XS4 : TN * XS1;
-    static constexpr int NS = GT<C, TM>::NS;
-    double w[GT<C, TM>::WS][BK / TB][TM * TB];   // TMA destination: 2 boxes of TM rows x 16 k, 128B-swizzled
+    static constexpr int NS = GT<C, TM, NJ>::NS;
+    double w[GT<C, TM, NJ>::WS][BK / TB][TM * TB];   // TMA destination: 2 boxes of TM rows x 16 k, 128B-swizzled
     double x[NS][XSZ];            // raw activation tile
     uint32_t mask[NS][TN];        // per item / point: the 32 state bits of the stage's K rows
     uint64_t kc[2][NI][KCW];       // the tile's state words covering each K segment
@@ -322,17 +330,19 @@ __device__ __forceinline__ uint32_t bits32(const uint64_t* key, int row, int val
 }
 
 // One TM-row x TN-column output tile of layer L.st (all K chunks + epilogue).
-template <int C, int TM = BM>
-__device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch& L, uint64_t* keys, int64_t n,
+template <int C, int TM = BM, int NJ = 2>
+__device__ __forceinline__ void gemm_tile(GemmSmem<C, TM, NJ>& S, const LayerLaunch& L, uint64_t* keys, int64_t n,
                                           const CUtensorMap* tmWp, const CUtensorMap* tmVp, int m0, int64_t n0,
                                           uint32_t& gchunk, bool wres = false) {
     const StepDev& st = L.st;
     double* const Zb = zbase(L);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    using T = GT<C, TM>;
+    using T = GT<C, TM, NJ>;
     static_assert(C == 4 || TM == 64, "the forward stage uses 64-row tiles");
-    const int wm = warp % T::WM, wn = warp / T::WM;   // warp tile: rows wm*32 .. +31, columns wn*16 .. +15
+    static_assert(C == 4 || NJ == 2, "the forward stage uses 32 x 16 warp tiles");
+    constexpr int WC = 8 * NJ;   // warp tile columns
+    const int wm = warp % T::WM, wn = warp / T::WM;   // warp tile: rows wm*32 .. +31, columns wn*WC .. +WC-1
     const bool lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && !(st.flags & AM_STEP_SC_FROM_INPUT);
     const int kc0 = (st.n_in + BK - 1) / BK;
     const int kc1 = lin ? (st.n_sin + BK - 1) / BK : 0;
@@ -345,7 +355,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
     {
         if (C == 1 && tid < BN) { S.bits[tid][0] = 0; S.bits[tid][1] = 0; }
         // state words of the tile's items covering both K segments (no global reads in issue())
-        constexpr int NI = GemmSmem<C, TM>::NI;
+        constexpr int NI = GemmSmem<C, TM, NJ>::NI;
         const int64_t item0 = C == 4 ? n0 / 4 : n0;
         int wbeg[2], wcnt[2];
         wbeg[0] = st.in_row_off >> 6;
@@ -417,11 +427,11 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
             cp_async_commit();
         };
 
-        double acc[2][2][4];
+        double acc[2][NJ][4];
 #pragma unroll
         for (int i = 0; i < 2; i++)
 #pragma unroll
-            for (int j = 0; j < 2; j++)
+            for (int j = 0; j < NJ; j++)
 #pragma unroll
                 for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
 
@@ -450,7 +460,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
             const double* xsm = S.x[s];
 #pragma unroll
             for (int kk = 0; kk < BK; kk += 4) {
-                double a[2][2], b[2];
+                double a[2][2], b[NJ];
 #pragma unroll
                 for (int mi = 0; mi < 2; mi++) {
                     int r = wm * 32 + mi * 16 + pg;
@@ -458,8 +468,8 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                     a[mi][1] = ws[(kk / TB) * TM * TB + swz(r + 8, (kk % TB) + t)];
                 }
 #pragma unroll
-                for (int nj = 0; nj < 2; nj++) {
-                    const int col = wn * 16 + nj * 8 + g;
+                for (int nj = 0; nj < NJ; nj++) {
+                    const int col = wn * WC + nj * 8 + g;
                     double v;
                     uint32_t mk;
                     if (C == 4) {
@@ -474,7 +484,7 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
 #pragma unroll
                 for (int mi = 0; mi < 2; mi++)
 #pragma unroll
-                    for (int nj = 0; nj < 2; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
+                    for (int nj = 0; nj < NJ; nj++) dmma_16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
             }
         }
         gchunk += nchunks;
@@ -490,8 +500,8 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
                 const bool rok = r < st.n_out;
                 const int row = st.row_off + r;
 #pragma unroll
-                for (int nj = 0; nj < 2; nj++) {
-                    const int64_t col = n0 + wn * 16 + nj * 8 + 2 * t;
+                for (int nj = 0; nj < NJ; nj++) {
+                    const int64_t col = n0 + wn * WC + nj * 8 + 2 * t;
                     double v0 = acc[mi][nj][half * 2], v1 = acc[mi][nj][half * 2 + 1];
                     if (C == 4) {
                         const int64_t item = col >> 2;
@@ -599,13 +609,13 @@ __device__ __forceinline__ void gemm_tile(GemmSmem<C, TM>& S, const LayerLaunch&
 // NST-stage ring: W by TMA (mbarrier), the raw activations by cp.async, the state mask of the
 // chunk as 16-bit words -- applied when the B fragments are read, so padding rows and
 // inactive neurons contribute exact zeros.
-template <int C, int TM>
-__global__ void __launch_bounds__(GT<C, TM>::NT, GT<C, TM>::CPS) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
+template <int C, int TM, int NJ = 2>
+__global__ void __launch_bounds__(GT<C, TM, NJ>::NT, GT<C, TM, NJ>::CPS) k_gemm_step(const __grid_constant__ CUtensorMap tmW,
                                                         const __grid_constant__ CUtensorMap tmV, LayerLaunch L) {
     extern __shared__ uint8_t smem_raw[];
     // 1 KB-aligned view derived by pointer arithmetic on the shared array (keeps LDS addressing)
-    GemmSmem<C, TM>& S = *reinterpret_cast<GemmSmem<C, TM>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-    using T = GT<C, TM>;
+    GemmSmem<C, TM, NJ>& S = *reinterpret_cast<GemmSmem<C, TM, NJ>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    using T = GT<C, TM, NJ>;
     const StepDev& st = L.st;
     const int tid = threadIdx.x;
     const bool lin = (st.flags & AM_STEP_SHORTCUT_LINEAR) && !(st.flags & AM_STEP_SC_FROM_INPUT);
@@ -651,32 +661,33 @@ __global__ void __launch_bounds__(GT<C, TM>::NT, GT<C, TM>::CPS) k_gemm_step(con
         // once per row tile from DRAM: ~7x the input on DeepSDF 512x8)
         const int m0 = (int)(tile % nty) * TM;
         const int64_t n0 = (tile / nty) * TN;
-        gemm_tile<C, TM>(S, L, keys, n, &tmW, &tmV, m0, n0, gchunk, wres);
+        gemm_tile<C, TM, NJ>(S, L, keys, n, &tmW, &tmV, m0, n0, gchunk, wres);
     }
     if (wres && blockIdx.x >= ntiles) mbar_wait(&S.wbar, 0);
 }
 
-template <int C, int TM>
+template <int C, int TM, int NJ = 2>
 static void launch_gemm_tm(const LayerLaunch& L, const CUtensorMap* tmW, const CUtensorMap* tmV, cudaStream_t s) {
-    using T = GT<C, TM>;
+    using T = GT<C, TM, NJ>;
     const int64_t cols = L.n_cap * C;
     const int64_t tiles = ((cols + T::TN - 1) / T::TN) * ((L.st.n_out + TM - 1) / TM);
     const int64_t grid = std::min<int64_t>(tiles, (int64_t)num_sms() * (L.grid_cap > 0 ? L.grid_cap : T::CPS));
-    const size_t smem = sizeof(GemmSmem<C, TM>) + 1024;
+    const size_t smem = sizeof(GemmSmem<C, TM, NJ>) + 1024;
     static bool init[64] = {};   // the attribute is per function and device
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 64 || !init[dev]) {
-        cudaFuncSetAttribute(k_gemm_step<C, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_gemm_step<C, TM, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (dev < 64) init[dev] = true;
     }
-    launch_k(k_gemm_step<C, TM>, (unsigned)grid, T::NT, smem, s, *tmW, tmV ? *tmV : *tmW, L);
+    launch_k(k_gemm_step<C, TM, NJ>, (unsigned)grid, T::NT, smem, s, *tmW, tmV ? *tmV : *tmW, L);
 }
 
 void launch_gemm_step(const LayerLaunch& L, int C, const CUtensorMap* tmW, const CUtensorMap* tmV, cudaStream_t s,
                       const CUtensorMap* tmW96, const CUtensorMap* tmV96) {
     if (L.n_cap <= 0) return;
     if (C == 4 && tmW96) launch_gemm_tm<4, 96>(L, tmW96, tmV96, s);
+    else if (C == 4 && L.nj4) launch_gemm_tm<4, 64, 4>(L, tmW, tmV, s);
     else if (C == 4) launch_gemm_tm<4, 64>(L, tmW, tmV, s);
     else launch_gemm_tm<1, 64>(L, tmW, tmV, s);
 }

@@ -167,6 +167,7 @@ struct am_engine {
     bool prefix = false;
     int near_depth = 2;         // AM_NEAR_DEPTH
     bool narrow_snake = true;   // AM_NARROW_SNAKE
+    int gemm_nj4 = 0;           // AM_GEMM_NJ4: 32 x 32 warp tiles in the 64-row compose GEMM
     // flips inserted by the face warps themselves (AM_FACE_UPSERT=1; single rank): bitwise-equal
     // marches but slower (configs[1] BFS 18.55 vs 17.76 ms, a 48-wave small net 3.78 vs 3.57):
     // the hash probes lengthen every cell's chain more than the separate launch costs
@@ -688,6 +689,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // where k_near keeps 32 warps per SM of row loads in flight
     if (const char* v = getenv("AM_NEAR_DEPTH")) e->near_depth = atoi(v);
     if (const char* v = getenv("AM_NARROW_SNAKE")) e->narrow_snake = atoi(v) != 0;
+    if (const char* v = getenv("AM_GEMM_NJ4")) e->gemm_nj4 = atoi(v) != 0;
     if (const char* v = getenv("AM_FACE_UPSERT")) e->face_upsert = atoi(v) != 0;
     if (const char* v = getenv("AM_FORWARD_NARROW")) e->forward_narrow = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_FUSED"))
@@ -846,6 +848,7 @@ static int run_steps(am_engine* e, int C, double* Z, uint64_t* keys, const unsig
         LayerLaunch L{};
         L.zpar = zpar;
         L.zstride = zstride;
+        L.nj4 = e->gemm_nj4;
         L.st = e->sdev[s];
         L.Z = Z;
         L.keys = keys;

@@ -143,6 +143,7 @@ struct LayerLaunch {
     // prefix reuse: Z double-buffered by iteration parity (*zpar & 1) x zstride doubles (null: Z)
     const unsigned long long* zpar;
     int64_t zstride;
+    int nj4;              // 64-row compose tiles with 32 x 32 warp tiles (AM_GEMM_NJ4)
 };
 __device__ __forceinline__ double* zbase(const LayerLaunch& L) {
     return L.zpar ? L.Z + (int64_t)(*L.zpar & 1ull) * L.zstride : L.Z;
