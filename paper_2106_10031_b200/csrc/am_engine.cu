@@ -218,6 +218,13 @@ struct am_engine {
     cudaGraphExec_t gexec = nullptr;
     bool graph_valid = false;
     cudaStream_t stream2 = nullptr;          // captures the conditional probe-stage body
+    cudaStream_t stream3 = nullptr;          // captures the gated iteration body
+    // AM_ITER_GATE=1: each graph-replayed iteration behind an IF node set by a gate kernel (no
+    // empty iterations at the end of a replay batch).  Bitwise-equal marches but slower (configs[1]
+    // BFS 19.16 vs 17.96 ms, small nets +0.5-1 ms): the conditional node costs every iteration
+    // more than the few empty iterations it saves, and it cuts the PDL chain
+    bool iter_gate = false;
+    unsigned long long gate_kernels = 0;     // kernels of one gated iteration body
     bool probe_in_graph = false;             // probe stage inside the iteration graph (sticky)
     unsigned long long cond_kernels = 0;     // kernels in that body
     // bisection trigger: engine-owned buffers and a captured 8-step graph (am_dichotomy)
@@ -530,6 +537,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
         e->own_stream = true;
     }
     CK(cudaStreamCreateWithFlags(&e->stream2, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&e->stream3, cudaStreamNonBlocking));
     e->P = *p;
     if (e->P.world < 1) e->P.world = 1;
     e->NB = net->n_bits;
@@ -689,6 +697,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     // where k_near keeps 32 warps per SM of row loads in flight
     if (const char* v = getenv("AM_NEAR_DEPTH")) e->near_depth = atoi(v);
     if (const char* v = getenv("AM_NARROW_SNAKE")) e->narrow_snake = atoi(v) != 0;
+    if (const char* v = getenv("AM_ITER_GATE")) e->iter_gate = atoi(v) != 0;
     if (const char* v = getenv("AM_GEMM_NJ4")) e->gemm_nj4 = atoi(v) != 0;
     if (const char* v = getenv("AM_FACE_UPSERT")) e->face_upsert = atoi(v) != 0;
     if (const char* v = getenv("AM_FORWARD_NARROW")) e->forward_narrow = atoi(v) != 0;
@@ -783,6 +792,7 @@ extern "C" int am_engine_destroy(am_engine* e) {
     if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->own_stream) cudaStreamDestroy(e->stream);
     if (e->stream2) cudaStreamDestroy(e->stream2);
+    if (e->stream3) cudaStreamDestroy(e->stream3);
     delete e;
     return AM_OK;
 }
@@ -1274,7 +1284,43 @@ static int capture(am_engine* e) {
     if (e->graph) { cudaGraphDestroy(e->graph); e->graph = nullptr; }
     unsigned long long before = g_launch_count;
     CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-    int rc = launch_iteration(e);
+    int rc = AM_OK;
+    if (e->iter_gate) {
+        // gate kernel + IF node whose body is the iteration (captured on stream3)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaGraph_t g0 = nullptr;
+        CK(cudaStreamGetCaptureInfo_v3(e->stream, &cs, nullptr, &g0, nullptr, nullptr, nullptr));
+        cudaGraphConditionalHandle hg{};
+        CK(cudaGraphConditionalHandleCreate(&hg, g0, 0, cudaGraphCondAssignDefault));
+        launch_iter_gate(e->ctr.p, hg, e->probe_in_graph ? 1 : 0, e->stream);
+        CK(cudaGetLastError());
+        const cudaGraphNode_t* deps = nullptr;
+        const cudaGraphEdgeData* ed = nullptr;
+        size_t nd = 0;
+        cudaGraph_t gt = nullptr;
+        CK(cudaStreamGetCaptureInfo_v3(e->stream, &cs, nullptr, &gt, &deps, &ed, &nd));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hg;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cn;
+        CK(cudaGraphAddNode(&cn, gt, deps, nd, &cp));
+        CK(cudaStreamBeginCaptureToGraph(e->stream3, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+        cudaStream_t s0 = e->stream;
+        e->stream = e->stream3;
+        const unsigned long long b0 = g_launch_count;
+        rc = launch_iteration(e);
+        e->gate_kernels = g_launch_count - b0;
+        e->stream = s0;
+        cudaGraph_t bout = nullptr;
+        cudaError_t be = cudaStreamEndCapture(e->stream3, &bout);
+        if (!rc && be != cudaSuccess) rc = fail(AM_ERR_CUDA, "gated iteration capture: %s", cudaGetErrorString(be));
+        if (!rc) CK(cudaStreamUpdateCaptureDependencies(e->stream, &cn, 1, cudaStreamSetCaptureDependencies));
+    } else {
+        rc = launch_iteration(e);
+    }
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
     if (rc) { if (g) cudaGraphDestroy(g); return rc; }
@@ -1347,6 +1393,12 @@ static int timed_iteration(am_engine* e) {
     return AM_OK;
 }
 
+// kernels launched by k replays of the iteration graph of which `ran` passed the gate
+static unsigned long long replay_kernels(const am_engine* e, int k, unsigned long long ran) {
+    if (!e->iter_gate) return (unsigned long long)k * e->graph_kernels;
+    return (unsigned long long)k + ran * (e->graph_kernels - 1);
+}
+
 // run up to `max_iters` iterations (graph replays), stopping when the queue drains
 static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
     int64_t n = 0;
@@ -1364,10 +1416,10 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
             for (int i = 0; i < k; i++) RC(timed_iteration(e));
         } else {
             if (!e->graph_valid) RC(capture(e));
-            const unsigned long long fl0 = e->hctr[C_NFLUSH];
+            const unsigned long long fl0 = e->hctr[C_NFLUSH], gt0 = e->hctr[C_GATED];
             for (int i = 0; i < k; i++) CK(cudaGraphLaunch(e->gexec, e->stream));
-            g_launch_count += (unsigned long long)k * e->graph_kernels;
             RC(sync_counters(e));
+            g_launch_count += replay_kernels(e, k, e->hctr[C_GATED] - gt0);
             g_launch_count += (e->hctr[C_NFLUSH] - fl0) * e->cond_kernels;
         }
         n += k;
@@ -1581,7 +1633,7 @@ extern "C" int am_shard_iterate(am_engine* e, int iters, int64_t cap, int64_t* h
         if (!e->probe_in_graph) { e->probe_in_graph = true; e->graph_valid = false; }   // probes stay on the device
         if (!e->graph_valid) RC(capture(e));
         for (int i = 0; i < k; i++) CK(cudaGraphLaunch(e->gexec, e->stream));
-        g_launch_count += (unsigned long long)k * e->graph_kernels;
+        g_launch_count += (unsigned long long)k * e->graph_kernels;   // gated: an upper bound (no sync here)
     }
     return AM_OK;
 }

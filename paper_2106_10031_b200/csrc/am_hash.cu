@@ -565,6 +565,20 @@ void launch_probe_records(const ProbeRecs& R, const HashSet& H, const int32_t* s
              h ? 1 : 0);
 }
 
+// iteration gate of a graph replay: the iteration (an IF node) runs only when it has work --
+// queued states, pending probe records, or (probe stage in the graph) probes to evaluate; a
+// replay batch whose queue drained part-way then costs one tiny kernel per left-over iteration
+__global__ void k_iter_gate(unsigned long long* ctr, cudaGraphConditionalHandle h, int probes_in_graph) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const bool work = ctr[C_QTAIL] > ctr[C_QHEAD] || ctr[C_NPEND] || (probes_in_graph && ctr[C_NPROBE]);
+        cudaGraphSetConditional(h, work ? 1u : 0u);
+        if (work) ctr[C_GATED] += 1ull;
+    }
+}
+void launch_iter_gate(unsigned long long* ctr, cudaGraphConditionalHandle h, int probes_in_graph, cudaStream_t s) {
+    k_iter_gate<<<1, 32, 0, s>>>(ctr, h, probes_in_graph);
+}
+
 __global__ void k_pend_finalize(unsigned long long* ctr, cudaGraphConditionalHandle h, int has_cond) {
     pdl_enter();
     if (threadIdx.x == 0 && blockIdx.x == 0) {

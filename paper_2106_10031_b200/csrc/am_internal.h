@@ -314,6 +314,7 @@ enum Ctr {
     // queue[QB ..) (prefix reuse takes the entries queued since the previous take from the
     // tail, so children meet their parents' rows; QMARK = the tail after that take)
     C_QA, C_QB, C_QMARK,
+    C_GATED,             // graph-replayed iterations the gate let run (launch accounting)
     C_BK0,               // [kMaxPrefixBuckets] cells of this iteration's batch per shared-step count
     C_BKT0 = C_BK0 + 12, // [kMaxPrefixBuckets] the same, summed over the march's iterations
     C_PRE0 = C_BKT0 + 12,// [kMaxPrefixBuckets] items of buckets f < s (the items step s composes)
@@ -376,6 +377,7 @@ void launch_prec_target(const ProbeRecs& R, const int32_t* status, const int32_t
                         unsigned long long* ctr, int64_t cap, double* probe_pts, int64_t cap_probe, cudaStream_t s);
 void launch_resolve(const ProbeRecs& R, const HashSet& H, const int32_t* val_buf, unsigned long long* ctr,
                     int64_t cap, double* probe_pts, int32_t* probe_shape, int64_t cap_probe, cudaStream_t s);
+void launch_iter_gate(unsigned long long* ctr, cudaGraphConditionalHandle h, int probes_in_graph, cudaStream_t s);
 void launch_pend_finalize(unsigned long long* ctr, const cudaGraphConditionalHandle* h, cudaStream_t s);
 void launch_probe_records(const ProbeRecs& R, const HashSet& H, const int32_t* status, const int32_t* dup_ref,
                           const int32_t* pool_idx, const int32_t* val_buf, unsigned long long* ctr, int64_t cap_new,
