@@ -22,7 +22,11 @@
 //            raw Z rows -> HBM (the face solver's planes), masked rows -> the other act buffer
 //   head     F = head . (s_L (.) Z_L) per cell from shared memory (reference network.py:440-442)
 //
-// so a BFS iteration's gather + L + 1 launches become one.  6 consumer warps (3 x 2 warp tiles
+// so a BFS iteration's gather + L + 1 launches become one.  With prefix reuse tiles
+// are formed per bucket of cells that share steps 0..f with their parents (k_take's blist): such a
+// tile copies the parents' rows of steps 1..f from the other half of the double-buffered Z, tests
+// step f's rows for constant neurons, and starts the DMMA chain at step f + 1 (the producer skips
+// the W boxes of the skipped steps).  6 consumer warps (3 x 2 warp tiles
 // of 32 x 16) + 1 producer warp, ~107 KB shared memory, 2 CTAs per SM.  Arithmetic per output
 // element is the same as k_gemm_step's (DMMA accumulation over K, then + bias), so the two
 // paths agree to the last bit on the same K order; parity is checked against the oracle.
