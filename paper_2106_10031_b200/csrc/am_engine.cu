@@ -253,6 +253,8 @@ struct am_engine {
     DBuf<int32_t> sshape;
     bool gather_input = true;   // k_gather_input: batch gather + input step in one launch
     int graph_batch = 32;   // iterations replayed per host synchronisation (A/B: 8 -> 25.7 ms, 16 -> 25.0, 32 -> 24.6)
+    int64_t tail_queue = 64;   // fewer queued cells at a synchronisation: replay tail_batch iterations (AM_TAIL_QUEUE)
+    int tail_batch = 8;        // AM_TAIL_BATCH
     int grid_cap = 0;    // >0: CTAs per SM for persistent GEMM launches
     unsigned long long graph_kernels = 0;
     // iterative trigger schemes (am_trace): per-start state
@@ -672,6 +674,8 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_TAU_GROW")) e->tau_grow = atof(v);
     if (const char* v = getenv("AM_BISECT_TREE")) e->bisect_tree = atoi(v) != 0;
     if (const char* v = getenv("AM_GRAPH_BATCH")) e->graph_batch = std::max(1, atoi(v));
+    if (const char* v = getenv("AM_TAIL_QUEUE")) e->tail_queue = atoll(v);
+    if (const char* v = getenv("AM_TAIL_BATCH")) e->tail_batch = std::max(1, atoi(v));
     if (const char* v = getenv("AM_GATHER_INPUT")) e->gather_input = atoi(v) != 0;
     if (e->narrow_check) {
         CK(e->Z2.reserve(e->Z.n, s)); CK(e->faces2.reserve(e->faces.n, s));
@@ -1411,6 +1415,10 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
             continue;
         }
         int k = (int)std::min<int64_t>(e->graph_batch, max_iters - n);
+        // the tail of a march (a few dozen queued cells) ends within a few iterations: a short
+        // replay batch there leaves at most 7 empty iterations (~19 us each) instead of up to 31
+        const int64_t queued = (int64_t)(e->hctr[C_QTAIL] - e->hctr[C_QHEAD]);
+        if (n > 0 && queued < e->tail_queue) k = std::min(k, e->tail_batch);
         RC(ensure_iter_room(e, k + 1));
         if (e->timing) {
             for (int i = 0; i < k; i++) RC(timed_iteration(e));
