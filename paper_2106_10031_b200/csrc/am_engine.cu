@@ -1406,8 +1406,10 @@ static unsigned long long replay_kernels(const am_engine* e, int k, unsigned lon
 // run up to `max_iters` iterations (graph replays), stopping when the queue drains
 static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
     int64_t n = 0;
+    bool fresh = false;   // host counters current (the GPU has been idle since they were read)
     while (n < max_iters) {
-        RC(sync_counters(e));
+        if (!fresh) RC(sync_counters(e));
+        fresh = false;
         if (e->hctr[C_OVF1]) return fail(AM_ERR_OVERFLOW, "output capacity overflow (%llu events)", e->hctr[C_OVF1]);
         if (e->hctr[C_QHEAD] >= e->hctr[C_QTAIL] && e->hctr[C_NPEND] == 0) {
             if (e->hctr[C_NPROBE] == 0) break;
@@ -1419,7 +1421,7 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
         // replay batch there leaves at most 7 empty iterations (~19 us each) instead of up to 31
         const int64_t queued = (int64_t)(e->hctr[C_QTAIL] - e->hctr[C_QHEAD]);
         if (n > 0 && queued < e->tail_queue) k = std::min(k, e->tail_batch);
-        RC(ensure_iter_room(e, k + 1));
+        RC(ensure_iter_room(e, k + 1, false));   // counters read above; nothing ran since
         if (e->timing) {
             for (int i = 0; i < k; i++) RC(timed_iteration(e));
         } else {
@@ -1431,7 +1433,8 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
             g_launch_count += (e->hctr[C_NFLUSH] - fl0) * e->cond_kernels;
         }
         n += k;
-        RC(sync_counters(e));
+        if (e->timing) RC(sync_counters(e));
+        fresh = true;
         if (e->hctr[C_STALL]) e->graph_valid = false;  // guard fired: the next round grows buffers
         if (e->hctr[C_NPROBE]) {
             // many probes per batch of iterations: evaluate them inside the graph from now on
@@ -1443,7 +1446,7 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
             RC(sync_counters(e));
         }
     }
-    RC(sync_counters(e));
+    if (!fresh) RC(sync_counters(e));
     e->iters = (int64_t)e->hctr[C_ITER];
     if (done) *done = n;
     return AM_OK;
