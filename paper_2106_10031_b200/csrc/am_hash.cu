@@ -52,7 +52,9 @@ static int grid_mult() {
     static int m = 0;
     if (!m) {
         const char* v = getenv("AM_GRID_MULT");
-        m = v ? std::max(1, atoi(v)) : 2;   // A/B on configs[1]: 8 -> 21.35 ms, 4 -> 20.8, 2 -> 20.5, 1 -> 20.4
+        // A/B on configs[1]: 8 -> 21.35 ms, 4 -> 20.8, 2 -> 20.5, 1 -> 20.4 (round 2, early); at the
+        // end of round 2: 2 -> 17.72, 1 -> 17.53 (DeepSDF first 1 M cells 444.8 -> 436.9 ms)
+        m = v ? std::max(1, atoi(v)) : 1;
     }
     return m;
 }
