@@ -331,7 +331,14 @@ __global__ void k_route_emitted(const uint64_t* scratch, const unsigned long lon
     }
 }
 
-void launch_take(const IterState& I, cudaStream_t s) { launch_k(k_take, 1, I.queue_par ? 1024 : 32, 0, s, I); }
+void launch_take(const IterState& I, cudaStream_t s) {
+    static int nt = 0;   // bucketing threads (AM_TAKE_THREADS)
+    if (!nt) {
+        const char* v = getenv("AM_TAKE_THREADS");
+        nt = v ? std::max(32, std::min(1024, atoi(v) / 32 * 32)) : 1024;
+    }
+    launch_k(k_take, 1, I.queue_par ? nt : 32, 0, s, I);
+}
 void launch_gather_batch(const uint64_t* pool, const double* pool_hint, const int32_t* queue,
                          const unsigned long long* ctr, int32_t* batch_pool, int64_t n_cap, int KW, uint64_t* ckey,
                          double* ckey_hint, int32_t* changed, int32_t* canon_pos, cudaStream_t s) {
