@@ -186,6 +186,13 @@ class MarchResult:
     # host (welded_mesh(tol) with the same tolerance takes its result)
     _weld: tuple | None = field(default=None, repr=False)
 
+    def __getstate__(self):
+        # device copies and the pending background weld stay with the process that marched
+        st = dict(self.__dict__)
+        st["_dev"] = None
+        st["_weld"] = None
+        return st
+
     @property
     def has_face(self) -> np.ndarray:
         return self.nverts > 0

@@ -144,3 +144,18 @@ def test_topology_check_octahedron():
     assert r["watertight"] and r["euler"] == 2 and r["components"] == 1 and r["open_edges"] == 0
     r = topology_check(TriangleMesh(v, t[:-1]))
     assert not r["watertight"] and r["open_edges"] == 3
+
+
+def test_march_result_pickles_without_device_state():
+    """A MarchResult crosses process boundaries (multiprocessing queues, pickle) without its
+    device copies or its pending background weld."""
+    import pickle
+    from concurrent.futures import Future
+    from paper_2106_10031_b200.marching import MarchReport, MarchResult
+    rep = MarchReport(cells_visited=1, faces_emitted=0, empty_faces=1, open_edges=0, seconds=0.0, seeds_used=1,
+                      capped=False, threads=1, waves=1, overflow=0)
+    r = MarchResult(np.zeros((1, 2), np.uint8), np.full(1, -1), np.zeros(1, np.int32), np.zeros((0, 3)),
+                    np.zeros(0, np.int32), np.zeros((0, 2), np.int32), rep, 10, _dev=(object(),), _weld=(1e-7, Future()))
+    back = pickle.loads(pickle.dumps(r))
+    assert back._dev is None and back._weld is None and back.n_bits == 10
+    assert np.array_equal(back.keys, r.keys)
