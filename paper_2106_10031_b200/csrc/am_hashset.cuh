@@ -84,6 +84,18 @@ __device__ __forceinline__ int32_t upsert_one(const HashSet& H, const uint64_t* 
     return st;
 }
 
+// atomicAdd(ctr, 1) for every converged lane of the warp with one atomic per warp (the frontier
+// and visited-cell counters are hit by every batch item): returns this lane's old value
+__device__ __forceinline__ unsigned long long warp_agg_inc(unsigned long long* ctr) {
+    const unsigned act = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(act) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(ctr, (unsigned long long)__popc(act));
+    base = __shfl_sync(act, base, leader);
+    return base + (unsigned long long)__popc(act & ((1u << lane) - 1u));
+}
+
 // One batch item after its composition (reference marching.py:221-245 with the canonical state
 // of _refine / canonical_state): a changed (canonicalised) key is inserted (or routed to its
 // owner rank); a new state joins the frontier (f_items / f_pool) unless the max_cells cap is
@@ -99,7 +111,7 @@ __device__ __forceinline__ void canon_frontier_one(const HashSet& H, const uint6
     const uint32_t fl = H.pool_flags[bp];
     H.pool_flags[bp] = (fl | 2u) & ~kPoolDeferred;   // composed (probe records can resolve)
     if (fl & kPoolDeferred) {   // a deferred cell solved again: visited and counted already
-        const unsigned long long kf = atomicAdd(ctr + C_NF, 1ull);
+        const unsigned long long kf = warp_agg_inc(ctr + C_NF);
         f_items[kf] = (int32_t)b;
         f_pool[kf] = bp;
         return;
@@ -123,12 +135,12 @@ __device__ __forceinline__ void canon_frontier_one(const HashSet& H, const uint6
         }
     }
     if (p < 0) return;
-    const unsigned long long tot = atomicAdd(ctr + C_TOTAL, 1ull);
+    const unsigned long long tot = warp_agg_inc(ctr + C_TOTAL);
     if ((long long)tot >= max_cells) {  // max_cells cap (reference marching.py:240-242)
         atomicAdd(ctr + C_CAPPED, 1ull);
         return;
     }
-    const unsigned long long kf = atomicAdd(ctr + C_NF, 1ull);
+    const unsigned long long kf = warp_agg_inc(ctr + C_NF);
     H.pool_flags[p] |= 1u;
     f_items[kf] = (int32_t)b;
     f_pool[kf] = p;
