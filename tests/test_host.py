@@ -5,6 +5,7 @@ import json
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -159,3 +160,34 @@ def test_march_result_pickles_without_device_state():
     back = pickle.loads(pickle.dumps(r))
     assert back._dev is None and back._weld is None and back.n_bits == 10
     assert np.array_equal(back.keys, r.keys)
+
+
+@pytest.mark.parametrize("case", [("geo", 24, 0), ("geo-rare", 40, 7)])
+def test_sample_seeds_host_logic_matches_reference_loop(case):
+    """seeding.sample_seeds' host logic -- stacked, memoised sample rounds, several retry rounds
+    evaluated per forward and replayed in order, vectorised first-positive / first-negative pick
+    -- chooses exactly the reference's bisection pairs (oracle.sample_seeds restates reference
+    seeding.py:123-162 stream by stream).  The engine is a CPU stand-in built on the oracle."""
+    import torch
+    from paper_2106_10031_b200 import seeding, synth
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    name, count, rng_seed = case
+    net = synth.geometric_mlp([12, 12], seed=3)
+    on = oracle.OracleNet(net)
+    bbox = ((-1.2,) * 3, (1.2,) * 3) if name == "geo" else ((0.3, 0.3, 0.3), (1.2, 1.2, 1.2))
+
+    class Eng:
+        def __init__(self):
+            self.net = net
+
+        def forward(self, pts):
+            return torch.as_tensor(on.forward_many(np.asarray(pts)))
+
+        def dichotomy(self, xp, xn, eps, tol):
+            return torch.as_tensor(np.stack([oracle._seed_dichotomy(on, a, b)[0] for a, b in zip(xp, xn)]))
+
+    seeding._ROUNDS.clear()
+    mine = seeding.sample_seeds(Eng(), count, bbox, rng_seed=rng_seed)
+    ref = oracle.sample_seeds(on, count, bbox, rng_seed=rng_seed)
+    np.testing.assert_array_equal(mine, ref)
