@@ -337,3 +337,23 @@ def test_narrow_point_forward_matches_per_layer_bitwise(precision, monkeypatch):
         del eng
     np.testing.assert_array_equal(out["1"][0], out["0"][0])
     np.testing.assert_array_equal(out["1"][1], out["0"][1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("heavy", [False, True])
+def test_max_cells_cap_is_exact(heavy):
+    """With max_cells reached the march returns exactly max_cells visited cells and the capped
+    flag (reference marching.py:240-242); heavy nets (no deferral) end the walk at the cap
+    instead of composing and discarding the rest of the queue."""
+    from paper_2106_10031_b200 import synth
+    from paper_2106_10031_b200.marching import clear_engine_cache
+    m = _gpu()
+    net = synth.deepsdf_mlp(width=192, depth=8, skip_at=4, seed=2) if heavy else synth.geometric_mlp([90] * 4, seed=1)
+    clear_engine_cache()
+    try:
+        r = m.march(net, m.MarchConfig(seeds=8, rng_seed=3, max_cells=3000))
+    finally:
+        clear_engine_cache()
+    assert r.report.capped
+    assert r.report.cells_visited == 3000
+    assert r.report.overflow == 0
