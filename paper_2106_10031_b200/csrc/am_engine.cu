@@ -226,6 +226,11 @@ struct am_engine {
     bool iter_gate = false;
     unsigned long long gate_kernels = 0;     // kernels of one gated iteration body
     bool probe_in_graph = false;             // probe stage inside the iteration graph (sticky)
+    // AM_PROBE_AUTO=1: switch the probe stage into the graph once a host round sees many probes.
+    // Off: the exact probe forwards of a round are evaluated together at its host synchronisation
+    // (complete DeepSDF march 6.56 -> 6.33 s: ~30 probes per iteration paid a whole per-layer
+    // forward pipeline and a conditional node -- which cuts the PDL chain -- every iteration)
+    bool probe_auto = false;
     unsigned long long cond_kernels = 0;     // kernels in that body
     // bisection trigger: engine-owned buffers and a captured 8-step graph (am_dichotomy)
     DBuf<double> dxp, dxn, dfp, dfn, dmid, dvals, dout, dtree, dtvals;
@@ -668,6 +673,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_TAU_MULT")) e->tau_mult = atof(v);
     if (const char* v = getenv("AM_COMPOSE_FUSED")) e->compose_fused = atoi(v) != 0;
     if (const char* v = getenv("AM_PROBE_IN_GRAPH")) e->probe_in_graph = atoi(v) != 0;
+    if (const char* v = getenv("AM_PROBE_AUTO")) e->probe_auto = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_REACH")) e->near_reach = atof(v);
     if (const char* v = getenv("AM_NEAR_CAP")) e->near_cap = atoi(v);
     if (const char* v = getenv("AM_MAX_ATTEMPTS")) e->max_attempts = atoi(v);
@@ -1438,7 +1444,7 @@ static int run_iterations(am_engine* e, int64_t max_iters, int64_t* done) {
         if (e->hctr[C_STALL]) e->graph_valid = false;  // guard fired: the next round grows buffers
         if (e->hctr[C_NPROBE]) {
             // many probes per batch of iterations: evaluate them inside the graph from now on
-            if (!e->probe_in_graph && e->hctr[C_NPROBE] > kProbeInGraph) {
+            if (!e->probe_in_graph && e->probe_auto && e->hctr[C_NPROBE] > kProbeInGraph) {
                 e->probe_in_graph = true;
                 e->graph_valid = false;
             }
