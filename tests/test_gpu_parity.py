@@ -269,7 +269,7 @@ def test_prefix_reuse_per_step_batch_of_shapes_is_bitwise_neutral(monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["narrow-fp64", "narrow-fp32", "per-step-deepsdf"])
+@pytest.mark.parametrize("case", ["narrow-fp64", "narrow-fp32", "narrow-varying-widths", "per-step-deepsdf"])
 def test_prefix_reuse_is_bitwise_neutral(case, monkeypatch):
     """Children composed from their parents' Z rows (prefix reuse, on the narrow and on the
     per-step path) give the same march, bit for bit, as composing every step; and the reuse
@@ -277,7 +277,10 @@ def test_prefix_reuse_is_bitwise_neutral(case, monkeypatch):
     from paper_2106_10031_b200 import synth
     from paper_2106_10031_b200.marching import _ENGINES, clear_engine_cache
     m = _gpu()
-    if case.startswith("narrow"):
+    if case == "narrow-varying-widths":   # steps of different widths (copied rows feed narrower steps)
+        net = synth.geometric_mlp([96, 48, 80, 32, 64], seed=4)
+        cfg = m.MarchConfig(bbox=((0.0, 0.0, 0.0), (0.6, 0.6, 0.6)), seeds=4, rng_seed=5)
+    elif case.startswith("narrow"):
         net = synth.geometric_mlp([90] * 4, seed=1)
         cfg = m.MarchConfig(bbox=((0.0, 0.0, 0.0), (0.5, 0.5, 0.5)), seeds=4, rng_seed=5,
                             precision=case.split("-")[1])
@@ -358,3 +361,17 @@ def test_max_cells_cap_is_exact(heavy):
     assert r.report.capped
     assert r.report.cells_visited == 3000
     assert r.report.overflow == 0
+
+
+@pytest.mark.gpu
+def test_narrow_varying_widths_matches_oracle():
+    """The fused narrow composition on a net whose layers differ in width (96, 48, 80, 32, 64:
+    step K extents and row counts change from step to step) == the oracle march."""
+    from paper_2106_10031_b200 import synth
+    m = _gpu()
+    net = synth.geometric_mlp([96, 48, 80, 32, 64], seed=4)
+    bbox = ((0.0, 0.0, 0.0), (0.6, 0.6, 0.6))
+    r = m.march(net, m.MarchConfig(bbox=bbox, seeds=4, rng_seed=5))
+    o = oracle.march(net, bbox=bbox, seed_points=r.seeds)
+    assert r.report.cells_visited > 1000
+    assert_same_march(r, o.keys, o.branch, o.nverts, o.verts, o.edge_nrefs, o.edge_refs)
