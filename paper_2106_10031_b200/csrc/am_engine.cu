@@ -231,6 +231,7 @@ struct am_engine {
     // (complete DeepSDF march 6.56 -> 6.33 s: ~30 probes per iteration paid a whole per-layer
     // forward pipeline and a conditional node -- which cuts the PDL chain -- every iteration)
     bool probe_auto = false;
+    bool shard_probe_in_graph = false;       // AM_SHARD_PROBE_IN_GRAPH
     unsigned long long cond_kernels = 0;     // kernels in that body
     // bisection trigger: engine-owned buffers and a captured 8-step graph (am_dichotomy)
     DBuf<double> dxp, dxn, dfp, dfn, dmid, dvals, dout, dtree, dtvals;
@@ -674,6 +675,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_COMPOSE_FUSED")) e->compose_fused = atoi(v) != 0;
     if (const char* v = getenv("AM_PROBE_IN_GRAPH")) e->probe_in_graph = atoi(v) != 0;
     if (const char* v = getenv("AM_PROBE_AUTO")) e->probe_auto = atoi(v) != 0;
+    if (const char* v = getenv("AM_SHARD_PROBE_IN_GRAPH")) e->shard_probe_in_graph = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_REACH")) e->near_reach = atof(v);
     if (const char* v = getenv("AM_NEAR_CAP")) e->near_cap = atoi(v);
     if (const char* v = getenv("AM_MAX_ATTEMPTS")) e->max_attempts = atoi(v);
@@ -1645,9 +1647,16 @@ extern "C" int am_shard_iterate(am_engine* e, int iters, int64_t cap, int64_t* h
     // room for the keys the coming exchange can deliver
     const bool queued = e->hctr[C_QHEAD] < e->hctr[C_QTAIL] || e->hctr[C_NPEND] || e->hctr[C_NPROBE];
     const int k = queued ? iters : 0;
-    RC(ensure_iter_room(e, k + 1, false, (int64_t)world * cap_next));
+    RC(ensure_iter_room(e, k + 1, false, (int64_t)world * cap_next + e->PB));
     if (k > 0) {
-        if (!e->probe_in_graph) { e->probe_in_graph = true; e->graph_valid = false; }   // probes stay on the device
+        // the exact probe evaluations queued by the previous round run first (device-side counts:
+        // no extra synchronisation); a conditional probe node in every iteration would cut the
+        // PDL chain of each one (AM_SHARD_PROBE_IN_GRAPH=1 restores it)
+        if (e->shard_probe_in_graph) {
+            if (!e->probe_in_graph) { e->probe_in_graph = true; e->graph_valid = false; }
+        } else if (e->hctr[C_NPROBE] && !e->probe_in_graph) {
+            RC(launch_probe_stage(e));
+        }
         if (!e->graph_valid) RC(capture(e));
         for (int i = 0; i < k; i++) CK(cudaGraphLaunch(e->gexec, e->stream));
         g_launch_count += (unsigned long long)k * e->graph_kernels;   // gated: an upper bound (no sync here)
