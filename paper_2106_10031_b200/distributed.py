@@ -39,7 +39,14 @@ import torch.distributed as dist
 from .engine import Engine
 from .seeding import sample_seeds
 
-ITERS_PER_ROUND = 4       # BFS iterations between exchanges
+# BFS iterations between exchanges.  With hash ownership ~(P-1)/P of a cell's neighbours belong to
+# other ranks, so the march advances about one BFS level per exchange whatever the round length;
+# the iterations after the first in a round only see the locally owned children (1/P of them,
+# then 1/P^2 ...) at the ~70 us per-iteration floor.  One rank: 4 (P = 1 A/B: 2 / 4 / 8 / 16 ->
+# 20.43 / 19.16 / 18.77 / 18.47 ms, `profiles/r02_sharded_p1.json`; 4 keeps the round latency low
+# when ranks are added); several ranks: 2 (the first iteration plus one pass over local children).
+ITERS_PER_ROUND = 4
+ITERS_PER_ROUND_MULTI = 2
 INITIAL_CAP = 1024        # keys per destination in the first exchange (grows from the headers)
 
 
@@ -78,7 +85,7 @@ class ShardedMarcher:
     """Hash-owned multi-GPU march (one instance per rank), device-driven rounds."""
 
     def __init__(self, net, bbox=((-1.2,) * 3, (1.2,) * 3), max_cells: int = 10_000_000, engine_factory=None,
-                 iters_per_round: int = ITERS_PER_ROUND, **kw):
+                 iters_per_round: int | None = None, **kw):
         """``net``: one network, or a list of same-architecture networks marched as ONE fused BFS
         (a batch of shapes: the shape word is part of every key, so ownership and dedup are
         per shape; ``max_cells`` then caps the batch total)."""
@@ -88,6 +95,8 @@ class ShardedMarcher:
         self.nets = list(net) if self.batch else [net]
         self.net = self.nets[0]
         self.bbox = bbox
+        if iters_per_round is None:
+            iters_per_round = ITERS_PER_ROUND if self.world == 1 else ITERS_PER_ROUND_MULTI
         self.iters = int(iters_per_round)
         self.max_cells = int(max_cells)
         share = cap_share(self.max_cells, self.rank, self.world)
