@@ -172,11 +172,11 @@ struct am_engine {
     // marches but slower (configs[1] BFS 18.55 vs 17.76 ms, a 48-wave small net 3.78 vs 3.57):
     // the hash probes lengthen every cell's chain more than the separate launch costs
     bool face_upsert = false;
-    // point forwards through k_forward_narrow on the narrow path (AM_FORWARD_NARROW=1): bitwise
-    // equal to the per-layer kernels but not faster (4096 trigger samples 0.114 vs 0.123 ms, the
-    // configs[1] BFS with its probe forwards 17.90 vs 17.71 ms): a 32-point tile walking every
-    // layer is as long a chain as the per-layer launches
-    bool forward_narrow = false;
+    // point forwards through k_forward_narrow on the narrow path (AM_FORWARD_NARROW=0: the
+    // per-layer kernels; bitwise equal).  The trigger: sample_seeds 1.43 -> 1.27 ms, e2e -0.3 ms;
+    // the BFS is unaffected since the exact probe forwards moved to the host rounds (17.64 vs
+    // 17.67 ms; with a per-iteration probe stage it had cost 0.2 ms)
+    bool forward_narrow = true;
     bool canon_in_narrow = false;   // canonical insert + frontier in k_compose_narrow (AM_CANON_IN_NARROW)
     bool near_fused = false;    // near lists built by k_compose_narrow (AM_NEAR_FUSED=1; default: k_near)
     DBuf<double> Zi;
