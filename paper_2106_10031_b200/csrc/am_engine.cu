@@ -177,6 +177,7 @@ struct am_engine {
     // the BFS is unaffected since the exact probe forwards moved to the host rounds (17.64 vs
     // 17.67 ms; with a per-iteration probe stage it had cost 0.2 ms)
     bool forward_narrow = true;
+    bool narrow_explicit = true;   // explicit-key compositions (seeds, affine maps) on k_compose_narrow (AM_NARROW_EXPLICIT)
     bool canon_in_narrow = false;   // canonical insert + frontier in k_compose_narrow (AM_CANON_IN_NARROW)
     bool near_fused = false;    // near lists built by k_compose_narrow (AM_NEAR_FUSED=1; default: k_near)
     DBuf<double> Zi;
@@ -713,6 +714,7 @@ extern "C" int am_engine_create(am_engine** out, const am_net_desc* net, const a
     if (const char* v = getenv("AM_GEMM_NJ4")) e->gemm_nj4 = atoi(v) != 0;
     if (const char* v = getenv("AM_FACE_UPSERT")) e->face_upsert = atoi(v) != 0;
     if (const char* v = getenv("AM_FORWARD_NARROW")) e->forward_narrow = atoi(v) != 0;
+    if (const char* v = getenv("AM_NARROW_EXPLICIT")) e->narrow_explicit = atoi(v) != 0;
     if (const char* v = getenv("AM_NEAR_FUSED"))
         e->near_fused = e->narrow_fused && !e->face_order && !e->narrow_check && atoi(v) != 0;
     if (const char* v = getenv("AM_CANON_FUSED")) e->canon_fused = atoi(v) != 0;
@@ -937,6 +939,26 @@ static int compose(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, do
     return AM_OK;
 }
 
+// composition of n explicit keys (in place: canonical keys, changed flags, Z rows, face planes):
+// the narrow kernel in explicit-key mode where the net is narrow (one launch for every layer;
+// bitwise equal to the per-layer path), else the per-layer kernels
+static int compose_keys(am_engine* e, uint64_t* keys, int32_t* changed, double* Z, double* faces, int64_t n) {
+    if (n <= 0) return AM_OK;
+    if (e->narrow_fused && e->narrow_explicit && !e->narrow_check) {
+        NarrowCompose N = *e->ncomp;
+        for (int q = 0; q < N.nsteps; q++) N.st[q] = e->sdev[q];
+        N.subs = reinterpret_cast<const SubDev*>(e->subdev.p);
+        N.keys_in = keys; N.keys = keys; N.Z = Z; N.faces = faces; N.changed = changed;
+        N.n_dev = nullptr; N.n_cap = n; N.KW = e->KW; N.zs = e->zs; N.shape_w = e->shape_w; N.fp32 = e->fp32;
+        N.prefix = 0; N.snake = 0; N.near_fused = 0; N.canon_fused = 0; N.ctr = e->ctr.p;
+        N.prof = e->dbg.p + 32;
+        launch_compose_narrow(N, e->stream);
+        CK(cudaGetLastError());
+        return AM_OK;
+    }
+    return compose(e, keys, changed, Z, faces, nullptr, n);
+}
+
 static int forward(am_engine* e, const double* pts, double* vals, uint64_t* keys, const unsigned long long* key_off,
                    double* Zw, const unsigned long long* n_dev, int64_t n_cap) {
     if (e->narrow_fused && e->forward_narrow && !key_off) {
@@ -1009,7 +1031,7 @@ extern "C" int am_affine_maps(am_engine* e, const uint64_t* d_keys, int64_t n, u
         int64_t m = std::min<int64_t>(e->B, n - o);
         CK(cudaMemcpyAsync(e->ckey.p, d_keys + o * e->KW, m * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
         CK(cudaMemsetAsync(e->changed.p, 0, m * sizeof(int32_t), e->stream));
-        RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, m));
+        RC(compose_keys(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, m));
         if (d_canon)
             CK(cudaMemcpyAsync(d_canon + o * e->KW, e->ckey.p, m * e->KW * 8, cudaMemcpyDeviceToDevice, e->stream));
         if (d_planes)
@@ -1572,7 +1594,7 @@ extern "C" int am_trace(am_engine* e, const double* d_x0, int64_t n, int scheme,
     auto grad = [&]() -> int {   // face planes of the current states -> e->faces
         CK(cudaMemcpyAsync(e->ckey.p, e->tk.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemsetAsync(e->changed.p, 0, n * sizeof(int32_t), s));
-        return compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n);
+        return compose_keys(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, n);
     };
     if (scheme == 0) RC(forward_host(e, e->tx.p, n, e->tf.p, e->tk.p));
     for (int it = 0; it <= max_iters; it++) {
@@ -1746,7 +1768,7 @@ extern "C" int am_seed_shapes(am_engine* e, const double* d_pts, const int32_t* 
         for (int it = 0; it < 3; it++) {
             CK(cudaMemcpyAsync(e->ckey.p, e->ss.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
             CK(cudaMemsetAsync(e->changed.p, 0, n * 4, s));
-            RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n));
+            RC(compose_keys(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, n));
             launch_seed_project(e->sx.p, e->faces.p, e->ckey.p, KW, e->M, e->ensemble, n, e->sact.p, e->sxp.p,
                                 e->sdone.p, s);
             launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, e->sdone.p, s);
@@ -1756,7 +1778,7 @@ extern "C" int am_seed_shapes(am_engine* e, const double* d_pts, const int32_t* 
         }
         CK(cudaMemcpyAsync(e->ckey.p, e->ss.p, n * KW * 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemsetAsync(e->changed.p, 0, n * 4, s));
-        RC(compose(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, nullptr, n));
+        RC(compose_keys(e, e->ckey.p, e->changed.p, e->Z.p, e->faces.p, n));
         launch_seed_check(nullptr, e->ckey.p, KW, n, e->sact.p, nullptr, nullptr, nullptr, e->sres.p, nullptr, s);
         // the seed point (inside the seed's cell, on the surface up to seed_tol) is the face
         // solver's hint, with a small initial reach that the solver widens as needed

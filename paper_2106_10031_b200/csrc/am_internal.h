@@ -254,6 +254,7 @@ struct NarrowCompose {
     // canonical insert + frontier of the tile's cells in its epilogue (canon_fused != 0;
     // am_hashset.cuh canon_frontier_one: k_canon_frontier's work without its launch)
     int canon_fused;
+    const uint64_t* keys_in;           // non-null: compose these n_cap keys (no queue / pool gather)
     HashSet H;
     int rank, world;
     uint64_t* outbox;

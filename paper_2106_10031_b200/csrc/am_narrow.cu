@@ -175,7 +175,11 @@ __device__ __forceinline__ void consume(NarrowSmem& S, const NarrowCompose& P, i
         for (int q = tid; q < NC * KW; q += NCT) {
             const int c = q / KW, w = q - c * KW;
             uint64_t v = 0;
-            if (c < ncell) {
+            if (c < ncell && P.keys_in) {   // explicit keys (seeds, affine maps): no queue, no pool
+                const int64_t b = pos0 + c;
+                v = P.keys_in[b * KW + w];
+                if (w == 0) S.bidx[c] = (int32_t)b;
+            } else if (c < ncell) {
                 const int64_t b = P.prefix ? (int64_t)P.blist[(int64_t)fsh * P.n_cap + pos0 + c] : pos0 + c;
                 const int32_t p = P.queue[batch_queue_index(P.ctr, b)];
                 v = P.pool[(int64_t)p * KW + w];

@@ -161,7 +161,7 @@ def test_fp32_mode_within_stated_tolerance():
                                   ("AM_NARROW_TILE", "2"), ("AM_CANON_FUSED", "0"), ("AM_FACE_ORDER", "1"),
                                   ("AM_PREFIX", "0"), ("AM_NEAR_FUSED", "1"), ("AM_CANON_IN_NARROW", "1"),
                                   ("AM_FACE_UPSERT", "1"), ("AM_ITER_GATE", "1"), ("AM_GEMM_NJ4", "1"),
-                                  ("AM_FORWARD_NARROW", "0")],
+                                  ("AM_FORWARD_NARROW", "0"), ("AM_NARROW_EXPLICIT", "0")],
                          ids=lambda k: f"{k[0]}={k[1]}")
 def test_engine_paths_match_oracle(knob, monkeypatch):
     """Every execution path of the engine is bit-exact, not only the default one: the probe stage
